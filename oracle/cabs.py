@@ -1,0 +1,400 @@
+"""FP64 oracle of the CABS hot path (TEST INFRASTRUCTURE ONLY).
+
+Plain, slow, obviously-correct NumPy float64 code that follows the paper step by
+step (Algorithm 2; the sketching routine of §4.1,
+P:222-232; weighted k-means, Eq. 6).  Where a step has a plain
+definition (gathers, nearest-centre argmin, the Frobenius residual) the oracle
+computes that definition directly.  Where the paper is silent we follow the
+readings Z1-Z25 listed in DESIGN.md ("Readings of the paper").
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+reference leg may import this module.  It shares no code with the CUDA path.
+
+Parity status per function:
+  gather, svd_w, sketch, embeddings, lloyd, snap, residual, cabs_run: pinned
+  (tests/test_oracle_*.py).  residual_sampled (implicit source): parity unpinned
+  beyond self-consistency (not on the round-1 path).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import rng
+
+STABILIZED = 0
+PSEUDO_SKELETON = 1
+
+WEIGHT_CONST = 0
+WEIGHT_POWER = 1
+
+DEFAULT_TOL = 1e-12  # keep sigma_i > tol * sigma_1
+NEAR_TIE_GAP = 1e-5  # BASELINE.json north_star: relative distance gap < 1e-5
+
+
+# --------------------------------------------------------------------------
+# Step 1 / step 3 gathers:  C = A[:, J], R = A[I, :], W = A[I, J]
+# --------------------------------------------------------------------------
+def check_indices(idx, N, what="index"):
+    idx = np.asarray(idx, dtype=np.int64)
+    if idx.size and (idx.min() < 0 or idx.max() >= N):
+        raise IndexError(f"{what} out of range [0, {N})")
+    if np.unique(idx).size != idx.size:
+        raise IndexError(f"duplicate {what}")
+    return idx
+
+
+def gather(A, I, J):
+    """P:195 "C = A_[:,I^c], R = A_[I^r,:], W = A_[I^r,I^c]".  Exact copies, as float64."""
+    m, n = A.shape
+    I = check_indices(I, m, "row index")
+    J = check_indices(J, n, "column index")
+    C = np.asarray(A[:, J], dtype=np.float64)
+    R = np.asarray(A[I, :], dtype=np.float64)
+    W = np.asarray(A[np.ix_(I, J)], dtype=np.float64)
+    return C, R, W
+
+
+# --------------------------------------------------------------------------
+# The k x k SVD of W ("Assuming an SVD W = U_w Sigma_w V_w^T")
+# --------------------------------------------------------------------------
+def canonical_signs(Uw, Vw):
+    """Z5: flip each singular pair so the largest-|.| entry of U_w's column is
+    positive (ties -> lowest row index).  Used so factor comparisons are direct;
+    every product the method forms is invariant to it."""
+    Uw = Uw.copy()
+    Vw = Vw.copy()
+    for i in range(Uw.shape[1]):
+        col = Uw[:, i]
+        if not np.any(col):
+            continue
+        p = int(np.argmax(np.abs(col)))  # first max -> lowest index
+        if col[p] < 0:
+            Uw[:, i] = -Uw[:, i]
+            Vw[:, i] = -Vw[:, i]
+    return Uw, Vw
+
+
+def svd_w(W, tol=DEFAULT_TOL):
+    """Thin SVD of W with sigma descending, truncated to sigma_i > tol*sigma_1 (Z4).
+
+    Returns (Uw[k, r], sigma[r], Vw[k, r]).  LAPACK is used as a library step; it
+    is pinned against closed forms in tests/test_oracle_sketch.py.
+    """
+    W = np.asarray(W, dtype=np.float64)
+    if not np.all(np.isfinite(W)):
+        raise ValueError("non-finite W")
+    if W.size == 0:
+        k = W.shape[0]
+        return np.zeros((k, 0)), np.zeros(0), np.zeros((W.shape[1], 0))
+    Uw, sig, Vwt = np.linalg.svd(W, full_matrices=False)
+    Vw = Vwt.T
+    if sig.size == 0 or sig[0] == 0.0:
+        r = 0
+    else:
+        r = int(np.sum(sig > tol * sig[0]))
+    Uw, Vw = canonical_signs(Uw[:, :r], Vw[:, :r])
+    return Uw, sig[:r].copy(), Vw
+
+
+# --------------------------------------------------------------------------
+# The sketching routine and the pseudo-skeleton (Eq. 2)
+# --------------------------------------------------------------------------
+@dataclass
+class Sketch:
+    U: np.ndarray      # m x r, columns normalised ("U = C V_w N_c^-1")
+    s: np.ndarray      # r, positive
+    V: np.ndarray      # n x r ("V = N_r^-1 U_w^T R", stored as its transpose)
+    sigma: np.ndarray  # singular values of W that survived (r,)
+    Uw: np.ndarray
+    Vw: np.ndarray
+    Nc: np.ndarray
+    Nr: np.ndarray
+
+    @property
+    def r(self):
+        return self.s.size
+
+    def dense(self):
+        return (self.U * self.s) @ self.V.T
+
+
+def sketch(C, R, W, m, n, k, mode=STABILIZED, tol=DEFAULT_TOL):
+    """The paper's `sketching` routine, step by step.
+
+    1. W = U_w Sigma_w V_w^T
+    2. keep sigma_i > tol*sigma_1                              (Z4)
+    3. extrapolate: Y_c = C V_w, Y_r = R^T U_w; N_c, N_r = column 2-norms
+    4. drop components with a zero extrapolated norm           (Z4)
+    5. U = Y_c N_c^-1, V = Y_r N_r^-1
+    6. STABILIZED: s = sigma * sqrt(m n) / k                   (Z3)
+       PSEUDO_SKELETON: s = N_c N_r / sigma, so U diag(s) V^T = C W_r^+ R exactly (Eq. 2)
+    Order = sigma order; signs canonical (Z5).
+    """
+    C = np.asarray(C, dtype=np.float64)
+    R = np.asarray(R, dtype=np.float64)
+    Uw, sig, Vw = svd_w(W, tol)
+    Yc = C @ Vw            # m x r
+    Yr = R.T @ Uw          # n x r
+    Nc = np.sqrt(np.sum(Yc * Yc, axis=0))
+    Nr = np.sqrt(np.sum(Yr * Yr, axis=0))
+    keep = (Nc > 0) & (Nr > 0)
+    U = Yc[:, keep] / Nc[keep]
+    V = Yr[:, keep] / Nr[keep]
+    if mode == STABILIZED:
+        s = sig[keep] * math.sqrt(float(m) * float(n)) / float(k)
+    elif mode == PSEUDO_SKELETON:
+        s = Nc[keep] * Nr[keep] / sig[keep]
+    else:
+        raise ValueError("unknown mode")
+    return Sketch(U=U, s=s, V=V, sigma=sig[keep], Uw=Uw[:, keep], Vw=Vw[:, keep],
+                  Nc=Nc[keep], Nr=Nr[keep])
+
+
+def pseudo_skeleton_dense(C, R, W, tol=DEFAULT_TOL):
+    """Eq. 2 written out: C W^+ R with the truncated pseudo-inverse (independent check)."""
+    Uw, sig, Vw = svd_w(W, tol)
+    Wp = (Vw / sig) @ Uw.T if sig.size else np.zeros((W.shape[1], W.shape[0]))
+    return np.asarray(C, np.float64) @ Wp @ np.asarray(R, np.float64)
+
+
+def embeddings(sk: Sketch):
+    """Alg. 2 step 2: P = U S^1/2, Q = V S^1/2."""
+    rs = np.sqrt(sk.s)
+    return sk.U * rs, sk.V * rs
+
+
+# --------------------------------------------------------------------------
+# Weighted k-means (Eq. 6) with Lloyd iterations
+# --------------------------------------------------------------------------
+def weights(X, kind=WEIGHT_CONST, p=2.0):
+    """w_l = Upsilon(||X_l||_2) (Eq. 6); constant for dense matrices (Z10)."""
+    X = np.asarray(X, dtype=np.float64)
+    if kind == WEIGHT_CONST:
+        return np.ones(X.shape[0])
+    if kind == WEIGHT_POWER:
+        return np.sqrt(np.sum(X * X, axis=1)) ** p
+    raise ValueError("unknown weight kind")
+
+
+def sq_dist(X, c):
+    """||X_l - c||^2 for every row l, by direct differences (Z18 / F3)."""
+    D = np.asarray(X, np.float64) - np.asarray(c, np.float64)[None, :]
+    return np.sum(D * D, axis=1)
+
+
+def sq_dist_all(X, centres, chunk=4096):
+    """N x k2 matrix of direct-difference squared distances."""
+    X = np.asarray(X, np.float64)
+    centres = np.asarray(centres, np.float64)
+    out = np.empty((X.shape[0], centres.shape[0]))
+    for a in range(0, X.shape[0], chunk):
+        Xb = X[a:a + chunk]
+        D = Xb[:, None, :] - centres[None, :, :]
+        out[a:a + chunk] = np.sum(D * D, axis=2)
+    return out
+
+
+def argmin_with_gap(Dm):
+    """Lowest-index argmin per row (Z11) and relative gap (d2 - d1)/d2 (Z18)."""
+    lab = np.argmin(Dm, axis=1)
+    d1 = Dm[np.arange(Dm.shape[0]), lab]
+    if Dm.shape[1] > 1:
+        part = np.partition(Dm, 1, axis=1)
+        d2 = part[:, 1]
+        with np.errstate(invalid="ignore", divide="ignore"):
+            gap = np.where(d2 > 0, (d2 - d1) / d2, 0.0)
+    else:
+        gap = np.full(Dm.shape[0], np.inf)
+    return lab.astype(np.int64), d1, gap
+
+
+@dataclass
+class KmeansResult:
+    centres: np.ndarray          # k2 x d after the c-th update
+    labels: np.ndarray           # assignment of the c-th iteration
+    objective: np.ndarray        # J_t, t = 1..c (Eq. 6 at the t-th assignment)
+    cluster_w: np.ndarray        # omega_j from the c-th assignment
+    gaps: list = field(default_factory=list)       # per-iteration relative gaps
+    labels_hist: list = field(default_factory=list)
+    centres_hist: list = field(default_factory=list)  # centres used by iteration t
+
+
+def lloyd(X, k2, iters, w=None, init_idx=None, init_centres=None, seed=0,
+          tag=rng.TAG_INIT_ROWS, check_monotone=True):
+    """Weighted Lloyd iterations (O6; Eq. 6; c iterations P:204).
+
+    init: centres = X[Floyd(N, k2, tag)] (Z9), or explicit indices / centres.
+    each iteration t: s_t(l) = argmin_j ||X_l - c_j||^2 (direct differences,
+    lowest j on ties); J_t = sum_l w_l ||X_l - c_{s_t(l)}||^2; then every cluster
+    with positive weight moves to its weighted mean, others keep their centre (Z12).
+    """
+    X = np.asarray(X, np.float64)
+    N = X.shape[0]
+    if w is None:
+        w = np.ones(N)
+    w = np.asarray(w, np.float64)
+    if k2 < 1 or iters < 1:
+        raise ValueError("k2 >= 1 and iters >= 1 required")
+    if int(np.sum(w > 0)) < k2:
+        raise ValueError("fewer than k2 points with nonzero weight")
+    if init_centres is not None:
+        centres = np.array(init_centres, dtype=np.float64, copy=True)
+    else:
+        if init_idx is None:
+            init_idx = rng.floyd(N, k2, seed, tag)
+        centres = X[np.asarray(init_idx, dtype=np.int64)].copy()
+    res = KmeansResult(centres=None, labels=None, objective=np.zeros(iters), cluster_w=None)
+    for t in range(iters):
+        res.centres_hist.append(centres.copy())
+        Dm = sq_dist_all(X, centres)
+        lab, d1, gap = argmin_with_gap(Dm)
+        res.objective[t] = float(np.sum(w * d1))
+        res.gaps.append(gap)
+        res.labels_hist.append(lab)
+        cw = np.bincount(lab, weights=w, minlength=k2)
+        new = centres.copy()
+        for j in range(k2):
+            if cw[j] > 0:
+                sel = lab == j
+                new[j] = np.sum(w[sel, None] * X[sel], axis=0) / cw[j]
+        centres = new
+        res.labels = lab
+        res.cluster_w = cw
+    if check_monotone:
+        # P8: J_{t+1} <= J_t up to rounding; the slack is relative to the data scale
+        # sum_l w_l ||X_l||^2 so exact-zero objectives tolerate the rounding of a mean.
+        ob = res.objective
+        scale = float(np.sum(w * np.sum(X * X, axis=1)))
+        for t in range(1, iters):
+            if ob[t] > ob[t - 1] + 1e-12 * (ob[t - 1] + scale):
+                raise AssertionError(f"Lloyd objective increased at t={t}: {ob[t-1]} -> {ob[t]}")
+    res.centres = centres
+    return res
+
+
+def encoding_error(X, reps, assignment, w=None):
+    """Eq. 3 / Eq. 6: sum_l w_l ||X_l - X_{reps[s(l)]}||^2."""
+    X = np.asarray(X, np.float64)
+    if w is None:
+        w = np.ones(X.shape[0])
+    Z = X[np.asarray(reps, dtype=np.int64)][np.asarray(assignment, dtype=np.int64)]
+    return float(np.sum(np.asarray(w) * np.sum((X - Z) ** 2, axis=1)))
+
+
+@dataclass
+class SnapResult:
+    reps_sorted: np.ndarray   # the follow-up index set, ascending
+    rep_of_centre: np.ndarray  # representative chosen by centre j
+    gap: np.ndarray           # relative gap best vs runner-up untaken point, per centre
+    order: np.ndarray         # visiting order of centres
+
+
+def snap(X, centres, cluster_w):
+    """P:169 "any k-means clustering center will be replaced with its closest
+    in-sample point"; duplicates resolved greedily in order (-omega_j, j), each
+    centre taking its nearest untaken point, lowest index on ties (Z13)."""
+    X = np.asarray(X, np.float64)
+    k2 = centres.shape[0]
+    order = sorted(range(k2), key=lambda j: (-float(cluster_w[j]), j))
+    taken = np.zeros(X.shape[0], dtype=bool)
+    rep = np.full(k2, -1, dtype=np.int64)
+    gap = np.zeros(k2)
+    for j in order:
+        d = sq_dist(X, centres[j])
+        d = np.where(taken, np.inf, d)
+        l = int(np.argmin(d))
+        if not np.isfinite(d[l]):
+            raise ValueError("no untaken point left for centre")
+        d1 = d[l]
+        d[l] = np.inf
+        d2 = float(np.min(d)) if d.size > 1 else np.inf
+        gap[j] = (d2 - d1) / d2 if (np.isfinite(d2) and d2 > 0) else (0.0 if d2 == 0 else np.inf)
+        rep[j] = l
+        taken[l] = True
+    return SnapResult(reps_sorted=np.sort(rep), rep_of_centre=rep, gap=gap,
+                      order=np.array(order, dtype=np.int64))
+
+
+# --------------------------------------------------------------------------
+# Residual  ||A - U diag(s) V^T||_F -- the evaluation step
+# --------------------------------------------------------------------------
+def residual(A, F, G, s=None, block=2048):
+    """Returns (r^2, a^2) with r^2 = sum_ij (A - F diag(s) G^T)_ij^2, a^2 = sum A^2,
+    accumulated in float64 over row blocks (O9)."""
+    F = np.asarray(F, np.float64)
+    G = np.asarray(G, np.float64)
+    if s is not None:
+        F = F * np.asarray(s, np.float64)[None, :]
+    r2 = 0.0
+    a2 = 0.0
+    for i in range(0, A.shape[0], block):
+        Ab = np.asarray(A[i:i + block], np.float64)
+        E = Ab - F[i:i + block] @ G.T
+        r2 += float(np.sum(E * E))
+        a2 += float(np.sum(Ab * Ab))
+    return r2, a2
+
+
+def relative_error(A, F, G, s=None):
+    r2, a2 = residual(A, F, G, s)
+    if a2 == 0.0:
+        raise ZeroDivisionError("||A||_F = 0: relative error undefined")
+    return math.sqrt(r2 / a2)
+
+
+# --------------------------------------------------------------------------
+# Algorithm 2 end to end
+# --------------------------------------------------------------------------
+@dataclass
+class CabsResult:
+    I: np.ndarray
+    J: np.ndarray
+    pilot: Sketch
+    P: np.ndarray
+    Q: np.ndarray
+    km_rows: KmeansResult
+    km_cols: KmeansResult
+    snap_rows: SnapResult
+    snap_cols: SnapResult
+    Ibar: np.ndarray
+    Jbar: np.ndarray
+    follow: Sketch
+    resid_sq: float = float("nan")
+    a_sq: float = float("nan")
+
+
+def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
+             weight_kind=WEIGHT_CONST, weight_p=2.0, I=None, J=None,
+             init_rows=None, init_cols=None, with_residual=True):
+    """Algorithm 2 plus the evaluation residual."""
+    m, n = A.shape
+    if not (1 <= k1 <= min(m, n)) or not (1 <= k2 <= min(m, n)):
+        raise ValueError("need 1 <= k1, k2 <= min(m, n)")
+    # step 1: pilot sampling
+    if I is None:
+        I = rng.floyd(m, k1, seed, rng.TAG_PILOT_ROWS)
+    if J is None:
+        J = rng.floyd(n, k1, seed, rng.TAG_PILOT_COLS)
+    C, R, W = gather(A, I, J)
+    # step 2: pilot sketching, P = U S^1/2, Q = V S^1/2
+    pilot = sketch(C, R, W, m, n, k1, mode, tol)
+    P, Q = embeddings(pilot)
+    # step 3: weighted k-means on P and Q, snap to in-sample points
+    km_r = lloyd(P, k2, iters, weights(P, weight_kind, weight_p), init_idx=init_rows,
+                 seed=seed, tag=rng.TAG_INIT_ROWS)
+    km_c = lloyd(Q, k2, iters, weights(Q, weight_kind, weight_p), init_idx=init_cols,
+                 seed=seed, tag=rng.TAG_INIT_COLS)
+    sn_r = snap(P, km_r.centres, km_r.cluster_w)
+    sn_c = snap(Q, km_c.centres, km_c.cluster_w)
+    Ib, Jb = sn_r.reps_sorted, sn_c.reps_sorted
+    # step 4: follow-up sketching
+    Cb, Rb, Wb = gather(A, Ib, Jb)
+    follow = sketch(Cb, Rb, Wb, m, n, k2, mode, tol)
+    res = CabsResult(I=I, J=J, pilot=pilot, P=P, Q=Q, km_rows=km_r, km_cols=km_c,
+                     snap_rows=sn_r, snap_cols=sn_c, Ibar=Ib, Jbar=Jb, follow=follow)
+    if with_residual:
+        res.resid_sq, res.a_sq = residual(A, follow.U, follow.V, follow.s)
+    return res

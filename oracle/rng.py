@@ -1,0 +1,135 @@
+"""Counter-based RNG of the method, oracle side (TEST INFRASTRUCTURE ONLY).
+
+Implements, from the written specification (SURVEY.md §8(c)
+Z17), the randomness that Algorithm 2 step 1 needs: "randomly select k columns
+and k rows" (Alg. 2 step 1) -- uniform sampling without
+replacement, deterministic per seed.
+
+* Philox4x32-10 (Salmon et al., SC'11), key = (seed mod 2^32, seed >> 32).
+* Sequential word stream w(q) = Philox(ctr=(b mod 2^32, b >> 32, tag, 0))[q mod 4]
+  with b = floor(q / 4).
+* Lemire multiply-shift bounded integer in [0, s) with rejection.
+* Floyd's algorithm for k distinct values in [0, N), output sorted ascending.
+
+Everything is integer arithmetic on Python ints (or numpy uint64), so the GPU
+implementation must agree bit for bit.  Shares no code with the CUDA path.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+M32 = 0xFFFFFFFF
+PHILOX_M0 = 0xD2511F53
+PHILOX_M1 = 0xCD9E8D57
+PHILOX_W0 = 0x9E3779B9
+PHILOX_W1 = 0xBB67AE85
+
+# Tags (SURVEY.md §8(c) Z17 / DESIGN.md "RNG").
+TAG_PILOT_ROWS = 1
+TAG_PILOT_COLS = 2
+TAG_INIT_ROWS = 3
+TAG_INIT_COLS = 4
+TAG_RESIDUAL_PAIRS = 5
+
+
+def philox4x32_10(ctr, key):
+    """One Philox4x32-10 block: 4 x uint32 counter, 2 x uint32 key -> 4 x uint32."""
+    c0, c1, c2, c3 = (int(x) & M32 for x in ctr)
+    k0, k1 = (int(x) & M32 for x in key)
+    for rnd in range(10):
+        p0 = PHILOX_M0 * c0
+        p1 = PHILOX_M1 * c2
+        hi0, lo0 = p0 >> 32, p0 & M32
+        hi1, lo1 = p1 >> 32, p1 & M32
+        c0, c1, c2, c3 = (hi1 ^ c1 ^ k0) & M32, lo1, (hi0 ^ c3 ^ k1) & M32, lo0
+        if rnd != 9:
+            k0 = (k0 + PHILOX_W0) & M32
+            k1 = (k1 + PHILOX_W1) & M32
+    return (c0, c1, c2, c3)
+
+
+def philox4x32_10_np(c0, c1, c2, c3, k0, k1):
+    """Vectorised Philox4x32-10 over numpy arrays of counters (uint64 holding uint32)."""
+    c0 = np.asarray(c0, dtype=np.uint64) & np.uint64(M32)
+    c1 = np.asarray(c1, dtype=np.uint64) & np.uint64(M32)
+    c2 = np.asarray(c2, dtype=np.uint64) & np.uint64(M32)
+    c3 = np.asarray(c3, dtype=np.uint64) & np.uint64(M32)
+    c0, c1, c2, c3 = np.broadcast_arrays(c0, c1, c2, c3)
+    k0 = np.uint64(int(k0) & M32)
+    k1 = np.uint64(int(k1) & M32)
+    m0, m1 = np.uint64(PHILOX_M0), np.uint64(PHILOX_M1)
+    mask, sh = np.uint64(M32), np.uint64(32)
+    for rnd in range(10):
+        p0 = m0 * c0  # < 2^64, exact in uint64
+        p1 = m1 * c2
+        hi0, lo0 = p0 >> sh, p0 & mask
+        hi1, lo1 = p1 >> sh, p1 & mask
+        c0, c1, c2, c3 = (hi1 ^ c1 ^ k0) & mask, lo1, (hi0 ^ c3 ^ k1) & mask, lo0
+        if rnd != 9:
+            k0 = np.uint64((int(k0) + PHILOX_W0) & M32)
+            k1 = np.uint64((int(k1) + PHILOX_W1) & M32)
+    return c0, c1, c2, c3
+
+
+def seed_key(seed: int):
+    seed = int(seed) & ((1 << 64) - 1)
+    return (seed & M32, seed >> 32)
+
+
+class WordStream:
+    """Sequential consumer of 32-bit words w(0), w(1), ... for (seed, tag)."""
+
+    def __init__(self, seed: int, tag: int):
+        self.key = seed_key(seed)
+        self.tag = int(tag) & M32
+        self.q = 0
+        self._block = None
+        self._block_id = -1
+
+    def word(self, q: int) -> int:
+        b = q // 4
+        if b != self._block_id:
+            self._block = philox4x32_10((b & M32, (b >> 32) & M32, self.tag, 0), self.key)
+            self._block_id = b
+        return self._block[q % 4]
+
+    def next(self) -> int:
+        w = self.word(self.q)
+        self.q += 1
+        return w
+
+
+def lemire_accept(x: int, s: int):
+    """Lemire multiply-shift step: returns (accepted, value) for word x and bound s."""
+    m = x * s
+    lo = m & M32
+    if lo < s:
+        thresh = ((1 << 32) - s) % s
+        if lo < thresh:
+            return False, None
+    return True, m >> 32
+
+
+def bounded(stream: WordStream, s: int) -> int:
+    """Uniform integer in [0, s), 1 <= s <= 2^32, drawing more words on rejection."""
+    if not (1 <= s <= (1 << 32)):
+        raise ValueError("bound out of range")
+    while True:
+        ok, v = lemire_accept(stream.next(), s)
+        if ok:
+            return v
+
+
+def floyd(N: int, k: int, seed: int, tag: int) -> np.ndarray:
+    """k distinct indices uniform in [0, N) (Floyd), sorted ascending, int64.
+
+    P:195 "randomly select k columns and k rows"; S:137-141 (k > N is an error).
+    """
+    if k < 0 or k > N:
+        raise ValueError(f"cannot draw k={k} distinct indices from N={N}")
+    stream = WordStream(seed, tag)
+    chosen = set()
+    for j in range(N - k, N):
+        t = bounded(stream, j + 1)
+        chosen.add(j if t in chosen else t)
+    return np.array(sorted(chosen), dtype=np.int64)
