@@ -1,0 +1,227 @@
+/*
+ * cabs.h -- C ABI of libcabs.so, the B200 (sm_100a) hot path of Cascaded
+ * Bilateral Sampling (CABS, arXiv 1607.07395).
+ *
+ * Citation keys: P:n = PAPER.md line n (the paper), S:n = SPEC.md line n.
+ *
+ * The method (Algorithm 2):
+ *   1. pilot sampling  : k1 uniform rows I and columns J; C = A(:,J), R = A(I,:),
+ *                        W = A(I,J)
+ *   2. pilot sketching : [U,S,V] = sketching(C,R,W); P = U S^1/2, Q = V S^1/2
+ *   3. follow-up       : weighted k-means on P and on Q, each centre snapped to
+ *                        its closest in-sample point -> Ibar, Jbar
+ *   4. follow-up sketch: [Ubar,Sbar,Vbar] = sketching(Cbar,Rbar,Wbar)
+ *   5. evaluation      : ||A - Ubar Sbar Vbar^T||_F
+ * The `sketching` routine is the paper's stabilized variant of the pseudo-skeleton
+ * (P:222-232); the plain pseudo-skeleton A ~ C W^+ R (Eq. 2) is a mode.
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ * - Memory: every pointer argument is DEVICE memory allocated by the caller,
+ *   unless the parameter comment says "host".  The library never allocates
+ *   device memory; it uses the caller's workspace `ws` of at least
+ *   cabs_workspace_bytes(plan) bytes (256-byte aligned).
+ * - Layout: dense matrices are row-major float32 with an explicit leading
+ *   dimension (elements).  Index arrays are int64, sorted ascending on output.
+ *   Factor buffers (C, P, Q, U, V, F, G, centres) must have ld >= k; columns
+ *   [r, ld) are written as zeros, so ld = cabs_padded_ld(k) is recommended.
+ * - Execution: asynchronous, stream-ordered on `stream` (a cudaStream_t; NULL =
+ *   legacy default stream).  No host synchronisation inside the hot path except
+ *   where a comment says so.  Reentrant across distinct (workspace, stream) pairs.
+ * - Errors: argument checks are synchronous and return a cabs_status.  Data-
+ *   dependent errors (non-finite input S:21/S:71, out-of-range or duplicate
+ *   supplied index S:62/S:66, snap exhaustion) set bits of a device status word
+ *   in `ws`, read with cabs_device_status().  A rank-0 sketch is not an error
+ *   (S:245): it yields r = 0.  No C++ exception crosses this ABI.
+ * - Multi-GPU: one process per GPU; A is split into contiguous row blocks and the
+ *   column-side embedding into contiguous column slices (cabs_plan).  Collectives
+ *   are delegated to the caller through cabs_comm (sum-allreduce callbacks,
+ *   stream-ordered).  comm == NULL or nranks == 1 means single GPU.
+ */
+#ifndef CABS_H_
+#define CABS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CABS_VERSION_MAJOR 0
+#define CABS_VERSION_MINOR 1
+#define CABS_KMAX 1024 /* largest supported k1, k2 */
+
+typedef enum {
+  CABS_OK = 0,
+  CABS_ERR_INVALID_ARG = 1, /* k < 1, k > min(m,n), iters < 1, bad mode/ld */
+  CABS_ERR_RANGE = 2,       /* supplied index out of range / duplicated */
+  CABS_ERR_DEGENERATE = 3,  /* ||A||_F = 0 where a relative error is asked */
+  CABS_ERR_CUDA = 4,        /* CUDA runtime failure; see cabs_last_error_string() */
+  CABS_ERR_COMM = 5,        /* a cabs_comm callback returned nonzero */
+  CABS_ERR_WORKSPACE = 6    /* ws NULL or smaller than cabs_workspace_bytes() */
+} cabs_status;
+
+/* Device status word bits (cabs_device_status). */
+#define CABS_DEV_NONFINITE 0x1u      /* a gathered entry of A was NaN/Inf */
+#define CABS_DEV_RANGE 0x2u          /* supplied index out of range */
+#define CABS_DEV_DUPLICATE 0x4u      /* supplied indices not distinct */
+#define CABS_DEV_SNAP_EXHAUSTED 0x8u /* multi-GPU snap ran out of candidates */
+#define CABS_DEV_TOO_FEW_POINTS 0x10u /* fewer than k2 points with nonzero weight */
+#define CABS_DEV_SVD_NOCONV 0x20u    /* Jacobi SVD hit its sweep cap */
+
+typedef enum {
+  CABS_STABILIZED = 0,     /* the paper's routine: U = C V_w N_c^-1, V = R^T U_w N_r^-1,
+                              S = Sigma_w sqrt(mn)/k */
+  CABS_PSEUDO_SKELETON = 1 /* Eq. 2: same factors, S = N_c N_r Sigma_w^-1 so that
+                              U S V^T = C W_r^+ R exactly */
+} cabs_mode;
+
+typedef enum {
+  CABS_WEIGHT_CONST = 0, /* Upsilon = 1 (dense matrices) */
+  CABS_WEIGHT_POWER = 1  /* Upsilon(x) = x^p (Eq. 6) */
+} cabs_weight_kind;
+
+/* Partition of the global m x n problem for this rank (host struct). */
+typedef struct cabs_plan {
+  int64_t m, n;                 /* global matrix dims */
+  int64_t row_begin, row_end;   /* rows of A held by this rank (P rows follow them) */
+  int64_t col_begin, col_end;   /* columns whose embedding rows (Q, V) this rank owns */
+  int32_t kmax;                 /* max(k1, k2) used with this workspace, <= CABS_KMAX */
+  int32_t rank, nranks;
+} cabs_plan;
+
+/* Dense float32 source (host struct).  Row i of the rank's block is at a + (i - row_begin)*lda. */
+typedef struct cabs_source {
+  const float* a; /* device, (row_end - row_begin) x n, row-major */
+  int64_t lda;    /* >= n */
+} cabs_source;
+
+/* Collectives supplied by the caller (host struct).  Each callback sums `count`
+ * elements of the device buffer `buf` in place across all ranks, ordered on
+ * `stream`, and returns 0 on success. */
+typedef struct cabs_comm {
+  int32_t rank, nranks;
+  int32_t (*allreduce_f64)(double* buf, int64_t count, void* ctx, void* stream);
+  int32_t (*allreduce_f32)(float* buf, int64_t count, void* ctx, void* stream);
+  void* ctx;
+} cabs_comm;
+
+/* ---------------------------------------------------------------- utilities */
+const char* cabs_status_string(int32_t status);
+const char* cabs_last_error_string(void);
+void cabs_version(int32_t* major, int32_t* minor);
+/* Recommended leading dimension for k-column factor buffers: k rounded up to 32. */
+int64_t cabs_padded_ld(int32_t k);
+/* Workspace bytes needed by every entry point for this plan. */
+size_t cabs_workspace_bytes(const cabs_plan* plan);
+/* Zero the device status word (stream-ordered). */
+int32_t cabs_clear_status(void* ws, void* stream);
+/* Synchronises `stream`, then copies the device status word to host *flags. */
+int32_t cabs_device_status(const void* ws, void* stream, uint32_t* flags);
+
+/* ---------------------------------------------------------------- S1-S3 pilot
+ * Algorithm 2 step 1: I = Floyd(m, k, seed, tag 1), J = Floyd(n, k, seed,
+ * tag 2) with the Philox4x32-10 / Lemire / Floyd generator of DESIGN.md "RNG";
+ * both sorted ascending.  C = A(:,J) for this rank's rows (m_loc x k, ldc);
+ * R = A(I,:) as k x n (ldr >= n), complete on every rank after the comm step;
+ * W = A(I,J) (k x k, ldw >= k).  Gathers are bit-exact copies.
+ * I, J: device int64[k].  Errors: k < 1 or k > min(m, n) -> INVALID_ARG. */
+int32_t cabs_pilot(const cabs_plan* plan, const cabs_source* src, int32_t k, uint64_t seed,
+                   int64_t* I, int64_t* J, float* C, int64_t ldc, float* R, int64_t ldr,
+                   float* W, int64_t ldw, void* ws, size_t ws_bytes, const cabs_comm* comm,
+                   void* stream);
+
+/* ---------------------------------------------------------------- S4-S5 embed
+ * Algorithm 2 step 2 using the sketching routine:
+ * W = U_w Sigma_w V_w^T (FP64 one-sided Jacobi; sigma descending; truncated to
+ * sigma_i > tol*sigma_1; canonical signs: largest-|.| entry of each U_w column
+ * positive), Y_c = C V_w, Y_r = R^T U_w, N_c/N_r their column norms, components
+ * with zero norm dropped; s_i = sigma_i sqrt(mn)/k (STABILIZED) or
+ * N_c,i N_r,i / sigma_i (PSEUDO_SKELETON); P = Y_c diag(sqrt(s)/N_c) (m_loc x k,
+ * ldp), Q = Y_r diag(sqrt(s)/N_r) for columns [col_begin, col_end) (ldq).
+ * Outputs: s (float[k], zeros past r), r (device int32), sigma (optional, device
+ * double[k], singular values of W before truncation, NULL to skip).
+ * k = number of sampled rows = sampled columns (Z3). */
+int32_t cabs_embed(const cabs_plan* plan, int32_t k, const float* C, int64_t ldc,
+                   const float* R, int64_t ldr, const float* W, int64_t ldw, int32_t mode,
+                   double tol, float* P, int64_t ldp, float* Q, int64_t ldq, float* s,
+                   int32_t* r, double* sigma, void* ws, size_t ws_bytes,
+                   const cabs_comm* comm, void* stream);
+
+/* ---------------------------------------------------------------- S6-S7 k-means
+ * Weighted Lloyd k-means (Eq. 6; c iterations) on the rows of
+ * X (n_loc local rows of n_glob, global index = row_off + local, d columns, ldx).
+ * Weights w_l = Upsilon(||X_l||) (weight_kind, weight_p).  Init: centres =
+ * X[init_idx] if init_idx != NULL (device int64[k2], global indices), else
+ * init_centres (device k2 x ldc) if != NULL, else X[Floyd(n_glob, k2, seed, tag)].
+ * Each iteration t: s(l) = argmin_j ||X_l - c_j||^2 (direct differences, FP32,
+ * lowest j on ties), objective[t] = sum_l w_l min_j d (FP64); every cluster with
+ * positive weight moves to its weighted mean, an empty one keeps its centre.
+ * Outputs: centres (k2 x ldc, after the last update), labels (int32[n_loc], last
+ * assignment), cluster_w (double[k2], weights of the last assignment),
+ * objective (double[iters]), near_ties (int32[iters] or NULL: points whose
+ * FP32 relative gap (d2-d1)/d2 < 1e-5, north_star near-tie rule). */
+int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t n_loc,
+                    int64_t n_glob, int64_t row_off, int32_t d, int32_t k2, int32_t iters,
+                    int32_t weight_kind, float weight_p, uint64_t seed, int32_t tag,
+                    const int64_t* init_idx, const float* init_centres, float* centres,
+                    int64_t ldc, int32_t* labels, double* cluster_w, double* objective,
+                    int32_t* near_ties, void* ws, size_t ws_bytes, const cabs_comm* comm,
+                    void* stream);
+
+/* ---------------------------------------------------------------- S8 select
+ * Snap ("any k-means clustering center will be replaced with its closest
+ * in-sample point"): centres visited in order (-cluster_w[j], j), each taking its
+ * nearest not-yet-taken point over all n_glob points (FP32 direct differences;
+ * ties -> lowest index).  Outputs: reps (int64[k2], sorted ascending: the
+ * follow-up index set), rep_of_centre (int64[k2] or NULL), gap (float[k2] or
+ * NULL: relative gap between the best and runner-up untaken point). */
+int32_t cabs_select(const cabs_plan* plan, const float* X, int64_t ldx, int64_t n_loc,
+                    int64_t n_glob, int64_t row_off, int32_t d, const float* centres,
+                    int64_t ldc, int32_t k2, const double* cluster_w, int64_t* reps,
+                    int64_t* rep_of_centre, float* gap, void* ws, size_t ws_bytes,
+                    const cabs_comm* comm, void* stream);
+
+/* ---------------------------------------------------------------- S9 sketch
+ * Follow-up sketching, or a sketch from any given index sets:
+ * gathers Cbar = A(:,Ic), Rbar = A(Ir,:), Wbar = A(Ir,Ic) (Ir, Ic: device int64[k],
+ * distinct, in range; else status bits RANGE/DUPLICATE), then the sketching
+ * routine as in cabs_embed with output U = Y_c N_c^-1 (m_loc x k, ldu),
+ * V = Y_r N_r^-1 (columns [col_begin, col_end), ldv), s (float[k]), r (int32).
+ * A ~ U diag(s) V^T. */
+int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t* Ir,
+                    const int64_t* Ic, int32_t k, int32_t mode, double tol, float* U,
+                    int64_t ldu, float* s, float* V, int64_t ldv, int32_t* r, double* sigma,
+                    void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream);
+
+/* ---------------------------------------------------------------- S10 residual
+ * Evaluation ("error ||A - A~||_F/||A||_F"): out[0] = sum_ij (A - F diag(s)
+ * G^T)_ij^2 and out[1] = sum_ij A_ij^2 over the global matrix (FP64, reduced over
+ * ranks).  F: this rank's m_loc x ncomp (ldf); G: all n rows x ncomp (ldg);
+ * s: float[ncomp] or NULL (= ones).  The reconstruction is never materialised.
+ * out: device double[2]. */
+int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float* F,
+                      int64_t ldf, const float* s, const float* G, int64_t ldg, int32_t ncomp,
+                      double* out, void* ws, size_t ws_bytes, const cabs_comm* comm,
+                      void* stream);
+
+/* ---------------------------------------------------------------- test hooks
+ * Building blocks exposed for step-level parity tests (same kernels as above). */
+/* Philox4x32-10 blocks: out[4*b + i] = Philox(ctr=(start+b lo, hi, tag, 0), key=seed)[i]. */
+int32_t cabs_philox_blocks(uint64_t seed, uint32_t tag, uint64_t start, int64_t count,
+                           uint32_t* out, void* stream);
+/* Floyd sample of k distinct values in [0, N), sorted (the generator of cabs_pilot). */
+int32_t cabs_uniform_indices(int64_t N, int32_t k, uint64_t seed, uint32_t tag, int64_t* out,
+                             void* stream);
+/* FP64 Jacobi SVD of W (k x k, ldw): sigma (double[k], descending, all k), Uw, Vw
+ * (double k x k row-major, column i = i-th singular vector, canonical signs,
+ * columns >= r zeroed), r (int32: count of sigma_i > tol*sigma_1). */
+int32_t cabs_svd(const cabs_plan* plan, int32_t k, const float* W, int64_t ldw, double tol,
+                 double* sigma, double* Uw, double* Vw, int32_t* r, void* ws, size_t ws_bytes,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CABS_H_ */

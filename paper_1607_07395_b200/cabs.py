@@ -1,0 +1,242 @@
+"""ctypes binding of libcabs.so -- argument marshalling only.
+
+Every function here has the name of the C entry point it wraps (include/cabs.h)
+and does nothing but convert torch tensors to (pointer, leading dimension) pairs,
+call the library and raise on a non-zero status.  Every step of the CABS path
+runs in the CUDA kernels of libcabs.so; there is no CPU fallback: if the library
+is missing this module raises at import of the first call.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import build as _build
+
+_LIB = None
+
+c_i32, c_i64, c_u32, c_u64, c_f32, c_f64 = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
+                                              ctypes.c_uint64, ctypes.c_float, ctypes.c_double)
+c_vp, c_sz = ctypes.c_void_p, ctypes.c_size_t
+
+STABILIZED = 0
+PSEUDO_SKELETON = 1
+WEIGHT_CONST = 0
+WEIGHT_POWER = 1
+KMAX = 1024
+
+DEV_NONFINITE = 0x1
+DEV_RANGE = 0x2
+DEV_DUPLICATE = 0x4
+DEV_SNAP_EXHAUSTED = 0x8
+DEV_TOO_FEW_POINTS = 0x10
+DEV_SVD_NOCONV = 0x20
+
+TAG_PILOT_ROWS, TAG_PILOT_COLS, TAG_INIT_ROWS, TAG_INIT_COLS = 1, 2, 3, 4
+
+
+class CabsError(RuntimeError):
+    pass
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [("m", c_i64), ("n", c_i64), ("row_begin", c_i64), ("row_end", c_i64),
+                ("col_begin", c_i64), ("col_end", c_i64), ("kmax", c_i32), ("rank", c_i32),
+                ("nranks", c_i32)]
+
+    @property
+    def m_loc(self):
+        return self.row_end - self.row_begin
+
+    @property
+    def n_sl(self):
+        return self.col_end - self.col_begin
+
+
+class Source(ctypes.Structure):
+    _fields_ = [("a", c_vp), ("lda", c_i64)]
+
+
+ALLREDUCE_FN = ctypes.CFUNCTYPE(c_i32, c_vp, c_i64, c_vp, c_vp)
+
+
+class Comm(ctypes.Structure):
+    _fields_ = [("rank", c_i32), ("nranks", c_i32), ("allreduce_f64", ALLREDUCE_FN),
+                ("allreduce_f32", ALLREDUCE_FN), ("ctx", c_vp)]
+
+
+_SIGS = {
+    "cabs_status_string": (ctypes.c_char_p, [c_i32]),
+    "cabs_last_error_string": (ctypes.c_char_p, []),
+    "cabs_version": (None, [ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
+    "cabs_padded_ld": (c_i64, [c_i32]),
+    "cabs_workspace_bytes": (c_sz, [ctypes.POINTER(Plan)]),
+    "cabs_clear_status": (c_i32, [c_vp, c_vp]),
+    "cabs_device_status": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_u32)]),
+    "cabs_pilot": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_i32, c_u64, c_vp, c_vp,
+                           c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_embed": (c_i32, [ctypes.POINTER(Plan), c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i32,
+                           c_f64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_sz,
+                           ctypes.POINTER(Comm), c_vp]),
+    "cabs_kmeans": (c_i32, [ctypes.POINTER(Plan), c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32,
+                            c_i32, c_f32, c_u64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,
+                            c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_select": (c_i32, [ctypes.POINTER(Plan), c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_vp, c_i64,
+                            c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_sketch": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_vp, c_vp, c_i32, c_i32, c_f64,
+                            c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz,
+                            ctypes.POINTER(Comm), c_vp]),
+    "cabs_residual": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_vp, c_i64, c_vp, c_vp, c_i64,
+                              c_i32, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_philox_blocks": (c_i32, [c_u64, c_u32, c_u64, c_i64, c_vp, c_vp]),
+    "cabs_uniform_indices": (c_i32, [c_i64, c_i32, c_u64, c_u32, c_vp, c_vp]),
+    "cabs_svd": (c_i32, [ctypes.POINTER(Plan), c_i32, c_vp, c_i64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                         c_sz, c_vp]),
+}
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_stale: bool = False):
+    """Load libcabs.so (in-tree).  Raises if it is missing: there is no fallback."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if build_if_stale:
+        _build.build()
+    path = lib_path()
+    if not os.path.exists(path):
+        raise CabsError(f"libcabs.so not found at {path}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _LIB = L
+    return L
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        L = load()
+        raise CabsError(f"{what}: {L.cabs_status_string(status).decode()} "
+                        f"({L.cabs_last_error_string().decode()})")
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _ld(t):
+    if t.dim() == 1:
+        return t.shape[0]
+    assert t.stride(1) == 1, "row-major tensors only"
+    return t.stride(0)
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _comm(comm):
+    return None if comm is None else ctypes.byref(comm.c)
+
+
+# ---------------------------------------------------------------- utilities
+def cabs_padded_ld(k: int) -> int:
+    return int(load().cabs_padded_ld(int(k)))
+
+
+def cabs_workspace_bytes(plan: Plan) -> int:
+    n = int(load().cabs_workspace_bytes(ctypes.byref(plan)))
+    if n == 0:
+        raise CabsError("invalid plan")
+    return n
+
+
+def cabs_version():
+    a, b = c_i32(), c_i32()
+    load().cabs_version(ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value
+
+
+def cabs_clear_status(ws, stream=None):
+    _check(load().cabs_clear_status(_p(ws), _stream(stream)), "cabs_clear_status")
+
+
+def cabs_device_status(ws, stream=None) -> int:
+    f = c_u32()
+    _check(load().cabs_device_status(_p(ws), _stream(stream), ctypes.byref(f)), "cabs_device_status")
+    return f.value
+
+
+# ---------------------------------------------------------------- entry points
+def cabs_pilot(plan, A, k, seed, I, J, C, R, W, ws, comm=None, stream=None):
+    src = Source(A.data_ptr(), _ld(A))
+    _check(load().cabs_pilot(ctypes.byref(plan), ctypes.byref(src), int(k), int(seed), _p(I), _p(J),
+                             _p(C), _ld(C), _p(R), _ld(R), _p(W), _ld(W), _p(ws), ws.numel(),
+                             _comm(comm), _stream(stream)), "cabs_pilot")
+
+
+def cabs_embed(plan, k, C, R, W, mode, tol, P, Q, s, r, ws, sigma=None, comm=None, stream=None):
+    _check(load().cabs_embed(ctypes.byref(plan), int(k), _p(C), _ld(C), _p(R), _ld(R), _p(W), _ld(W),
+                             int(mode), float(tol), _p(P), _ld(P), _p(Q), _ld(Q), _p(s), _p(r),
+                             _p(sigma), _p(ws), ws.numel(), _comm(comm), _stream(stream)), "cabs_embed")
+
+
+def cabs_kmeans(plan, X, n_loc, n_glob, row_off, d, k2, iters, weight_kind, weight_p, seed, tag,
+                centres, labels, cluster_w, objective, ws, near_ties=None, init_idx=None,
+                init_centres=None, comm=None, stream=None):
+    _check(load().cabs_kmeans(ctypes.byref(plan), _p(X), _ld(X), int(n_loc), int(n_glob), int(row_off),
+                              int(d), int(k2), int(iters), int(weight_kind), float(weight_p), int(seed),
+                              int(tag), _p(init_idx), _p(init_centres), _p(centres), _ld(centres),
+                              _p(labels), _p(cluster_w), _p(objective), _p(near_ties), _p(ws), ws.numel(),
+                              _comm(comm), _stream(stream)), "cabs_kmeans")
+
+
+def cabs_select(plan, X, n_loc, n_glob, row_off, d, centres, k2, cluster_w, reps, ws,
+                rep_of_centre=None, gap=None, comm=None, stream=None):
+    _check(load().cabs_select(ctypes.byref(plan), _p(X), _ld(X), int(n_loc), int(n_glob), int(row_off),
+                              int(d), _p(centres), _ld(centres), int(k2), _p(cluster_w), _p(reps),
+                              _p(rep_of_centre), _p(gap), _p(ws), ws.numel(), _comm(comm),
+                              _stream(stream)), "cabs_select")
+
+
+def cabs_sketch(plan, A, Ir, Ic, k, mode, tol, U, s, V, r, ws, sigma=None, comm=None, stream=None):
+    src = Source(A.data_ptr(), _ld(A))
+    _check(load().cabs_sketch(ctypes.byref(plan), ctypes.byref(src), _p(Ir), _p(Ic), int(k), int(mode),
+                              float(tol), _p(U), _ld(U), _p(s), _p(V), _ld(V), _p(r), _p(sigma), _p(ws),
+                              ws.numel(), _comm(comm), _stream(stream)), "cabs_sketch")
+
+
+def cabs_residual(plan, A, F, s, G, ncomp, out, ws, comm=None, stream=None):
+    src = Source(A.data_ptr(), _ld(A))
+    _check(load().cabs_residual(ctypes.byref(plan), ctypes.byref(src), _p(F), _ld(F), _p(s), _p(G),
+                                _ld(G), int(ncomp), _p(out), _p(ws), ws.numel(), _comm(comm),
+                                _stream(stream)), "cabs_residual")
+
+
+# ---------------------------------------------------------------- test hooks
+def cabs_philox_blocks(seed, tag, start, count, out, stream=None):
+    _check(load().cabs_philox_blocks(int(seed), int(tag), int(start), int(count), _p(out), _stream(stream)),
+           "cabs_philox_blocks")
+
+
+def cabs_uniform_indices(N, k, seed, tag, out, stream=None):
+    _check(load().cabs_uniform_indices(int(N), int(k), int(seed), int(tag), _p(out), _stream(stream)),
+           "cabs_uniform_indices")
+
+
+def cabs_svd(plan, k, W, tol, sigma, Uw, Vw, r, ws, stream=None):
+    _check(load().cabs_svd(ctypes.byref(plan), int(k), _p(W), _ld(W), float(tol), _p(sigma), _p(Uw),
+                           _p(Vw), _p(r), _p(ws), ws.numel(), _stream(stream)), "cabs_svd")

@@ -1,0 +1,332 @@
+// api.cu -- the extern "C" boundary of libcabs.so (declared and documented in include/cabs.h).
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace cabsk;
+
+static thread_local char g_err[512] = "";
+
+void cabs_set_cuda_error(cudaError_t e, const char* where) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+}
+void cabs_set_error_msg(const char* msg) { snprintf(g_err, sizeof(g_err), "%s", msg); }
+
+static int32_t arg_error(const char* msg) {
+  cabs_set_error_msg(msg);
+  return CABS_ERR_INVALID_ARG;
+}
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static int32_t check_plan(const cabs_plan* p) {
+  if (!p) return arg_error("plan is NULL");
+  if (p->m < 1 || p->n < 1) return arg_error("plan: m, n must be >= 1");
+  if (p->row_begin < 0 || p->row_end < p->row_begin || p->row_end > p->m) return arg_error("plan: bad row range");
+  if (p->col_begin < 0 || p->col_end < p->col_begin || p->col_end > p->n) return arg_error("plan: bad column range");
+  if (p->kmax < 1 || p->kmax > CABS_KMAX) return arg_error("plan: kmax out of [1, CABS_KMAX]");
+  if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return arg_error("plan: bad rank/nranks");
+  return CABS_OK;
+}
+
+static int32_t check_ws(const cabs_plan* p, void* ws, size_t bytes, Ws* L) {
+  *L = ws_layout(*p);
+  if (!ws || bytes < L->total) {
+    cabs_set_error_msg("workspace missing or smaller than cabs_workspace_bytes()");
+    return CABS_ERR_WORKSPACE;
+  }
+  return CABS_OK;
+}
+
+static bool multi(const cabs_comm* c) { return c && c->nranks > 1; }
+
+static int32_t comm_f64(const cabs_comm* c, double* buf, int64_t count, void* stream) {
+  if (!multi(c)) return CABS_OK;
+  if (!c->allreduce_f64 || c->allreduce_f64(buf, count, c->ctx, stream) != 0) {
+    cabs_set_error_msg("allreduce_f64 callback failed");
+    return CABS_ERR_COMM;
+  }
+  return CABS_OK;
+}
+static int32_t comm_f32(const cabs_comm* c, float* buf, int64_t count, void* stream) {
+  if (!multi(c)) return CABS_OK;
+  if (!c->allreduce_f32 || c->allreduce_f32(buf, count, c->ctx, stream) != 0) {
+    cabs_set_error_msg("allreduce_f32 callback failed");
+    return CABS_ERR_COMM;
+  }
+  return CABS_OK;
+}
+
+extern "C" {
+
+const char* cabs_status_string(int32_t s) {
+  switch (s) {
+    case CABS_OK: return "ok";
+    case CABS_ERR_INVALID_ARG: return "invalid argument";
+    case CABS_ERR_RANGE: return "index out of range or duplicated";
+    case CABS_ERR_DEGENERATE: return "degenerate input (||A||_F = 0)";
+    case CABS_ERR_CUDA: return "CUDA error";
+    case CABS_ERR_COMM: return "communication callback failed";
+    case CABS_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+const char* cabs_last_error_string(void) { return g_err; }
+
+void cabs_version(int32_t* major, int32_t* minor) {
+  if (major) *major = CABS_VERSION_MAJOR;
+  if (minor) *minor = CABS_VERSION_MINOR;
+}
+
+int64_t cabs_padded_ld(int32_t k) { return round_up(k < 1 ? 1 : k, 32); }
+
+size_t cabs_workspace_bytes(const cabs_plan* plan) {
+  if (check_plan(plan) != CABS_OK) return 0;
+  return ws_layout(*plan).total;
+}
+
+int32_t cabs_clear_status(void* ws, void* stream) {
+  if (!ws) return CABS_ERR_WORKSPACE;
+  CABS_CUDA_TRY(cudaMemsetAsync(ws, 0, 256, S(stream)));
+  return CABS_OK;
+}
+
+int32_t cabs_device_status(const void* ws, void* stream, uint32_t* flags) {
+  if (!ws || !flags) return CABS_ERR_INVALID_ARG;
+  CABS_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  CABS_CUDA_TRY(cudaMemcpy(flags, ws, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return CABS_OK;
+}
+
+// ---------------------------------------------------------------- test hooks
+int32_t cabs_philox_blocks(uint64_t seed, uint32_t tag, uint64_t start, int64_t count, uint32_t* out, void* stream) {
+  if (count < 0 || (count > 0 && !out)) return arg_error("philox_blocks: bad count/out");
+  launch_philox_blocks(seed, tag, start, count, out, S(stream));
+  CABS_LAUNCH_CHECK("philox_blocks");
+  return CABS_OK;
+}
+
+int32_t cabs_uniform_indices(int64_t N, int32_t k, uint64_t seed, uint32_t tag, int64_t* out, void* stream) {
+  if (k < 0 || k > CABS_KMAX || k > N || N >= 0xFFFFFFFFll) return arg_error("uniform_indices: need 0 <= k <= min(N, KMAX)");
+  if (k == 0) return CABS_OK;
+  launch_floyd2(N, k, tag, out, 0, 0, 0, nullptr, seed, S(stream));
+  CABS_LAUNCH_CHECK("floyd");
+  return CABS_OK;
+}
+
+int32_t cabs_svd(const cabs_plan* plan, int32_t k, const float* W, int64_t ldw, double tol, double* sigma, double* Uw,
+                 double* Vw, int32_t* r, void* ws, size_t ws_bytes, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  if (k < 1 || k > plan->kmax || ldw < k || !W) return arg_error("svd: bad k/ldw");
+  launch_svd(k, W, ldw, tol, ws, L, sigma, Uw, Vw, r, S(stream));
+  CABS_LAUNCH_CHECK("svd");
+  return CABS_OK;
+}
+
+// ---------------------------------------------------------------- S1-S3
+int32_t cabs_pilot(const cabs_plan* plan, const cabs_source* src, int32_t k, uint64_t seed, int64_t* I, int64_t* J,
+                   float* C, int64_t ldc, float* R, int64_t ldr, float* W, int64_t ldw, void* ws, size_t ws_bytes,
+                   const cabs_comm* comm, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  const cabs_plan& p = *plan;
+  if (k < 1 || k > p.kmax || k > p.m || k > p.n) return arg_error("pilot: need 1 <= k <= min(m, n, kmax)");
+  if (!src || !src->a || src->lda < p.n) return arg_error("pilot: bad source");
+  if (!I || !J || !C || !R || !W || ldc < k || ldr < p.n || ldw < k) return arg_error("pilot: bad output buffers");
+  if (p.m >= 0xFFFFFFFFll || p.n >= 0xFFFFFFFFll) return arg_error("pilot: dims must be < 2^32 - 1");
+  cudaStream_t st = S(stream);
+  const int64_t m_loc = p.row_end - p.row_begin;
+  launch_floyd2(p.m, k, 1u, I, p.n, k, 2u, J, seed, st);  // tags ROWS_PILOT = 1, COLS_PILOT = 2
+  CABS_LAUNCH_CHECK("floyd");
+  launch_gather_cols(src->a, src->lda, m_loc, J, k, C, ldc, ws, st);
+  CABS_LAUNCH_CHECK("gather_cols");
+  if (multi(comm)) CABS_CUDA_TRY(cudaMemsetAsync(R, 0, sizeof(float) * ldr * k, st));
+  launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, I, k, p.n, R, ldr, ws, st);
+  CABS_LAUNCH_CHECK("gather_rows");
+  CABS_TRY(comm_f32(comm, R, ldr * (int64_t)k, stream));
+  launch_gather_w(R, ldr, J, k, W, ldw, st);
+  CABS_LAUNCH_CHECK("gather_w");
+  return CABS_OK;
+}
+
+// shared S4-S5 core: kind 0 = pilot embeddings (P, Q), kind 1 = sketch factors (U, V)
+static int32_t embed_core(const cabs_plan& p, const Ws& L, int32_t k, const float* C, int64_t ldc, const float* R,
+                          int64_t ldr, const float* W, int64_t ldw, int32_t mode, double tol, float* Y1, int64_t ld1,
+                          float* Y2, int64_t ld2, float* s, int32_t* r, double* sigma, int kind, void* ws,
+                          const cabs_comm* comm, void* stream) {
+  cudaStream_t st = S(stream);
+  const int64_t m_loc = p.row_end - p.row_begin, n_sl = p.col_end - p.col_begin;
+  launch_svd(k, W, ldw, tol, ws, L, sigma, nullptr, nullptr, nullptr, st);
+  CABS_LAUNCH_CHECK("svd");
+  if (m_loc > 0) CABS_CUDA_TRY(cudaMemsetAsync(Y1, 0, sizeof(float) * ld1 * m_loc, st));
+  if (n_sl > 0) CABS_CUDA_TRY(cudaMemsetAsync(Y2, 0, sizeof(float) * ld2 * n_sl, st));
+  launch_embed_products(m_loc, n_sl, k, C, ldc, R + p.col_begin, ldr, Y1, ld1, Y2, ld2, ws, L, st);
+  CABS_LAUNCH_CHECK("embed_products");
+  double* norms = wsp<double>(ws, L.norms);
+  if (multi(comm)) {
+    // one message carries both norm vectors: [N_c^2 (Kp) | N_r^2 (Kp)]
+    CABS_TRY(comm_f64(comm, norms, 2 * L.Kp, stream));
+  }
+  launch_embed_finalize(k, mode, static_cast<double>(p.m), static_cast<double>(p.n), static_cast<double>(k), kind, s, r,
+                        ws, L, st);
+  CABS_LAUNCH_CHECK("embed_finalize");
+  launch_scale_compact(Y1, ld1, m_loc, k, 0, ws, L, st);
+  launch_scale_compact(Y2, ld2, n_sl, k, 1, ws, L, st);
+  CABS_LAUNCH_CHECK("scale_compact");
+  return CABS_OK;
+}
+
+int32_t cabs_embed(const cabs_plan* plan, int32_t k, const float* C, int64_t ldc, const float* R, int64_t ldr,
+                   const float* W, int64_t ldw, int32_t mode, double tol, float* P, int64_t ldp, float* Q, int64_t ldq,
+                   float* s, int32_t* r, double* sigma, void* ws, size_t ws_bytes, const cabs_comm* comm,
+                   void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  if (k < 1 || k > plan->kmax) return arg_error("embed: bad k");
+  if (mode != CABS_STABILIZED && mode != CABS_PSEUDO_SKELETON) return arg_error("embed: bad mode");
+  if (!C || !R || !W || !P || !Q || !s || ldc < k || ldr < plan->n || ldw < k || ldp < k || ldq < k)
+    return arg_error("embed: bad buffers");
+  return embed_core(*plan, L, k, C, ldc, R, ldr, W, ldw, mode, tol, P, ldp, Q, ldq, s, r, sigma, 0, ws, comm, stream);
+}
+
+int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t* Ir, const int64_t* Ic, int32_t k,
+                    int32_t mode, double tol, float* U, int64_t ldu, float* s, float* V, int64_t ldv, int32_t* r,
+                    double* sigma, void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  const cabs_plan& p = *plan;
+  if (k < 1 || k > p.kmax || k > p.m || k > p.n) return arg_error("sketch: need 1 <= k <= min(m, n, kmax)");
+  if (mode != CABS_STABILIZED && mode != CABS_PSEUDO_SKELETON) return arg_error("sketch: bad mode");
+  if (!src || !src->a || src->lda < p.n || !Ir || !Ic || !U || !V || !s || ldu < k || ldv < k)
+    return arg_error("sketch: bad buffers");
+  cudaStream_t st = S(stream);
+  const int64_t m_loc = p.row_end - p.row_begin;
+  launch_validate_idx(Ir, k, p.m, ws, st);
+  launch_validate_idx(Ic, k, p.n, ws, st);
+  float* Cb = wsp<float>(ws, L.cb);
+  float* Rb = wsp<float>(ws, L.rb);
+  float* Wb = wsp<float>(ws, L.wb);
+  launch_gather_cols(src->a, src->lda, m_loc, Ic, k, Cb, L.Kp, ws, st);
+  if (multi(comm)) CABS_CUDA_TRY(cudaMemsetAsync(Rb, 0, sizeof(float) * L.ldrb * k, st));
+  launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, Ir, k, p.n, Rb, L.ldrb, ws, st);
+  CABS_LAUNCH_CHECK("sketch gathers");
+  CABS_TRY(comm_f32(comm, Rb, L.ldrb * (int64_t)k, stream));
+  launch_gather_w(Rb, L.ldrb, Ic, k, Wb, L.Kp, st);
+  CABS_LAUNCH_CHECK("gather_w");
+  return embed_core(p, L, k, Cb, L.Kp, Rb, L.ldrb, Wb, L.Kp, mode, tol, U, ldu, V, ldv, s, r, sigma, 1, ws, comm,
+                    stream);
+}
+
+// ---------------------------------------------------------------- S6-S7
+int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t n_loc, int64_t n_glob, int64_t row_off,
+                    int32_t d, int32_t k2, int32_t iters, int32_t weight_kind, float weight_p, uint64_t seed,
+                    int32_t tag, const int64_t* init_idx, const float* init_centres, float* centres, int64_t ldc,
+                    int32_t* labels, double* cluster_w, double* objective, int32_t* near_ties, void* ws,
+                    size_t ws_bytes, const cabs_comm* comm, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  if (k2 < 1 || k2 > plan->kmax || k2 > n_glob) return arg_error("kmeans: need 1 <= k2 <= min(n_glob, kmax)");
+  if (iters < 1) return arg_error("kmeans: iters must be >= 1");
+  if (d < 1 || d > L.Kp || ldx < d || ldc < d || n_loc < 0 || n_loc > L.Nmax) return arg_error("kmeans: bad dims");
+  if (weight_kind != CABS_WEIGHT_CONST && weight_kind != CABS_WEIGHT_POWER) return arg_error("kmeans: bad weight");
+  if (!centres || (n_loc > 0 && (!X || !labels)) || !cluster_w || !objective) return arg_error("kmeans: bad buffers");
+  cudaStream_t st = S(stream);
+  float* w = wsp<float>(ws, L.km_w);
+  int* cnt = wsp<int>(ws, L.km_cnt);
+  CABS_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * 4, st));
+  launch_km_weights(X, ldx, n_loc, d, weight_kind, weight_p, w, cnt, st);
+  CABS_LAUNCH_CHECK("km_weights");
+  // initial centres
+  const int64_t* idx = init_idx;
+  if (!init_idx && !init_centres) {
+    int64_t* tmp = wsp<int64_t>(ws, L.idx);
+    launch_floyd2(n_glob, k2, static_cast<uint32_t>(tag), tmp, 0, 0, 0, nullptr, seed, st);
+    CABS_LAUNCH_CHECK("floyd init");
+    idx = tmp;
+  }
+  launch_km_init(X, ldx, n_loc, row_off, d, k2, init_centres ? nullptr : idx, init_centres, ldc, centres, ldc, st);
+  CABS_LAUNCH_CHECK("km_init");
+  if (!init_centres) CABS_TRY(comm_f32(comm, centres, ldc * (int64_t)k2, stream));
+  double* red = wsp<double>(ws, L.km_red);
+  const int64_t payload = (int64_t)k2 * d + k2 + 2;
+  for (int t = 0; t < iters; ++t) {
+    int ga = 1, gacc = 1;
+    if (n_loc > 0) {
+      launch_km_assign(X, ldx, n_loc, d, centres, ldc, k2, w, labels, wsp<double>(ws, L.km_pobj),
+                       wsp<int>(ws, L.km_ptie), &ga, st);
+      launch_km_accum(X, ldx, n_loc, d, labels, w, k2, wsp<float>(ws, L.km_psum), wsp<double>(ws, L.km_pw), L.Kp, &gacc,
+                      st);
+      CABS_LAUNCH_CHECK("km_assign/accum");
+      launch_km_reduce(wsp<float>(ws, L.km_psum), wsp<double>(ws, L.km_pw), gacc, k2, d, L.Kp,
+                       wsp<double>(ws, L.km_pobj), wsp<int>(ws, L.km_ptie), ga, red, st);
+    } else {
+      CABS_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(double) * payload, st));
+    }
+    CABS_LAUNCH_CHECK("km_reduce");
+    CABS_TRY(comm_f64(comm, red, payload, stream));  // ONE fused message per iteration
+    launch_km_finalize(red, k2, d, centres, ldc, objective, near_ties, cluster_w, t, st);
+    CABS_LAUNCH_CHECK("km_finalize");
+  }
+  return CABS_OK;
+}
+
+// ---------------------------------------------------------------- S8
+int32_t cabs_select(const cabs_plan* plan, const float* X, int64_t ldx, int64_t n_loc, int64_t n_glob, int64_t row_off,
+                    int32_t d, const float* centres, int64_t ldc, int32_t k2, const double* cluster_w, int64_t* reps,
+                    int64_t* rep_of_centre, float* gap, void* ws, size_t ws_bytes, const cabs_comm* comm,
+                    void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  if (k2 < 1 || k2 > plan->kmax || k2 > n_glob) return arg_error("select: bad k2");
+  if (d < 1 || ldx < d || ldc < d || n_loc < 0 || n_loc > L.Nmax) return arg_error("select: bad dims");
+  if (!centres || !cluster_w || !reps || (n_loc > 0 && !X)) return arg_error("select: bad buffers");
+  cudaStream_t st = S(stream);
+  float* D = wsp<float>(ws, L.dist);
+  float* cd = wsp<float>(ws, L.cand_d);
+  int64_t* ci = wsp<int64_t>(ws, L.cand_i);
+  const bool mr = multi(comm);
+  const int T = mr ? kSnapTMulti : kSnapT;
+  launch_km_distmat(X, ldx, n_loc, d, centres, ldc, k2, D, L.Nmax, st);
+  launch_snap_topT(D, L.Nmax, n_loc, k2, row_off, T, cd, ci, st);
+  CABS_LAUNCH_CHECK("snap distmat/topT");
+  if (mr) {
+    double* all = wsp<double>(ws, L.cand_all);
+    launch_snap_pack(cd, ci, k2, T, comm->rank, comm->nranks, all, st);
+    CABS_LAUNCH_CHECK("snap_pack");
+    CABS_TRY(comm_f64(comm, all, 2LL * comm->nranks * k2 * T, stream));
+    launch_snap_merge(all, k2, T, comm->nranks, cd, ci, st);
+    CABS_LAUNCH_CHECK("snap_merge");
+  }
+  launch_snap_dedupe(cd, ci, k2, T, cluster_w, D, L.Nmax, n_loc, row_off, !mr, rep_of_centre, gap, reps, ws, st);
+  CABS_LAUNCH_CHECK("snap_dedupe");
+  return CABS_OK;
+}
+
+// ---------------------------------------------------------------- S10
+int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float* F, int64_t ldf, const float* s,
+                      const float* G, int64_t ldg, int32_t ncomp, double* out, void* ws, size_t ws_bytes,
+                      const cabs_comm* comm, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  const cabs_plan& p = *plan;
+  if (!src || !src->a || src->lda < p.n || !F || !G || !out || ncomp < 0 || ldf < ncomp || ldg < ncomp)
+    return arg_error("residual: bad arguments");
+  const int64_t m_loc = p.row_end - p.row_begin;
+  launch_residual(src->a, src->lda, m_loc, p.n, F, ldf, s, G, ldg, ncomp, wsp<double>(ws, L.res_part), out, S(stream));
+  CABS_LAUNCH_CHECK("residual");
+  CABS_TRY(comm_f64(comm, out, 2, stream));
+  return CABS_OK;
+}
+
+}  // extern "C"

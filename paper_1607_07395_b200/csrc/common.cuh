@@ -1,0 +1,144 @@
+// common.cuh -- shared helpers of libcabs (workspace layout, status word, reductions).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/cabs.h"
+
+namespace cabsk {
+
+constexpr int kNumSM = 148;           // B200: 2 dies x 74 SMs
+constexpr int kSnapT = 8;             // per-centre candidate list length in the snap
+constexpr int kSnapTMulti = 32;       // ... when candidates are merged across ranks
+constexpr int kAccGrid = 2 * kNumSM;  // k-means accumulation CTAs (per-CTA partials)
+constexpr int kAssignGrid = 4 * kNumSM;
+constexpr int kResGrid = 8 * kNumSM;  // persistent residual CTAs (upper bound)
+constexpr int kNormTile = 64;         // points per embed-GEMM tile (norm partial rows)
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// ---------------------------------------------------------------- workspace
+struct Ws {
+  size_t status, scal;
+  size_t w64, a64, v64, sig64, uw32, vw32;
+  size_t norm_part, norms, scales;
+  size_t km_w, km_psum, km_pw, km_pobj, km_ptie, km_red, km_cnt;
+  size_t dist, cand_d, cand_i, cand_all;
+  size_t idx;
+  size_t cb, rb, wb;
+  size_t res_part;
+  size_t total;
+  // dims
+  int64_t K, Kp, m_loc, n_sl, Nmax, n, ldrb, npt;
+};
+
+inline Ws ws_layout(const cabs_plan& p) {
+  Ws w{};
+  w.K = p.kmax;
+  w.Kp = round_up(w.K, 32);
+  w.m_loc = p.row_end - p.row_begin;
+  w.n_sl = p.col_end - p.col_begin;
+  w.Nmax = w.m_loc > w.n_sl ? w.m_loc : w.n_sl;
+  if (w.Nmax < 1) w.Nmax = 1;
+  w.n = p.n;
+  w.ldrb = round_up(p.n, 4);
+  w.npt = ceil_div(w.Nmax, kNormTile);
+  const int64_t K = w.K, Kp = w.Kp;
+  const int nr = p.nranks > 0 ? p.nranks : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  w.status = take(256);
+  w.scal = take(4096);
+  w.w64 = take(sizeof(double) * K * K);
+  w.a64 = take(sizeof(double) * K * K);
+  w.v64 = take(sizeof(double) * K * K);
+  w.sig64 = take(sizeof(double) * Kp);
+  w.uw32 = take(sizeof(float) * K * Kp);
+  w.vw32 = take(sizeof(float) * K * Kp);
+  w.norm_part = take(sizeof(double) * 2 * w.npt * Kp);
+  w.norms = take(sizeof(double) * 2 * Kp);
+  w.scales = take(sizeof(float) * 8 * Kp);
+  w.km_w = take(sizeof(float) * w.Nmax);
+  w.km_psum = take(sizeof(float) * (size_t)kAccGrid * K * Kp);
+  w.km_pw = take(sizeof(double) * (size_t)kAccGrid * K);
+  w.km_pobj = take(sizeof(double) * kAssignGrid);
+  w.km_ptie = take(sizeof(int) * kAssignGrid);
+  w.km_red = take(sizeof(double) * (K * Kp + K + 2));
+  w.km_cnt = take(sizeof(int) * 64);
+  w.dist = take(sizeof(float) * K * w.Nmax);
+  w.cand_d = take(sizeof(float) * K * kSnapTMulti);
+  w.cand_i = take(sizeof(int64_t) * K * kSnapTMulti);
+  w.cand_all = take(sizeof(double) * 2 * nr * K * kSnapTMulti);
+  w.idx = take(sizeof(int64_t) * 8 * Kp);
+  w.cb = take(sizeof(float) * (w.m_loc > 0 ? w.m_loc : 1) * Kp);
+  w.rb = take(sizeof(float) * K * w.ldrb);
+  w.wb = take(sizeof(float) * K * Kp);
+  w.res_part = take(sizeof(double) * 2 * kResGrid);
+  w.total = off;
+  return w;
+}
+
+template <typename T>
+inline T* wsp(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+// scalar slots inside ws.scal (ints)
+enum ScalSlot : int { SCAL_R_PILOT = 0, SCAL_R_TMP = 1, SCAL_NRANKS = 2, SCAL_EXHAUST = 3 };
+
+__device__ inline void set_status(void* ws, uint32_t bit) {
+  atomicOr(reinterpret_cast<unsigned int*>(ws), bit);
+}
+
+// ---------------------------------------------------------------- warp helpers
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// (d, idx) lexicographic "less"
+__device__ __forceinline__ bool lex_less(float da, int64_t ia, float db, int64_t ib) {
+  return da < db || (da == db && ia < ib);
+}
+
+}  // namespace cabsk
+
+// ---------------------------------------------------------------- error plumbing
+void cabs_set_cuda_error(cudaError_t e, const char* where);
+void cabs_set_error_msg(const char* msg);
+
+#define CABS_LAUNCH_CHECK(where)                       \
+  do {                                                 \
+    cudaError_t e_ = cudaGetLastError();               \
+    if (e_ != cudaSuccess) {                           \
+      cabs_set_cuda_error(e_, where);                  \
+      return CABS_ERR_CUDA;                            \
+    }                                                  \
+  } while (0)
+
+#define CABS_CUDA_TRY(x)                               \
+  do {                                                 \
+    cudaError_t e_ = (x);                              \
+    if (e_ != cudaSuccess) {                           \
+      cabs_set_cuda_error(e_, #x);                     \
+      return CABS_ERR_CUDA;                            \
+    }                                                  \
+  } while (0)
+
+#define CABS_TRY(x)                                    \
+  do {                                                 \
+    int32_t s_ = (x);                                  \
+    if (s_ != CABS_OK) return s_;                      \
+  } while (0)

@@ -1,0 +1,60 @@
+// kernels.cuh -- host launchers of libcabs kernels (internal; the public ABI is include/cabs.h).
+#pragma once
+#include "common.cuh"
+
+namespace cabsk {
+
+// sample_gather.cu
+int launch_floyd2(int64_t N0, int32_t k0, uint32_t tag0, int64_t* out0, int64_t N1, int32_t k1, uint32_t tag1,
+                  int64_t* out1, uint64_t seed, cudaStream_t st);
+void launch_philox_blocks(uint64_t seed, uint32_t tag, uint64_t start, int64_t count, uint32_t* out, cudaStream_t st);
+void launch_validate_idx(const int64_t* idx, int32_t k, int64_t N, void* ws, cudaStream_t st);
+void launch_gather_rows(const float* A, int64_t lda, int64_t row_begin, int64_t row_end, const int64_t* I, int32_t k,
+                        int64_t n, float* R, int64_t ldr, void* ws, cudaStream_t st);
+void launch_gather_cols(const float* A, int64_t lda, int64_t m_loc, const int64_t* J, int32_t k, float* C, int64_t ldc,
+                        void* ws, cudaStream_t st);
+void launch_gather_w(const float* R, int64_t ldr, const int64_t* J, int32_t k, float* W, int64_t ldw, cudaStream_t st);
+
+// svd.cu
+int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const Ws& L, double* sigma_user, double* Uw64,
+               double* Vw64, int* r_user, cudaStream_t st);
+
+// embed.cu
+int launch_embed_products(int64_t m_loc, int64_t n_sl, int k, const float* C, int64_t ldc, const float* R_slice,
+                          int64_t ldr, float* Yc, int64_t ldyc, float* Yr, int64_t ldyr, void* ws, const Ws& L,
+                          cudaStream_t st);
+int launch_embed_finalize(int k, int mode, double m, double n, double ksamp, int kind, float* s_out, int* r_user,
+                          void* ws, const Ws& L, cudaStream_t st);
+int launch_scale_compact(float* Y, int64_t ldy, int64_t N, int k, int which, void* ws, const Ws& L, cudaStream_t st);
+
+// kmeans.cu
+void launch_km_weights(const float* X, int64_t ldx, int64_t N, int d, int kind, float p, float* w, int* cnt,
+                       cudaStream_t st);
+void launch_km_init(const float* X, int64_t ldx, int64_t n_loc, int64_t row_off, int d, int k2, const int64_t* idx,
+                    const float* init_c, int64_t ldic, float* centres, int64_t ldc, cudaStream_t st);
+void launch_km_assign(const float* X, int64_t ldx, int64_t N, int d, const float* centres, int64_t ldc, int k2,
+                      const float* w, int* labels, double* pobj, int* ptie, int* grid_out, cudaStream_t st);
+void launch_km_distmat(const float* X, int64_t ldx, int64_t N, int d, const float* centres, int64_t ldc, int k2,
+                       float* D, int64_t ldd, cudaStream_t st);
+void launch_km_accum(const float* X, int64_t ldx, int64_t N, int d, const int* labels, const float* w, int k2,
+                     float* psum, double* pw, int64_t ldps, int* grid_out, cudaStream_t st);
+void launch_km_reduce(const float* psum, const double* pw, int G, int k2, int d, int64_t ldps, const double* pobj,
+                      const int* ptie, int Gobj, double* red, cudaStream_t st);
+void launch_km_finalize(const double* red, int k2, int d, float* centres, int64_t ldc, double* objective,
+                        int* near_ties, double* cluster_w, int t, cudaStream_t st);
+
+// select.cu
+void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t row_off, int T, float* cand_d,
+                      int64_t* cand_i, cudaStream_t st);
+void launch_snap_pack(const float* cand_d, const int64_t* cand_i, int k2, int T, int rank, int nranks, double* all,
+                      cudaStream_t st);
+void launch_snap_merge(const double* all, int k2, int T, int nranks, float* cand_d, int64_t* cand_i, cudaStream_t st);
+void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int T, const double* cluster_w,
+                        const float* D, int64_t ldd, int64_t N, int64_t row_off, bool can_rescan,
+                        int64_t* rep_of_centre, float* gap, int64_t* reps_sorted, void* ws, cudaStream_t st);
+
+// residual.cu
+int launch_residual(const float* A, int64_t lda, int64_t m_loc, int64_t n, const float* F, int64_t ldf, const float* s,
+                    const float* G, int64_t ldg, int ncomp, double* part, double* out, cudaStream_t st);
+
+}  // namespace cabsk

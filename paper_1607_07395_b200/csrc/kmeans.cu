@@ -1,0 +1,376 @@
+// kmeans.cu -- S6/S7: weighted Lloyd k-means (Eq. 6; c iterations P:204).
+//
+// assign : s(l) = argmin_j ||X_l - c_j||^2 by DIRECT differences in FP32 (SURVEY F3:
+//          the expanded form flips labels on clustered data), lowest j on ties;
+//          objective partial sum_l w_l d_min in FP64 per CTA; near-tie count.
+// accum  : deterministic dimension-owned segmented reduction of w_l X_l by label
+//          into per-CTA partial sums (no atomics, fixed order).
+// reduce : fixed-order FP64 sum of the per-CTA partials -> one payload
+//          [k2*d sums | k2 weights | objective | near ties]  (the allreduce buffer).
+// finalize: c_j = sums_j / weight_j, empty clusters keep their centre (Z12).
+#include <float.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cabsk {
+
+constexpr int kTileP = 64, kTileC = 64, kTileD = 16;
+constexpr float kNearTie = 1e-5f;
+
+// ---------------------------------------------------------------- weights
+__global__ void __launch_bounds__(256) km_weights_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
+                                                         int kind, float p, float* __restrict__ w, int* cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int pos = 0;
+  for (int64_t l = warp; l < N; l += nw) {
+    float ss = 0.f;
+    for (int i = lane; i < d; i += 32) {
+      float x = X[l * ldx + i];
+      ss = fmaf(x, x, ss);
+    }
+    ss = warp_sum_f(ss);
+    float wl;
+    if (kind == CABS_WEIGHT_CONST) wl = 1.f;
+    else if (p == 2.f) wl = ss;
+    else wl = powf(sqrtf(ss), p);
+    if (lane == 0) {
+      w[l] = wl;
+      pos += wl > 0.f;
+    }
+  }
+  if (lane == 0 && pos) atomicAdd(cnt, pos);
+}
+
+void launch_km_weights(const float* X, int64_t ldx, int64_t N, int d, int kind, float p, float* w, int* cnt,
+                       cudaStream_t st) {
+  if (N <= 0) return;
+  int64_t blocks = ceil_div(N, 8);
+  if (blocks > 8 * kNumSM) blocks = 8 * kNumSM;
+  km_weights_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(X, ldx, N, d, kind, p, w, cnt);
+}
+
+// ---------------------------------------------------------------- init
+// centres[j] = X[idx[j]] if this rank owns that row (zeros otherwise: the
+// caller's sum-allreduce completes it), or a copy of init_c.
+__global__ void km_init_kernel(const float* __restrict__ X, int64_t ldx, int64_t n_loc, int64_t row_off, int d,
+                               const int64_t* __restrict__ idx, const float* __restrict__ init_c, int64_t ldic,
+                               float* __restrict__ centres, int64_t ldc) {
+  const int j = blockIdx.x;
+  const float* src = nullptr;
+  if (init_c) src = init_c + (int64_t)j * ldic;
+  else {
+    int64_t g = idx[j] - row_off;
+    if (g >= 0 && g < n_loc) src = X + g * ldx;
+  }
+  for (int i = threadIdx.x; i < ldc; i += blockDim.x)
+    centres[(int64_t)j * ldc + i] = (src && i < d) ? src[i] : 0.f;
+}
+
+void launch_km_init(const float* X, int64_t ldx, int64_t n_loc, int64_t row_off, int d, int k2, const int64_t* idx,
+                    const float* init_c, int64_t ldic, float* centres, int64_t ldc, cudaStream_t st) {
+  km_init_kernel<<<k2, 128, 0, st>>>(X, ldx, n_loc, row_off, d, idx, init_c, ldic, centres, ldc);
+}
+
+// ---------------------------------------------------------------- assign / distance matrix
+// Tile: 64 points x 64 centres; thread (tp = tid & 15, tc = tid >> 4) owns points
+// tp + 16a and centres tc + 16b (a, b = 0..3).  Dimensions are staged 16 at a time;
+// every distance is accumulated over i = 0..d-1 in ascending order.
+template <bool DISTMAT>
+__global__ void __launch_bounds__(256) km_assign_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
+                                                        const float* __restrict__ centres, int64_t ldc, int k2,
+                                                        const float* __restrict__ w, int* __restrict__ labels,
+                                                        double* __restrict__ pobj, int* __restrict__ ptie,
+                                                        float* __restrict__ D, int64_t ldd) {
+  __shared__ float Xs[kTileD][kTileP + 4];
+  __shared__ float Cs[kTileD][kTileC + 4];
+  __shared__ float sb_d[16][kTileP + 1];
+  __shared__ int sb_j[16][kTileP + 1];
+  __shared__ float ss_d[16][kTileP + 1];
+  __shared__ double s_red[8];
+  __shared__ int s_tie[8];
+  const int tid = threadIdx.x, tp = tid & 15, tc = tid >> 4;
+  const int64_t ntiles = ceil_div(N, kTileP);
+  double obj = 0.0;
+  int ties = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t p0 = tile * kTileP;
+    float bd[4], sd[4];
+    int bj[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) { bd[a] = FLT_MAX; sd[a] = FLT_MAX; bj[a] = 0x7fffffff; }
+    for (int j0 = 0; j0 < k2; j0 += kTileC) {
+      float acc[4][4] = {};
+      for (int i0 = 0; i0 < d; i0 += kTileD) {
+        {
+          const int pp = tid >> 2, ii = (tid & 3) * 4;
+          const int64_t p = p0 + pp;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = i0 + ii + q;
+            Xs[ii + q][pp] = (p < N && i < d) ? __ldg(X + p * ldx + i) : 0.f;
+          }
+          const int j = j0 + pp;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = i0 + ii + q;
+            Cs[ii + q][pp] = (j < k2 && i < d) ? __ldg(centres + (int64_t)j * ldc + i) : 0.f;
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ii = 0; ii < kTileD; ++ii) {
+          float x[4], c[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) x[a] = Xs[ii][tp + 16 * a];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) c[b] = Cs[ii][tc + 16 * b];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const float df = x[a] - c[b];
+              acc[a][b] = fmaf(df, df, acc[a][b]);
+            }
+        }
+        __syncthreads();
+      }
+      if (DISTMAT) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int j = j0 + tc + 16 * b;
+          if (j >= k2) continue;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const int64_t p = p0 + tp + 16 * a;
+            if (p < N) D[(int64_t)j * ldd + p] = acc[a][b];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int j = j0 + tc + 16 * b;
+          if (j >= k2) continue;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const float v = acc[a][b];
+            if (v < bd[a] || (v == bd[a] && j < bj[a])) {
+              sd[a] = bd[a];
+              bd[a] = v;
+              bj[a] = j;
+            } else {
+              sd[a] = fminf(sd[a], v);
+            }
+          }
+        }
+      }
+    }
+    if (!DISTMAT) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        sb_d[tc][tp + 16 * a] = bd[a];
+        sb_j[tc][tp + 16 * a] = bj[a];
+        ss_d[tc][tp + 16 * a] = sd[a];
+      }
+      __syncthreads();
+      if (tid < kTileP) {
+        const int64_t p = p0 + tid;
+        float B = sb_d[0][tid], S = ss_d[0][tid];
+        int Bj = sb_j[0][tid];
+        for (int t = 1; t < 16; ++t) {
+          const float b2 = sb_d[t][tid], s2 = ss_d[t][tid];
+          const int j2 = sb_j[t][tid];
+          if (b2 < B || (b2 == B && j2 < Bj)) {
+            S = fminf(fminf(S, s2), B);
+            B = b2;
+            Bj = j2;
+          } else {
+            S = fminf(fminf(S, s2), b2);
+          }
+        }
+        if (p < N) {
+          labels[p] = Bj;
+          obj += static_cast<double>(w[p]) * static_cast<double>(B);
+          ties += (S - B) < kNearTie * S;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (!DISTMAT) {
+    obj = warp_sum_d(obj);
+    int t = ties;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((tid & 31) == 0) {
+      s_red[tid >> 5] = obj;
+      s_tie[tid >> 5] = t;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0;
+      int tt = 0;
+      for (int q = 0; q < 8; ++q) { s += s_red[q]; tt += s_tie[q]; }
+      pobj[blockIdx.x] = s;
+      ptie[blockIdx.x] = tt;
+    }
+  }
+}
+
+static int assign_grid(int64_t N) {
+  int64_t t = ceil_div(N, kTileP);
+  if (t > kAssignGrid) t = kAssignGrid;
+  return static_cast<int>(t < 1 ? 1 : t);
+}
+
+void launch_km_assign(const float* X, int64_t ldx, int64_t N, int d, const float* centres, int64_t ldc, int k2,
+                      const float* w, int* labels, double* pobj, int* ptie, int* grid_out, cudaStream_t st) {
+  const int g = assign_grid(N);
+  *grid_out = g;
+  km_assign_kernel<false><<<g, 256, 0, st>>>(X, ldx, N, d, centres, ldc, k2, w, labels, pobj, ptie, nullptr, 0);
+}
+
+void launch_km_distmat(const float* X, int64_t ldx, int64_t N, int d, const float* centres, int64_t ldc, int k2,
+                       float* D, int64_t ldd, cudaStream_t st) {
+  if (N <= 0) return;
+  const int g = assign_grid(N);
+  km_assign_kernel<true><<<g, 256, 0, st>>>(X, ldx, N, d, centres, ldc, k2, nullptr, nullptr, nullptr, nullptr, D, ldd);
+}
+
+// ---------------------------------------------------------------- accumulate
+// grid (G, ceil(d/32)).  CTA b owns the contiguous point chunk b; warp w owns the
+// clusters j with j % 8 == w; lane = dimension.  Points are visited in index
+// order, so every (j, dim) partial is a fixed-order FP32 sum.
+constexpr int kAccSub = 128;
+
+__global__ void __launch_bounds__(256) km_accum_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
+                                                       const int* __restrict__ labels, const float* __restrict__ w,
+                                                       int k2, float* __restrict__ psum, double* __restrict__ pw,
+                                                       int64_t ldps) {
+  extern __shared__ float acc_s[];  // [k2][32]
+  __shared__ float Xt[kAccSub][33];
+  __shared__ int labs[kAccSub];
+  __shared__ float wts[kAccSub];
+  double* wsum = reinterpret_cast<double*>(acc_s + (size_t)k2 * 32);  // [k2] (only blockIdx.y == 0)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ds0 = blockIdx.y * 32;
+  const int64_t chunk = ceil_div(N, gridDim.x);
+  const int64_t pbeg = blockIdx.x * chunk;
+  int64_t pend = pbeg + chunk;
+  if (pend > N) pend = N;
+  for (int e = tid; e < k2 * 32; e += blockDim.x) acc_s[e] = 0.f;
+  for (int e = tid; e < k2; e += blockDim.x) wsum[e] = 0.0;
+  __syncthreads();
+  for (int64_t s0 = pbeg; s0 < pend; s0 += kAccSub) {
+    const int cnt = static_cast<int>((pend - s0) < kAccSub ? (pend - s0) : kAccSub);
+    for (int pp = warp; pp < cnt; pp += 8) {
+      const int i = ds0 + lane;
+      Xt[pp][lane] = i < d ? X[(s0 + pp) * ldx + i] : 0.f;
+    }
+    for (int pp = tid; pp < cnt; pp += blockDim.x) {
+      labs[pp] = labels[s0 + pp];
+      wts[pp] = w[s0 + pp];
+    }
+    __syncthreads();
+    for (int pp = 0; pp < cnt; ++pp) {
+      const int j = labs[pp];
+      if ((j & 7) == warp) {
+        const float wl = wts[pp];
+        acc_s[j * 32 + lane] = fmaf(wl, Xt[pp][lane], acc_s[j * 32 + lane]);
+        if (lane == 0 && blockIdx.y == 0) wsum[j] += static_cast<double>(wl);
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t base = (int64_t)blockIdx.x * k2 * ldps;
+  for (int e = tid; e < k2 * 32; e += blockDim.x) {
+    const int j = e >> 5, i = ds0 + (e & 31);
+    if (i < d) psum[base + (int64_t)j * ldps + i] = acc_s[e];
+  }
+  if (blockIdx.y == 0)
+    for (int j = tid; j < k2; j += blockDim.x) pw[(int64_t)blockIdx.x * k2 + j] = wsum[j];
+}
+
+void launch_km_accum(const float* X, int64_t ldx, int64_t N, int d, const int* labels, const float* w, int k2,
+                     float* psum, double* pw, int64_t ldps, int* grid_out, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(km_accum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  int64_t G = ceil_div(N, 64);
+  if (G > kAccGrid) G = kAccGrid;
+  if (G < 1) G = 1;
+  *grid_out = static_cast<int>(G);
+  dim3 grid(static_cast<unsigned>(G), static_cast<unsigned>(ceil_div(d, 32)));
+  size_t smem = (size_t)k2 * 32 * sizeof(float) + (size_t)k2 * sizeof(double);
+  km_accum_kernel<<<grid, 256, smem, st>>>(X, ldx, N, d, labels, w, k2, psum, pw, ldps);
+}
+
+// ---------------------------------------------------------------- reduce
+// red = [k2*d sums | k2 weights | objective | near ties], each a fixed-order FP64 sum over CTAs.
+__global__ void km_reduce_kernel(const float* __restrict__ psum, const double* __restrict__ pw, int G, int k2, int d,
+                                 int64_t ldps, const double* __restrict__ pobj, const int* __restrict__ ptie, int Gobj,
+                                 double* __restrict__ red) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nsum = (int64_t)k2 * d;
+  if (e < nsum) {
+    const int j = static_cast<int>(e / d), i = static_cast<int>(e % d);
+    double s = 0.0;
+    for (int b = 0; b < G; ++b) s += static_cast<double>(psum[((int64_t)b * k2 + j) * ldps + i]);
+    red[e] = s;
+  } else if (e < nsum + k2) {
+    const int j = static_cast<int>(e - nsum);
+    double s = 0.0;
+    for (int b = 0; b < G; ++b) s += pw[(int64_t)b * k2 + j];
+    red[e] = s;
+  } else if (e == nsum + k2) {
+    double s = 0.0;
+    for (int b = 0; b < Gobj; ++b) s += pobj[b];
+    red[e] = s;
+  } else if (e == nsum + k2 + 1) {
+    long long t = 0;
+    for (int b = 0; b < Gobj; ++b) t += ptie[b];
+    red[e] = static_cast<double>(t);
+  }
+}
+
+void launch_km_reduce(const float* psum, const double* pw, int G, int k2, int d, int64_t ldps, const double* pobj,
+                      const int* ptie, int Gobj, double* red, cudaStream_t st) {
+  const int64_t total = (int64_t)k2 * d + k2 + 2;
+  km_reduce_kernel<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, st>>>(psum, pw, G, k2, d, ldps, pobj, ptie,
+                                                                                 Gobj, red);
+}
+
+__global__ void km_finalize_kernel(const double* __restrict__ red, int k2, int d, float* __restrict__ centres,
+                                   int64_t ldc, double* __restrict__ objective, int* __restrict__ near_ties,
+                                   double* __restrict__ cluster_w, int t) {
+  const int64_t nsum = (int64_t)k2 * d;
+  const double* wts = red + nsum;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nsum; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(e / d), i = static_cast<int>(e % d);
+    const double wj = wts[j];
+    if (wj > 0) centres[(int64_t)j * ldc + i] = static_cast<float>(red[e] / wj);
+  }
+  if (blockIdx.x == 0) {
+    for (int j = threadIdx.x; j < k2; j += blockDim.x)
+      if (cluster_w) cluster_w[j] = wts[j];
+    if (threadIdx.x == 0) {
+      if (objective) objective[t] = red[nsum + k2];
+      if (near_ties) near_ties[t] = static_cast<int>(red[nsum + k2 + 1]);
+    }
+  }
+}
+
+void launch_km_finalize(const double* red, int k2, int d, float* centres, int64_t ldc, double* objective,
+                        int* near_ties, double* cluster_w, int t, cudaStream_t st) {
+  int64_t blocks = ceil_div((int64_t)k2 * d, 256);
+  if (blocks > 4 * kNumSM) blocks = 4 * kNumSM;
+  if (blocks < 1) blocks = 1;
+  km_finalize_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(red, k2, d, centres, ldc, objective, near_ties,
+                                                                     cluster_w, t);
+}
+
+}  // namespace cabsk

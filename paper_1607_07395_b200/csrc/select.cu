@@ -1,0 +1,274 @@
+// select.cu -- S8: the snap ("any k-means clustering center will be replaced
+// with its closest in-sample point").  Readings Z13/Z14: nearest over ALL points,
+// duplicates resolved greedily in order (-omega_j, j), each centre taking its
+// nearest untaken point, ties -> lowest point index.
+//
+// distmat (kmeans.cu) writes D[j, p] = ||X_p - c_j||^2 (FP32 direct differences);
+// topT keeps each centre's T nearest (d, index) pairs; dedupe runs the greedy
+// pass in one CTA, rescanning D for a centre whose list is exhausted.
+#include <float.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cabsk {
+
+// ---------------------------------------------------------------- per-centre top-T
+template <int T>
+__global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict__ D, int64_t ldd, int64_t N,
+                                                        int64_t row_off, float* __restrict__ cand_d,
+                                                        int64_t* __restrict__ cand_i) {
+  __shared__ float hd[256];
+  __shared__ int64_t hi[256];
+  __shared__ int s_win;
+  const int j = blockIdx.x, tid = threadIdx.x;
+  float ld[T];
+  int64_t li[T];
+#pragma unroll
+  for (int q = 0; q < T; ++q) { ld[q] = FLT_MAX; li[q] = INT64_MAX; }
+  const float* row = D + (int64_t)j * ldd;
+  for (int64_t p = tid; p < N; p += blockDim.x) {
+    const float v = row[p];
+    const int64_t gi = row_off + p;
+    if (lex_less(v, gi, ld[T - 1], li[T - 1])) {
+      // insertion into the sorted list (compile-time indices only)
+      float cv = v;
+      int64_t ci = gi;
+#pragma unroll
+      for (int q = 0; q < T; ++q) {
+        if (lex_less(cv, ci, ld[q], li[q])) {
+          float td = ld[q];
+          int64_t ti = li[q];
+          ld[q] = cv;
+          li[q] = ci;
+          cv = td;
+          ci = ti;
+        }
+      }
+    }
+  }
+  // merge: T rounds of block-wide lexicographic argmin over the list heads
+  int head = 0;
+  for (int round = 0; round < T; ++round) {
+    float d0 = FLT_MAX;
+    int64_t i0 = INT64_MAX;
+#pragma unroll
+    for (int q = 0; q < T; ++q)
+      if (q == head) { d0 = ld[q]; i0 = li[q]; }
+    hd[tid] = d0;
+    hi[tid] = i0;
+    __syncthreads();
+    if (tid < 32) {
+      float bd = FLT_MAX;
+      int64_t bi = INT64_MAX;
+      int bt = 0;
+      for (int t = tid; t < 256; t += 32)
+        if (lex_less(hd[t], hi[t], bd, bi)) { bd = hd[t]; bi = hi[t]; bt = t; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        float od = __shfl_xor_sync(0xffffffffu, bd, o);
+        int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+        if (lex_less(od, oi, bd, bi)) { bd = od; bi = oi; bt = ot; }
+      }
+      if (tid == 0) {
+        cand_d[(int64_t)j * T + round] = bd;
+        cand_i[(int64_t)j * T + round] = bi == INT64_MAX ? -1 : bi;
+        s_win = bt;
+      }
+    }
+    __syncthreads();
+    if (tid == s_win) ++head;
+    __syncthreads();
+  }
+}
+
+void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t row_off, int T, float* cand_d,
+                      int64_t* cand_i, cudaStream_t st) {
+  if (T == kSnapT)
+    snap_topT_kernel<kSnapT><<<k2, 256, 0, st>>>(D, ldd, N, row_off, cand_d, cand_i);
+  else
+    snap_topT_kernel<kSnapTMulti><<<k2, 256, 0, st>>>(D, ldd, N, row_off, cand_d, cand_i);
+}
+
+// ---------------------------------------------------------------- multi-rank candidate exchange
+// all[rank][j][t][{d, idx}] as doubles (exact: idx < 2^53), zero elsewhere; summed by the caller.
+__global__ void snap_pack_kernel(const float* __restrict__ cand_d, const int64_t* __restrict__ cand_i, int k2, int T,
+                                 int rank, int nranks, double* __restrict__ all) {
+  const int64_t per = (int64_t)k2 * T;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per * nranks;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(e / per);
+    const int64_t q = e % per;
+    all[2 * e] = r == rank ? static_cast<double>(cand_d[q]) : 0.0;
+    all[2 * e + 1] = r == rank ? static_cast<double>(cand_i[q]) : 0.0;
+  }
+}
+
+void launch_snap_pack(const float* cand_d, const int64_t* cand_i, int k2, int T, int rank, int nranks, double* all,
+                      cudaStream_t st) {
+  snap_pack_kernel<<<64, 256, 0, st>>>(cand_d, cand_i, k2, T, rank, nranks, all);
+}
+
+__global__ void snap_merge_kernel(const double* __restrict__ all, int k2, int T, int nranks, float* __restrict__ cand_d,
+                                  int64_t* __restrict__ cand_i) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k2) return;
+  float pd = -FLT_MAX;
+  int64_t pi = -1;  // previous winner (lists are merged by repeated lexicographic successor search)
+  for (int t = 0; t < T; ++t) {
+    float bd = FLT_MAX;
+    int64_t bi = INT64_MAX;
+    for (int r = 0; r < nranks; ++r)
+      for (int q = 0; q < T; ++q) {
+        const int64_t e = (((int64_t)r * k2 + j) * T + q) * 2;
+        const float d = static_cast<float>(all[e]);
+        const int64_t i = static_cast<int64_t>(all[e + 1]);
+        if (i < 0) continue;
+        if (lex_less(pd, pi, d, i) && lex_less(d, i, bd, bi)) { bd = d; bi = i; }
+      }
+    cand_d[(int64_t)j * T + t] = bd;
+    cand_i[(int64_t)j * T + t] = bi == INT64_MAX ? -1 : bi;
+    pd = bd;
+    pi = bi;
+  }
+}
+
+void launch_snap_merge(const double* all, int k2, int T, int nranks, float* cand_d, int64_t* cand_i, cudaStream_t st) {
+  snap_merge_kernel<<<static_cast<unsigned>(ceil_div(k2, 128)), 128, 0, st>>>(all, k2, T, nranks, cand_d, cand_i);
+}
+
+// ---------------------------------------------------------------- greedy dedupe (one CTA)
+constexpr int kTakenBits = 11;  // capacity 2048 >= 2 * CABS_KMAX
+constexpr int kTakenCap = 1 << kTakenBits;
+
+__device__ __forceinline__ uint32_t taken_hash(int64_t x) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(x) * 0x9E3779B97F4A7C15ull) >> (64 - kTakenBits));
+}
+__device__ __forceinline__ bool taken_has(const int64_t* tab, int64_t x) {
+  uint32_t h = taken_hash(x);
+  while (tab[h] != -1) {
+    if (tab[h] == x) return true;
+    h = (h + 1) & (kTakenCap - 1);
+  }
+  return false;
+}
+__device__ __forceinline__ void taken_put(int64_t* tab, int64_t x) {
+  uint32_t h = taken_hash(x);
+  while (tab[h] != -1) h = (h + 1) & (kTakenCap - 1);
+  tab[h] = x;
+}
+
+__global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* __restrict__ cand_d,
+                                                          const int64_t* __restrict__ cand_i, int k2, int T,
+                                                          const double* __restrict__ cluster_w,
+                                                          const float* __restrict__ D, int64_t ldd, int64_t N,
+                                                          int64_t row_off, bool can_rescan,
+                                                          int64_t* __restrict__ rep_of_centre, float* __restrict__ gap,
+                                                          int64_t* __restrict__ reps_sorted, void* ws) {
+  __shared__ int64_t tab[kTakenCap];
+  __shared__ int order[CABS_KMAX];
+  __shared__ int64_t reps[CABS_KMAX];
+  __shared__ int s_next;      // next position in `order` to process
+  __shared__ int s_rescan;    // centre needing a rescan, or -1
+  __shared__ float rd[256], rs[256];
+  __shared__ int64_t ri[256];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kTakenCap; e += blockDim.x) tab[e] = -1;
+  // visiting order (-omega_j, j)
+  for (int j = tid; j < k2; j += blockDim.x) {
+    const double wj = cluster_w[j];
+    int rk = 0;
+    for (int q = 0; q < k2; ++q) {
+      const double wq = cluster_w[q];
+      rk += (wq > wj) || (wq == wj && q < j);
+    }
+    order[rk] = j;
+  }
+  if (tid == 0) s_next = 0;
+  __syncthreads();
+  for (;;) {
+    if (tid == 0) {
+      s_rescan = -1;
+      int o = s_next;
+      for (; o < k2; ++o) {
+        const int j = order[o];
+        float d1 = FLT_MAX, d2 = FLT_MAX;
+        int64_t i1 = -1, i2 = -1;
+        for (int t = 0; t < T; ++t) {
+          const int64_t ci = cand_i[(int64_t)j * T + t];
+          if (ci < 0 || taken_has(tab, ci)) continue;
+          if (i1 < 0) { i1 = ci; d1 = cand_d[(int64_t)j * T + t]; }
+          else { i2 = ci; d2 = cand_d[(int64_t)j * T + t]; break; }
+        }
+        if (i2 < 0) {  // best or runner-up not resolved from the list
+          if (can_rescan) { s_rescan = j; break; }
+          if (i1 < 0) { set_status(ws, CABS_DEV_SNAP_EXHAUSTED); i1 = 0; d1 = 0.f; }
+        }
+        taken_put(tab, i1);
+        reps[j] = i1;
+        rep_of_centre ? (void)(rep_of_centre[j] = i1) : (void)0;
+        if (gap) gap[j] = (i2 < 0) ? FLT_MAX : (d2 > 0.f ? (d2 - d1) / d2 : 0.f);
+      }
+      s_next = o;
+    }
+    __syncthreads();
+    const int j = s_rescan;
+    if (j < 0) break;
+    // block-wide rescan of D[j, :] for the best and runner-up untaken points
+    float b1 = FLT_MAX, b2 = FLT_MAX;
+    int64_t i1 = INT64_MAX, i2 = INT64_MAX;
+    const float* row = D + (int64_t)j * ldd;
+    for (int64_t p = tid; p < N; p += blockDim.x) {
+      const int64_t gi = row_off + p;
+      if (taken_has(tab, gi)) continue;
+      const float v = row[p];
+      if (lex_less(v, gi, b1, i1)) { b2 = b1; i2 = i1; b1 = v; i1 = gi; }
+      else if (lex_less(v, gi, b2, i2)) { b2 = v; i2 = gi; }
+    }
+    // reduce (best, runner-up) pairs: serial merge by thread 0 in fixed order
+    rd[tid] = b1; ri[tid] = i1; rs[tid] = b2;
+    __shared__ int64_t ri2[256];
+    ri2[tid] = i2;
+    __syncthreads();
+    if (tid == 0) {
+      float B1 = FLT_MAX, B2 = FLT_MAX;
+      int64_t I1 = INT64_MAX, I2 = INT64_MAX;
+      for (int t = 0; t < 256; ++t) {
+        const float cands_d[2] = {rd[t], rs[t]};
+        const int64_t cands_i[2] = {ri[t], ri2[t]};
+        for (int q = 0; q < 2; ++q) {
+          const float v = cands_d[q];
+          const int64_t gi = cands_i[q];
+          if (gi == INT64_MAX) continue;
+          if (lex_less(v, gi, B1, I1)) { B2 = B1; I2 = I1; B1 = v; I1 = gi; }
+          else if (lex_less(v, gi, B2, I2)) { B2 = v; I2 = gi; }
+        }
+      }
+      if (I1 == INT64_MAX) { set_status(ws, CABS_DEV_SNAP_EXHAUSTED); I1 = 0; B1 = 0.f; }
+      taken_put(tab, I1);
+      reps[j] = I1;
+      if (rep_of_centre) rep_of_centre[j] = I1;
+      if (gap) gap[j] = (I2 == INT64_MAX) ? FLT_MAX : (B2 > 0.f ? (B2 - B1) / B2 : 0.f);
+      s_next = s_next + 1;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  // sorted representatives (distinct)
+  for (int j = tid; j < k2; j += blockDim.x) {
+    const int64_t v = reps[j];
+    int rk = 0;
+    for (int q = 0; q < k2; ++q) rk += reps[q] < v;
+    reps_sorted[rk] = v;
+  }
+}
+
+void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int T, const double* cluster_w,
+                        const float* D, int64_t ldd, int64_t N, int64_t row_off, bool can_rescan,
+                        int64_t* rep_of_centre, float* gap, int64_t* reps_sorted, void* ws, cudaStream_t st) {
+  snap_dedupe_kernel<<<1, 256, 0, st>>>(cand_d, cand_i, k2, T, cluster_w, D, ldd, N, row_off, can_rescan, rep_of_centre,
+                                        gap, reps_sorted, ws);
+}
+
+}  // namespace cabsk

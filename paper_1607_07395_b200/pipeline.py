@@ -1,0 +1,158 @@
+"""CABS Algorithm 2 + evaluation through the C ABI.
+
+`CabsPipeline` owns the device buffers of one (plan, config) and runs the six
+entry points of libcabs.so in order on one stream:
+
+  S1-S3 cabs_pilot    pilot sampling and gathers C, R, W
+  S4-S5 cabs_embed    pilot sketch -> embeddings P, Q
+  S6-S7 cabs_kmeans   weighted Lloyd on P (rows) and on Q (columns)  (Eq. 6)
+  S8    cabs_select   snap centres to in-sample rows / columns
+  S9    cabs_sketch   follow-up gathers + sketch -> Ubar, sbar, Vbar
+  S10   cabs_residual ||A - Ubar diag(sbar) Vbar^T||_F^2, ||A||_F^2
+
+Buffers are allocated once, so repeated runs (benchmark steps) allocate nothing.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import cabs as C
+from .dist import make_plan
+
+
+@dataclass
+class CabsConfig:
+    k1: int
+    k2: int
+    iters: int
+    seed: int = 0
+    mode: int = C.STABILIZED
+    tol: float = 1e-12
+    weight_kind: int = C.WEIGHT_CONST
+    weight_p: float = 2.0
+
+
+STEPS = ("pilot", "embed", "kmeans", "select", "sketch", "residual")
+
+
+class CabsPipeline:
+    def __init__(self, A_local: torch.Tensor, m: int, n: int, cfg: CabsConfig, rank: int = 0,
+                 nranks: int = 1, comm=None, align: int = 1, plan=None):
+        C.load()
+        self.A = A_local
+        self.cfg = cfg
+        self.comm = comm
+        self.plan = plan if plan is not None else make_plan(m, n, max(cfg.k1, cfg.k2), rank, nranks, align)
+        p = self.plan
+        assert A_local.shape[0] == p.m_loc and A_local.shape[1] >= n
+        dev = A_local.device
+        self.device = dev
+        k1, k2 = cfg.k1, cfg.k2
+        l1, l2 = C.cabs_padded_ld(k1), C.cabs_padded_ld(k2)
+        ldr = (n + 3) // 4 * 4
+        f32, f64, i64, i32 = torch.float32, torch.float64, torch.int64, torch.int32
+        z = lambda *s, dt=f32: torch.zeros(*s, dtype=dt, device=dev)  # noqa: E731
+        self.ws = torch.zeros(C.cabs_workspace_bytes(p), dtype=torch.uint8, device=dev)
+        self.I, self.J = z(k1, dt=i64), z(k1, dt=i64)
+        self.Cm = z(p.m_loc, l1)
+        self.R = z(k1, ldr)
+        self.W = z(k1, l1)
+        self.P, self.Q = z(p.m_loc, l1), z(p.n_sl, l1)
+        self.s1, self.r1, self.sigma1 = z(k1), z(1, dt=i32), z(k1, dt=f64)
+        self.cen_r, self.cen_c = z(k2, l1), z(k2, l1)
+        self.lab_r, self.lab_c = z(max(p.m_loc, 1), dt=i32), z(max(p.n_sl, 1), dt=i32)
+        self.cw_r, self.cw_c = z(k2, dt=f64), z(k2, dt=f64)
+        self.obj_r, self.obj_c = z(cfg.iters, dt=f64), z(cfg.iters, dt=f64)
+        self.tie_r, self.tie_c = z(cfg.iters, dt=i32), z(cfg.iters, dt=i32)
+        self.Ib, self.Jb = z(k2, dt=i64), z(k2, dt=i64)
+        self.rep_r, self.rep_c = z(k2, dt=i64), z(k2, dt=i64)
+        self.gap_r, self.gap_c = z(k2), z(k2)
+        self.U, self.V = z(p.m_loc, l2), z(p.n_sl, l2)
+        self.s2, self.r2, self.sigma2 = z(k2), z(1, dt=i32), z(k2, dt=f64)
+        self.G = self.V if p.nranks == 1 else z(n, l2)
+        self.out = z(2, dt=f64)
+        self.events = None
+
+    # ------------------------------------------------------------------ steps
+    def pilot(self):
+        c, p = self.cfg, self.plan
+        C.cabs_pilot(p, self.A, c.k1, c.seed, self.I, self.J, self.Cm, self.R, self.W, self.ws, self.comm)
+
+    def embed(self):
+        c, p = self.cfg, self.plan
+        C.cabs_embed(p, c.k1, self.Cm, self.R, self.W, c.mode, c.tol, self.P, self.Q, self.s1, self.r1,
+                     self.ws, sigma=self.sigma1, comm=self.comm)
+
+    def kmeans(self, init_rows=None, init_cols=None):
+        c, p = self.cfg, self.plan
+        C.cabs_kmeans(p, self.P, p.m_loc, p.m, p.row_begin, c.k1, c.k2, c.iters, c.weight_kind, c.weight_p,
+                      c.seed, C.TAG_INIT_ROWS, self.cen_r, self.lab_r, self.cw_r, self.obj_r, self.ws,
+                      near_ties=self.tie_r, init_idx=init_rows, comm=self.comm)
+        C.cabs_kmeans(p, self.Q, p.n_sl, p.n, p.col_begin, c.k1, c.k2, c.iters, c.weight_kind, c.weight_p,
+                      c.seed, C.TAG_INIT_COLS, self.cen_c, self.lab_c, self.cw_c, self.obj_c, self.ws,
+                      near_ties=self.tie_c, init_idx=init_cols, comm=self.comm)
+
+    def select(self):
+        c, p = self.cfg, self.plan
+        C.cabs_select(p, self.P, p.m_loc, p.m, p.row_begin, c.k1, self.cen_r, c.k2, self.cw_r, self.Ib,
+                      self.ws, rep_of_centre=self.rep_r, gap=self.gap_r, comm=self.comm)
+        C.cabs_select(p, self.Q, p.n_sl, p.n, p.col_begin, c.k1, self.cen_c, c.k2, self.cw_c, self.Jb,
+                      self.ws, rep_of_centre=self.rep_c, gap=self.gap_c, comm=self.comm)
+
+    def sketch(self):
+        c, p = self.cfg, self.plan
+        C.cabs_sketch(p, self.A, self.Ib, self.Jb, c.k2, c.mode, c.tol, self.U, self.s2, self.V, self.r2,
+                      self.ws, sigma=self.sigma2, comm=self.comm)
+        if p.nranks > 1:  # the residual needs every column's factor row: gather V by slices
+            self.G.zero_()
+            self.G[p.col_begin:p.col_end] = self.V
+            self.comm.allreduce_tensor(self.G)
+
+    def residual(self):
+        c, p = self.cfg, self.plan
+        C.cabs_residual(p, self.A, self.U, self.s2, self.G, c.k2, self.out, self.ws, self.comm)
+
+    # ------------------------------------------------------------------ whole path
+    def run(self, with_residual=True, timed=False, init_rows=None, init_cols=None):
+        """One pass of the hot path, stream-ordered; returns per-step CUDA events if timed."""
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(STEPS) + 1)] if timed else None
+        if timed:
+            ev[0].record()
+        self.pilot()
+        timed and ev[1].record()
+        self.embed()
+        timed and ev[2].record()
+        self.kmeans(init_rows, init_cols)
+        timed and ev[3].record()
+        self.select()
+        timed and ev[4].record()
+        self.sketch()
+        timed and ev[5].record()
+        if with_residual:
+            self.residual()
+        timed and ev[6].record()
+        self.events = ev
+        return ev
+
+    def step_ms(self):
+        """Per-step milliseconds of the last timed run (synchronises)."""
+        ev = self.events
+        torch.cuda.synchronize()
+        return {s: ev[i].elapsed_time(ev[i + 1]) for i, s in enumerate(STEPS)}
+
+    def results(self):
+        """Host copies of everything the parity tests compare."""
+        r1 = int(self.r1.item())
+        r2 = int(self.r2.item())
+        cpu = lambda t: t.detach().cpu()  # noqa: E731
+        return dict(I=cpu(self.I), J=cpu(self.J), C=cpu(self.Cm), R=cpu(self.R), W=cpu(self.W),
+                    r1=r1, s1=cpu(self.s1), sigma1=cpu(self.sigma1), P=cpu(self.P), Q=cpu(self.Q),
+                    cen_r=cpu(self.cen_r), cen_c=cpu(self.cen_c), lab_r=cpu(self.lab_r),
+                    lab_c=cpu(self.lab_c), cw_r=cpu(self.cw_r), cw_c=cpu(self.cw_c),
+                    obj_r=cpu(self.obj_r), obj_c=cpu(self.obj_c), tie_r=cpu(self.tie_r),
+                    tie_c=cpu(self.tie_c), Ib=cpu(self.Ib), Jb=cpu(self.Jb), rep_r=cpu(self.rep_r),
+                    rep_c=cpu(self.rep_c), gap_r=cpu(self.gap_r), gap_c=cpu(self.gap_c),
+                    r2=r2, U=cpu(self.U), V=cpu(self.V), s2=cpu(self.s2), sigma2=cpu(self.sigma2),
+                    resid_sq=float(self.out[0]), a_sq=float(self.out[1]))

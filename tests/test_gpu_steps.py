@@ -1,0 +1,345 @@
+"""GPU parity, step by step (teacher-forced): each CUDA step through the C ABI
+against the FP64 oracle on identical inputs.  Tolerances: DESIGN.md "Parity".
+
+  S1 indices            bit-exact          S2/S3 gathers      bit-exact
+  S4 sigma              1e-12 * sigma_1    S5 P, Q            1e-4 rel. Frobenius
+  S6 labels             exact except logged near ties (oracle gap < 1e-5)
+  S7 centres            1e-5 rel.          S8 representatives exact except near ties
+  S9 factors            1e-4               S10 residual       1e-4 rel. (+ FP32 floor)
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cabs as O
+from oracle import rng
+from tests.helpers import NEAR_TIE, align_signs, label_mismatches, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+C = pytest.importorskip("paper_1607_07395_b200.cabs")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    C.load()
+    return torch.device("cuda:0")
+
+
+def _plan(m, n, kmax):
+    from paper_1607_07395_b200.dist import make_plan
+    return make_plan(m, n, kmax)
+
+
+def _ws(plan, dev):
+    return torch.zeros(C.cabs_workspace_bytes(plan), dtype=torch.uint8, device=dev)
+
+
+def _A(m, n, seed, dev, r=8, noise=0.01, lda=None):
+    g = np.random.default_rng(seed)
+    A = (g.standard_normal((m, r)) @ (g.standard_normal((r, n)) / np.arange(1, r + 1)[:, None])
+         + noise * g.standard_normal((m, n))).astype(np.float32)
+    lda = lda or n
+    T = torch.zeros((m, lda), dtype=torch.float32, device=dev)
+    T[:, :n] = torch.from_numpy(A).to(dev)
+    return A, T
+
+
+# ------------------------------------------------------------------ S1 RNG
+def test_philox_blocks_match_oracle(dev):
+    count = 1 << 18  # 2^20 words
+    out = torch.zeros(4 * count, dtype=torch.int32, device=dev)
+    seed, tag, start = 0x1234_5678_9ABC_DEF0, 7, (1 << 32) - 100
+    C.cabs_philox_blocks(seed, tag, start, count, out)
+    got = out.cpu().numpy().view(np.uint32).reshape(count, 4)
+    b = np.arange(count, dtype=np.uint64) + np.uint64(start)
+    k0, k1 = rng.seed_key(seed)
+    ref = rng.philox4x32_10_np(b & np.uint64(0xFFFFFFFF), b >> np.uint64(32), tag, 0, k0, k1)
+    for i in range(4):
+        assert np.array_equal(got[:, i].astype(np.uint64), ref[i])
+
+
+@pytest.mark.parametrize("N,k,seed,tag", [(5, 5, 0, 1), (100, 10, 7, 1), (20000, 50, 0, 1), (10000, 50, 0, 2),
+                                          (2_000_000, 300, 3, 4), (1000, 1, 9, 3), (1024, 1024, 11, 2),
+                                          (4_000_000_000, 200, 5, 1)])
+def test_uniform_indices_bit_exact(dev, N, k, seed, tag):
+    out = torch.zeros(k, dtype=torch.int64, device=dev)
+    C.cabs_uniform_indices(N, k, seed, tag, out)
+    assert np.array_equal(out.cpu().numpy(), rng.floyd(N, k, seed, tag))
+
+
+def test_uniform_indices_rejects_k_gt_n(dev):
+    out = torch.zeros(8, dtype=torch.int64, device=dev)
+    with pytest.raises(C.CabsError):
+        C.cabs_uniform_indices(4, 5, 0, 1, out)
+
+
+# ------------------------------------------------------------------ S2/S3 gathers
+@pytest.mark.parametrize("m,n,k,lda", [(2000, 1500, 20, None), (777, 333, 31, 340), (129, 67, 1, None),
+                                       (300, 250, 250, 251)])
+def test_pilot_gathers_bit_exact(dev, m, n, k, lda):
+    A, T = _A(m, n, m + n, dev, lda=lda)
+    plan = _plan(m, n, k)
+    ws = _ws(plan, dev)
+    ld = C.cabs_padded_ld(k)
+    I = torch.zeros(k, dtype=torch.int64, device=dev); J = torch.zeros_like(I)
+    Cm = torch.zeros((m, ld), device=dev); R = torch.zeros((k, (n + 3) // 4 * 4), device=dev)
+    W = torch.zeros((k, ld), device=dev)
+    C.cabs_pilot(plan, T, k, 42, I, J, Cm, R, W, ws)
+    I_ref, J_ref = rng.floyd(m, k, 42, rng.TAG_PILOT_ROWS), rng.floyd(n, k, 42, rng.TAG_PILOT_COLS)
+    assert np.array_equal(I.cpu().numpy(), I_ref) and np.array_equal(J.cpu().numpy(), J_ref)
+    Cr, Rr, Wr = O.gather(A, I_ref, J_ref)
+    assert np.array_equal(Cm.cpu().numpy()[:, :k], Cr.astype(np.float32))
+    assert np.array_equal(R.cpu().numpy()[:, :n], Rr.astype(np.float32))
+    assert np.array_equal(W.cpu().numpy()[:, :k], Wr.astype(np.float32))
+    assert C.cabs_device_status(ws) == 0
+
+
+def test_pilot_flags_nonfinite(dev):
+    A, T = _A(200, 150, 1, dev)
+    T[:, :] = float("nan")
+    plan = _plan(200, 150, 5)
+    ws = _ws(plan, dev)
+    ld = C.cabs_padded_ld(5)
+    I = torch.zeros(5, dtype=torch.int64, device=dev); J = torch.zeros_like(I)
+    C.cabs_pilot(plan, T, 5, 0, I, J, torch.zeros((200, ld), device=dev), torch.zeros((5, 152), device=dev),
+                 torch.zeros((5, ld), device=dev), ws)
+    assert C.cabs_device_status(ws) & C.DEV_NONFINITE
+
+
+def test_pilot_invalid_k(dev):
+    A, T = _A(50, 40, 1, dev)
+    plan = _plan(50, 40, 41)
+    ws = _ws(plan, dev)
+    I = torch.zeros(41, dtype=torch.int64, device=dev)
+    with pytest.raises(C.CabsError):
+        C.cabs_pilot(plan, T, 41, 0, I, I, torch.zeros((50, 64), device=dev), torch.zeros((41, 40), device=dev),
+                     torch.zeros((41, 64), device=dev), ws)
+
+
+# ------------------------------------------------------------------ S4 SVD
+@pytest.mark.parametrize("k,rank", [(20, 20), (50, 50), (100, 100), (112, 60), (150, 150), (7, 3), (1, 1)])
+def test_svd_matches_lapack(dev, k, rank):
+    g = np.random.default_rng(k * 7 + rank)
+    W = (g.standard_normal((k, rank)) @ g.standard_normal((rank, k))).astype(np.float32)
+    plan = _plan(max(k, 2), max(k, 2), k)
+    ws = _ws(plan, dev)
+    Wt = torch.from_numpy(W).to(dev)
+    sig = torch.zeros(k, dtype=torch.float64, device=dev)
+    Uw = torch.zeros((k, k), dtype=torch.float64, device=dev); Vw = torch.zeros_like(Uw)
+    r = torch.zeros(1, dtype=torch.int32, device=dev)
+    C.cabs_svd(plan, k, Wt, 1e-12, sig, Uw, Vw, r, ws)
+    assert C.cabs_device_status(ws) == 0
+    s_ref = np.linalg.svd(W.astype(np.float64), compute_uv=False)
+    sg = sig.cpu().numpy()
+    assert np.all(np.abs(sg - s_ref) <= 1e-12 * s_ref[0] + 1e-13 * s_ref)
+    Ur, sr, Vr = O.svd_w(W)
+    rr = int(r.item())
+    assert rr == sr.size
+    Ug, Vg = Uw.cpu().numpy()[:, :rr], Vw.cpu().numpy()[:, :rr]
+    # reconstruction and orthogonality of the GPU factors
+    assert np.linalg.norm((Ug * sg[:rr]) @ Vg.T - W) <= 1e-10 * np.linalg.norm(W)
+    assert np.allclose(Vg.T @ Vg, np.eye(rr), atol=1e-10)
+    # singular vectors match LAPACK (canonical signs) where the spectrum is well separated
+    gaps = np.abs(np.diff(np.concatenate([[np.inf], sr, [0]])))
+    for c in range(rr):
+        if min(gaps[c], gaps[c + 1]) > 1e-6 * sr[0]:
+            assert np.linalg.norm(Ug[:, c] - Ur[:, c]) < 1e-8 * sr[0] / min(gaps[c], gaps[c + 1])
+
+
+# ------------------------------------------------------------------ S4-S5 embed
+@pytest.mark.parametrize("mode", [C.STABILIZED, C.PSEUDO_SKELETON])
+@pytest.mark.parametrize("m,n,k", [(2000, 1500, 20), (1037, 611, 45), (500, 400, 100)])
+def test_embed_matches_oracle(dev, mode, m, n, k):
+    A, T = _A(m, n, m * 3 + k, dev, r=min(k + 5, 60))
+    plan = _plan(m, n, k)
+    ws = _ws(plan, dev)
+    ld = C.cabs_padded_ld(k)
+    I = torch.zeros(k, dtype=torch.int64, device=dev); J = torch.zeros_like(I)
+    Cm = torch.zeros((m, ld), device=dev); R = torch.zeros((k, (n + 3) // 4 * 4), device=dev)
+    W = torch.zeros((k, ld), device=dev)
+    C.cabs_pilot(plan, T, k, 1, I, J, Cm, R, W, ws)
+    P = torch.zeros((m, ld), device=dev); Q = torch.zeros((n, ld), device=dev)
+    s = torch.zeros(k, device=dev); r = torch.zeros(1, dtype=torch.int32, device=dev)
+    C.cabs_embed(plan, k, Cm, R, W, mode, 1e-12, P, Q, s, r, ws)
+    sk = O.sketch(*O.gather(A, I.cpu().numpy(), J.cpu().numpy()), m, n, k, mode=mode)
+    Pr, Qr = O.embeddings(sk)
+    rr = int(r.item())
+    assert rr == sk.r
+    assert rel_fro(s.cpu().numpy()[:rr], sk.s) < 1e-5
+    Pg, Qg = P.cpu().numpy(), Q.cpu().numpy()
+    assert np.all(Pg[:, rr:] == 0) and np.all(Qg[:, rr:] == 0)
+    assert rel_fro(align_signs(Pg[:, :rr], Pr), Pr) < 1e-4
+    assert rel_fro(align_signs(Qg[:, :rr], Qr), Qr) < 1e-4
+    # P Q^T = U S V^T (P11) -- product is sign invariant
+    assert rel_fro(Pg[:, :rr] @ Qg[:, :rr].T, sk.dense()) < 1e-4
+
+
+# ------------------------------------------------------------------ S6-S7 k-means (teacher-forced)
+def _clustered(N, d, ncl, seed, spread=0.05):
+    g = np.random.default_rng(seed)
+    cen = g.standard_normal((ncl, d)) * 3
+    lab = g.integers(0, ncl, N)
+    return (cen[lab] + spread * g.standard_normal((N, d))).astype(np.float32)
+
+
+@pytest.mark.parametrize("N,d,k2,iters,wk", [(3000, 20, 20, 10, C.WEIGHT_CONST), (20000, 50, 50, 5, C.WEIGHT_CONST),
+                                             (1111, 37, 13, 6, C.WEIGHT_POWER), (700, 100, 100, 3, C.WEIGHT_CONST),
+                                             (5000, 8, 300, 2, C.WEIGHT_CONST)])
+def test_kmeans_matches_oracle(dev, N, d, k2, iters, wk):
+    X = _clustered(N, d, max(k2 // 2, 2), N + d)
+    ld = C.cabs_padded_ld(d)
+    Xt = torch.zeros((N, ld), device=dev); Xt[:, :d] = torch.from_numpy(X).to(dev)
+    plan = _plan(N, N, max(d, k2))
+    ws = _ws(plan, dev)
+    cen = torch.zeros((k2, ld), device=dev)
+    lab = torch.zeros(N, dtype=torch.int32, device=dev)
+    cw = torch.zeros(k2, dtype=torch.float64, device=dev)
+    obj = torch.zeros(iters, dtype=torch.float64, device=dev)
+    ties = torch.zeros(iters, dtype=torch.int32, device=dev)
+    C.cabs_kmeans(plan, Xt, N, N, 0, d, k2, iters, wk, 2.0, 5, C.TAG_INIT_ROWS, cen, lab, cw, obj, ws,
+                  near_ties=ties)
+    w = O.weights(X, wk, 2.0)
+    ref = O.lloyd(X, k2, iters, w, seed=5, tag=rng.TAG_INIT_ROWS)
+    log = []
+    bad, unexcused = label_mismatches(lab.cpu().numpy(), ref.labels, ref.gaps[-1], log, "labels")
+    assert not unexcused, f"label flips without near tie: {log[:5]}"
+    if bad.size == 0:
+        assert rel_fro(cen.cpu().numpy()[:, :d], ref.centres) < 1e-5
+        assert np.allclose(cw.cpu().numpy(), ref.cluster_w, rtol=1e-6)
+        assert np.allclose(obj.cpu().numpy(), ref.objective, rtol=1e-4, atol=1e-6 * ref.objective[0])
+    og = obj.cpu().numpy()
+    assert np.all(og[1:] <= og[:-1] * (1 + 1e-6))   # P8 on the GPU
+
+
+def test_kmeans_explicit_init_and_empty_cluster(dev):
+    X = np.array([[0.0], [1.0], [2.0], [10.0], [11.0]], dtype=np.float32)
+    Xt = torch.zeros((5, 32), device=dev); Xt[:, :1] = torch.from_numpy(X).to(dev)
+    plan = _plan(5, 5, 32)
+    ws = _ws(plan, dev)
+    cen = torch.zeros((2, 32), device=dev)
+    lab = torch.zeros(5, dtype=torch.int32, device=dev)
+    cw = torch.zeros(2, dtype=torch.float64, device=dev)
+    obj = torch.zeros(10, dtype=torch.float64, device=dev)
+    init = torch.tensor([0, 1], dtype=torch.int64, device=dev)
+    C.cabs_kmeans(plan, Xt, 5, 5, 0, 1, 2, 10, C.WEIGHT_CONST, 2.0, 0, 3, cen, lab, cw, obj, ws, init_idx=init)
+    assert sorted(cen.cpu().numpy()[:, 0].tolist()) == [1.0, 10.5]
+    reps = torch.zeros(2, dtype=torch.int64, device=dev)
+    gap = torch.zeros(2, device=dev)
+    rep_of = torch.zeros(2, dtype=torch.int64, device=dev)
+    C.cabs_select(plan, Xt, 5, 5, 0, 1, cen, 2, cw, reps, ws, rep_of_centre=rep_of, gap=gap)
+    assert reps.cpu().tolist() == [1, 3]          # exact tie 10 vs 11 -> lowest index
+    j = int(np.argmax(cen.cpu().numpy()[:, 0]))
+    assert gap.cpu().numpy()[j] == 0.0
+    # empty cluster keeps its centre (Z12)
+    init_c = torch.zeros((2, 32), device=dev); init_c[0, 0] = 1.0; init_c[1, 0] = 100.0
+    C.cabs_kmeans(plan, Xt[:3], 3, 3, 0, 1, 2, 2, C.WEIGHT_CONST, 2.0, 0, 3, cen, lab, cw, obj, ws,
+                  init_centres=init_c)
+    assert cen.cpu().numpy()[1, 0] == 100.0 and cw.cpu().numpy()[1] == 0.0
+
+
+# ------------------------------------------------------------------ S8 select (teacher-forced)
+@pytest.mark.parametrize("N,d,k2", [(3000, 20, 20), (20000, 50, 50), (999, 17, 64), (4000, 10, 300)])
+def test_select_matches_oracle(dev, N, d, k2):
+    X = _clustered(N, d, max(k2 // 3, 2), N * 2 + d, spread=0.3)
+    ld = C.cabs_padded_ld(d)
+    Xt = torch.zeros((N, ld), device=dev); Xt[:, :d] = torch.from_numpy(X).to(dev)
+    g = np.random.default_rng(d)
+    cen = X[g.choice(N, k2, replace=False)] + 0.01 * g.standard_normal((k2, d)).astype(np.float32)
+    cw = g.integers(0, 50, k2).astype(np.float64)
+    plan = _plan(N, N, max(d, k2))
+    ws = _ws(plan, dev)
+    cen_t = torch.zeros((k2, ld), device=dev); cen_t[:, :d] = torch.from_numpy(cen).to(dev)
+    reps = torch.zeros(k2, dtype=torch.int64, device=dev)
+    rep_of = torch.zeros(k2, dtype=torch.int64, device=dev)
+    gap = torch.zeros(k2, device=dev)
+    C.cabs_select(plan, Xt, N, N, 0, d, cen_t, k2, torch.from_numpy(cw).to(dev), reps, ws, rep_of_centre=rep_of,
+                  gap=gap)
+    ref = O.snap(X, cen.astype(np.float64), cw)
+    got = rep_of.cpu().numpy()
+    if not np.array_equal(got, ref.rep_of_centre):
+        # the first disagreement in visiting order must be a near tie
+        for j in ref.order:
+            if got[j] != ref.rep_of_centre[j]:
+                assert ref.gap[j] < NEAR_TIE, f"centre {j}: {got[j]} vs {ref.rep_of_centre[j]} gap {ref.gap[j]}"
+                break
+    else:
+        assert np.array_equal(reps.cpu().numpy(), ref.reps_sorted)
+    assert np.unique(got).size == k2
+
+
+# ------------------------------------------------------------------ S9 sketch with given indices
+@pytest.mark.parametrize("mode", [C.STABILIZED, C.PSEUDO_SKELETON])
+def test_sketch_given_indices(dev, mode):
+    m, n, k = 1500, 1100, 40
+    A, T = _A(m, n, 77, dev, r=30)
+    g = np.random.default_rng(3)
+    Ir = np.sort(g.choice(m, k, replace=False)); Ic = np.sort(g.choice(n, k, replace=False))
+    plan = _plan(m, n, k)
+    ws = _ws(plan, dev)
+    ld = C.cabs_padded_ld(k)
+    U = torch.zeros((m, ld), device=dev); V = torch.zeros((n, ld), device=dev)
+    s = torch.zeros(k, device=dev); r = torch.zeros(1, dtype=torch.int32, device=dev)
+    C.cabs_sketch(plan, T, torch.from_numpy(Ir).to(dev), torch.from_numpy(Ic).to(dev), k, mode, 1e-12, U, s, V, r, ws)
+    sk = O.sketch(*O.gather(A, Ir, Ic), m, n, k, mode=mode)
+    rr = int(r.item())
+    assert rr == sk.r
+    assert rel_fro(align_signs(U.cpu().numpy()[:, :rr], sk.U), sk.U) < 1e-4
+    assert rel_fro(align_signs(V.cpu().numpy()[:, :rr], sk.V), sk.V) < 1e-4
+    assert rel_fro(s.cpu().numpy()[:rr], sk.s) < 1e-4
+
+
+def test_sketch_flags_bad_indices(dev):
+    m, n, k = 100, 80, 4
+    A, T = _A(m, n, 5, dev)
+    plan = _plan(m, n, k)
+    ws = _ws(plan, dev)
+    U = torch.zeros((m, 32), device=dev); V = torch.zeros((n, 32), device=dev)
+    s = torch.zeros(k, device=dev); r = torch.zeros(1, dtype=torch.int32, device=dev)
+    Ir = torch.tensor([0, 1, 1, 3], dtype=torch.int64, device=dev)
+    Ic = torch.tensor([0, 1, 2, 79], dtype=torch.int64, device=dev)
+    C.cabs_sketch(plan, T, Ir, Ic, k, C.STABILIZED, 1e-12, U, s, V, r, ws)
+    assert C.cabs_device_status(ws) & C.DEV_DUPLICATE
+
+
+# ------------------------------------------------------------------ S10 residual
+@pytest.mark.parametrize("m,n,k,use_s", [(2000, 1500, 20, True), (1000, 777, 50, False), (129, 257, 7, True),
+                                         (4096, 2048, 100, True), (300, 200, 1, False)])
+def test_residual_matches_oracle(dev, m, n, k, use_s):
+    A, T = _A(m, n, m + k, dev, r=k)
+    g = np.random.default_rng(k)
+    F = g.standard_normal((m, k)).astype(np.float32) * 0.1
+    G = g.standard_normal((n, k)).astype(np.float32) * 0.1
+    s = g.uniform(0.5, 2.0, k).astype(np.float32) if use_s else None
+    plan = _plan(m, n, k)
+    ws = _ws(plan, dev)
+    ld = C.cabs_padded_ld(k)
+    Ft = torch.zeros((m, ld), device=dev); Ft[:, :k] = torch.from_numpy(F).to(dev)
+    Gt = torch.zeros((n, ld), device=dev); Gt[:, :k] = torch.from_numpy(G).to(dev)
+    st = torch.from_numpy(s).to(dev) if use_s else None
+    out = torch.zeros(2, dtype=torch.float64, device=dev)
+    C.cabs_residual(plan, T, Ft, st, Gt, k, out, ws)
+    r2, a2 = O.residual(A, F, G, s)
+    o = out.cpu().numpy()
+    assert abs(o[1] - a2) <= 1e-6 * a2
+    assert abs(math.sqrt(o[0]) - math.sqrt(r2)) <= 1e-4 * math.sqrt(r2) + 1e-6 * math.sqrt(a2)
+
+
+def test_residual_exact_factorisation_is_small(dev):
+    # A = F G^T exactly representable: residual at the FP32 rounding floor, far below ||A||
+    m, n, k = 1024, 768, 16
+    g = np.random.default_rng(0)
+    F = g.integers(-3, 4, (m, k)).astype(np.float32)
+    G = g.integers(-3, 4, (n, k)).astype(np.float32)
+    A = (F.astype(np.float64) @ G.T.astype(np.float64)).astype(np.float32)  # small integers: exact
+    plan = _plan(m, n, k)
+    ws = _ws(plan, dev)
+    out = torch.zeros(2, dtype=torch.float64, device=dev)
+    Ft = torch.zeros((m, 32), device=dev); Ft[:, :k] = torch.from_numpy(F).to(dev)
+    Gt = torch.zeros((n, 32), device=dev); Gt[:, :k] = torch.from_numpy(G).to(dev)
+    C.cabs_residual(plan, torch.from_numpy(A).to(dev), Ft, None, Gt, k, out, ws)
+    assert out[0].item() == 0.0 and out[1].item() == float(np.sum(A.astype(np.float64) ** 2))
