@@ -117,6 +117,9 @@ int64_t cabs_padded_ld(int32_t k);
 size_t cabs_workspace_bytes(const cabs_plan* plan);
 /* Zero the device status word (stream-ordered). */
 int32_t cabs_clear_status(void* ws, void* stream);
+/* Number of kernel launches this library has issued in this process (host-side counter;
+ * benchmarks report the delta over a timed region as their launch count). */
+int64_t cabs_launch_count(void);
 /* Synchronises `stream`, then copies the device status word to host *flags. */
 int32_t cabs_device_status(const void* ws, void* stream, uint32_t* flags);
 

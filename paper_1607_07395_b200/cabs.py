@@ -72,6 +72,7 @@ _SIGS = {
     "cabs_last_error_string": (ctypes.c_char_p, []),
     "cabs_version": (None, [ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "cabs_padded_ld": (c_i64, [c_i32]),
+    "cabs_launch_count": (c_i64, []),
     "cabs_workspace_bytes": (c_sz, [ctypes.POINTER(Plan)]),
     "cabs_clear_status": (c_i32, [c_vp, c_vp]),
     "cabs_device_status": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_u32)]),
@@ -162,6 +163,10 @@ def cabs_workspace_bytes(plan: Plan) -> int:
     if n == 0:
         raise CabsError("invalid plan")
     return n
+
+
+def cabs_launch_count() -> int:
+    return int(load().cabs_launch_count())
 
 
 def cabs_version():

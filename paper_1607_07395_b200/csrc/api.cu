@@ -2,12 +2,19 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 using namespace cabsk;
 
 static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+namespace cabsk {
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace cabsk
 
 void cabs_set_cuda_error(cudaError_t e, const char* where) {
   snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
@@ -75,6 +82,8 @@ const char* cabs_status_string(int32_t s) {
 }
 
 const char* cabs_last_error_string(void) { return g_err; }
+
+int64_t cabs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 void cabs_version(int32_t* major, int32_t* minor) {
   if (major) *major = CABS_VERSION_MAJOR;

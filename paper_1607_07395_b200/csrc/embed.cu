@@ -117,7 +117,9 @@ int launch_embed_products(int64_t m_loc, int64_t n_sl, int k, const float* C, in
   // Y_c = C V_w
   if (m_loc > 0) {
     dim3 g(static_cast<unsigned>(ceil_div(m_loc, kGemmBM)), gy);
+    note_launch();
     embed_gemm_kernel<false><<<g, 256, 0, st>>>(C, ldc, m_loc, k, wsp<float>(ws, L.vw32), L.Kp, Yc, ldyc, part, L.Kp);
+    note_launch();
     reduce_cols_kernel<<<k, 256, 0, st>>>(part, ceil_div(m_loc, kGemmBM), L.Kp, k, norms);
   } else {
     cudaMemsetAsync(norms, 0, sizeof(double) * k, st);
@@ -126,8 +128,10 @@ int launch_embed_products(int64_t m_loc, int64_t n_sl, int k, const float* C, in
   double* part_r = part + L.npt * L.Kp;
   if (n_sl > 0) {
     dim3 g(static_cast<unsigned>(ceil_div(n_sl, kGemmBM)), gy);
+    note_launch();
     embed_gemm_kernel<true><<<g, 256, 0, st>>>(R_slice, ldr, n_sl, k, wsp<float>(ws, L.uw32), L.Kp, Yr, ldyr, part_r,
                                                L.Kp);
+    note_launch();
     reduce_cols_kernel<<<k, 256, 0, st>>>(part_r, ceil_div(n_sl, kGemmBM), L.Kp, k, norms + L.Kp);
   } else {
     cudaMemsetAsync(norms + L.Kp, 0, sizeof(double) * k, st);
@@ -228,6 +232,7 @@ int launch_embed_finalize(int k, int mode, double m, double n, double ksamp, int
   int* newpos = reinterpret_cast<int*>(sc + 2 * L.Kp);
   const double* norms = wsp<double>(ws, L.norms);
   int* scal = wsp<int>(ws, L.scal);
+  note_launch();
   embed_finalize_kernel<<<1, 32, 0, st>>>(k, wsp<double>(ws, L.sig64), scal + SCAL_R_TMP, norms, norms + L.Kp, mode, m,
                                           n, ksamp, kind, sc, sc + L.Kp, newpos, s_out, scal + SCAL_R_TMP, r_user);
   return 0;
@@ -239,6 +244,7 @@ int launch_scale_compact(float* Y, int64_t ldy, int64_t N, int k, int which, voi
   int* newpos = reinterpret_cast<int*>(sc + 2 * L.Kp);
   int64_t blocks = ceil_div(N, 8);
   if (blocks > 8 * kNumSM) blocks = 8 * kNumSM;
+  note_launch();
   scale_compact_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(Y, ldy, N, k, sc + which * L.Kp, newpos);
   return 0;
 }

@@ -4,6 +4,9 @@
 
 namespace cabsk {
 
+// host-side count of kernel launches issued by this library (cabs_launch_count)
+void note_launch();
+
 // sample_gather.cu
 int launch_floyd2(int64_t N0, int32_t k0, uint32_t tag0, int64_t* out0, int64_t N1, int32_t k1, uint32_t tag1,
                   int64_t* out1, uint64_t seed, cudaStream_t st);

@@ -49,6 +49,7 @@ void launch_km_weights(const float* X, int64_t ldx, int64_t N, int d, int kind, 
   if (N <= 0) return;
   int64_t blocks = ceil_div(N, 8);
   if (blocks > 8 * kNumSM) blocks = 8 * kNumSM;
+  note_launch();
   km_weights_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(X, ldx, N, d, kind, p, w, cnt);
 }
 
@@ -71,6 +72,7 @@ __global__ void km_init_kernel(const float* __restrict__ X, int64_t ldx, int64_t
 
 void launch_km_init(const float* X, int64_t ldx, int64_t n_loc, int64_t row_off, int d, int k2, const int64_t* idx,
                     const float* init_c, int64_t ldic, float* centres, int64_t ldc, cudaStream_t st) {
+  note_launch();
   km_init_kernel<<<k2, 128, 0, st>>>(X, ldx, n_loc, row_off, d, idx, init_c, ldic, centres, ldc);
 }
 
@@ -229,6 +231,7 @@ void launch_km_assign(const float* X, int64_t ldx, int64_t N, int d, const float
                       const float* w, int* labels, double* pobj, int* ptie, int* grid_out, cudaStream_t st) {
   const int g = assign_grid(N);
   *grid_out = g;
+  note_launch();
   km_assign_kernel<false><<<g, 256, 0, st>>>(X, ldx, N, d, centres, ldc, k2, w, labels, pobj, ptie, nullptr, 0);
 }
 
@@ -236,6 +239,7 @@ void launch_km_distmat(const float* X, int64_t ldx, int64_t N, int d, const floa
                        float* D, int64_t ldd, cudaStream_t st) {
   if (N <= 0) return;
   const int g = assign_grid(N);
+  note_launch();
   km_assign_kernel<true><<<g, 256, 0, st>>>(X, ldx, N, d, centres, ldc, k2, nullptr, nullptr, nullptr, nullptr, D, ldd);
 }
 
@@ -306,6 +310,7 @@ void launch_km_accum(const float* X, int64_t ldx, int64_t N, int d, const int* l
   *grid_out = static_cast<int>(G);
   dim3 grid(static_cast<unsigned>(G), static_cast<unsigned>(ceil_div(d, 32)));
   size_t smem = (size_t)k2 * 32 * sizeof(float) + (size_t)k2 * sizeof(double);
+  note_launch();
   km_accum_kernel<<<grid, 256, smem, st>>>(X, ldx, N, d, labels, w, k2, psum, pw, ldps);
 }
 
@@ -340,6 +345,7 @@ __global__ void km_reduce_kernel(const float* __restrict__ psum, const double* _
 void launch_km_reduce(const float* psum, const double* pw, int G, int k2, int d, int64_t ldps, const double* pobj,
                       const int* ptie, int Gobj, double* red, cudaStream_t st) {
   const int64_t total = (int64_t)k2 * d + k2 + 2;
+  note_launch();
   km_reduce_kernel<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, st>>>(psum, pw, G, k2, d, ldps, pobj, ptie,
                                                                                  Gobj, red);
 }
@@ -369,6 +375,7 @@ void launch_km_finalize(const double* red, int k2, int d, float* centres, int64_
   int64_t blocks = ceil_div((int64_t)k2 * d, 256);
   if (blocks > 4 * kNumSM) blocks = 4 * kNumSM;
   if (blocks < 1) blocks = 1;
+  note_launch();
   km_finalize_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(red, k2, d, centres, ldc, objective, near_ties,
                                                                      cluster_w, t);
 }

@@ -111,10 +111,13 @@ int launch_residual(const float* A, int64_t lda, int64_t m_loc, int64_t n, const
   const int64_t ntiles = ceil_div(m_loc, kRBM) * ceil_div(n, kRBN);
   int64_t g = ntiles < kResGrid ? ntiles : kResGrid;
   if (g < 1) g = 1;
-  if (m_loc > 0 && n > 0)
+  if (m_loc > 0 && n > 0) {
+    note_launch();
     residual_ffma_kernel<<<static_cast<unsigned>(g), 256, 0, st>>>(A, lda, m_loc, n, F, ldf, s, G, ldg, ncomp, part);
-  else
+  } else {
     cudaMemsetAsync(part, 0, sizeof(double) * 2 * g, st);
+  }
+  note_launch();
   residual_final_kernel<<<1, 256, 0, st>>>(part, static_cast<int>(g), out);
   return 0;
 }

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(64) floyd_kernel(FloydJob j0, FloydJob j1, uin
 int launch_floyd2(int64_t N0, int32_t k0, uint32_t tag0, int64_t* out0, int64_t N1, int32_t k1,
                   uint32_t tag1, int64_t* out1, uint64_t seed, cudaStream_t st) {
   FloydJob a{N0, k0, tag0, out0}, b{N1, k1, tag1, out1};
+  note_launch();
   floyd_kernel<<<1, 64, 0, st>>>(a, b, seed);
   return 0;
 }
@@ -82,6 +83,7 @@ __global__ void philox_blocks_kernel(uint64_t seed, uint32_t tag, uint64_t start
 void launch_philox_blocks(uint64_t seed, uint32_t tag, uint64_t start, int64_t count, uint32_t* out,
                           cudaStream_t st) {
   if (count <= 0) return;
+  note_launch();
   philox_blocks_kernel<<<static_cast<unsigned>(ceil_div(count, 256)), 256, 0, st>>>(seed, tag, start, count,
                                                                                     out);
 }
@@ -98,6 +100,7 @@ __global__ void validate_idx_kernel(const int64_t* idx, int32_t k, int64_t N, vo
 }
 
 void launch_validate_idx(const int64_t* idx, int32_t k, int64_t N, void* ws, cudaStream_t st) {
+  note_launch();
   validate_idx_kernel<<<1, 256, 0, st>>>(idx, k, N, ws);
 }
 
@@ -145,6 +148,7 @@ void launch_gather_rows(const float* A, int64_t lda, int64_t row_begin, int64_t 
   if (gx > 64) gx = 64;
   if (gx < 1) gx = 1;
   dim3 grid(gx, k);
+  note_launch();
   gather_rows_kernel<<<grid, 256, 0, st>>>(A, lda, row_begin, row_end, I, n, R, ldr, vec4, ws);
 }
 
@@ -194,6 +198,7 @@ void launch_gather_cols(const float* A, int64_t lda, int64_t m_loc, const int64_
   int64_t warps = ceil_div(m_loc, kColRowsPerWarp);
   int64_t blocks = ceil_div(warps, 8);
   if (blocks > 16 * kNumSM) blocks = 16 * kNumSM;
+  note_launch();
   gather_cols_kernel<<<static_cast<unsigned>(blocks), 256, sizeof(int32_t) * k, st>>>(A, lda, m_loc, J, k, C,
                                                                                       ldc, ws);
 }
@@ -207,6 +212,7 @@ __global__ void gather_w_kernel(const float* __restrict__ R, int64_t ldr, const 
 
 void launch_gather_w(const float* R, int64_t ldr, const int64_t* J, int32_t k, float* W, int64_t ldw,
                      cudaStream_t st) {
+  note_launch();
   gather_w_kernel<<<k, 128, 0, st>>>(R, ldr, J, k, W, ldw);
 }
 

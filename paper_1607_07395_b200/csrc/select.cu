@@ -85,10 +85,13 @@ __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict_
 
 void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t row_off, int T, float* cand_d,
                       int64_t* cand_i, cudaStream_t st) {
-  if (T == kSnapT)
+  if (T == kSnapT) {
+    note_launch();
     snap_topT_kernel<kSnapT><<<k2, 256, 0, st>>>(D, ldd, N, row_off, cand_d, cand_i);
-  else
+  } else {
+    note_launch();
     snap_topT_kernel<kSnapTMulti><<<k2, 256, 0, st>>>(D, ldd, N, row_off, cand_d, cand_i);
+  }
 }
 
 // ---------------------------------------------------------------- multi-rank candidate exchange
@@ -107,6 +110,7 @@ __global__ void snap_pack_kernel(const float* __restrict__ cand_d, const int64_t
 
 void launch_snap_pack(const float* cand_d, const int64_t* cand_i, int k2, int T, int rank, int nranks, double* all,
                       cudaStream_t st) {
+  note_launch();
   snap_pack_kernel<<<64, 256, 0, st>>>(cand_d, cand_i, k2, T, rank, nranks, all);
 }
 
@@ -135,6 +139,7 @@ __global__ void snap_merge_kernel(const double* __restrict__ all, int k2, int T,
 }
 
 void launch_snap_merge(const double* all, int k2, int T, int nranks, float* cand_d, int64_t* cand_i, cudaStream_t st) {
+  note_launch();
   snap_merge_kernel<<<static_cast<unsigned>(ceil_div(k2, 128)), 128, 0, st>>>(all, k2, T, nranks, cand_d, cand_i);
 }
 
@@ -267,6 +272,7 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* __restric
 void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int T, const double* cluster_w,
                         const float* D, int64_t ldd, int64_t N, int64_t row_off, bool can_rescan,
                         int64_t* rep_of_centre, float* gap, int64_t* reps_sorted, void* ws, cudaStream_t st) {
+  note_launch();
   snap_dedupe_kernel<<<1, 256, 0, st>>>(cand_d, cand_i, k2, T, cluster_w, D, ldd, N, row_off, can_rescan, rep_of_centre,
                                         gap, reps_sorted, ws);
 }

@@ -183,6 +183,7 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
   size_t smem = use_smem ? 2 * (size_t)k * k * sizeof(double) : 0;
   double* sig = sigma_user ? sigma_user : wsp<double>(ws, L.sig64);
   int* r_ws = wsp<int>(ws, L.scal) + SCAL_R_TMP;
+  note_launch();
   svd_jacobi_kernel<<<1, kSvdThreads, smem, st>>>(k, W, ldw, tol, wsp<double>(ws, L.a64), wsp<double>(ws, L.v64),
                                                   sig, Uw64, Vw64, wsp<float>(ws, L.uw32), wsp<float>(ws, L.vw32),
                                                   L.Kp, r_ws, r_user, use_smem, ws);
