@@ -1,5 +1,6 @@
 // api.cu -- the extern "C" boundary of libcabs.so (declared and documented in include/cabs.h).
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -265,6 +266,16 @@ int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   launch_km_init(X, ldx, n_loc, row_off, d, k2, init_centres ? nullptr : idx, init_centres, ldc, centres, ldc, st);
   CABS_LAUNCH_CHECK("km_init");
   if (!init_centres) CABS_TRY(comm_f32(comm, centres, ldc * (int64_t)k2, stream));
+  const char* path = getenv("CABS_KMEANS_PATH");  // "loop" forces the per-iteration kernels (tests)
+  const bool allow_persistent = !(path && strcmp(path, "loop") == 0);
+  if (allow_persistent && !multi(comm) && n_loc > 0 &&
+      launch_lloyd_persistent(X, ldx, n_loc, d, k2, iters, w, centres, ldc, labels, objective, near_ties, cluster_w,
+                              wsp<float>(ws, L.km_psum), wsp<double>(ws, L.km_pw), wsp<double>(ws, L.km_pobj),
+                              wsp<int>(ws, L.km_ptie), kAccGrid, st)) {
+    CABS_LAUNCH_CHECK("lloyd_persistent");
+    return CABS_OK;
+  }
+  cudaGetLastError();  // a refused cooperative launch is not an error: use the per-iteration kernels
   double* red = wsp<double>(ws, L.km_red);
   const int64_t payload = (int64_t)k2 * d + k2 + 2;
   for (int t = 0; t < iters; ++t) {

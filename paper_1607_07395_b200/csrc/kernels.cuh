@@ -46,6 +46,12 @@ void launch_km_reduce(const float* psum, const double* pw, int G, int k2, int d,
 void launch_km_finalize(const double* red, int k2, int d, float* centres, int64_t ldc, double* objective,
                         int* near_ties, double* cluster_w, int t, cudaStream_t st);
 
+// lloyd.cu (single-GPU persistent Lloyd loop; false -> use the per-iteration kernels)
+bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int k2, int iters, const float* w,
+                             float* centres, int64_t ldc, int* labels, double* objective, int* near_ties,
+                             double* cluster_w, float* psum, double* pw, double* pobj, int* ptie, int max_grid,
+                             cudaStream_t st);
+
 // select.cu
 void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t row_off, int T, float* cand_d,
                       int64_t* cand_i, cudaStream_t st);

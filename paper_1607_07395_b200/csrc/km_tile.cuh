@@ -1,0 +1,156 @@
+// km_tile.cuh -- the 64-point x all-centres distance tile shared by the k-means kernels.
+// Squared distances by DIRECT differences in FP32, dimensions in ascending order
+// (the same arithmetic in every kernel, so labels never depend on the launch shape).
+#pragma once
+#include <float.h>
+
+#include "common.cuh"
+
+namespace cabsk {
+
+constexpr int kTileP = 64, kTileC = 64, kTileD = 16;
+constexpr float kNearTie = 1e-5f;  // north_star near-tie rule: relative gap (d2 - d1)/d2 < 1e-5
+
+struct KmTileSmem {
+  float Xs[kTileD][kTileP + 4];
+  float Cs[kTileD][kTileC + 4];
+  float sb_d[16][kTileP + 1];
+  int sb_j[16][kTileP + 1];
+  float ss_d[16][kTileP + 1];
+};
+
+// centres may be rewritten by other CTAs inside a persistent kernel: COHERENT loads
+// them through L2 only (ld.global.cg) instead of the read-only path.
+template <bool COHERENT>
+__device__ __forceinline__ float ld_centre(const float* p) {
+  if (COHERENT) return __ldcg(p);
+  return __ldg(p);
+}
+
+// acc[a][b] = ||X_{p0 + tp + 16a} - c_{j0 + tc + 16b}||^2 for one 64 x 64 block.
+template <bool COHERENT>
+__device__ __forceinline__ void km_tile_block(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
+                                              const float* __restrict__ centres, int64_t ldc, int k2, int64_t p0,
+                                              int j0, KmTileSmem& sm, float (&acc)[4][4]) {
+  const int tid = threadIdx.x, tp = tid & 15, tc = tid >> 4;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+  for (int i0 = 0; i0 < d; i0 += kTileD) {
+    {
+      const int pp = tid >> 2, ii = (tid & 3) * 4;
+      const int64_t p = p0 + pp;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + ii + q;
+        sm.Xs[ii + q][pp] = (p < N && i < d) ? __ldg(X + p * ldx + i) : 0.f;
+      }
+      const int j = j0 + pp;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + ii + q;
+        sm.Cs[ii + q][pp] = (j < k2 && i < d) ? ld_centre<COHERENT>(centres + (int64_t)j * ldc + i) : 0.f;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ii = 0; ii < kTileD; ++ii) {
+      float x[4], c[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) x[a] = sm.Xs[ii][tp + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) c[b] = sm.Cs[ii][tc + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const float df = x[a] - c[b];
+          acc[a][b] = fmaf(df, df, acc[a][b]);
+        }
+    }
+    __syncthreads();
+  }
+}
+
+// Nearest centre (lowest index on ties), its distance and the runner-up distance for the
+// 64 points starting at p0 -> lab_s, d1_s, d2_s (shared).  Block-wide; ends synchronised.
+template <bool COHERENT>
+__device__ __forceinline__ void km_tile_argmin(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
+                                               const float* __restrict__ centres, int64_t ldc, int k2, int64_t p0,
+                                               KmTileSmem& sm, int* lab_s, float* d1_s, float* d2_s) {
+  const int tid = threadIdx.x, tp = tid & 15, tc = tid >> 4;
+  float bd[4], sd[4];
+  int bj[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) { bd[a] = FLT_MAX; sd[a] = FLT_MAX; bj[a] = 0x7fffffff; }
+  for (int j0 = 0; j0 < k2; j0 += kTileC) {
+    float acc[4][4];
+    km_tile_block<COHERENT>(X, ldx, N, d, centres, ldc, k2, p0, j0, sm, acc);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = j0 + tc + 16 * b;
+      if (j >= k2) continue;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const float v = acc[a][b];
+        if (v < bd[a] || (v == bd[a] && j < bj[a])) {
+          sd[a] = bd[a];
+          bd[a] = v;
+          bj[a] = j;
+        } else {
+          sd[a] = fminf(sd[a], v);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    sm.sb_d[tc][tp + 16 * a] = bd[a];
+    sm.sb_j[tc][tp + 16 * a] = bj[a];
+    sm.ss_d[tc][tp + 16 * a] = sd[a];
+  }
+  __syncthreads();
+  if (tid < kTileP) {
+    float B = sm.sb_d[0][tid], S = sm.ss_d[0][tid];
+    int Bj = sm.sb_j[0][tid];
+    for (int t = 1; t < 16; ++t) {
+      const float b2 = sm.sb_d[t][tid], s2 = sm.ss_d[t][tid];
+      const int j2 = sm.sb_j[t][tid];
+      if (b2 < B || (b2 == B && j2 < Bj)) {
+        S = fminf(fminf(S, s2), B);
+        B = b2;
+        Bj = j2;
+      } else {
+        S = fminf(fminf(S, s2), b2);
+      }
+    }
+    lab_s[tid] = Bj;
+    d1_s[tid] = B;
+    d2_s[tid] = S;
+  }
+  __syncthreads();
+}
+
+// D[j, p] for the 64 points starting at p0 and every centre.
+__device__ __forceinline__ void km_tile_distmat(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
+                                                const float* __restrict__ centres, int64_t ldc, int k2, int64_t p0,
+                                                KmTileSmem& sm, float* __restrict__ D, int64_t ldd) {
+  const int tid = threadIdx.x, tp = tid & 15, tc = tid >> 4;
+  for (int j0 = 0; j0 < k2; j0 += kTileC) {
+    float acc[4][4];
+    km_tile_block<false>(X, ldx, N, d, centres, ldc, k2, p0, j0, sm, acc);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = j0 + tc + 16 * b;
+      if (j >= k2) continue;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int64_t p = p0 + tp + 16 * a;
+        if (p < N) D[(int64_t)j * ldd + p] = acc[a][b];
+      }
+    }
+  }
+}
+
+}  // namespace cabsk

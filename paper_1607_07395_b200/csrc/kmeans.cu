@@ -12,11 +12,10 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "km_tile.cuh"
 
 namespace cabsk {
 
-constexpr int kTileP = 64, kTileC = 64, kTileD = 16;
-constexpr float kNearTie = 1e-5f;
 
 // ---------------------------------------------------------------- weights
 __global__ void __launch_bounds__(256) km_weights_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
@@ -79,121 +78,33 @@ void launch_km_init(const float* X, int64_t ldx, int64_t n_loc, int64_t row_off,
 // ---------------------------------------------------------------- assign / distance matrix
 // Tile: 64 points x 64 centres; thread (tp = tid & 15, tc = tid >> 4) owns points
 // tp + 16a and centres tc + 16b (a, b = 0..3).  Dimensions are staged 16 at a time;
-// every distance is accumulated over i = 0..d-1 in ascending order.
+// every distance is accumulated over i = 0..d-1 in ascending order (km_tile.cuh).
 template <bool DISTMAT>
 __global__ void __launch_bounds__(256) km_assign_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
                                                         const float* __restrict__ centres, int64_t ldc, int k2,
                                                         const float* __restrict__ w, int* __restrict__ labels,
                                                         double* __restrict__ pobj, int* __restrict__ ptie,
                                                         float* __restrict__ D, int64_t ldd) {
-  __shared__ float Xs[kTileD][kTileP + 4];
-  __shared__ float Cs[kTileD][kTileC + 4];
-  __shared__ float sb_d[16][kTileP + 1];
-  __shared__ int sb_j[16][kTileP + 1];
-  __shared__ float ss_d[16][kTileP + 1];
+  __shared__ KmTileSmem sm;
+  __shared__ int lab_s[kTileP];
+  __shared__ float d1_s[kTileP], d2_s[kTileP];
   __shared__ double s_red[8];
   __shared__ int s_tie[8];
-  const int tid = threadIdx.x, tp = tid & 15, tc = tid >> 4;
+  const int tid = threadIdx.x;
   const int64_t ntiles = ceil_div(N, kTileP);
   double obj = 0.0;
   int ties = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t p0 = tile * kTileP;
-    float bd[4], sd[4];
-    int bj[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) { bd[a] = FLT_MAX; sd[a] = FLT_MAX; bj[a] = 0x7fffffff; }
-    for (int j0 = 0; j0 < k2; j0 += kTileC) {
-      float acc[4][4] = {};
-      for (int i0 = 0; i0 < d; i0 += kTileD) {
-        {
-          const int pp = tid >> 2, ii = (tid & 3) * 4;
-          const int64_t p = p0 + pp;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int i = i0 + ii + q;
-            Xs[ii + q][pp] = (p < N && i < d) ? __ldg(X + p * ldx + i) : 0.f;
-          }
-          const int j = j0 + pp;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int i = i0 + ii + q;
-            Cs[ii + q][pp] = (j < k2 && i < d) ? __ldg(centres + (int64_t)j * ldc + i) : 0.f;
-          }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int ii = 0; ii < kTileD; ++ii) {
-          float x[4], c[4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) x[a] = Xs[ii][tp + 16 * a];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) c[b] = Cs[ii][tc + 16 * b];
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const float df = x[a] - c[b];
-              acc[a][b] = fmaf(df, df, acc[a][b]);
-            }
-        }
-        __syncthreads();
-      }
-      if (DISTMAT) {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int j = j0 + tc + 16 * b;
-          if (j >= k2) continue;
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const int64_t p = p0 + tp + 16 * a;
-            if (p < N) D[(int64_t)j * ldd + p] = acc[a][b];
-          }
-        }
-      } else {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int j = j0 + tc + 16 * b;
-          if (j >= k2) continue;
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const float v = acc[a][b];
-            if (v < bd[a] || (v == bd[a] && j < bj[a])) {
-              sd[a] = bd[a];
-              bd[a] = v;
-              bj[a] = j;
-            } else {
-              sd[a] = fminf(sd[a], v);
-            }
-          }
-        }
-      }
-    }
-    if (!DISTMAT) {
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        sb_d[tc][tp + 16 * a] = bd[a];
-        sb_j[tc][tp + 16 * a] = bj[a];
-        ss_d[tc][tp + 16 * a] = sd[a];
-      }
-      __syncthreads();
+    if (DISTMAT) {
+      km_tile_distmat(X, ldx, N, d, centres, ldc, k2, p0, sm, D, ldd);
+    } else {
+      km_tile_argmin<false>(X, ldx, N, d, centres, ldc, k2, p0, sm, lab_s, d1_s, d2_s);
       if (tid < kTileP) {
         const int64_t p = p0 + tid;
-        float B = sb_d[0][tid], S = ss_d[0][tid];
-        int Bj = sb_j[0][tid];
-        for (int t = 1; t < 16; ++t) {
-          const float b2 = sb_d[t][tid], s2 = ss_d[t][tid];
-          const int j2 = sb_j[t][tid];
-          if (b2 < B || (b2 == B && j2 < Bj)) {
-            S = fminf(fminf(S, s2), B);
-            B = b2;
-            Bj = j2;
-          } else {
-            S = fminf(fminf(S, s2), b2);
-          }
-        }
         if (p < N) {
-          labels[p] = Bj;
+          const float B = d1_s[tid], S = d2_s[tid];
+          labels[p] = lab_s[tid];
           obj += static_cast<double>(w[p]) * static_cast<double>(B);
           ties += (S - B) < kNearTie * S;
         }
@@ -315,36 +226,37 @@ void launch_km_accum(const float* X, int64_t ldx, int64_t N, int d, const int* l
 }
 
 // ---------------------------------------------------------------- reduce
-// red = [k2*d sums | k2 weights | objective | near ties], each a fixed-order FP64 sum over CTAs.
+// red = [k2*d sums | k2 weights | objective | near ties], each a fixed-order FP64 sum over
+// CTAs: 8 lanes per element (lane l sums CTAs l, l+8, ...), xor-butterfly combine.
 __global__ void km_reduce_kernel(const float* __restrict__ psum, const double* __restrict__ pw, int G, int k2, int d,
                                  int64_t ldps, const double* __restrict__ pobj, const int* __restrict__ ptie, int Gobj,
                                  double* __restrict__ red) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t e = gt >> 3;
+  const int sub = static_cast<int>(gt & 7);
+  const unsigned gmask = 0xffu << (threadIdx.x & 24);
   const int64_t nsum = (int64_t)k2 * d;
+  if (e >= nsum + k2 + 2) return;  // whole 8-lane groups exit together
+  double s = 0.0;
   if (e < nsum) {
     const int j = static_cast<int>(e / d), i = static_cast<int>(e % d);
-    double s = 0.0;
-    for (int b = 0; b < G; ++b) s += static_cast<double>(psum[((int64_t)b * k2 + j) * ldps + i]);
-    red[e] = s;
+    for (int b = sub; b < G; b += 8) s += static_cast<double>(psum[((int64_t)b * k2 + j) * ldps + i]);
   } else if (e < nsum + k2) {
     const int j = static_cast<int>(e - nsum);
-    double s = 0.0;
-    for (int b = 0; b < G; ++b) s += pw[(int64_t)b * k2 + j];
-    red[e] = s;
+    for (int b = sub; b < G; b += 8) s += pw[(int64_t)b * k2 + j];
   } else if (e == nsum + k2) {
-    double s = 0.0;
-    for (int b = 0; b < Gobj; ++b) s += pobj[b];
-    red[e] = s;
-  } else if (e == nsum + k2 + 1) {
-    long long t = 0;
-    for (int b = 0; b < Gobj; ++b) t += ptie[b];
-    red[e] = static_cast<double>(t);
+    for (int b = sub; b < Gobj; b += 8) s += pobj[b];
+  } else {
+    for (int b = sub; b < Gobj; b += 8) s += static_cast<double>(ptie[b]);
   }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) s += __shfl_xor_sync(gmask, s, o);
+  if (sub == 0) red[e] = s;
 }
 
 void launch_km_reduce(const float* psum, const double* pw, int G, int k2, int d, int64_t ldps, const double* pobj,
                       const int* ptie, int Gobj, double* red, cudaStream_t st) {
-  const int64_t total = (int64_t)k2 * d + k2 + 2;
+  const int64_t total = 8 * ((int64_t)k2 * d + k2 + 2);
   note_launch();
   km_reduce_kernel<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, st>>>(psum, pw, G, k2, d, ldps, pobj, ptie,
                                                                                  Gobj, red);

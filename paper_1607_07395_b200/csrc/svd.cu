@@ -46,6 +46,7 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
 
   const int np = (k + 1) & ~1;  // even number of players (dummy = k when k is odd)
   const double tol_rot = 2.0 * sqrt(static_cast<double>(k)) * DBL_EPSILON;
+  const double tol_rot2 = tol_rot * tol_rot;
   int sweep = 0;
   if (k > 1) {
     for (; sweep < kSvdMaxSweeps; ++sweep) {
@@ -68,12 +69,18 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
           al = warp_sum_d(al);
           be = warp_sum_d(be);
           ga = warp_sum_d(ga);
-          if (ga != 0.0 && fabs(ga) > tol_rot * sqrt(al) * sqrt(be)) {
-            double zeta = (be - al) / (2.0 * ga);
-            double t;
-            if (fabs(zeta) > 1e150) t = 0.5 / zeta;
-            else t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          if (ga != 0.0 && ga * ga > tol_rot2 * al * be) {
+            // t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2 ga), evaluated in FP32 on
+            // power-of-two-scaled operands: t's accuracy only sets the convergence rate.  c = 1/sqrt(1+t^2)
+            // in FP64 and s = c t make the rotation orthogonal to FP64 rounding whatever t is.
+            const double x = be - al, y = 2.0 * ga;
+            int ex;
+            frexp(fmax(fabs(x), fabs(y)), &ex);
+            const float xf = static_cast<float>(ldexp(x, -ex)), yf = static_cast<float>(ldexp(y, -ex));
+            const float tf = copysignf(1.f, xf) * yf / (fabsf(xf) + sqrtf(fmaf(xf, xf, yf * yf)));
+            if (tf == 0.f) continue;
+            const double t = static_cast<double>(tf);
+            const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
             for (int i = lane; i < k; i += 32) {
               double x = ap[i], y = aq[i];
               ap[i] = c * x - s * y;
@@ -97,6 +104,7 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
       if (rot == 0) break;
     }
     if (sweep == kSvdMaxSweeps && tid == 0) set_status(ws, CABS_DEV_SVD_NOCONV);
+    if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;  // diagnostics: sweeps of the last SVD
   }
 
   // singular values = column norms

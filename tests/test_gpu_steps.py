@@ -343,3 +343,26 @@ def test_residual_exact_factorisation_is_small(dev):
     Gt = torch.zeros((n, 32), device=dev); Gt[:, :k] = torch.from_numpy(G).to(dev)
     C.cabs_residual(plan, torch.from_numpy(A).to(dev), Ft, None, Gt, k, out, ws)
     assert out[0].item() == 0.0 and out[1].item() == float(np.sum(A.astype(np.float64) ** 2))
+
+
+def test_kmeans_persistent_and_loop_paths_agree(dev, monkeypatch):
+    """The single-GPU persistent Lloyd kernel and the per-iteration kernels (multi-GPU path)
+    compute the same thing; only the CTA partition of the FP32 partial sums differs."""
+    N, d, k2, iters = 20000, 50, 50, 8
+    X = _clustered(N, d, 30, 11)
+    ld = C.cabs_padded_ld(d)
+    Xt = torch.zeros((N, ld), device=dev); Xt[:, :d] = torch.from_numpy(X).to(dev)
+    plan = _plan(N, N, max(d, k2))
+    ws = _ws(plan, dev)
+    outs = []
+    for path in ("persistent", "loop"):
+        monkeypatch.setenv("CABS_KMEANS_PATH", path)
+        cen = torch.zeros((k2, ld), device=dev)
+        lab = torch.zeros(N, dtype=torch.int32, device=dev)
+        cw = torch.zeros(k2, dtype=torch.float64, device=dev)
+        obj = torch.zeros(iters, dtype=torch.float64, device=dev)
+        C.cabs_kmeans(plan, Xt, N, N, 0, d, k2, iters, C.WEIGHT_CONST, 2.0, 1, 3, cen, lab, cw, obj, ws)
+        outs.append((cen.cpu().numpy(), lab.cpu().numpy(), cw.cpu().numpy(), obj.cpu().numpy()))
+    (c1, l1, w1, o1), (c2, l2, w2, o2) = outs
+    assert np.array_equal(l1, l2) and np.array_equal(w1, w2)
+    assert rel_fro(c1, c2) < 1e-6 and np.allclose(o1, o2, rtol=1e-6)
