@@ -343,7 +343,16 @@ int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float
   if (!src || !src->a || src->lda < p.n || !F || !G || !out || ncomp < 0 || ldf < ncomp || ldg < ncomp)
     return arg_error("residual: bad arguments");
   const int64_t m_loc = p.row_end - p.row_begin;
-  launch_residual(src->a, src->lda, m_loc, p.n, F, ldf, s, G, ldg, ncomp, wsp<double>(ws, L.res_part), out, S(stream));
+  if (residual_tc_supported(src->a, src->lda, m_loc, p.n, ncomp)) {
+    if (launch_residual_tc(src->a, src->lda, m_loc, p.n, F, ldf, s, G, ldg, ncomp, wsp<float>(ws, L.res_split),
+                           wsp<double>(ws, L.res_part), out, S(stream)) != 0) {
+      cabs_set_error_msg("residual: tensor map encoding failed");
+      return CABS_ERR_CUDA;
+    }
+  } else {
+    launch_residual(src->a, src->lda, m_loc, p.n, F, ldf, s, G, ldg, ncomp, wsp<double>(ws, L.res_part), out,
+                    S(stream));
+  }
   CABS_LAUNCH_CHECK("residual");
   CABS_TRY(comm_f64(comm, out, 2, stream));
   return CABS_OK;

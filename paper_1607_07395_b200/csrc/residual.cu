@@ -106,6 +106,11 @@ __global__ void __launch_bounds__(256) residual_final_kernel(const double* __res
   if (threadIdx.x == 0) { out[0] = s0[0]; out[1] = s1[0]; }
 }
 
+void launch_residual_final(const double* part, int G, double* out, cudaStream_t st) {
+  note_launch();
+  residual_final_kernel<<<1, 256, 0, st>>>(part, G, out);
+}
+
 int launch_residual(const float* A, int64_t lda, int64_t m_loc, int64_t n, const float* F, int64_t ldf, const float* s,
                     const float* G, int64_t ldg, int ncomp, double* part, double* out, cudaStream_t st) {
   const int64_t ntiles = ceil_div(m_loc, kRBM) * ceil_div(n, kRBN);
@@ -117,8 +122,7 @@ int launch_residual(const float* A, int64_t lda, int64_t m_loc, int64_t n, const
   } else {
     cudaMemsetAsync(part, 0, sizeof(double) * 2 * g, st);
   }
-  note_launch();
-  residual_final_kernel<<<1, 256, 0, st>>>(part, static_cast<int>(g), out);
+  launch_residual_final(part, static_cast<int>(g), out, st);
   return 0;
 }
 

@@ -1,0 +1,66 @@
+"""Quick GPU probes (timings + diagnostics) for development; not part of the product path."""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_1607_07395_b200 import cabs as C  # noqa: E402
+from paper_1607_07395_b200.dist import make_plan  # noqa: E402
+
+
+def probe_svd(k=50, reps=5):
+    dev = torch.device("cuda:0")
+    plan = make_plan(1000, 1000, k)
+    ws = torch.zeros(C.cabs_workspace_bytes(plan), dtype=torch.uint8, device=dev)
+    g = np.random.default_rng(0)
+    W = torch.from_numpy(g.standard_normal((k, k)).astype(np.float32)).to(dev)
+    sig = torch.zeros(k, dtype=torch.float64, device=dev)
+    U = torch.zeros((k, k), dtype=torch.float64, device=dev)
+    V = torch.zeros_like(U)
+    r = torch.zeros(1, dtype=torch.int32, device=dev)
+    C.cabs_svd(plan, k, W, 1e-12, sig, U, V, r, ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        C.cabs_svd(plan, k, W, 1e-12, sig, U, V, r, ws)
+    e1.record()
+    torch.cuda.synchronize()
+    sweeps = int(ws[32:36].view(torch.int32).item())
+    print(f"svd k={k}: {e0.elapsed_time(e1) / reps * 1e3:.1f} us/call, sweeps={sweeps}, r={int(r.item())}")
+
+
+def probe_residual(m=20000, n=10000, k=50, reps=5):
+    dev = torch.device("cuda:0")
+    plan = make_plan(m, n, k)
+    ws = torch.zeros(C.cabs_workspace_bytes(plan), dtype=torch.uint8, device=dev)
+    A = torch.randn(m, n, device=dev)
+    ld = C.cabs_padded_ld(k)
+    F = torch.zeros(m, ld, device=dev); F[:, :k] = torch.randn(m, k, device=dev) * 0.1
+    G = torch.zeros(n, ld, device=dev); G[:, :k] = torch.randn(n, k, device=dev) * 0.1
+    s = torch.rand(k, device=dev) + 0.5
+    out = torch.zeros(2, dtype=torch.float64, device=dev)
+    C.cabs_residual(plan, A, F, s, G, k, out, ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        C.cabs_residual(plan, A, F, s, G, k, out, ws)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ref_r = ((A.double() - (F[:, :k].double() * s.double()) @ G[:, :k].double().T) ** 2).sum().item()
+    print(f"residual {m}x{n} k={k}: {ms * 1e3:.1f} us, {4 * m * n / ms / 1e6:.0f} GB/s, "
+          f"rel diff {abs(out[0].item() - ref_r) / ref_r:.2e}, a2 rel {abs(out[1].item() - (A.double()**2).sum().item()) / out[1].item():.1e}")
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("svd", "all"):
+        for k in (20, 50, 100, 200):
+            probe_svd(k)
+    if what in ("residual", "all"):
+        for (m, n, k) in ((20000, 10000, 50), (2000, 1500, 20), (20000, 10000, 64), (4097, 3001, 33)):
+            probe_residual(m, n, k)
