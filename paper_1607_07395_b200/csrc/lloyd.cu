@@ -7,6 +7,7 @@
 // range in index order, fixed-order FP64 cross-CTA reduction, empty clusters keep
 // their centre (Z12).  Eq. 6, c iterations.
 #include <cooperative_groups.h>
+#include <float.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -36,27 +37,59 @@ struct LloydArgs {
 };
 
 constexpr int kLloydThreads = 256;
+constexpr int kXt = kTileP + 1;  // row pitch of the transposed point tile (conflict-free both ways)
+
+// Dynamic shared memory layout (floats unless noted):
+//   cs   [round_up(k2,64)][d+1]   centres of this iteration
+//   xt   [d][65]                  the current 64-point tile, transposed
+//   acc  [groups][k2][d]          per-group partial sums
+//   wacc [groups][k2] (double)    per-group partial weights
+//   ws_  [64]                     weights of the tile's points
+struct LloydSmem {
+  size_t cs, xt, acc, wacc, wts, total;
+};
+__host__ __device__ inline LloydSmem lloyd_smem(int d, int k2, int groups) {
+  LloydSmem L;
+  size_t o = 0;
+  auto take = [&](size_t b) { size_t r = o; o += (b + 15) & ~size_t(15); return r; };
+  L.cs = take(sizeof(float) * round_up(k2, 64) * (d + 1));
+  L.xt = take(sizeof(float) * (size_t)d * kXt);
+  L.acc = take(sizeof(float) * (size_t)groups * k2 * d);
+  L.wacc = take(sizeof(double) * (size_t)groups * k2);
+  L.wts = take(sizeof(float) * kTileP);
+  L.total = o;
+  return L;
+}
 
 __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ KmTileSmem sm;
+  __shared__ float sb_d[16][kTileP + 1];
+  __shared__ int sb_j[16][kTileP + 1];
+  __shared__ float ss_d[16][kTileP + 1];
   __shared__ int lab_s[kTileP];
-  __shared__ float d1_s[kTileP], d2_s[kTileP];
   __shared__ double s_red[8];
   __shared__ int s_tie[8];
   cg::grid_group grid = cg::this_grid();
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, tp = tid & 15, tc = tid >> 4;
   const int G = gridDim.x, b = blockIdx.x;
-  const int k2 = a.k2, d = a.d;
-  float* acc = reinterpret_cast<float*>(dyn);                                      // [groups][k2][d]
-  const size_t wacc_off = (sizeof(float) * (size_t)a.groups * k2 * d + 15) & ~size_t(15);
-  double* wacc = reinterpret_cast<double*>(dyn + wacc_off);  // [groups][k2]
+  const int k2 = a.k2, d = a.d, cst = d + 1;
+  const LloydSmem L = lloyd_smem(d, k2, a.groups);
+  float* cs = reinterpret_cast<float*>(dyn + L.cs);
+  float* xt = reinterpret_cast<float*>(dyn + L.xt);
+  float* acc = reinterpret_cast<float*>(dyn + L.acc);
+  double* wacc = reinterpret_cast<double*>(dyn + L.wacc);
+  float* wts = reinterpret_cast<float*>(dyn + L.wts);
   const int grp = tid / a.dgroup, gi = tid % a.dgroup;  // accumulation group / dimension
+  const int k2p = static_cast<int>(round_up(k2, 64));
   const int64_t ntiles = ceil_div(a.N, kTileP);
   const int64_t t_beg = (ntiles * b) / G, t_end = (ntiles * (b + 1)) / G;  // contiguous tiles
 
   for (int it = 0; it < a.iters; ++it) {
     // ---------------- phase A: assign + per-CTA partial sums
+    for (int e = tid; e < k2p * d; e += blockDim.x) {
+      const int j = e / d, i = e - j * d;
+      cs[j * cst + i] = j < k2 ? __ldcg(a.centres + (int64_t)j * a.ldc + i) : 0.f;
+    }
     for (int e = tid; e < a.groups * k2 * d; e += blockDim.x) acc[e] = 0.f;
     for (int e = tid; e < a.groups * k2; e += blockDim.x) wacc[e] = 0.0;
     double obj = 0.0;
@@ -64,27 +97,83 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
     __syncthreads();
     for (int64_t tile = t_beg; tile < t_end; ++tile) {
       const int64_t p0 = tile * kTileP;
-      km_tile_argmin<true>(a.X, a.ldx, a.N, d, a.centres, a.ldc, k2, p0, sm, lab_s, d1_s, d2_s);
-      if (tid < kTileP) {
-        const int64_t p = p0 + tid;
-        if (p < a.N) {
-          const float B = d1_s[tid], S = d2_s[tid];
-          a.labels[p] = lab_s[tid];
-          obj += static_cast<double>(a.w[p]) * static_cast<double>(B);
-          ties += (S - B) < kNearTie * S;
+      // stage the tile transposed: xt[i][pp] (coalesced global reads along i)
+      for (int e = tid; e < kTileP * d; e += blockDim.x) {
+        const int pp = e / d, i = e - pp * d;
+        const int64_t p = p0 + pp;
+        xt[i * kXt + pp] = p < a.N ? __ldg(a.X + p * a.ldx + i) : 0.f;
+      }
+      if (tid < kTileP) wts[tid] = (p0 + tid < a.N) ? a.w[p0 + tid] : 0.f;
+      __syncthreads();
+      // distances (direct differences, ascending i -- identical arithmetic to km_tile.cuh)
+      float bd[4], sd[4];
+      int bj[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { bd[q] = FLT_MAX; sd[q] = FLT_MAX; bj[q] = 0x7fffffff; }
+      for (int j0 = 0; j0 < k2; j0 += kTileC) {
+        float accd[4][4] = {};
+        const float* c0 = cs + (j0 + tc) * cst;
+        for (int i = 0; i < d; ++i) {
+          float x[4], c[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = xt[i * kXt + tp + 16 * q];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) c[q] = c0[16 * q * cst + i];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const float df = x[u] - c[v];
+              accd[u][v] = fmaf(df, df, accd[u][v]);
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int j = j0 + tc + 16 * v;
+          if (j >= k2) continue;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float val = accd[u][v];
+            if (val < bd[u] || (val == bd[u] && j < bj[u])) { sd[u] = bd[u]; bd[u] = val; bj[u] = j; }
+            else sd[u] = fminf(sd[u], val);
+          }
         }
       }
-      // group grp accumulates points [grp*per, (grp+1)*per) of the tile, in index order;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        sb_d[tc][tp + 16 * u] = bd[u];
+        sb_j[tc][tp + 16 * u] = bj[u];
+        ss_d[tc][tp + 16 * u] = sd[u];
+      }
+      __syncthreads();
+      if (tid < kTileP) {
+        float B = sb_d[0][tid], Sd = ss_d[0][tid];
+        int Bj = sb_j[0][tid];
+        for (int t = 1; t < 16; ++t) {
+          const float b2 = sb_d[t][tid], s2 = ss_d[t][tid];
+          const int j2 = sb_j[t][tid];
+          if (b2 < B || (b2 == B && j2 < Bj)) { Sd = fminf(fminf(Sd, s2), B); B = b2; Bj = j2; }
+          else Sd = fminf(fminf(Sd, s2), b2);
+        }
+        lab_s[tid] = Bj;
+        const int64_t p = p0 + tid;
+        if (p < a.N) {
+          a.labels[p] = Bj;
+          obj += static_cast<double>(wts[tid]) * static_cast<double>(B);
+          ties += (Sd - B) < kNearTie * Sd;
+        }
+      }
+      __syncthreads();
+      // group grp accumulates points [grp*per, (grp+1)*per) of the tile in index order;
       // thread gi owns dimension gi (and gi + dgroup, ... when d > dgroup)
       const int per = kTileP / a.groups;
       float* ag = acc + (size_t)grp * k2 * d;
       double* wg = wacc + (size_t)grp * k2;
       for (int pp = grp * per; pp < (grp + 1) * per; ++pp) {
-        const int64_t p = p0 + pp;
-        if (p >= a.N) break;
+        if (p0 + pp >= a.N) break;
         const int j = lab_s[pp];
-        const float wl = a.w[p];
-        for (int i = gi; i < d; i += a.dgroup) ag[j * d + i] = fmaf(wl, __ldg(a.X + p * a.ldx + i), ag[j * d + i]);
+        const float wl = wts[pp];
+        for (int i = gi; i < d; i += a.dgroup) ag[j * d + i] = fmaf(wl, xt[i * kXt + pp], ag[j * d + i]);
         if (gi == 0) wg[j] += static_cast<double>(wl);
       }
       __syncthreads();
@@ -168,7 +257,7 @@ bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int 
   if (N <= 0) return false;
   const int dgroup = static_cast<int>(round_up(d < 256 ? d : 256, 32));
   const int groups = kLloydThreads / dgroup;
-  const size_t smem = (sizeof(float) * (size_t)groups * k2 * d + 15 & ~size_t(15)) + sizeof(double) * groups * k2;
+  const size_t smem = lloyd_smem(d, k2, groups).total;
   if (smem > 160 * 1024) return false;
   static int attr_smem = -1;
   if (attr_smem < 0) {

@@ -21,6 +21,87 @@ __device__ __forceinline__ int rr_player(int j, int r, int np) {
   return j == 0 ? 0 : 1 + ((j - 1 + r) % (np - 1));
 }
 
+
+// Cyclic one-sided Jacobi sweeps until no pair needs a rotation (or the sweep cap).
+// Warp-uniform control flow: every lane of a warp runs the same pair, holding its
+// L elements of each column in registers (rows lane + 32 l), so the three dot
+// products are butterfly shuffles with no divergence.
+template <int L>
+__device__ int jacobi_sweeps(double* A, double* V, int k, int* s_rot) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int np = (k + 1) & ~1;  // even number of players (dummy = k when k is odd)
+  const double tol_rot = 2.0 * sqrt(static_cast<double>(k)) * DBL_EPSILON;
+  const double tol_rot2 = tol_rot * tol_rot;
+  int sweep = 0;
+  for (; sweep < kSvdMaxSweeps; ++sweep) {
+    if (tid == 0) *s_rot = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < np - 1; ++rnd) {
+      for (int pr = warp; pr < np / 2; pr += nwarps) {
+        int p = rr_player(pr, rnd, np), q = rr_player(np - 1 - pr, rnd, np);
+        if (p > q) { const int t = p; p = q; q = t; }
+        const bool real = q < k;  // warp-uniform: false for the dummy player's pair
+        const int pp = real ? p : 0, qq = real ? q : 0;
+        double* ap = A + (size_t)pp * k;
+        double* aq = A + (size_t)qq * k;
+        double x[L], y[L];
+        double al = 0, be = 0, ga = 0;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          const int i = lane + 32 * l;
+          const bool in = real && i < k;
+          x[l] = in ? ap[i] : 0.0;
+          y[l] = in ? aq[i] : 0.0;
+          al = fma(x[l], x[l], al);
+          be = fma(y[l], y[l], be);
+          ga = fma(x[l], y[l], ga);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        // t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2 ga), evaluated in FP32 on
+        // power-of-two-scaled operands: t's accuracy only sets the convergence rate.  c = 1/sqrt(1+t^2)
+        // in FP64 and s = c t make the rotation orthogonal to FP64 rounding whatever t is.
+        float tf = 0.f;
+        if (ga != 0.0 && ga * ga > tol_rot2 * al * be) {
+          const double dx = be - al, dy = 2.0 * ga;
+          int ex;
+          frexp(fmax(fabs(dx), fabs(dy)), &ex);
+          const float xf = static_cast<float>(ldexp(dx, -ex)), yf = static_cast<float>(ldexp(dy, -ex));
+          tf = copysignf(1.f, xf) * yf / (fabsf(xf) + sqrtf(fmaf(xf, xf, yf * yf)));
+        }
+        if (tf != 0.f) {  // warp-uniform (all lanes hold identical sums)
+          const double t = static_cast<double>(tf);
+          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+          double* vp = V + (size_t)p * k;
+          double* vq = V + (size_t)q * k;
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            const int i = lane + 32 * l;
+            if (i < k) {
+              ap[i] = c * x[l] - sn * y[l];
+              aq[i] = sn * x[l] + c * y[l];
+              const double u = vp[i], v = vq[i];
+              vp[i] = c * u - sn * v;
+              vq[i] = sn * u + c * v;
+            }
+          }
+          if (lane == 0) atomicAdd(s_rot, 1);
+        }
+      }
+      __syncthreads();
+    }
+    const int rot = *s_rot;
+    __syncthreads();
+    if (rot == 0) break;
+  }
+  return sweep;
+}
+
+template <int L>
 __global__ void __launch_bounds__(kSvdThreads, 1)
 svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, double* gA, double* gV,
                   double* __restrict__ sigma_out, double* __restrict__ Uw64, double* __restrict__ Vw64,
@@ -35,8 +116,8 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
 
   // load: A[c*k + i] = W[i, c] (column-major), V = I
-  for (int64_t e = tid; e < (int64_t)k * k; e += blockDim.x) {
-    int c = static_cast<int>(e / k), i = static_cast<int>(e % k);
+  for (int e = tid; e < k * k; e += blockDim.x) {
+    const int c = e / k, i = e - c * k;
     float w = W[(int64_t)i * ldw + c];
     if (!isfinite(w)) set_status(ws, CABS_DEV_NONFINITE);
     A[e] = static_cast<double>(w);
@@ -44,65 +125,9 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
   }
   __syncthreads();
 
-  const int np = (k + 1) & ~1;  // even number of players (dummy = k when k is odd)
-  const double tol_rot = 2.0 * sqrt(static_cast<double>(k)) * DBL_EPSILON;
-  const double tol_rot2 = tol_rot * tol_rot;
   int sweep = 0;
   if (k > 1) {
-    for (; sweep < kSvdMaxSweeps; ++sweep) {
-      if (tid == 0) s_rot = 0;
-      __syncthreads();
-      for (int rnd = 0; rnd < np - 1; ++rnd) {
-        for (int pr = warp; pr < np / 2; pr += nwarps) {
-          int p = rr_player(pr, rnd, np), q = rr_player(np - 1 - pr, rnd, np);
-          if (p > q) { int t = p; p = q; q = t; }
-          if (q >= k) continue;  // dummy player
-          double* ap = A + (size_t)p * k;
-          double* aq = A + (size_t)q * k;
-          double al = 0, be = 0, ga = 0;
-          for (int i = lane; i < k; i += 32) {
-            double x = ap[i], y = aq[i];
-            al = fma(x, x, al);
-            be = fma(y, y, be);
-            ga = fma(x, y, ga);
-          }
-          al = warp_sum_d(al);
-          be = warp_sum_d(be);
-          ga = warp_sum_d(ga);
-          if (ga != 0.0 && ga * ga > tol_rot2 * al * be) {
-            // t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2 ga), evaluated in FP32 on
-            // power-of-two-scaled operands: t's accuracy only sets the convergence rate.  c = 1/sqrt(1+t^2)
-            // in FP64 and s = c t make the rotation orthogonal to FP64 rounding whatever t is.
-            const double x = be - al, y = 2.0 * ga;
-            int ex;
-            frexp(fmax(fabs(x), fabs(y)), &ex);
-            const float xf = static_cast<float>(ldexp(x, -ex)), yf = static_cast<float>(ldexp(y, -ex));
-            const float tf = copysignf(1.f, xf) * yf / (fabsf(xf) + sqrtf(fmaf(xf, xf, yf * yf)));
-            if (tf == 0.f) continue;
-            const double t = static_cast<double>(tf);
-            const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
-            for (int i = lane; i < k; i += 32) {
-              double x = ap[i], y = aq[i];
-              ap[i] = c * x - s * y;
-              aq[i] = s * x + c * y;
-            }
-            double* vp = V + (size_t)p * k;
-            double* vq = V + (size_t)q * k;
-            for (int i = lane; i < k; i += 32) {
-              double x = vp[i], y = vq[i];
-              vp[i] = c * x - s * y;
-              vq[i] = s * x + c * y;
-            }
-            if (lane == 0) atomicAdd(&s_rot, 1);
-          }
-        }
-        __syncthreads();
-      }
-      __syncthreads();
-      int rot = s_rot;
-      __syncthreads();
-      if (rot == 0) break;
-    }
+    sweep = jacobi_sweeps<L>(A, V, k, &s_rot);
     if (sweep == kSvdMaxSweeps && tid == 0) set_status(ws, CABS_DEV_SVD_NOCONV);
     if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;  // diagnostics: sweeps of the last SVD
   }
@@ -184,17 +209,21 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
                double* Uw64, double* Vw64, int* r_user, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(svd_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSvdSmemK * kSvdSmemK * 8);
+    const int smax = 2 * kSvdSmemK * kSvdSmemK * 8;
+    cudaFuncSetAttribute(svd_jacobi_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    cudaFuncSetAttribute(svd_jacobi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    cudaFuncSetAttribute(svd_jacobi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
     attr_set = true;
   }
   const bool use_smem = k <= kSvdSmemK;
   size_t smem = use_smem ? 2 * (size_t)k * k * sizeof(double) : 0;
   double* sig = sigma_user ? sigma_user : wsp<double>(ws, L.sig64);
   int* r_ws = wsp<int>(ws, L.scal) + SCAL_R_TMP;
+  auto kern = k <= 32 ? svd_jacobi_kernel<1> : k <= 64 ? svd_jacobi_kernel<2> : k <= 128 ? svd_jacobi_kernel<4>
+            : k <= 256 ? svd_jacobi_kernel<8> : k <= 320 ? svd_jacobi_kernel<10> : svd_jacobi_kernel<32>;
   note_launch();
-  svd_jacobi_kernel<<<1, kSvdThreads, smem, st>>>(k, W, ldw, tol, wsp<double>(ws, L.a64), wsp<double>(ws, L.v64),
-                                                  sig, Uw64, Vw64, wsp<float>(ws, L.uw32), wsp<float>(ws, L.vw32),
-                                                  L.Kp, r_ws, r_user, use_smem, ws);
+  kern<<<1, kSvdThreads, smem, st>>>(k, W, ldw, tol, wsp<double>(ws, L.a64), wsp<double>(ws, L.v64), sig, Uw64, Vw64,
+                                     wsp<float>(ws, L.uw32), wsp<float>(ws, L.vw32), L.Kp, r_ws, r_user, use_smem, ws);
   if (sigma_user && sigma_user != wsp<double>(ws, L.sig64)) {
     cudaMemcpyAsync(wsp<double>(ws, L.sig64), sigma_user, sizeof(double) * k, cudaMemcpyDeviceToDevice, st);
   }

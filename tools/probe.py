@@ -64,3 +64,28 @@ if __name__ == "__main__":
     if what in ("residual", "all"):
         for (m, n, k) in ((20000, 10000, 50), (2000, 1500, 20), (20000, 10000, 64), (4097, 3001, 33)):
             probe_residual(m, n, k)
+
+
+def probe_kmeans(N=20000, d=50, k2=50, iters=20, reps=3):
+    dev = torch.device("cuda:0")
+    plan = make_plan(N, N, max(d, k2))
+    ws = torch.zeros(C.cabs_workspace_bytes(plan), dtype=torch.uint8, device=dev)
+    ld = C.cabs_padded_ld(d)
+    X = torch.zeros(N, ld, device=dev); X[:, :d] = torch.randn(N, d, device=dev)
+    cen = torch.zeros(k2, ld, device=dev); lab = torch.zeros(N, dtype=torch.int32, device=dev)
+    cw = torch.zeros(k2, dtype=torch.float64, device=dev); obj = torch.zeros(iters, dtype=torch.float64, device=dev)
+    C.cabs_kmeans(plan, X, N, N, 0, d, k2, iters, 0, 2.0, 0, 3, cen, lab, cw, obj, ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        C.cabs_kmeans(plan, X, N, N, 0, d, k2, iters, 0, 2.0, 0, 3, cen, lab, cw, obj, ws)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    print(f"kmeans N={N} d={d} k2={k2} iters={iters}: {ms * 1e3:.1f} us ({ms * 1e3 / iters:.1f} us/iter)")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] in ("kmeans", "all2"):
+    for cfg in ((20000, 50, 50), (10000, 50, 50), (100000, 100, 100), (2000, 20, 20)):
+        probe_kmeans(*cfg)
