@@ -23,13 +23,17 @@ __device__ __forceinline__ int rr_player(int j, int r, int np) {
 
 
 // Cyclic one-sided Jacobi sweeps until no pair needs a rotation (or the sweep cap).
-// Warp-uniform control flow: every lane of a warp runs the same pair, holding its
-// L elements of each column in registers (rows lane + 32 l), so the three dot
-// products are butterfly shuffles with no divergence.
-template <int L>
+// A group of LP lanes (LP | 32) runs one column pair, each lane holding E = ceil(k/LP)
+// elements of both columns in registers (rows g + LP e), so a warp advances 32/LP
+// pairs at once and the dot products are LP-lane butterflies.  One CTA issues every
+// instruction of a round, so fewer, fuller warps per round is what shortens it.
+template <int LP, int E>
 __device__ int jacobi_sweeps(double* A, double* V, int k, int* s_rot) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  constexpr int kGroups = 32 / LP;
+  const int grp = lane / LP, gl = lane % LP;
   const int np = (k + 1) & ~1;  // even number of players (dummy = k when k is odd)
+  const int npairs = np / 2;
   const double tol_rot = 2.0 * sqrt(static_cast<double>(k)) * DBL_EPSILON;
   const double tol_rot2 = tol_rot * tol_rot;
   int sweep = 0;
@@ -37,59 +41,69 @@ __device__ int jacobi_sweeps(double* A, double* V, int k, int* s_rot) {
     if (tid == 0) *s_rot = 0;
     __syncthreads();
     for (int rnd = 0; rnd < np - 1; ++rnd) {
-      for (int pr = warp; pr < np / 2; pr += nwarps) {
-        int p = rr_player(pr, rnd, np), q = rr_player(np - 1 - pr, rnd, np);
+      // warp-uniform trip count; the pair index differs per lane group
+      for (int base = warp * kGroups; base < npairs; base += nwarps * kGroups) {
+        const int pr = base + grp;
+        int p = rr_player(pr < npairs ? pr : 0, rnd, np), q = rr_player(np - 1 - (pr < npairs ? pr : 0), rnd, np);
         if (p > q) { const int t = p; p = q; q = t; }
-        const bool real = q < k;  // warp-uniform: false for the dummy player's pair
+        const bool real = pr < npairs && q < k;  // group-uniform
         const int pp = real ? p : 0, qq = real ? q : 0;
         double* ap = A + (size_t)pp * k;
         double* aq = A + (size_t)qq * k;
-        double x[L], y[L];
+        double x[E], y[E];
         double al = 0, be = 0, ga = 0;
 #pragma unroll
-        for (int l = 0; l < L; ++l) {
-          const int i = lane + 32 * l;
+        for (int e = 0; e < E; ++e) {
+          const int i = gl + LP * e;
           const bool in = real && i < k;
-          x[l] = in ? ap[i] : 0.0;
-          y[l] = in ? aq[i] : 0.0;
-          al = fma(x[l], x[l], al);
-          be = fma(y[l], y[l], be);
-          ga = fma(x[l], y[l], ga);
+          x[e] = in ? ap[i] : 0.0;
+          y[e] = in ? aq[i] : 0.0;
+          al = fma(x[e], x[e], al);
+          be = fma(y[e], y[e], be);
+          ga = fma(x[e], y[e], ga);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = LP / 2; o > 0; o >>= 1) {
           al += __shfl_xor_sync(0xffffffffu, al, o);
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        // t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2 ga), evaluated in FP32 on
-        // power-of-two-scaled operands: t's accuracy only sets the convergence rate.  c = 1/sqrt(1+t^2)
-        // in FP64 and s = c t make the rotation orthogonal to FP64 rounding whatever t is.
+        // t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2 ga), evaluated in FP32
+        // (scaled by a power of two when out of FP32 range): t's accuracy only sets the convergence
+        // rate.  c = 1/sqrt(1+t^2) in FP64 and s = c t keep the rotation orthogonal to FP64 rounding.
         float tf = 0.f;
         if (ga != 0.0 && ga * ga > tol_rot2 * al * be) {
           const double dx = be - al, dy = 2.0 * ga;
-          int ex;
-          frexp(fmax(fabs(dx), fabs(dy)), &ex);
-          const float xf = static_cast<float>(ldexp(dx, -ex)), yf = static_cast<float>(ldexp(dy, -ex));
-          tf = copysignf(1.f, xf) * yf / (fabsf(xf) + sqrtf(fmaf(xf, xf, yf * yf)));
+          const double mx = fmax(fabs(dx), fabs(dy));
+          float xf, yf;
+          if (mx > 1e-30 && mx < 1e30) {
+            xf = static_cast<float>(dx);
+            yf = static_cast<float>(dy);
+          } else {
+            int ex;
+            frexp(mx, &ex);
+            xf = static_cast<float>(ldexp(dx, -ex));
+            yf = static_cast<float>(ldexp(dy, -ex));
+          }
+          tf = copysignf(1.f, xf) * __fdividef(yf, fabsf(xf) + sqrtf(fmaf(xf, xf, yf * yf)));
         }
-        if (tf != 0.f) {  // warp-uniform (all lanes hold identical sums)
+        if (tf != 0.f) {  // group-uniform (all lanes of the group hold identical sums)
           const double t = static_cast<double>(tf);
           const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
           double* vp = V + (size_t)p * k;
           double* vq = V + (size_t)q * k;
 #pragma unroll
-          for (int l = 0; l < L; ++l) {
-            const int i = lane + 32 * l;
+          for (int e = 0; e < E; ++e) {
+            const int i = gl + LP * e;
             if (i < k) {
-              ap[i] = c * x[l] - sn * y[l];
-              aq[i] = sn * x[l] + c * y[l];
+              ap[i] = c * x[e] - sn * y[e];
+              aq[i] = sn * x[e] + c * y[e];
               const double u = vp[i], v = vq[i];
               vp[i] = c * u - sn * v;
               vq[i] = sn * u + c * v;
             }
           }
-          if (lane == 0) atomicAdd(s_rot, 1);
+          if (gl == 0) atomicAdd(s_rot, 1);
         }
       }
       __syncthreads();
@@ -127,7 +141,9 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
 
   int sweep = 0;
   if (k > 1) {
-    sweep = jacobi_sweeps<L>(A, V, k, &s_rot);
+    // L = ceil(k/32) class -> (lanes per pair, elements per lane): 8 elements per lane
+    // while k <= 256, so small k packs several pairs into each warp
+    sweep = jacobi_sweeps<(L <= 1 ? 4 : L == 2 ? 8 : L == 4 ? 16 : 32), (L <= 4 ? 8 : L)>(A, V, k, &s_rot);
     if (sweep == kSvdMaxSweeps && tid == 0) set_status(ws, CABS_DEV_SVD_NOCONV);
     if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;  // diagnostics: sweeps of the last SVD
   }
