@@ -17,8 +17,12 @@ constexpr int kSvdThreads = 1024;
 constexpr int kSvdMaxSweeps = 60;
 constexpr int kSvdSmemK = 112;
 
+// Circle-method tournament: player 0 fixed, the others rotate by one seat per round.
+// 0 <= j - 1 + r < 2 (np - 1), so the modulo is one conditional subtraction.
 __device__ __forceinline__ int rr_player(int j, int r, int np) {
-  return j == 0 ? 0 : 1 + ((j - 1 + r) % (np - 1));
+  int x = j - 1 + r;
+  if (x >= np - 1) x -= np - 1;
+  return j == 0 ? 0 : 1 + x;
 }
 
 
@@ -115,7 +119,7 @@ __device__ int jacobi_sweeps(double* A, double* V, int k, int* s_rot) {
   return sweep;
 }
 
-template <int L>
+template <int L, bool SMEM>
 __global__ void __launch_bounds__(kSvdThreads, 1)
 svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, double* gA, double* gV,
                   double* __restrict__ sigma_out, double* __restrict__ Uw64, double* __restrict__ Vw64,
@@ -125,8 +129,9 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
   __shared__ int s_rot;
   __shared__ double s_sig[CABS_KMAX];
   __shared__ int s_perm[CABS_KMAX];  // s_perm[rank] = column
-  double* A = use_smem ? smem_d : gA;
-  double* V = use_smem ? smem_d + (size_t)k * k : gV;
+  // SMEM is a compile-time choice so the columns are addressed as shared memory (LDS/STS)
+  double* A = SMEM ? smem_d : gA;
+  double* V = SMEM ? smem_d + (size_t)k * k : gV;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
 
   // load: A[c*k + i] = W[i, c] (column-major), V = I
@@ -226,17 +231,19 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
   static bool attr_set = false;
   if (!attr_set) {
     const int smax = 2 * kSvdSmemK * kSvdSmemK * 8;
-    cudaFuncSetAttribute(svd_jacobi_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-    cudaFuncSetAttribute(svd_jacobi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-    cudaFuncSetAttribute(svd_jacobi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    cudaFuncSetAttribute(svd_jacobi_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    cudaFuncSetAttribute(svd_jacobi_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    cudaFuncSetAttribute(svd_jacobi_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
     attr_set = true;
   }
   const bool use_smem = k <= kSvdSmemK;
   size_t smem = use_smem ? 2 * (size_t)k * k * sizeof(double) : 0;
   double* sig = sigma_user ? sigma_user : wsp<double>(ws, L.sig64);
   int* r_ws = wsp<int>(ws, L.scal) + SCAL_R_TMP;
-  auto kern = k <= 32 ? svd_jacobi_kernel<1> : k <= 64 ? svd_jacobi_kernel<2> : k <= 128 ? svd_jacobi_kernel<4>
-            : k <= 256 ? svd_jacobi_kernel<8> : k <= 320 ? svd_jacobi_kernel<10> : svd_jacobi_kernel<32>;
+  auto kern = k <= 32 ? svd_jacobi_kernel<1, true> : k <= 64 ? svd_jacobi_kernel<2, true>
+            : k <= kSvdSmemK ? svd_jacobi_kernel<4, true> : k <= 128 ? svd_jacobi_kernel<4, false>
+            : k <= 256 ? svd_jacobi_kernel<8, false> : k <= 320 ? svd_jacobi_kernel<10, false>
+                       : svd_jacobi_kernel<32, false>;
   note_launch();
   kern<<<1, kSvdThreads, smem, st>>>(k, W, ldw, tol, wsp<double>(ws, L.a64), wsp<double>(ws, L.v64), sig, Uw64, Vw64,
                                      wsp<float>(ws, L.uw32), wsp<float>(ws, L.vw32), L.Kp, r_ws, r_user, use_smem, ws);
