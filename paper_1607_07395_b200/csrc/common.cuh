@@ -109,6 +109,33 @@ __device__ __forceinline__ float warp_sum_f(float v) {
   return v;
 }
 
+// ---------------------------------------------------------------- grid barrier
+// Sense-reversing barrier for persistent kernels launched cooperatively (all CTAs
+// co-resident).  bar[0] = arrivals, bar[1] = generation; both zero before launch.
+// Release/acquire at GPU scope; data exchanged across CTAs must be read through L2
+// (ld.global.cg / atomics), since no L1 invalidation is performed.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+    if (atomicAdd(bar, 1u) == nb - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicExch(bar + 1, gen + 1);
+    } else {
+      while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(32);
+    }
+  }
+  ++gen;
+  __syncthreads();
+}
+
 // (d, idx) lexicographic "less"
 __device__ __forceinline__ bool lex_less(float da, int64_t ia, float db, int64_t ib) {
   return da < db || (da == db && ia < ib);

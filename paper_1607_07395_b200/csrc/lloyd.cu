@@ -41,7 +41,7 @@ struct LloydArgs {
   double* cluster_w;
   long long* fsum;  // [3][k2*d] fixed-point sums
   long long* fw;    // [3][k2]   fixed-point weights
-  unsigned* gmax;   // [2] bit patterns of max|x|, max w
+  unsigned* gmax;   // [4] bit patterns of max|x|, max w; grid barrier {arrivals, generation}
   double* pobj;     // [iters][G]
   int* ptie;        // [iters][G]
   int groups, dgroup, resident, tpc;
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
   __shared__ double s_red[8];
   __shared__ int s_tie[8];
   __shared__ float s_max[2][8];
-  cg::grid_group grid = cg::this_grid();
+  unsigned gen = 0;  // grid-barrier generation (a.gmax + 2 = {arrivals, generation})
   const int tid = threadIdx.x, tp = tid & 15, tc = tid >> 4, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x, b = blockIdx.x;
   const int k2 = a.k2, d = a.d, cst = d + 1;
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
       cs[j * cst + i] = j < k2 ? __ldcg(a.centres + (int64_t)j * a.ldc + i) : 0.f;
     }
   }
-  grid.sync();
+  grid_barrier(a.gmax + 2, gen);
   const double xmax = static_cast<double>(__uint_as_float(__ldcg(a.gmax)));
   const double wmax = static_cast<double>(__uint_as_float(__ldcg(a.gmax + 1)));
   const int S = scale_exp(static_cast<double>(a.N) * wmax * xmax);
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
       a.pobj[(size_t)it * G + b] = s;
       a.ptie[(size_t)it * G + b] = q;
     }
-    grid.sync();
+    grid_barrier(a.gmax + 2, gen);
   }
   // ---------------- epilogue (CTA 0): final centres, cluster weights, objective history
   if (b == 0) {
@@ -331,6 +331,7 @@ bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int 
   for (int per_sm = 2; per_sm >= 1 && G == 0; --per_sm) {
     int64_t g = (int64_t)nsm * per_sm;
     if (g > ntiles) g = ntiles;
+    g = ceil_div(ntiles, ceil_div(ntiles, g));  // balanced: every CTA gets the same tile count (+-1)
     const int t = static_cast<int>(ceil_div(ntiles, g));
     size_t s_res = lloyd_smem(d, k2, groups, t).total;
     size_t s_str = lloyd_smem(d, k2, groups, 1).total;

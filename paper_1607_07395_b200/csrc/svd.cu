@@ -17,6 +17,10 @@ constexpr int kSvdThreads = 1024;
 constexpr int kSvdMaxSweeps = 60;
 constexpr int kSvdSmemK = 112;
 
+#ifdef CABS_PROFILE_SVD
+__device__ long long g_svd_prof[8];
+#endif
+
 // Circle-method tournament: player 0 fixed, the others rotate by one seat per round.
 // 0 <= j - 1 + r < 2 (np - 1), so the modulo is one conditional subtraction.
 __device__ __forceinline__ int rr_player(int j, int r, int np) {
@@ -41,10 +45,19 @@ __device__ int jacobi_sweeps(double* A, double* V, int k, int* s_rot) {
   const double tol_rot = 2.0 * sqrt(static_cast<double>(k)) * DBL_EPSILON;
   const double tol_rot2 = tol_rot * tol_rot;
   int sweep = 0;
+#ifdef CABS_PROFILE_SVD
+  long long prof[6] = {0, 0, 0, 0, 0, 0}, t0 = 0;
+#define PROF_MARK(i) do { if (tid == 0) { long long t1 = clock64(); prof[i] += t1 - t0; t0 = t1; } } while (0)
+#else
+#define PROF_MARK(i) do { } while (0)
+#endif
   for (; sweep < kSvdMaxSweeps; ++sweep) {
     if (tid == 0) *s_rot = 0;
     __syncthreads();
     for (int rnd = 0; rnd < np - 1; ++rnd) {
+#ifdef CABS_PROFILE_SVD
+      if (tid == 0) t0 = clock64();
+#endif
       // warp-uniform trip count; the pair index differs per lane group
       for (int base = warp * kGroups; base < npairs; base += nwarps * kGroups) {
         const int pr = base + grp;
@@ -55,23 +68,35 @@ __device__ int jacobi_sweeps(double* A, double* V, int k, int* s_rot) {
         double* ap = A + (size_t)pp * k;
         double* aq = A + (size_t)qq * k;
         double x[E], y[E];
-        double al = 0, be = 0, ga = 0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const int i = gl + LP * e;
           const bool in = real && i < k;
           x[e] = in ? ap[i] : 0.0;
           y[e] = in ? aq[i] : 0.0;
-          al = fma(x[e], x[e], al);
-          be = fma(y[e], y[e], be);
-          ga = fma(x[e], y[e], ga);
         }
+        // two interleaved partial sums per dot product halve the dependent FMA chains
+        double al0 = 0, be0 = 0, ga0 = 0, al1 = 0, be1 = 0, ga1 = 0;
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+          al0 = fma(x[e], x[e], al0);
+          be0 = fma(y[e], y[e], be0);
+          ga0 = fma(x[e], y[e], ga0);
+          if (e + 1 < E) {
+            al1 = fma(x[e + 1], x[e + 1], al1);
+            be1 = fma(y[e + 1], y[e + 1], be1);
+            ga1 = fma(x[e + 1], y[e + 1], ga1);
+          }
+        }
+        double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
+        PROF_MARK(0);
 #pragma unroll
         for (int o = LP / 2; o > 0; o >>= 1) {
           al += __shfl_xor_sync(0xffffffffu, al, o);
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
+        PROF_MARK(1);
         // t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2 ga), evaluated in FP32
         // (scaled by a power of two when out of FP32 range): t's accuracy only sets the convergence
         // rate.  c = 1/sqrt(1+t^2) in FP64 and s = c t keep the rotation orthogonal to FP64 rounding.
@@ -91,31 +116,48 @@ __device__ int jacobi_sweeps(double* A, double* V, int k, int* s_rot) {
           }
           tf = copysignf(1.f, xf) * __fdividef(yf, fabsf(xf) + sqrtf(fmaf(xf, xf, yf * yf)));
         }
+        PROF_MARK(2);
         if (tf != 0.f) {  // group-uniform (all lanes of the group hold identical sums)
           const double t = static_cast<double>(tf);
           const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
           double* vp = V + (size_t)p * k;
           double* vq = V + (size_t)q * k;
+          // all loads before any store (A and V share one smem array: no aliasing stalls)
+          double u[E], v[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = gl + LP * e;
+            u[e] = i < k ? vp[i] : 0.0;
+            v[e] = i < k ? vq[i] : 0.0;
+          }
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int i = gl + LP * e;
             if (i < k) {
               ap[i] = c * x[e] - sn * y[e];
               aq[i] = sn * x[e] + c * y[e];
-              const double u = vp[i], v = vq[i];
-              vp[i] = c * u - sn * v;
-              vq[i] = sn * u + c * v;
+              vp[i] = c * u[e] - sn * v[e];
+              vq[i] = sn * u[e] + c * v[e];
             }
           }
           if (gl == 0) atomicAdd(s_rot, 1);
         }
+        PROF_MARK(3);
       }
       __syncthreads();
+      PROF_MARK(4);
     }
     const int rot = *s_rot;
     __syncthreads();
     if (rot == 0) break;
   }
+#ifdef CABS_PROFILE_SVD
+  if (tid == 0) {
+    extern __shared__ double smem_d[];
+    (void)smem_d;
+    for (int i = 0; i < 5; ++i) g_svd_prof[i] = prof[i];
+  }
+#endif
   return sweep;
 }
 
@@ -151,6 +193,10 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
     sweep = jacobi_sweeps<(L <= 1 ? 4 : L == 2 ? 8 : L == 4 ? 16 : 32), (L <= 4 ? 8 : L)>(A, V, k, &s_rot);
     if (sweep == kSvdMaxSweeps && tid == 0) set_status(ws, CABS_DEV_SVD_NOCONV);
     if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;  // diagnostics: sweeps of the last SVD
+#ifdef CABS_PROFILE_SVD
+    if (tid == 0)
+      for (int i = 0; i < 5; ++i) reinterpret_cast<long long*>(ws)[8 + i] = g_svd_prof[i];
+#endif
   }
 
   // singular values = column norms

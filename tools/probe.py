@@ -89,3 +89,26 @@ def probe_kmeans(N=20000, d=50, k2=50, iters=20, reps=3):
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] in ("kmeans", "all2"):
     for cfg in ((20000, 50, 50), (10000, 50, 50), (100000, 100, 100), (2000, 20, 20)):
         probe_kmeans(*cfg)
+
+
+def probe_svd_prof(k=50):
+    """Needs libcabs built with -DCABS_PROFILE_SVD: per-phase cycles of warp 0 summed over rounds."""
+    dev = torch.device("cuda:0")
+    plan = make_plan(1000, 1000, k)
+    ws = torch.zeros(C.cabs_workspace_bytes(plan), dtype=torch.uint8, device=dev)
+    g = np.random.default_rng(0)
+    W = torch.from_numpy(g.standard_normal((k, k)).astype(np.float32)).to(dev)
+    sig = torch.zeros(k, dtype=torch.float64, device=dev)
+    r = torch.zeros(1, dtype=torch.int32, device=dev)
+    C.cabs_svd(plan, k, W, 1e-12, sig, None, None, r, ws)
+    torch.cuda.synchronize()
+    sweeps = int(ws[32:36].view(torch.int32).item())
+    prof = ws[64:104].view(torch.int64).tolist()
+    rounds = sweeps * (k - 1 + (k % 2))
+    names = ["loads+dots", "shuffles", "rotation", "updates", "barrier"]
+    print(f"k={k} sweeps={sweeps} rounds~{rounds}: " + ", ".join(f"{n} {p / max(rounds, 1):.0f} cyc" for n, p in zip(names, prof)))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "svdprof":
+    for k in (20, 50, 100):
+        probe_svd_prof(k)
