@@ -270,7 +270,8 @@ int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   const bool allow_persistent = !(path && strcmp(path, "loop") == 0);
   if (allow_persistent && !multi(comm) && n_loc > 0 &&
       launch_lloyd_persistent(X, ldx, n_loc, d, k2, iters, w, centres, ldc, labels, objective, near_ties, cluster_w,
-                              wsp<float>(ws, L.km_psum), sizeof(float) * (size_t)kAccGrid * L.K * L.Kp, st)) {
+                              wsp<float>(ws, L.km_psum), sizeof(float) * (size_t)kAccGrid * L.K * L.Kp,
+                              reinterpret_cast<long long*>(ws) + 8, st)) {
     CABS_LAUNCH_CHECK("lloyd_persistent");
     return CABS_OK;
   }

@@ -49,7 +49,8 @@ void launch_km_finalize(const double* red, int k2, int d, float* centres, int64_
 // lloyd.cu (single-GPU persistent Lloyd loop; false -> use the per-iteration kernels)
 bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int k2, int iters, const float* w,
                              float* centres, int64_t ldc, int* labels, double* objective, int* near_ties,
-                             double* cluster_w, void* scratch, size_t scratch_bytes, cudaStream_t st);
+                             double* cluster_w, void* scratch, size_t scratch_bytes, long long* prof,
+                             cudaStream_t st);
 
 // select.cu
 void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t row_off, int T, float* cand_d,

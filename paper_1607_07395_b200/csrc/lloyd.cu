@@ -45,10 +45,11 @@ struct LloydArgs {
   double* pobj;     // [iters][G]
   int* ptie;        // [iters][G]
   int groups, dgroup, resident, tpc;
+  long long* prof;  // diagnostics (CABS_PROFILE_LLOYD builds): per-phase cycles of CTA 0
 };
 
 struct LloydSmem {
-  size_t cs, xt, acc, wacc, wts, total;
+  size_t cs, xt, acc, wacc, wts, winv, total;
 };
 __host__ __device__ inline LloydSmem lloyd_smem(int d, int k2, int groups, int ntile_buf) {
   LloydSmem L;
@@ -59,6 +60,7 @@ __host__ __device__ inline LloydSmem lloyd_smem(int d, int k2, int groups, int n
   L.acc = take(sizeof(float) * (size_t)groups * k2 * d);
   L.wacc = take(sizeof(double) * (size_t)groups * k2);
   L.wts = take(sizeof(float) * (size_t)ntile_buf * kTileP);
+  L.winv = take(sizeof(double) * (size_t)k2);
   L.total = o;
   return L;
 }
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
   float* acc = reinterpret_cast<float*>(dyn + L.acc);
   double* wacc = reinterpret_cast<double*>(dyn + L.wacc);
   float* wts_all = reinterpret_cast<float*>(dyn + L.wts);
+  double* winv = reinterpret_cast<double*>(dyn + L.winv);
   const int grp = tid / a.dgroup, gi = tid % a.dgroup;
   const int k2p = static_cast<int>(round_up(k2, 64));
   const int64_t ntiles = ceil_div(a.N, kTileP);
@@ -142,6 +145,12 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
   const int Sw = scale_exp(static_cast<double>(a.N) * wmax);
   const double scale = ldexp(1.0, S), scale_w = ldexp(1.0, Sw);
 
+#ifdef CABS_PROFILE_LLOYD
+  long long prof[6] = {0, 0, 0, 0, 0, 0}, t0 = clock64();
+#define LPROF(i) do { if (b == 0 && tid == 0) { long long t1 = clock64(); prof[i] += t1 - t0; t0 = t1; } } while (0)
+#else
+#define LPROF(i) do { } while (0)
+#endif
   for (int it = 0; it < a.iters; ++it) {
     long long* fs_cur = a.fsum + (size_t)(it % 3) * nsum;
     long long* fw_cur = a.fw + (size_t)(it % 3) * k2;
@@ -149,12 +158,16 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
     if (it > 0) {
       const long long* fs_prev = a.fsum + (size_t)((it + 2) % 3) * nsum;
       const long long* fw_prev = a.fw + (size_t)((it + 2) % 3) * k2;
+      // 1 / (weight_j * scale) once per cluster (0 marks an empty cluster), then one multiply per entry
+      for (int j = tid; j < k2; j += blockDim.x) {
+        const long long wj = __ldcg(fw_prev + j);
+        winv[j] = wj > 0 ? scale_w / (static_cast<double>(wj) * scale) : 0.0;
+      }
+      __syncthreads();
       for (int e = tid; e < nsum; e += blockDim.x) {
         const int j = e / d, i = e - j * d;
-        const long long wj = __ldcg(fw_prev + j);
-        if (wj > 0)
-          cs[j * cst + i] = static_cast<float>((static_cast<double>(__ldcg(fs_prev + e)) / scale) /
-                                               (static_cast<double>(wj) / scale_w));
+        const double wi = winv[j];
+        if (wi > 0) cs[j * cst + i] = static_cast<float>(static_cast<double>(__ldcg(fs_prev + e)) * wi);
       }
       // zero the slot the next iteration accumulates into (last read before the previous barrier)
       long long* fs_next = a.fsum + (size_t)((it + 1) % 3) * nsum;
@@ -169,6 +182,7 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
     double obj = 0.0;
     int ties = 0;
     __syncthreads();
+    LPROF(0);
     for (int64_t tile = t_beg; tile < t_end; ++tile) {
       const int64_t p0 = tile * kTileP;
       float* xt = xt_all;
@@ -239,6 +253,7 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
         }
       }
       __syncthreads();
+      LPROF(1);
       // group grp accumulates points [grp*per, (grp+1)*per) of the tile in index order;
       // thread gi owns dimension gi (and gi + dgroup, ... when d > dgroup)
       const int per = kTileP / a.groups;
@@ -253,6 +268,7 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
       }
       __syncthreads();
     }
+    LPROF(2);
     // publish: groups combined in fixed order, added to the global sums in fixed point
     for (int e = tid; e < nsum; e += blockDim.x) {
       float s = acc[e];
@@ -279,8 +295,14 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
       a.pobj[(size_t)it * G + b] = s;
       a.ptie[(size_t)it * G + b] = q;
     }
+    LPROF(3);
     grid_barrier(a.gmax + 2, gen);
+    LPROF(4);
   }
+#ifdef CABS_PROFILE_LLOYD
+  if (b == 0 && tid == 0)
+    for (int i = 0; i < 5; ++i) a.prof[i] = prof[i];
+#endif
   // ---------------- epilogue (CTA 0): final centres, cluster weights, objective history
   if (b == 0) {
     const long long* fs_last = a.fsum + (size_t)((a.iters - 1) % 3) * nsum;
@@ -308,7 +330,8 @@ __global__ void __launch_bounds__(kLloydThreads) lloyd_persistent_kernel(LloydAr
 // Returns false when the fast path does not apply (caller uses the per-iteration kernels).
 bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int k2, int iters, const float* w,
                              float* centres, int64_t ldc, int* labels, double* objective, int* near_ties,
-                             double* cluster_w, void* scratch, size_t scratch_bytes, cudaStream_t st) {
+                             double* cluster_w, void* scratch, size_t scratch_bytes, long long* prof,
+                             cudaStream_t st) {
   if (N <= 0) return false;
   const int dgroup = static_cast<int>(round_up(d < 256 ? d : 256, 32));
   const int groups = kLloydThreads / dgroup;
@@ -363,7 +386,7 @@ bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int 
   int* ptie = reinterpret_cast<int*>(pobj + (size_t)iters * G);
   if (cudaMemsetAsync(base, 0, sizeof(long long) * (3 * nsum + 3 * k2) + 16, st) != cudaSuccess) return false;
   LloydArgs a{X, ldx, N, d, k2, iters, w, centres, ldc, labels, objective, near_ties, cluster_w,
-              fsum, fw, gmax, pobj, ptie, groups, dgroup, resident, tpc};
+              fsum, fw, gmax, pobj, ptie, groups, dgroup, resident, tpc, prof};
   void* params[] = {&a};
   note_launch();
   cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lloyd_persistent_kernel),

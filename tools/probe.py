@@ -112,3 +112,24 @@ def probe_svd_prof(k=50):
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "svdprof":
     for k in (20, 50, 100):
         probe_svd_prof(k)
+
+
+def probe_lloyd_prof(N=20000, d=50, k2=50, iters=20):
+    """Needs libcabs built with -DCABS_PROFILE_LLOYD: per-phase cycles of CTA 0 per iteration."""
+    dev = torch.device("cuda:0")
+    plan = make_plan(N, N, max(d, k2))
+    ws = torch.zeros(C.cabs_workspace_bytes(plan), dtype=torch.uint8, device=dev)
+    ld = C.cabs_padded_ld(d)
+    X = torch.zeros(N, ld, device=dev); X[:, :d] = torch.randn(N, d, device=dev)
+    cen = torch.zeros(k2, ld, device=dev); lab = torch.zeros(N, dtype=torch.int32, device=dev)
+    cw = torch.zeros(k2, dtype=torch.float64, device=dev); obj = torch.zeros(iters, dtype=torch.float64, device=dev)
+    C.cabs_kmeans(plan, X, N, N, 0, d, k2, iters, 0, 2.0, 0, 3, cen, lab, cw, obj, ws)
+    torch.cuda.synchronize()
+    prof = ws[64:104].view(torch.int64).tolist()
+    names = ["centres+zero", "tiles:dist", "tiles:accum", "publish", "barrier"]
+    print(f"lloyd N={N} d={d} k2={k2}: " + ", ".join(f"{n} {p / iters:.0f} cyc" for n, p in zip(names, prof)))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "lloydprof":
+    for cfg in ((20000, 50, 50), (10000, 50, 50), (100000, 100, 100)):
+        probe_lloyd_prof(*cfg)
