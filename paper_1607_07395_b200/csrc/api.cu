@@ -317,16 +317,19 @@ int32_t cabs_select(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   const bool mr = multi(comm);
   const int T = mr ? kSnapTMulti : kSnapT;
   launch_km_distmat(X, ldx, n_loc, d, centres, ldc, k2, D, L.Nmax, st);
-  launch_snap_topT(D, L.Nmax, n_loc, k2, row_off, T, cd, ci, st);
+  // per-centre top-T over S point segments in parallel; lists packed as doubles so that
+  // other ranks' slots (zeros here) are completed by ONE sum-allreduce, then merged
+  int S = static_cast<int>(ceil_div(n_loc > 0 ? n_loc : 1, 4096));
+  if (S > kSnapSeg) S = kSnapSeg;
+  const int nr = mr ? comm->nranks : 1;
+  double* all = wsp<double>(ws, L.cand_all);
+  const int64_t nall = 2LL * nr * S * k2 * T;
+  if (mr) CABS_CUDA_TRY(cudaMemsetAsync(all, 0, sizeof(double) * nall, st));
+  if (n_loc > 0) launch_snap_topT(D, L.Nmax, n_loc, k2, row_off, T, S, (mr ? comm->rank : 0) * S, all, st);
   CABS_LAUNCH_CHECK("snap distmat/topT");
-  if (mr) {
-    double* all = wsp<double>(ws, L.cand_all);
-    launch_snap_pack(cd, ci, k2, T, comm->rank, comm->nranks, all, st);
-    CABS_LAUNCH_CHECK("snap_pack");
-    CABS_TRY(comm_f64(comm, all, 2LL * comm->nranks * k2 * T, stream));
-    launch_snap_merge(all, k2, T, comm->nranks, cd, ci, st);
-    CABS_LAUNCH_CHECK("snap_merge");
-  }
+  CABS_TRY(comm_f64(comm, all, nall, stream));
+  launch_snap_merge(all, k2, T, nr * S, cd, ci, st);
+  CABS_LAUNCH_CHECK("snap_merge");
   launch_snap_dedupe(cd, ci, k2, T, cluster_w, D, L.Nmax, n_loc, row_off, !mr, rep_of_centre, gap, reps, ws, st);
   CABS_LAUNCH_CHECK("snap_dedupe");
   return CABS_OK;

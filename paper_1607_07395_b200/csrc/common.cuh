@@ -11,6 +11,7 @@ namespace cabsk {
 constexpr int kNumSM = 148;           // B200: 2 dies x 74 SMs
 constexpr int kSnapT = 8;             // per-centre candidate list length in the snap
 constexpr int kSnapTMulti = 32;       // ... when candidates are merged across ranks
+constexpr int kSnapSeg = 8;           // point segments scanned in parallel per centre
 constexpr int kAccGrid = 2 * kNumSM;  // k-means accumulation CTAs (per-CTA partials)
 constexpr int kAssignGrid = 4 * kNumSM;
 constexpr int kResGrid = 8 * kNumSM;  // persistent residual CTAs (upper bound)
@@ -74,7 +75,7 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.dist = take(sizeof(float) * K * w.Nmax);
   w.cand_d = take(sizeof(float) * K * kSnapTMulti);
   w.cand_i = take(sizeof(int64_t) * K * kSnapTMulti);
-  w.cand_all = take(sizeof(double) * 2 * nr * K * kSnapTMulti);
+  w.cand_all = take(sizeof(double) * 2 * nr * kSnapSeg * K * kSnapTMulti);
   w.idx = take(sizeof(int64_t) * 8 * Kp);
   w.cb = take(sizeof(float) * (w.m_loc > 0 ? w.m_loc : 1) * Kp);
   w.rb = take(sizeof(float) * K * w.ldrb);

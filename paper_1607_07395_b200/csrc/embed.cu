@@ -143,60 +143,98 @@ int launch_embed_products(int64_t m_loc, int64_t n_sl, int k, const float* C, in
 // kind 0 (embed):  alpha = sqrt(s)/N_c, beta = sqrt(s)/N_r
 // kind 1 (sketch): alpha = 1/N_c,       beta = 1/N_r,  s_out = s
 // s = sigma sqrt(m n)/k (STABILIZED) or N_c N_r / sigma (PSEUDO_SKELETON, Eq. 2).
-__global__ void embed_finalize_kernel(int k, const double* __restrict__ sig, const int* __restrict__ r_in,
-                                      const double* __restrict__ nc2, const double* __restrict__ nr2, int mode,
-                                      double m, double n, double ksamp, int kind, double* __restrict__ alpha,
-                                      double* __restrict__ beta, int* __restrict__ newpos, float* __restrict__ s_out,
-                                      int* __restrict__ r_out, int* __restrict__ r_out2) {
-  if (threadIdx.x != 0) return;
+// One thread per component; newpos = exclusive prefix count of kept components (block scan).
+// flags[0] = r_eff, flags[1] = 1 when the kept components are exactly 0..r_eff-1 (no compaction).
+__global__ void __launch_bounds__(1024) embed_finalize_kernel(int k, const double* __restrict__ sig,
+                                                              const int* __restrict__ r_in,
+                                                              const double* __restrict__ nc2,
+                                                              const double* __restrict__ nr2, int mode, double m,
+                                                              double n, double ksamp, int kind,
+                                                              double* __restrict__ alpha, double* __restrict__ beta,
+                                                              int* __restrict__ newpos, float* __restrict__ s_out,
+                                                              int* __restrict__ r_out, int* __restrict__ r_out2,
+                                                              int* __restrict__ flags) {
+  __shared__ int warp_cnt[32];
+  __shared__ int s_total, s_hole;
+  const int c = threadIdx.x, lane = c & 31, warp = c >> 5;
   const int r = *r_in;
-  int pos = 0;
-  for (int c = 0; c < k; ++c) {
+  bool keep = false;
+  double s = 0, a = 0, bb = 0;
+  if (c < k) {
     const double Nc = sqrt(nc2[c]), Nr = sqrt(nr2[c]);
-    const bool keep = c < r && Nc > 0 && Nr > 0;
-    if (!keep) {
-      newpos[c] = -1;
-      alpha[c] = 0;
-      beta[c] = 0;
-      continue;
+    keep = c < r && Nc > 0 && Nr > 0;
+    if (keep) {
+      s = (mode == CABS_STABILIZED) ? sig[c] * sqrt(m * n) / ksamp : Nc * Nr / sig[c];
+      if (kind == 0) {
+        const double rs = sqrt(s);
+        a = rs / Nc;
+        bb = rs / Nr;
+      } else {
+        a = 1.0 / Nc;
+        bb = 1.0 / Nr;
+      }
     }
-    const double s = (mode == CABS_STABILIZED) ? sig[c] * sqrt(m * n) / ksamp : Nc * Nr / sig[c];
-    if (kind == 0) {
-      const double rs = sqrt(s);
-      alpha[c] = rs / Nc;
-      beta[c] = rs / Nr;
-    } else {
-      alpha[c] = 1.0 / Nc;
-      beta[c] = 1.0 / Nr;
-    }
-    if (s_out) s_out[pos] = static_cast<float>(s);
-    newpos[c] = pos++;
   }
-  if (s_out)
-    for (int c = pos; c < k; ++c) s_out[c] = 0.f;
-  if (r_out) *r_out = pos;
-  if (r_out2) *r_out2 = pos;
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  if (lane == 0) warp_cnt[warp] = __popc(bal);
+  if (c == 0) s_hole = 0;
+  __syncthreads();
+  if (c == 0) {
+    int t = 0;
+    for (int w = 0; w < 32; ++w) { const int x = warp_cnt[w]; warp_cnt[w] = t; t += x; }
+    s_total = t;
+  }
+  __syncthreads();
+  const int pos = warp_cnt[warp] + __popc(bal & ((1u << lane) - 1u));
+  if (c < k) {
+    newpos[c] = keep ? pos : -1;
+    alpha[c] = a;
+    beta[c] = bb;
+    if (keep && pos != c) atomicOr(&s_hole, 1);
+  }
+  __syncthreads();
+  const int reff = s_total;
+  if (c < k && s_out) s_out[c] = 0.f;
+  __syncthreads();
+  if (keep && s_out) s_out[pos] = static_cast<float>(s);
+  if (c == 0) {
+    if (r_out) *r_out = reff;
+    if (r_out2) *r_out2 = reff;
+    flags[0] = reff;
+    flags[1] = s_hole ? 0 : 1;
+  }
 }
 
-// In-place: row[newpos[c]] = row[c] * scale[c] for kept c, zeros in [r_eff, k).
+// Element-wise fast path (kept components are 0..r_eff-1): Y[p, c] *= scale[c], zero c >= r_eff.
+__global__ void __launch_bounds__(256) scale_ident_kernel(float* __restrict__ Y, int64_t ldy, int64_t N, int k,
+                                                          const double* __restrict__ scale,
+                                                          const int* __restrict__ flags) {
+  if (flags[1] == 0) return;  // compaction needed: scale_compact_kernel does it
+  const int reff = flags[0];
+  const int64_t total = N * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / k;
+    const int c = static_cast<int>(e - p * k);
+    float* y = Y + p * ldy + c;
+    *y = c < reff ? static_cast<float>(static_cast<double>(*y) * scale[c]) : 0.f;
+  }
+}
+
+// In-place compaction (a dropped component inside [0, r)): row[newpos[c]] = row[c] * scale[c]
+// for kept c, zeros in [r_eff, k).  Rare; one warp per row.
 __global__ void __launch_bounds__(256) scale_compact_kernel(float* __restrict__ Y, int64_t ldy, int64_t N, int k,
                                                             const double* __restrict__ scale,
-                                                            const int* __restrict__ newpos) {
+                                                            const int* __restrict__ newpos,
+                                                            const int* __restrict__ flags) {
+  if (flags[1] != 0) return;  // identity layout: handled element-wise by scale_ident_kernel
   __shared__ double s_scale[CABS_KMAX];
   __shared__ int s_pos[CABS_KMAX];
-  __shared__ int s_reff;
   for (int c = threadIdx.x; c < k; c += blockDim.x) {
     s_scale[c] = scale[c];
     s_pos[c] = newpos[c];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int r = 0;
-    for (int c = 0; c < k; ++c) r += s_pos[c] >= 0;
-    s_reff = r;
-  }
-  __syncthreads();
-  const int reff = s_reff;
+  const int reff = flags[0];
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -210,7 +248,6 @@ __global__ void __launch_bounds__(256) scale_compact_kernel(float* __restrict__ 
       v[q] = c < k ? row[c] : 0.f;
     }
     __syncwarp();
-    // positions [r_eff, k) become zero; kept values land in [0, r_eff) (newpos < r_eff)
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       const int c = lane + 32 * q;
@@ -230,11 +267,13 @@ int launch_embed_finalize(int k, int mode, double m, double n, double ksamp, int
                           void* ws, const Ws& L, cudaStream_t st) {
   double* sc = wsp<double>(ws, L.scales);
   int* newpos = reinterpret_cast<int*>(sc + 2 * L.Kp);
+  int* flags = newpos + L.Kp;
   const double* norms = wsp<double>(ws, L.norms);
   int* scal = wsp<int>(ws, L.scal);
   note_launch();
-  embed_finalize_kernel<<<1, 32, 0, st>>>(k, wsp<double>(ws, L.sig64), scal + SCAL_R_TMP, norms, norms + L.Kp, mode, m,
-                                          n, ksamp, kind, sc, sc + L.Kp, newpos, s_out, scal + SCAL_R_TMP, r_user);
+  embed_finalize_kernel<<<1, 1024, 0, st>>>(k, wsp<double>(ws, L.sig64), scal + SCAL_R_TMP, norms, norms + L.Kp, mode,
+                                            m, n, ksamp, kind, sc, sc + L.Kp, newpos, s_out, scal + SCAL_R_TMP,
+                                            r_user, flags);
   return 0;
 }
 
@@ -242,10 +281,16 @@ int launch_scale_compact(float* Y, int64_t ldy, int64_t N, int k, int which, voi
   if (N <= 0) return 0;
   double* sc = wsp<double>(ws, L.scales);
   int* newpos = reinterpret_cast<int*>(sc + 2 * L.Kp);
-  int64_t blocks = ceil_div(N, 8);
+  int* flags = newpos + L.Kp;
+  int64_t blocks = ceil_div(N * k, 256 * 4);
+  if (blocks > 8 * kNumSM) blocks = 8 * kNumSM;
+  if (blocks < 1) blocks = 1;
+  note_launch();
+  scale_ident_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(Y, ldy, N, k, sc + which * L.Kp, flags);
+  blocks = ceil_div(N, 8);
   if (blocks > 8 * kNumSM) blocks = 8 * kNumSM;
   note_launch();
-  scale_compact_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(Y, ldy, N, k, sc + which * L.Kp, newpos);
+  scale_compact_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(Y, ldy, N, k, sc + which * L.Kp, newpos, flags);
   return 0;
 }
 

@@ -14,20 +14,25 @@
 namespace cabsk {
 
 // ---------------------------------------------------------------- per-centre top-T
+// grid (k2, S): block (j, s) keeps the T nearest (d, index) of centre j among points of
+// segment s and writes them as list (slot0 + s) of the packed candidate array
+// all[list][k2][T][{d, idx}] (doubles; idx < 2^53 exact).  Empty entries: idx = -1.
 template <int T>
 __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict__ D, int64_t ldd, int64_t N,
-                                                        int64_t row_off, float* __restrict__ cand_d,
-                                                        int64_t* __restrict__ cand_i) {
+                                                        int64_t row_off, int k2, int slot0,
+                                                        double* __restrict__ all) {
   __shared__ float hd[256];
   __shared__ int64_t hi[256];
   __shared__ int s_win;
   const int j = blockIdx.x, tid = threadIdx.x;
+  const int64_t seg = ceil_div(N, gridDim.y);
+  const int64_t pbeg = blockIdx.y * seg, pend = pbeg + seg < N ? pbeg + seg : N;
   float ld[T];
   int64_t li[T];
 #pragma unroll
   for (int q = 0; q < T; ++q) { ld[q] = FLT_MAX; li[q] = INT64_MAX; }
   const float* row = D + (int64_t)j * ldd;
-  for (int64_t p = tid; p < N; p += blockDim.x) {
+  for (int64_t p = pbeg + tid; p < pend; p += blockDim.x) {
     const float v = row[p];
     const int64_t gi = row_off + p;
     if (lex_less(v, gi, ld[T - 1], li[T - 1])) {
@@ -72,8 +77,9 @@ __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict_
         if (lex_less(od, oi, bd, bi)) { bd = od; bi = oi; bt = ot; }
       }
       if (tid == 0) {
-        cand_d[(int64_t)j * T + round] = bd;
-        cand_i[(int64_t)j * T + round] = bi == INT64_MAX ? -1 : bi;
+        const int64_t e = ((((int64_t)slot0 + blockIdx.y) * k2 + j) * T + round) * 2;
+        all[e] = static_cast<double>(bd);
+        all[e + 1] = bi == INT64_MAX ? -1.0 : static_cast<double>(bi);
         s_win = bt;
       }
     }
@@ -83,37 +89,20 @@ __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict_
   }
 }
 
-void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t row_off, int T, float* cand_d,
-                      int64_t* cand_i, cudaStream_t st) {
+void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t row_off, int T, int nseg, int slot0,
+                      double* all, cudaStream_t st) {
+  dim3 grid(k2, nseg);
+  note_launch();
   if (T == kSnapT) {
-    note_launch();
-    snap_topT_kernel<kSnapT><<<k2, 256, 0, st>>>(D, ldd, N, row_off, cand_d, cand_i);
+    snap_topT_kernel<kSnapT><<<grid, 256, 0, st>>>(D, ldd, N, row_off, k2, slot0, all);
   } else {
-    note_launch();
-    snap_topT_kernel<kSnapTMulti><<<k2, 256, 0, st>>>(D, ldd, N, row_off, cand_d, cand_i);
+    snap_topT_kernel<kSnapTMulti><<<grid, 256, 0, st>>>(D, ldd, N, row_off, k2, slot0, all);
   }
 }
 
 // ---------------------------------------------------------------- multi-rank candidate exchange
-// all[rank][j][t][{d, idx}] as doubles (exact: idx < 2^53), zero elsewhere; summed by the caller.
-__global__ void snap_pack_kernel(const float* __restrict__ cand_d, const int64_t* __restrict__ cand_i, int k2, int T,
-                                 int rank, int nranks, double* __restrict__ all) {
-  const int64_t per = (int64_t)k2 * T;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per * nranks;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = static_cast<int>(e / per);
-    const int64_t q = e % per;
-    all[2 * e] = r == rank ? static_cast<double>(cand_d[q]) : 0.0;
-    all[2 * e + 1] = r == rank ? static_cast<double>(cand_i[q]) : 0.0;
-  }
-}
-
-void launch_snap_pack(const float* cand_d, const int64_t* cand_i, int k2, int T, int rank, int nranks, double* all,
-                      cudaStream_t st) {
-  note_launch();
-  snap_pack_kernel<<<64, 256, 0, st>>>(cand_d, cand_i, k2, T, rank, nranks, all);
-}
-
+// Merge of the packed per-segment (and per-rank) lists: the global T nearest per centre,
+// ordered by (d, idx).  Lists of other ranks are zero-filled slots completed by a sum-allreduce.
 __global__ void snap_merge_kernel(const double* __restrict__ all, int k2, int T, int nranks, float* __restrict__ cand_d,
                                   int64_t* __restrict__ cand_i) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -164,13 +153,13 @@ __device__ __forceinline__ void taken_put(int64_t* tab, int64_t x) {
   tab[h] = x;
 }
 
-__global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* __restrict__ cand_d,
-                                                          const int64_t* __restrict__ cand_i, int k2, int T,
+__global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, const int64_t* cand_i, int k2, int T,
                                                           const double* __restrict__ cluster_w,
                                                           const float* __restrict__ D, int64_t ldd, int64_t N,
                                                           int64_t row_off, bool can_rescan,
                                                           int64_t* __restrict__ rep_of_centre, float* __restrict__ gap,
-                                                          int64_t* __restrict__ reps_sorted, void* ws) {
+                                                          int64_t* __restrict__ reps_sorted, void* ws,
+                                                          bool stage_cands) {
   __shared__ int64_t tab[kTakenCap];
   __shared__ int order[CABS_KMAX];
   __shared__ int64_t reps[CABS_KMAX];
@@ -178,8 +167,21 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* __restric
   __shared__ int s_rescan;    // centre needing a rescan, or -1
   __shared__ float rd[256], rs[256];
   __shared__ int64_t ri[256];
+  extern __shared__ __align__(16) unsigned char cand_smem[];
   const int tid = threadIdx.x;
   for (int e = tid; e < kTakenCap; e += blockDim.x) tab[e] = -1;
+  // the sequential greedy pass reads candidates from shared memory when they fit
+  const bool staged = stage_cands;
+  if (staged) {
+    int64_t* si = reinterpret_cast<int64_t*>(cand_smem);
+    float* sd = reinterpret_cast<float*>(si + (size_t)k2 * T);
+    for (int e = tid; e < k2 * T; e += blockDim.x) {
+      si[e] = cand_i[e];
+      sd[e] = cand_d[e];
+    }
+    cand_i = si;
+    cand_d = sd;
+  }
   // visiting order (-omega_j, j)
   for (int j = tid; j < k2; j += blockDim.x) {
     const double wj = cluster_w[j];
@@ -272,9 +274,17 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* __restric
 void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int T, const double* cluster_w,
                         const float* D, int64_t ldd, int64_t N, int64_t row_off, bool can_rescan,
                         int64_t* rep_of_centre, float* gap, int64_t* reps_sorted, void* ws, cudaStream_t st) {
+  constexpr size_t kCap = 160 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(snap_dedupe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCap));
+    attr = true;
+  }
+  const size_t bytes = (size_t)k2 * T * (sizeof(int64_t) + sizeof(float));
+  const bool stage = bytes <= kCap;
   note_launch();
-  snap_dedupe_kernel<<<1, 256, 0, st>>>(cand_d, cand_i, k2, T, cluster_w, D, ldd, N, row_off, can_rescan, rep_of_centre,
-                                        gap, reps_sorted, ws);
+  snap_dedupe_kernel<<<1, 256, stage ? bytes : 0, st>>>(cand_d, cand_i, k2, T, cluster_w, D, ldd, N, row_off, can_rescan,
+                                                        rep_of_centre, gap, reps_sorted, ws, stage);
 }
 
 }  // namespace cabsk

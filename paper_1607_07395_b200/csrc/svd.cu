@@ -36,7 +36,7 @@ __device__ __forceinline__ int rr_player(int j, int r, int np) {
 // pairs at once and the dot products are LP-lane butterflies.  One CTA issues every
 // instruction of a round, so fewer, fuller warps per round is what shortens it.
 template <int LP, int E>
-__device__ int jacobi_sweeps(double* A, double* V, int k, int* s_rot) {
+__device__ int jacobi_sweeps(double* A, int k, int* s_rot) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   constexpr int kGroups = 32 / LP;
   const int grp = lane / LP, gl = lane % LP;
@@ -120,24 +120,12 @@ __device__ int jacobi_sweeps(double* A, double* V, int k, int* s_rot) {
         if (tf != 0.f) {  // group-uniform (all lanes of the group hold identical sums)
           const double t = static_cast<double>(tf);
           const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
-          double* vp = V + (size_t)p * k;
-          double* vq = V + (size_t)q * k;
-          // all loads before any store (A and V share one smem array: no aliasing stalls)
-          double u[E], v[E];
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int i = gl + LP * e;
-            u[e] = i < k ? vp[i] : 0.0;
-            v[e] = i < k ? vq[i] : 0.0;
-          }
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int i = gl + LP * e;
             if (i < k) {
               ap[i] = c * x[e] - sn * y[e];
               aq[i] = sn * x[e] + c * y[e];
-              vp[i] = c * u[e] - sn * v[e];
-              vq[i] = sn * u[e] + c * v[e];
             }
           }
           if (gl == 0) atomicAdd(s_rot, 1);
@@ -171,18 +159,18 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
   __shared__ int s_rot;
   __shared__ double s_sig[CABS_KMAX];
   __shared__ int s_perm[CABS_KMAX];  // s_perm[rank] = column
+  __shared__ double s_h[CABS_KMAX];  // Gram-Schmidt coefficients
   // SMEM is a compile-time choice so the columns are addressed as shared memory (LDS/STS)
   double* A = SMEM ? smem_d : gA;
   double* V = SMEM ? smem_d + (size_t)k * k : gV;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
 
-  // load: A[c*k + i] = W[i, c] (column-major), V = I
+  // load: A[c*k + i] = W[i, c] (column-major)
   for (int e = tid; e < k * k; e += blockDim.x) {
     const int c = e / k, i = e - c * k;
     float w = W[(int64_t)i * ldw + c];
     if (!isfinite(w)) set_status(ws, CABS_DEV_NONFINITE);
     A[e] = static_cast<double>(w);
-    V[e] = (c == i) ? 1.0 : 0.0;
   }
   __syncthreads();
 
@@ -190,7 +178,7 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
   if (k > 1) {
     // L = ceil(k/32) class -> (lanes per pair, elements per lane): 8 elements per lane
     // while k <= 256, so small k packs several pairs into each warp
-    sweep = jacobi_sweeps<(L <= 1 ? 4 : L == 2 ? 8 : L == 4 ? 16 : 32), (L <= 4 ? 8 : L)>(A, V, k, &s_rot);
+    sweep = jacobi_sweeps<(L <= 1 ? 4 : L == 2 ? 8 : L == 4 ? 16 : 32), (L <= 4 ? 8 : L)>(A, k, &s_rot);
     if (sweep == kSvdMaxSweeps && tid == 0) set_status(ws, CABS_DEV_SVD_NOCONV);
     if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;  // diagnostics: sweeps of the last SVD
 #ifdef CABS_PROFILE_SVD
@@ -231,6 +219,52 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
   for (int j = tid; j < k; j += blockDim.x) {
     if (sigma_out) sigma_out[j] = s_sig[s_perm[j]];
   }
+  // Right singular vectors without accumulating the rotations (which would double the
+  // shared-memory traffic of every round): W^T W V = V S^2 and A = W V = U S give
+  // v_c = W^T a_c / sigma_c^2 for the kept components, then two passes of classical
+  // Gram-Schmidt in descending sigma order restore orthonormality to FP64 rounding.
+  for (int e = tid; e < k * k; e += blockDim.x) {
+    const int c = e / k, i = e - c * k;
+    const double sg = s_sig[c];
+    double v = 0.0;
+    if (sg > tol * smax && sg > 0) {
+      const double* ac = A + (size_t)c * k;
+      for (int rr = 0; rr < k; ++rr) v = fma(static_cast<double>(W[(int64_t)rr * ldw + i]), ac[rr], v);
+      v /= sg * sg;
+    }
+    V[e] = v;
+  }
+  __syncthreads();
+  for (int j = 1; j < r; ++j) {
+    double* vj = V + (size_t)s_perm[j] * k;
+    for (int pass = 0; pass < 2; ++pass) {
+      // coefficients h_i = v_i . v_j for the j earlier (larger-sigma) columns, one warp each
+      for (int i = warp; i < j; i += nwarps) {
+        const double* vi = V + (size_t)s_perm[i] * k;
+        double h = 0;
+        for (int e = lane; e < k; e += 32) h = fma(vi[e], vj[e], h);
+        h = warp_sum_d(h);
+        if (lane == 0) s_h[i] = h;
+      }
+      __syncthreads();
+      for (int e = tid; e < k; e += blockDim.x) {
+        double x = vj[e];
+        for (int i = 0; i < j; ++i) x = fma(-s_h[i], V[(size_t)s_perm[i] * k + e], x);
+        vj[e] = x;
+      }
+      __syncthreads();
+    }
+  }
+  // unit norms (column j of V now orthogonal to the earlier ones)
+  for (int j = warp; j < r; j += nwarps) {
+    double* vj = V + (size_t)s_perm[j] * k;
+    double ss = 0;
+    for (int e = lane; e < k; e += 32) ss = fma(vj[e], vj[e], ss);
+    ss = warp_sum_d(ss);
+    const double inv = ss > 0 ? 1.0 / sqrt(ss) : 0.0;
+    for (int e = lane; e < k; e += 32) vj[e] *= inv;
+  }
+  __syncthreads();
   // write U_w, V_w columns in rank order with canonical sign
   for (int j = warp; j < k; j += nwarps) {
     const int c = s_perm[j];

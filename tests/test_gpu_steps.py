@@ -366,3 +366,29 @@ def test_kmeans_persistent_and_loop_paths_agree(dev, monkeypatch):
     (c1, l1, w1, o1), (c2, l2, w2, o2) = outs
     assert np.array_equal(l1, l2) and np.array_equal(w1, w2)
     assert rel_fro(c1, c2) < 1e-6 and np.allclose(o1, o2, rtol=1e-6)
+
+
+def test_embed_drops_zero_norm_component_with_compaction(dev):
+    """S:244 drop rule with a hole: component 0 extrapolates to zero, component 1 is kept,
+    so the kept component must be compacted to position 0 (inconsistent triple, as in the
+    oracle's safeguard test)."""
+    m, n, k = 3, 4, 2
+    plan = _plan(m, n, k)
+    ws = _ws(plan, dev)
+    C_np = np.array([[0.0, 1.0], [0.0, 0.0], [0.0, 0.0]], dtype=np.float32)
+    R_np = np.array([[1.0, 0.5, 0.0, 2.0], [0.0, 1.0, 1.0, 0.0]], dtype=np.float32)
+    W_np = np.diag([2.0, 1.0]).astype(np.float32)
+    ld = C.cabs_padded_ld(k)
+    Ct = torch.zeros((m, ld), device=dev); Ct[:, :k] = torch.from_numpy(C_np).to(dev)
+    Rt = torch.zeros((k, 4), device=dev); Rt[:, :n] = torch.from_numpy(R_np).to(dev)
+    Wt = torch.zeros((k, ld), device=dev); Wt[:, :k] = torch.from_numpy(W_np).to(dev)
+    P = torch.zeros((m, ld), device=dev); Q = torch.zeros((n, ld), device=dev)
+    s = torch.zeros(k, device=dev); r = torch.zeros(1, dtype=torch.int32, device=dev)
+    C.cabs_embed(plan, k, Ct, Rt, Wt, C.STABILIZED, 1e-12, P, Q, s, r, ws)
+    sk = O.sketch(C_np, R_np, W_np, m, n, k)
+    Pr, Qr = O.embeddings(sk)
+    assert int(r.item()) == sk.r == 1
+    assert rel_fro(align_signs(P.cpu().numpy()[:, :1], Pr), Pr) < 1e-6
+    assert rel_fro(align_signs(Q.cpu().numpy()[:, :1], Qr), Qr) < 1e-6
+    assert np.all(P.cpu().numpy()[:, 1:] == 0) and np.all(Q.cpu().numpy()[:, 1:] == 0)
+    assert abs(s[0].item() - sk.s[0]) < 1e-6 * sk.s[0] and s[1].item() == 0.0
