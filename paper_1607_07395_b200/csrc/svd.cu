@@ -7,6 +7,7 @@
 // otherwise in the (L2-resident) workspace.  Output: sigma descending, truncation
 // count r = #{sigma_i > tol sigma_1} (Z4), canonical signs (Z5).
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -33,10 +34,12 @@ __device__ __forceinline__ int rr_player(int j, int r, int np) {
 // Cyclic one-sided Jacobi sweeps until no pair needs a rotation (or the sweep cap).
 // A group of LP lanes (LP | 32) runs one column pair, each lane holding E = ceil(k/LP)
 // elements of both columns in registers (rows g + LP e), so a warp advances 32/LP
-// pairs at once and the dot products are LP-lane butterflies.  One CTA issues every
-// instruction of a round, so fewer, fuller warps per round is what shortens it.
+// pairs at once and the dot products are LP-lane butterflies.  A round is one
+// dependent chain (loads -> dots -> butterfly -> angle -> update -> barrier), so the
+// body is branch-free: the angle is always computed (t = 0 when no rotation is due),
+// the update always stored, and the rotation count rides on the round's barrier.
 template <int LP, int E>
-__device__ int jacobi_sweeps(double* A, int k, int* s_rot) {
+__device__ int jacobi_sweeps(double* A, int k) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   constexpr int kGroups = 32 / LP;
   const int grp = lane / LP, gl = lane % LP;
@@ -45,28 +48,19 @@ __device__ int jacobi_sweeps(double* A, int k, int* s_rot) {
   const double tol_rot = 2.0 * sqrt(static_cast<double>(k)) * DBL_EPSILON;
   const double tol_rot2 = tol_rot * tol_rot;
   int sweep = 0;
-#ifdef CABS_PROFILE_SVD
-  long long prof[6] = {0, 0, 0, 0, 0, 0}, t0 = 0;
-#define PROF_MARK(i) do { if (tid == 0) { long long t1 = clock64(); prof[i] += t1 - t0; t0 = t1; } } while (0)
-#else
-#define PROF_MARK(i) do { } while (0)
-#endif
   for (; sweep < kSvdMaxSweeps; ++sweep) {
-    if (tid == 0) *s_rot = 0;
-    __syncthreads();
+    int rotations = 0;
     for (int rnd = 0; rnd < np - 1; ++rnd) {
-#ifdef CABS_PROFILE_SVD
-      if (tid == 0) t0 = clock64();
-#endif
+      int rotated = 0;
       // warp-uniform trip count; the pair index differs per lane group
       for (int base = warp * kGroups; base < npairs; base += nwarps * kGroups) {
         const int pr = base + grp;
-        int p = rr_player(pr < npairs ? pr : 0, rnd, np), q = rr_player(np - 1 - (pr < npairs ? pr : 0), rnd, np);
-        if (p > q) { const int t = p; p = q; q = t; }
-        const bool real = pr < npairs && q < k;  // group-uniform
-        const int pp = real ? p : 0, qq = real ? q : 0;
-        double* ap = A + (size_t)pp * k;
-        double* aq = A + (size_t)qq * k;
+        const int prc = pr < npairs ? pr : 0;
+        int p = rr_player(prc, rnd, np), q = rr_player(np - 1 - prc, rnd, np);
+        const int lo = p < q ? p : q, hi = p < q ? q : p;
+        const bool real = pr < npairs && hi < k;  // group-uniform
+        double* ap = A + (size_t)(real ? lo : 0) * k;
+        double* aq = A + (size_t)(real ? hi : 0) * k;
         double x[E], y[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -89,65 +83,49 @@ __device__ int jacobi_sweeps(double* A, int k, int* s_rot) {
           }
         }
         double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
-        PROF_MARK(0);
 #pragma unroll
         for (int o = LP / 2; o > 0; o >>= 1) {
           al += __shfl_xor_sync(0xffffffffu, al, o);
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        PROF_MARK(1);
         // t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2 ga), evaluated in FP32
-        // (scaled by a power of two when out of FP32 range): t's accuracy only sets the convergence
-        // rate.  c = 1/sqrt(1+t^2) in FP64 and s = c t keep the rotation orthogonal to FP64 rounding.
-        float tf = 0.f;
-        if (ga != 0.0 && ga * ga > tol_rot2 * al * be) {
-          const double dx = be - al, dy = 2.0 * ga;
-          const double mx = fmax(fabs(dx), fabs(dy));
-          float xf, yf;
-          if (mx > 1e-30 && mx < 1e30) {
-            xf = static_cast<float>(dx);
-            yf = static_cast<float>(dy);
-          } else {
-            int ex;
-            frexp(mx, &ex);
-            xf = static_cast<float>(ldexp(dx, -ex));
-            yf = static_cast<float>(ldexp(dy, -ex));
-          }
-          tf = copysignf(1.f, xf) * __fdividef(yf, fabsf(xf) + sqrtf(fmaf(xf, xf, yf * yf)));
-        }
-        PROF_MARK(2);
-        if (tf != 0.f) {  // group-uniform (all lanes of the group hold identical sums)
-          const double t = static_cast<double>(tf);
-          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+        // on operands scaled by an exact power of two (exponent arithmetic on the bits): t's
+        // accuracy only sets the convergence rate.  c = 1/sqrt(1+t^2) to FP64 accuracy (FP32
+        // seed + two Newton steps) and s = c t keep the rotation orthogonal to FP64 rounding.
+        const bool need = ga != 0.0 && ga * ga > tol_rot2 * al * be;
+        const double dx = be - al, dy = 2.0 * ga;
+        const double mx = fmax(fabs(dx), fabs(dy));
+        const int ex = static_cast<int>((__double_as_longlong(mx) >> 52) & 0x7ff);  // biased exponent
+        const double scl = __longlong_as_double(static_cast<long long>(2046 - ex) << 52);  // 2^(1023-(ex-1023))
+        const float xf = static_cast<float>(dx * scl), yf = static_cast<float>(dy * scl);
+        const float hyp = fmaf(xf, xf, yf * yf);
+        const float den = fabsf(xf) + hyp * __frsqrt_rn(hyp);  // |x| + sqrt(x^2 + y^2)
+        float tf = copysignf(1.f, xf) * __fdividef(yf, den);
+        tf = (need && ex > 0 && ex < 2046 && den > 0.f) ? tf : 0.f;
+        const double t = static_cast<double>(tf);
+        const double q1 = fma(t, t, 1.0);
+        double c = static_cast<double>(__frsqrt_rn(static_cast<float>(q1)));
+        c = c * fma(-0.5 * q1, c * c, 1.5);
+        c = c * fma(-0.5 * q1, c * c, 1.5);
+        const double sn = c * t;
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int i = gl + LP * e;
-            if (i < k) {
-              ap[i] = c * x[e] - sn * y[e];
-              aq[i] = sn * x[e] + c * y[e];
-            }
+        for (int e = 0; e < E; ++e) {
+          const int i = gl + LP * e;
+          if (real && i < k) {
+            ap[i] = c * x[e] - sn * y[e];
+            aq[i] = sn * x[e] + c * y[e];
           }
-          if (gl == 0) atomicAdd(s_rot, 1);
         }
-        PROF_MARK(3);
+        rotated |= tf != 0.f;
       }
-      __syncthreads();
-      PROF_MARK(4);
+      rotations += __syncthreads_count(rotated);
     }
-    const int rot = *s_rot;
-    __syncthreads();
-    if (rot == 0) break;
+    if (rotations == 0) break;
   }
-#ifdef CABS_PROFILE_SVD
-  if (tid == 0) {
-    extern __shared__ double smem_d[];
-    (void)smem_d;
-    for (int i = 0; i < 5; ++i) g_svd_prof[i] = prof[i];
-  }
-#endif
   return sweep;
 }
+
 
 template <int L, bool SMEM>
 __global__ void __launch_bounds__(kSvdThreads, 1)
@@ -178,7 +156,7 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
   if (k > 1) {
     // L = ceil(k/32) class -> (lanes per pair, elements per lane): 8 elements per lane
     // while k <= 256, so small k packs several pairs into each warp
-    sweep = jacobi_sweeps<(L <= 1 ? 4 : L == 2 ? 8 : L == 4 ? 16 : 32), (L <= 4 ? 8 : L)>(A, k, &s_rot);
+    sweep = jacobi_sweeps<(L <= 1 ? 4 : L == 2 ? 8 : L == 4 ? 16 : 32), (L <= 4 ? 8 : L)>(A, k);
     if (sweep == kSvdMaxSweeps && tid == 0) set_status(ws, CABS_DEV_SVD_NOCONV);
     if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;  // diagnostics: sweeps of the last SVD
 #ifdef CABS_PROFILE_SVD
@@ -325,7 +303,9 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
             : k <= 256 ? svd_jacobi_kernel<8, false> : k <= 320 ? svd_jacobi_kernel<10, false>
                        : svd_jacobi_kernel<32, false>;
   note_launch();
-  kern<<<1, kSvdThreads, smem, st>>>(k, W, ldw, tol, wsp<double>(ws, L.a64), wsp<double>(ws, L.v64), sig, Uw64, Vw64,
+  int nthreads = kSvdThreads;
+  if (const char* e = getenv("CABS_SVD_THREADS")) nthreads = atoi(e);  // experiments only
+  kern<<<1, nthreads, smem, st>>>(k, W, ldw, tol, wsp<double>(ws, L.a64), wsp<double>(ws, L.v64), sig, Uw64, Vw64,
                                      wsp<float>(ws, L.uw32), wsp<float>(ws, L.vw32), L.Kp, r_ws, r_user, use_smem, ws);
   if (sigma_user && sigma_user != wsp<double>(ws, L.sig64)) {
     cudaMemcpyAsync(wsp<double>(ws, L.sig64), sigma_user, sizeof(double) * k, cudaMemcpyDeviceToDevice, st);

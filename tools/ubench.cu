@@ -50,6 +50,41 @@ __global__ void lat_rsqrt64(double* out, int n) {
   out[threadIdx.x] = x;
   if (threadIdx.x == 0) out[1000] = (double)(t1 - t0) / n;
 }
+__global__ void lat_f2f(double* out, int n) {
+  double x = out[threadIdx.x] + 1.5;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    float f = static_cast<float>(x);
+    x = static_cast<double>(f * 1.0000001f);
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = x;
+  if (threadIdx.x == 0) out[1000] = (double)(t1 - t0) / n;
+}
+__global__ void lat_dsetp(double* out, int n) {
+  double x = out[threadIdx.x] + 1.5;
+  int c = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    if (x * x > 2.0) c++;
+    x = x * 1.0000001 + (double)(c & 1) * 1e-30;
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = x + c;
+  if (threadIdx.x == 0) out[1000] = (double)(t1 - t0) / n;
+}
+__global__ void lat_atoms(double* out, int n) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    if ((threadIdx.x & 7) == 0) atomicAdd(&cnt, 1);
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[1000] = (double)(t1 - t0) / n;
+}
 __global__ void lat_syncthreads(double* out, int n) {
   long long t0 = clock64();
   for (int i = 0; i < n; ++i) __syncthreads();
@@ -113,6 +148,12 @@ int main() {
   CK(cudaMemcpy(&h, d + 1000, 8, cudaMemcpyDeviceToHost)); printf("dependent LDS.64 (+cvt)     %.1f cycles\n", h);
   lat_rsqrt64<<<1, 32>>>(d, n);
   CK(cudaMemcpy(&h, d + 1000, 8, cudaMemcpyDeviceToHost)); printf("dependent rsqrt(double)+add %.1f cycles\n", h);
+  lat_f2f<<<1, 32>>>(d, n);
+  CK(cudaMemcpy(&h, d + 1000, 8, cudaMemcpyDeviceToHost)); printf("dependent F2F f64->f32->f64 + FMUL %.1f cycles\n", h);
+  lat_dsetp<<<1, 32>>>(d, n);
+  CK(cudaMemcpy(&h, d + 1000, 8, cudaMemcpyDeviceToHost)); printf("dependent DMUL+DSETP+branch %.1f cycles\n", h);
+  lat_atoms<<<1, 256>>>(d, n);
+  CK(cudaMemcpy(&h, d + 1000, 8, cudaMemcpyDeviceToHost)); printf("smem atomic (32 lanes) + sync %.1f cycles\n", h);
   lat_syncthreads<<<1, 1024>>>(d, n);
   CK(cudaMemcpy(&h, d + 1000, 8, cudaMemcpyDeviceToHost)); printf("__syncthreads (1024 thr)    %.1f cycles\n", h);
   CK(cudaDeviceSynchronize());
