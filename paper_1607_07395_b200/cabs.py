@@ -73,6 +73,7 @@ _SIGS = {
     "cabs_version": (None, [ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "cabs_padded_ld": (c_i64, [c_i32]),
     "cabs_launch_count": (c_i64, []),
+    "cabs_debug_counters": (c_i32, [ctypes.POINTER(c_i64), c_i32]),
     "cabs_workspace_bytes": (c_sz, [ctypes.POINTER(Plan)]),
     "cabs_clear_status": (c_i32, [c_vp, c_vp]),
     "cabs_device_status": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_u32)]),
@@ -163,6 +164,12 @@ def cabs_workspace_bytes(plan: Plan) -> int:
     if n == 0:
         raise CabsError("invalid plan")
     return n
+
+
+def cabs_debug_counters(n=16):
+    buf = (c_i64 * n)()
+    _check(load().cabs_debug_counters(buf, n), "cabs_debug_counters")
+    return list(buf)
 
 
 def cabs_launch_count() -> int:

@@ -84,6 +84,13 @@ const char* cabs_status_string(int32_t s) {
 
 const char* cabs_last_error_string(void) { return g_err; }
 
+int32_t cabs_debug_counters(int64_t* out, int32_t n) {
+  if (!out || n < 0) return CABS_ERR_INVALID_ARG;
+  cudaDeviceSynchronize();
+  residual_debug_counters(reinterpret_cast<long long*>(out), n);
+  return CABS_OK;
+}
+
 int64_t cabs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 void cabs_version(int32_t* major, int32_t* minor) {

@@ -4,49 +4,106 @@
 // epilogue that streams the matching A tile through shared memory (TMA), so
 // A - F G^T is never materialised and A is read from HBM exactly once.
 //
-// Persistent, warp-specialised, one CTA per SM:
-//   warp 0  TMA producer: F_hi/F_lo row band (resident while the band lasts),
-//           G_hi/G_lo column tiles and A tiles, double-buffered (mbarrier ring)
-//   warp 1  TMEM allocator + single-thread MMA issuer: per 128 x 64 tile and per
-//           8-wide k step, D += Fh Gh^T + Fh Gl^T + Fl Gh^T into one of two TMEM
-//           accumulators (64 columns each)
-//   warps 2-5 epilogue: tcgen05.ld the accumulator row (lane = row), read the A row
-//           from the 128B-swizzled smem tile, accumulate (a - a~)^2 and a^2 in FP32
-//           per tile, FP64 across tiles; fixed-order block and grid reductions.
-// Tile order is row-band major over a static contiguous tile range per CTA, so the
-// result is bit-reproducible.  Requires ncomp <= 64 (two 32-float K atoms).
+// Persistent, warp-specialised, one CTA per SM, tiles of 128 rows x 128 columns:
+//   warp 0   TMA producer: G_hi/G_lo column tiles (2-deep ring), A quarter tiles
+//            (128 x 32, 6-deep ring)
+//   warp 1   TMEM allocator + single-thread MMA issuer.  The row band's F_hi/F_lo
+//            live in TMEM (double-buffered across bands) and are the MMA's A operand,
+//            so every MMA reads only its 128 x 8 G slice from shared memory (an SS MMA
+//            would re-read 4 KB of F per instruction and saturate shared memory).
+//            Per 8-wide k step: D += Fh Gh^T + Fh Gl^T + Fl Gh^T (TMEM, 2 stages).
+//   warps 2-5 epilogue: write F rows into TMEM (one band ahead), tcgen05.ld the
+//            accumulator row (lane = row), read the A row from the 128B-swizzled smem
+//            tile, accumulate (a - a~)^2 and a^2 in FP32 per tile, FP64 across tiles.
+// Tile order is row-band major over a static contiguous tile range per CTA; fixed-order
+// block and grid reductions: bit-reproducible.  Requires ncomp <= 64.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
 
 namespace cabsk {
 
-constexpr int kTcBM = 128, kTcBN = 64, kTcKA = 2;  // K atoms of 32 floats (128 B)
-constexpr int kTcThreads = 192;
-constexpr uint32_t kFAtomBytes = kTcBM * 128;      // 16 KB
-constexpr uint32_t kGAtomBytes = kTcBN * 128;      // 8 KB
-constexpr uint32_t kABoxBytes = kTcBM * 128;       // 16 KB: 128 rows x 32 floats
+constexpr int kTcBM = 128, kTcBN = 128;            // N = 128: a full-rate tcgen05 shape (N <= 96 is
+                                                    // bound by a ~47-cycle per-instruction floor)
+constexpr int kAS = 6, kGS = 2, kCS = 2;            // A quarter-tile / G tile / TMEM accumulator stages
+constexpr int kAQ = kTcBN / 32;                     // A boxes (128 x 32) per tile
+constexpr int kTcThreads = 224;                     // 0 TMA (A), 1 MMA, 2-5 epilogue, 6 TMA (G)
+constexpr int kKp = 64;                             // K padded (two 32-float swizzle atoms)
+constexpr uint32_t kGAtomBytes = kTcBN * 128;      // 16 KB
+constexpr uint32_t kABoxBytes = kTcBM * 128;       // 16 KB: 128 rows x 32 floats = a quarter A tile
+// TMEM columns: [0, 256) accumulators (2 stages x 128); [256, 512) F buffers (2 x {hi 64 | lo 64})
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kFCol0 = kCS * kTcBN;
 
 struct TcSmem {
-  // 1024-byte aligned operand tiles (128B swizzle atoms)
-  uint8_t fh[kTcKA][kFAtomBytes];
-  uint8_t fl[kTcKA][kFAtomBytes];
-  uint8_t gh[2][kTcKA][kGAtomBytes];
-  uint8_t gl[2][kTcKA][kGAtomBytes];
-  uint8_t a[2][2][kABoxBytes];  // [stage][column half]
-  uint64_t f_full, f_empty;
-  uint64_t g_full[2], g_empty[2];
-  uint64_t a_full[2], a_empty[2];
-  uint64_t acc_full[2], acc_empty[2];
+  uint8_t gh[kGS][2][kGAtomBytes];  // 1024-byte aligned 128B-swizzle atoms
+  uint8_t gl[kGS][2][kGAtomBytes];
+  uint8_t a[kAS][kABoxBytes];
+  uint64_t f_ready[2], f_free[2];
+  uint64_t g_full[kGS], g_empty[kGS];
+  uint64_t a_full[kAS], a_empty[kAS];
+  uint64_t acc_full[kCS], acc_empty[kCS];
   uint32_t tmem_base;
   double red[2][4];
 };
 
+#ifdef CABS_PROFILE_RES
+__device__ long long g_res_prof[16];
+#define RES_WAIT(slot, call) do { long long t0_ = clock64(); call; prof[slot] += clock64() - t0_; } while (0)
+#else
+#define RES_WAIT(slot, call) call
+#endif
+
+// phase parity of the n-th (0-based) completion of a ring slot used every `stages` items
+__device__ __forceinline__ uint32_t ring_parity(int64_t i, int stages) { return static_cast<uint32_t>((i / stages) & 1); }
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// 32 lanes x 32 columns: registers -> TMEM (this warp's lane quarter)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
+// Epilogue warps: F_hi/F_lo rows of band rb -> TMEM buffer fb (row = lane quarter q * 32 + lane).
+__device__ __forceinline__ void load_f_band(const float* __restrict__ fh, const float* __restrict__ fl, int64_t m,
+                                            int64_t rb, int q, int lane, uint32_t tmem, int fb, uint64_t* ready) {
+  const int64_t r = rb * kTcBM + q * 32 + lane;
+  const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + kFCol0 + static_cast<uint32_t>(fb * 2 * kKp);
+#pragma unroll
+  for (int part = 0; part < 4; ++part) {  // hi cols 0-31, 32-63; lo cols 0-31, 32-63
+    const float* src = (part < 2 ? fh : fl) + r * kKp + (part & 1) * 32;
+    float v[32];
+#pragma unroll
+    for (int c = 0; c < 32; c += 4) {
+      float4 x = r < m ? __ldg(reinterpret_cast<const float4*>(src + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[c] = x.x; v[c + 1] = x.y; v[c + 2] = x.z; v[c + 3] = x.w;
+    }
+    tmem_st32(tq + static_cast<uint32_t>(part * 32), v);
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  tc::fence_before_sync();
+  __syncwarp();
+  if (lane == 0) tc::mbar_arrive(ready);
+}
+
 __global__ void __launch_bounds__(kTcThreads, 1)
-residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmFh,
-                   const __grid_constant__ CUtensorMap tmFl, const __grid_constant__ CUtensorMap tmGh,
-                   const __grid_constant__ CUtensorMap tmGl, int64_t m, int64_t n, int ksteps,
-                   double* __restrict__ part) {
+residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmGh,
+                   const __grid_constant__ CUtensorMap tmGl, const float* __restrict__ fh,
+                   const float* __restrict__ fl, int64_t m, int64_t n, int ksteps, double* __restrict__ part) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -54,131 +111,159 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   const int64_t T = ntr * ntc;
   const int64_t t_beg = (T * blockIdx.x) / gridDim.x, t_end = (T * (blockIdx.x + 1)) / gridDim.x;
   const int katoms = ksteps > 4 ? 2 : 1;  // 8-wide k steps per 32-float atom = 4
+  const int64_t rb0 = t_beg / ntc, nbands = (t_end - 1) / ntc - rb0 + 1;
 
   if (warp == 0 && lane == 0) {
-    tc::tma_prefetch(&tmA); tc::tma_prefetch(&tmFh); tc::tma_prefetch(&tmFl);
-    tc::tma_prefetch(&tmGh); tc::tma_prefetch(&tmGl);
-    tc::mbar_init(&S.f_full, 1);
-    tc::mbar_init(&S.f_empty, 1);
-    for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(&S.g_full[s], 1);
-      tc::mbar_init(&S.g_empty[s], 1);
-      tc::mbar_init(&S.a_full[s], 1);
-      tc::mbar_init(&S.a_empty[s], 4);
-      tc::mbar_init(&S.acc_full[s], 1);
-      tc::mbar_init(&S.acc_empty[s], 4);
-    }
+    tc::tma_prefetch(&tmA); tc::tma_prefetch(&tmGh); tc::tma_prefetch(&tmGl);
+    for (int b = 0; b < 2; ++b) { tc::mbar_init(&S.f_ready[b], 4); tc::mbar_init(&S.f_free[b], 1); }
+    for (int s = 0; s < kGS; ++s) { tc::mbar_init(&S.g_full[s], 1); tc::mbar_init(&S.g_empty[s], 1); }
+    for (int s = 0; s < kAS; ++s) { tc::mbar_init(&S.a_full[s], 1); tc::mbar_init(&S.a_empty[s], 4); }
+    for (int s = 0; s < kCS; ++s) { tc::mbar_init(&S.acc_full[s], 1); tc::mbar_init(&S.acc_empty[s], 4); }
     tc::mbar_fence_init();
   }
-  if (warp == 1) tc::tmem_alloc(&S.tmem_base, 128);
+  if (warp == 1) tc::tmem_alloc(&S.tmem_base, kTmemCols);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem_base;
+#ifdef CABS_PROFILE_RES
+  long long prof[16] = {0};
+  const long long t_start = clock64();
+#endif
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      int64_t prev_rb = -1;
-      uint32_t nf = 0;
       for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
         const int64_t rb = t / ntc, cb = t % ntc;
-        const int s = static_cast<int>(i & 1);
-        if (rb != prev_rb) {
-          if (nf > 0) tc::mbar_wait(&S.f_empty, (nf - 1) & 1);
-          tc::mbar_expect_tx(&S.f_full, 2 * katoms * kFAtomBytes);
-          for (int a = 0; a < katoms; ++a) {
-            tc::tma_load_2d(S.fh[a], &tmFh, a * 32, static_cast<int>(rb * kTcBM), &S.f_full);
-            tc::tma_load_2d(S.fl[a], &tmFl, a * 32, static_cast<int>(rb * kTcBM), &S.f_full);
-          }
-          ++nf;
-          prev_rb = rb;
+        // A (the HBM stream the kernel is bound by): kAQ boxes of 128 x 32 per tile
+        for (int h = 0; h < kAQ; ++h) {
+          const int64_t ia = kAQ * i + h;
+          const int sa = static_cast<int>(ia % kAS);
+          if (ia >= kAS) RES_WAIT(1, tc::mbar_wait(&S.a_empty[sa], ring_parity(ia - kAS, kAS)));
+          tc::mbar_expect_tx(&S.a_full[sa], kABoxBytes);
+          tc::tma_load_2d(S.a[sa], &tmA, static_cast<int>(cb * kTcBN + 32 * h), static_cast<int>(rb * kTcBM),
+                          &S.a_full[sa]);
         }
-        if (i >= 2) tc::mbar_wait(&S.g_empty[s], ((i >> 1) - 1) & 1);
-        tc::mbar_expect_tx(&S.g_full[s], 2 * katoms * kGAtomBytes);
+      }
+    }
+  } else if (warp == 6) {
+    // ------------------------------------------------------------ TMA producer (G tiles), its own
+    // thread so that a full A ring never delays the next tile's MMA operands
+    if (lane == 0) {
+      for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
+        const int64_t cb = t % ntc;
+        const int sg = static_cast<int>(i % kGS);
+        if (i >= kGS) RES_WAIT(2, tc::mbar_wait(&S.g_empty[sg], ring_parity(i - kGS, kGS)));
+        tc::mbar_expect_tx(&S.g_full[sg], 2 * katoms * kGAtomBytes);
         for (int a = 0; a < katoms; ++a) {
-          tc::tma_load_2d(S.gh[s][a], &tmGh, a * 32, static_cast<int>(cb * kTcBN), &S.g_full[s]);
-          tc::tma_load_2d(S.gl[s][a], &tmGl, a * 32, static_cast<int>(cb * kTcBN), &S.g_full[s]);
+          tc::tma_load_2d(S.gh[sg][a], &tmGh, a * 32, static_cast<int>(cb * kTcBN), &S.g_full[sg]);
+          tc::tma_load_2d(S.gl[sg][a], &tmGl, a * 32, static_cast<int>(cb * kTcBN), &S.g_full[sg]);
         }
-        if (i >= 2) tc::mbar_wait(&S.a_empty[s], ((i >> 1) - 1) & 1);
-        tc::mbar_expect_tx(&S.a_full[s], 2 * kABoxBytes);
-        for (int h = 0; h < 2; ++h)
-          tc::tma_load_2d(S.a[s][h], &tmA, static_cast<int>(cb * kTcBN + h * 32), static_cast<int>(rb * kTcBM),
-                          &S.a_full[s]);
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+    // ------------------------------------------------------------ MMA issuer (A operand = F in TMEM)
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_tf32(kTcBM, kTcBN);
-      int64_t prev_rb = -1;
-      uint32_t nf = 0;
+      uint64_t dgh[kGS][2], dgl[kGS][2];
+#pragma unroll
+      for (int g = 0; g < kGS; ++g)
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          dgh[g][a] = tc::desc_sw128(tc::smem_u32(S.gh[g][a]));
+          dgl[g][a] = tc::desc_sw128(tc::smem_u32(S.gl[g][a]));
+        }
+      int64_t prev_rb = -1, band = -1;
+      uint32_t fcol = 0;
       for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
         const int64_t rb = t / ntc;
-        const int s = static_cast<int>(i & 1);
+        const int sg = static_cast<int>(i % kGS), sc = static_cast<int>(i % kCS);
         if (rb != prev_rb) {
-          tc::mbar_wait(&S.f_full, nf & 1);
-          ++nf;
+          if (band >= 0) tc::mma_commit(&S.f_free[band & 1]);  // previous band's F no longer read
+          ++band;
+          RES_WAIT(4, tc::mbar_wait(&S.f_ready[band & 1], static_cast<uint32_t>((band >> 1) & 1)));
+          fcol = tmem + kFCol0 + static_cast<uint32_t>((band & 1) * 2 * kKp);
           prev_rb = rb;
         }
-        tc::mbar_wait(&S.g_full[s], (i >> 1) & 1);
-        if (i >= 2) tc::mbar_wait(&S.acc_empty[s], ((i >> 1) - 1) & 1);
+        RES_WAIT(5, tc::mbar_wait(&S.g_full[sg], ring_parity(i, kGS)));
+        if (i >= kCS) RES_WAIT(6, tc::mbar_wait(&S.acc_empty[sc], ring_parity(i - kCS, kCS)));
         tc::fence_after_sync();
-        const uint32_t d = tmem + static_cast<uint32_t>(s * kTcBN);
+        const uint32_t d = tmem + static_cast<uint32_t>(sc * kTcBN);
         for (int kk = 0; kk < ksteps; ++kk) {
           const int a = kk >> 2;
-          const uint32_t off = static_cast<uint32_t>((kk & 3) * 32);
-          const uint64_t fh = tc::desc_sw128(tc::smem_u32(S.fh[a]) + off);
-          const uint64_t fl = tc::desc_sw128(tc::smem_u32(S.fl[a]) + off);
-          const uint64_t gh = tc::desc_sw128(tc::smem_u32(S.gh[s][a]) + off);
-          const uint64_t gl = tc::desc_sw128(tc::smem_u32(S.gl[s][a]) + off);
-          tc::mma_tf32(d, fh, gh, idesc, kk > 0 ? 1u : 0u);
-          tc::mma_tf32(d, fh, gl, idesc, 1u);
-          tc::mma_tf32(d, fl, gh, idesc, 1u);
+          const uint64_t off = static_cast<uint64_t>((kk & 3) * 2);
+          const uint64_t gh = (sg == 0 ? dgh[0][a] : dgh[1][a]) + off;
+          const uint64_t gl = (sg == 0 ? dgl[0][a] : dgl[1][a]) + off;
+          const uint32_t fh_t = fcol + static_cast<uint32_t>(kk * 8), fl_t = fh_t + kKp;
+          mma_tf32_ts(d, fh_t, gh, idesc, kk > 0 ? 1u : 0u);
+          mma_tf32_ts(d, fh_t, gl, idesc, 1u);
+          mma_tf32_ts(d, fl_t, gh, idesc, 1u);
         }
-        tc::mma_commit(&S.g_empty[s]);
-        tc::mma_commit(&S.acc_full[s]);
-        const bool band_ends = (t + 1 == t_end) || ((t + 1) / ntc != rb);
-        if (band_ends) tc::mma_commit(&S.f_empty);
+        tc::mma_commit(&S.g_empty[sg]);
+        tc::mma_commit(&S.acc_full[sc]);
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 2-5)
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;    // row within the 128-row tile
+    // F of the first two bands, then one band ahead of the MMA
+    load_f_band(fh, fl, m, rb0, q, lane, tmem, 0, &S.f_ready[0]);
+    if (nbands > 1) load_f_band(fh, fl, m, rb0 + 1, q, lane, tmem, 1, &S.f_ready[1]);
     double r2 = 0.0, a2 = 0.0;
+    int64_t prev_rb = rb0;
     for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
-      const int s = static_cast<int>(i & 1);
-      const uint32_t ph = static_cast<uint32_t>((i >> 1) & 1);
-      tc::mbar_wait(&S.acc_full[s], ph);
+      const int64_t rb = t / ntc;
+      if (rb != prev_rb) {  // entering band j = rb - rb0: stage band j + 1 into the buffer band j - 1 used
+        prev_rb = rb;
+        const int64_t j = rb - rb0;
+        if (j + 1 < nbands) {
+          const int fb = static_cast<int>((j + 1) & 1);
+          tc::mbar_wait(&S.f_free[fb], static_cast<uint32_t>(((j - 1) >> 1) & 1));
+          tc::fence_after_sync();
+          load_f_band(fh, fl, m, rb + 1, q, lane, tmem, fb, &S.f_ready[fb]);
+        }
+      }
+      const int sc = static_cast<int>(i % kCS);
+      RES_WAIT(11, tc::mbar_wait(&S.acc_full[sc], ring_parity(i, kCS)));
       tc::fence_after_sync();
-      tc::mbar_wait(&S.a_full[s], ph);
-      float tr = 0.f, ta = 0.f;
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(sc * kTcBN);
+      float tr0 = 0.f, ta0 = 0.f, tr1 = 0.f, ta1 = 0.f;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float v[32];
-        tc::tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(s * kTcBN + h * 32), v);
-        const uint8_t* arow = S.a[s][h] + row * 128;
+      for (int h = 0; h < kAQ; ++h) {
+        // A row from a 128B-swizzled box (16-byte chunk c of row r is at chunk c ^ (r & 7));
+        // the box slot is released as soon as its values are in registers
+        const int64_t ia = kAQ * i + h;
+        const int sa = static_cast<int>(ia % kAS);
+        RES_WAIT(10, tc::mbar_wait(&S.a_full[sa], ring_parity(ia, kAS)));
+        float av[32];
+        const uint8_t* arow = S.a[sa] + row * 128;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const float4 a4 = *reinterpret_cast<const float4*>(arow + ((c ^ (row & 7)) << 4));
-          const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+          av[4 * c] = a4.x; av[4 * c + 1] = a4.y; av[4 * c + 2] = a4.z; av[4 * c + 3] = a4.w;
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.a_empty[sa]);
+        float v[32];
+        tc::tmem_ld32(tbase + 32 * h, v);
+        if (h == kAQ - 1) {
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);
+        }
 #pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            const float e = av[x] - v[c * 4 + x];
-            tr = fmaf(e, e, tr);
-            ta = fmaf(av[x], av[x], ta);
-          }
+        for (int x = 0; x < 32; x += 2) {
+          const float e0 = av[x] - v[x], e1 = av[x + 1] - v[x + 1];
+          tr0 = fmaf(e0, e0, tr0);
+          ta0 = fmaf(av[x], av[x], ta0);
+          tr1 = fmaf(e1, e1, tr1);
+          ta1 = fmaf(av[x + 1], av[x + 1], ta1);
         }
       }
-      tc::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) {
-        tc::mbar_arrive(&S.acc_empty[s]);
-        tc::mbar_arrive(&S.a_empty[s]);
-      }
-      r2 += static_cast<double>(tr);
-      a2 += static_cast<double>(ta);
+      r2 += static_cast<double>(tr0 + tr1);
+      a2 += static_cast<double>(ta0 + ta1);
     }
     r2 = warp_sum_d(r2);
     a2 = warp_sum_d(a2);
@@ -187,11 +272,18 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       S.red[1][q] = a2;
     }
   }
+#ifdef CABS_PROFILE_RES
+  if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 1 || warp == 2)) {
+    const long long tot = clock64() - t_start;
+    for (int s2 = 0; s2 < 16; ++s2) if (prof[s2]) g_res_prof[s2] = prof[s2];
+    g_res_prof[warp == 0 ? 3 : warp == 1 ? 7 : 12] = tot;
+  }
+#endif
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 1) {
     tc::fence_after_sync();
-    tc::tmem_dealloc(tmem, 128);
+    tc::tmem_dealloc(tmem, kTmemCols);
   }
   if (threadIdx.x == 0) {
     part[2 * blockIdx.x] = ((S.red[0][0] + S.red[0][1]) + S.red[0][2]) + S.red[0][3];
@@ -208,9 +300,20 @@ __global__ void split_tf32_kernel(const float* __restrict__ X, int64_t ldx, int6
     const int c = static_cast<int>(e % kp);
     float x = 0.f;
     if (c < ncomp) x = X[r * ldx + c] * (s ? s[c] : 1.f);
-    const float h = tc::tf32_rna(x);
+    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);  // TF32 operand bits
     hi[e] = h;
-    lo[e] = x - h;
+    if (lo) lo[e] = x - h;
+  }
+}
+
+// G copied with zero padding to kp columns (raw FP32: split inside the kernel).
+__global__ void pad_copy_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int ncomp,
+                                float* __restrict__ out, int kp) {
+  const int64_t total = rows * kp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / kp;
+    const int c = static_cast<int>(e % kp);
+    out[e] = c < ncomp ? X[r * ldx + c] : 0.f;
   }
 }
 
@@ -244,8 +347,16 @@ static bool make_map(CUtensorMap* tm, const float* base, int64_t cols, int64_t r
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+void residual_debug_counters(long long* out, int n) {
+#ifdef CABS_PROFILE_RES
+  cudaMemcpyFromSymbol(out, g_res_prof, sizeof(long long) * (n < 16 ? n : 16));
+#else
+  for (int i = 0; i < n; ++i) out[i] = 0;
+#endif
+}
+
 bool residual_tc_supported(const float* A, int64_t lda, int64_t m_loc, int64_t n, int ncomp) {
-  if (ncomp < 1 || ncomp > kTcKA * 32 || m_loc < 1 || n < 1) return false;
+  if (ncomp < 1 || ncomp > kKp || m_loc < 1 || n < 1) return false;
   if ((lda % 4) != 0 || (reinterpret_cast<uintptr_t>(A) & 15) != 0) return false;
   if (m_loc > 0x7fffffff || n > 0x7fffffff) return false;
   if (getenv("CABS_RESIDUAL_FFMA")) return false;
@@ -255,7 +366,7 @@ bool residual_tc_supported(const float* A, int64_t lda, int64_t m_loc, int64_t n
 int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, const float* F, int64_t ldf,
                        const float* s, const float* G, int64_t ldg, int ncomp, float* split, double* part, double* out,
                        cudaStream_t st) {
-  const int kp = ncomp > 32 ? 64 : 32;
+  const int kp = kKp;
   float* fh = split;
   float* fl = fh + m_loc * kp;
   float* gh = fl + m_loc * kp;
@@ -264,9 +375,8 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
   split_tf32_kernel<<<2 * kNumSM, 256, 0, st>>>(F, ldf, m_loc, ncomp, s, fh, fl, kp);
   note_launch();
   split_tf32_kernel<<<2 * kNumSM, 256, 0, st>>>(G, ldg, n, ncomp, nullptr, gh, gl, kp);
-  CUtensorMap tA, tFh, tFl, tGh, tGl;
-  if (!make_map(&tA, A, n, m_loc, lda, kTcBM) || !make_map(&tFh, fh, kp, m_loc, kp, kTcBM) ||
-      !make_map(&tFl, fl, kp, m_loc, kp, kTcBM) || !make_map(&tGh, gh, kp, n, kp, kTcBN) ||
+  CUtensorMap tA, tGh, tGl;
+  if (!make_map(&tA, A, n, m_loc, lda, kTcBM) || !make_map(&tGh, gh, kp, n, kp, kTcBN) ||
       !make_map(&tGl, gl, kp, n, kp, kTcBN))
     return -1;
   static bool attr = false;
@@ -282,7 +392,7 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
   int64_t g = T < nsm ? T : nsm;
   const int ksteps = static_cast<int>(ceil_div(ncomp, 8));
   note_launch();
-  residual_tc_kernel<<<static_cast<unsigned>(g), kTcThreads, smem, st>>>(tA, tFh, tFl, tGh, tGl, m_loc, n, ksteps, part);
+  residual_tc_kernel<<<static_cast<unsigned>(g), kTcThreads, smem, st>>>(tA, tGh, tGl, fh, fl, m_loc, n, ksteps, part);
   launch_residual_final(part, static_cast<int>(g), out, st);
   return 0;
 }

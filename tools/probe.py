@@ -133,3 +133,13 @@ def probe_lloyd_prof(N=20000, d=50, k2=50, iters=20):
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "lloydprof":
     for cfg in ((20000, 50, 50), (10000, 50, 50), (100000, 100, 100)):
         probe_lloyd_prof(*cfg)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "resprof":
+    probe_residual(20000, 10000, 50, reps=1)
+    c = C.cabs_debug_counters(16)
+    names = {0: "prod wait f_empty", 1: "prod wait a_empty", 2: "prod wait g_empty", 3: "prod total",
+             4: "mma wait f_full", 5: "mma wait g_split", 6: "mma wait acc_empty", 7: "mma total",
+             8: "split wait g_full", 9: "split total", 10: "epi wait a_full", 11: "epi wait acc_full", 12: "epi total"}
+    for i, nm in names.items():
+        print(f"{nm:22s} {c[i]:12d} cycles")
