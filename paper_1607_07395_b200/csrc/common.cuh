@@ -29,7 +29,7 @@ struct Ws {
   size_t dist, cand_d, cand_i, cand_all;
   size_t idx;
   size_t cb, rb, wb;
-  size_t res_part, res_split;
+  size_t res_part, res_split;  // res_split: G_hi, G_lo (n x 64 each)
   size_t total;
   // dims
   int64_t K, Kp, m_loc, n_sl, Nmax, n, ldrb, npt;
@@ -81,7 +81,7 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.rb = take(sizeof(float) * K * w.ldrb);
   w.wb = take(sizeof(float) * K * Kp);
   w.res_part = take(sizeof(double) * 2 * kResGrid);
-  w.res_split = take(sizeof(float) * 2 * (size_t)(w.m_loc + p.n) * 64);
+  w.res_split = take(sizeof(float) * 2 * (size_t)p.n * 64);
   w.total = off;
   return w;
 }

@@ -55,7 +55,7 @@ bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int 
 // select.cu
 void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t row_off, int T, int nseg, int slot0,
                       double* all, cudaStream_t st);
-void launch_snap_merge(const double* all, int k2, int T, int nranks, float* cand_d, int64_t* cand_i, cudaStream_t st);
+void launch_snap_merge(const double* all, int k2, int T, int nlists, float* cand_d, int64_t* cand_i, cudaStream_t st);
 void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int T, const double* cluster_w,
                         const float* D, int64_t ldd, int64_t N, int64_t row_off, bool can_rescan,
                         int64_t* rep_of_centre, float* gap, int64_t* reps_sorted, void* ws, cudaStream_t st);

@@ -5,16 +5,18 @@
 // A - F G^T is never materialised and A is read from HBM exactly once.
 //
 // Persistent, warp-specialised, one CTA per SM, tiles of 128 rows x 128 columns:
-//   warp 0   TMA producer: G_hi/G_lo column tiles (2-deep ring), A quarter tiles
-//            (128 x 32, 6-deep ring)
+//   warp 0   TMA producer of the A stream (quarter tiles of 128 x 32, 6-deep ring)
+//   warp 6   TMA producer of the G_hi/G_lo column tiles (2-deep ring), on its own
+//            thread so that a full A ring never delays the next tile's MMA operands
 //   warp 1   TMEM allocator + single-thread MMA issuer.  The row band's F_hi/F_lo
 //            live in TMEM (double-buffered across bands) and are the MMA's A operand,
 //            so every MMA reads only its 128 x 8 G slice from shared memory (an SS MMA
 //            would re-read 4 KB of F per instruction and saturate shared memory).
 //            Per 8-wide k step: D += Fh Gh^T + Fh Gl^T + Fl Gh^T (TMEM, 2 stages).
-//   warps 2-5 epilogue: write F rows into TMEM (one band ahead), tcgen05.ld the
-//            accumulator row (lane = row), read the A row from the 128B-swizzled smem
-//            tile, accumulate (a - a~)^2 and a^2 in FP32 per tile, FP64 across tiles.
+//   warps 2-5 epilogue: split F diag(s) rows into TF32 hi/lo and write them into TMEM
+//            one band ahead; per tile, tcgen05.ld the accumulator row (lane = row),
+//            read the A row from the 128B-swizzled smem box, accumulate (a - a~)^2
+//            and a^2 in FP32 per tile, FP64 across tiles.
 // Tile order is row-band major over a static contiguous tile range per CTA; fixed-order
 // block and grid reductions: bit-reproducible.  Requires ncomp <= 64.
 #include "common.cuh"
@@ -78,21 +80,49 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       : "memory");
 }
 
-// Epilogue warps: F_hi/F_lo rows of band rb -> TMEM buffer fb (row = lane quarter q * 32 + lane).
-__device__ __forceinline__ void load_f_band(const float* __restrict__ fh, const float* __restrict__ fl, int64_t m,
-                                            int64_t rb, int q, int lane, uint32_t tmem, int fb, uint64_t* ready) {
+// Epilogue warps: row r of F diag(s), split into TF32 hi + exact lo, -> TMEM buffer fb
+// (row = lane quarter q * 32 + lane; hi in columns [0, 64), lo in [64, 128)).
+struct FArgs {
+  const float* f;
+  int64_t ldf;
+  const float* s;  // may be null (scale 1)
+  int ncomp;
+  bool vec;        // f and ldf 16-byte aligned
+};
+
+__device__ __forceinline__ void load_f_band(const FArgs& F, int64_t m, int64_t rb, int q, int lane, uint32_t tmem,
+                                            int fb, uint64_t* ready) {
   const int64_t r = rb * kTcBM + q * 32 + lane;
   const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + kFCol0 + static_cast<uint32_t>(fb * 2 * kKp);
+  const float* src = F.f + (r < m ? r : 0) * F.ldf;
 #pragma unroll
-  for (int part = 0; part < 4; ++part) {  // hi cols 0-31, 32-63; lo cols 0-31, 32-63
-    const float* src = (part < 2 ? fh : fl) + r * kKp + (part & 1) * 32;
-    float v[32];
+  for (int half = 0; half < 2; ++half) {  // columns [32 half, 32 half + 32)
+    float x[32];
+    if (F.vec) {
 #pragma unroll
-    for (int c = 0; c < 32; c += 4) {
-      float4 x = r < m ? __ldg(reinterpret_cast<const float4*>(src + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      v[c] = x.x; v[c + 1] = x.y; v[c + 2] = x.z; v[c + 3] = x.w;
+      for (int c = 0; c < 32; c += 4) {
+        const int col = 32 * half + c;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < m && col < F.ncomp) v = __ldg(reinterpret_cast<const float4*>(src + col));
+        x[c] = v.x; x[c + 1] = v.y; x[c + 2] = v.z; x[c + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const int col = 32 * half + c;
+        x[c] = (r < m && col < F.ncomp) ? __ldg(src + col) : 0.f;
+      }
     }
-    tmem_st32(tq + static_cast<uint32_t>(part * 32), v);
+    float hi[32], lo[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const int col = 32 * half + c;
+      const float v = col < F.ncomp ? x[c] * (F.s ? __ldg(F.s + col) : 1.f) : 0.f;
+      hi[c] = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);  // TF32 operand bits
+      lo[c] = v - hi[c];                                            // exact
+    }
+    tmem_st32(tq + static_cast<uint32_t>(32 * half), hi);
+    tmem_st32(tq + static_cast<uint32_t>(kKp + 32 * half), lo);
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   tc::fence_before_sync();
@@ -102,8 +132,8 @@ __device__ __forceinline__ void load_f_band(const float* __restrict__ fh, const 
 
 __global__ void __launch_bounds__(kTcThreads, 1)
 residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmGh,
-                   const __grid_constant__ CUtensorMap tmGl, const float* __restrict__ fh,
-                   const float* __restrict__ fl, int64_t m, int64_t n, int ksteps, double* __restrict__ part) {
+                   const __grid_constant__ CUtensorMap tmGl, const FArgs fa, int64_t m, int64_t n, int ksteps,
+                   double* __restrict__ part) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -209,8 +239,8 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;    // row within the 128-row tile
     // F of the first two bands, then one band ahead of the MMA
-    load_f_band(fh, fl, m, rb0, q, lane, tmem, 0, &S.f_ready[0]);
-    if (nbands > 1) load_f_band(fh, fl, m, rb0 + 1, q, lane, tmem, 1, &S.f_ready[1]);
+    load_f_band(fa, m, rb0, q, lane, tmem, 0, &S.f_ready[0]);
+    if (nbands > 1) load_f_band(fa, m, rb0 + 1, q, lane, tmem, 1, &S.f_ready[1]);
     double r2 = 0.0, a2 = 0.0;
     int64_t prev_rb = rb0;
     for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
@@ -222,7 +252,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           const int fb = static_cast<int>((j + 1) & 1);
           tc::mbar_wait(&S.f_free[fb], static_cast<uint32_t>(((j - 1) >> 1) & 1));
           tc::fence_after_sync();
-          load_f_band(fh, fl, m, rb + 1, q, lane, tmem, fb, &S.f_ready[fb]);
+          load_f_band(fa, m, rb + 1, q, lane, tmem, fb, &S.f_ready[fb]);
         }
       }
       const int sc = static_cast<int>(i % kCS);
@@ -291,29 +321,16 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   }
 }
 
-// Fh = tf32(F diag(s)), Fl = F diag(s) - Fh (exact), zero-padded to kp columns; same for G.
-__global__ void split_tf32_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int ncomp,
-                                  const float* __restrict__ s, float* __restrict__ hi, float* __restrict__ lo, int kp) {
-  const int64_t total = rows * kp;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / kp;
-    const int c = static_cast<int>(e % kp);
-    float x = 0.f;
-    if (c < ncomp) x = X[r * ldx + c] * (s ? s[c] : 1.f);
-    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);  // TF32 operand bits
-    hi[e] = h;
-    if (lo) lo[e] = x - h;
-  }
-}
-
-// G copied with zero padding to kp columns (raw FP32: split inside the kernel).
-__global__ void pad_copy_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int ncomp,
-                                float* __restrict__ out, int kp) {
-  const int64_t total = rows * kp;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / kp;
-    const int c = static_cast<int>(e % kp);
-    out[e] = c < ncomp ? X[r * ldx + c] : 0.f;
+// G_hi = tf32(G), G_lo = G - G_hi (exact), zero-padded to kKp columns; 4 rows x 64 columns per
+// 256-thread block iteration (the F side is split on the fly by the epilogue warps).
+__global__ void __launch_bounds__(256) split_g_kernel(const float* __restrict__ G, int64_t ldg, int64_t rows, int ncomp,
+                                                      float* __restrict__ hi, float* __restrict__ lo) {
+  const int c = threadIdx.x & (kKp - 1);
+  for (int64_t r = blockIdx.x * 4LL + (threadIdx.x >> 6); r < rows; r += gridDim.x * 4LL) {
+    const float x = c < ncomp ? __ldg(G + r * ldg + c) : 0.f;
+    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    hi[r * kKp + c] = h;
+    lo[r * kKp + c] = x - h;
   }
 }
 
@@ -367,14 +384,11 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
                        const float* s, const float* G, int64_t ldg, int ncomp, float* split, double* part, double* out,
                        cudaStream_t st) {
   const int kp = kKp;
-  float* fh = split;
-  float* fl = fh + m_loc * kp;
-  float* gh = fl + m_loc * kp;
+  float* gh = split;
   float* gl = gh + n * kp;
   note_launch();
-  split_tf32_kernel<<<2 * kNumSM, 256, 0, st>>>(F, ldf, m_loc, ncomp, s, fh, fl, kp);
-  note_launch();
-  split_tf32_kernel<<<2 * kNumSM, 256, 0, st>>>(G, ldg, n, ncomp, nullptr, gh, gl, kp);
+  split_g_kernel<<<4 * kNumSM, 256, 0, st>>>(G, ldg, n, ncomp, gh, gl);
+  FArgs fa{F, ldf, s, ncomp, (reinterpret_cast<uintptr_t>(F) & 15) == 0 && (ldf % 4) == 0};
   CUtensorMap tA, tGh, tGl;
   if (!make_map(&tA, A, n, m_loc, lda, kTcBM) || !make_map(&tGh, gh, kp, n, kp, kTcBN) ||
       !make_map(&tGl, gl, kp, n, kp, kTcBN))
@@ -392,7 +406,7 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
   int64_t g = T < nsm ? T : nsm;
   const int ksteps = static_cast<int>(ceil_div(ncomp, 8));
   note_launch();
-  residual_tc_kernel<<<static_cast<unsigned>(g), kTcThreads, smem, st>>>(tA, tGh, tGl, fh, fl, m_loc, n, ksteps, part);
+  residual_tc_kernel<<<static_cast<unsigned>(g), kTcThreads, smem, st>>>(tA, tGh, tGl, fa, m_loc, n, ksteps, part);
   launch_residual_final(part, static_cast<int>(g), out, st);
   return 0;
 }

@@ -103,33 +103,52 @@ void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t ro
 // ---------------------------------------------------------------- multi-rank candidate exchange
 // Merge of the packed per-segment (and per-rank) lists: the global T nearest per centre,
 // ordered by (d, idx).  Lists of other ranks are zero-filled slots completed by a sum-allreduce.
-__global__ void snap_merge_kernel(const double* __restrict__ all, int k2, int T, int nranks, float* __restrict__ cand_d,
-                                  int64_t* __restrict__ cand_i) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per centre: T rounds of a warp-wide search for the lexicographic successor of
+// the previous winner over all nlists * T entries (indices are distinct across lists:
+// segments and ranks partition the points).
+__global__ void __launch_bounds__(128) snap_merge_kernel(const double* __restrict__ all, int k2, int T, int nlists,
+                                                         float* __restrict__ cand_d, int64_t* __restrict__ cand_i) {
+  const int j = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (j >= k2) return;
+  const int ne = nlists * T;
   float pd = -FLT_MAX;
-  int64_t pi = -1;  // previous winner (lists are merged by repeated lexicographic successor search)
+  int64_t pi = -1;  // previous winner
   for (int t = 0; t < T; ++t) {
     float bd = FLT_MAX;
     int64_t bi = INT64_MAX;
-    for (int r = 0; r < nranks; ++r)
-      for (int q = 0; q < T; ++q) {
-        const int64_t e = (((int64_t)r * k2 + j) * T + q) * 2;
-        const float d = static_cast<float>(all[e]);
-        const int64_t i = static_cast<int64_t>(all[e + 1]);
-        if (i < 0) continue;
-        if (lex_less(pd, pi, d, i) && lex_less(d, i, bd, bi)) { bd = d; bi = i; }
+    for (int e = lane; e < ne; e += 32) {
+      const int r = e / T, q = e - r * T;
+      const int64_t off = (((int64_t)r * k2 + j) * T + q) * 2;
+      const int64_t i = static_cast<int64_t>(all[off + 1]);
+      if (i < 0) continue;
+      const float d = static_cast<float>(all[off]);
+      if (lex_less(pd, pi, d, i) && lex_less(d, i, bd, bi)) { bd = d; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (lex_less(od, oi, bd, bi)) { bd = od; bi = oi; }
+    }
+    if (lane == 0) {
+      cand_d[(int64_t)j * T + t] = bd;
+      cand_i[(int64_t)j * T + t] = bi == INT64_MAX ? -1 : bi;
+    }
+    if (bi == INT64_MAX) {  // lists exhausted: the remaining slots stay empty
+      for (int t2 = t + 1 + lane; t2 < T; t2 += 32) {
+        cand_d[(int64_t)j * T + t2] = FLT_MAX;
+        cand_i[(int64_t)j * T + t2] = -1;
       }
-    cand_d[(int64_t)j * T + t] = bd;
-    cand_i[(int64_t)j * T + t] = bi == INT64_MAX ? -1 : bi;
+      break;
+    }
     pd = bd;
     pi = bi;
   }
 }
 
-void launch_snap_merge(const double* all, int k2, int T, int nranks, float* cand_d, int64_t* cand_i, cudaStream_t st) {
+void launch_snap_merge(const double* all, int k2, int T, int nlists, float* cand_d, int64_t* cand_i, cudaStream_t st) {
   note_launch();
-  snap_merge_kernel<<<static_cast<unsigned>(ceil_div(k2, 128)), 128, 0, st>>>(all, k2, T, nranks, cand_d, cand_i);
+  snap_merge_kernel<<<static_cast<unsigned>(ceil_div(k2, 4)), 128, 0, st>>>(all, k2, T, nlists, cand_d, cand_i);
 }
 
 // ---------------------------------------------------------------- greedy dedupe (one CTA)

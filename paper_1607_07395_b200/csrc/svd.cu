@@ -18,9 +18,6 @@ constexpr int kSvdThreads = 1024;
 constexpr int kSvdMaxSweeps = 60;
 constexpr int kSvdSmemK = 112;
 
-#ifdef CABS_PROFILE_SVD
-__device__ long long g_svd_prof[8];
-#endif
 
 // Circle-method tournament: player 0 fixed, the others rotate by one seat per round.
 // 0 <= j - 1 + r < 2 (np - 1), so the modulo is one conditional subtraction.
@@ -30,6 +27,62 @@ __device__ __forceinline__ int rr_player(int j, int r, int np) {
   return j == 0 ? 0 : 1 + x;
 }
 
+
+// Jacobi rotation for the pair (x, y) with al = x.x, be = y.y, ga = x.y:
+// t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2 ga), evaluated in FP32
+// on operands scaled by an exact power of two (exponent arithmetic on the bits): t's
+// accuracy only sets the convergence rate.  c = 1/sqrt(1+t^2) to FP64 accuracy (FP32
+// seed + two Newton steps) and s = c t keep the rotation orthogonal to FP64 rounding.
+// Returns t == 0 (c = 1, s = 0) when the pair is already orthogonal to tol_rot.
+__device__ __forceinline__ float jacobi_angle(double al, double be, double ga, double tol_rot2, double& c,
+                                              double& sn) {
+  const bool need = ga != 0.0 && ga * ga > tol_rot2 * al * be;
+  const double dx = be - al, dy = 2.0 * ga;
+  const double mx = fmax(fabs(dx), fabs(dy));
+  const int ex = static_cast<int>((__double_as_longlong(mx) >> 52) & 0x7ff);
+  const double scl = __longlong_as_double(static_cast<long long>(2046 - ex) << 52);
+  const float xf = static_cast<float>(dx * scl), yf = static_cast<float>(dy * scl);
+  const float hyp = fmaf(xf, xf, yf * yf);
+  const float den = fabsf(xf) + hyp * __frsqrt_rn(hyp);
+  float tf = copysignf(1.f, xf) * __fdividef(yf, den);
+  tf = (need && ex > 0 && ex < 2046 && den > 0.f) ? tf : 0.f;
+  const double t = static_cast<double>(tf);
+  const double q1 = fma(t, t, 1.0);
+  double cc = static_cast<double>(__frsqrt_rn(static_cast<float>(q1)));
+  cc = cc * fma(-0.5 * q1, cc * cc, 1.5);
+  cc = cc * fma(-0.5 * q1, cc * cc, 1.5);
+  c = cc;
+  sn = cc * t;
+  return tf;
+}
+
+// The same rotation with FP64 approximate reciprocal / rsqrt (MUFU) for t: inputs are
+// squares of FP32-born data, so dx^2 + dy^2 cannot overflow FP64.  Returns "rotated".
+__device__ __forceinline__ double rsqrt_approx64(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+__device__ __forceinline__ double rcp_approx64(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+__device__ __forceinline__ bool jacobi_angle_fast(double al, double be, double ga, double tol_rot2, double& c,
+                                                  double& sn) {
+  const bool need = ga != 0.0 && ga * ga > tol_rot2 * al * be;
+  const double dx = be - al, dy = 2.0 * ga;
+  const double h = fma(dx, dx, dy * dy);
+  const double den = fabs(dx) + h * rsqrt_approx64(h);      // |dx| + sqrt(dx^2 + dy^2)
+  const double t = need ? copysign(1.0, dx) * dy * rcp_approx64(den) : 0.0;
+  const double q1 = fma(t, t, 1.0);
+  double cc = rsqrt_approx64(q1);
+  cc = cc * fma(-0.5 * q1, cc * cc, 1.5);
+  cc = cc * fma(-0.5 * q1, cc * cc, 1.5);
+  c = cc;
+  sn = cc * t;
+  return need;
+}
 
 // Cyclic one-sided Jacobi sweeps until no pair needs a rotation (or the sweep cap).
 // A group of LP lanes (LP | 32) runs one column pair, each lane holding E = ceil(k/LP)
@@ -89,26 +142,8 @@ __device__ int jacobi_sweeps(double* A, int k) {
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        // t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2 ga), evaluated in FP32
-        // on operands scaled by an exact power of two (exponent arithmetic on the bits): t's
-        // accuracy only sets the convergence rate.  c = 1/sqrt(1+t^2) to FP64 accuracy (FP32
-        // seed + two Newton steps) and s = c t keep the rotation orthogonal to FP64 rounding.
-        const bool need = ga != 0.0 && ga * ga > tol_rot2 * al * be;
-        const double dx = be - al, dy = 2.0 * ga;
-        const double mx = fmax(fabs(dx), fabs(dy));
-        const int ex = static_cast<int>((__double_as_longlong(mx) >> 52) & 0x7ff);  // biased exponent
-        const double scl = __longlong_as_double(static_cast<long long>(2046 - ex) << 52);  // 2^(1023-(ex-1023))
-        const float xf = static_cast<float>(dx * scl), yf = static_cast<float>(dy * scl);
-        const float hyp = fmaf(xf, xf, yf * yf);
-        const float den = fabsf(xf) + hyp * __frsqrt_rn(hyp);  // |x| + sqrt(x^2 + y^2)
-        float tf = copysignf(1.f, xf) * __fdividef(yf, den);
-        tf = (need && ex > 0 && ex < 2046 && den > 0.f) ? tf : 0.f;
-        const double t = static_cast<double>(tf);
-        const double q1 = fma(t, t, 1.0);
-        double c = static_cast<double>(__frsqrt_rn(static_cast<float>(q1)));
-        c = c * fma(-0.5 * q1, c * c, 1.5);
-        c = c * fma(-0.5 * q1, c * c, 1.5);
-        const double sn = c * t;
+        double c, sn;
+        const float tf = jacobi_angle(al, be, ga, tol_rot2, c, sn);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const int i = gl + LP * e;
@@ -127,6 +162,276 @@ __device__ int jacobi_sweeps(double* A, int k) {
 }
 
 
+// ---------------------------------------------------------------- shared epilogue
+// Singular values = column norms of the converged A; rank order descending (ties -> lower
+// column); truncation count r = #{sigma_i > tol sigma_1} (Z4).  Ends with a barrier.
+__device__ int svd_sigma(const double* A, int k, double tol, double* s_sig, int* s_perm, double* sigma_out,
+                         int* r_out, int* r_out2) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  for (int c = warp; c < k; c += nwarps) {
+    const double* ac = A + (size_t)c * k;
+    double ss = 0;
+    for (int i = lane; i < k; i += 32) ss = fma(ac[i], ac[i], ss);
+    ss = warp_sum_d(ss);
+    if (lane == 0) s_sig[c] = sqrt(ss);
+  }
+  __syncthreads();
+  for (int c = tid; c < k; c += blockDim.x) {
+    const double sc = s_sig[c];
+    int rk = 0;
+    for (int j = 0; j < k; ++j) {
+      const double sj = s_sig[j];
+      rk += (sj > sc) || (sj == sc && j < c);
+    }
+    s_perm[rk] = c;
+  }
+  __syncthreads();
+  const double smax = s_sig[s_perm[0]];
+  int r = 0;
+  if (smax > 0) {
+    for (int j = 0; j < k; ++j) r += s_sig[j] > tol * smax;
+  }
+  if (tid == 0) {
+    if (r_out) *r_out = r;
+    if (r_out2) *r_out2 = r;
+  }
+  for (int j = tid; j < k; j += blockDim.x) {
+    if (sigma_out) sigma_out[j] = s_sig[s_perm[j]];
+  }
+  return r;
+}
+
+// U_w = a_c / sigma_c and V_w in rank order, canonical sign (Z5: the largest-|.| entry of
+// each U_w column positive, lowest index on ties); dropped components written as zeros.
+__device__ void svd_write(const double* A, const double* V, int k, int r, const double* s_sig, const int* s_perm,
+                          double* __restrict__ Uw64, double* __restrict__ Vw64, float* __restrict__ uw32,
+                          float* __restrict__ vw32, int64_t ld32) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  for (int j = warp; j < k; j += nwarps) {
+    const int c = s_perm[j];
+    const double sg = s_sig[c];
+    const bool keep = j < r;
+    const double* ac = A + (size_t)c * k;
+    const double* vc = V + (size_t)c * k;
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = lane; i < k; i += 32) {
+      const double v = fabs(ac[i]);
+      if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const double sign = (bi < k && ac[bi] < 0) ? -1.0 : 1.0;
+    const double inv = (keep && sg > 0) ? sign / sg : 0.0;
+    const double vs = keep ? sign : 0.0;
+    for (int i = lane; i < k; i += 32) {
+      const double u = ac[i] * inv, v = vc[i] * vs;
+      if (Uw64) Uw64[(size_t)i * k + j] = u;
+      if (Vw64) Vw64[(size_t)i * k + j] = v;
+      if (uw32) uw32[(size_t)i * ld32 + j] = static_cast<float>(u);
+      if (vw32) vw32[(size_t)i * ld32 + j] = static_cast<float>(v);
+    }
+  }
+  if (uw32) {  // zero padding columns [k, ld32)
+    for (int64_t e = tid; e < (int64_t)k * (ld32 - k); e += blockDim.x) {
+      const int64_t i = e / (ld32 - k), c = k + e % (ld32 - k);
+      uw32[i * ld32 + c] = 0.f;
+      vw32[i * ld32 + c] = 0.f;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- k <= 64: register-resident, odd-even
+// Each pair slot g (a group of LP lanes; lane l holds rows l + LP e, e < E) keeps the
+// columns at positions 2g (L) and 2g+1 (R) of A AND of V in registers.  Ordering: the
+// odd-even transposition network (every round swaps the columns of each active pair, so
+// after n = 2P rounds every pair has met exactly once):
+//   even rounds  pairs (2g, 2g+1): inside the slot, no data movement, no barrier;
+//   odd rounds   pairs (2g+1, 2g+2): each slot publishes L and R through shared memory
+//                (double-buffered by odd-round parity), ONE barrier, then computes both
+//                pairs it takes part in (bit-identical to its neighbours' copies) and
+//                keeps its own rotated halves.  Idle ends (positions 0 and n-1) use the
+//                rotation (c, s) = (0, -/+1), which with the swap leaves them in place.
+// Rotations are accumulated into V on the way, so V is orthogonal to FP64 rounding
+// without a Gram-Schmidt pass.
+template <int E>
+__device__ __forceinline__ void pair_dots(const double (&x)[E], const double (&y)[E], double& al, double& be,
+                                          double& ga) {
+  double al0 = 0, be0 = 0, ga0 = 0, al1 = 0, be1 = 0, ga1 = 0;
+#pragma unroll
+  for (int e = 0; e < E; e += 2) {
+    al0 = fma(x[e], x[e], al0);
+    be0 = fma(y[e], y[e], be0);
+    ga0 = fma(x[e], y[e], ga0);
+    if (e + 1 < E) {
+      al1 = fma(x[e + 1], x[e + 1], al1);
+      be1 = fma(y[e + 1], y[e + 1], be1);
+      ga1 = fma(x[e + 1], y[e + 1], ga1);
+    }
+  }
+  al = al0 + al1;
+  be = be0 + be1;
+  ga = ga0 + ga1;
+}
+
+template <int LP>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = LP / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int LP, int E>
+__global__ void __launch_bounds__(128, 1)
+svd_systolic_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, double* __restrict__ sigma_out,
+                    double* __restrict__ Uw64, double* __restrict__ Vw64, float* __restrict__ uw32,
+                    float* __restrict__ vw32, int64_t ld32, int* r_out, int* r_out2, void* ws) {
+  constexpr int G = 32 / LP;        // pair slots per warp
+  // doubles per published column, padded so that consecutive seats start 32 bytes apart
+  // modulo 128 (the 8 slots of a warp then cover the 32 banks twice: conflict-free)
+  constexpr int SEAT = E * LP + ((4 - (E * LP) % 16) + 16) % 16;
+  extern __shared__ __align__(16) double smem_d[];
+  __shared__ double s_sig[64];
+  __shared__ int s_perm[64];
+  __shared__ int s_id[2][2][34];    // [parity][L|R][seat]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int gl = lane % LP, gw = lane / LP;
+  const int g = warp * G + gw;
+  const int np = (k + 1) & ~1, P = np / 2;
+  const int nseat = nw * G + 2;     // seat g + 1 <- slot g; seats 0 and nw G + 1 stay zero
+  const bool live = g < P;
+  // published columns: [parity][seat][e][LP] for A_L, A_R, V_L, V_R
+  const size_t arr = (size_t)2 * nseat * SEAT;
+  double* bAL = smem_d;
+  double* bAR = bAL + arr;
+  double* bVL = bAR + arr;
+  double* bVR = bVL + arr;
+  for (int e = tid; e < 4 * (int)arr; e += blockDim.x) smem_d[e] = 0.0;
+
+  double aL[E], aR[E], vL[E], vR[E];
+  int idL = 2 * g, idR = 2 * g + 1;  // column ids (>= k: dummy zero column)
+  bool bad = false;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = gl + LP * e;
+    float wl = 0.f, wr = 0.f;
+    if (live && i < k && idL < k) wl = W[(int64_t)i * ldw + idL];
+    if (live && i < k && idR < k) wr = W[(int64_t)i * ldw + idR];
+    bad |= !isfinite(wl) || !isfinite(wr);
+    aL[e] = wl;
+    aR[e] = wr;
+    vL[e] = (i == idL && idL < k) ? 1.0 : 0.0;
+    vR[e] = (i == idR && idR < k) ? 1.0 : 0.0;
+  }
+  if (bad) set_status(ws, CABS_DEV_NONFINITE);
+  __syncthreads();
+  const double tol_rot = 2.0 * sqrt(static_cast<double>(k)) * DBL_EPSILON;
+  const double tol_rot2 = tol_rot * tol_rot;
+  const bool left_edge = g == 0, right_edge = g == P - 1;
+  int sweep = 0;
+  if (k > 1) {
+    for (; sweep < kSvdMaxSweeps; ++sweep) {
+      int rotated = 0;
+      for (int rnd = 0; rnd < np; ++rnd) {
+        if ((rnd & 1) == 0) {
+          // ---- even round: pair (L, R) of this slot; rotate and swap
+          double al, be, ga, c, sn;
+          pair_dots<E>(aL, aR, al, be, ga);
+          al = group_sum<LP>(al);
+          be = group_sum<LP>(be);
+          ga = group_sum<LP>(ga);
+          rotated |= jacobi_angle_fast(al, be, ga, tol_rot2, c, sn) && live;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const double x = aL[e], y = aR[e], vx = vL[e], vy = vR[e];
+            aL[e] = sn * x + c * y;  // position 2g <- y'
+            aR[e] = c * x - sn * y;  // position 2g+1 <- x'
+            vL[e] = sn * vx + c * vy;
+            vR[e] = c * vx - sn * vy;
+          }
+          const int t = idL;
+          idL = idR;
+          idR = t;
+          continue;
+        }
+        // ---- odd round: publish, barrier, pairs (R_{g-1}, L_g) and (R_g, L_{g+1})
+        const int par = (rnd >> 1) & 1;
+        const size_t pub = ((size_t)par * nseat + g + 1) * SEAT + gl;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          bAL[pub + e * LP] = aL[e];
+          bAR[pub + e * LP] = aR[e];
+          bVL[pub + e * LP] = vL[e];
+          bVR[pub + e * LP] = vR[e];
+        }
+        if (gl == 0) {
+          s_id[par][0][g + 1] = idL;
+          s_id[par][1][g + 1] = idR;
+        }
+        __syncthreads();
+        const size_t lft = ((size_t)par * nseat + g) * SEAT + gl;      // slot g - 1 (seat 0: zeros)
+        const size_t rgt = ((size_t)par * nseat + g + 2) * SEAT + gl;  // slot g + 1
+        double rm[E], lp[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          rm[e] = bAR[lft + e * LP];
+          lp[e] = bAL[rgt + e * LP];
+        }
+        double alA, beA, gaA, alB, beB, gaB, cA, sA, cB, sB;
+        pair_dots<E>(rm, aL, alA, beA, gaA);
+        pair_dots<E>(aR, lp, alB, beB, gaB);
+        alA = group_sum<LP>(alA);
+        beA = group_sum<LP>(beA);
+        gaA = group_sum<LP>(gaA);
+        alB = group_sum<LP>(alB);
+        beB = group_sum<LP>(beB);
+        gaB = group_sum<LP>(gaB);
+        const bool rA = jacobi_angle_fast(alA, beA, gaA, tol_rot2, cA, sA);
+        const bool rB = jacobi_angle_fast(alB, beB, gaB, tol_rot2, cB, sB);
+        rotated |= live && ((rA && !left_edge) || (rB && !right_edge));
+        if (left_edge) { cA = 0.0; sA = -1.0; }
+        if (right_edge) { cB = 0.0; sB = 1.0; }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const double vm = bVR[lft + e * LP], vp = bVL[rgt + e * LP];
+          aL[e] = cA * rm[e] - sA * aL[e];  // x' of the left pair
+          aR[e] = sB * aR[e] + cB * lp[e];  // y' of the right pair
+          vL[e] = cA * vm - sA * vL[e];
+          vR[e] = sB * vR[e] + cB * vp;
+        }
+        if (!left_edge) idL = s_id[par][1][g];
+        if (!right_edge) idR = s_id[par][0][g + 2];
+      }
+      rotated = __syncthreads_or(rotated);
+      if (!rotated) break;
+    }
+    if (sweep == kSvdMaxSweeps && tid == 0) set_status(ws, CABS_DEV_SVD_NOCONV);
+  }
+  if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;  // diagnostics: sweeps of the last SVD
+  __syncthreads();
+  // ---- converged columns -> shared memory (column-major by original column id)
+  double* As = smem_d;
+  double* Vs = smem_d + (size_t)k * k;
+  if (live) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = gl + LP * e;
+      if (i < k) {
+        if (idL < k) { As[(size_t)idL * k + i] = aL[e]; Vs[(size_t)idL * k + i] = vL[e]; }
+        if (idR < k) { As[(size_t)idR * k + i] = aR[e]; Vs[(size_t)idR * k + i] = vR[e]; }
+      }
+    }
+  }
+  __syncthreads();
+  const int r = svd_sigma(As, k, tol, s_sig, s_perm, sigma_out, r_out, r_out2);
+  svd_write(As, Vs, k, r, s_sig, s_perm, Uw64, Vw64, uw32, vw32, ld32);
+}
+
+// ---------------------------------------------------------------- k > 64: columns in memory
 template <int L, bool SMEM>
 __global__ void __launch_bounds__(kSvdThreads, 1)
 svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, double* gA, double* gV,
@@ -134,7 +439,6 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
                   float* __restrict__ uw32, float* __restrict__ vw32, int64_t ld32, int* r_out, int* r_out2,
                   bool use_smem, void* ws) {
   extern __shared__ __align__(16) double smem_d[];
-  __shared__ int s_rot;
   __shared__ double s_sig[CABS_KMAX];
   __shared__ int s_perm[CABS_KMAX];  // s_perm[rank] = column
   __shared__ double s_h[CABS_KMAX];  // Gram-Schmidt coefficients
@@ -158,45 +462,12 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
     // while k <= 256, so small k packs several pairs into each warp
     sweep = jacobi_sweeps<(L <= 1 ? 4 : L == 2 ? 8 : L == 4 ? 16 : 32), (L <= 4 ? 8 : L)>(A, k);
     if (sweep == kSvdMaxSweeps && tid == 0) set_status(ws, CABS_DEV_SVD_NOCONV);
-    if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;  // diagnostics: sweeps of the last SVD
-#ifdef CABS_PROFILE_SVD
-    if (tid == 0)
-      for (int i = 0; i < 5; ++i) reinterpret_cast<long long*>(ws)[8 + i] = g_svd_prof[i];
-#endif
   }
+  if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;
 
-  // singular values = column norms
-  for (int c = warp; c < k; c += nwarps) {
-    const double* ac = A + (size_t)c * k;
-    double ss = 0;
-    for (int i = lane; i < k; i += 32) ss = fma(ac[i], ac[i], ss);
-    ss = warp_sum_d(ss);
-    if (lane == 0) s_sig[c] = sqrt(ss);
-  }
-  __syncthreads();
-  // descending rank, ties -> lower column first
-  for (int c = tid; c < k; c += blockDim.x) {
-    double sc = s_sig[c];
-    int rk = 0;
-    for (int j = 0; j < k; ++j) {
-      double sj = s_sig[j];
-      rk += (sj > sc) || (sj == sc && j < c);
-    }
-    s_perm[rk] = c;
-  }
+  const int r = svd_sigma(A, k, tol, s_sig, s_perm, sigma_out, r_out, r_out2);
   __syncthreads();
   const double smax = s_sig[s_perm[0]];
-  int r = 0;
-  if (smax > 0) {
-    for (int j = 0; j < k; ++j) r += s_sig[j] > tol * smax;
-  }
-  if (tid == 0) {
-    if (r_out) *r_out = r;
-    if (r_out2) *r_out2 = r;
-  }
-  for (int j = tid; j < k; j += blockDim.x) {
-    if (sigma_out) sigma_out[j] = s_sig[s_perm[j]];
-  }
   // Right singular vectors without accumulating the rotations (which would double the
   // shared-memory traffic of every round): W^T W V = V S^2 and A = W V = U S give
   // v_c = W^T a_c / sigma_c^2 for the kept components, then two passes of classical
@@ -243,70 +514,59 @@ svd_jacobi_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, d
     for (int e = lane; e < k; e += 32) vj[e] *= inv;
   }
   __syncthreads();
-  // write U_w, V_w columns in rank order with canonical sign
-  for (int j = warp; j < k; j += nwarps) {
-    const int c = s_perm[j];
-    const double sg = s_sig[c];
-    const bool keep = j < r;
-    const double* ac = A + (size_t)c * k;
-    const double* vc = V + (size_t)c * k;
-    // argmax |a_c| (lowest index on ties)
-    double best = -1.0;
-    int bi = 0x7fffffff;
-    for (int i = lane; i < k; i += 32) {
-      double v = fabs(ac[i]);
-      if (v > best || (v == best && i < bi)) { best = v; bi = i; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    const double sign = (bi < k && ac[bi] < 0) ? -1.0 : 1.0;
-    const double inv = (keep && sg > 0) ? sign / sg : 0.0;
-    const double vs = keep ? sign : 0.0;
-    for (int i = lane; i < k; i += 32) {
-      double u = ac[i] * inv, v = vc[i] * vs;
-      if (Uw64) Uw64[(size_t)i * k + j] = u;
-      if (Vw64) Vw64[(size_t)i * k + j] = v;
-      if (uw32) uw32[(size_t)i * ld32 + j] = static_cast<float>(u);
-      if (vw32) vw32[(size_t)i * ld32 + j] = static_cast<float>(v);
-    }
+  svd_write(A, V, k, r, s_sig, s_perm, Uw64, Vw64, uw32, vw32, ld32);
+}
+
+template <int LP, int E>
+static void launch_systolic(int k, const float* W, int64_t ldw, double tol, double* sig, double* Uw64, double* Vw64,
+                            float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st) {
+  constexpr int G = 32 / LP;
+  const int P = ((k + 1) & ~1) / 2;
+  const int nw = (P + G - 1) / G;
+  constexpr int SEAT = E * LP + ((4 - (E * LP) % 16) + 16) % 16;
+  const size_t seats = sizeof(double) * 4 * 2 * (size_t)(nw * G + 2) * SEAT;  // [AL|AR|VL|VR][parity][seat]
+  const size_t fin = sizeof(double) * 2 * (size_t)k * k;
+  const size_t smem = seats > fin ? seats : fin;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(svd_systolic_kernel<LP, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
   }
-  // zero padding columns [k, ld32)
-  if (uw32) {
-    for (int64_t e = tid; e < (int64_t)k * (ld32 - k); e += blockDim.x) {
-      int64_t i = e / (ld32 - k), c = k + e % (ld32 - k);
-      uw32[i * ld32 + c] = 0.f;
-      vw32[i * ld32 + c] = 0.f;
-    }
-  }
+  svd_systolic_kernel<LP, E><<<1, 32 * nw, smem, st>>>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws,
+                                                      r_user, ws);
 }
 
 int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const Ws& L, double* sigma_user,
                double* Uw64, double* Vw64, int* r_user, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    const int smax = 2 * kSvdSmemK * kSvdSmemK * 8;
-    cudaFuncSetAttribute(svd_jacobi_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-    cudaFuncSetAttribute(svd_jacobi_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-    cudaFuncSetAttribute(svd_jacobi_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
-    attr_set = true;
-  }
-  const bool use_smem = k <= kSvdSmemK;
-  size_t smem = use_smem ? 2 * (size_t)k * k * sizeof(double) : 0;
   double* sig = sigma_user ? sigma_user : wsp<double>(ws, L.sig64);
   int* r_ws = wsp<int>(ws, L.scal) + SCAL_R_TMP;
-  auto kern = k <= 32 ? svd_jacobi_kernel<1, true> : k <= 64 ? svd_jacobi_kernel<2, true>
-            : k <= kSvdSmemK ? svd_jacobi_kernel<4, true> : k <= 128 ? svd_jacobi_kernel<4, false>
-            : k <= 256 ? svd_jacobi_kernel<8, false> : k <= 320 ? svd_jacobi_kernel<10, false>
-                       : svd_jacobi_kernel<32, false>;
+  float* uw32 = wsp<float>(ws, L.uw32);
+  float* vw32 = wsp<float>(ws, L.vw32);
   note_launch();
-  int nthreads = kSvdThreads;
-  if (const char* e = getenv("CABS_SVD_THREADS")) nthreads = atoi(e);  // experiments only
-  kern<<<1, nthreads, smem, st>>>(k, W, ldw, tol, wsp<double>(ws, L.a64), wsp<double>(ws, L.v64), sig, Uw64, Vw64,
-                                     wsp<float>(ws, L.uw32), wsp<float>(ws, L.vw32), L.Kp, r_ws, r_user, use_smem, ws);
+  if (k <= 64 && !getenv("CABS_SVD_SMEM")) {
+    // register-resident systolic Jacobi, 4 lanes per column pair
+    if (k <= 16) launch_systolic<4, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    else if (k <= 32) launch_systolic<4, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    else if (k <= 52) launch_systolic<4, 13>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    else launch_systolic<4, 16>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+  } else {
+    static bool attr_set = false;
+    if (!attr_set) {
+      const int smax = 2 * kSvdSmemK * kSvdSmemK * 8;
+      cudaFuncSetAttribute(svd_jacobi_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+      cudaFuncSetAttribute(svd_jacobi_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+      cudaFuncSetAttribute(svd_jacobi_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+      attr_set = true;
+    }
+    const bool use_smem = k <= kSvdSmemK;
+    const size_t smem = use_smem ? 2 * (size_t)k * k * sizeof(double) : 0;
+    auto kern = k <= 32 ? svd_jacobi_kernel<1, true> : k <= 64 ? svd_jacobi_kernel<2, true>
+              : k <= kSvdSmemK ? svd_jacobi_kernel<4, true> : k <= 128 ? svd_jacobi_kernel<4, false>
+              : k <= 256 ? svd_jacobi_kernel<8, false> : k <= 320 ? svd_jacobi_kernel<10, false>
+                         : svd_jacobi_kernel<32, false>;
+    kern<<<1, kSvdThreads, smem, st>>>(k, W, ldw, tol, wsp<double>(ws, L.a64), wsp<double>(ws, L.v64), sig, Uw64, Vw64,
+                                       uw32, vw32, L.Kp, r_ws, r_user, use_smem, ws);
+  }
   if (sigma_user && sigma_user != wsp<double>(ws, L.sig64)) {
     cudaMemcpyAsync(wsp<double>(ws, L.sig64), sigma_user, sizeof(double) * k, cudaMemcpyDeviceToDevice, st);
   }

@@ -10,12 +10,17 @@ from paper_1607_07395_b200 import cabs as C  # noqa: E402
 from paper_1607_07395_b200.dist import make_plan  # noqa: E402
 
 
-def probe_svd(k=50, reps=5):
+def probe_svd(k=50, reps=5, graded=False):
     dev = torch.device("cuda:0")
     plan = make_plan(1000, 1000, k)
     ws = torch.zeros(C.cabs_workspace_bytes(plan), dtype=torch.uint8, device=dev)
     g = np.random.default_rng(0)
-    W = torch.from_numpy(g.standard_normal((k, k)).astype(np.float32)).to(dev)
+    Wn = g.standard_normal((k, k))
+    if graded:  # singular values i^-1.5 plus 1e-3 noise, like W gathered from the c2 matrix
+        Q1, _ = np.linalg.qr(g.standard_normal((k, k)))
+        Q2, _ = np.linalg.qr(g.standard_normal((k, k)))
+        Wn = (Q1 * np.arange(1, k + 1) ** -1.5) @ Q2.T + 1e-3 * Wn
+    W = torch.from_numpy(Wn.astype(np.float32)).to(dev)
     sig = torch.zeros(k, dtype=torch.float64, device=dev)
     U = torch.zeros((k, k), dtype=torch.float64, device=dev)
     V = torch.zeros_like(U)
@@ -29,7 +34,13 @@ def probe_svd(k=50, reps=5):
     e1.record()
     torch.cuda.synchronize()
     sweeps = int(ws[32:36].view(torch.int32).item())
-    print(f"svd k={k}: {e0.elapsed_time(e1) / reps * 1e3:.1f} us/call, sweeps={sweeps}, r={int(r.item())}")
+    Wd = W.double().cpu().numpy()
+    sv = np.linalg.svd(Wd, compute_uv=False)
+    Uh, Vh, sh = U.cpu().numpy(), V.cpu().numpy(), sig.cpu().numpy()
+    rec = np.linalg.norm(Uh * sh @ Vh.T - Wd) / np.linalg.norm(Wd)
+    orth = max(np.abs(Uh.T @ Uh - np.eye(k)).max(), np.abs(Vh.T @ Vh - np.eye(k)).max())
+    print(f"svd k={k}{' graded' if graded else ''}: {e0.elapsed_time(e1) / reps * 1e3:.1f} us/call, sweeps={sweeps}, "
+          f"r={int(r.item())}, sigma rel err {np.abs(sh - sv).max() / sv[0]:.1e}, recon {rec:.1e}, orth {orth:.1e}")
 
 
 def probe_residual(m=20000, n=10000, k=50, reps=5):
@@ -59,8 +70,10 @@ def probe_residual(m=20000, n=10000, k=50, reps=5):
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("svd", "all"):
-        for k in (20, 50, 100, 200):
+        for k in (2, 3, 16, 20, 33, 50, 64, 100, 200):
             probe_svd(k)
+        for k in (20, 50, 64):
+            probe_svd(k, graded=True)
     if what in ("residual", "all"):
         for (m, n, k) in ((20000, 10000, 50), (2000, 1500, 20), (20000, 10000, 64), (4097, 3001, 33)):
             probe_residual(m, n, k)
