@@ -260,7 +260,8 @@ int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   float* w = wsp<float>(ws, L.km_w);
   int* cnt = wsp<int>(ws, L.km_cnt);
   CABS_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * 4, st));
-  launch_km_weights(X, ldx, n_loc, d, weight_kind, weight_p, w, cnt, st);
+  unsigned* bounds = reinterpret_cast<unsigned*>(cnt + 2);  // max|x|, max w (zeroed above)
+  launch_km_weights(X, ldx, n_loc, d, weight_kind, weight_p, w, cnt, bounds, st);
   CABS_LAUNCH_CHECK("km_weights");
   // initial centres
   const int64_t* idx = init_idx;
@@ -276,7 +277,8 @@ int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   const char* path = getenv("CABS_KMEANS_PATH");  // "loop" forces the per-iteration kernels (tests)
   const bool allow_persistent = !(path && strcmp(path, "loop") == 0);
   if (allow_persistent && !multi(comm) && n_loc > 0 &&
-      launch_lloyd_persistent(X, ldx, n_loc, d, k2, iters, w, centres, ldc, labels, objective, near_ties, cluster_w,
+      launch_lloyd_persistent(X, ldx, n_loc, d, k2, iters, w, bounds, centres, ldc, labels, objective, near_ties,
+                              cluster_w,
                               wsp<float>(ws, L.km_psum), sizeof(float) * (size_t)kAccGrid * L.K * L.Kp,
                               reinterpret_cast<long long*>(ws) + 8, st)) {
     CABS_LAUNCH_CHECK("lloyd_persistent");
@@ -285,16 +287,18 @@ int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   cudaGetLastError();  // a refused cooperative launch is not an error: use the per-iteration kernels
   double* red = wsp<double>(ws, L.km_red);
   const int64_t payload = (int64_t)k2 * d + k2 + 2;
+  long long* fsum = wsp<long long>(ws, L.km_psum);  // exact int64 sums (km_fixed.cuh), re-zeroed by km_reduce
+  long long* fwt = fsum + (int64_t)k2 * d;
+  CABS_CUDA_TRY(cudaMemsetAsync(fsum, 0, sizeof(long long) * ((int64_t)k2 * d + k2), st));
   for (int t = 0; t < iters; ++t) {
-    int ga = 1, gacc = 1;
+    int ga = 1;
     if (n_loc > 0) {
       launch_km_assign(X, ldx, n_loc, d, centres, ldc, k2, w, labels, wsp<double>(ws, L.km_pobj),
                        wsp<int>(ws, L.km_ptie), &ga, st);
-      launch_km_accum(X, ldx, n_loc, d, labels, w, k2, wsp<float>(ws, L.km_psum), wsp<double>(ws, L.km_pw), L.Kp, &gacc,
-                      st);
+      launch_km_accum(X, ldx, n_loc, d, labels, w, bounds, fsum, fwt, st);
       CABS_LAUNCH_CHECK("km_assign/accum");
-      launch_km_reduce(wsp<float>(ws, L.km_psum), wsp<double>(ws, L.km_pw), gacc, k2, d, L.Kp,
-                       wsp<double>(ws, L.km_pobj), wsp<int>(ws, L.km_ptie), ga, red, st);
+      launch_km_reduce(fsum, fwt, bounds, n_loc, k2, d, wsp<double>(ws, L.km_pobj), wsp<int>(ws, L.km_ptie), ga, red,
+                       st);
     } else {
       CABS_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(double) * payload, st));
     }

@@ -32,24 +32,24 @@ int launch_scale_compact(float* Y, int64_t ldy, int64_t N, int k, int which, voi
 
 // kmeans.cu
 void launch_km_weights(const float* X, int64_t ldx, int64_t N, int d, int kind, float p, float* w, int* cnt,
-                       cudaStream_t st);
+                       unsigned* bounds, cudaStream_t st);
 void launch_km_init(const float* X, int64_t ldx, int64_t n_loc, int64_t row_off, int d, int k2, const int64_t* idx,
                     const float* init_c, int64_t ldic, float* centres, int64_t ldc, cudaStream_t st);
 void launch_km_assign(const float* X, int64_t ldx, int64_t N, int d, const float* centres, int64_t ldc, int k2,
                       const float* w, int* labels, double* pobj, int* ptie, int* grid_out, cudaStream_t st);
 void launch_km_distmat(const float* X, int64_t ldx, int64_t N, int d, const float* centres, int64_t ldc, int k2,
                        float* D, int64_t ldd, cudaStream_t st);
-void launch_km_accum(const float* X, int64_t ldx, int64_t N, int d, const int* labels, const float* w, int k2,
-                     float* psum, double* pw, int64_t ldps, int* grid_out, cudaStream_t st);
-void launch_km_reduce(const float* psum, const double* pw, int G, int k2, int d, int64_t ldps, const double* pobj,
-                      const int* ptie, int Gobj, double* red, cudaStream_t st);
+void launch_km_accum(const float* X, int64_t ldx, int64_t N, int d, const int* labels, const float* w,
+                     const unsigned* bounds, long long* fsum, long long* fw, cudaStream_t st);
+void launch_km_reduce(long long* fsum, long long* fw, const unsigned* bounds, int64_t N, int k2, int d,
+                      const double* pobj, const int* ptie, int Gobj, double* red, cudaStream_t st);
 void launch_km_finalize(const double* red, int k2, int d, float* centres, int64_t ldc, double* objective,
                         int* near_ties, double* cluster_w, int t, cudaStream_t st);
 
 // lloyd.cu (single-GPU persistent Lloyd loop; false -> use the per-iteration kernels)
 bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int k2, int iters, const float* w,
-                             float* centres, int64_t ldc, int* labels, double* objective, int* near_ties,
-                             double* cluster_w, void* scratch, size_t scratch_bytes, long long* prof,
+                             const unsigned* bounds, float* centres, int64_t ldc, int* labels, double* objective,
+                             int* near_ties, double* cluster_w, void* scratch, size_t scratch_bytes, long long* prof,
                              cudaStream_t st);
 
 // select.cu

@@ -3,32 +3,38 @@
 // assign : s(l) = argmin_j ||X_l - c_j||^2 by DIRECT differences in FP32 (SURVEY F3:
 //          the expanded form flips labels on clustered data), lowest j on ties;
 //          objective partial sum_l w_l d_min in FP64 per CTA; near-tie count.
-// accum  : deterministic dimension-owned segmented reduction of w_l X_l by label
-//          into per-CTA partial sums (no atomics, fixed order).
-// reduce : fixed-order FP64 sum of the per-CTA partials -> one payload
-//          [k2*d sums | k2 weights | objective | near ties]  (the allreduce buffer).
+// accum  : exact int64 fixed-point sums of w_l X_l and w_l by label (km_fixed.cuh):
+//          order-free, so identical to the persistent kernel (lloyd.cu).
+// reduce : sums / 2^S -> one FP64 payload [k2*d sums | k2 weights | objective | near
+//          ties] (the allreduce buffer); the integer sums are re-zeroed for the next pass.
 // finalize: c_j = sums_j / weight_j, empty clusters keep their centre (Z12).
 #include <float.h>
+#include <limits.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "km_fixed.cuh"
 #include "km_tile.cuh"
 
 namespace cabsk {
 
 
 // ---------------------------------------------------------------- weights
+// Also the fixed-point bounds max|x| and max w (bounds[0], bounds[1]; km_fixed.cuh).
 __global__ void __launch_bounds__(256) km_weights_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
-                                                         int kind, float p, float* __restrict__ w, int* cnt) {
+                                                         int kind, float p, float* __restrict__ w, int* cnt,
+                                                         unsigned* bounds) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int pos = 0;
+  float mx = 0.f, mw = 0.f;
   for (int64_t l = warp; l < N; l += nw) {
     float ss = 0.f;
     for (int i = lane; i < d; i += 32) {
       float x = X[l * ldx + i];
       ss = fmaf(x, x, ss);
+      mx = fmaxf(mx, fabsf(x));
     }
     ss = warp_sum_f(ss);
     float wl;
@@ -38,18 +44,25 @@ __global__ void __launch_bounds__(256) km_weights_kernel(const float* __restrict
     if (lane == 0) {
       w[l] = wl;
       pos += wl > 0.f;
+      mw = fmaxf(mw, wl);
     }
   }
-  if (lane == 0 && pos) atomicAdd(cnt, pos);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) {
+    if (pos) atomicAdd(cnt, pos);
+    atomicMax(bounds, __float_as_uint(mx));
+    atomicMax(bounds + 1, __float_as_uint(mw));
+  }
 }
 
 void launch_km_weights(const float* X, int64_t ldx, int64_t N, int d, int kind, float p, float* w, int* cnt,
-                       cudaStream_t st) {
+                       unsigned* bounds, cudaStream_t st) {
   if (N <= 0) return;
   int64_t blocks = ceil_div(N, 8);
   if (blocks > 8 * kNumSM) blocks = 8 * kNumSM;
   note_launch();
-  km_weights_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(X, ldx, N, d, kind, p, w, cnt);
+  km_weights_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(X, ldx, N, d, kind, p, w, cnt, bounds);
 }
 
 // ---------------------------------------------------------------- init
@@ -155,110 +168,92 @@ void launch_km_distmat(const float* X, int64_t ldx, int64_t N, int d, const floa
 }
 
 // ---------------------------------------------------------------- accumulate
-// grid (G, ceil(d/32)).  CTA b owns the contiguous point chunk b; warp w owns the
-// clusters j with j % 8 == w; lane = dimension.  Points are visited in index
-// order, so every (j, dim) partial is a fixed-order FP32 sum.
-constexpr int kAccSub = 128;
-
+// CTA b takes tiles b, b + G, ... of 64 points; each tile is bucketed by label and added
+// to the global int64 sums (km_fixed.cuh).
 __global__ void __launch_bounds__(256) km_accum_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
                                                        const int* __restrict__ labels, const float* __restrict__ w,
-                                                       int k2, float* __restrict__ psum, double* __restrict__ pw,
-                                                       int64_t ldps) {
-  extern __shared__ float acc_s[];  // [k2][32]
-  __shared__ float Xt[kAccSub][33];
-  __shared__ int labs[kAccSub];
-  __shared__ float wts[kAccSub];
-  double* wsum = reinterpret_cast<double*>(acc_s + (size_t)k2 * 32);  // [k2] (only blockIdx.y == 0)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ds0 = blockIdx.y * 32;
-  const int64_t chunk = ceil_div(N, gridDim.x);
-  const int64_t pbeg = blockIdx.x * chunk;
-  int64_t pend = pbeg + chunk;
-  if (pend > N) pend = N;
-  for (int e = tid; e < k2 * 32; e += blockDim.x) acc_s[e] = 0.f;
-  for (int e = tid; e < k2; e += blockDim.x) wsum[e] = 0.0;
-  __syncthreads();
-  for (int64_t s0 = pbeg; s0 < pend; s0 += kAccSub) {
-    const int cnt = static_cast<int>((pend - s0) < kAccSub ? (pend - s0) : kAccSub);
-    for (int pp = warp; pp < cnt; pp += 8) {
-      const int i = ds0 + lane;
-      Xt[pp][lane] = i < d ? X[(s0 + pp) * ldx + i] : 0.f;
+                                                       const unsigned* bounds, long long* fsum, long long* fw) {
+  extern __shared__ float xs[];  // [d][64]
+  __shared__ __align__(16) int lab_s[kTileP];
+  __shared__ int order_s[kTileP], slab_s[kTileP], ustart_s[kTileP + 1], ucl_s[kTileP];
+  __shared__ float wts[kTileP];
+  __shared__ unsigned smask_s[8];
+  __shared__ int nu_s;
+  double scale, scale_w;
+  fx_scales(bounds, N, scale, scale_w);
+  const int64_t ntiles = ceil_div(N, kTileP);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t p0 = t * kTileP;
+    const int np = static_cast<int>(N - p0 < kTileP ? N - p0 : kTileP);
+    for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
+      const int pp = e / d, i = e - pp * d;
+      xs[i * kTileP + pp] = __ldg(X + (p0 + pp) * ldx + i);
     }
-    for (int pp = tid; pp < cnt; pp += blockDim.x) {
-      labs[pp] = labels[s0 + pp];
-      wts[pp] = w[s0 + pp];
+    for (int pp = threadIdx.x; pp < kTileP; pp += blockDim.x) {
+      lab_s[pp] = pp < np ? labels[p0 + pp] : INT_MAX;
+      wts[pp] = pp < np ? w[p0 + pp] : 0.f;
     }
     __syncthreads();
-    for (int pp = 0; pp < cnt; ++pp) {
-      const int j = labs[pp];
-      if ((j & 7) == warp) {
-        const float wl = wts[pp];
-        acc_s[j * 32 + lane] = fmaf(wl, Xt[pp][lane], acc_s[j * 32 + lane]);
-        if (lane == 0 && blockIdx.y == 0) wsum[j] += static_cast<double>(wl);
-      }
-    }
-    __syncthreads();
+    fx_tile_accumulate(
+        np, lab_s, wts, [&](int i, int p) { return xs[i * kTileP + p]; }, d, scale, scale_w,
+        [&](int e, long long v) { if (v != 0) red_add_u64(fsum + e, v); },
+        [&](int j, long long v) { if (v != 0) red_add_u64(fw + j, v); }, order_s, slab_s, ustart_s, ucl_s, smask_s,
+        &nu_s);
   }
-  const int64_t base = (int64_t)blockIdx.x * k2 * ldps;
-  for (int e = tid; e < k2 * 32; e += blockDim.x) {
-    const int j = e >> 5, i = ds0 + (e & 31);
-    if (i < d) psum[base + (int64_t)j * ldps + i] = acc_s[e];
-  }
-  if (blockIdx.y == 0)
-    for (int j = tid; j < k2; j += blockDim.x) pw[(int64_t)blockIdx.x * k2 + j] = wsum[j];
 }
 
-void launch_km_accum(const float* X, int64_t ldx, int64_t N, int d, const int* labels, const float* w, int k2,
-                     float* psum, double* pw, int64_t ldps, int* grid_out, cudaStream_t st) {
+void launch_km_accum(const float* X, int64_t ldx, int64_t N, int d, const int* labels, const float* w,
+                     const unsigned* bounds, long long* fsum, long long* fw, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(km_accum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  int64_t G = ceil_div(N, 64);
-  if (G > kAccGrid) G = kAccGrid;
+  int64_t G = ceil_div(N, kTileP);
+  if (G > 4 * kNumSM) G = 4 * kNumSM;
   if (G < 1) G = 1;
-  *grid_out = static_cast<int>(G);
-  dim3 grid(static_cast<unsigned>(G), static_cast<unsigned>(ceil_div(d, 32)));
-  size_t smem = (size_t)k2 * 32 * sizeof(float) + (size_t)k2 * sizeof(double);
   note_launch();
-  km_accum_kernel<<<grid, 256, smem, st>>>(X, ldx, N, d, labels, w, k2, psum, pw, ldps);
+  km_accum_kernel<<<static_cast<unsigned>(G), 256, sizeof(float) * (size_t)d * kTileP, st>>>(X, ldx, N, d, labels, w,
+                                                                                             bounds, fsum, fw);
 }
 
 // ---------------------------------------------------------------- reduce
-// red = [k2*d sums | k2 weights | objective | near ties], each a fixed-order FP64 sum over
-// CTAs: 8 lanes per element (lane l sums CTAs l, l+8, ...), xor-butterfly combine.
-__global__ void km_reduce_kernel(const float* __restrict__ psum, const double* __restrict__ pw, int G, int k2, int d,
-                                 int64_t ldps, const double* __restrict__ pobj, const int* __restrict__ ptie, int Gobj,
+// red = [k2*d sums | k2 weights | objective | near ties]: integer sums / 2^S (then zeroed
+// for the next pass); objective / near ties as fixed-order FP64 sums over the assign CTAs
+// (8 lanes per element, lane l sums CTAs l, l+8, ..., xor-butterfly combine).
+__global__ void km_reduce_kernel(long long* fsum, long long* fw, const unsigned* bounds, int64_t N, int k2, int d,
+                                 const double* __restrict__ pobj, const int* __restrict__ ptie, int Gobj,
                                  double* __restrict__ red) {
-  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t e = gt >> 3;
-  const int sub = static_cast<int>(gt & 7);
-  const unsigned gmask = 0xffu << (threadIdx.x & 24);
   const int64_t nsum = (int64_t)k2 * d;
-  if (e >= nsum + k2 + 2) return;  // whole 8-lane groups exit together
-  double s = 0.0;
-  if (e < nsum) {
-    const int j = static_cast<int>(e / d), i = static_cast<int>(e % d);
-    for (int b = sub; b < G; b += 8) s += static_cast<double>(psum[((int64_t)b * k2 + j) * ldps + i]);
-  } else if (e < nsum + k2) {
-    const int j = static_cast<int>(e - nsum);
-    for (int b = sub; b < G; b += 8) s += pw[(int64_t)b * k2 + j];
-  } else if (e == nsum + k2) {
-    for (int b = sub; b < Gobj; b += 8) s += pobj[b];
-  } else {
-    for (int b = sub; b < Gobj; b += 8) s += static_cast<double>(ptie[b]);
+  double scale, scale_w;
+  fx_scales(bounds, N, scale, scale_w);
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gt < nsum) {
+    red[gt] = static_cast<double>(fsum[gt]) / scale;
+    fsum[gt] = 0;
+  } else if (gt < nsum + k2) {
+    red[gt] = static_cast<double>(fw[gt - nsum]) / scale_w;
+    fw[gt - nsum] = 0;
   }
+  if (blockIdx.x == 0 && threadIdx.x < 16) {  // two 8-lane groups: objective, near ties
+    const int sub = threadIdx.x & 7;
+    double s = 0.0;
+    if (threadIdx.x < 8) {
+      for (int b = sub; b < Gobj; b += 8) s += pobj[b];
+    } else {
+      for (int b = sub; b < Gobj; b += 8) s += static_cast<double>(ptie[b]);
+    }
 #pragma unroll
-  for (int o = 4; o > 0; o >>= 1) s += __shfl_xor_sync(gmask, s, o);
-  if (sub == 0) red[e] = s;
+    for (int o = 4; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffu, s, o);
+    if (sub == 0) red[nsum + k2 + (threadIdx.x >> 3)] = s;
+  }
 }
 
-void launch_km_reduce(const float* psum, const double* pw, int G, int k2, int d, int64_t ldps, const double* pobj,
-                      const int* ptie, int Gobj, double* red, cudaStream_t st) {
-  const int64_t total = 8 * ((int64_t)k2 * d + k2 + 2);
+void launch_km_reduce(long long* fsum, long long* fw, const unsigned* bounds, int64_t N, int k2, int d,
+                      const double* pobj, const int* ptie, int Gobj, double* red, cudaStream_t st) {
+  const int64_t total = (int64_t)k2 * d + k2;
   note_launch();
-  km_reduce_kernel<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, st>>>(psum, pw, G, k2, d, ldps, pobj, ptie,
+  km_reduce_kernel<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, st>>>(fsum, fw, bounds, N, k2, d, pobj, ptie,
                                                                                  Gobj, red);
 }
 
@@ -270,7 +265,7 @@ __global__ void km_finalize_kernel(const double* __restrict__ red, int k2, int d
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nsum; e += (int64_t)gridDim.x * blockDim.x) {
     const int j = static_cast<int>(e / d), i = static_cast<int>(e % d);
     const double wj = wts[j];
-    if (wj > 0) centres[(int64_t)j * ldc + i] = static_cast<float>(red[e] / wj);
+    if (wj > 0) centres[(int64_t)j * ldc + i] = static_cast<float>(red[e] * (1.0 / wj));  // = lloyd.cu
   }
   if (blockIdx.x == 0) {
     for (int j = threadIdx.x; j < k2; j += blockDim.x)

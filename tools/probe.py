@@ -138,8 +138,9 @@ def probe_lloyd_prof(N=20000, d=50, k2=50, iters=20):
     cw = torch.zeros(k2, dtype=torch.float64, device=dev); obj = torch.zeros(iters, dtype=torch.float64, device=dev)
     C.cabs_kmeans(plan, X, N, N, 0, d, k2, iters, 0, 2.0, 0, 3, cen, lab, cw, obj, ws)
     torch.cuda.synchronize()
-    prof = ws[64:104].view(torch.int64).tolist()
-    names = ["centres+zero", "tiles:dist", "tiles:accum", "publish", "barrier"]
+    prof = ws[64:144].view(torch.int64).tolist()
+    names = ["centres+zero", "dist+argmin", "bucket", "obj-publish", "barrier", "cluster.sync1", "dsmem-reduce+red",
+             "fence", "cluster.sync2"]
     print(f"lloyd N={N} d={d} k2={k2}: " + ", ".join(f"{n} {p / iters:.0f} cyc" for n, p in zip(names, prof)))
 
 

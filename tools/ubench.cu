@@ -128,6 +128,63 @@ __global__ void gather_sector(const float* __restrict__ A, long long lda, long l
   }
 }
 
+// conversion / packed-FP32 latencies and throughputs used by the Lloyd accumulation
+__global__ void lat_cvt_f32_f64(double* out, int n) {
+  float f = (float)out[threadIdx.x] + 1.5f;
+  double acc = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    double d = static_cast<double>(f);  // F2F.F64.F32
+    acc = fma(d, 1.0000001, acc);
+    f = __uint_as_float(__float_as_uint(f) ^ (static_cast<unsigned>(__double_as_longlong(acc)) & 1u));
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = acc + f;
+  if (threadIdx.x == 0) out[1000] = (double)(t1 - t0) / n;
+}
+__global__ void lat_f2i64(double* out, int n) {
+  double x = out[threadIdx.x] + 1.5;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    long long v = llrint(x);  // F2I.S64.F64
+    x = static_cast<double>(v & 7) + 1.25;
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = x;
+  if (threadIdx.x == 0) out[1000] = (double)(t1 - t0) / n;
+}
+__global__ void thr_cvt(double* out, int n, int kind) {
+  float f[8];
+  double a[8];
+  long long q[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) { f[j] = (float)out[(threadIdx.x + j) & 1023] + j; a[j] = 0; q[j] = 0; }
+  for (int i = 0; i < n; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (kind == 0) { a[j] += static_cast<double>(f[j]); f[j] += 1.0f; }
+      else if (kind == 1) { q[j] += llrint(a[j]); a[j] += 1.0; }
+      else { a[j] = fma(a[j], 0.999, 0.001); }
+    }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j] + f[j] + q[j];
+  if (s == 12345.0) out[0] = s;
+}
+__global__ void thr_ffma2(float* out, int n) {
+  unsigned long long a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = __double_as_longlong((double)out[(threadIdx.x + j) & 1023]);
+  const unsigned long long m = 0x3f7ff9723f7ff972ull, c = 0x3a83126f3a83126full;
+  for (int i = 0; i < n; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[j]) : "l"(m), "l"(c));
+  unsigned long long s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s ^= a[j];
+  if (s == 12345) out[0] = 1.f;
+}
+
 int main() {
   double* d;
   float* f;
@@ -202,5 +259,28 @@ int main() {
   printf("random-sector gather        %.1f GB/s sectors (%.1f GB/s useful)\n", 32.0 * m * k / ms / 1e6,
          4.0 * m * k / ms / 1e6);
   printf("SMs %d, clock %d kHz\n", nsm, clk);
+  lat_cvt_f32_f64<<<1, 32>>>(d, n);
+  CK(cudaMemcpy(&h, d + 1000, 8, cudaMemcpyDeviceToHost)); printf("dependent F2F.F64.F32+DFMA+LOP %.1f cycles\n", h);
+  lat_f2i64<<<1, 32>>>(d, n);
+  CK(cudaMemcpy(&h, d + 1000, 8, cudaMemcpyDeviceToHost)); printf("dependent F2I.S64.F64+I2F+DADD %.1f cycles\n", h);
+  const char* kn[3] = {"F2F.F64.F32 (+DADD)", "F2I.S64.F64 (+DADD,IADD)", "DFMA"};
+  for (int kind = 0; kind < 3; ++kind) {
+    thr_cvt<<<nsm * 4, 512>>>(d, 1000, kind);
+    cudaEventRecord(e0);
+    thr_cvt<<<nsm * 4, 512>>>(d, 4000, kind);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = 8.0 * 4000 * nsm * 4 * 512;
+    printf("throughput %-26s %.1f G ops/s = %.1f per SM per clock\n", kn[kind], ops / ms / 1e6,
+           ops / ms / 1e6 / nsm / (clk / 1e6));
+  }
+  thr_ffma2<<<nsm * 4, 512>>>(f, 1000);
+  cudaEventRecord(e0);
+  thr_ffma2<<<nsm * 4, 512>>>(f, 10000);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("FFMA2 peak                  %.1f TFLOP/s\n", 4.0 * 8 * 10000 * (double)nsm * 4 * 512 / ms / 1e9);
   return 0;
 }
