@@ -173,6 +173,32 @@ int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
                     int32_t* near_ties, void* ws, size_t ws_bytes, const cabs_comm* comm,
                     void* stream);
 
+/* One k-means problem of cabs_kmeans_pair: the arguments of cabs_kmeans that differ
+ * between the row side (X = P, rows of A) and the column side (X = Q, columns of A). */
+typedef struct cabs_km_problem {
+  const float* X;               /* device n_loc x ldx */
+  int64_t ldx, n_loc, n_glob, row_off;
+  int32_t d, k2, tag;           /* tag: Philox stream of the Floyd initialisation */
+  const int64_t* init_idx;      /* device int64[k2] or NULL */
+  const float* init_centres;    /* device k2 x ldc or NULL */
+  float* centres;               /* device k2 x ldc (out) */
+  int64_t ldc;
+  int32_t* labels;              /* device int32[n_loc] (out) */
+  double* cluster_w;            /* device double[k2] (out) */
+  double* objective;            /* device double[iters] (out) */
+  int32_t* near_ties;           /* device int32[iters] (out) or NULL */
+} cabs_km_problem;
+
+/* Alg. 2 steps 6-7 for BOTH sides at once: exactly cabs_kmeans(a) and cabs_kmeans(b) with
+ * the shared iters / weight / seed arguments (same results, bit for bit: the sums are exact
+ * integers), run by ONE persistent kernel on a single GPU whose grid barrier and cluster
+ * reductions serve both problems each iteration.  Multi-rank (comm with nranks > 1) runs
+ * the two problems one after the other.  Errors as cabs_kmeans; nothing is written when an
+ * argument check fails. */
+int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const cabs_km_problem* b,
+                         int32_t iters, int32_t weight_kind, float weight_p, uint64_t seed, void* ws,
+                         size_t ws_bytes, const cabs_comm* comm, void* stream);
+
 /* ---------------------------------------------------------------- S8 select
  * Snap ("any k-means clustering center will be replaced with its closest
  * in-sample point"): centres visited in order (-cluster_w[j], j), each taking its

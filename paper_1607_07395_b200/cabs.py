@@ -67,6 +67,14 @@ class Comm(ctypes.Structure):
                 ("allreduce_f32", ALLREDUCE_FN), ("ctx", c_vp)]
 
 
+class KmProblem(ctypes.Structure):
+    """cabs_km_problem: one side (rows or columns) of cabs_kmeans_pair."""
+    _fields_ = [("X", c_vp), ("ldx", c_i64), ("n_loc", c_i64), ("n_glob", c_i64), ("row_off", c_i64),
+                ("d", c_i32), ("k2", c_i32), ("tag", c_i32), ("init_idx", c_vp), ("init_centres", c_vp),
+                ("centres", c_vp), ("ldc", c_i64), ("labels", c_vp), ("cluster_w", c_vp), ("objective", c_vp),
+                ("near_ties", c_vp)]
+
+
 _SIGS = {
     "cabs_status_string": (ctypes.c_char_p, [c_i32]),
     "cabs_last_error_string": (ctypes.c_char_p, []),
@@ -85,6 +93,8 @@ _SIGS = {
     "cabs_kmeans": (c_i32, [ctypes.POINTER(Plan), c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32,
                             c_i32, c_f32, c_u64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,
                             c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_kmeans_pair": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(KmProblem), ctypes.POINTER(KmProblem), c_i32,
+                                 c_i32, c_f32, c_u64, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_select": (c_i32, [ctypes.POINTER(Plan), c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_vp, c_i64,
                             c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_sketch": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_vp, c_vp, c_i32, c_i32, c_f64,
@@ -214,6 +224,22 @@ def cabs_kmeans(plan, X, n_loc, n_glob, row_off, d, k2, iters, weight_kind, weig
                               int(tag), _p(init_idx), _p(init_centres), _p(centres), _ld(centres),
                               _p(labels), _p(cluster_w), _p(objective), _p(near_ties), _p(ws), ws.numel(),
                               _comm(comm), _stream(stream)), "cabs_kmeans")
+
+
+def km_problem(X, n_loc, n_glob, row_off, d, k2, tag, centres, labels, cluster_w, objective, near_ties=None,
+               init_idx=None, init_centres=None):
+    """Describe one side of cabs_kmeans_pair (tensors must outlive the call)."""
+    def ptr(t):
+        return None if t is None else t.data_ptr()
+    return KmProblem(ptr(X), _ld(X), int(n_loc), int(n_glob), int(row_off), int(d), int(k2), int(tag), ptr(init_idx),
+                     ptr(init_centres), ptr(centres), _ld(centres), ptr(labels), ptr(cluster_w), ptr(objective),
+                     ptr(near_ties))
+
+
+def cabs_kmeans_pair(plan, a, b, iters, weight_kind, weight_p, seed, ws, comm=None, stream=None):
+    _check(load().cabs_kmeans_pair(ctypes.byref(plan), ctypes.byref(a), ctypes.byref(b), int(iters),
+                                   int(weight_kind), float(weight_p), int(seed), _p(ws), ws.numel(), _comm(comm),
+                                   _stream(stream)), "cabs_kmeans_pair")
 
 
 def cabs_select(plan, X, n_loc, n_glob, row_off, d, centres, k2, cluster_w, reps, ws,

@@ -243,6 +243,101 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
 }
 
 // ---------------------------------------------------------------- S6-S7
+static int32_t km_check(const cabs_plan* plan, const Ws& L, const cabs_km_problem& p, int32_t iters,
+                        int32_t weight_kind) {
+  if (p.k2 < 1 || p.k2 > plan->kmax || p.k2 > p.n_glob) return arg_error("kmeans: need 1 <= k2 <= min(n_glob, kmax)");
+  if (iters < 1) return arg_error("kmeans: iters must be >= 1");  // S:335
+  if (p.d < 1 || p.d > L.Kp || p.ldx < p.d || p.ldc < p.d || p.n_loc < 0 || p.n_loc > L.Nmax)
+    return arg_error("kmeans: bad dims");
+  if (weight_kind != CABS_WEIGHT_CONST && weight_kind != CABS_WEIGHT_POWER) return arg_error("kmeans: bad weight");
+  if (!p.centres || (p.n_loc > 0 && (!p.X || !p.labels)) || !p.cluster_w || !p.objective)
+    return arg_error("kmeans: bad buffers");
+  return CABS_OK;
+}
+
+// workspace of problem slot q (0 or 1)
+struct KmSlot {
+  float* w;
+  int* cnt;
+  unsigned* bounds;
+  int64_t* idx;
+  void* scr;
+  size_t scr_bytes;
+};
+static KmSlot km_slot(void* ws, const Ws& L, int q) {
+  KmSlot k;
+  k.w = wsp<float>(ws, L.km_w) + (size_t)q * L.Nmax;
+  k.cnt = wsp<int>(ws, L.km_cnt) + 16 * q;
+  k.bounds = reinterpret_cast<unsigned*>(k.cnt + 2);
+  k.idx = wsp<int64_t>(ws, L.idx) + (size_t)(4 * q) * L.Kp;
+  k.scr = static_cast<char*>(wsp<char>(ws, L.km_scr)) + (size_t)q * L.km_scr_bytes;
+  k.scr_bytes = L.km_scr_bytes;
+  return k;
+}
+
+// weights w_l = Upsilon(||X_l||) and the fixed-point bounds; initial centres (replicated)
+static int32_t km_prepare(const cabs_km_problem& p, int32_t weight_kind, float weight_p, uint64_t seed,
+                          const KmSlot& k, const cabs_comm* comm, void* stream) {
+  cudaStream_t st = S(stream);
+  CABS_CUDA_TRY(cudaMemsetAsync(k.cnt, 0, sizeof(int) * 4, st));
+  launch_km_weights(p.X, p.ldx, p.n_loc, p.d, weight_kind, weight_p, k.w, k.cnt, k.bounds, st);
+  CABS_LAUNCH_CHECK("km_weights");
+  const int64_t* idx = p.init_idx;
+  if (!p.init_idx && !p.init_centres) {
+    launch_floyd2(p.n_glob, p.k2, static_cast<uint32_t>(p.tag), k.idx, 0, 0, 0, nullptr, seed, st);
+    CABS_LAUNCH_CHECK("floyd init");
+    idx = k.idx;
+  }
+  launch_km_init(p.X, p.ldx, p.n_loc, p.row_off, p.d, p.k2, p.init_centres ? nullptr : idx, p.init_centres, p.ldc,
+                 p.centres, p.ldc, st);
+  CABS_LAUNCH_CHECK("km_init");
+  if (!p.init_centres) CABS_TRY(comm_f32(comm, p.centres, p.ldc * (int64_t)p.k2, stream));
+  return CABS_OK;
+}
+
+static LloydJob km_job(const cabs_km_problem& p, const KmSlot& k) {
+  LloydJob j;
+  j.X = p.X; j.ldx = p.ldx; j.N = p.n_loc; j.d = p.d; j.k2 = p.k2; j.w = k.w; j.bounds = k.bounds;
+  j.centres = p.centres; j.ldc = p.ldc; j.labels = p.labels; j.objective = p.objective; j.near_ties = p.near_ties;
+  j.cluster_w = p.cluster_w; j.scratch = k.scr; j.scratch_bytes = k.scr_bytes;
+  return j;
+}
+
+static bool km_persistent_allowed(const cabs_comm* comm) {
+  const char* path = getenv("CABS_KMEANS_PATH");  // "loop" forces the per-iteration kernels (tests)
+  return !(path && strcmp(path, "loop") == 0) && !multi(comm);
+}
+
+// per-iteration kernels (multi-rank, or when the persistent kernel does not apply)
+static int32_t km_loop(const cabs_km_problem& p, int32_t iters, const KmSlot& k, void* ws, const Ws& L,
+                       const cabs_comm* comm, void* stream) {
+  cudaStream_t st = S(stream);
+  const int k2 = p.k2, d = p.d;
+  double* red = wsp<double>(ws, L.km_red);
+  const int64_t payload = (int64_t)k2 * d + k2 + 2;
+  long long* fsum = static_cast<long long*>(k.scr);  // exact int64 sums (km_fixed.cuh), re-zeroed by km_reduce
+  long long* fwt = fsum + (int64_t)k2 * d;
+  CABS_CUDA_TRY(cudaMemsetAsync(fsum, 0, sizeof(long long) * ((int64_t)k2 * d + k2), st));
+  for (int t = 0; t < iters; ++t) {
+    int ga = 1;
+    if (p.n_loc > 0) {
+      launch_km_assign(p.X, p.ldx, p.n_loc, d, p.centres, p.ldc, k2, k.w, p.labels, wsp<double>(ws, L.km_pobj),
+                       wsp<int>(ws, L.km_ptie), &ga, st);
+      launch_km_accum(p.X, p.ldx, p.n_loc, d, p.labels, k.w, k.bounds, fsum, fwt, st);
+      CABS_LAUNCH_CHECK("km_assign/accum");
+      launch_km_reduce(fsum, fwt, k.bounds, p.n_loc, k2, d, wsp<double>(ws, L.km_pobj), wsp<int>(ws, L.km_ptie), ga,
+                       red, st);
+    } else {
+      CABS_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(double) * payload, st));
+    }
+    CABS_LAUNCH_CHECK("km_reduce");
+    CABS_TRY(comm_f64(comm, red, payload, stream));  // ONE fused message per iteration
+    launch_km_finalize(red, k2, d, p.centres, p.ldc, p.objective, p.near_ties, p.cluster_w, t, st);
+    CABS_LAUNCH_CHECK("km_finalize");
+  }
+  return CABS_OK;
+}
+
 int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t n_loc, int64_t n_glob, int64_t row_off,
                     int32_t d, int32_t k2, int32_t iters, int32_t weight_kind, float weight_p, uint64_t seed,
                     int32_t tag, const int64_t* init_idx, const float* init_centres, float* centres, int64_t ldc,
@@ -251,61 +346,54 @@ int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   CABS_TRY(check_plan(plan));
   Ws L;
   CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
-  if (k2 < 1 || k2 > plan->kmax || k2 > n_glob) return arg_error("kmeans: need 1 <= k2 <= min(n_glob, kmax)");
-  if (iters < 1) return arg_error("kmeans: iters must be >= 1");  // S:335
-  if (d < 1 || d > L.Kp || ldx < d || ldc < d || n_loc < 0 || n_loc > L.Nmax) return arg_error("kmeans: bad dims");
-  if (weight_kind != CABS_WEIGHT_CONST && weight_kind != CABS_WEIGHT_POWER) return arg_error("kmeans: bad weight");
-  if (!centres || (n_loc > 0 && (!X || !labels)) || !cluster_w || !objective) return arg_error("kmeans: bad buffers");
-  cudaStream_t st = S(stream);
-  float* w = wsp<float>(ws, L.km_w);
-  int* cnt = wsp<int>(ws, L.km_cnt);
-  CABS_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * 4, st));
-  unsigned* bounds = reinterpret_cast<unsigned*>(cnt + 2);  // max|x|, max w (zeroed above)
-  launch_km_weights(X, ldx, n_loc, d, weight_kind, weight_p, w, cnt, bounds, st);
-  CABS_LAUNCH_CHECK("km_weights");
-  // initial centres
-  const int64_t* idx = init_idx;
-  if (!init_idx && !init_centres) {
-    int64_t* tmp = wsp<int64_t>(ws, L.idx);
-    launch_floyd2(n_glob, k2, static_cast<uint32_t>(tag), tmp, 0, 0, 0, nullptr, seed, st);
-    CABS_LAUNCH_CHECK("floyd init");
-    idx = tmp;
-  }
-  launch_km_init(X, ldx, n_loc, row_off, d, k2, init_centres ? nullptr : idx, init_centres, ldc, centres, ldc, st);
-  CABS_LAUNCH_CHECK("km_init");
-  if (!init_centres) CABS_TRY(comm_f32(comm, centres, ldc * (int64_t)k2, stream));
-  const char* path = getenv("CABS_KMEANS_PATH");  // "loop" forces the per-iteration kernels (tests)
-  const bool allow_persistent = !(path && strcmp(path, "loop") == 0);
-  if (allow_persistent && !multi(comm) && n_loc > 0 &&
-      launch_lloyd_persistent(X, ldx, n_loc, d, k2, iters, w, bounds, centres, ldc, labels, objective, near_ties,
-                              cluster_w,
-                              wsp<float>(ws, L.km_psum), sizeof(float) * (size_t)kAccGrid * L.K * L.Kp,
-                              reinterpret_cast<long long*>(ws) + 8, st)) {
-    CABS_LAUNCH_CHECK("lloyd_persistent");
-    return CABS_OK;
+  const cabs_km_problem p{X, ldx, n_loc, n_glob, row_off, d, k2, tag, init_idx, init_centres, centres, ldc,
+                          labels, cluster_w, objective, near_ties};
+  CABS_TRY(km_check(plan, L, p, iters, weight_kind));
+  const KmSlot k = km_slot(ws, L, 0);
+  CABS_TRY(km_prepare(p, weight_kind, weight_p, seed, k, comm, stream));
+  if (km_persistent_allowed(comm) && n_loc > 0) {
+    const LloydJob j = km_job(p, k);
+    if (launch_lloyd_persistent(&j, 1, iters, reinterpret_cast<long long*>(ws) + 8, S(stream))) {
+      CABS_LAUNCH_CHECK("lloyd_persistent");
+      return CABS_OK;
+    }
   }
   cudaGetLastError();  // a refused cooperative launch is not an error: use the per-iteration kernels
-  double* red = wsp<double>(ws, L.km_red);
-  const int64_t payload = (int64_t)k2 * d + k2 + 2;
-  long long* fsum = wsp<long long>(ws, L.km_psum);  // exact int64 sums (km_fixed.cuh), re-zeroed by km_reduce
-  long long* fwt = fsum + (int64_t)k2 * d;
-  CABS_CUDA_TRY(cudaMemsetAsync(fsum, 0, sizeof(long long) * ((int64_t)k2 * d + k2), st));
-  for (int t = 0; t < iters; ++t) {
-    int ga = 1;
-    if (n_loc > 0) {
-      launch_km_assign(X, ldx, n_loc, d, centres, ldc, k2, w, labels, wsp<double>(ws, L.km_pobj),
-                       wsp<int>(ws, L.km_ptie), &ga, st);
-      launch_km_accum(X, ldx, n_loc, d, labels, w, bounds, fsum, fwt, st);
-      CABS_LAUNCH_CHECK("km_assign/accum");
-      launch_km_reduce(fsum, fwt, bounds, n_loc, k2, d, wsp<double>(ws, L.km_pobj), wsp<int>(ws, L.km_ptie), ga, red,
-                       st);
-    } else {
-      CABS_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(double) * payload, st));
+  return km_loop(p, iters, k, ws, L, comm, stream);
+}
+
+int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const cabs_km_problem* b, int32_t iters,
+                         int32_t weight_kind, float weight_p, uint64_t seed, void* ws, size_t ws_bytes,
+                         const cabs_comm* comm, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  if (!a || !b) return arg_error("kmeans_pair: null problem");
+  CABS_TRY(km_check(plan, L, *a, iters, weight_kind));
+  CABS_TRY(km_check(plan, L, *b, iters, weight_kind));
+  const KmSlot ka = km_slot(ws, L, 0), kb = km_slot(ws, L, 1);
+  CABS_TRY(km_prepare(*a, weight_kind, weight_p, seed, ka, comm, stream));
+  CABS_TRY(km_prepare(*b, weight_kind, weight_p, seed, kb, comm, stream));
+  if (km_persistent_allowed(comm) && a->n_loc > 0 && b->n_loc > 0) {
+    const LloydJob j[2] = {km_job(*a, ka), km_job(*b, kb)};
+    if (launch_lloyd_persistent(j, 2, iters, reinterpret_cast<long long*>(ws) + 8, S(stream))) {
+      CABS_LAUNCH_CHECK("lloyd_persistent");
+      return CABS_OK;
     }
-    CABS_LAUNCH_CHECK("km_reduce");
-    CABS_TRY(comm_f64(comm, red, payload, stream));  // ONE fused message per iteration
-    launch_km_finalize(red, k2, d, centres, ldc, objective, near_ties, cluster_w, t, st);
-    CABS_LAUNCH_CHECK("km_finalize");
+  }
+  cudaGetLastError();
+  // one problem at a time (each may still take the single-problem persistent kernel)
+  const cabs_km_problem* pp[2] = {a, b};
+  const KmSlot* kk[2] = {&ka, &kb};
+  for (int q = 0; q < 2; ++q) {
+    bool done = false;
+    if (km_persistent_allowed(comm) && pp[q]->n_loc > 0) {
+      const LloydJob j = km_job(*pp[q], *kk[q]);
+      done = launch_lloyd_persistent(&j, 1, iters, reinterpret_cast<long long*>(ws) + 8, S(stream));
+      if (done) CABS_LAUNCH_CHECK("lloyd_persistent");
+    }
+    cudaGetLastError();
+    if (!done) CABS_TRY(km_loop(*pp[q], iters, *kk[q], ws, L, comm, stream));
   }
   return CABS_OK;
 }

@@ -16,6 +16,7 @@ constexpr int kAccGrid = 2 * kNumSM;  // k-means accumulation CTAs (per-CTA part
 constexpr int kAssignGrid = 4 * kNumSM;
 constexpr int kResGrid = 8 * kNumSM;  // persistent residual CTAs (upper bound)
 constexpr int kNormTile = 64;         // points per embed-GEMM tile (norm partial rows)
+constexpr int kKmItersCap = 256;      // Lloyd iterations the persistent kernel's scratch covers
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
@@ -25,7 +26,8 @@ struct Ws {
   size_t status, scal;
   size_t w64, a64, v64, sig64, uw32, vw32;
   size_t norm_part, norms, scales;
-  size_t km_w, km_psum, km_pw, km_pobj, km_ptie, km_red, km_cnt;
+  size_t km_w, km_scr, km_pobj, km_ptie, km_red, km_cnt;  // km_w, km_scr, km_cnt: two problems
+  size_t km_scr_bytes;                                     // per problem
   size_t dist, cand_d, cand_i, cand_all;
   size_t idx;
   size_t cb, rb, wb;
@@ -65,9 +67,12 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.norm_part = take(sizeof(double) * 2 * w.npt * Kp);
   w.norms = take(sizeof(double) * 2 * Kp);
   w.scales = take(sizeof(float) * 8 * Kp);
-  w.km_w = take(sizeof(float) * w.Nmax);
-  w.km_psum = take(sizeof(float) * (size_t)kAccGrid * K * Kp);
-  w.km_pw = take(sizeof(double) * (size_t)kAccGrid * K);
+  w.km_w = take(sizeof(float) * 2 * w.Nmax);
+  // k-means scratch per problem: int64 sums [3][K*Kp + K] | grid barrier | objective and
+  // near-tie partials [kKmItersCap][kNumSM] (the persistent kernel; the per-iteration path
+  // uses the first K*Kp + K sums)
+  w.km_scr_bytes = (sizeof(long long) * 3 * ((size_t)K * Kp + K) + 16 + (sizeof(double) + sizeof(int)) * kKmItersCap * kNumSM + 255) & ~size_t(255);
+  w.km_scr = take(2 * w.km_scr_bytes);
   w.km_pobj = take(sizeof(double) * kAssignGrid);
   w.km_ptie = take(sizeof(int) * kAssignGrid);
   w.km_red = take(sizeof(double) * (K * Kp + K + 2));

@@ -46,11 +46,24 @@ void launch_km_reduce(long long* fsum, long long* fw, const unsigned* bounds, in
 void launch_km_finalize(const double* red, int k2, int d, float* centres, int64_t ldc, double* objective,
                         int* near_ties, double* cluster_w, int t, cudaStream_t st);
 
-// lloyd.cu (single-GPU persistent Lloyd loop; false -> use the per-iteration kernels)
-bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int k2, int iters, const float* w,
-                             const unsigned* bounds, float* centres, int64_t ldc, int* labels, double* objective,
-                             int* near_ties, double* cluster_w, void* scratch, size_t scratch_bytes, long long* prof,
-                             cudaStream_t st);
+// lloyd.cu (single-GPU persistent Lloyd loop of one or two problems; false -> use the
+// per-iteration kernels)
+struct LloydJob {
+  const float* X;
+  int64_t ldx, N;
+  int d, k2;
+  const float* w;
+  const unsigned* bounds;
+  float* centres;
+  int64_t ldc;
+  int* labels;
+  double* objective;
+  int* near_ties;
+  double* cluster_w;
+  void* scratch;
+  size_t scratch_bytes;
+};
+bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long long* prof, cudaStream_t st);
 
 // select.cu
 void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t row_off, int T, int nseg, int slot0,

@@ -1,19 +1,21 @@
-// lloyd.cu -- the whole Lloyd loop of one k-means call in ONE persistent kernel (single
-// GPU): c iterations x {centres | assign | accumulate | cluster reduce | grid sync}, no
-// host round trips, no per-iteration launches, ONE grid-wide barrier per iteration.
+// lloyd.cu -- the whole Lloyd loop of one or two k-means problems (the row side and the
+// column side of CABS, Alg. 2 steps 6-7) in ONE persistent kernel (single GPU):
+// c iterations x {centres | assign | accumulate | cluster reduce | grid sync}, no host round
+// trips, no per-iteration launches, ONE grid-wide barrier per iteration for both problems.
+// Every CTA (one per SM) holds a balanced contiguous slice of the points of EACH problem, so
+// the two problems share the synchronisation latency instead of paying it twice.
 //
 // Arithmetic (Eq. 6; c iterations P:204):
 //  * distances by direct differences in FP32, dimensions ascending (= km_tile.cuh), lowest
 //    centre index on ties; two centres per packed FP32x2 instruction (FADD2/FFMA2: the same
-//    IEEE rounding as the scalar ops, half the instructions), 8 points x 8 centres per
-//    thread so that shared-memory operands are reused 8 times;
-//  * sums w_l X_l and w_l accumulated EXACTLY as int64 fixed point (km_fixed.cuh): every
-//    CTA buckets its 128 points by label into a dense int64 partial in shared memory, the
-//    CTAs of a thread-block cluster (8) add their partials through distributed shared
-//    memory (each CTA one slice), and one red.global.add.u64 per (cluster, entry) lands in
-//    the global sums -- order-free, so deterministic and identical to the per-iteration
-//    kernels of kmeans.cu;
-//  * centres = (sum / 2^S) / (weight / 2^Sw) in FP64; an empty cluster keeps its centre (Z12).
+//    IEEE rounding as the scalar ops, half the instructions);
+//  * sums w_l X_l and w_l accumulated EXACTLY as int64 fixed point (km_fixed.cuh): a dense
+//    int64 partial per CTA in shared memory, the CTAs of a thread-block cluster add their
+//    partials through distributed shared memory (each CTA one slice), and one
+//    red.global.add.u64 per (cluster, entry) lands in the global sums -- order-free, so
+//    deterministic and identical to the per-iteration kernels of kmeans.cu;
+//  * centres = (sum / 2^S) * (1 / (weight / 2^Sw)) in FP64; an empty cluster keeps its
+//    centre (Z12).
 // Global sums rotate over three slots: slot it%3 accumulates, slot (it-1)%3 is read by
 // every CTA to form this iteration's centres, slot (it+1)%3 is zeroed for the next one.
 #include <cooperative_groups.h>
@@ -31,14 +33,15 @@ namespace cg = cooperative_groups;
 namespace cabsk {
 
 constexpr int kLT = 256;       // threads per CTA (one CTA per SM)
-constexpr int kLA = 9;         // point rows per thread
-constexpr int kLP = 16 * kLA;  // points per chunk: thread (pt = tid & 15, ct = tid >> 4) owns points pt + 16u, u < 9
+constexpr int kLA = 9;         // max point rows per thread
+constexpr int kLP = 16 * kLA;  // max points per chunk: thread (pt = tid & 15, ct = tid >> 4) owns points pt + 16u
 constexpr int kLC = 64;        // centres per block: ... and centres j0 + ct + 16v, v < 4
+constexpr int kMaxProb = 2;
 
-struct LloydArgs {
+struct LloydProb {
   const float* X;
   int64_t ldx, N;
-  int d, k2, iters;
+  int d, k2;
   const float* w;
   float* centres;  // in: initial centres; out: final centres
   int64_t ldc;
@@ -48,29 +51,34 @@ struct LloydArgs {
   double* cluster_w;
   long long* fsum;         // [3][k2*d + k2] fixed-point sums | weights
   const unsigned* bounds;  // [2] max|x|, max w (km_weights)
-  unsigned* gbar;          // [2] grid barrier {arrivals, generation}
   double* pobj;            // [iters][G]
   int* ptie;               // [iters][G]
-  int resident, cpc;       // X chunks resident in smem; max chunks per CTA
-  long long* prof;         // diagnostics (CABS_PROFILE_LLOYD builds): per-phase cycles of the last CTA
+  int pitch;               // resident chunk pitch (points, multiple of 16), or kLP when streaming
 };
 
-// dynamic smem: centre pairs | per resident chunk: point pairs [d][kLP], point rows [kLP][d],
-// w * 2^S (FP64), llrint(w * 2^Sw), weights | dense partial | 1 / cluster weight (FP64).
-// (X is not re-read from global memory: every cluster.sync invalidates L1.)
-struct LloydSmem {
-  size_t cs, xp, xr, wsc, iw, wts, part, wd, total;
+struct LloydArgs {
+  LloydProb pr[kMaxProb];
+  int nprob, iters, resident;
+  unsigned* gbar;   // [2] grid barrier {arrivals, generation}
+  long long* prof;  // diagnostics (CABS_PROFILE_LLOYD builds): per-phase cycles of the last CTA
 };
-__host__ __device__ inline LloydSmem lloyd_smem(int d, int k2, int nchunk_buf) {
+
+// dynamic smem per problem: centre pairs [k2p/64][d][2][16][2] | points x [d][pitch] |
+// rows [pitch][d] | w 2^S (FP64) | llrint(w 2^Sw) | w | dense partial [k2*d + k2] |
+// 1 / cluster weight.  (X is never re-read from global memory: cluster.sync invalidates L1.)
+struct LloydSmem {
+  size_t cs, xs, xr, wsc, iw, wts, part, wd, total;
+};
+__host__ __device__ inline LloydSmem lloyd_smem(int d, int k2, int pitch, size_t base) {
   LloydSmem L;
-  size_t o = 0;
+  size_t o = base;
   auto take = [&](size_t b) { size_t r = o; o += (b + 15) & ~size_t(15); return r; };
   L.cs = take(sizeof(float) * round_up(k2, kLC) * d);
-  L.xp = take(sizeof(float) * 2 * (size_t)nchunk_buf * d * kLP);
-  L.xr = take(sizeof(float) * (size_t)nchunk_buf * d * kLP);
-  L.wsc = take(sizeof(double) * (size_t)nchunk_buf * kLP);
-  L.iw = take(sizeof(long long) * (size_t)nchunk_buf * kLP);
-  L.wts = take(sizeof(float) * (size_t)nchunk_buf * kLP);
+  L.xs = take(sizeof(float) * (size_t)d * pitch);
+  L.xr = take(sizeof(float) * (size_t)d * pitch);
+  L.wsc = take(sizeof(double) * (size_t)pitch);
+  L.iw = take(sizeof(long long) * (size_t)pitch);
+  L.wts = take(sizeof(float) * (size_t)pitch);
   L.part = take(sizeof(long long) * ((size_t)k2 * d + k2));
   L.wd = take(sizeof(double) * (size_t)k2);
   L.total = o;
@@ -85,6 +93,11 @@ __device__ __forceinline__ int cpair_idx(int j, int i, int d) {
   return ((((j >> 6) * d + i) * 2 + (jj >> 5)) * 16 + (jj & 15)) * 2 + ((jj >> 4) & 1);
 }
 
+__device__ __forceinline__ unsigned long long f2_dup(float x) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
   unsigned long long r;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -98,36 +111,40 @@ __device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsig
 __device__ __forceinline__ float f2_lo(unsigned long long v) { return __uint_as_float(static_cast<unsigned>(v)); }
 __device__ __forceinline__ float f2_hi(unsigned long long v) { return __uint_as_float(static_cast<unsigned>(v >> 32)); }
 
-struct ChunkBufs {
-  float *xp, *xr;
-  double* wsc;
-  long long* iw;
-  float* wts;
+// per-problem views of the CTA's shared memory
+struct ProbSmem {
+  float *cs, *xs, *xr, *wts;
+  double *wsc, *wd;
+  long long *iw, *part;
 };
-__device__ __forceinline__ ChunkBufs chunk_bufs(unsigned char* dyn, const LloydSmem& L, int d, int c) {
-  ChunkBufs cb;
-  cb.xp = reinterpret_cast<float*>(dyn + L.xp) + (size_t)c * d * kLP * 2;
-  cb.xr = reinterpret_cast<float*>(dyn + L.xr) + (size_t)c * d * kLP;
-  cb.wsc = reinterpret_cast<double*>(dyn + L.wsc) + (size_t)c * kLP;
-  cb.iw = reinterpret_cast<long long*>(dyn + L.iw) + (size_t)c * kLP;
-  cb.wts = reinterpret_cast<float*>(dyn + L.wts) + (size_t)c * kLP;
-  return cb;
+__device__ __forceinline__ ProbSmem prob_smem(unsigned char* dyn, const LloydSmem& L) {
+  ProbSmem s;
+  s.cs = reinterpret_cast<float*>(dyn + L.cs);
+  s.xs = reinterpret_cast<float*>(dyn + L.xs);
+  s.xr = reinterpret_cast<float*>(dyn + L.xr);
+  s.wsc = reinterpret_cast<double*>(dyn + L.wsc);
+  s.iw = reinterpret_cast<long long*>(dyn + L.iw);
+  s.wts = reinterpret_cast<float*>(dyn + L.wts);
+  s.part = reinterpret_cast<long long*>(dyn + L.part);
+  s.wd = reinterpret_cast<double*>(dyn + L.wd);
+  return s;
 }
-// chunk of up to kLP points -> (x, x) pairs [i][kLP], w 2^S, llrint(w 2^Sw), w (zeros beyond)
-__device__ __forceinline__ void stage_chunk(const LloydArgs& a, int64_t p0, int np, const ChunkBufs& cb, double scale,
+
+// chunk of np <= pitch points -> x [i][pitch], rows [p][d], w 2^S, llrint(w 2^Sw), w (zeros beyond)
+__device__ __forceinline__ void stage_chunk(const LloydProb& pr, int64_t p0, int np, const ProbSmem& S, double scale,
                                             double scale_w) {
-  const int d = a.d;
-  for (int e = threadIdx.x; e < kLP * d; e += blockDim.x) {
+  const int d = pr.d, P = pr.pitch;
+  for (int e = threadIdx.x; e < P * d; e += blockDim.x) {
     const int pp = e / d, i = e - pp * d;
-    const float x = pp < np ? __ldg(a.X + (p0 + pp) * a.ldx + i) : 0.f;
-    reinterpret_cast<float2*>(cb.xp)[i * kLP + pp] = make_float2(x, x);
-    cb.xr[e] = x;
+    const float x = pp < np ? __ldg(pr.X + (p0 + pp) * pr.ldx + i) : 0.f;
+    S.xs[i * P + pp] = x;
+    S.xr[e] = x;
   }
-  for (int pp = threadIdx.x; pp < kLP; pp += blockDim.x) {
-    const float w = pp < np ? a.w[p0 + pp] : 0.f;
-    cb.wsc[pp] = static_cast<double>(w) * scale;  // exact (power-of-two scale)
-    cb.iw[pp] = llrint(static_cast<double>(w) * scale_w);
-    cb.wts[pp] = w;
+  for (int pp = threadIdx.x; pp < P; pp += blockDim.x) {
+    const float w = pp < np ? pr.w[p0 + pp] : 0.f;
+    S.wsc[pp] = static_cast<double>(w) * scale;  // exact (power-of-two scale)
+    S.iw[pp] = llrint(static_cast<double>(w) * scale_w);
+    S.wts[pp] = w;
   }
 }
 
@@ -135,24 +152,26 @@ __device__ __forceinline__ void stage_chunk(const LloydArgs& a, int64_t p0, int 
 // differences, dimensions ascending), running (best, index, runner-up) per point, merged over
 // the two centre lanes of the warp and written to the per-warp slots sb_*[warp][point].
 template <int NA>
-__device__ __forceinline__ void dist_rows(const unsigned long long* __restrict__ xq, const float* cs, int d, int k2,
-                                          int pt, int ct, int lane, int warp, float (*sb_d)[kLP], int (*sb_j)[kLP],
+__device__ __forceinline__ void dist_rows(const float* __restrict__ xs, int P, const float* cs, int d, int k2, int pt,
+                                          int ct, int lane, int warp, float (*sb_d)[kLP], int (*sb_j)[kLP],
                                           float (*ss_d)[kLP]) {
   float bd[NA], sd[NA];
   int bj[NA];
 #pragma unroll
   for (int q = 0; q < NA; ++q) { bd[q] = FLT_MAX; sd[q] = FLT_MAX; bj[q] = 0x7fffffff; }
+  const float* xq = xs + pt;
   for (int j0 = 0; j0 < k2; j0 += kLC) {
     unsigned long long acc[2][NA] = {};
     const unsigned long long* cq = reinterpret_cast<const unsigned long long*>(cs) + (size_t)(j0 >> 6) * d * 32 + ct;
     for (int i = 0; i < d; ++i) {
       const unsigned long long c0 = cq[i * 32], c1 = cq[i * 32 + 16];
-      unsigned long long x[NA];
+      float x[NA];
 #pragma unroll
-      for (int u = 0; u < NA; ++u) x[u] = xq[i * kLP + 16 * u];
+      for (int u = 0; u < NA; ++u) x[u] = xq[i * P + 16 * u];
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
-        const unsigned long long df0 = f2_sub(x[u], c0), df1 = f2_sub(x[u], c1);
+        const unsigned long long xx = f2_dup(x[u]);
+        const unsigned long long df0 = f2_sub(xx, c0), df1 = f2_sub(xx, c1);
         acc[0][u] = f2_fma(df0, df0, acc[0][u]);
         acc[1][u] = f2_fma(df1, df1, acc[1][u]);
       }
@@ -187,44 +206,54 @@ __device__ __forceinline__ void dist_rows(const unsigned long long* __restrict__
   }
 }
 
-static_assert(kLT == 256, "the accumulation maps 8 warps x 8 clusters onto 64-cluster blocks");
+static_assert(kLT == 256, "8 warps: cluster ownership j % 8 and the 16 x 16 distance lanes");
 __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ float sb_d[8][kLP];  // per point: best / runner-up of each warp's two centre lanes
   __shared__ int sb_j[8][kLP];
   __shared__ float ss_d[8][kLP];
   __shared__ int lab_s[kLP];
-  __shared__ double s_red[kLT / 32];
-  __shared__ int s_tie[kLT / 32];
+  __shared__ double s_red[kMaxProb][kLT / 32];
+  __shared__ int s_tie[kMaxProb][kLT / 32];
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = static_cast<int>(cluster.block_rank()), csize = static_cast<int>(cluster.num_blocks());
   unsigned gen = 0;  // grid-barrier generation
   const int tid = threadIdx.x, pt = tid & 15, ct = tid >> 4, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x, b = blockIdx.x;
-  const int k2 = a.k2, d = a.d;
-  const int64_t nsum = (int64_t)k2 * d, E = nsum + k2;
-  const LloydSmem L = lloyd_smem(d, k2, a.resident ? a.cpc : 1);
-  float* cs = reinterpret_cast<float*>(dyn + L.cs);
-  long long* part = reinterpret_cast<long long*>(dyn + L.part);  // [E]
-  double* wd = reinterpret_cast<double*>(dyn + L.wd);           // 1 / weight_j (0: empty cluster)
-  const int k2p = static_cast<int>(round_up(k2, kLC));
-  // balanced contiguous point range of this CTA, in chunks of kLP
-  const int64_t p_beg = (a.N * b) / G, p_end = (a.N * (b + 1)) / G;
-  double scale, scale_w;
-  fx_scales(a.bounds, a.N, scale, scale_w);
-  const double inv_scale = 1.0 / scale, inv_scale_w = 1.0 / scale_w;  // exact: powers of two
-  // this CTA's slice of the cluster reduction
-  const int64_t e_beg = E * crank / csize, e_end = E * (crank + 1) / csize;
+  const int G = gridDim.x, b = blockIdx.x, np_ = a.nprob;
+
+  // per problem: smem views, point range, scales, reduction slice
+  LloydSmem Ls[kMaxProb];
+  int64_t pbeg[kMaxProb], pend[kMaxProb], Eq[kMaxProb], ebeg[kMaxProb], eend[kMaxProb];
+  double scale[kMaxProb], scale_w[kMaxProb];
+  {
+    size_t off = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxProb; ++q) {
+      if (q >= np_) break;
+      const LloydProb& pr = a.pr[q];
+      Ls[q] = lloyd_smem(pr.d, pr.k2, pr.pitch, off);
+      off = Ls[q].total;
+      pbeg[q] = (pr.N * b) / G;
+      pend[q] = (pr.N * (b + 1)) / G;
+      Eq[q] = (int64_t)pr.k2 * pr.d + pr.k2;
+      ebeg[q] = Eq[q] * crank / csize;
+      eend[q] = Eq[q] * (crank + 1) / csize;
+      fx_scales(pr.bounds, pr.N, scale[q], scale_w[q]);
+    }
+  }
 
   // ---------------- prologue: resident chunks, initial centres (padding centres = 0)
-  if (a.resident)
-    for (int64_t p0 = p_beg, c = 0; p0 < p_end; p0 += kLP, ++c) {
-      const int np = static_cast<int>(p_end - p0 < kLP ? p_end - p0 : kLP);
-      stage_chunk(a, p0, np, chunk_bufs(dyn, L, d, static_cast<int>(c)), scale, scale_w);
+#pragma unroll
+  for (int q = 0; q < kMaxProb; ++q) {
+    if (q >= np_) break;
+    const LloydProb& pr = a.pr[q];
+    const ProbSmem S = prob_smem(dyn, Ls[q]);
+    if (a.resident) stage_chunk(pr, pbeg[q], static_cast<int>(pend[q] - pbeg[q]), S, scale[q], scale_w[q]);
+    const int k2p = static_cast<int>(round_up(pr.k2, kLC));
+    for (int e = tid; e < k2p * pr.d; e += blockDim.x) {
+      const int j = e / pr.d, i = e - j * pr.d;
+      S.cs[cpair_idx(j, i, pr.d)] = j < pr.k2 ? __ldcg(pr.centres + (int64_t)j * pr.ldc + i) : 0.f;
     }
-  for (int e = tid; e < k2p * d; e += blockDim.x) {
-    const int j = e / d, i = e - j * d;
-    cs[cpair_idx(j, i, d)] = j < k2 ? __ldcg(a.centres + (int64_t)j * a.ldc + i) : 0.f;
   }
 
 #ifdef CABS_PROFILE_LLOYD
@@ -234,140 +263,147 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
 #define LPROF(i) do { } while (0)
 #endif
   for (int it = 0; it < a.iters; ++it) {
-    long long* fs_cur = a.fsum + (size_t)(it % 3) * E;
     if (it > 0) {
-      // centres of this iteration from the previous iteration's exact sums (empty cluster: keep)
-      const long long* fs_prev = a.fsum + (size_t)((it + 2) % 3) * E;
-      for (int j = tid; j < k2; j += blockDim.x) {
-        const long long wj = __ldcg(fs_prev + nsum + j);
-        wd[j] = wj > 0 ? 1.0 / (static_cast<double>(wj) * inv_scale_w) : 0.0;
-      }
-      constexpr int U = 8;  // independent L2 loads in flight per thread
-      long long sv[U];
-      const int ns = static_cast<int>(nsum);
+      // centres of this iteration from the previous iteration's exact sums (empty cluster: keep);
+      // the loads of both problems are issued before the first wait
+      constexpr int U = 8;  // independent L2 loads in flight per thread (per problem)
+      long long sv[kMaxProb][U];
+  #pragma unroll
+    for (int q = 0; q < kMaxProb; ++q) {
+      if (q >= np_) break;
+        const LloydProb& pr = a.pr[q];
+        const ProbSmem S = prob_smem(dyn, Ls[q]);
+        const int64_t nsum = (int64_t)pr.k2 * pr.d;
+        const long long* fs_prev = pr.fsum + (size_t)((it + 2) % 3) * Eq[q];
+        for (int j = tid; j < pr.k2; j += blockDim.x) {
+          const long long wj = __ldcg(fs_prev + nsum + j);
+          S.wd[j] = wj > 0 ? 1.0 / (static_cast<double>(wj) * (1.0 / scale_w[q])) : 0.0;
+        }
 #pragma unroll
-      for (int u = 0; u < U; ++u) sv[u] = tid + u * kLT < ns ? __ldcg(fs_prev + tid + u * kLT) : 0;
+        for (int u = 0; u < U; ++u) sv[q][u] = tid + u * kLT < nsum ? __ldcg(fs_prev + tid + u * kLT) : 0;
+      }
       __syncthreads();  // wd ready
-      for (int e0 = tid; e0 < ns; e0 += U * kLT) {
-        if (e0 != tid) {
+  #pragma unroll
+    for (int q = 0; q < kMaxProb; ++q) {
+      if (q >= np_) break;
+        const LloydProb& pr = a.pr[q];
+        const ProbSmem S = prob_smem(dyn, Ls[q]);
+        const int d = pr.d, ns = pr.k2 * pr.d;
+        const double inv_scale = 1.0 / scale[q];
+        const long long* fs_prev = pr.fsum + (size_t)((it + 2) % 3) * Eq[q];
+        for (int e0 = tid; e0 < ns; e0 += U * kLT) {
+          long long v[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int e = e0 + u * kLT;
-            sv[u] = e < ns ? __ldcg(fs_prev + e) : 0;
+            v[u] = e0 == tid ? sv[q][u] : (e < ns ? __ldcg(fs_prev + e) : 0);
           }
-        }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = e0 + u * kLT;
-          if (e < ns) {
-            const int j = e / d, i = e - j * d;
-            const double rw = wd[j];
-            if (rw > 0) cs[cpair_idx(j, i, d)] = static_cast<float>((static_cast<double>(sv[u]) * inv_scale) * rw);
+          for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * kLT;
+            if (e < ns) {
+              const int j = e / d, i = e - j * d;
+              const double rw = S.wd[j];
+              if (rw > 0) S.cs[cpair_idx(j, i, d)] = static_cast<float>((static_cast<double>(v[u]) * inv_scale) * rw);
+            }
           }
         }
+        // zero the slot the next iteration accumulates into (last read before the previous barrier)
+        long long* fs_next = pr.fsum + (size_t)((it + 1) % 3) * Eq[q];
+        for (int64_t e = (int64_t)b * blockDim.x + tid; e < Eq[q]; e += (int64_t)G * blockDim.x) fs_next[e] = 0;
       }
-      // zero the slot the next iteration accumulates into (last read before the previous barrier)
-      long long* fs_next = a.fsum + (size_t)((it + 1) % 3) * E;
-      for (int64_t e = (int64_t)b * blockDim.x + tid; e < E; e += (int64_t)G * blockDim.x) fs_next[e] = 0;
     }
-    for (int64_t e = tid; e < E; e += blockDim.x) part[e] = 0;
-    double obj = 0.0;
-    int ties = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxProb; ++q) {
+      if (q >= np_) break;
+      const ProbSmem S = prob_smem(dyn, Ls[q]);
+      for (int64_t e = tid; e < Eq[q]; e += blockDim.x) S.part[e] = 0;
+    }
     __syncthreads();
     LPROF(0);
-    for (int64_t p0 = p_beg, c = 0; p0 < p_end; p0 += kLP, ++c) {
-      const int np = static_cast<int>(p_end - p0 < kLP ? p_end - p0 : kLP);
-      const ChunkBufs cb = chunk_bufs(dyn, L, d, a.resident ? static_cast<int>(c) : 0);
-      if (!a.resident) {
-        __syncthreads();  // previous chunk fully consumed
-        stage_chunk(a, p0, np, cb, scale, scale_w);
-        __syncthreads();
-      }
-      // distances: points pt + 16u x centres j0 + ct + 16v (v < 4), rows u < NA = ceil(np / 16)
-      {
-        const unsigned long long* xq = reinterpret_cast<const unsigned long long*>(cb.xp) + pt;
-        const int na = (np + 15) >> 4;
-        if (na <= 3) dist_rows<3>(xq, cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
-        else if (na <= 5) dist_rows<5>(xq, cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
-        else if (na <= 7) dist_rows<7>(xq, cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
-        else dist_rows<9>(xq, cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
-      }
-      __syncthreads();
-      for (int p = tid; p < np; p += kLT) {  // merge the 8 warps (lowest index on ties)
-        float B = sb_d[0][p], Sd = ss_d[0][p];
-        int Bj = sb_j[0][p];
-        for (int t = 1; t < kLT / 32; ++t) {
-          const float b2 = sb_d[t][p], s2 = ss_d[t][p];
-          const int j2 = sb_j[t][p];
-          if (b2 < B || (b2 == B && j2 < Bj)) { Sd = fminf(fminf(Sd, s2), B); B = b2; Bj = j2; }
-          else Sd = fminf(fminf(Sd, s2), b2);
+#pragma unroll
+    for (int q = 0; q < kMaxProb; ++q) {
+      if (q >= np_) break;
+      const LloydProb& pr = a.pr[q];
+      const ProbSmem S = prob_smem(dyn, Ls[q]);
+      const int d = pr.d, k2 = pr.k2;
+      const int64_t nsum = (int64_t)k2 * d;
+      double obj = 0.0;
+      int ties = 0;
+      for (int64_t p0 = pbeg[q]; p0 < pend[q]; p0 += pr.pitch) {
+        const int np = static_cast<int>(pend[q] - p0 < pr.pitch ? pend[q] - p0 : pr.pitch);
+        if (!a.resident) {
+          __syncthreads();  // previous chunk fully consumed
+          stage_chunk(pr, p0, np, S, scale[q], scale_w[q]);
+          __syncthreads();
         }
-        lab_s[p] = Bj;
-        if (p < np) {
-          a.labels[p0 + p] = Bj;
-          obj += static_cast<double>(cb.wts[p]) * static_cast<double>(B);
+        // distances: rows u < ceil(np / 16)
+        {
+          const int na = (np + 15) >> 4;
+          if (na <= 3) dist_rows<3>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
+          else if (na <= 5) dist_rows<5>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
+          else if (na <= 7) dist_rows<7>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
+          else dist_rows<9>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
+        }
+        __syncthreads();
+        for (int p = tid; p < np; p += kLT) {  // merge the 8 warps (lowest index on ties)
+          float B = sb_d[0][p], Sd = ss_d[0][p];
+          int Bj = sb_j[0][p];
+          for (int t = 1; t < kLT / 32; ++t) {
+            const float b2 = sb_d[t][p], s2 = ss_d[t][p];
+            const int j2 = sb_j[t][p];
+            if (b2 < B || (b2 == B && j2 < Bj)) { Sd = fminf(fminf(Sd, s2), B); B = b2; Bj = j2; }
+            else Sd = fminf(fminf(Sd, s2), b2);
+          }
+          lab_s[p] = Bj;
+          pr.labels[p0 + p] = Bj;
+          obj += static_cast<double>(S.wts[p]) * static_cast<double>(B);
           ties += (Sd - B) < kNearTie * Sd;
         }
-      }
-      __syncthreads();
-      LPROF(1);
-      // exact sums (km_fixed.cuh): warp w owns the clusters j = jb + w + 8t (t < 8) and keeps
-      // their sums over the chunk in registers, lanes over dimensions; a ballot over 32 labels
-      // at a time finds its points, whose llrint(w 2^S x_pi) it adds (integer adds: any order).
-      for (int jb = 0; jb < k2; jb += 64) {
-        for (int i0 = 0; i0 < d; i0 += 64) {
-          const int ia = i0 + lane, ib = i0 + 32 + lane;
-          long long sa[8], sbv[8], sw[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) { sa[t] = 0; sbv[t] = 0; sw[t] = 0; }
+        __syncthreads();
+        LPROF(1);
+        // exact sums (km_fixed.cuh): warp w owns the clusters j with j % 8 == w (exclusive, so
+        // plain read-modify-writes of the shared partial); a ballot over 32 labels at a time finds
+        // its points, whose llrint(w 2^S x_pi) the lanes (dimensions) add (integer adds: any order)
+        {
+          long long* __restrict__ pp = S.part;
+          const float* __restrict__ xr = S.xr;
           for (int q0 = 0; q0 < np; q0 += 32) {
-            const int q = q0 + lane;
-            const int jr = q < np ? lab_s[q] - jb - warp : -1;
-            unsigned m = __ballot_sync(0xffffffffu, jr >= 0 && jr < 64 && (jr & 7) == 0);
-            while (m) {  // two points per step: independent load -> convert chains
-              const int p1 = q0 + __ffs(m) - 1;
+            const int qq = q0 + lane;
+            unsigned m = __ballot_sync(0xffffffffu, qq < np && (lab_s[qq] & 7) == warp);
+            while (m) {
+              const int p = q0 + __ffs(m) - 1;
               m &= m - 1;
-              const bool two = m != 0;
-              const int p2 = two ? q0 + __ffs(m) - 1 : p1;
-              if (two) m &= m - 1;
-              const int t1 = (lab_s[p1] - jb - warp) >> 3, t2 = (lab_s[p2] - jb - warp) >> 3;
-              const double ws1 = cb.wsc[p1], ws2 = two ? cb.wsc[p2] : 0.0;
-              const float* x1 = cb.xr + p1 * d;
-              const float* x2 = cb.xr + p2 * d;
-              const long long va1 = ia < d ? fx_prod_magic(ws1, x1[ia]) : 0;
-              const long long vb1 = ib < d ? fx_prod_magic(ws1, x1[ib]) : 0;
-              const long long va2 = ia < d ? fx_prod_magic(ws2, x2[ia]) : 0;
-              const long long vb2 = ib < d ? fx_prod_magic(ws2, x2[ib]) : 0;
-              const long long vw1 = cb.iw[p1], vw2 = two ? cb.iw[p2] : 0;
-#pragma unroll
-              for (int tt = 0; tt < 8; ++tt) {
-                if (tt == t1) { sa[tt] += va1; sbv[tt] += vb1; sw[tt] += vw1; }
-                if (tt == t2) { sa[tt] += va2; sbv[tt] += vb2; sw[tt] += vw2; }
-              }
-            }
-          }
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const int j = jb + warp + 8 * t;
-            if (j < k2) {
-              if (ia < d) part[j * d + ia] += sa[t];
-              if (ib < d) part[j * d + ib] += sbv[t];
-              if (i0 == 0 && lane == 0) part[nsum + j] += sw[t];
+              const int j = lab_s[p];
+              const double ws = S.wsc[p];
+              const float* xrow = xr + p * d;
+              long long* prow = pp + (int64_t)j * d;
+              for (int i = lane; i < d; i += 32) prow[i] += fx_prod_magic(ws, xrow[i]);
+              if (lane == 0) pp[nsum + j] += S.iw[p];
             }
           }
         }
+        __syncthreads();
+        LPROF(2);
       }
-      __syncthreads();
+      obj = warp_sum_d(obj);
+      int tt = ties;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tt += __shfl_xor_sync(0xffffffffu, tt, o);
+      if (lane == 0) { s_red[q][warp] = obj; s_tie[q][warp] = tt; }
     }
-    LPROF(2);
     // cluster reduction of the dense partials (DSMEM), one global integer add per entry
     cluster.sync();
     LPROF(5);
-    {
+#pragma unroll
+    for (int q = 0; q < kMaxProb; ++q) {
+      if (q >= np_) break;
+      const ProbSmem S = prob_smem(dyn, Ls[q]);
+      long long* fs_cur = a.pr[q].fsum + (size_t)(it % 3) * Eq[q];
       const long long* rp[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) rp[r] = r < csize ? cluster.map_shared_rank(part, r) : part;
-      for (int64_t e = e_beg + tid; e < e_end; e += blockDim.x) {
+      for (int r = 0; r < 8; ++r) rp[r] = r < csize ? cluster.map_shared_rank(S.part, r) : S.part;
+      for (int64_t e = ebeg[q] + tid; e < eend[q]; e += blockDim.x) {
         long long v[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) v[r] = r < csize ? rp[r][e] : 0;
@@ -377,22 +413,21 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
         if (s != 0) red_add_u64(fs_cur + e, s);
       }
     }
-    obj = warp_sum_d(obj);
-    int tt = ties;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tt += __shfl_xor_sync(0xffffffffu, tt, o);
-    if (lane == 0) { s_red[warp] = obj; s_tie[warp] = tt; }
     LPROF(6);
     __threadfence();
     LPROF(7);
     cluster.sync();  // partials free again; this cluster's global adds issued and fenced
     LPROF(8);
     if (tid == 0) {
-      double s = 0;
-      int q = 0;
-      for (int w = 0; w < kLT / 32; ++w) { s += s_red[w]; q += s_tie[w]; }
-      a.pobj[(size_t)it * G + b] = s;
-      a.ptie[(size_t)it * G + b] = q;
+  #pragma unroll
+    for (int q = 0; q < kMaxProb; ++q) {
+      if (q >= np_) break;
+        double s = 0;
+        int qq = 0;
+        for (int w = 0; w < kLT / 32; ++w) { s += s_red[q][w]; qq += s_tie[q][w]; }
+        a.pr[q].pobj[(size_t)it * G + b] = s;
+        a.pr[q].ptie[(size_t)it * G + b] = qq;
+      }
     }
     LPROF(3);
     grid_barrier(a.gbar, gen);
@@ -404,32 +439,43 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
 #endif
   // ---------------- epilogue (CTA 0): final centres, cluster weights, objective history
   if (b == 0) {
-    const long long* fs_last = a.fsum + (size_t)((a.iters - 1) % 3) * E;
-    for (int e = tid; e < nsum; e += blockDim.x) {
-      const int j = e / d, i = e - j * d;
-      const long long wj = __ldcg(fs_last + nsum + j);
-      a.centres[(int64_t)j * a.ldc + i] =
-          wj > 0 ? static_cast<float>((static_cast<double>(__ldcg(fs_last + e)) * inv_scale) *
-                                      (1.0 / (static_cast<double>(wj) * inv_scale_w)))
-                 : cs[cpair_idx(j, i, d)];
-    }
-    for (int j = tid; j < k2; j += blockDim.x) a.cluster_w[j] = static_cast<double>(__ldcg(fs_last + nsum + j)) / scale_w;
-    for (int it = tid; it < a.iters; it += blockDim.x) {
-      double s = 0;
-      long long q = 0;
-      for (int g = 0; g < G; ++g) { s += __ldcg(a.pobj + (size_t)it * G + g); q += __ldcg(a.ptie + (size_t)it * G + g); }
-      a.objective[it] = s;
-      if (a.near_ties) a.near_ties[it] = static_cast<int>(q);
+#pragma unroll
+    for (int q = 0; q < kMaxProb; ++q) {
+      if (q >= np_) break;
+      const LloydProb& pr = a.pr[q];
+      const ProbSmem S = prob_smem(dyn, Ls[q]);
+      const int d = pr.d, k2 = pr.k2, nsum = k2 * d;
+      const double inv_scale = 1.0 / scale[q], inv_scale_w = 1.0 / scale_w[q];
+      const long long* fs_last = pr.fsum + (size_t)((a.iters - 1) % 3) * Eq[q];
+      for (int e = tid; e < nsum; e += blockDim.x) {
+        const int j = e / d, i = e - j * d;
+        const long long wj = __ldcg(fs_last + nsum + j);
+        pr.centres[(int64_t)j * pr.ldc + i] =
+            wj > 0 ? static_cast<float>((static_cast<double>(__ldcg(fs_last + e)) * inv_scale) *
+                                        (1.0 / (static_cast<double>(wj) * inv_scale_w)))
+                   : S.cs[cpair_idx(j, i, d)];
+      }
+      for (int j = tid; j < k2; j += blockDim.x)
+        pr.cluster_w[j] = static_cast<double>(__ldcg(fs_last + nsum + j)) / scale_w[q];
+      for (int it = tid; it < a.iters; it += blockDim.x) {
+        double s = 0;
+        long long qq = 0;
+        for (int g = 0; g < G; ++g) {
+          s += __ldcg(pr.pobj + (size_t)it * G + g);
+          qq += __ldcg(pr.ptie + (size_t)it * G + g);
+        }
+        pr.objective[it] = s;
+        if (pr.near_ties) pr.near_ties[it] = static_cast<int>(qq);
+      }
     }
   }
 }
 
 // Returns false when the fast path does not apply (caller uses the per-iteration kernels).
-bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int k2, int iters, const float* w,
-                             const unsigned* bounds, float* centres, int64_t ldc, int* labels, double* objective,
-                             int* near_ties, double* cluster_w, void* scratch, size_t scratch_bytes, long long* prof,
-                             cudaStream_t st) {
-  if (N <= 0) return false;
+bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long long* prof, cudaStream_t st) {
+  if (njobs < 1 || njobs > kMaxProb) return false;
+  for (int q = 0; q < njobs; ++q)
+    if (jobs[q].N <= 0) return false;
   constexpr size_t kSmemCap = 200 * 1024;
   static bool attr = false;
   if (!attr) {
@@ -441,22 +487,31 @@ bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int 
   int dev = 0, nsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // grid: one CTA per SM, every CTA a balanced contiguous range of ~N / #SM points (chunks of
-  // kLP); the largest cluster size (8, 4, 2, 1) whose clusters can all be resident
-  int64_t G = nsm;  // all SMs: the per-CTA point count sets the iteration time
-  if (G > N) G = N;
-  const int cpc = static_cast<int>(ceil_div(ceil_div(N, G), kLP));
+  int64_t Nmin = jobs[0].N;
+  for (int q = 1; q < njobs; ++q) Nmin = jobs[q].N < Nmin ? jobs[q].N : Nmin;
+  // grid: one CTA per SM (every CTA holds ~N / #SM points of each problem); the largest
+  // cluster size (8, 4, 2, 1) whose clusters can all be resident
+  int64_t G = nsm;
+  if (G > Nmin) G = Nmin;
+  auto smem_for = [&](int64_t g, int& resident, int* pitch) {
+    resident = 1;
+    size_t total = 0;
+    for (int q = 0; q < njobs; ++q) {
+      const int64_t per = ceil_div(jobs[q].N, g);
+      pitch[q] = per <= kLP ? static_cast<int>(round_up(per, 16)) : kLP;
+      if (per > kLP) resident = 0;
+      total = lloyd_smem(jobs[q].d, jobs[q].k2, pitch[q], total).total;
+    }
+    return total;
+  };
+  LloydArgs a{};
+  a.nprob = njobs;
+  a.iters = iters;
+  a.prof = prof;
+  int pitch[kMaxProb] = {kLP, kLP};
   int resident = 1;
-  size_t smem = lloyd_smem(d, k2, cpc).total;
-  if (smem > kSmemCap) {
-    resident = 0;
-    smem = lloyd_smem(d, k2, 1).total;
-  }
-  if (smem > kSmemCap) return false;
-  // co-residency of all CTAs (the grid barrier) is checked, not assumed
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kLT);
-  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -467,11 +522,15 @@ bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int 
   cfg.attrs = at;
   cfg.numAttrs = 2;
   int csize = 0;
+  size_t smem = 0;
   for (int c = 8; c >= 1 && csize == 0; c >>= 1) {
     const int64_t g = G / c * c;  // round down: every CTA still gets <= ceil(N / g) points
     if (g < 1) continue;
+    smem = smem_for(g, resident, pitch);
+    if (smem > kSmemCap) continue;
     at[0].val.clusterDim.x = static_cast<unsigned>(c);
     cfg.gridDim = dim3(static_cast<unsigned>(g));
+    cfg.dynamicSmemBytes = smem;
     int ncl = 0;
     if (cudaOccupancyMaxActiveClusters(&ncl, lloyd_persistent_kernel, &cfg) == cudaSuccess && (int64_t)ncl * c >= g) {
       csize = c;
@@ -480,19 +539,25 @@ bool launch_lloyd_persistent(const float* X, int64_t ldx, int64_t N, int d, int 
   }
   cudaGetLastError();
   if (csize == 0) return false;
-  const int cpc_final = static_cast<int>(ceil_div(ceil_div(N, G), kLP));  // <= cpc: smem suffices
-  // scratch: fsum [3][k2*d + k2] | gbar [2] (+pad) | pobj [iters][G] | ptie [iters][G]
-  const size_t E = (size_t)k2 * d + k2;
-  const size_t need = sizeof(long long) * 3 * E + 16 + (sizeof(double) + sizeof(int)) * iters * G;
-  if (need > scratch_bytes) return false;
-  char* base = static_cast<char*>(scratch);
-  long long* fsum = reinterpret_cast<long long*>(base);
-  unsigned* gbar = reinterpret_cast<unsigned*>(fsum + 3 * E);
-  double* pobj = reinterpret_cast<double*>(gbar + 4);
-  int* ptie = reinterpret_cast<int*>(pobj + (size_t)iters * G);
-  if (cudaMemsetAsync(base, 0, sizeof(long long) * 3 * E + 16, st) != cudaSuccess) return false;
-  LloydArgs a{X, ldx, N, d, k2, iters, w, centres, ldc, labels, objective, near_ties, cluster_w,
-              fsum, bounds, gbar, pobj, ptie, resident, cpc_final, prof};
+  a.resident = resident;
+  // scratch of each job: fsum [3][k2*d + k2] | pobj [iters][G] | ptie [iters][G]; barrier in job 0's
+  for (int q = 0; q < njobs; ++q) {
+    const LloydJob& j = jobs[q];
+    const size_t E = (size_t)j.k2 * j.d + j.k2;
+    const size_t need = sizeof(long long) * 3 * E + 16 + (sizeof(double) + sizeof(int)) * iters * G;
+    if (need > j.scratch_bytes) return false;
+    char* base = static_cast<char*>(j.scratch);
+    LloydProb& p = a.pr[q];
+    p.X = j.X; p.ldx = j.ldx; p.N = j.N; p.d = j.d; p.k2 = j.k2; p.w = j.w;
+    p.centres = j.centres; p.ldc = j.ldc; p.labels = j.labels; p.objective = j.objective;
+    p.near_ties = j.near_ties; p.cluster_w = j.cluster_w; p.bounds = j.bounds; p.pitch = pitch[q];
+    p.fsum = reinterpret_cast<long long*>(base);
+    unsigned* gb = reinterpret_cast<unsigned*>(p.fsum + 3 * E);
+    if (q == 0) a.gbar = gb;
+    p.pobj = reinterpret_cast<double*>(gb + 4);
+    p.ptie = reinterpret_cast<int*>(p.pobj + (size_t)iters * G);
+    if (cudaMemsetAsync(base, 0, sizeof(long long) * 3 * E + 16, st) != cudaSuccess) return false;
+  }
   note_launch();
   return cudaLaunchKernelEx(&cfg, lloyd_persistent_kernel, a) == cudaSuccess;
 }

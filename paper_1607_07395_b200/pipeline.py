@@ -5,7 +5,7 @@ entry points of libcabs.so in order on one stream:
 
   S1-S3 cabs_pilot    pilot sampling and gathers C, R, W
   S4-S5 cabs_embed    pilot sketch -> embeddings P, Q
-  S6-S7 cabs_kmeans   weighted Lloyd on P (rows) and on Q (columns)  (Eq. 6)
+  S6-S7 cabs_kmeans_pair  weighted Lloyd on P (rows) and on Q (columns), one kernel  (Eq. 6)
   S8    cabs_select   snap centres to in-sample rows / columns
   S9    cabs_sketch   follow-up gathers + sketch -> Ubar, sbar, Vbar
   S10   cabs_residual ||A - Ubar diag(sbar) Vbar^T||_F^2, ||A||_F^2
@@ -87,12 +87,12 @@ class CabsPipeline:
 
     def kmeans(self, init_rows=None, init_cols=None):
         c, p = self.cfg, self.plan
-        C.cabs_kmeans(p, self.P, p.m_loc, p.m, p.row_begin, c.k1, c.k2, c.iters, c.weight_kind, c.weight_p,
-                      c.seed, C.TAG_INIT_ROWS, self.cen_r, self.lab_r, self.cw_r, self.obj_r, self.ws,
-                      near_ties=self.tie_r, init_idx=init_rows, comm=self.comm)
-        C.cabs_kmeans(p, self.Q, p.n_sl, p.n, p.col_begin, c.k1, c.k2, c.iters, c.weight_kind, c.weight_p,
-                      c.seed, C.TAG_INIT_COLS, self.cen_c, self.lab_c, self.cw_c, self.obj_c, self.ws,
-                      near_ties=self.tie_c, init_idx=init_cols, comm=self.comm)
+        # both sides in one call: one persistent kernel serves the two problems (single GPU)
+        rows = C.km_problem(self.P, p.m_loc, p.m, p.row_begin, c.k1, c.k2, C.TAG_INIT_ROWS, self.cen_r, self.lab_r,
+                            self.cw_r, self.obj_r, near_ties=self.tie_r, init_idx=init_rows)
+        cols = C.km_problem(self.Q, p.n_sl, p.n, p.col_begin, c.k1, c.k2, C.TAG_INIT_COLS, self.cen_c, self.lab_c,
+                            self.cw_c, self.obj_c, near_ties=self.tie_c, init_idx=init_cols)
+        C.cabs_kmeans_pair(p, rows, cols, c.iters, c.weight_kind, c.weight_p, c.seed, self.ws, comm=self.comm)
 
     def select(self):
         c, p = self.cfg, self.plan

@@ -368,6 +368,47 @@ def test_kmeans_persistent_and_loop_paths_agree(dev, monkeypatch):
     assert rel_fro(c1, c2) < 1e-6 and np.allclose(o1, o2, rtol=1e-6)
 
 
+def test_kmeans_pair_equals_two_single_calls(dev, monkeypatch):
+    """cabs_kmeans_pair (one persistent kernel for both sides) == cabs_kmeans on each side:
+    the sums are exact integers, so labels, centres and cluster weights agree bit for bit;
+    the objective is an FP64 sum over a different CTA partition."""
+    d, k2, iters = 40, 30, 6
+    Na, Nb = 9000, 4100
+    Xa_np, Xb_np = _clustered(Na, d, 25, 21), _clustered(Nb, d, 20, 22)
+    ld = C.cabs_padded_ld(d)
+    Xa = torch.zeros((Na, ld), device=dev); Xa[:, :d] = torch.from_numpy(Xa_np).to(dev)
+    Xb = torch.zeros((Nb, ld), device=dev); Xb[:, :d] = torch.from_numpy(Xb_np).to(dev)
+    plan = _plan(Na, Nb, max(d, k2))
+    ws = _ws(plan, dev)
+
+    def bufs(N):
+        return (torch.zeros((k2, ld), device=dev), torch.zeros(N, dtype=torch.int32, device=dev),
+                torch.zeros(k2, dtype=torch.float64, device=dev), torch.zeros(iters, dtype=torch.float64, device=dev),
+                torch.zeros(iters, dtype=torch.int32, device=dev))
+
+    single = []
+    for X, N, tag in ((Xa, Na, C.TAG_INIT_ROWS), (Xb, Nb, C.TAG_INIT_COLS)):
+        cen, lab, cw, obj, tie = bufs(N)
+        C.cabs_kmeans(plan, X, N, N, 0, d, k2, iters, C.WEIGHT_POWER, 2.0, 7, tag, cen, lab, cw, obj, ws, near_ties=tie)
+        single.append([t.cpu().numpy() for t in (cen, lab, cw, obj, tie)])
+    ba, bb = bufs(Na), bufs(Nb)
+    pa = C.km_problem(Xa, Na, Na, 0, d, k2, C.TAG_INIT_ROWS, ba[0], ba[1], ba[2], ba[3], near_ties=ba[4])
+    pb = C.km_problem(Xb, Nb, Nb, 0, d, k2, C.TAG_INIT_COLS, bb[0], bb[1], bb[2], bb[3], near_ties=bb[4])
+    C.cabs_kmeans_pair(plan, pa, pb, iters, C.WEIGHT_POWER, 2.0, 7, ws)
+    for got, ref in ((ba, single[0]), (bb, single[1])):
+        g = [t.cpu().numpy() for t in got]
+        assert np.array_equal(g[1], ref[1]) and np.array_equal(g[2], ref[2]) and np.array_equal(g[0], ref[0])
+        assert np.allclose(g[3], ref[3], rtol=1e-12) and np.array_equal(g[4], ref[4])
+    # and the per-iteration path (forced) agrees as well
+    monkeypatch.setenv("CABS_KMEANS_PATH", "loop")
+    bl = bufs(Na)
+    pl = C.km_problem(Xa, Na, Na, 0, d, k2, C.TAG_INIT_ROWS, bl[0], bl[1], bl[2], bl[3], near_ties=bl[4])
+    bl2 = bufs(Nb)  # kept alive: the problem struct holds raw pointers
+    pl2 = C.km_problem(Xb, Nb, Nb, 0, d, k2, C.TAG_INIT_COLS, bl2[0], bl2[1], bl2[2], bl2[3])
+    C.cabs_kmeans_pair(plan, pl, pl2, iters, C.WEIGHT_POWER, 2.0, 7, ws)
+    assert np.array_equal(bl[1].cpu().numpy(), single[0][1]) and np.array_equal(bl[0].cpu().numpy(), single[0][0])
+
+
 def test_embed_drops_zero_norm_component_with_compaction(dev):
     """S:244 drop rule with a hole: component 0 extrapolates to zero, component 1 is kept,
     so the kept component must be compacted to position 0 (inconsistent triple, as in the
