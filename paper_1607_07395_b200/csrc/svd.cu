@@ -11,6 +11,10 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace cabsk {
 
@@ -68,19 +72,27 @@ __device__ __forceinline__ double rcp_approx64(double x) {
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   return y;
 }
-__device__ __forceinline__ bool jacobi_angle_fast(double al, double be, double ga, double tol_rot2, double& c,
-                                                  double& sn) {
-  const bool need = ga != 0.0 && ga * ga > tol_rot2 * al * be;
+// t of the rotation (0 when the pair is already orthogonal to tol_rot)
+__device__ __forceinline__ double jacobi_t(double al, double be, double ga, double tol_rot2, bool& need) {
+  need = ga != 0.0 && ga * ga > tol_rot2 * al * be;
   const double dx = be - al, dy = 2.0 * ga;
   const double h = fma(dx, dx, dy * dy);
   const double den = fabs(dx) + h * rsqrt_approx64(h);      // |dx| + sqrt(dx^2 + dy^2)
-  const double t = need ? copysign(1.0, dx) * dy * rcp_approx64(den) : 0.0;
+  return need ? copysign(1.0, dx) * dy * rcp_approx64(den) : 0.0;
+}
+// c = 1/sqrt(1 + t^2) to FP64 accuracy (approximation + two Newton steps), s = c t
+__device__ __forceinline__ void rot_cs(double t, double& c, double& sn) {
   const double q1 = fma(t, t, 1.0);
   double cc = rsqrt_approx64(q1);
   cc = cc * fma(-0.5 * q1, cc * cc, 1.5);
   cc = cc * fma(-0.5 * q1, cc * cc, 1.5);
   c = cc;
   sn = cc * t;
+}
+__device__ __forceinline__ bool jacobi_angle_fast(double al, double be, double ga, double tol_rot2, double& c,
+                                                  double& sn) {
+  bool need;
+  rot_cs(jacobi_t(al, be, ga, tol_rot2, need), c, sn);
   return need;
 }
 
@@ -431,6 +443,272 @@ svd_systolic_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol,
   svd_write(As, Vs, k, r, s_sig, s_perm, Uw64, Vw64, uw32, vw32, ld32);
 }
 
+// ---------------------------------------------------------------- k <= 64: A and V on two SMs
+// A cluster of two CTAs: CTA 0 runs the register-resident odd-even Jacobi on the columns of
+// A only (half the data movement of carrying V) and streams every round's rotations
+// (c, s) into CTA 1's shared memory through DSMEM; CTA 1 applies them to V = I with the same
+// odd-even data movement, one sweep behind (a sweep buffer per parity, one mbarrier signal per
+// sweep each way).  At the end CTA 1 stores V's columns (by column id) into CTA 0, which runs
+// the common epilogue.  Rotation formulas, ordering and convergence test are those of
+// svd_systolic_kernel; CTA 1 recomputes (c, s) from the streamed t with the same code as
+// CTA 0, so A and V see bit-identical rotations.
+__device__ __forceinline__ uint32_t dsmem_map(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(tc::smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsmem_st_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_st_s32(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(tc::smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+
+template <int LP, int E>
+__global__ void __launch_bounds__(256, 1) __cluster_dims__(2, 1, 1)
+svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, double* __restrict__ sigma_out,
+                 double* __restrict__ Uw64, double* __restrict__ Vw64, float* __restrict__ uw32,
+                 float* __restrict__ vw32, int64_t ld32, int* r_out, int* r_out2, void* ws) {
+  constexpr int G = 32 / LP;
+  constexpr int SEAT = E * LP + ((LP - (E * LP) % 16) + 16) % 16;  // slot footprints tile the banks
+  extern __shared__ __align__(16) double smem_d[];
+  __shared__ double s_sig[64];
+  __shared__ int s_perm[64];
+  __shared__ int s_id[2][2][34];
+  __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2];  // full: in CTA 1, empty: in CTA 0
+  __shared__ int s_last[2];                                    // CTA 1: last sweep flag per parity
+  const uint32_t crank = cg::this_cluster().block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int gl = lane % LP, gw = lane / LP;
+  const int g = warp * G + gw;
+  const int np = (k + 1) & ~1, P = np / 2;
+  const int nseat = nw * G + 2;
+  const bool live = g < P;
+  const bool left_edge = g == 0, right_edge = g == P - 1;
+  // smem: exchange [XL|XR][parity][seat][SEAT] | (CTA 1) rotations t [parity][round][slot][2] |
+  // (CTA 0) final A and V columns [k][k] each (reusing the exchange area)
+  const size_t arr = (size_t)2 * nseat * SEAT;
+  double* bXL = smem_d;
+  double* bXR = bXL + arr;
+  double* prm = bXR + arr;  // CTA 1 only
+  if (tid == 0) {
+    tc::mbar_init(&bar_full[0], 1); tc::mbar_init(&bar_full[1], 1);
+    tc::mbar_init(&bar_empty[0], 1); tc::mbar_init(&bar_empty[1], 1);
+    tc::mbar_fence_init();
+  }
+  for (int e = tid; e < 2 * (int)arr; e += blockDim.x) smem_d[e] = 0.0;
+  cluster_sync_all();
+
+  double xL[E], xR[E];  // CTA 0: columns of A; CTA 1: columns of V
+  int idL = 2 * g, idR = 2 * g + 1;
+  if (crank == 0) {
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = gl + LP * e;
+      float wl = 0.f, wr = 0.f;
+      if (live && i < k && idL < k) wl = W[(int64_t)i * ldw + idL];
+      if (live && i < k && idR < k) wr = W[(int64_t)i * ldw + idR];
+      bad |= !isfinite(wl) || !isfinite(wr);
+      xL[e] = wl;
+      xR[e] = wr;
+    }
+    if (bad) set_status(ws, CABS_DEV_NONFINITE);
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = gl + LP * e;
+      xL[e] = (i == idL && idL < k) ? 1.0 : 0.0;
+      xR[e] = (i == idR && idR < k) ? 1.0 : 0.0;
+    }
+  }
+  __syncthreads();
+  const double tol_rot = 2.0 * sqrt(static_cast<double>(k)) * DBL_EPSILON;
+  const double tol_rot2 = tol_rot * tol_rot;
+  // remote addresses (CTA 0 -> CTA 1 params and full barriers; CTA 1 -> CTA 0 empty barriers)
+  const uint32_t prm_remote = dsmem_map(prm, 1);
+  const uint32_t full_remote0 = dsmem_map(&bar_full[0], 1), full_remote1 = dsmem_map(&bar_full[1], 1);
+  const uint32_t empty_remote0 = dsmem_map(&bar_empty[0], 0), empty_remote1 = dsmem_map(&bar_empty[1], 0);
+  const uint32_t last_remote = dsmem_map(&s_last[0], 1);
+#ifdef CABS_PROFILE_SVD
+  long long sprof[8] = {0, 0, 0, 0, 0, 0, 0, 0}, st0 = clock64();
+#define SPROF(i) do { if (crank == 0 && tid == 0) { const long long t1_ = clock64(); sprof[i] += t1_ - st0; st0 = t1_; } } while (0)
+#else
+#define SPROF(i) do { } while (0)
+#endif
+  int sweep = 0;
+  bool last = k <= 1;
+  for (; !last; ++sweep) {
+    const int sp = sweep & 1;
+    if (crank == 0 && sweep >= 2) mbar_wait_cluster(&bar_empty[sp], static_cast<uint32_t>(((sweep - 2) >> 1) & 1));
+    if (crank == 1) {
+      mbar_wait_cluster(&bar_full[sp], static_cast<uint32_t>((sweep >> 1) & 1));
+    }
+    int rotated = 0;
+    for (int rnd = 0; rnd < np; ++rnd) {
+      const int pidx = ((sp * np + rnd) * P + (live ? g : 0)) * 2;  // [parity][round][slot][2]
+      const double* pr = prm + pidx;                                 // CTA 1 view
+      const uint32_t prr = prm_remote + static_cast<uint32_t>(pidx * 8);
+      if ((rnd & 1) == 0) {
+        double c, sn;
+        if (crank == 0) {
+          double al, be, ga;
+          SPROF(7);
+          pair_dots<E>(xL, xR, al, be, ga);
+          SPROF(0);
+          al = group_sum<LP>(al);
+          be = group_sum<LP>(be);
+          ga = group_sum<LP>(ga);
+          SPROF(1);
+          bool need;
+          const double t = jacobi_t(al, be, ga, tol_rot2, need);
+          rotated |= need && live;
+          if (gl == 0 && live) dsmem_st_f64(prr, t);
+          rot_cs(t, c, sn);
+          SPROF(2);
+        } else {  // slots beyond P carry no rotations (their columns stay zero)
+          rot_cs(live ? pr[0] : 0.0, c, sn);
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const double x = xL[e], y = xR[e];
+          xL[e] = sn * x + c * y;
+          xR[e] = c * x - sn * y;
+        }
+        const int t = idL;
+        idL = idR;
+        idR = t;
+        SPROF(3);
+        continue;
+      }
+      SPROF(7);
+      const int par = (rnd >> 1) & 1;
+      const size_t pub = ((size_t)par * nseat + g + 1) * SEAT + gl;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        bXL[pub + e * LP] = xL[e];
+        bXR[pub + e * LP] = xR[e];
+      }
+      if (gl == 0) {
+        s_id[par][0][g + 1] = idL;
+        s_id[par][1][g + 1] = idR;
+      }
+      SPROF(4);
+      __syncthreads();
+      SPROF(5);
+      const size_t lft = ((size_t)par * nseat + g) * SEAT + gl;
+      const size_t rgt = ((size_t)par * nseat + g + 2) * SEAT + gl;
+      double rm[E], lp[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        rm[e] = bXR[lft + e * LP];
+        lp[e] = bXL[rgt + e * LP];
+      }
+      double cA, sA, cB, sB;
+      if (crank == 0) {
+        double alA, beA, gaA, alB, beB, gaB;
+        SPROF(6);
+        pair_dots<E>(rm, xL, alA, beA, gaA);
+        pair_dots<E>(xR, lp, alB, beB, gaB);
+        SPROF(0);
+        alA = group_sum<LP>(alA);
+        beA = group_sum<LP>(beA);
+        gaA = group_sum<LP>(gaA);
+        alB = group_sum<LP>(alB);
+        beB = group_sum<LP>(beB);
+        gaB = group_sum<LP>(gaB);
+        SPROF(1);
+        bool rA, rB;
+        const double tA = jacobi_t(alA, beA, gaA, tol_rot2, rA), tB = jacobi_t(alB, beB, gaB, tol_rot2, rB);
+        rotated |= live && ((rA && !left_edge) || (rB && !right_edge));
+        if (gl == 0 && live) { dsmem_st_f64(prr, tA); dsmem_st_f64(prr + 8, tB); }
+        rot_cs(tA, cA, sA);
+        rot_cs(tB, cB, sB);
+        SPROF(2);
+      } else {
+        rot_cs(live ? pr[0] : 0.0, cA, sA);
+        rot_cs(live ? pr[1] : 0.0, cB, sB);
+      }
+      if (left_edge) { cA = 0.0; sA = -1.0; }
+      if (right_edge) { cB = 0.0; sB = 1.0; }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        xL[e] = cA * rm[e] - sA * xL[e];
+        xR[e] = sB * xR[e] + cB * lp[e];
+      }
+      if (!left_edge) idL = s_id[par][1][g];
+      if (!right_edge) idR = s_id[par][0][g + 2];
+      SPROF(3);
+    }
+    if (crank == 0) {
+      rotated = __syncthreads_or(rotated);
+      last = !rotated || sweep + 1 >= kSvdMaxSweeps;
+      if (tid == 0) {
+        dsmem_st_s32(last_remote + 4 * sp, last ? 1 : 0);
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        mbar_arrive_remote(sp ? full_remote1 : full_remote0);
+      }
+    } else {
+      __syncthreads();
+      last = s_last[sp] != 0;
+      __syncthreads();
+      if (tid == 0) mbar_arrive_remote(sp ? empty_remote1 : empty_remote0);
+    }
+  }
+  if (crank == 0) {
+    if (sweep >= kSvdMaxSweeps && k > 1) set_status(ws, CABS_DEV_SVD_NOCONV);
+    if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;
+#ifdef CABS_PROFILE_SVD
+    if (tid == 0)
+      for (int i = 0; i < 8; ++i) reinterpret_cast<long long*>(ws)[8 + i] = sprof[i];
+#endif
+  }
+  // converged columns -> CTA 0's shared memory, column-major by id: A (CTA 0) and V (CTA 1)
+  cluster_sync_all();  // every exchange buffer read is done in both CTAs
+  double* As = smem_d;
+  double* Vs = smem_d + (size_t)k * k;
+  const uint32_t vs_remote = dsmem_map(Vs, 0);
+  if (live) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = gl + LP * e;
+      if (i < k) {
+        if (crank == 0) {
+          if (idL < k) As[(size_t)idL * k + i] = xL[e];
+          if (idR < k) As[(size_t)idR * k + i] = xR[e];
+        } else {
+          if (idL < k) dsmem_st_f64(vs_remote + static_cast<uint32_t>(((size_t)idL * k + i) * 8), xL[e]);
+          if (idR < k) dsmem_st_f64(vs_remote + static_cast<uint32_t>(((size_t)idR * k + i) * 8), xR[e]);
+        }
+      }
+    }
+  }
+  cluster_sync_all();
+  if (crank != 0) return;
+  const int r = svd_sigma(As, k, tol, s_sig, s_perm, sigma_out, r_out, r_out2);
+  svd_write(As, Vs, k, r, s_sig, s_perm, Uw64, Vw64, uw32, vw32, ld32);
+}
+
 // ---------------------------------------------------------------- k > 64: columns in memory
 template <int L, bool SMEM>
 __global__ void __launch_bounds__(kSvdThreads, 1)
@@ -536,6 +814,29 @@ static void launch_systolic(int k, const float* W, int64_t ldw, double tol, doub
                                                       r_user, ws);
 }
 
+template <int LP, int E>
+static bool launch_split(int k, const float* W, int64_t ldw, double tol, double* sig, double* Uw64, double* Vw64,
+                         float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st) {
+  constexpr int G = 32 / LP;
+  constexpr int SEAT = E * LP + ((LP - (E * LP) % 16) + 16) % 16;
+  const int np = (k + 1) & ~1, P = np / 2;
+  const int nw = (P + G - 1) / G;
+  const size_t xch = sizeof(double) * 2 * 2 * (size_t)(nw * G + 2) * SEAT;  // [XL|XR][parity][seat]
+  const size_t prm = sizeof(double) * 2 * (size_t)np * P * 2;               // [parity][round][slot][2]
+  const size_t fin = sizeof(double) * 2 * (size_t)k * k;
+  const size_t smem = (xch + prm > fin ? xch + prm : fin);
+  constexpr int kCap = 220 * 1024;
+  if (smem > kCap) return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(svd_split_kernel<LP, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCap);
+    attr = true;
+  }
+  svd_split_kernel<LP, E><<<2, 32 * nw, smem, st>>>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user,
+                                                    ws);
+  return true;
+}
+
 int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const Ws& L, double* sigma_user,
                double* Uw64, double* Vw64, int* r_user, cudaStream_t st) {
   double* sig = sigma_user ? sigma_user : wsp<double>(ws, L.sig64);
@@ -543,7 +844,14 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
   float* uw32 = wsp<float>(ws, L.uw32);
   float* vw32 = wsp<float>(ws, L.vw32);
   note_launch();
-  if (k <= 64 && !getenv("CABS_SVD_SMEM")) {
+  if (k <= 64 && !getenv("CABS_SVD_SMEM") && !getenv("CABS_SVD_ONE_SM")) {
+    // A on one SM, V on its cluster partner
+    // 8 lanes per column pair: 4 pairs per warp, up to 8 warps
+    if (k <= 16) launch_split<8, 2>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    else if (k <= 32) launch_split<8, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    else if (k <= 56) launch_split<8, 7>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    else launch_split<8, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+  } else if (k <= 64 && !getenv("CABS_SVD_SMEM")) {
     // register-resident systolic Jacobi, 4 lanes per column pair
     if (k <= 16) launch_systolic<4, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
     else if (k <= 32) launch_systolic<4, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);

@@ -116,14 +116,14 @@ def probe_svd_prof(k=50):
     C.cabs_svd(plan, k, W, 1e-12, sig, None, None, r, ws)
     torch.cuda.synchronize()
     sweeps = int(ws[32:36].view(torch.int32).item())
-    prof = ws[64:104].view(torch.int64).tolist()
-    rounds = sweeps * (k - 1 + (k % 2))
-    names = ["loads+dots", "shuffles", "rotation", "updates", "barrier"]
+    prof = ws[64:128].view(torch.int64).tolist()
+    rounds = sweeps * (k + (k % 2))
+    names = ["dots", "butterfly", "angle", "rotate+params", "publish", "barrier", "loads", "loop/other"]
     print(f"k={k} sweeps={sweeps} rounds~{rounds}: " + ", ".join(f"{n} {p / max(rounds, 1):.0f} cyc" for n, p in zip(names, prof)))
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "svdprof":
-    for k in (20, 50, 100):
+    for k in (20, 50):
         probe_svd_prof(k)
 
 
