@@ -212,6 +212,27 @@ int32_t cabs_select(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
                     int64_t* rep_of_centre, float* gap, void* ws, size_t ws_bytes,
                     const cabs_comm* comm, void* stream);
 
+/* One snap problem of cabs_select_pair: the arguments of cabs_select. */
+typedef struct cabs_sel_problem {
+  const float* X;               /* device n_loc x ldx (the embedding the k-means ran on) */
+  int64_t ldx, n_loc, n_glob, row_off;
+  int32_t d;
+  const float* centres;         /* device k2 x ldc */
+  int64_t ldc;
+  int32_t k2;
+  const double* cluster_w;      /* device double[k2] */
+  int64_t* reps;                /* device int64[k2] (out, ascending) */
+  int64_t* rep_of_centre;       /* device int64[k2] (out) or NULL */
+  float* gap;                   /* device float[k2] (out) or NULL */
+} cabs_sel_problem;
+
+/* Alg. 2 step 8 for BOTH sides: exactly cabs_select(a) and cabs_select(b) (same results),
+ * on a single GPU run concurrently -- b on a library-owned side stream forked from and
+ * joined back into `stream` -- with separate scratch.  Multi-rank runs them one after the
+ * other on `stream`.  Errors as cabs_select. */
+int32_t cabs_select_pair(const cabs_plan* plan, const cabs_sel_problem* a, const cabs_sel_problem* b,
+                         void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream);
+
 /* ---------------------------------------------------------------- S9 sketch
  * Follow-up sketching, or a sketch from any given index sets:
  * gathers Cbar = A(:,Ic), Rbar = A(Ir,:), Wbar = A(Ir,Ic) (Ir, Ic: device int64[k],

@@ -75,6 +75,13 @@ class KmProblem(ctypes.Structure):
                 ("near_ties", c_vp)]
 
 
+class SelProblem(ctypes.Structure):
+    """cabs_sel_problem: one side (rows or columns) of cabs_select_pair."""
+    _fields_ = [("X", c_vp), ("ldx", c_i64), ("n_loc", c_i64), ("n_glob", c_i64), ("row_off", c_i64),
+                ("d", c_i32), ("centres", c_vp), ("ldc", c_i64), ("k2", c_i32), ("cluster_w", c_vp),
+                ("reps", c_vp), ("rep_of_centre", c_vp), ("gap", c_vp)]
+
+
 _SIGS = {
     "cabs_status_string": (ctypes.c_char_p, [c_i32]),
     "cabs_last_error_string": (ctypes.c_char_p, []),
@@ -97,6 +104,8 @@ _SIGS = {
                                  c_i32, c_f32, c_u64, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_select": (c_i32, [ctypes.POINTER(Plan), c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_vp, c_i64,
                             c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_select_pair": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(SelProblem), ctypes.POINTER(SelProblem), c_vp,
+                                 c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_sketch": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_vp, c_vp, c_i32, c_i32, c_f64,
                             c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz,
                             ctypes.POINTER(Comm), c_vp]),
@@ -248,6 +257,19 @@ def cabs_select(plan, X, n_loc, n_glob, row_off, d, centres, k2, cluster_w, reps
                               int(d), _p(centres), _ld(centres), int(k2), _p(cluster_w), _p(reps),
                               _p(rep_of_centre), _p(gap), _p(ws), ws.numel(), _comm(comm),
                               _stream(stream)), "cabs_select")
+
+
+def sel_problem(X, n_loc, n_glob, row_off, d, centres, k2, cluster_w, reps, rep_of_centre=None, gap=None):
+    """Describe one side of cabs_select_pair (tensors must outlive the call)."""
+    def ptr(t):
+        return None if t is None else t.data_ptr()
+    return SelProblem(ptr(X), _ld(X), int(n_loc), int(n_glob), int(row_off), int(d), ptr(centres), _ld(centres),
+                      int(k2), ptr(cluster_w), ptr(reps), ptr(rep_of_centre), ptr(gap))
+
+
+def cabs_select_pair(plan, a, b, ws, comm=None, stream=None):
+    _check(load().cabs_select_pair(ctypes.byref(plan), ctypes.byref(a), ctypes.byref(b), _p(ws), ws.numel(),
+                                   _comm(comm), _stream(stream)), "cabs_select_pair")
 
 
 def cabs_sketch(plan, A, Ir, Ic, k, mode, tol, U, s, V, r, ws, sigma=None, comm=None, stream=None):

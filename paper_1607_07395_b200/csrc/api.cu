@@ -399,6 +399,41 @@ int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const 
 }
 
 // ---------------------------------------------------------------- S8
+static int32_t sel_check(const cabs_plan* plan, const Ws& L, const cabs_sel_problem& p) {
+  if (p.k2 < 1 || p.k2 > plan->kmax || p.k2 > p.n_glob) return arg_error("select: bad k2");
+  if (p.d < 1 || p.ldx < p.d || p.ldc < p.d || p.n_loc < 0 || p.n_loc > L.Nmax) return arg_error("select: bad dims");
+  if (!p.centres || !p.cluster_w || !p.reps || (p.n_loc > 0 && !p.X)) return arg_error("select: bad buffers");
+  return CABS_OK;
+}
+
+// snap of one problem with the scratch of slot q
+static int32_t sel_run(const cabs_sel_problem& p, int q, void* ws, const Ws& L, const cabs_comm* comm, void* stream) {
+  cudaStream_t st = S(stream);
+  float* D = wsp<float>(ws, q ? L.dist2 : L.dist);
+  float* cd = wsp<float>(ws, q ? L.cand_d2 : L.cand_d);
+  int64_t* ci = wsp<int64_t>(ws, q ? L.cand_i2 : L.cand_i);
+  double* all = wsp<double>(ws, q ? L.cand_all2 : L.cand_all);
+  const bool mr = multi(comm);
+  const int T = mr ? kSnapTMulti : kSnapT;
+  launch_km_distmat(p.X, p.ldx, p.n_loc, p.d, p.centres, p.ldc, p.k2, D, L.Nmax, st);
+  // per-centre top-T over S point segments in parallel; lists packed as doubles so that
+  // other ranks' slots (zeros here) are completed by ONE sum-allreduce, then merged
+  int Sg = static_cast<int>(ceil_div(p.n_loc > 0 ? p.n_loc : 1, 4096));
+  if (Sg > kSnapSeg) Sg = kSnapSeg;
+  const int nr = mr ? comm->nranks : 1;
+  const int64_t nall = 2LL * nr * Sg * p.k2 * T;
+  if (mr) CABS_CUDA_TRY(cudaMemsetAsync(all, 0, sizeof(double) * nall, st));
+  if (p.n_loc > 0) launch_snap_topT(D, L.Nmax, p.n_loc, p.k2, p.row_off, T, Sg, (mr ? comm->rank : 0) * Sg, all, st);
+  CABS_LAUNCH_CHECK("snap distmat/topT");
+  CABS_TRY(comm_f64(comm, all, nall, stream));
+  launch_snap_merge(all, p.k2, T, nr * Sg, cd, ci, st);
+  CABS_LAUNCH_CHECK("snap_merge");
+  launch_snap_dedupe(cd, ci, p.k2, T, p.cluster_w, D, L.Nmax, p.n_loc, p.row_off, !mr, p.rep_of_centre, p.gap,
+                     p.reps, ws, st);
+  CABS_LAUNCH_CHECK("snap_dedupe");
+  return CABS_OK;
+}
+
 int32_t cabs_select(const cabs_plan* plan, const float* X, int64_t ldx, int64_t n_loc, int64_t n_glob, int64_t row_off,
                     int32_t d, const float* centres, int64_t ldc, int32_t k2, const double* cluster_w, int64_t* reps,
                     int64_t* rep_of_centre, float* gap, void* ws, size_t ws_bytes, const cabs_comm* comm,
@@ -406,32 +441,54 @@ int32_t cabs_select(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   CABS_TRY(check_plan(plan));
   Ws L;
   CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
-  if (k2 < 1 || k2 > plan->kmax || k2 > n_glob) return arg_error("select: bad k2");
-  if (d < 1 || ldx < d || ldc < d || n_loc < 0 || n_loc > L.Nmax) return arg_error("select: bad dims");
-  if (!centres || !cluster_w || !reps || (n_loc > 0 && !X)) return arg_error("select: bad buffers");
-  cudaStream_t st = S(stream);
-  float* D = wsp<float>(ws, L.dist);
-  float* cd = wsp<float>(ws, L.cand_d);
-  int64_t* ci = wsp<int64_t>(ws, L.cand_i);
-  const bool mr = multi(comm);
-  const int T = mr ? kSnapTMulti : kSnapT;
-  launch_km_distmat(X, ldx, n_loc, d, centres, ldc, k2, D, L.Nmax, st);
-  // per-centre top-T over S point segments in parallel; lists packed as doubles so that
-  // other ranks' slots (zeros here) are completed by ONE sum-allreduce, then merged
-  int S = static_cast<int>(ceil_div(n_loc > 0 ? n_loc : 1, 4096));
-  if (S > kSnapSeg) S = kSnapSeg;
-  const int nr = mr ? comm->nranks : 1;
-  double* all = wsp<double>(ws, L.cand_all);
-  const int64_t nall = 2LL * nr * S * k2 * T;
-  if (mr) CABS_CUDA_TRY(cudaMemsetAsync(all, 0, sizeof(double) * nall, st));
-  if (n_loc > 0) launch_snap_topT(D, L.Nmax, n_loc, k2, row_off, T, S, (mr ? comm->rank : 0) * S, all, st);
-  CABS_LAUNCH_CHECK("snap distmat/topT");
-  CABS_TRY(comm_f64(comm, all, nall, stream));
-  launch_snap_merge(all, k2, T, nr * S, cd, ci, st);
-  CABS_LAUNCH_CHECK("snap_merge");
-  launch_snap_dedupe(cd, ci, k2, T, cluster_w, D, L.Nmax, n_loc, row_off, !mr, rep_of_centre, gap, reps, ws, st);
-  CABS_LAUNCH_CHECK("snap_dedupe");
+  const cabs_sel_problem p{X, ldx, n_loc, n_glob, row_off, d, centres, ldc, k2, cluster_w, reps, rep_of_centre, gap};
+  CABS_TRY(sel_check(plan, L, p));
+  return sel_run(p, 0, ws, L, comm, stream);
+}
+
+// A library-owned non-blocking side stream per device (and fork/join events) for the
+// second problem of the *_pair entry points.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static int32_t side_stream(SideStream** out) {
+  static SideStream side[64];
+  int dev = 0;
+  CABS_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return arg_error("device index out of range");
+  SideStream& ss = side[dev];
+  if (!ss.s) {
+    CABS_CUDA_TRY(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    CABS_CUDA_TRY(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    CABS_CUDA_TRY(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  *out = &ss;
   return CABS_OK;
+}
+
+int32_t cabs_select_pair(const cabs_plan* plan, const cabs_sel_problem* a, const cabs_sel_problem* b, void* ws,
+                         size_t ws_bytes, const cabs_comm* comm, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  if (!a || !b) return arg_error("select_pair: null problem");
+  CABS_TRY(sel_check(plan, L, *a));
+  CABS_TRY(sel_check(plan, L, *b));
+  if (multi(comm)) {  // the collectives run on the caller's stream: one problem after the other
+    CABS_TRY(sel_run(*a, 0, ws, L, comm, stream));
+    return sel_run(*b, 1, ws, L, comm, stream);
+  }
+  SideStream* ss = nullptr;
+  CABS_TRY(side_stream(&ss));
+  cudaStream_t st = S(stream);
+  CABS_CUDA_TRY(cudaEventRecord(ss->fork, st));
+  CABS_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+  const int32_t ra = sel_run(*a, 0, ws, L, comm, stream);
+  const int32_t rb = sel_run(*b, 1, ws, L, comm, ss->s);
+  CABS_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
+  CABS_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));
+  return ra != CABS_OK ? ra : rb;
 }
 
 // ---------------------------------------------------------------- S10

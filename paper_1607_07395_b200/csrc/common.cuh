@@ -28,7 +28,8 @@ struct Ws {
   size_t norm_part, norms, scales;
   size_t km_w, km_scr, km_pobj, km_ptie, km_red, km_cnt;  // km_w, km_scr, km_cnt: two problems
   size_t km_scr_bytes;                                     // per problem
-  size_t dist, cand_d, cand_i, cand_all;
+  size_t dist, cand_d, cand_i, cand_all;  // snap scratch of problem slot 0 ...
+  size_t dist2, cand_d2, cand_i2, cand_all2;  // ... and slot 1 (cabs_select_pair)
   size_t idx;
   size_t cb, rb, wb;
   size_t res_part, res_split;  // res_split: G_hi, G_lo (n x 64 each)
@@ -81,6 +82,10 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.cand_d = take(sizeof(float) * K * kSnapTMulti);
   w.cand_i = take(sizeof(int64_t) * K * kSnapTMulti);
   w.cand_all = take(sizeof(double) * 2 * nr * kSnapSeg * K * kSnapTMulti);
+  w.dist2 = take(sizeof(float) * K * w.Nmax);
+  w.cand_d2 = take(sizeof(float) * K * kSnapTMulti);
+  w.cand_i2 = take(sizeof(int64_t) * K * kSnapTMulti);
+  w.cand_all2 = take(sizeof(double) * 2 * nr * kSnapSeg * K * kSnapTMulti);
   w.idx = take(sizeof(int64_t) * 8 * Kp);
   w.cb = take(sizeof(float) * (w.m_loc > 0 ? w.m_loc : 1) * Kp);
   w.rb = take(sizeof(float) * K * w.ldrb);

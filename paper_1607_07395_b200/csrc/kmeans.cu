@@ -49,8 +49,16 @@ __global__ void __launch_bounds__(256) km_weights_kernel(const float* __restrict
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) {
-    if (pos) atomicAdd(cnt, pos);
+  // block-level combine: one set of atomics per CTA (the bounds are maxima: order-free)
+  __shared__ float s_mx[8], s_mw[8];
+  __shared__ int s_pos[8];
+  const int wib = threadIdx.x >> 5;
+  if (lane == 0) { s_mx[wib] = mx; s_mw[wib] = mw; s_pos[wib] = pos; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tp = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { mx = fmaxf(mx, s_mx[q]); mw = fmaxf(mw, s_mw[q]); tp += s_pos[q]; }
+    if (tp) atomicAdd(cnt, tp);
     atomicMax(bounds, __float_as_uint(mx));
     atomicMax(bounds + 1, __float_as_uint(mw));
   }
@@ -60,7 +68,7 @@ void launch_km_weights(const float* X, int64_t ldx, int64_t N, int d, int kind, 
                        unsigned* bounds, cudaStream_t st) {
   if (N <= 0) return;
   int64_t blocks = ceil_div(N, 8);
-  if (blocks > 8 * kNumSM) blocks = 8 * kNumSM;
+  if (blocks > 2 * kNumSM) blocks = 2 * kNumSM;
   note_launch();
   km_weights_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(X, ldx, N, d, kind, p, w, cnt, bounds);
 }

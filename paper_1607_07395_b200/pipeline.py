@@ -6,7 +6,7 @@ entry points of libcabs.so in order on one stream:
   S1-S3 cabs_pilot    pilot sampling and gathers C, R, W
   S4-S5 cabs_embed    pilot sketch -> embeddings P, Q
   S6-S7 cabs_kmeans_pair  weighted Lloyd on P (rows) and on Q (columns), one kernel  (Eq. 6)
-  S8    cabs_select   snap centres to in-sample rows / columns
+  S8    cabs_select_pair   snap centres to in-sample rows / columns
   S9    cabs_sketch   follow-up gathers + sketch -> Ubar, sbar, Vbar
   S10   cabs_residual ||A - Ubar diag(sbar) Vbar^T||_F^2, ||A||_F^2
 
@@ -96,10 +96,12 @@ class CabsPipeline:
 
     def select(self):
         c, p = self.cfg, self.plan
-        C.cabs_select(p, self.P, p.m_loc, p.m, p.row_begin, c.k1, self.cen_r, c.k2, self.cw_r, self.Ib,
-                      self.ws, rep_of_centre=self.rep_r, gap=self.gap_r, comm=self.comm)
-        C.cabs_select(p, self.Q, p.n_sl, p.n, p.col_begin, c.k1, self.cen_c, c.k2, self.cw_c, self.Jb,
-                      self.ws, rep_of_centre=self.rep_c, gap=self.gap_c, comm=self.comm)
+        # both sides in one call: concurrent on a single GPU
+        rows = C.sel_problem(self.P, p.m_loc, p.m, p.row_begin, c.k1, self.cen_r, c.k2, self.cw_r, self.Ib,
+                             rep_of_centre=self.rep_r, gap=self.gap_r)
+        cols = C.sel_problem(self.Q, p.n_sl, p.n, p.col_begin, c.k1, self.cen_c, c.k2, self.cw_c, self.Jb,
+                             rep_of_centre=self.rep_c, gap=self.gap_c)
+        C.cabs_select_pair(p, rows, cols, self.ws, comm=self.comm)
 
     def sketch(self):
         c, p = self.cfg, self.plan

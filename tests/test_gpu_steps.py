@@ -409,6 +409,35 @@ def test_kmeans_pair_equals_two_single_calls(dev, monkeypatch):
     assert np.array_equal(bl[1].cpu().numpy(), single[0][1]) and np.array_equal(bl[0].cpu().numpy(), single[0][0])
 
 
+def test_select_pair_equals_two_single_calls(dev):
+    """cabs_select_pair (second side on the library's side stream) == cabs_select per side."""
+    d, k2 = 30, 25
+    Na, Nb = 7000, 3000
+    ld = C.cabs_padded_ld(d)
+    Xa = torch.zeros((Na, ld), device=dev); Xa[:, :d] = torch.from_numpy(_clustered(Na, d, 20, 31)).to(dev)
+    Xb = torch.zeros((Nb, ld), device=dev); Xb[:, :d] = torch.from_numpy(_clustered(Nb, d, 15, 32)).to(dev)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    ca = torch.zeros((k2, ld), device=dev); ca[:, :d] = torch.randn(k2, d, generator=g).to(dev)
+    cb = torch.zeros((k2, ld), device=dev); cb[:, :d] = torch.randn(k2, d, generator=g).to(dev)
+    wa = torch.rand(k2, generator=g, dtype=torch.float64).to(dev)
+    wb = torch.rand(k2, generator=g, dtype=torch.float64).to(dev)
+    plan = _plan(Na, Nb, max(d, k2))
+    ws = _ws(plan, dev)
+    ref = []
+    for X, N, cen, cw in ((Xa, Na, ca, wa), (Xb, Nb, cb, wb)):
+        reps = torch.zeros(k2, dtype=torch.int64, device=dev)
+        roc = torch.zeros(k2, dtype=torch.int64, device=dev)
+        C.cabs_select(plan, X, N, N, 0, d, cen, k2, cw, reps, ws, rep_of_centre=roc)
+        ref.append((reps.cpu().numpy(), roc.cpu().numpy()))
+    out = [(torch.zeros(k2, dtype=torch.int64, device=dev), torch.zeros(k2, dtype=torch.int64, device=dev))
+           for _ in range(2)]
+    pa = C.sel_problem(Xa, Na, Na, 0, d, ca, k2, wa, out[0][0], rep_of_centre=out[0][1])
+    pb = C.sel_problem(Xb, Nb, Nb, 0, d, cb, k2, wb, out[1][0], rep_of_centre=out[1][1])
+    C.cabs_select_pair(plan, pa, pb, ws)
+    for (r, c), (rr, cc) in zip(out, ref):
+        assert np.array_equal(r.cpu().numpy(), rr) and np.array_equal(c.cpu().numpy(), cc)
+
+
 def test_embed_drops_zero_norm_component_with_compaction(dev):
     """S:244 drop rule with a hole: component 0 extrapolates to zero, component 1 is kept,
     so the kept component must be compacted to position 0 (inconsistent triple, as in the
