@@ -371,15 +371,32 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
           for (int q0 = 0; q0 < np; q0 += 32) {
             const int qq = q0 + lane;
             unsigned m = __ballot_sync(0xffffffffu, qq < np && (lab_s[qq] & 7) == warp);
-            while (m) {
-              const int p = q0 + __ffs(m) - 1;
+            while (m) {  // two points per step: independent convert chains, one RMW if same cluster
+              const int p1 = q0 + __ffs(m) - 1;
               m &= m - 1;
-              const int j = lab_s[p];
-              const double ws = S.wsc[p];
-              const float* xrow = xr + p * d;
-              long long* prow = pp + (int64_t)j * d;
-              for (int i = lane; i < d; i += 32) prow[i] += fx_prod_magic(ws, xrow[i]);
-              if (lane == 0) pp[nsum + j] += S.iw[p];
+              const bool two = m != 0;
+              const int p2 = two ? q0 + __ffs(m) - 1 : p1;
+              if (two) m &= m - 1;
+              const int j1 = lab_s[p1], j2 = lab_s[p2];
+              const double w1 = S.wsc[p1], w2 = two ? S.wsc[p2] : 0.0;
+              const float* x1 = xr + p1 * d;
+              const float* x2 = xr + p2 * d;
+              long long* r1 = pp + (int64_t)j1 * d;
+              long long* r2 = pp + (int64_t)j2 * d;
+#pragma unroll 2
+              for (int i = lane; i < d; i += 32) {
+                const long long v1 = fx_prod_magic(w1, x1[i]), v2 = fx_prod_magic(w2, x2[i]);
+                if (j1 == j2) {
+                  r1[i] += v1 + v2;
+                } else {
+                  r1[i] += v1;
+                  r2[i] += v2;
+                }
+              }
+              if (lane == 0) {
+                pp[nsum + j1] += S.iw[p1];
+                if (two) pp[nsum + j2] += S.iw[p2];
+              }
             }
           }
         }
@@ -414,23 +431,36 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
       }
     }
     LPROF(6);
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < kMaxProb; ++q) {
+        if (q >= np_) break;
+        double sacc = 0;
+        int qq = 0;
+        for (int w = 0; w < kLT / 32; ++w) { sacc += s_red[q][w]; qq += s_tie[q][w]; }
+        a.pr[q].pobj[(size_t)it * G + b] = sacc;
+        a.pr[q].ptie[(size_t)it * G + b] = qq;
+      }
+    }
     __threadfence();
     LPROF(7);
     cluster.sync();  // partials free again; this cluster's global adds issued and fenced
     LPROF(8);
-    if (tid == 0) {
-  #pragma unroll
-    for (int q = 0; q < kMaxProb; ++q) {
-      if (q >= np_) break;
-        double s = 0;
-        int qq = 0;
-        for (int w = 0; w < kLT / 32; ++w) { s += s_red[q][w]; qq += s_tie[q][w]; }
-        a.pr[q].pobj[(size_t)it * G + b] = s;
-        a.pr[q].ptie[(size_t)it * G + b] = qq;
+    // grid barrier between cluster leaders only, then the cluster barrier releases the members
+    if (crank == 0 && tid == 0) {
+      unsigned* bar = a.gbar;
+      const unsigned nb = static_cast<unsigned>(G / csize);
+      if (atomicAdd(bar, 1u) == nb - 1) {
+        atomicExch(bar, 0u);
+        __threadfence();
+        atomicExch(bar + 1, gen + 1);
+      } else {
+        while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(20);
       }
     }
+    ++gen;
     LPROF(3);
-    grid_barrier(a.gbar, gen);
+    cluster.sync();
     LPROF(4);
   }
 #ifdef CABS_PROFILE_LLOYD
