@@ -47,6 +47,19 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def traffic_of(traffic, key):
+    t = traffic.get(key)
+    return t.get("dram_bytes_per_launch") if isinstance(t, dict) else None
+
+
+def m_loc_rows(plan):
+    return plan.row_end - plan.row_begin
+
+
+def n_loc_cols(plan):
+    return plan.col_end - plan.col_begin
+
+
 def load_traffic():
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
@@ -270,14 +283,36 @@ def main():
         return 0
     peaks, peak_src = load_peaks()
     traffic = load_traffic()
-    # ---- roofline of the dominant kernel: the fused residual (S10), HBM-bound: it must
-    # stream A once (m*n*4 bytes) plus the factors F (m*k2*4) and G (n*k2*4).
+    # ---- rooflines.  The dominant kernel of the step is the persistent
+    # Lloyd kernel (S6-S7, both sides in one launch): FP32 ALU-bound -- per (point, centre,
+    # dimension) one FADD + one FFMA (direct differences) = 3 flops in 2 FP32 lane-ops, so the
+    # attainable peak is 3/4 of the FFMA peak 148 SM x 128 lanes x 2 flops x max SM clock.
+    # Timed as the k-means phase (the launch plus the small weight / init kernels before it).
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    ffma_tf = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+    lloyd_peak = 0.75 * ffma_tf
+    d_emb = int(pipe.r1.item())  # embedding dimension r <= k1 the k-means runs on
+    lloyd_flops = 3.0 * cfg.iters * (m_loc_rows(plan) + n_loc_cols(plan)) * cfg.k2 * d_emb
+    km_ms = step_mean["kmeans"]
+    lloyd = {"kernel": "lloyd_persistent_kernel (cabs_kmeans_pair: both sides, all iterations, one launch)",
+             "bound": "alu", "achieved": lloyd_flops / (km_ms / 1e3) / 1e12, "peak": lloyd_peak, "unit": "TFLOP/s",
+             "traffic": traffic_of(traffic, "lloyd"),
+             "peak_source": f"derived: 0.75 x FFMA peak (148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz = "
+                            f"{ffma_tf:.1f} TFLOP/s); direct-difference op mix FADD+FFMA",
+             "algorithmic_flops_per_launch": lloyd_flops, "launch_ms": km_ms}
+    lloyd["frac"] = lloyd["achieved"] / lloyd["peak"]
+    # the fused residual (S10), HBM-bound: it must stream A once (m*n*4 bytes) plus the factors
+    # F (m*k2*4) and G (n*k2*4).
     m_loc = plan.row_end - plan.row_begin
     res_bytes = 4.0 * (m_loc * cfg.n + m_loc * cfg.k2 + cfg.n * cfg.k2)
     res_ms = step_mean["residual"]
     achieved = res_bytes / (res_ms / 1e3) / 1e9
     peak = float(peaks["hbm_gbs"])
-    t_res = traffic.get("residual", {}).get("dram_bytes_per_launch") if isinstance(traffic.get("residual"), dict) else None
+    residual = {"kernel": "residual_tc_kernel (cabs_residual: fused F diag(s) G^T - A, squared-sum)", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic_of(traffic, "residual"),
+                "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
+                "algorithmic_bytes_per_launch": res_bytes, "launch_ms": res_ms}
     kmeans_pts = cfg.iters * (cfg.m + cfg.n) / (step_mean["kmeans"] / 1e3)
     sketch_ms = sum(step_mean[s] for s in STEPS if s != "residual")
     line = {
@@ -292,10 +327,8 @@ def main():
         "sketch_ms": sketch_ms,
         "sketch_rows_cols_per_s": (cfg.m + cfg.n) / (sketch_ms / 1e3),
         "kmeans_pts_per_s": kmeans_pts,
-        "roofline": {"kernel": "residual (cabs_residual: fused F diag(s) G^T - A, squared-sum)", "bound": "hbm",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": t_res, "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
-                     "algorithmic_bytes_per_launch": res_bytes, "launch_ms": res_ms},
+        "roofline": lloyd,
+        "rooflines": {"lloyd": lloyd, "residual": residual},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "quality": {"rel_err_followup": math.sqrt(max(res["resid_sq"], 0) / res["a_sq"]),

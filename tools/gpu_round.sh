@@ -1,7 +1,7 @@
 #!/usr/bin/env bash
 # gpu_round.sh -- one GPU box session: build, GPU tests, smoke, bench, ncu launch list and
 # one full capture of the named kernel.  Usage (under gpurun):
-#   bash tools/gpu_round.sh [kernel-regex] [tag]
+#   bash tools/gpu_round.sh ["kernel-regex ..."] [tag]   (one full capture per regex)
 # Outputs land in gpurun_out/<tag>_*.
 set -u
 K=${1:-residual_tc_kernel}
@@ -16,6 +16,8 @@ timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${T}_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/${T}_ncu_launch.log 2>&1
 echo "ncu launch exit=$?" >> $O/${T}_ncu_launch.log
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${K}" -s 3 -c 1 -o $O/${T}_full -f \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/${T}_ncu_full.log 2>&1
-echo "ncu full exit=$?" >> $O/${T}_ncu_full.log
+for KK in $K; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${KK}" -s 3 -c 1 -o $O/${T}_full_${KK} -f \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/${T}_ncu_full_${KK}.log 2>&1
+  echo "ncu full exit=$?" >> $O/${T}_ncu_full_${KK}.log
+done

@@ -63,8 +63,8 @@ def main():
     bj = os.path.join(go, f"{tag}_bench.json")
     if os.path.exists(bj):
         shutil.copy(bj, os.path.join(prof, f"{tag}_bench.json"))
-    rep = os.path.join(go, f"{tag}_full.ncu-rep")
-    if os.path.exists(rep):
+    import glob
+    for rep in sorted(glob.glob(os.path.join(go, f"{tag}_full*.ncu-rep"))):
         h, u, data = ncu_raw(rep)
         for v in data:
             name = v[h.index("Kernel Name")].split("(")[0].replace("void ", "").replace("cabsk::", "")
@@ -80,7 +80,8 @@ def main():
             wr = float(v[h.index("dram__bytes_write.sum")]) * scale[u[h.index("dram__bytes_write.sum")]]
             tj = os.path.join(prof, "traffic.json")
             t = json.load(open(tj)) if os.path.exists(tj) else {}
-            t[key] = {"kernel": name, "dram_bytes_per_launch": rd + wr, "source": f"profiles/{tag}_{name}_ncu.txt"}
+            k = "lloyd" if "lloyd" in name else ("residual" if "residual" in name else ("svd" if "svd" in name else key))
+            t[k] = {"kernel": name, "dram_bytes_per_launch": rd + wr, "source": f"profiles/{tag}_{name}_ncu.txt"}
             json.dump(t, open(tj, "w"), indent=1)
             print(open(os.path.join(prof, f"{tag}_{name}_ncu.txt")).read())
 
