@@ -68,6 +68,7 @@ def main():
         h, u, data = ncu_raw(rep)
         for v in data:
             name = v[h.index("Kernel Name")].split("(")[0].replace("void ", "").replace("cabsk::", "")
+            name = name.replace("<", "_").replace(">", "").replace(", ", "_").replace(",", "_").replace(" ", "")
             lines = [f"# ncu --set full --clock-control none, one launch of {name}"]
             for k in KEYS:
                 if k in h:
