@@ -497,6 +497,7 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
   __shared__ int s_id[2][2][34];
   __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2];  // full: in CTA 1, empty: in CTA 0
   __shared__ int s_last[2];                                    // CTA 1: last sweep flag per parity
+  __shared__ double s_nrm[2][2][34];                           // CTA 0: published squared norms [parity][L|R][seat]
   const uint32_t crank = cg::this_cluster().block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int gl = lane % LP, gw = lane / LP;
@@ -517,6 +518,7 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
     tc::mbar_fence_init();
   }
   for (int e = tid; e < 2 * (int)arr; e += blockDim.x) smem_d[e] = 0.0;
+  for (int e = tid; e < 2 * 2 * 34; e += blockDim.x) (&s_nrm[0][0][0])[e] = 0.0;
   cluster_sync_all();
 
   double xL[E], xR[E];  // CTA 0: columns of A; CTA 1: columns of V
@@ -565,6 +567,16 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
       mbar_wait_cluster(&bar_full[sp], static_cast<uint32_t>((sweep >> 1) & 1));
     }
     int rotated = 0;
+    // squared column norms: recomputed exactly at every sweep start, then carried through
+    // the rotations by the exact 2x2 formulas, so a round reduces only the cross products
+    double nL = 0.0, nR = 0.0;
+    if (crank == 0) {
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) { t0 = fma(xL[e], xL[e], t0); t1 = fma(xR[e], xR[e], t1); }
+      nL = group_sum<LP>(t0);
+      nR = group_sum<LP>(t1);
+    }
     for (int rnd = 0; rnd < np; ++rnd) {
       const int pidx = ((sp * np + rnd) * P + (live ? g : 0)) * 2;  // [parity][round][slot][2]
       const double* pr = prm + pidx;                                 // CTA 1 view
@@ -572,19 +584,26 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
       if ((rnd & 1) == 0) {
         double c, sn;
         if (crank == 0) {
-          double al, be, ga;
           SPROF(7);
-          pair_dots<E>(xL, xR, al, be, ga);
+          double ga0 = 0.0, ga1 = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; e += 2) {
+            ga0 = fma(xL[e], xR[e], ga0);
+            if (e + 1 < E) ga1 = fma(xL[e + 1], xR[e + 1], ga1);
+          }
           SPROF(0);
-          al = group_sum<LP>(al);
-          be = group_sum<LP>(be);
-          ga = group_sum<LP>(ga);
+          const double ga = group_sum<LP>(ga0 + ga1);
           SPROF(1);
           bool need;
-          const double t = jacobi_t(al, be, ga, tol_rot2, need);
+          const double t = jacobi_t(nL, nR, ga, tol_rot2, need);
           rotated |= need && live;
           if (gl == 0 && live) dsmem_st_f64(prr, t);
           rot_cs(t, c, sn);
+          // new L = s x + c y, new R = c x - s y (the swap of the odd-even network)
+          const double cs2 = 2.0 * c * sn * ga, c2 = c * c, s2 = sn * sn;
+          const double nx = fma(c2, nL, fma(s2, nR, -cs2)), ny = fma(s2, nL, fma(c2, nR, cs2));
+          nL = ny;
+          nR = nx;
           SPROF(2);
         } else {  // slots beyond P carry no rotations (their columns stay zero)
           rot_cs(live ? pr[0] : 0.0, c, sn);
@@ -612,6 +631,10 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
       if (gl == 0) {
         s_id[par][0][g + 1] = idL;
         s_id[par][1][g + 1] = idR;
+        if (crank == 0) {
+          s_nrm[par][0][g + 1] = nL;
+          s_nrm[par][1][g + 1] = nR;
+        }
       }
       SPROF(4);
       __syncthreads();
@@ -626,24 +649,34 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
       }
       double cA, sA, cB, sB;
       if (crank == 0) {
-        double alA, beA, gaA, alB, beB, gaB;
         SPROF(6);
-        pair_dots<E>(rm, xL, alA, beA, gaA);
-        pair_dots<E>(xR, lp, alB, beB, gaB);
+        double gA0 = 0.0, gA1 = 0.0, gB0 = 0.0, gB1 = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+          gA0 = fma(rm[e], xL[e], gA0);
+          gB0 = fma(xR[e], lp[e], gB0);
+          if (e + 1 < E) {
+            gA1 = fma(rm[e + 1], xL[e + 1], gA1);
+            gB1 = fma(xR[e + 1], lp[e + 1], gB1);
+          }
+        }
+        const double nRm = s_nrm[par][1][g], nLp = s_nrm[par][0][g + 2];
         SPROF(0);
-        alA = group_sum<LP>(alA);
-        beA = group_sum<LP>(beA);
-        gaA = group_sum<LP>(gaA);
-        alB = group_sum<LP>(alB);
-        beB = group_sum<LP>(beB);
-        gaB = group_sum<LP>(gaB);
+        const double gaA = group_sum<LP>(gA0 + gA1), gaB = group_sum<LP>(gB0 + gB1);
         SPROF(1);
         bool rA, rB;
-        const double tA = jacobi_t(alA, beA, gaA, tol_rot2, rA), tB = jacobi_t(alB, beB, gaB, tol_rot2, rB);
+        const double tA = jacobi_t(nRm, nL, gaA, tol_rot2, rA), tB = jacobi_t(nR, nLp, gaB, tol_rot2, rB);
         rotated |= live && ((rA && !left_edge) || (rB && !right_edge));
         if (gl == 0 && live) { dsmem_st_f64(prr, tA); dsmem_st_f64(prr + 8, tB); }
         rot_cs(tA, cA, sA);
         rot_cs(tB, cB, sB);
+        if (left_edge) { cA = 0.0; sA = -1.0; }
+        if (right_edge) { cB = 0.0; sB = 1.0; }
+        // new L = x'_A = cA Rm - sA L, new R = y'_B = sB R + cB Lp
+        const double nxA = fma(cA * cA, nRm, fma(sA * sA, nL, -2.0 * cA * sA * gaA));
+        const double nyB = fma(sB * sB, nR, fma(cB * cB, nLp, 2.0 * cB * sB * gaB));
+        nL = nxA;
+        nR = nyB;
         SPROF(2);
       } else {
         rot_cs(live ? pr[0] : 0.0, cA, sA);

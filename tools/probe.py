@@ -38,9 +38,13 @@ def probe_svd(k=50, reps=5, graded=False):
     sv = np.linalg.svd(Wd, compute_uv=False)
     Uh, Vh, sh = U.cpu().numpy(), V.cpu().numpy(), sig.cpu().numpy()
     rec = np.linalg.norm(Uh * sh @ Vh.T - Wd) / np.linalg.norm(Wd)
+    Ul, sl, Vlt = np.linalg.svd(Wd)
+    sgn = np.sign(np.sum(Ul * Uh, axis=0)); sgn[sgn == 0] = 1
+    udiff = np.abs(Uh * sgn - Ul).max()
     orth = max(np.abs(Uh.T @ Uh - np.eye(k)).max(), np.abs(Vh.T @ Vh - np.eye(k)).max())
     print(f"svd k={k}{' graded' if graded else ''}: {e0.elapsed_time(e1) / reps * 1e3:.1f} us/call, sweeps={sweeps}, "
-          f"r={int(r.item())}, sigma rel err {np.abs(sh - sv).max() / sv[0]:.1e}, recon {rec:.1e}, orth {orth:.1e}")
+          f"r={int(r.item())}, sigma rel err {np.abs(sh - sv).max() / sv[0]:.1e}, recon {rec:.1e}, orth {orth:.1e}, "
+          f"U vs LAPACK {udiff:.1e}")
 
 
 def probe_residual(m=20000, n=10000, k=50, reps=5):
@@ -142,6 +146,42 @@ def probe_lloyd_prof(N=20000, d=50, k2=50, iters=20):
     names = ["centres+zero", "dist+argmin", "bucket", "obj-publish", "barrier", "cluster.sync1", "dsmem-reduce+red",
              "fence", "cluster.sync2"]
     print(f"lloyd N={N} d={d} k2={k2}: " + ", ".join(f"{n} {p / iters:.0f} cyc" for n, p in zip(names, prof)))
+
+
+def probe_lloyd_pair(Na=20000, Nb=10000, d=50, k2=50, iters=20, prof=False):
+    """cabs_kmeans_pair timing (and, with -DCABS_PROFILE_LLOYD, per-phase cycles of the last CTA)."""
+    dev = torch.device("cuda:0")
+    plan = make_plan(Na, Nb, max(d, k2))
+    ws = torch.zeros(C.cabs_workspace_bytes(plan), dtype=torch.uint8, device=dev)
+    ld = C.cabs_padded_ld(d)
+    bufs = []
+    probs = []
+    for N, tag in ((Na, 3), (Nb, 4)):
+        X = torch.zeros(N, ld, device=dev); X[:, :d] = torch.randn(N, d, device=dev)
+        b = (X, torch.zeros(k2, ld, device=dev), torch.zeros(N, dtype=torch.int32, device=dev),
+             torch.zeros(k2, dtype=torch.float64, device=dev), torch.zeros(iters, dtype=torch.float64, device=dev))
+        bufs.append(b)
+        probs.append(C.km_problem(b[0], N, N, 0, d, k2, tag, b[1], b[2], b[3], b[4]))
+    C.cabs_kmeans_pair(plan, probs[0], probs[1], iters, 0, 2.0, 0, ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        C.cabs_kmeans_pair(plan, probs[0], probs[1], iters, 0, 2.0, 0, ws)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 3 * 1e3
+    line = f"kmeans_pair Na={Na} Nb={Nb} d={d} k2={k2} iters={iters}: {t:.1f} us ({t / iters:.1f} us/iter)"
+    if prof:
+        p = ws[64:144].view(torch.int64).tolist()
+        names = ["centres+zero", "dist+argmin(last prob)", "accum(last prob)", "obj-publish", "cluster.sync3",
+                 "cluster.sync1", "dsmem-reduce+red", "fence", "cluster.sync2+leader barrier"]
+        line += "\n  " + ", ".join(f"{n} {v / iters:.0f}" for n, v in zip(names, p))
+    print(line)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "lloydpair":
+    probe_lloyd_pair(prof=len(sys.argv) > 2)
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "lloydprof":

@@ -7,3 +7,5 @@ if which == "svd":
     P.probe_svd(int(sys.argv[2]), reps=1)
 elif which == "kmeans":
     P.probe_kmeans(int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]), reps=1)
+elif which == "kmpair":
+    P.probe_lloyd_pair()
