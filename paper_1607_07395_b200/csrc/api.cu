@@ -145,6 +145,27 @@ int32_t cabs_svd(const cabs_plan* plan, int32_t k, const float* W, int64_t ldw, 
   return CABS_OK;
 }
 
+// A library-owned non-blocking side stream per device (and fork/join events) for the
+// second problem of the *_pair entry points.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static int32_t side_stream(SideStream** out) {
+  static SideStream side[64];
+  int dev = 0;
+  CABS_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return arg_error("device index out of range");
+  SideStream& ss = side[dev];
+  if (!ss.s) {
+    CABS_CUDA_TRY(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    CABS_CUDA_TRY(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    CABS_CUDA_TRY(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  *out = &ss;
+  return CABS_OK;
+}
+
 // ---------------------------------------------------------------- S1-S3
 int32_t cabs_pilot(const cabs_plan* plan, const cabs_source* src, int32_t k, uint64_t seed, int64_t* I, int64_t* J,
                    float* C, int64_t ldc, float* R, int64_t ldr, float* W, int64_t ldw, void* ws, size_t ws_bytes,
@@ -176,11 +197,13 @@ int32_t cabs_pilot(const cabs_plan* plan, const cabs_source* src, int32_t k, uin
 static int32_t embed_core(const cabs_plan& p, const Ws& L, int32_t k, const float* C, int64_t ldc, const float* R,
                           int64_t ldr, const float* W, int64_t ldw, int32_t mode, double tol, float* Y1, int64_t ld1,
                           float* Y2, int64_t ld2, float* s, int32_t* r, double* sigma, int kind, void* ws,
-                          const cabs_comm* comm, void* stream) {
+                          const cabs_comm* comm, void* stream, bool svd_done = false) {
   cudaStream_t st = S(stream);
   const int64_t m_loc = p.row_end - p.row_begin, n_sl = p.col_end - p.col_begin;
-  launch_svd(k, W, ldw, tol, ws, L, sigma, nullptr, nullptr, nullptr, st);
-  CABS_LAUNCH_CHECK("svd");
+  if (!svd_done) {
+    launch_svd(k, W, ldw, tol, ws, L, sigma, nullptr, nullptr, nullptr, st);
+    CABS_LAUNCH_CHECK("svd");
+  }
   if (m_loc > 0) CABS_CUDA_TRY(cudaMemsetAsync(Y1, 0, sizeof(float) * ld1 * m_loc, st));
   if (n_sl > 0) CABS_CUDA_TRY(cudaMemsetAsync(Y2, 0, sizeof(float) * ld2 * n_sl, st));
   launch_embed_products(m_loc, n_sl, k, C, ldc, R + p.col_begin, ldr, Y1, ld1, Y2, ld2, ws, L, st);
@@ -231,6 +254,25 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
   float* Cb = wsp<float>(ws, L.cb);
   float* Rb = wsp<float>(ws, L.rb);
   float* Wb = wsp<float>(ws, L.wb);
+  if (!multi(comm)) {
+    // single GPU: W = A(Ir, Ic) first, its SVD on the side stream (2 SMs) while the large C
+    // and R gathers run on the caller's stream, then join
+    launch_gather_w_direct(src->a, src->lda, p.row_begin, Ir, Ic, k, Wb, L.Kp, st);
+    CABS_LAUNCH_CHECK("gather_w_direct");
+    SideStream* ss = nullptr;
+    CABS_TRY(side_stream(&ss));
+    CABS_CUDA_TRY(cudaEventRecord(ss->fork, st));
+    CABS_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+    launch_svd(k, Wb, L.Kp, tol, ws, L, sigma, nullptr, nullptr, nullptr, ss->s);
+    CABS_LAUNCH_CHECK("svd");
+    launch_gather_cols(src->a, src->lda, m_loc, Ic, k, Cb, L.Kp, ws, st);
+    launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, Ir, k, p.n, Rb, L.ldrb, ws, st);
+    CABS_LAUNCH_CHECK("sketch gathers");
+    CABS_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
+    CABS_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));
+    return embed_core(p, L, k, Cb, L.Kp, Rb, L.ldrb, Wb, L.Kp, mode, tol, U, ldu, V, ldv, s, r, sigma, 1, ws, comm,
+                      stream, true);
+  }
   launch_gather_cols(src->a, src->lda, m_loc, Ic, k, Cb, L.Kp, ws, st);
   if (multi(comm)) CABS_CUDA_TRY(cudaMemsetAsync(Rb, 0, sizeof(float) * L.ldrb * k, st));
   launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, Ir, k, p.n, Rb, L.ldrb, ws, st);
@@ -444,27 +486,6 @@ int32_t cabs_select(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   const cabs_sel_problem p{X, ldx, n_loc, n_glob, row_off, d, centres, ldc, k2, cluster_w, reps, rep_of_centre, gap};
   CABS_TRY(sel_check(plan, L, p));
   return sel_run(p, 0, ws, L, comm, stream);
-}
-
-// A library-owned non-blocking side stream per device (and fork/join events) for the
-// second problem of the *_pair entry points.
-struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-static int32_t side_stream(SideStream** out) {
-  static SideStream side[64];
-  int dev = 0;
-  CABS_CUDA_TRY(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 64) return arg_error("device index out of range");
-  SideStream& ss = side[dev];
-  if (!ss.s) {
-    CABS_CUDA_TRY(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
-    CABS_CUDA_TRY(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
-    CABS_CUDA_TRY(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
-  }
-  *out = &ss;
-  return CABS_OK;
 }
 
 int32_t cabs_select_pair(const cabs_plan* plan, const cabs_sel_problem* a, const cabs_sel_problem* b, void* ws,
