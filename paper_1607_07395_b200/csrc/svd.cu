@@ -567,6 +567,7 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
       mbar_wait_cluster(&bar_full[sp], static_cast<uint32_t>((sweep >> 1) & 1));
     }
     int rotated = 0;
+    double tmax = 0.0;  // largest |t| of this sweep (CTA 0)
     // squared column norms: recomputed exactly at every sweep start, then carried through
     // the rotations by the exact 2x2 formulas, so a round reduces only the cross products
     double nL = 0.0, nR = 0.0;
@@ -597,6 +598,7 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
           bool need;
           const double t = jacobi_t(nL, nR, ga, tol_rot2, need);
           rotated |= need && live;
+          if (live) tmax = fmax(tmax, fabs(t));
           if (gl == 0 && live) dsmem_st_f64(prr, t);
           rot_cs(t, c, sn);
           // new L = s x + c y, new R = c x - s y (the swap of the odd-even network)
@@ -667,6 +669,8 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
         bool rA, rB;
         const double tA = jacobi_t(nRm, nL, gaA, tol_rot2, rA), tB = jacobi_t(nR, nLp, gaB, tol_rot2, rB);
         rotated |= live && ((rA && !left_edge) || (rB && !right_edge));
+        if (live && !left_edge) tmax = fmax(tmax, fabs(tA));
+        if (live && !right_edge) tmax = fmax(tmax, fabs(tB));
         if (gl == 0 && live) { dsmem_st_f64(prr, tA); dsmem_st_f64(prr + 8, tB); }
         rot_cs(tA, cA, sA);
         rot_cs(tB, cB, sB);
@@ -695,7 +699,10 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
     }
     if (crank == 0) {
       rotated = __syncthreads_or(rotated);
-      last = !rotated || sweep + 1 >= kSvdMaxSweeps;
+      // quadratic convergence: after a sweep whose rotations all had |t| < 1e-8 the next
+      // sweep's would be below the rotation threshold (|t| ~ 1e-16), so it is not run
+      const int small = __syncthreads_and(tmax < 1e-8);
+      last = !rotated || small || sweep + 1 >= kSvdMaxSweeps;
       if (tid == 0) {
         dsmem_st_s32(last_remote + 4 * sp, last ? 1 : 0);
         asm volatile("fence.acq_rel.cluster;" ::: "memory");
