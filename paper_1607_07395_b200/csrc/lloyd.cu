@@ -264,13 +264,12 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
 #endif
   for (int it = 0; it < a.iters; ++it) {
     if (it > 0) {
-      // centres of this iteration from the previous iteration's exact sums (empty cluster: keep);
-      // the loads of both problems are issued before the first wait
-      constexpr int U = 8;  // independent L2 loads in flight per thread (per problem)
-      long long sv[kMaxProb][U];
-  #pragma unroll
-    for (int q = 0; q < kMaxProb; ++q) {
-      if (q >= np_) break;
+      // centres of this iteration from the previous iteration's exact sums (empty cluster: keep).
+      // Each CTA forms the centres of ITS slice of the entries (the slice it reduced) and stores
+      // them into the centre arrays of all CTAs of its cluster (DSMEM); one cluster barrier.
+#pragma unroll
+      for (int q = 0; q < kMaxProb; ++q) {
+        if (q >= np_) break;
         const LloydProb& pr = a.pr[q];
         const ProbSmem S = prob_smem(dyn, Ls[q]);
         const int64_t nsum = (int64_t)pr.k2 * pr.d;
@@ -279,32 +278,50 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
           const long long wj = __ldcg(fs_prev + nsum + j);
           S.wd[j] = wj > 0 ? 1.0 / (static_cast<double>(wj) * (1.0 / scale_w[q])) : 0.0;
         }
+      }
+      constexpr int U = 4;  // slice entries per thread per problem (c2: ~2.5)
+      long long sv[kMaxProb][U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) sv[q][u] = tid + u * kLT < nsum ? __ldcg(fs_prev + tid + u * kLT) : 0;
+      for (int q = 0; q < kMaxProb; ++q) {
+        if (q >= np_) break;
+        const LloydProb& pr = a.pr[q];
+        const int64_t nsum = (int64_t)pr.k2 * pr.d;
+        const long long* fs_prev = pr.fsum + (size_t)((it + 2) % 3) * Eq[q];
+        const int64_t se = eend[q] < nsum ? eend[q] : nsum;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t e = ebeg[q] + tid + (int64_t)u * kLT;
+          sv[q][u] = e < se ? __ldcg(fs_prev + e) : 0;
+        }
       }
       __syncthreads();  // wd ready
-  #pragma unroll
-    for (int q = 0; q < kMaxProb; ++q) {
-      if (q >= np_) break;
+#pragma unroll
+      for (int q = 0; q < kMaxProb; ++q) {
+        if (q >= np_) break;
         const LloydProb& pr = a.pr[q];
         const ProbSmem S = prob_smem(dyn, Ls[q]);
-        const int d = pr.d, ns = pr.k2 * pr.d;
+        const int d = pr.d;
+        const int64_t nsum = (int64_t)pr.k2 * d;
         const double inv_scale = 1.0 / scale[q];
         const long long* fs_prev = pr.fsum + (size_t)((it + 2) % 3) * Eq[q];
-        for (int e0 = tid; e0 < ns; e0 += U * kLT) {
-          long long v[U];
+        const int64_t se = eend[q] < nsum ? eend[q] : nsum;
+        float* rcs[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) rcs[r] = r < csize ? cluster.map_shared_rank(S.cs, r) : S.cs;
+        for (int64_t e0 = ebeg[q] + tid, u0 = 0; e0 < se; e0 += (int64_t)U * kLT, u0 += U) {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const int e = e0 + u * kLT;
-            v[u] = e0 == tid ? sv[q][u] : (e < ns ? __ldcg(fs_prev + e) : 0);
-          }
+            const int64_t e = e0 + (int64_t)u * kLT;
+            if (e >= se) break;
+            const long long v = u0 == 0 ? sv[q][u] : __ldcg(fs_prev + e);
+            const int j = static_cast<int>(e / d), i = static_cast<int>(e - (int64_t)j * d);
+            const double rw = S.wd[j];
+            if (rw > 0) {
+              const float c = static_cast<float>((static_cast<double>(v) * inv_scale) * rw);
+              const int ci = cpair_idx(j, i, d);
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int e = e0 + u * kLT;
-            if (e < ns) {
-              const int j = e / d, i = e - j * d;
-              const double rw = S.wd[j];
-              if (rw > 0) S.cs[cpair_idx(j, i, d)] = static_cast<float>((static_cast<double>(v[u]) * inv_scale) * rw);
+              for (int r = 0; r < 8; ++r)
+                if (r < csize) rcs[r][ci] = c;
             }
           }
         }
@@ -319,7 +336,8 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
       const ProbSmem S = prob_smem(dyn, Ls[q]);
       for (int64_t e = tid; e < Eq[q]; e += blockDim.x) S.part[e] = 0;
     }
-    __syncthreads();
+    if (it > 0) cluster.sync();  // every CTA of the cluster has stored its slice of the centres
+    else __syncthreads();
     LPROF(0);
 #pragma unroll
     for (int q = 0; q < kMaxProb; ++q) {
