@@ -212,7 +212,9 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
   __shared__ float sb_d[8][kLP];  // per point: best / runner-up of each warp's two centre lanes
   __shared__ int sb_j[8][kLP];
   __shared__ float ss_d[8][kLP];
-  __shared__ int lab_s[kLP];
+  __shared__ int lab_s[kLP], order_s[kLP], slab_s[kLP];
+  __shared__ int hist_s[CABS_KMAX];
+  __shared__ int wstart_s[kLT / 32 + 1];
   __shared__ double s_red[kMaxProb][kLT / 32];
   __shared__ int s_tie[kMaxProb][kLT / 32];
   cg::cluster_group cluster = cg::this_cluster();
@@ -380,41 +382,81 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
         }
         __syncthreads();
         LPROF(1);
-        // exact sums (km_fixed.cuh): warp w owns the clusters j with j % 8 == w (exclusive, so
-        // plain read-modify-writes of the shared partial); a ballot over 32 labels at a time finds
-        // its points, whose llrint(w 2^S x_pi) the lanes (dimensions) add (integer adds: any order)
+        // exact sums (km_fixed.cuh).  Counting sort of the chunk's points by label (the order
+        // inside a label is irrelevant: integer sums), then warp w takes a contiguous range of
+        // the sorted points aligned to label-run starts (every cluster belongs to ONE warp) and
+        // keeps the running sums of the current run in registers, lanes over dimensions:
+        // no read-modify-write chains, one flush per run.
         {
+          for (int j = tid; j < k2; j += kLT) hist_s[j] = 0;
+          __syncthreads();
+          for (int p = tid; p < np; p += kLT) atomicAdd(&hist_s[lab_s[p]], 1);
+          __syncthreads();
+          if (warp == 0) {  // exclusive scan of the k2 counts: lane owns a contiguous block
+            const int per = (k2 + 31) >> 5;
+            const int b0 = lane * per, b1 = b0 + per < k2 ? b0 + per : k2;
+            int sl = 0;
+            for (int j = b0; j < b1; ++j) sl += hist_s[j];
+            int inc = sl;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int t = __shfl_up_sync(0xffffffffu, inc, o);
+              if (lane >= o) inc += t;
+            }
+            int run = inc - sl;
+            for (int j = b0; j < b1; ++j) {
+              const int c = hist_s[j];
+              hist_s[j] = run;
+              run += c;
+            }
+          }
+          __syncthreads();
+          for (int p = tid; p < np; p += kLT) {
+            const int l = lab_s[p];
+            const int pos = atomicAdd(&hist_s[l], 1);
+            order_s[pos] = p;
+            slab_s[pos] = l;
+          }
+          __syncthreads();
+          if (tid <= kLT / 32) {
+            int q = (tid * np) / (kLT / 32);
+            if (tid < kLT / 32) {
+              while (q > 0 && q < np && slab_s[q] == slab_s[q - 1]) ++q;
+            } else {
+              q = np;
+            }
+            wstart_s[tid] = q;
+          }
+          __syncthreads();
+          const int qb = wstart_s[warp], qe = wstart_s[warp + 1];
           long long* __restrict__ pp = S.part;
           const float* __restrict__ xr = S.xr;
-          for (int q0 = 0; q0 < np; q0 += 32) {
-            const int qq = q0 + lane;
-            unsigned m = __ballot_sync(0xffffffffu, qq < np && (lab_s[qq] & 7) == warp);
-            while (m) {  // two points per step: independent convert chains, one RMW if same cluster
-              const int p1 = q0 + __ffs(m) - 1;
-              m &= m - 1;
-              const bool two = m != 0;
-              const int p2 = two ? q0 + __ffs(m) - 1 : p1;
-              if (two) m &= m - 1;
-              const int j1 = lab_s[p1], j2 = lab_s[p2];
-              const double w1 = S.wsc[p1], w2 = two ? S.wsc[p2] : 0.0;
-              const float* x1 = xr + p1 * d;
-              const float* x2 = xr + p2 * d;
-              long long* r1 = pp + (int64_t)j1 * d;
-              long long* r2 = pp + (int64_t)j2 * d;
-#pragma unroll 2
-              for (int i = lane; i < d; i += 32) {
-                const long long v1 = fx_prod_magic(w1, x1[i]), v2 = fx_prod_magic(w2, x2[i]);
-                if (j1 == j2) {
-                  r1[i] += v1 + v2;
-                } else {
-                  r1[i] += v1;
-                  r2[i] += v2;
+          if (qb < qe) {
+            for (int i0 = 0; i0 < d; i0 += 64) {
+              const int ia = i0 + lane, ib = i0 + 32 + lane;
+              const bool wl = i0 == 0 && lane == 0;
+              long long sa = 0, sbv = 0, sw = 0;
+              int jc = slab_s[qb];
+#pragma unroll 4
+              for (int q = qb; q < qe; ++q) {
+                const int j = slab_s[q];
+                if (j != jc) {  // run of cluster jc ends: flush (this warp owns jc)
+                  if (ia < d) pp[(int64_t)jc * d + ia] += sa;
+                  if (ib < d) pp[(int64_t)jc * d + ib] += sbv;
+                  if (wl) pp[nsum + jc] += sw;
+                  sa = 0; sbv = 0; sw = 0;
+                  jc = j;
                 }
+                const int p = order_s[q];
+                const double ws = S.wsc[p];
+                const float* xrow = xr + p * d;
+                if (ia < d) sa += fx_prod_magic(ws, xrow[ia]);
+                if (ib < d) sbv += fx_prod_magic(ws, xrow[ib]);
+                if (wl) sw += S.iw[p];
               }
-              if (lane == 0) {
-                pp[nsum + j1] += S.iw[p1];
-                if (two) pp[nsum + j2] += S.iw[p2];
-              }
+              if (ia < d) pp[(int64_t)jc * d + ia] += sa;
+              if (ib < d) pp[(int64_t)jc * d + ib] += sbv;
+              if (wl) pp[nsum + jc] += sw;
             }
           }
         }
