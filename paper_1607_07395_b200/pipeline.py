@@ -138,6 +138,19 @@ class CabsPipeline:
         self.events = ev
         return ev
 
+    def capture(self, stream=None):
+        """Capture one pass of the hot path (run()) into a CUDA graph; replay() re-runs it with
+        the same buffers.  Single GPU only (no host round trips in run()); call after warm-up
+        runs so that every lazily-initialised kernel attribute and the library's side stream
+        exist.  Returns (graph, library launches per replay)."""
+        if self.plan.nranks > 1:
+            raise ValueError("capture: single-GPU pipelines only")
+        n0 = C.cabs_launch_count()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            self.run()
+        return g, C.cabs_launch_count() - n0
+
     def step_ms(self):
         """Per-step milliseconds of the last timed run (synchronises)."""
         ev = self.events

@@ -181,3 +181,44 @@ def test_e2e_deterministic(dev):
             assert torch.equal(g1[key], g2[key]), key
         else:
             assert g1[key] == g2[key], key
+
+
+def test_e2e_cuda_graph_replay_matches_eager(dev):
+    """The whole hot path captured as one CUDA graph (bench.py's timed step) replays to the
+    same results as the stream-ordered run, bit for bit, also on new data written in place."""
+    from paper_1607_07395_b200.pipeline import CabsConfig, CabsPipeline
+    from workloads import CONFIGS, make_A, scaled
+    cfg = scaled(CONFIGS["c2"], 3000, 2000, k1=40, k2=40, iters=8)
+    A_t = make_A(cfg, device=dev)
+    pipe = CabsPipeline(A_t, cfg.m, cfg.n, CabsConfig(40, 40, 8, seed=cfg.seed))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        pipe.run()
+        ref = pipe.results()
+        graph, launches = pipe.capture(stream=s)
+    torch.cuda.synchronize()
+    assert launches > 10
+    pipe.out.zero_()
+    pipe.U.zero_()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        graph.replay()
+    torch.cuda.synchronize()
+    got = pipe.results()
+    for key in ref:
+        if isinstance(ref[key], torch.Tensor):
+            assert torch.equal(got[key], ref[key]), key
+        else:
+            assert got[key] == ref[key], key
+    # new data in the same buffer: the replay recomputes (compare against an eager run)
+    A2 = make_A(scaled(CONFIGS["c2"], 3000, 2000, k1=40, k2=40, iters=8, seed=cfg.seed + 1), device=dev)
+    pipe.A.copy_(A2)
+    s.wait_stream(torch.cuda.current_stream())  # the copy is on the default stream
+    with torch.cuda.stream(s):
+        graph.replay()
+    torch.cuda.synchronize()
+    got2 = pipe.results()
+    _, ref2 = _run(A2, cfg.m, cfg.n, 40, 40, 8, seed=cfg.seed)
+    bad = [k for k in ref2 if (not torch.equal(got2[k], ref2[k]) if isinstance(ref2[k], torch.Tensor)
+                               else got2[k] != ref2[k])]
+    assert not bad, bad
