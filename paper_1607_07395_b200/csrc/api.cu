@@ -414,8 +414,30 @@ int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const 
   CABS_TRY(km_check(plan, L, *a, iters, weight_kind));
   CABS_TRY(km_check(plan, L, *b, iters, weight_kind));
   const KmSlot ka = km_slot(ws, L, 0), kb = km_slot(ws, L, 1);
-  CABS_TRY(km_prepare(*a, weight_kind, weight_p, seed, ka, comm, stream));
-  CABS_TRY(km_prepare(*b, weight_kind, weight_p, seed, kb, comm, stream));
+  if (!multi(comm)) {
+    // both sides' weights, Floyd initialisations and initial centres in one launch each
+    cudaStream_t st = S(stream);
+    CABS_CUDA_TRY(cudaMemsetAsync(ka.cnt, 0, sizeof(int) * 20, st));  // slot 0 [0, 4), slot 1 [16, 20)
+    const KmWeightJob wa{a->X, a->ldx, a->n_loc, a->d, ka.w, ka.cnt, ka.bounds};
+    const KmWeightJob wb{b->X, b->ldx, b->n_loc, b->d, kb.w, kb.cnt, kb.bounds};
+    launch_km_weights2(wa, &wb, weight_kind, weight_p, st);
+    CABS_LAUNCH_CHECK("km_weights");
+    const bool fa = !a->init_idx && !a->init_centres, fb = !b->init_idx && !b->init_centres;
+    if (fa || fb) {
+      launch_floyd2(a->n_glob, fa ? a->k2 : 0, static_cast<uint32_t>(a->tag), fa ? ka.idx : nullptr, b->n_glob,
+                    fb ? b->k2 : 0, static_cast<uint32_t>(b->tag), fb ? kb.idx : nullptr, seed, st);
+      CABS_LAUNCH_CHECK("floyd init");
+    }
+    const KmInitJob ia{a->X, a->ldx, a->n_loc, a->row_off, a->d, a->k2, fa ? ka.idx : a->init_idx,
+                       a->init_centres, a->ldc, a->centres, a->ldc};  // init_centres takes precedence
+    const KmInitJob ib{b->X, b->ldx, b->n_loc, b->row_off, b->d, b->k2, fb ? kb.idx : b->init_idx,
+                       b->init_centres, b->ldc, b->centres, b->ldc};
+    launch_km_init2(ia, &ib, st);
+    CABS_LAUNCH_CHECK("km_init");
+  } else {
+    CABS_TRY(km_prepare(*a, weight_kind, weight_p, seed, ka, comm, stream));
+    CABS_TRY(km_prepare(*b, weight_kind, weight_p, seed, kb, comm, stream));
+  }
   if (km_persistent_allowed(comm) && a->n_loc > 0 && b->n_loc > 0) {
     const LloydJob j[2] = {km_job(*a, ka), km_job(*b, kb)};
     if (launch_lloyd_persistent(j, 2, iters, reinterpret_cast<long long*>(ws) + 8, S(stream))) {

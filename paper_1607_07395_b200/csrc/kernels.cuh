@@ -33,6 +33,26 @@ int launch_embed_finalize(int k, int mode, double m, double n, double ksamp, int
 int launch_scale_compact(float* Y, int64_t ldy, int64_t N, int k, int which, void* ws, const Ws& L, cudaStream_t st);
 
 // kmeans.cu
+struct KmWeightJob {
+  const float* X;
+  int64_t ldx, N;
+  int d;
+  float* w;
+  int* cnt;
+  unsigned* bounds;
+};
+struct KmInitJob {
+  const float* X;
+  int64_t ldx, n_loc, row_off;
+  int d, k2;
+  const int64_t* idx;
+  const float* init_c;
+  int64_t ldic;
+  float* centres;
+  int64_t ldc;
+};
+void launch_km_weights2(const KmWeightJob& j0, const KmWeightJob* j1, int kind, float p, cudaStream_t st);
+void launch_km_init2(const KmInitJob& j0, const KmInitJob* j1, cudaStream_t st);
 void launch_km_weights(const float* X, int64_t ldx, int64_t N, int d, int kind, float p, float* w, int* cnt,
                        unsigned* bounds, cudaStream_t st);
 void launch_km_init(const float* X, int64_t ldx, int64_t n_loc, int64_t row_off, int d, int k2, const int64_t* idx,

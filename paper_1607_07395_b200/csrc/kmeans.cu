@@ -21,9 +21,12 @@ namespace cabsk {
 
 // ---------------------------------------------------------------- weights
 // Also the fixed-point bounds max|x| and max w (bounds[0], bounds[1]; km_fixed.cuh).
-__global__ void __launch_bounds__(256) km_weights_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
-                                                         int kind, float p, float* __restrict__ w, int* cnt,
-                                                         unsigned* bounds) {
+// blockIdx.y selects one of two jobs (the two sides of cabs_kmeans_pair in one launch).
+__global__ void __launch_bounds__(256) km_weights_kernel(KmWeightJob j0, KmWeightJob j1, int kind, float p) {
+  const KmWeightJob j = blockIdx.y == 0 ? j0 : j1;
+  const float* __restrict__ X = j.X;
+  const int64_t ldx = j.ldx, N = j.N;
+  const int d = j.d;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -42,7 +45,7 @@ __global__ void __launch_bounds__(256) km_weights_kernel(const float* __restrict
     else if (p == 2.f) wl = ss;
     else wl = powf(sqrtf(ss), p);
     if (lane == 0) {
-      w[l] = wl;
+      j.w[l] = wl;
       pos += wl > 0.f;
       mw = fmaxf(mw, wl);
     }
@@ -58,42 +61,54 @@ __global__ void __launch_bounds__(256) km_weights_kernel(const float* __restrict
   if (threadIdx.x == 0) {
     int tp = 0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { mx = fmaxf(mx, s_mx[q]); mw = fmaxf(mw, s_mw[q]); tp += s_pos[q]; }
-    if (tp) atomicAdd(cnt, tp);
-    atomicMax(bounds, __float_as_uint(mx));
-    atomicMax(bounds + 1, __float_as_uint(mw));
+    if (tp) atomicAdd(j.cnt, tp);
+    atomicMax(j.bounds, __float_as_uint(mx));
+    atomicMax(j.bounds + 1, __float_as_uint(mw));
   }
 }
 
-void launch_km_weights(const float* X, int64_t ldx, int64_t N, int d, int kind, float p, float* w, int* cnt,
-                       unsigned* bounds, cudaStream_t st) {
+void launch_km_weights2(const KmWeightJob& j0, const KmWeightJob* j1, int kind, float p, cudaStream_t st) {
+  int64_t N = j0.N > (j1 ? j1->N : 0) ? j0.N : j1->N;
   if (N <= 0) return;
   int64_t blocks = ceil_div(N, 8);
   if (blocks > 2 * kNumSM) blocks = 2 * kNumSM;
   note_launch();
-  km_weights_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(X, ldx, N, d, kind, p, w, cnt, bounds);
+  km_weights_kernel<<<dim3(static_cast<unsigned>(blocks), j1 ? 2 : 1), 256, 0, st>>>(j0, j1 ? *j1 : j0, kind, p);
+}
+
+void launch_km_weights(const float* X, int64_t ldx, int64_t N, int d, int kind, float p, float* w, int* cnt,
+                       unsigned* bounds, cudaStream_t st) {
+  const KmWeightJob j{X, ldx, N, d, w, cnt, bounds};
+  launch_km_weights2(j, nullptr, kind, p, st);
 }
 
 // ---------------------------------------------------------------- init
 // centres[j] = X[idx[j]] if this rank owns that row (zeros otherwise: the
-// caller's sum-allreduce completes it), or a copy of init_c.
-__global__ void km_init_kernel(const float* __restrict__ X, int64_t ldx, int64_t n_loc, int64_t row_off, int d,
-                               const int64_t* __restrict__ idx, const float* __restrict__ init_c, int64_t ldic,
-                               float* __restrict__ centres, int64_t ldc) {
+// caller's sum-allreduce completes it), or a copy of init_c.  blockIdx.y: job.
+__global__ void km_init_kernel(KmInitJob j0, KmInitJob j1) {
+  const KmInitJob jb = blockIdx.y == 0 ? j0 : j1;
   const int j = blockIdx.x;
+  if (j >= jb.k2) return;
   const float* src = nullptr;
-  if (init_c) src = init_c + (int64_t)j * ldic;
+  if (jb.init_c) src = jb.init_c + (int64_t)j * jb.ldic;
   else {
-    int64_t g = idx[j] - row_off;
-    if (g >= 0 && g < n_loc) src = X + g * ldx;
+    int64_t g = jb.idx[j] - jb.row_off;
+    if (g >= 0 && g < jb.n_loc) src = jb.X + g * jb.ldx;
   }
-  for (int i = threadIdx.x; i < ldc; i += blockDim.x)
-    centres[(int64_t)j * ldc + i] = (src && i < d) ? src[i] : 0.f;
+  for (int i = threadIdx.x; i < jb.ldc; i += blockDim.x)
+    jb.centres[(int64_t)j * jb.ldc + i] = (src && i < jb.d) ? src[i] : 0.f;
+}
+
+void launch_km_init2(const KmInitJob& j0, const KmInitJob* j1, cudaStream_t st) {
+  const int kx = j0.k2 > (j1 ? j1->k2 : 0) ? j0.k2 : j1->k2;
+  note_launch();
+  km_init_kernel<<<dim3(kx, j1 ? 2 : 1), 128, 0, st>>>(j0, j1 ? *j1 : j0);
 }
 
 void launch_km_init(const float* X, int64_t ldx, int64_t n_loc, int64_t row_off, int d, int k2, const int64_t* idx,
                     const float* init_c, int64_t ldic, float* centres, int64_t ldc, cudaStream_t st) {
-  note_launch();
-  km_init_kernel<<<k2, 128, 0, st>>>(X, ldx, n_loc, row_off, d, idx, init_c, ldic, centres, ldc);
+  const KmInitJob j{X, ldx, n_loc, row_off, d, k2, idx, init_c, ldic, centres, ldc};
+  launch_km_init2(j, nullptr, st);
 }
 
 // ---------------------------------------------------------------- assign / distance matrix
