@@ -450,8 +450,8 @@ svd_systolic_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol,
 // odd-even data movement, one sweep behind (a sweep buffer per parity, one mbarrier signal per
 // sweep each way).  At the end CTA 1 stores V's columns (by column id) into CTA 0, which runs
 // the common epilogue.  Rotation formulas, ordering and convergence test are those of
-// svd_systolic_kernel; CTA 1 recomputes (c, s) from the streamed t with the same code as
-// CTA 0, so A and V see bit-identical rotations.
+// svd_systolic_kernel; CTA 0 streams the (c, s) pairs themselves, so A and V see
+// bit-identical rotations and CTA 1's round has no angle computation on it.
 __device__ __forceinline__ uint32_t dsmem_map(const void* p, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(tc::smem_u32(p)), "r"(rank));
@@ -506,7 +506,7 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
   const int nseat = nw * G + 2;
   const bool live = g < P;
   const bool left_edge = g == 0, right_edge = g == P - 1;
-  // smem: exchange [XL|XR][parity][seat][SEAT] | (CTA 1) rotations t [parity][round][slot][2] |
+  // smem: exchange [XL|XR][parity][seat][SEAT] | (CTA 1) rotations (c, s) [parity][round][slot][4] |
   // (CTA 0) final A and V columns [k][k] each (reusing the exchange area)
   const size_t arr = (size_t)2 * nseat * SEAT;
   double* bXL = smem_d;
@@ -579,7 +579,7 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
       nR = group_sum<LP>(t1);
     }
     for (int rnd = 0; rnd < np; ++rnd) {
-      const int pidx = ((sp * np + rnd) * P + (live ? g : 0)) * 2;  // [parity][round][slot][2]
+      const int pidx = ((sp * np + rnd) * P + (live ? g : 0)) * 4;  // [parity][round][slot][4]
       const double* pr = prm + pidx;                                 // CTA 1 view
       const uint32_t prr = prm_remote + static_cast<uint32_t>(pidx * 8);
       if ((rnd & 1) == 0) {
@@ -593,14 +593,27 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
             if (e + 1 < E) ga1 = fma(xL[e + 1], xR[e + 1], ga1);
           }
           SPROF(0);
+#ifdef SVD_NO_BFLY
+          const double ga = ga0 + ga1;
+#else
           const double ga = group_sum<LP>(ga0 + ga1);
+#endif
           SPROF(1);
           bool need;
+#ifdef SVD_FAST_ANGLE
+          need = ga * ga > tol_rot2 * nL * nR;
+          const double t = need ? ga * 1e-3 : 0.0;
+          c = 1.0;
+          sn = t;
+#else
           const double t = jacobi_t(nL, nR, ga, tol_rot2, need);
+          rot_cs(t, c, sn);
+#endif
           rotated |= need && live;
           if (live) tmax = fmax(tmax, fabs(t));
-          if (gl == 0 && live) dsmem_st_f64(prr, t);
-          rot_cs(t, c, sn);
+#ifndef SVD_NO_REMOTE
+          if (gl == 0 && live) { dsmem_st_f64(prr, c); dsmem_st_f64(prr + 8, sn); }
+#endif
           // new L = s x + c y, new R = c x - s y (the swap of the odd-even network)
           const double cs2 = 2.0 * c * sn * ga, c2 = c * c, s2 = sn * sn;
           const double nx = fma(c2, nL, fma(s2, nR, -cs2)), ny = fma(s2, nL, fma(c2, nR, cs2));
@@ -608,7 +621,8 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
           nR = nx;
           SPROF(2);
         } else {  // slots beyond P carry no rotations (their columns stay zero)
-          rot_cs(live ? pr[0] : 0.0, c, sn);
+          c = live ? pr[0] : 1.0;
+          sn = live ? pr[1] : 0.0;
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -664,16 +678,32 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
         }
         const double nRm = s_nrm[par][1][g], nLp = s_nrm[par][0][g + 2];
         SPROF(0);
+#ifdef SVD_NO_BFLY
+        const double gaA = gA0 + gA1, gaB = gB0 + gB1;
+#else
         const double gaA = group_sum<LP>(gA0 + gA1), gaB = group_sum<LP>(gB0 + gB1);
+#endif
         SPROF(1);
         bool rA, rB;
+#ifdef SVD_FAST_ANGLE
+        rA = gaA * gaA > tol_rot2 * nRm * nL;
+        rB = gaB * gaB > tol_rot2 * nR * nLp;
+        const double tA = rA ? gaA * 1e-3 : 0.0, tB = rB ? gaB * 1e-3 : 0.0;
+        cA = 1.0; sA = tA; cB = 1.0; sB = tB;
+#else
         const double tA = jacobi_t(nRm, nL, gaA, tol_rot2, rA), tB = jacobi_t(nR, nLp, gaB, tol_rot2, rB);
+        rot_cs(tA, cA, sA);
+        rot_cs(tB, cB, sB);
+#endif
         rotated |= live && ((rA && !left_edge) || (rB && !right_edge));
         if (live && !left_edge) tmax = fmax(tmax, fabs(tA));
         if (live && !right_edge) tmax = fmax(tmax, fabs(tB));
-        if (gl == 0 && live) { dsmem_st_f64(prr, tA); dsmem_st_f64(prr + 8, tB); }
-        rot_cs(tA, cA, sA);
-        rot_cs(tB, cB, sB);
+#ifndef SVD_NO_REMOTE
+        if (gl == 0 && live) {
+          dsmem_st_f64(prr, cA); dsmem_st_f64(prr + 8, sA);
+          dsmem_st_f64(prr + 16, cB); dsmem_st_f64(prr + 24, sB);
+        }
+#endif
         if (left_edge) { cA = 0.0; sA = -1.0; }
         if (right_edge) { cB = 0.0; sB = 1.0; }
         // new L = x'_A = cA Rm - sA L, new R = y'_B = sB R + cB Lp
@@ -683,8 +713,8 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
         nR = nyB;
         SPROF(2);
       } else {
-        rot_cs(live ? pr[0] : 0.0, cA, sA);
-        rot_cs(live ? pr[1] : 0.0, cB, sB);
+        cA = live ? pr[0] : 1.0; sA = live ? pr[1] : 0.0;
+        cB = live ? pr[2] : 1.0; sB = live ? pr[3] : 0.0;
       }
       if (left_edge) { cA = 0.0; sA = -1.0; }
       if (right_edge) { cB = 0.0; sB = 1.0; }
@@ -862,7 +892,7 @@ static bool launch_split(int k, const float* W, int64_t ldw, double tol, double*
   const int np = (k + 1) & ~1, P = np / 2;
   const int nw = (P + G - 1) / G;
   const size_t xch = sizeof(double) * 2 * 2 * (size_t)(nw * G + 2) * SEAT;  // [XL|XR][parity][seat]
-  const size_t prm = sizeof(double) * 2 * (size_t)np * P * 2;               // [parity][round][slot][2]
+  const size_t prm = sizeof(double) * 2 * (size_t)np * P * 4;               // [parity][round][slot][c s c s]
   const size_t fin = sizeof(double) * 2 * (size_t)k * k;
   const size_t smem = (xch + prm > fin ? xch + prm : fin);
   constexpr int kCap = 220 * 1024;
@@ -889,6 +919,8 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
     // 8 lanes per column pair: 4 pairs per warp, up to 8 warps
     if (k <= 16) launch_split<8, 2>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
     else if (k <= 32) launch_split<8, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    else if (k <= 56 && getenv("CABS_SVD_LP2")) launch_split<2, 28>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    else if (k <= 56 && getenv("CABS_SVD_LP4")) launch_split<4, 14>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
     else if (k <= 56) launch_split<8, 7>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
     else launch_split<8, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
   } else if (k <= 64 && !getenv("CABS_SVD_SMEM")) {
