@@ -460,6 +460,18 @@ __device__ __forceinline__ uint32_t dsmem_map(const void* p, uint32_t rank) {
 __device__ __forceinline__ void dsmem_st_f64(uint32_t addr, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
+// Generic-address form for stores inside the sweep loop: the peer address is mapped once
+// (mapa on the generic address), and the store carries no compiler memory clobber (the
+// ordering that matters -- before the cluster fence + mbarrier release at the sweep end --
+// is kept because both are volatile asm).
+__device__ __forceinline__ double* dsmem_map_generic(const void* p, uint32_t rank) {
+  uint64_t r;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(p), "r"(rank));
+  return reinterpret_cast<double*>(r);
+}
+__device__ __forceinline__ void dsmem_st2_f64(double* gaddr, double a, double b) {
+  asm volatile("st.v2.f64 [%0], {%1, %2};" ::"l"(gaddr), "d"(a), "d"(b));
+}
 __device__ __forceinline__ void dsmem_st_s32(uint32_t addr, int v) {
   asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
@@ -779,6 +791,486 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
   svd_write(As, Vs, k, r, s_sig, s_perm, Uw64, Vw64, uw32, vw32, ld32);
 }
 
+// Scaled rotations.  Columns are kept as actual = d * stored.  The rotation of the pair (x, y)
+// at positions (p, p + 1), actual (X, Y) -> (s X + c Y, c X - s Y) (the odd-even network's swap
+// included), t = s / c, is applied to the stored columns as
+//   p: y + al x  (scale c dy),   p + 1: x - be y  (scale c dx),   al = t dx / dy, be = t dy / dx,
+// one FMA per element, and only t (not c) is on the critical path; norms follow the exact
+// 2 x 2 formulas.  One lane evaluates it for ITS position: left (p, own column x) or right
+// (p + 1, own column y); (on, od, oi) its own n, d, 1 / d, (pn, pd, pi) the other position's,
+// gs the stored dot.  Each lane gets its own position's new n, d, 1 / d (the column moving in
+// is the partner's, scaled by c).
+struct LaneRot {
+  double tu, tv, t, n, d, i;
+  bool need;
+};
+__device__ __forceinline__ void lane_rot(bool left, double on, double od, double oi, double pn, double pd, double pi,
+                                         double gs, double tol_rot2, LaneRot& r) {
+  // left lane: x = own, y = partner; right lane: the mirror image.  Every product below is
+  // formed from the same two factors on both lanes (commutation only), dx = ny - nx exactly
+  // negated on the right lane, so t is bit-identical on the pair's lanes.
+  const double dl = pn - on;
+  const double g = gs * (od * pd);
+  r.need = g != 0.0 && g * g > tol_rot2 * (on * pn);
+  const double dx = left ? dl : -dl, dy = 2.0 * g;
+  const double h = fma(dx, dx, dy * dy);
+  const double den = fabs(dx) + h * rsqrt_approx64(h);  // |dx| + sqrt(dx^2 + dy^2)
+  const double t = r.need ? copysign(1.0, dx) * dy * rcp_approx64(den) : 0.0;
+  r.t = t;
+  // tu = al (left lane) / be (right lane), tv the other: al = t dx / dy, be = t dy / dx
+  r.tu = t * (od * pi);
+  r.tv = t * (pd * oi);
+  const double q1 = fma(t, t, 1.0);
+  double c = rsqrt_approx64(q1);
+  c = c * fma(-0.5 * q1, c * c, 1.5);
+  c = c * fma(-0.5 * q1, c * c, 1.5);
+  const double kg = (left ? 2.0 : -2.0) * g;
+  // |s X + c Y|^2 (left), |c X - s Y|^2 (right); the column moving in is the partner's
+  r.n = (c * c) * (fma(t * t, on, pn) + t * kg);
+  r.d = c * pd;
+  r.i = pi * (q1 * c);
+}
+
+// ---------------------------------------------------------------- k <= 64: four columns per slot
+// As svd_split_kernel (A on CTA 0, V on CTA 1 of a cluster pair, rotations streamed through
+// DSMEM), but every slot (LP lanes) holds FOUR consecutive positions of the odd-even network:
+// even rounds rotate (0,1) and (2,3), odd rounds (1,2) inside the slot and (3, next slot's 0)
+// across slots -- only two of the four columns move per odd round (half the shared-memory
+// traffic of two-column slots), and every round has two or three independent rotation chains
+// per warp.  n' = round_up(k, 4) positions (zero columns pad).
+template <int LP, int E>
+__global__ void __launch_bounds__(256, 1) __cluster_dims__(2, 1, 1)
+svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, double* __restrict__ sigma_out,
+                double* __restrict__ Uw64, double* __restrict__ Vw64, float* __restrict__ uw32,
+                float* __restrict__ vw32, int64_t ld32, int* r_out, int* r_out2, void* ws) {
+  constexpr int G = 32 / LP;
+  constexpr int SEAT = E * LP + ((LP - (E * LP) % 16) + 16) % 16;
+  extern __shared__ __align__(16) double smem_d[];
+  __shared__ double s_sig[64];
+  __shared__ int s_perm[64];
+  __shared__ int s_id[2][2][36];      // [parity][col0 | col3][seat]
+  __shared__ double s_st[2][18][4][3];  // CTA 0: published n, d, 1 / d [parity][seat][position]
+  __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2];
+  __shared__ int s_last[2];
+  const uint32_t crank = cg::this_cluster().block_rank();
+#ifdef CABS_PROFILE_SVD
+  const long long q_k0 = clock64();
+#endif
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int gl = lane % LP, gw = lane / LP;
+  const int g = warp * G + gw;
+  const int n4 = (k + 3) & ~3, Q = n4 / 4;
+  const int nseat = nw * G + 2;
+  const bool live = g < Q;
+  const bool first = g == 0, lastslot = g == Q - 1;
+  const size_t arr = (size_t)2 * nseat * SEAT;
+  double* b0 = smem_d;       // published column 0 of each slot  [parity][seat][SEAT]
+  double* b3 = b0 + arr;     // published column 3
+  double* prm = b3 + arr;    // CTA 1: rotations [parity][round][slot][4]
+  if (tid == 0) {
+    tc::mbar_init(&bar_full[0], 1); tc::mbar_init(&bar_full[1], 1);
+    tc::mbar_init(&bar_empty[0], 1); tc::mbar_init(&bar_empty[1], 1);
+    tc::mbar_fence_init();
+  }
+  for (int e = tid; e < 2 * (int)arr; e += blockDim.x) smem_d[e] = 0.0;
+  for (int e = tid; e < 2 * 18 * 4 * 3; e += blockDim.x) (&s_st[0][0][0][0])[e] = (e % 3 == 0) ? 0.0 : 1.0;
+  for (int e = tid; e < 2 * 2 * 36; e += blockDim.x) (&s_id[0][0][0])[e] = 1 << 30;
+  cluster_sync_all();
+
+  double a[4][E];
+  int id[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) id[c] = 4 * g + c;
+  if (crank == 0) {
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = gl + LP * e;
+        float w = 0.f;
+        if (live && i < k && id[c] < k) w = W[(int64_t)i * ldw + id[c]];
+        bad |= !isfinite(w);
+        a[c][e] = w;
+      }
+    if (bad) set_status(ws, CABS_DEV_NONFINITE);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = gl + LP * e;
+        a[c][e] = (live && i == id[c] && id[c] < k) ? 1.0 : 0.0;
+      }
+  }
+  __syncthreads();
+  const double tol_rot = 2.0 * sqrt(static_cast<double>(k)) * DBL_EPSILON;
+  const double tol_rot2 = tol_rot * tol_rot;
+  double* const prm_remote = dsmem_map_generic(prm, 1);
+  const uint32_t full_remote0 = dsmem_map(&bar_full[0], 1), full_remote1 = dsmem_map(&bar_full[1], 1);
+  const uint32_t empty_remote0 = dsmem_map(&bar_empty[0], 0), empty_remote1 = dsmem_map(&bar_empty[1], 0);
+  const uint32_t last_remote = dsmem_map(&s_last[0], 1);
+  double* dvs = prm + (size_t)2 * n4 * Q * 4;  // CTA 1: column scales at sweep end [parity][position]
+  const uint32_t dvs_remote = dsmem_map(dvs, 1);
+  // Scaled columns: actual column = d * stored.  The scalar state of position p of the slot
+  // (squared norm n, scale d, 1 / d) lives on lanes 2p, 2p + 1 of the group ("owners"), and
+  // each rotation's scalar chain runs once per lane: a pair's two owner pairs of lanes compute
+  // it together (bit-identical inputs), each keeping its own position's new state.  CTA 1's V
+  // columns carry the same scales (they see the same rotations).
+  const int own = gl >> 1;                 // position owned
+  const int base = lane & ~(LP - 1);       // first lane of the group
+  const bool hi = (gl & 4) != 0, mid = (gl & 2) != 0;
+  double on = 0.0, od = 1.0, oi = 1.0;     // own position's n, d, 1 / d
+  int sweep = 0;
+  bool last = k <= 1;
+#ifdef CABS_PROFILE_SVD
+  long long q_wait = 0, q_t0 = clock64(), q_sweep = 0;
+#endif
+  for (; !last; ++sweep) {
+    const int sp = sweep & 1;
+#ifdef CABS_PROFILE_SVD
+    const long long w0 = clock64();
+#endif
+    if (crank == 0 && sweep >= 2) mbar_wait_cluster(&bar_empty[sp], static_cast<uint32_t>(((sweep - 2) >> 1) & 1));
+    if (crank == 1) mbar_wait_cluster(&bar_full[sp], static_cast<uint32_t>((sweep >> 1) & 1));
+#ifdef CABS_PROFILE_SVD
+    q_wait += clock64() - w0;
+    const long long s0 = clock64();
+#endif
+    int rotated = 0;
+    double tmax = 0.0;
+    if (crank == 0) {  // fold the scales in; exact squared norms at every sweep start, then by formula
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double dc = __shfl_sync(0xffffffffu, od, base + 2 * c);
+        double t0 = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          a[c][e] *= dc;
+          t0 = fma(a[c][e], a[c][e], t0);
+        }
+        t0 = group_sum<LP>(t0);
+        if (c == own) on = t0;
+      }
+      od = 1.0;
+      oi = 1.0;
+    }
+    for (int rnd = 0; rnd < n4; rnd += 2) {
+      // ---- even round: pairs (0,1) (lanes 0-3) and (2,3) (lanes 4-7), rotated and swapped
+      const int pidx = ((sp * n4 + rnd) * Q + (live ? g : 0)) * 4;  // [parity][round][slot][4]
+      double al01, be01, al23, be23;
+      if (crank == 0) {
+        double p01a = 0.0, p01b = 0.0, p23a = 0.0, p23b = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+          p01a = fma(a[0][e], a[1][e], p01a);
+          p23a = fma(a[2][e], a[3][e], p23a);
+          if (e + 1 < E) {
+            p01b = fma(a[0][e + 1], a[1][e + 1], p01b);
+            p23b = fma(a[2][e + 1], a[3][e + 1], p23b);
+          }
+        }
+        const double p01 = p01a + p01b, p23 = p23a + p23b;
+        // reduce-scatter: lanes 0-3 end with the (0,1) dot, lanes 4-7 with the (2,3) dot
+        double gsum = (hi ? p23 : p01) + __shfl_xor_sync(0xffffffffu, hi ? p01 : p23, 4);
+        gsum += __shfl_xor_sync(0xffffffffu, gsum, 2);
+        gsum += __shfl_xor_sync(0xffffffffu, gsum, 1);
+        const double pn = __shfl_xor_sync(0xffffffffu, on, 2);
+        const double pd = __shfl_xor_sync(0xffffffffu, od, 2);
+        const double pi = __shfl_xor_sync(0xffffffffu, oi, 2);
+        LaneRot r;
+        lane_rot(!mid, on, od, oi, pn, pd, pi, gsum, tol_rot2, r);
+        al01 = __shfl_sync(0xffffffffu, r.tu, base);  // lanes 0 and 4: left lanes
+        be01 = __shfl_sync(0xffffffffu, r.tv, base);
+        al23 = __shfl_sync(0xffffffffu, r.tu, base + 4);
+        be23 = __shfl_sync(0xffffffffu, r.tv, base + 4);
+        rotated |= live && r.need;
+        if (live) tmax = fmax(tmax, fabs(r.t));
+        if ((gl & 3) == 0 && live) dsmem_st2_f64(prm_remote + pidx + (hi ? 2 : 0), r.tu, r.tv);
+        on = r.n; od = r.d; oi = r.i;
+      } else {
+        const double* pr = prm + pidx;
+        al01 = live ? pr[0] : 0.0; be01 = live ? pr[1] : 0.0;
+        al23 = live ? pr[2] : 0.0; be23 = live ? pr[3] : 0.0;
+      }
+      // new position 0 = y + alpha x (the old 1 moves left), new 1 = x - beta y
+      double e0[E], e1[E], e2[E], e3[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        e0[e] = fma(al01, a[0][e], a[1][e]);
+        e1[e] = fma(-be01, a[1][e], a[0][e]);
+        e2[e] = fma(al23, a[2][e], a[3][e]);
+        e3[e] = fma(-be23, a[3][e], a[2][e]);
+      }
+      {
+        int t = id[0]; id[0] = id[1]; id[1] = t;
+        t = id[2]; id[2] = id[3]; id[3] = t;
+      }
+      // ---- odd round: (1,2) inside (lanes 2-5), (3, right slot's 0) (lanes 6,7) and
+      // (left slot's 3, 0) (lanes 0,1) across
+      const int par = ((rnd + 1) >> 1) & 1;
+      const size_t pub = ((size_t)par * nseat + g + 1) * SEAT + gl;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        b0[pub + e * LP] = e0[e];
+        b3[pub + e * LP] = e3[e];
+      }
+      if (gl == 0) {
+        s_id[par][0][g + 1] = id[0];
+        s_id[par][1][g + 1] = id[3];
+      }
+      if (crank == 0 && (gl & 1) == 0) {  // every position's n, d, 1 / d: [parity][seat][position]
+        s_st[par][g + 1][own][0] = on; s_st[par][g + 1][own][1] = od; s_st[par][g + 1][own][2] = oi;
+      }
+      __syncthreads();
+      const size_t lft = ((size_t)par * nseat + g) * SEAT + gl;      // left slot's column 3
+      const size_t rgt = ((size_t)par * nseat + g + 2) * SEAT + gl;  // right slot's column 0
+      double rl[E], rr[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        rl[e] = b3[lft + e * LP];
+        rr[e] = b0[rgt + e * LP];
+      }
+      const int pido = pidx + Q * 4;  // round rnd + 1
+      double al12, be12, alR, beL;
+      if (crank == 0) {
+        double p12a = 0.0, p12b = 0.0, pRa = 0.0, pRb = 0.0, pLa = 0.0, pLb = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+          p12a = fma(e1[e], e2[e], p12a);
+          pRa = fma(e3[e], rr[e], pRa);
+          pLa = fma(rl[e], e0[e], pLa);
+          if (e + 1 < E) {
+            p12b = fma(e1[e + 1], e2[e + 1], p12b);
+            pRb = fma(e3[e + 1], rr[e + 1], pRb);
+            pLb = fma(rl[e + 1], e0[e + 1], pLb);
+          }
+        }
+        const double p12 = p12a + p12b, pR = pRa + pRb, pL = pLa + pLb;
+        // reduce-scatter: lanes 0,1 end with the left crossing dot, 2-5 with (1,2), 6,7 with
+        // the right crossing dot (every sum is formed in a commutation of the same tree)
+        const double q12 = p12 + __shfl_xor_sync(0xffffffffu, p12, 4);
+        const double qX = (hi ? pR : pL) + __shfl_xor_sync(0xffffffffu, hi ? pL : pR, 4);
+        double gsum = ((hi != mid) ? q12 : qX) + __shfl_xor_sync(0xffffffffu, (hi != mid) ? qX : q12, 2);
+        gsum += __shfl_xor_sync(0xffffffffu, gsum, 1);
+        // partner position: 0 <- left slot's 3, 1 <-> 2, 3 <- right slot's 0
+        const int pseat = own == 0 ? g : (own == 3 ? g + 2 : g + 1), ppos = own ^ 3;
+        const double* ps = s_st[par][pseat][ppos];
+        LaneRot r;
+        lane_rot(mid, on, od, oi, ps[0], ps[1], ps[2], gsum, tol_rot2, r);
+        al12 = __shfl_sync(0xffffffffu, r.tu, base + 2);  // lanes 2 and 6: left lanes
+        be12 = __shfl_sync(0xffffffffu, r.tv, base + 2);
+        const double alR0 = __shfl_sync(0xffffffffu, r.tu, base + 6);
+        const double beL0 = __shfl_sync(0xffffffffu, r.tu, base);  // lanes 0, 1: right lanes
+        alR = lastslot ? 1.0 : alR0;
+        beL = first ? -1.0 : beL0;
+        const bool idle = (first && gl < 2) || (lastslot && gl >= 6);  // positions 0 and n' - 1 stay
+        rotated |= live && !idle && r.need;
+        if (live && !idle) tmax = fmax(tmax, fabs(r.t));
+        if ((gl == 2 || gl == 6) && live) dsmem_st2_f64(prm_remote + pido + (hi ? 2 : 0), r.tu, r.tv);
+        if (!idle) { on = r.n; od = r.d; oi = r.i; }
+      } else {
+        const double* pr = prm + pido;
+        al12 = live ? pr[0] : 0.0; be12 = live ? pr[1] : 0.0;
+        alR = lastslot ? 1.0 : (live ? pr[2] : 0.0);
+        // the left crossing pair is the left slot's right crossing pair
+        beL = first ? -1.0 : (live ? prm[pido - 4 + 3] : 0.0);
+      }
+      // idle end positions (0 and n' - 1) keep their column: coefficient 1 against the zero
+      // column of the never-written outer seat (or of a dead slot)
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        a[1][e] = fma(al12, e1[e], e2[e]);
+        a[2][e] = fma(-be12, e2[e], e1[e]);
+        a[3][e] = fma(alR, e3[e], rr[e]);
+        a[0][e] = fma(-beL, e0[e], rl[e]);
+      }
+      {
+        const int t = id[1]; id[1] = id[2]; id[2] = t;
+      }
+      if (!lastslot) id[3] = s_id[par][0][g + 2];
+      if (!first) id[0] = s_id[par][1][g];
+    }
+#ifdef CABS_PROFILE_SVD
+    q_sweep += clock64() - s0;
+#endif
+    if (crank == 0) {
+      if ((gl & 1) == 0 && live)  // the scales the sweep ended with, for CTA 1's V columns
+        dsmem_st_f64(dvs_remote + static_cast<uint32_t>((sp * n4 + 4 * g + own) * 8), od);
+      rotated = __syncthreads_or(rotated);
+      const int small = __syncthreads_and(tmax < 1e-8);
+      last = !rotated || small || sweep + 1 >= kSvdMaxSweeps;
+      if (tid == 0) {
+        dsmem_st_s32(last_remote + 4 * sp, last ? 1 : 0);
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        mbar_arrive_remote(sp ? full_remote1 : full_remote0);
+      }
+    } else {
+      if (live) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double dc = dvs[sp * n4 + 4 * g + c];
+#pragma unroll
+          for (int e = 0; e < E; ++e) a[c][e] *= dc;
+        }
+      }
+      __syncthreads();
+      last = s_last[sp] != 0;
+      __syncthreads();
+      if (tid == 0) mbar_arrive_remote(sp ? empty_remote1 : empty_remote0);
+    }
+  }
+  if (crank == 0) {
+    if (sweep >= kSvdMaxSweeps && k > 1) set_status(ws, CABS_DEV_SVD_NOCONV);
+    if (tid == 0) reinterpret_cast<int*>(ws)[8] = sweep;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double dc = __shfl_sync(0xffffffffu, od, base + 2 * c);
+#pragma unroll
+      for (int e = 0; e < E; ++e) a[c][e] *= dc;
+    }
+  }
+#ifdef CABS_PROFILE_SVD
+  if (tid == 0) {  // [CTA][wait, rounds, total]
+    long long* pw = reinterpret_cast<long long*>(ws) + 8 + 3 * crank;
+    pw[0] = q_wait; pw[1] = q_sweep; pw[2] = clock64() - q_t0;
+  }
+#endif
+  // ---- epilogue from the registers: sigma_c = |a_c| and the canonical sign (the largest-|.|
+  // entry of U_w's column positive, lowest row on ties) per column, rank order by one thread
+  // per column, then every group writes its own columns (CTA 0: U_w, CTA 1: V_w) in rank order.
+  __shared__ double s_sgn[64];
+  __shared__ int s_rank[64];
+  __shared__ int s_r;
+#ifdef CABS_PROFILE_SVD
+  const long long q_e0 = clock64();
+#endif
+  if (crank == 0) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double ss = 0.0, best = -1.0;
+      int bi = 0x7fffffff;
+      bool neg = false;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = gl + LP * e;
+        ss = fma(a[c][e], a[c][e], ss);
+        const double v = fabs(a[c][e]);
+        if (i < k && v > best) { best = v; bi = i; neg = a[c][e] < 0.0; }
+      }
+      ss = group_sum<LP>(ss);
+#pragma unroll
+      for (int o = LP / 2; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const bool on2 = __shfl_xor_sync(0xffffffffu, neg, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; neg = on2; }
+      }
+      if (gl == 0 && live && id[c] < k) {
+        s_sig[id[c]] = sqrt(ss);
+        s_sgn[id[c]] = neg ? -1.0 : 1.0;
+      }
+    }
+    __syncthreads();
+    const uint32_t rank_remote = dsmem_map(s_rank, 1), sgn_remote = dsmem_map(s_sgn, 1);
+    for (int c = tid; c < k; c += blockDim.x) {
+      const double sc = s_sig[c];
+      int rk = 0;
+      for (int j2 = 0; j2 < k; ++j2) {
+        const double sj = s_sig[j2];
+        rk += (sj > sc) || (sj == sc && j2 < c);
+      }
+      s_rank[c] = rk;
+      s_perm[rk] = c;
+      dsmem_st_s32(rank_remote + 4 * c, rk);
+      dsmem_st_f64(sgn_remote + 8 * c, s_sgn[c]);
+    }
+    __syncthreads();
+    if (warp == 0) {  // rank r: sigma_j > tol * sigma_max
+      const double smax = s_sig[s_perm[0]];
+      int cnt = 0;
+      for (int c = lane; c < k; c += 32) cnt += smax > 0 && s_sig[c] > tol * smax;
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if (lane == 0) {
+        s_r = cnt;
+        dsmem_st_s32(dsmem_map(&s_r, 1), cnt);
+        if (r_out) *r_out = cnt;
+        if (r_out2) *r_out2 = cnt;
+      }
+    }
+    if (sigma_out)
+      for (int j2 = tid; j2 < k; j2 += blockDim.x) sigma_out[j2] = s_sig[s_perm[j2]];
+  }
+  cluster_sync_all();
+#ifdef CABS_PROFILE_SVD
+  const long long q_e1 = clock64();
+#endif
+  {
+    const int r = s_r;
+    double* o64 = crank == 0 ? Uw64 : Vw64;
+    float* o32 = crank == 0 ? uw32 : vw32;
+    if (live) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (id[c] >= k) continue;
+        const int jr = s_rank[id[c]];
+        const bool keep = jr < r;
+        double mul;
+        if (crank == 0) {
+          const double sg = s_sig[id[c]];
+          mul = (keep && sg > 0) ? s_sgn[id[c]] / sg : 0.0;
+        } else {
+          mul = keep ? s_sgn[id[c]] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = gl + LP * e;
+          if (i < k) {
+            const double u = a[c][e] * mul;
+            if (o64) o64[(size_t)i * k + jr] = u;
+            if (o32) o32[(size_t)i * ld32 + jr] = static_cast<float>(u);
+          }
+        }
+      }
+    }
+    if (o32) {  // zero padding columns [k, ld32)
+      for (int64_t e = tid; e < (int64_t)k * (ld32 - k); e += blockDim.x) {
+        const int64_t i = e / (ld32 - k), c = k + e % (ld32 - k);
+        o32[i * ld32 + c] = 0.f;
+      }
+    }
+  }
+#ifdef CABS_PROFILE_SVD
+  __syncthreads();
+  if (crank == 0 && tid == 0) {  // [start -> loop start, loop end -> epilogue start, sigma, write]
+    long long* pw = reinterpret_cast<long long*>(ws) + 14;
+    pw[0] = q_t0 - q_k0; pw[1] = q_e0 - q_t0; pw[2] = q_e1 - q_e0; pw[3] = clock64() - q_e1;
+  }
+#endif
+}
+
+template <int LP, int E>
+static bool launch_quad(int k, const float* W, int64_t ldw, double tol, double* sig, double* Uw64, double* Vw64,
+                        float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st) {
+  constexpr int G = 32 / LP;
+  constexpr int SEAT = E * LP + ((LP - (E * LP) % 16) + 16) % 16;
+  const int n4 = (k + 3) & ~3, Q = n4 / 4;
+  const int nw = (Q + G - 1) / G;
+  const size_t xch = sizeof(double) * 2 * 2 * (size_t)(nw * G + 2) * SEAT;
+  const size_t prm = sizeof(double) * 2 * (size_t)n4 * (Q * 4 + 1);
+  const size_t smem = xch + prm;
+  constexpr int kCap = 200 * 1024;
+  if (smem > kCap) return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(svd_quad_kernel<LP, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCap);
+    attr = true;
+  }
+  svd_quad_kernel<LP, E><<<2, 32 * nw, smem, st>>>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user,
+                                                   ws);
+  return true;
+}
+
 // ---------------------------------------------------------------- k > 64: columns in memory
 template <int L, bool SMEM>
 __global__ void __launch_bounds__(kSvdThreads, 1)
@@ -915,14 +1407,22 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
   float* vw32 = wsp<float>(ws, L.vw32);
   note_launch();
   if (k <= 64 && !getenv("CABS_SVD_SMEM") && !getenv("CABS_SVD_ONE_SM")) {
-    // A on one SM, V on its cluster partner
-    // 8 lanes per column pair: 4 pairs per warp, up to 8 warps
-    if (k <= 16) launch_split<8, 2>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
-    else if (k <= 32) launch_split<8, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
-    else if (k <= 56 && getenv("CABS_SVD_LP2")) launch_split<2, 28>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
-    else if (k <= 56 && getenv("CABS_SVD_LP4")) launch_split<4, 14>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
-    else if (k <= 56) launch_split<8, 7>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
-    else launch_split<8, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    // A on one SM, V on its cluster partner; four columns per 8-lane slot (the two-column
+    // svd_split_kernel stays selectable for comparison)
+    if (!getenv("CABS_SVD_SPLIT")) {
+      if (k <= 16) launch_quad<8, 2>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+      else if (k <= 32) launch_quad<8, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+      else if (k <= 56) launch_quad<8, 7>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+      else launch_quad<8, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    } else if (k <= 16) {
+      launch_split<8, 2>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    } else if (k <= 32) {
+      launch_split<8, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    } else if (k <= 56) {
+      launch_split<8, 7>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    } else {
+      launch_split<8, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+    }
   } else if (k <= 64 && !getenv("CABS_SVD_SMEM")) {
     // register-resident systolic Jacobi, 4 lanes per column pair
     if (k <= 16) launch_systolic<4, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);

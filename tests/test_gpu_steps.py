@@ -122,8 +122,19 @@ def test_pilot_invalid_k(dev):
 
 
 # ------------------------------------------------------------------ S4 SVD
-@pytest.mark.parametrize("k,rank", [(20, 20), (50, 50), (100, 100), (112, 60), (150, 150), (7, 3), (1, 1)])
-def test_svd_matches_lapack(dev, k, rank):
+_SVD_KERNELS = {"quad": None, "split": "CABS_SVD_SPLIT", "one_sm": "CABS_SVD_ONE_SM", "smem": "CABS_SVD_SMEM"}
+
+
+@pytest.mark.parametrize("kernel", ["quad", "split", "one_sm", "smem"])
+@pytest.mark.parametrize("k,rank", [(20, 20), (50, 50), (64, 40), (100, 100), (112, 60), (150, 150), (7, 3),
+                                    (1, 1)])
+def test_svd_matches_lapack(dev, k, rank, kernel, monkeypatch):
+    """Every SVD kernel variant (k <= 64: the default 4-columns-per-slot cluster pair, the
+    2-column pair, the one-SM systolic and the shared-memory kernels; selected per call)."""
+    if kernel != "quad" and k > 64:
+        pytest.skip("one kernel beyond k = 64")
+    if _SVD_KERNELS[kernel]:
+        monkeypatch.setenv(_SVD_KERNELS[kernel], "1")
     g = np.random.default_rng(k * 7 + rank)
     W = (g.standard_normal((k, rank)) @ g.standard_normal((rank, k))).astype(np.float32)
     plan = _plan(max(k, 2), max(k, 2), k)

@@ -126,6 +126,30 @@ def probe_svd_prof(k=50):
     print(f"k={k} sweeps={sweeps} rounds~{rounds}: " + ", ".join(f"{n} {p / max(rounds, 1):.0f} cyc" for n, p in zip(names, prof)))
 
 
+def probe_svd_quad_prof(k=50):
+    """Needs -DCABS_PROFILE_SVD: per-CTA wait / round-loop / total cycles."""
+    dev = torch.device("cuda:0")
+    plan = make_plan(1000, 1000, k)
+    ws = torch.zeros(C.cabs_workspace_bytes(plan), dtype=torch.uint8, device=dev)
+    g = np.random.default_rng(0)
+    W = torch.from_numpy(g.standard_normal((k, k)).astype(np.float32)).to(dev)
+    sig = torch.zeros(k, dtype=torch.float64, device=dev)
+    r = torch.zeros(1, dtype=torch.int32, device=dev)
+    C.cabs_svd(plan, k, W, 1e-12, sig, None, None, r, ws)
+    torch.cuda.synchronize()
+    sweeps = int(ws[32:36].view(torch.int32).item())
+    p = ws[64:144].view(torch.int64).tolist()
+    print(f"  CTA0: start->loop {p[6]}, loop->epilogue {p[7]}, sigma {p[8]}, write {p[9]} cycles")
+    rounds = sweeps * ((k + 3) & ~3)
+    print(f"k={k} sweeps={sweeps}: CTA0 wait {p[0]} rounds {p[1]} ({p[1] / rounds:.0f}/round) total {p[2]}; "
+          f"CTA1 wait {p[3]} rounds {p[4]} ({p[4] / rounds:.0f}/round) total {p[5]}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "svdqprof":
+    probe_svd_quad_prof(50)
+    probe_svd_quad_prof(20)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "svdprof":
     for k in (20, 50):
         probe_svd_prof(k)
