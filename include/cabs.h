@@ -264,9 +264,11 @@ int32_t cabs_philox_blocks(uint64_t seed, uint32_t tag, uint64_t start, int64_t 
 /* Floyd sample of k distinct values in [0, N), sorted (the generator of cabs_pilot). */
 int32_t cabs_uniform_indices(int64_t N, int32_t k, uint64_t seed, uint32_t tag, int64_t* out,
                              void* stream);
-/* Diagnostic counters of profiling builds (-DCABS_PROFILE_RES): per-role cycle sums of the
- * tensor-core residual kernel's CTA 0 (host out[n], n <= 16); zeros in normal builds.
- * Synchronises the device. */
+/* Diagnostic counters of profiling builds: out[0..16) per-role cycle sums of the tensor-core
+ * residual kernel's CTA 0 (-DCABS_PROFILE_RES); out[16 + 16 b + i] the global-timer stamps
+ * (ns) of phase boundary i of iteration 10 in CTA b of the persistent Lloyd kernel
+ * (-DCABS_PROFILE_LLOYD, b < 320).  Host out[n]; zeros in normal builds.  Synchronises the
+ * device. */
 int32_t cabs_debug_counters(int64_t* out, int32_t n);
 /* FP64 Jacobi SVD of W (k x k, ldw): sigma (double[k], descending, all k), Uw, Vw
  * (double k x k row-major, column i = i-th singular vector, canonical signs,

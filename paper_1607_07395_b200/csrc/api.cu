@@ -87,7 +87,8 @@ const char* cabs_last_error_string(void) { return g_err; }
 int32_t cabs_debug_counters(int64_t* out, int32_t n) {
   if (!out || n < 0) return CABS_ERR_INVALID_ARG;
   cudaDeviceSynchronize();
-  residual_debug_counters(reinterpret_cast<long long*>(out), n);
+  residual_debug_counters(reinterpret_cast<long long*>(out), n < 16 ? n : 16);
+  if (n > 16) lloyd_debug_timeline(reinterpret_cast<long long*>(out) + 16, n - 16);
   return CABS_OK;
 }
 

@@ -69,10 +69,11 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.norms = take(sizeof(double) * 2 * Kp);
   w.scales = take(sizeof(float) * 8 * Kp);
   w.km_w = take(sizeof(float) * 2 * w.Nmax);
-  // k-means scratch per problem: int64 sums [3][K*Kp + K] | grid barrier | objective and
-  // near-tie partials [kKmItersCap][kNumSM] (the persistent kernel; the per-iteration path
-  // uses the first K*Kp + K sums)
-  w.km_scr_bytes = (sizeof(long long) * 3 * ((size_t)K * Kp + K) + 16 + (sizeof(double) + sizeof(int)) * kKmItersCap * kNumSM + 255) & ~size_t(255);
+  // k-means scratch per problem: int64 sums [3][K*Kp + K (+1: 16-byte slots)] | grid barrier |
+  // objective and near-tie partials [kKmItersCap][2 kNumSM] (the persistent kernel: up to two
+  // CTAs per SM; the per-iteration path uses the first K*Kp + K sums)
+  w.km_scr_bytes = (sizeof(long long) * 3 * ((size_t)K * Kp + K + 1) + 16 +
+                    (sizeof(double) + sizeof(int)) * kKmItersCap * 2 * kNumSM + 255) & ~size_t(255);
   w.km_scr = take(2 * w.km_scr_bytes);
   w.km_pobj = take(sizeof(double) * kAssignGrid);
   w.km_ptie = take(sizeof(int) * kAssignGrid);

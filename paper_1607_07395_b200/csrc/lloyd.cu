@@ -1,42 +1,58 @@
 // lloyd.cu -- the whole Lloyd loop of one or two k-means problems (the row side and the
 // column side of CABS, Alg. 2 steps 6-7) in ONE persistent kernel (single GPU):
-// c iterations x {centres | assign | accumulate | cluster reduce | grid sync}, no host round
-// trips, no per-iteration launches, ONE grid-wide barrier per iteration for both problems.
-// Every CTA (one per SM) holds a balanced contiguous slice of the points of EACH problem, so
-// the two problems share the synchronisation latency instead of paying it twice.
+// c iterations x {centres | assign | accumulate | cluster reduce | grid barrier}, no host
+// round trips, no per-iteration launches, ONE grid-wide barrier per iteration for both
+// problems.  Every CTA (one per SM) holds a balanced contiguous slice of the points of EACH
+// problem, so the two problems share the synchronisation latency instead of paying it twice.
 //
 // Arithmetic (Eq. 6; c iterations P:204):
 //  * distances by direct differences in FP32, dimensions ascending (= km_tile.cuh), lowest
 //    centre index on ties; two centres per packed FP32x2 instruction (FADD2/FFMA2: the same
 //    IEEE rounding as the scalar ops, half the instructions);
 //  * sums w_l X_l and w_l accumulated EXACTLY as int64 fixed point (km_fixed.cuh): a dense
-//    int64 partial per CTA in shared memory, the CTAs of a thread-block cluster add their
+//    int64 partial per CTA in shared memory (warp w owns the clusters j = w mod 8, so the
+//    read-modify-writes need no atomics), the CTAs of a thread-block cluster add their
 //    partials through distributed shared memory (each CTA one slice), and one
 //    red.global.add.u64 per (cluster, entry) lands in the global sums -- order-free, so
 //    deterministic and identical to the per-iteration kernels of kmeans.cu;
-//  * centres = (sum / 2^S) * (1 / (weight / 2^Sw)) in FP64; an empty cluster keeps its
-//    centre (Z12).
+//  * centres = (sum / 2^S) * (1 / (weight / 2^Sw)) in FP64, formed by every CTA for all
+//    entries straight from the global sums; an empty cluster keeps its centre (Z12).
 // Global sums rotate over three slots: slot it%3 accumulates, slot (it-1)%3 is read by
 // every CTA to form this iteration's centres, slot (it+1)%3 is zeroed for the next one.
+// Synchronisation per iteration: one cluster barrier (partials complete) and one grid
+// barrier (a monotonic arrival counter; the partials and the rotating slots make every
+// other hazard one iteration apart).
 #include <cooperative_groups.h>
 #include <float.h>
 #include <limits.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
 #include "km_fixed.cuh"
 #include "km_tile.cuh"
+#include "tc_ptx.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace cabsk {
 
 constexpr int kLT = 256;       // threads per CTA (one CTA per SM)
-constexpr int kLA = 9;         // max point rows per thread
+constexpr int kLA = 7;         // max point rows per thread
 constexpr int kLP = 16 * kLA;  // max points per chunk: thread (pt = tid & 15, ct = tid >> 4) owns points pt + 16u
 constexpr int kLC = 64;        // centres per block: ... and centres j0 + ct + 16v, v < 4
 constexpr int kMaxProb = 2;
+#ifdef CABS_PROFILE_LLOYD
+// per-CTA global-timer stamps of iteration kTlIter (phase boundaries), for cabs_debug_counters
+constexpr int kTlIter = 10;
+__device__ long long g_ll_tl[320][16];
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 
 struct LloydProb {
   const float* X;
@@ -53,21 +69,23 @@ struct LloydProb {
   const unsigned* bounds;  // [2] max|x|, max w (km_weights)
   double* pobj;            // [iters][G]
   int* ptie;               // [iters][G]
-  int pitch;               // resident chunk pitch (points, multiple of 16), or kLP when streaming
+  int cap;                 // points per chunk (multiple of 16, <= kLP): all of the CTA's when resident
+  int pitch;               // cap + 1: odd, so a warp reading one point's dimensions is conflict-free
 };
 
 struct LloydArgs {
   LloydProb pr[kMaxProb];
   int nprob, iters, resident;
-  unsigned* gbar;   // [2] grid barrier {arrivals, generation}
+  int g0;           // CTAs of problem 0 (the rest, gridDim.x - g0, run problem 1)
+  unsigned* gbar;   // grid barrier: monotonic arrival counter (zeroed at launch)
   long long* prof;  // diagnostics (CABS_PROFILE_LLOYD builds): per-phase cycles of the last CTA
 };
 
 // dynamic smem per problem: centre pairs [k2p/64][d][2][16][2] | points x [d][pitch] |
-// rows [pitch][d] | w 2^S (FP64) | llrint(w 2^Sw) | w | dense partial [k2*d + k2] |
-// 1 / cluster weight.  (X is never re-read from global memory: cluster.sync invalidates L1.)
+// w 2^S (FP64) | llrint(w 2^Sw) | w | dense partial [k2*d + k2] | 1 / cluster weight.
+// (X is never re-read from global memory: cluster.sync invalidates L1.)
 struct LloydSmem {
-  size_t cs, xs, xr, wsc, iw, wts, part, wd, total;
+  size_t cs, xs, wsc, iw, wts, part, wd, total;
 };
 __host__ __device__ inline LloydSmem lloyd_smem(int d, int k2, int pitch, size_t base) {
   LloydSmem L;
@@ -75,11 +93,10 @@ __host__ __device__ inline LloydSmem lloyd_smem(int d, int k2, int pitch, size_t
   auto take = [&](size_t b) { size_t r = o; o += (b + 15) & ~size_t(15); return r; };
   L.cs = take(sizeof(float) * round_up(k2, kLC) * d);
   L.xs = take(sizeof(float) * (size_t)d * pitch);
-  L.xr = take(sizeof(float) * (size_t)d * pitch);
   L.wsc = take(sizeof(double) * (size_t)pitch);
   L.iw = take(sizeof(long long) * (size_t)pitch);
   L.wts = take(sizeof(float) * (size_t)pitch);
-  L.part = take(sizeof(long long) * ((size_t)k2 * d + k2));
+  L.part = take(sizeof(long long) * (((size_t)k2 * d + k2 + 1) & ~size_t(1)));
   L.wd = take(sizeof(double) * (size_t)k2);
   L.total = o;
   return L;
@@ -113,7 +130,7 @@ __device__ __forceinline__ float f2_hi(unsigned long long v) { return __uint_as_
 
 // per-problem views of the CTA's shared memory
 struct ProbSmem {
-  float *cs, *xs, *xr, *wts;
+  float *cs, *xs, *wts;
   double *wsc, *wd;
   long long *iw, *part;
 };
@@ -121,7 +138,6 @@ __device__ __forceinline__ ProbSmem prob_smem(unsigned char* dyn, const LloydSme
   ProbSmem s;
   s.cs = reinterpret_cast<float*>(dyn + L.cs);
   s.xs = reinterpret_cast<float*>(dyn + L.xs);
-  s.xr = reinterpret_cast<float*>(dyn + L.xr);
   s.wsc = reinterpret_cast<double*>(dyn + L.wsc);
   s.iw = reinterpret_cast<long long*>(dyn + L.iw);
   s.wts = reinterpret_cast<float*>(dyn + L.wts);
@@ -130,21 +146,55 @@ __device__ __forceinline__ ProbSmem prob_smem(unsigned char* dyn, const LloydSme
   return s;
 }
 
-// chunk of np <= pitch points -> x [i][pitch], rows [p][d], w 2^S, llrint(w 2^Sw), w (zeros beyond)
+// chunk of np <= cap points -> x [i][pitch], w 2^S, llrint(w 2^Sw), w (zeros beyond)
 __device__ __forceinline__ void stage_chunk(const LloydProb& pr, int64_t p0, int np, const ProbSmem& S, double scale,
                                             double scale_w) {
-  const int d = pr.d, P = pr.pitch;
-  for (int e = threadIdx.x; e < P * d; e += blockDim.x) {
+  const int d = pr.d, P = pr.pitch, cap = pr.cap;
+  for (int e = threadIdx.x; e < cap * d; e += blockDim.x) {
     const int pp = e / d, i = e - pp * d;
-    const float x = pp < np ? __ldg(pr.X + (p0 + pp) * pr.ldx + i) : 0.f;
-    S.xs[i * P + pp] = x;
-    S.xr[e] = x;
+    S.xs[i * P + pp] = pp < np ? __ldg(pr.X + (p0 + pp) * pr.ldx + i) : 0.f;
   }
-  for (int pp = threadIdx.x; pp < P; pp += blockDim.x) {
+  for (int pp = threadIdx.x; pp < cap; pp += blockDim.x) {
     const float w = pp < np ? pr.w[p0 + pp] : 0.f;
     S.wsc[pp] = static_cast<double>(w) * scale;  // exact (power-of-two scale)
     S.iw[pp] = llrint(static_cast<double>(w) * scale_w);
     S.wts[pp] = w;
+  }
+}
+
+// Exact sums of the chunk (km_fixed.cuh) into the CTA's dense partial: warp w owns the
+// clusters j = w mod 8; for each it collects the chunk's points with label j (ballots over
+// the labels, held in registers), lanes over dimensions, and keeps the sums in registers --
+// one store (ADD when the CTA streams several chunks) per entry, no atomics, no sort.
+template <bool ADD>
+__device__ __forceinline__ void accumulate_owned(const int* lab, int np, const ProbSmem& S, int P, int d, int k2) {
+  constexpr int NB = (kLP + 31) / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nsum = k2 * d;
+  long long* __restrict__ part = S.part;
+  int labr[NB];
+#pragma unroll
+  for (int t = 0; t < NB; ++t) labr[t] = lane + 32 * t < np ? lab[lane + 32 * t] : -1;
+  for (int j = warp; j < k2; j += kLT / 32) {
+    for (int i0 = 0; i0 < d; i0 += 64) {
+      const int ia = i0 + lane, ib = i0 + 32 + lane;
+      long long sa = 0, sb = 0, sw = 0;
+#pragma unroll
+      for (int t = 0; t < NB; ++t) {
+        unsigned m = __ballot_sync(0xffffffffu, labr[t] == j);
+        while (m) {
+          const int p = 32 * t + __ffs(m) - 1;
+          m &= m - 1;
+          const double ws = S.wsc[p];
+          if (ia < d) sa += fx_prod_magic(ws, S.xs[ia * P + p]);
+          if (ib < d) sb += fx_prod_magic(ws, S.xs[ib * P + p]);
+          sw += S.iw[p];
+        }
+      }
+      if (ia < d) part[j * d + ia] = ADD ? part[j * d + ia] + sa : sa;
+      if (ib < d) part[j * d + ib] = ADD ? part[j * d + ib] + sb : sb;
+      if (i0 == 0 && lane == 0) part[nsum + j] = ADD ? part[nsum + j] + sw : sw;
+    }
   }
 }
 
@@ -206,38 +256,51 @@ __device__ __forceinline__ void dist_rows(const float* __restrict__ xs, int P, c
   }
 }
 
+void lloyd_debug_timeline(long long* out, int n) {
+#ifdef CABS_PROFILE_LLOYD
+  const int m = n < 320 * 16 ? n : 320 * 16;
+  cudaMemcpyFromSymbol(out, g_ll_tl, sizeof(long long) * m);
+#else
+  for (int i = 0; i < n; ++i) out[i] = 0;
+#endif
+}
+
 static_assert(kLT == 256, "8 warps: cluster ownership j % 8 and the 16 x 16 distance lanes");
-__global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
+static_assert(kLA == 7, "dist_rows instantiations cover up to 7 rows");
+__global__ void __launch_bounds__(kLT, 2) lloyd_persistent_kernel(LloydArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ float sb_d[8][kLP];  // per point: best / runner-up of each warp's two centre lanes
   __shared__ int sb_j[8][kLP];
   __shared__ float ss_d[8][kLP];
-  __shared__ int lab_s[kLP], order_s[kLP], slab_s[kLP];
-  __shared__ int hist_s[CABS_KMAX];
-  __shared__ int wstart_s[kLT / 32 + 1];
+  __shared__ int lab_s[kLP];
   __shared__ double s_red[kMaxProb][kLT / 32];
   __shared__ int s_tie[kMaxProb][kLT / 32];
+  __shared__ __align__(8) uint64_t s_mbar;  // the multicast sums of one iteration landed
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = static_cast<int>(cluster.block_rank()), csize = static_cast<int>(cluster.num_blocks());
-  unsigned gen = 0;  // grid-barrier generation
   const int tid = threadIdx.x, pt = tid & 15, ct = tid >> 4, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x, b = blockIdx.x, np_ = a.nprob;
+  const int G = gridDim.x, np_ = a.nprob;
+  // each CTA runs ONE problem (two CTAs per SM: the problems' latency-bound phases overlap);
+  // b / Gb: the CTA's index / count among its problem's CTAs (clusters never mix problems)
+  const int myq = (np_ > 1 && static_cast<int>(blockIdx.x) >= a.g0) ? 1 : 0;
+  const int b = myq ? static_cast<int>(blockIdx.x) - a.g0 : static_cast<int>(blockIdx.x);
+  const int Gb = np_ > 1 ? (myq ? G - a.g0 : a.g0) : G;
 
   // per problem: smem views, point range, scales, reduction slice
   LloydSmem Ls[kMaxProb];
-  int64_t pbeg[kMaxProb], pend[kMaxProb], Eq[kMaxProb], ebeg[kMaxProb], eend[kMaxProb];
+  int64_t pbeg[kMaxProb], pend[kMaxProb], Eq[kMaxProb], Eqp[kMaxProb], ebeg[kMaxProb], eend[kMaxProb];
   double scale[kMaxProb], scale_w[kMaxProb];
   {
-    size_t off = 0;
 #pragma unroll
     for (int q = 0; q < kMaxProb; ++q) {
       if (q >= np_) break;
+      if (q != myq) continue;
       const LloydProb& pr = a.pr[q];
-      Ls[q] = lloyd_smem(pr.d, pr.k2, pr.pitch, off);
-      off = Ls[q].total;
-      pbeg[q] = (pr.N * b) / G;
-      pend[q] = (pr.N * (b + 1)) / G;
+      Ls[q] = lloyd_smem(pr.d, pr.k2, pr.pitch, 0);
+      pbeg[q] = (pr.N * b) / Gb;
+      pend[q] = (pr.N * (b + 1)) / Gb;
       Eq[q] = (int64_t)pr.k2 * pr.d + pr.k2;
+      Eqp[q] = (Eq[q] + 1) & ~int64_t(1);  // slot stride: 16-byte aligned slots for the bulk copies
       ebeg[q] = Eq[q] * crank / csize;
       eend[q] = Eq[q] * (crank + 1) / csize;
       fx_scales(pr.bounds, pr.N, scale[q], scale_w[q]);
@@ -245,9 +308,14 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
   }
 
   // ---------------- prologue: resident chunks, initial centres (padding centres = 0)
+  if (tid == 0) {
+    tc::mbar_init(&s_mbar, 1);
+    tc::mbar_fence_init();  // visible to the cluster by the first cluster barrier
+  }
 #pragma unroll
   for (int q = 0; q < kMaxProb; ++q) {
     if (q >= np_) break;
+    if (q != myq) continue;
     const LloydProb& pr = a.pr[q];
     const ProbSmem S = prob_smem(dyn, Ls[q]);
     if (a.resident) stage_chunk(pr, pbeg[q], static_cast<int>(pend[q] - pbeg[q]), S, scale[q], scale_w[q]);
@@ -260,98 +328,106 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
 
 #ifdef CABS_PROFILE_LLOYD
   long long prof[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, t0 = clock64();
-#define LPROF(i) do { if (b == G - 1 && tid == 0) { long long t1 = clock64(); prof[i] += t1 - t0; t0 = t1; } } while (0)
+  int tl_n = 0;
+#define LPROF(i) do { if (blockIdx.x == G - 1 && tid == 0) { long long t1 = clock64(); prof[i] += t1 - t0; t0 = t1; } \
+                      if (it == kTlIter && tid == 0 && tl_n < 16) g_ll_tl[blockIdx.x][tl_n++] = globaltimer_ns(); } while (0)
 #else
 #define LPROF(i) do { } while (0)
 #endif
   for (int it = 0; it < a.iters; ++it) {
+    LPROF(9);
     if (it > 0) {
-      // centres of this iteration from the previous iteration's exact sums (empty cluster: keep).
-      // Each CTA forms the centres of ITS slice of the entries (the slice it reduced) and stores
-      // them into the centre arrays of all CTAs of its cluster (DSMEM); one cluster barrier.
+      // centres of this iteration from the previous iteration's exact sums, all entries, in
+      // every CTA (an empty cluster keeps its centre).  The sums reach every CTA of the
+      // cluster by bulk copies multicast from the CTAs' slices (one L2 read per cluster) into
+      // the partial buffers (free: read by the cluster before the last grid barrier).
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        uint32_t total = 0;
 #pragma unroll
-      for (int q = 0; q < kMaxProb; ++q) {
-        if (q >= np_) break;
-        const LloydProb& pr = a.pr[q];
-        const ProbSmem S = prob_smem(dyn, Ls[q]);
-        const int64_t nsum = (int64_t)pr.k2 * pr.d;
-        const long long* fs_prev = pr.fsum + (size_t)((it + 2) % 3) * Eq[q];
-        for (int j = tid; j < pr.k2; j += blockDim.x) {
-          const long long wj = __ldcg(fs_prev + nsum + j);
-          S.wd[j] = wj > 0 ? 1.0 / (static_cast<double>(wj) * (1.0 / scale_w[q])) : 0.0;
+        for (int q = 0; q < kMaxProb; ++q)
+          if (q == myq) total += static_cast<uint32_t>(Eqp[q] * 8);
+        tc::mbar_expect_tx(&s_mbar, total);
+#pragma unroll
+        for (int q = 0; q < kMaxProb; ++q) {
+          if (q >= np_) break;
+          if (q != myq) continue;
+          const ProbSmem S = prob_smem(dyn, Ls[q]);
+          const int64_t n16 = Eqp[q] / 2;  // 16-byte units
+          const int64_t c0 = n16 * crank / csize, c1 = n16 * (crank + 1) / csize;
+          if (c1 > c0) {
+            const long long* src = a.pr[q].fsum + (size_t)((it + 2) % 3) * Eqp[q] + 2 * c0;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+                "[%0], [%1], %2, [%3], %4;" ::"r"(tc::smem_u32(S.part + 2 * c0)),
+                "l"(src), "r"(static_cast<uint32_t>((c1 - c0) * 16)), "r"(tc::smem_u32(&s_mbar)),
+                "h"(static_cast<uint16_t>((1u << csize) - 1u))
+                : "memory");
+          }
         }
       }
-      constexpr int U = 4;  // slice entries per thread per problem (c2: ~2.5)
-      long long sv[kMaxProb][U];
+      tc::mbar_wait(&s_mbar, static_cast<uint32_t>((it - 1) & 1));
+      LPROF(8);
 #pragma unroll
       for (int q = 0; q < kMaxProb; ++q) {
         if (q >= np_) break;
+        if (q != myq) continue;
         const LloydProb& pr = a.pr[q];
-        const int64_t nsum = (int64_t)pr.k2 * pr.d;
-        const long long* fs_prev = pr.fsum + (size_t)((it + 2) % 3) * Eq[q];
-        const int64_t se = eend[q] < nsum ? eend[q] : nsum;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t e = ebeg[q] + tid + (int64_t)u * kLT;
-          sv[q][u] = e < se ? __ldcg(fs_prev + e) : 0;
+        const ProbSmem S = prob_smem(dyn, Ls[q]);
+        const int nsum = pr.k2 * pr.d;
+        for (int j = tid; j < pr.k2; j += blockDim.x) {
+          const long long wj = S.part[nsum + j];
+          S.wd[j] = wj > 0 ? 1.0 / (static_cast<double>(wj) * (1.0 / scale_w[q])) : 0.0;
         }
       }
       __syncthreads();  // wd ready
 #pragma unroll
       for (int q = 0; q < kMaxProb; ++q) {
         if (q >= np_) break;
+        if (q != myq) continue;
         const LloydProb& pr = a.pr[q];
         const ProbSmem S = prob_smem(dyn, Ls[q]);
         const int d = pr.d;
-        const int64_t nsum = (int64_t)pr.k2 * d;
         const double inv_scale = 1.0 / scale[q];
-        const long long* fs_prev = pr.fsum + (size_t)((it + 2) % 3) * Eq[q];
-        const int64_t se = eend[q] < nsum ? eend[q] : nsum;
-        float* rcs[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) rcs[r] = r < csize ? cluster.map_shared_rank(S.cs, r) : S.cs;
-        for (int64_t e0 = ebeg[q] + tid, u0 = 0; e0 < se; e0 += (int64_t)U * kLT, u0 += U) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int64_t e = e0 + (int64_t)u * kLT;
-            if (e >= se) break;
-            const long long v = u0 == 0 ? sv[q][u] : __ldcg(fs_prev + e);
-            const int j = static_cast<int>(e / d), i = static_cast<int>(e - (int64_t)j * d);
-            const double rw = S.wd[j];
-            if (rw > 0) {
-              const float c = static_cast<float>((static_cast<double>(v) * inv_scale) * rw);
-              const int ci = cpair_idx(j, i, d);
-#pragma unroll
-              for (int r = 0; r < 8; ++r)
-                if (r < csize) rcs[r][ci] = c;
-            }
+        // thread (j mod 64, i group): lanes over centres, so the stores into the pair layout
+        // are conflict-free; no division per entry
+        for (int j = tid & 63; j < pr.k2; j += 64) {
+          const double rw = S.wd[j];
+          if (rw > 0) {
+#pragma unroll 4
+            for (int i = tid >> 6; i < d; i += kLT / 64)
+              S.cs[cpair_idx(j, i, d)] = static_cast<float>((static_cast<double>(S.part[j * d + i]) * inv_scale) * rw);
           }
         }
-        // zero the slot the next iteration accumulates into (last read before the previous barrier)
-        long long* fs_next = pr.fsum + (size_t)((it + 1) % 3) * Eq[q];
-        for (int64_t e = (int64_t)b * blockDim.x + tid; e < Eq[q]; e += (int64_t)G * blockDim.x) fs_next[e] = 0;
+        // zero this CTA's share of the slot the next iteration accumulates into (last read
+        // before the previous grid barrier)
+        long long* fs_next = pr.fsum + (size_t)((it + 1) % 3) * Eqp[q];
+        for (int64_t e = (int64_t)b * blockDim.x + tid; e < Eq[q]; e += (int64_t)Gb * blockDim.x) fs_next[e] = 0;
+      }
+      __syncthreads();  // staged sums consumed: the partial buffers are free
+    }
+    if (!a.resident) {
+#pragma unroll
+      for (int q = 0; q < kMaxProb; ++q) {  // the partials the streamed chunks add into
+        if (q >= np_) break;
+        if (q != myq) continue;
+        const ProbSmem S = prob_smem(dyn, Ls[q]);
+        for (int64_t e = tid; e < Eq[q]; e += blockDim.x) S.part[e] = 0;
       }
     }
-#pragma unroll
-    for (int q = 0; q < kMaxProb; ++q) {
-      if (q >= np_) break;
-      const ProbSmem S = prob_smem(dyn, Ls[q]);
-      for (int64_t e = tid; e < Eq[q]; e += blockDim.x) S.part[e] = 0;
-    }
-    if (it > 0) cluster.sync();  // every CTA of the cluster has stored its slice of the centres
-    else __syncthreads();
+    __syncthreads();
     LPROF(0);
 #pragma unroll
     for (int q = 0; q < kMaxProb; ++q) {
       if (q >= np_) break;
+      if (q != myq) continue;
       const LloydProb& pr = a.pr[q];
       const ProbSmem S = prob_smem(dyn, Ls[q]);
       const int d = pr.d, k2 = pr.k2;
-      const int64_t nsum = (int64_t)k2 * d;
       double obj = 0.0;
       int ties = 0;
-      for (int64_t p0 = pbeg[q]; p0 < pend[q]; p0 += pr.pitch) {
-        const int np = static_cast<int>(pend[q] - p0 < pr.pitch ? pend[q] - p0 : pr.pitch);
+      for (int64_t p0 = pbeg[q]; p0 < pend[q]; p0 += pr.cap) {
+        const int np = static_cast<int>(pend[q] - p0 < pr.cap ? pend[q] - p0 : pr.cap);
         if (!a.resident) {
           __syncthreads();  // previous chunk fully consumed
           stage_chunk(pr, p0, np, S, scale[q], scale_w[q]);
@@ -362,8 +438,7 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
           const int na = (np + 15) >> 4;
           if (na <= 3) dist_rows<3>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
           else if (na <= 5) dist_rows<5>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
-          else if (na <= 7) dist_rows<7>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
-          else dist_rows<9>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
+          else dist_rows<7>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
         }
         __syncthreads();
         for (int p = tid; p < np; p += kLT) {  // merge the 8 warps (lowest index on ties)
@@ -382,85 +457,12 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
         }
         __syncthreads();
         LPROF(1);
-        // exact sums (km_fixed.cuh).  Counting sort of the chunk's points by label (the order
-        // inside a label is irrelevant: integer sums), then warp w takes a contiguous range of
-        // the sorted points aligned to label-run starts (every cluster belongs to ONE warp) and
-        // keeps the running sums of the current run in registers, lanes over dimensions:
-        // no read-modify-write chains, one flush per run.
-        {
-          for (int j = tid; j < k2; j += kLT) hist_s[j] = 0;
-          __syncthreads();
-          for (int p = tid; p < np; p += kLT) atomicAdd(&hist_s[lab_s[p]], 1);
-          __syncthreads();
-          if (warp == 0) {  // exclusive scan of the k2 counts: lane owns a contiguous block
-            const int per = (k2 + 31) >> 5;
-            const int b0 = lane * per, b1 = b0 + per < k2 ? b0 + per : k2;
-            int sl = 0;
-            for (int j = b0; j < b1; ++j) sl += hist_s[j];
-            int inc = sl;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int t = __shfl_up_sync(0xffffffffu, inc, o);
-              if (lane >= o) inc += t;
-            }
-            int run = inc - sl;
-            for (int j = b0; j < b1; ++j) {
-              const int c = hist_s[j];
-              hist_s[j] = run;
-              run += c;
-            }
-          }
-          __syncthreads();
-          for (int p = tid; p < np; p += kLT) {
-            const int l = lab_s[p];
-            const int pos = atomicAdd(&hist_s[l], 1);
-            order_s[pos] = p;
-            slab_s[pos] = l;
-          }
-          __syncthreads();
-          if (tid <= kLT / 32) {
-            int q = (tid * np) / (kLT / 32);
-            if (tid < kLT / 32) {
-              while (q > 0 && q < np && slab_s[q] == slab_s[q - 1]) ++q;
-            } else {
-              q = np;
-            }
-            wstart_s[tid] = q;
-          }
-          __syncthreads();
-          const int qb = wstart_s[warp], qe = wstart_s[warp + 1];
-          long long* __restrict__ pp = S.part;
-          const float* __restrict__ xr = S.xr;
-          if (qb < qe) {
-            for (int i0 = 0; i0 < d; i0 += 64) {
-              const int ia = i0 + lane, ib = i0 + 32 + lane;
-              const bool wl = i0 == 0 && lane == 0;
-              long long sa = 0, sbv = 0, sw = 0;
-              int jc = slab_s[qb];
-#pragma unroll 4
-              for (int q = qb; q < qe; ++q) {
-                const int j = slab_s[q];
-                if (j != jc) {  // run of cluster jc ends: flush (this warp owns jc)
-                  if (ia < d) pp[(int64_t)jc * d + ia] += sa;
-                  if (ib < d) pp[(int64_t)jc * d + ib] += sbv;
-                  if (wl) pp[nsum + jc] += sw;
-                  sa = 0; sbv = 0; sw = 0;
-                  jc = j;
-                }
-                const int p = order_s[q];
-                const double ws = S.wsc[p];
-                const float* xrow = xr + p * d;
-                if (ia < d) sa += fx_prod_magic(ws, xrow[ia]);
-                if (ib < d) sbv += fx_prod_magic(ws, xrow[ib]);
-                if (wl) sw += S.iw[p];
-              }
-              if (ia < d) pp[(int64_t)jc * d + ia] += sa;
-              if (ib < d) pp[(int64_t)jc * d + ib] += sbv;
-              if (wl) pp[nsum + jc] += sw;
-            }
-          }
+        if (a.resident) {
+          accumulate_owned<false>(lab_s, np, S, pr.pitch, d, k2);
+        } else {
+          accumulate_owned<true>(lab_s, np, S, pr.pitch, d, k2);
+          __syncthreads();  // lab_s and the chunk are reused
         }
-        __syncthreads();
         LPROF(2);
       }
       obj = warp_sum_d(obj);
@@ -475,8 +477,9 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
 #pragma unroll
     for (int q = 0; q < kMaxProb; ++q) {
       if (q >= np_) break;
+      if (q != myq) continue;
       const ProbSmem S = prob_smem(dyn, Ls[q]);
-      long long* fs_cur = a.pr[q].fsum + (size_t)(it % 3) * Eq[q];
+      long long* fs_cur = a.pr[q].fsum + (size_t)(it % 3) * Eqp[q];
       const long long* rp[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) rp[r] = r < csize ? cluster.map_shared_rank(S.part, r) : S.part;
@@ -490,41 +493,36 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
         if (s != 0) red_add_u64(fs_cur + e, s);
       }
     }
-    LPROF(6);
     if (tid == 0) {
 #pragma unroll
       for (int q = 0; q < kMaxProb; ++q) {
         if (q >= np_) break;
+        if (q != myq) continue;
         double sacc = 0;
         int qq = 0;
         for (int w = 0; w < kLT / 32; ++w) { sacc += s_red[q][w]; qq += s_tie[q][w]; }
-        a.pr[q].pobj[(size_t)it * G + b] = sacc;
-        a.pr[q].ptie[(size_t)it * G + b] = qq;
+        a.pr[q].pobj[(size_t)it * Gb + b] = sacc;
+        a.pr[q].ptie[(size_t)it * Gb + b] = qq;
       }
     }
-    __threadfence();
+    // the partial buffers are overwritten next by the async proxy (the multicast sums)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    LPROF(6);
+    // grid barrier: monotonic arrival counter.  The partials are re-zeroed only after it (no
+    // CTA still reads them), and the slots rotate, so nothing else needs a barrier.
+    __syncthreads();
     LPROF(7);
-    cluster.sync();  // partials free again; this cluster's global adds issued and fenced
-    LPROF(8);
-    // grid barrier between cluster leaders only, then the cluster barrier releases the members
-    if (crank == 0 && tid == 0) {
-      unsigned* bar = a.gbar;
-      const unsigned nb = static_cast<unsigned>(G / csize);
-      if (atomicAdd(bar, 1u) == nb - 1) {
-        atomicExch(bar, 0u);
-        __threadfence();
-        atomicExch(bar + 1, gen + 1);
-      } else {
-        while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(20);
-      }
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(a.gbar, 1u);
+      const unsigned target = static_cast<unsigned>(G) * static_cast<unsigned>(it + 1);
+      while (ld_acquire_gpu(a.gbar) < target) __nanosleep(20);
     }
-    ++gen;
+    __syncthreads();
     LPROF(3);
-    cluster.sync();
-    LPROF(4);
   }
 #ifdef CABS_PROFILE_LLOYD
-  if (b == G - 1 && tid == 0)
+  if (blockIdx.x == G - 1 && tid == 0)
     for (int i = 0; i < 10; ++i) a.prof[i] = prof[i];
 #endif
   // ---------------- epilogue (CTA 0): final centres, cluster weights, objective history
@@ -532,11 +530,12 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
 #pragma unroll
     for (int q = 0; q < kMaxProb; ++q) {
       if (q >= np_) break;
+      if (q != myq) continue;
       const LloydProb& pr = a.pr[q];
       const ProbSmem S = prob_smem(dyn, Ls[q]);
       const int d = pr.d, k2 = pr.k2, nsum = k2 * d;
       const double inv_scale = 1.0 / scale[q], inv_scale_w = 1.0 / scale_w[q];
-      const long long* fs_last = pr.fsum + (size_t)((a.iters - 1) % 3) * Eq[q];
+      const long long* fs_last = pr.fsum + (size_t)((a.iters - 1) % 3) * Eqp[q];
       for (int e = tid; e < nsum; e += blockDim.x) {
         const int j = e / d, i = e - j * d;
         const long long wj = __ldcg(fs_last + nsum + j);
@@ -550,9 +549,9 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
       for (int it = tid; it < a.iters; it += blockDim.x) {
         double s = 0;
         long long qq = 0;
-        for (int g = 0; g < G; ++g) {
-          s += __ldcg(pr.pobj + (size_t)it * G + g);
-          qq += __ldcg(pr.ptie + (size_t)it * G + g);
+        for (int g = 0; g < Gb; ++g) {
+          s += __ldcg(pr.pobj + (size_t)it * Gb + g);
+          qq += __ldcg(pr.ptie + (size_t)it * Gb + g);
         }
         pr.objective[it] = s;
         if (pr.near_ties) pr.near_ties[it] = static_cast<int>(qq);
@@ -564,6 +563,8 @@ __global__ void __launch_bounds__(kLT, 1) lloyd_persistent_kernel(LloydArgs a) {
 // Returns false when the fast path does not apply (caller uses the per-iteration kernels).
 bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long long* prof, cudaStream_t st) {
   if (njobs < 1 || njobs > kMaxProb) return false;
+  for (int q = 0; q < njobs; ++q)
+    if (jobs[q].k2 > CABS_KMAX) return false;
   for (int q = 0; q < njobs; ++q)
     if (jobs[q].N <= 0) return false;
   constexpr size_t kSmemCap = 200 * 1024;
@@ -577,28 +578,14 @@ bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long lo
   int dev = 0, nsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  int64_t Nmin = jobs[0].N;
-  for (int q = 1; q < njobs; ++q) Nmin = jobs[q].N < Nmin ? jobs[q].N : Nmin;
-  // grid: one CTA per SM (every CTA holds ~N / #SM points of each problem); the largest
-  // cluster size (8, 4, 2, 1) whose clusters can all be resident
-  int64_t G = nsm;
-  if (G > Nmin) G = Nmin;
-  auto smem_for = [&](int64_t g, int& resident, int* pitch) {
-    resident = 1;
-    size_t total = 0;
-    for (int q = 0; q < njobs; ++q) {
-      const int64_t per = ceil_div(jobs[q].N, g);
-      pitch[q] = per <= kLP ? static_cast<int>(round_up(per, 16)) : kLP;
-      if (per > kLP) resident = 0;
-      total = lloyd_smem(jobs[q].d, jobs[q].k2, pitch[q], total).total;
-    }
-    return total;
-  };
+  // grid: two CTAs per SM when they fit (else one), each running ONE problem -- the problems
+  // get CTAs in proportion to their points (whole clusters each) -- and the largest cluster
+  // size (8, 4, 2, 1) whose clusters can all be resident
   LloydArgs a{};
   a.nprob = njobs;
   a.iters = iters;
   a.prof = prof;
-  int pitch[kMaxProb] = {kLP, kLP};
+  int cap[kMaxProb] = {kLP, kLP};
   int resident = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kLT);
@@ -612,35 +599,70 @@ bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long lo
   cfg.attrs = at;
   cfg.numAttrs = 2;
   int csize = 0;
+  int64_t G = 0, Gq[kMaxProb] = {0, 0};
   size_t smem = 0;
-  for (int c = 8; c >= 1 && csize == 0; c >>= 1) {
-    const int64_t g = G / c * c;  // round down: every CTA still gets <= ceil(N / g) points
-    if (g < 1) continue;
-    smem = smem_for(g, resident, pitch);
-    if (smem > kSmemCap) continue;
-    at[0].val.clusterDim.x = static_cast<unsigned>(c);
-    cfg.gridDim = dim3(static_cast<unsigned>(g));
-    cfg.dynamicSmemBytes = smem;
-    int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, lloyd_persistent_kernel, &cfg) == cudaSuccess && (int64_t)ncl * c >= g) {
-      csize = c;
-      G = g;
+  const double Ntot = static_cast<double>(jobs[0].N) + (njobs > 1 ? static_cast<double>(jobs[1].N) : 0.0);
+  const int per_sm0 = getenv("CABS_LLOYD_ONE_PER_SM") ? 1 : 2;
+  for (int per_sm = per_sm0; per_sm >= 1 && csize == 0; --per_sm) {
+    const int cmax = getenv("CABS_LLOYD_MAX_CLUSTER") ? atoi(getenv("CABS_LLOYD_MAX_CLUSTER")) : 8;
+    for (int c = 8; c >= 1 && csize == 0; c >>= 1) {
+      if (c > cmax) continue;
+      const int64_t tot = (int64_t)nsm * per_sm / c * c;
+      if (tot < c * njobs) continue;
+      int64_t g[kMaxProb] = {tot, 0};
+      if (njobs > 1) {
+        g[0] = (int64_t)llround(static_cast<double>(tot) * static_cast<double>(jobs[0].N) / Ntot / c) * c;
+        g[0] = g[0] < c ? c : (g[0] > tot - c ? tot - c : g[0]);
+        g[1] = tot - g[0];
+      }
+      bool ok = true;
+      int r = 1, cp[kMaxProb] = {kLP, kLP};
+      size_t sm = 0;
+      for (int q = 0; q < njobs; ++q) {
+        if (g[q] > jobs[q].N) ok = false;
+        const int64_t per = ceil_div(jobs[q].N, g[q] > 0 ? g[q] : 1);
+        cp[q] = per <= kLP ? static_cast<int>(round_up(per, 16)) : kLP;
+        if (per > kLP) r = 0;
+        const size_t t = lloyd_smem(jobs[q].d, jobs[q].k2, cp[q] + 1, 0).total;
+        sm = t > sm ? t : sm;
+      }
+      if (!ok || sm > kSmemCap) continue;
+      at[0].val.clusterDim.x = static_cast<unsigned>(c);
+      cfg.gridDim = dim3(static_cast<unsigned>(tot));
+      cfg.dynamicSmemBytes = sm;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, lloyd_persistent_kernel, &cfg) == cudaSuccess &&
+          (int64_t)ncl * c >= tot) {
+        csize = c;
+        G = tot;
+        Gq[0] = g[0];
+        Gq[1] = g[1];
+        smem = sm;
+        resident = r;
+        cap[0] = cp[0];
+        cap[1] = cp[1];
+      }
     }
   }
   cudaGetLastError();
   if (csize == 0) return false;
+  cfg.gridDim = dim3(static_cast<unsigned>(G));
+  cfg.dynamicSmemBytes = smem;
+  at[0].val.clusterDim.x = static_cast<unsigned>(csize);
   a.resident = resident;
+  a.g0 = static_cast<int>(Gq[0]);
   // scratch of each job: fsum [3][k2*d + k2] | pobj [iters][G] | ptie [iters][G]; barrier in job 0's
   for (int q = 0; q < njobs; ++q) {
     const LloydJob& j = jobs[q];
-    const size_t E = (size_t)j.k2 * j.d + j.k2;
+    const size_t E = ((size_t)j.k2 * j.d + j.k2 + 1) & ~size_t(1);  // slot stride (16-byte aligned)
     const size_t need = sizeof(long long) * 3 * E + 16 + (sizeof(double) + sizeof(int)) * iters * G;
     if (need > j.scratch_bytes) return false;
     char* base = static_cast<char*>(j.scratch);
     LloydProb& p = a.pr[q];
     p.X = j.X; p.ldx = j.ldx; p.N = j.N; p.d = j.d; p.k2 = j.k2; p.w = j.w;
     p.centres = j.centres; p.ldc = j.ldc; p.labels = j.labels; p.objective = j.objective;
-    p.near_ties = j.near_ties; p.cluster_w = j.cluster_w; p.bounds = j.bounds; p.pitch = pitch[q];
+    p.near_ties = j.near_ties; p.cluster_w = j.cluster_w; p.bounds = j.bounds; p.cap = cap[q];
+    p.pitch = cap[q] + 1;
     p.fsum = reinterpret_cast<long long*>(base);
     unsigned* gb = reinterpret_cast<unsigned*>(p.fsum + 3 * E);
     if (q == 0) a.gbar = gb;

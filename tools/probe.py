@@ -1,4 +1,5 @@
 """Quick GPU probes (timings + diagnostics) for development; not part of the product path."""
+import ctypes
 import sys
 import time
 
@@ -198,14 +199,30 @@ def probe_lloyd_pair(Na=20000, Nb=10000, d=50, k2=50, iters=20, prof=False):
     line = f"kmeans_pair Na={Na} Nb={Nb} d={d} k2={k2} iters={iters}: {t:.1f} us ({t / iters:.1f} us/iter)"
     if prof:
         p = ws[64:144].view(torch.int64).tolist()
-        names = ["centres+zero", "dist+argmin(last prob)", "accum(last prob)", "obj-publish", "cluster.sync3",
-                 "cluster.sync1", "dsmem-reduce+red", "fence", "cluster.sync2+leader barrier"]
-        line += "\n  " + ", ".join(f"{n} {v / iters:.0f}" for n, v in zip(names, p))
+        names = ["centres+zero", "dist+merge", "accum", "grid barrier", "-", "cluster.sync", "dsmem-reduce+red"]
+        line += "\n  " + ", ".join(f"{n} {v / iters:.0f}" for n, v in zip(names, p) if n != "-")
     print(line)
+
+
+def lloyd_timeline(G=148):
+    """Per-CTA phase stamps of iteration 10 (-DCABS_PROFILE_LLOYD): duration statistics over
+    the CTAs, and where the iteration's critical path goes (relative to the first CTA's start)."""
+    t = np.array(C.cabs_debug_counters(16 + 320 * 16), dtype=np.int64)[16:].reshape(320, 16)
+    t = t[(t[:, 0] > 0)]
+    names = ["top", "mbar", "centres", "dist", "acc", "csync", "reduce", "prebar", "passbar"]
+    t = t[:, :len(names)].astype(np.float64)
+    t0 = t[:, 0].min()
+    print(f"  timeline of {t.shape[0]} CTAs (ns; start = first CTA at iteration top)")
+    for i in range(1, len(names)):
+        dur = t[:, i] - t[:, i - 1]
+        print(f"    {names[i]:8s} dur min {dur.min():7.0f} med {np.median(dur):7.0f} max {dur.max():7.0f}"
+              f" | reached at min {t[:, i].min() - t0:7.0f} max {t[:, i].max() - t0:7.0f}")
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "lloydpair":
     probe_lloyd_pair(prof=len(sys.argv) > 2)
+    if len(sys.argv) > 2:
+        lloyd_timeline()
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "lloydprof":
