@@ -198,6 +198,58 @@ __device__ __forceinline__ void accumulate_owned(const int* lab, int np, const P
   }
 }
 
+// One block of centres jc + 16 v, v < NV (jc = j0 + ct), against the points pt + 16 u: pairs
+// (v, v + 1) in one FFMA2 lane pair, an odd last centre in scalar FP32 (the same IEEE ops).
+template <int NA, int NV>
+__device__ __forceinline__ void dist_block(const float* __restrict__ xq, int P, const unsigned long long* cq, int d,
+                                           int jc, int k2, float* bd, float* sd, int* bj) {
+  unsigned long long acc0[NA], acc1[NA];
+  float accs[NA];
+#pragma unroll
+  for (int u = 0; u < NA; ++u) { acc0[u] = 0ull; acc1[u] = 0ull; accs[u] = 0.f; }
+  for (int i = 0; i < d; ++i) {
+    const unsigned long long c0 = cq[i * 32];
+    const unsigned long long c1 = NV >= 3 ? cq[i * 32 + 16] : 0ull;
+    float x[NA];
+#pragma unroll
+    for (int u = 0; u < NA; ++u) x[u] = xq[i * P + 16 * u];
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      if (NV >= 2) {
+        const unsigned long long xx = f2_dup(x[u]);
+        const unsigned long long df0 = f2_sub(xx, c0);
+        acc0[u] = f2_fma(df0, df0, acc0[u]);
+        if (NV == 4) {
+          const unsigned long long df1 = f2_sub(xx, c1);
+          acc1[u] = f2_fma(df1, df1, acc1[u]);
+        } else if (NV == 3) {
+          const float df = x[u] - f2_lo(c1);
+          accs[u] = fmaf(df, df, accs[u]);
+        }
+      } else {
+        const float df = x[u] - f2_lo(c0);
+        accs[u] = fmaf(df, df, accs[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int j = jc + 16 * v;
+    if (j >= k2) continue;
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      float val;
+      if (NV == 1) val = accs[u];
+      else if (v == 0) val = f2_lo(acc0[u]);
+      else if (v == 1) val = f2_hi(acc0[u]);
+      else if (v == 2) val = NV == 3 ? accs[u] : f2_lo(acc1[u]);
+      else val = f2_hi(acc1[u]);
+      if (val < bd[u] || (val == bd[u] && j < bj[u])) { sd[u] = bd[u]; bd[u] = val; bj[u] = j; }
+      else sd[u] = fminf(sd[u], val);
+    }
+  }
+}
+
 // Distances of the chunk's points pt + 16u (u < NA) to all centres (two per FFMA2; direct
 // differences, dimensions ascending), running (best, index, runner-up) per point, merged over
 // the two centre lanes of the warp and written to the per-warp slots sb_*[warp][point].
@@ -211,32 +263,15 @@ __device__ __forceinline__ void dist_rows(const float* __restrict__ xs, int P, c
   for (int q = 0; q < NA; ++q) { bd[q] = FLT_MAX; sd[q] = FLT_MAX; bj[q] = 0x7fffffff; }
   const float* xq = xs + pt;
   for (int j0 = 0; j0 < k2; j0 += kLC) {
-    unsigned long long acc[2][NA] = {};
+    // centres ct + 16 v (v < nv) of the block hold real centres for this warp (its two ct are
+    // 2 warp and 2 warp + 1): the padding of the last block costs no arithmetic
+    const int rem = k2 - j0 - 2 * warp;
+    const int nv = rem <= 0 ? 0 : (rem >= 64 ? 4 : (rem + 15) >> 4);
     const unsigned long long* cq = reinterpret_cast<const unsigned long long*>(cs) + (size_t)(j0 >> 6) * d * 32 + ct;
-    for (int i = 0; i < d; ++i) {
-      const unsigned long long c0 = cq[i * 32], c1 = cq[i * 32 + 16];
-      float x[NA];
-#pragma unroll
-      for (int u = 0; u < NA; ++u) x[u] = xq[i * P + 16 * u];
-#pragma unroll
-      for (int u = 0; u < NA; ++u) {
-        const unsigned long long xx = f2_dup(x[u]);
-        const unsigned long long df0 = f2_sub(xx, c0), df1 = f2_sub(xx, c1);
-        acc[0][u] = f2_fma(df0, df0, acc[0][u]);
-        acc[1][u] = f2_fma(df1, df1, acc[1][u]);
-      }
-    }
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int j = j0 + ct + 16 * v;
-      if (j >= k2) continue;
-#pragma unroll
-      for (int u = 0; u < NA; ++u) {
-        const float val = (v & 1) ? f2_hi(acc[v >> 1][u]) : f2_lo(acc[v >> 1][u]);
-        if (val < bd[u] || (val == bd[u] && j < bj[u])) { sd[u] = bd[u]; bd[u] = val; bj[u] = j; }
-        else sd[u] = fminf(sd[u], val);
-      }
-    }
+    if (nv == 4) dist_block<NA, 4>(xq, P, cq, d, j0 + ct, k2, bd, sd, bj);
+    else if (nv == 3) dist_block<NA, 3>(xq, P, cq, d, j0 + ct, k2, bd, sd, bj);
+    else if (nv == 2) dist_block<NA, 2>(xq, P, cq, d, j0 + ct, k2, bd, sd, bj);
+    else if (nv == 1) dist_block<NA, 1>(xq, P, cq, d, j0 + ct, k2, bd, sd, bj);
   }
   // merge the two centre lanes of this warp (lanes l and l ^ 16 hold the same points)
 #pragma unroll
