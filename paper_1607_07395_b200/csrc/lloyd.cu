@@ -207,6 +207,7 @@ __device__ __forceinline__ void dist_block(const float* __restrict__ xq, int P, 
   float accs[NA];
 #pragma unroll
   for (int u = 0; u < NA; ++u) { acc0[u] = 0ull; acc1[u] = 0ull; accs[u] = 0.f; }
+#pragma unroll 2
   for (int i = 0; i < d; ++i) {
     const unsigned long long c0 = cq[i * 32];
     const unsigned long long c1 = NV >= 3 ? cq[i * 32 + 16] : 0ull;
