@@ -205,6 +205,13 @@ static int32_t embed_core(const cabs_plan& p, const Ws& L, int32_t k, const floa
     launch_svd(k, W, ldw, tol, ws, L, sigma, nullptr, nullptr, nullptr, st);
     CABS_LAUNCH_CHECK("svd");
   }
+  if (!multi(comm) && !getenv("CABS_EMBED_UNFUSED") &&
+      launch_embed_fused(m_loc, n_sl, k, C, ldc, R + p.col_begin, ldr, Y1, ld1, Y2, ld2, mode,
+                         static_cast<double>(p.m), static_cast<double>(p.n), static_cast<double>(k), kind, s, r, ws,
+                         L, st)) {
+    CABS_LAUNCH_CHECK("embed_fused");
+    return CABS_OK;
+  }
   if (m_loc > 0) CABS_CUDA_TRY(cudaMemsetAsync(Y1, 0, sizeof(float) * ld1 * m_loc, st));
   if (n_sl > 0) CABS_CUDA_TRY(cudaMemsetAsync(Y2, 0, sizeof(float) * ld2 * n_sl, st));
   launch_embed_products(m_loc, n_sl, k, C, ldc, R + p.col_begin, ldr, Y1, ld1, Y2, ld2, ws, L, st);

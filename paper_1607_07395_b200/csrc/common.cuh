@@ -103,7 +103,7 @@ inline T* wsp(void* ws, size_t off) {
 }
 
 // scalar slots inside ws.scal (ints)
-enum ScalSlot : int { SCAL_R_PILOT = 0, SCAL_R_TMP = 1, SCAL_NRANKS = 2, SCAL_EXHAUST = 3 };
+enum ScalSlot : int { SCAL_R_PILOT = 0, SCAL_R_TMP = 1, SCAL_NRANKS = 2, SCAL_EXHAUST = 3, SCAL_EBAR = 4 /* [2] */ };
 
 __device__ inline void set_status(void* ws, uint32_t bit) {
   atomicOr(reinterpret_cast<unsigned int*>(ws), bit);

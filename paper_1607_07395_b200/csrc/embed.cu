@@ -13,17 +13,19 @@ constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;
 // X[i*ldx + p] (TRANS: rows of R, i.e. R^T).  FP32 FFMA, ascending i.  Epilogue:
 // per-tile FP64 column sums of squares -> norm_part[tile, c] (fixed order).
 template <bool TRANS>
-__global__ void __launch_bounds__(256) embed_gemm_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int k,
-                                                         const float* __restrict__ B, int64_t ldb,
-                                                         float* __restrict__ Y, int64_t ldy,
-                                                         double* __restrict__ norm_part, int64_t ldn) {
+__device__ __forceinline__ void gemm_tile(const float* __restrict__ X, int64_t ldx, int64_t N, int k,
+                                          const float* __restrict__ B, int64_t ldb, int64_t bx, int by,
+                                          float (&acc)[4][4], double* __restrict__ norm_part, int64_t ldn) {
   __shared__ float Xs[kGemmBK][kGemmBM + 4];
   __shared__ float Bs[kGemmBK][kGemmBN + 4];
   __shared__ double red[16][kGemmBN];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t p0 = (int64_t)blockIdx.x * kGemmBM;
-  const int c0 = blockIdx.y * kGemmBN;
-  float acc[4][4] = {};
+  const int64_t p0 = bx * kGemmBM;
+  const int c0 = by * kGemmBN;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
   for (int i0 = 0; i0 < k; i0 += kGemmBK) {
     if (!TRANS) {
       const int pp = tid >> 2, ii = (tid & 3) * 4;
@@ -75,20 +77,37 @@ __global__ void __launch_bounds__(256) embed_gemm_kernel(const float* __restrict
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int c = c0 + tx * 4 + v;
-      if (c < k) {
-        Y[p * ldy + c] = acc[u][v];
-        ss[v] += static_cast<double>(acc[u][v]) * static_cast<double>(acc[u][v]);
-      }
+      if (c < k) ss[v] += static_cast<double>(acc[u][v]) * static_cast<double>(acc[u][v]);
     }
   }
 #pragma unroll
   for (int v = 0; v < 4; ++v) red[ty][tx * 4 + v] = ss[v];
   __syncthreads();
   if (tid < kGemmBN) {
-    double s = 0;
-    for (int t = 0; t < 16; ++t) s += red[t][tid];
+    double s2 = 0;
+    for (int t = 0; t < 16; ++t) s2 += red[t][tid];
     const int c = c0 + tid;
-    if (c < k) norm_part[(int64_t)blockIdx.x * ldn + c] = s;
+    if (c < k) norm_part[bx * ldn + c] = s2;
+  }
+}
+
+template <bool TRANS>
+__global__ void __launch_bounds__(256) embed_gemm_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int k,
+                                                         const float* __restrict__ B, int64_t ldb,
+                                                         float* __restrict__ Y, int64_t ldy,
+                                                         double* __restrict__ norm_part, int64_t ldn) {
+  float acc[4][4];
+  gemm_tile<TRANS>(X, ldx, N, k, B, ldb, blockIdx.x, blockIdx.y, acc, norm_part, ldn);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t p = (int64_t)blockIdx.x * kGemmBM + ty * 4 + u;
+    if (p >= N) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int c = blockIdx.y * kGemmBN + tx * 4 + v;
+      if (c < k) Y[p * ldy + c] = acc[u][v];
+    }
   }
 }
 
@@ -292,6 +311,185 @@ int launch_scale_compact(float* Y, int64_t ldy, int64_t N, int k, int which, voi
   note_launch();
   scale_compact_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(Y, ldy, N, k, sc + which * L.Kp, newpos, flags);
   return 0;
+}
+
+// ---------------------------------------------------------------- single-GPU fused S5
+// ONE cooperative launch for both products and the normalisation: GEMM tiles of Y_c = C V_w
+// and Y_r = R^T U_w (accumulators stay in registers) | grid barrier | column norms from the
+// tile partials (fixed order, as reduce_cols_kernel) | grid barrier | every CTA forms the
+// scales and the compaction map (as embed_finalize_kernel) and writes its tile of P, Q (or
+// U, V) scaled, compacted and zero-padded -- no memsets, no second pass over Y.
+struct EmbedFused {
+  const float* X[2];
+  int64_t ldx[2], N[2];
+  const float* B[2];
+  int64_t ldb;
+  float* Y[2];
+  int64_t ldy[2];
+  int k, gy;
+  int64_t tiles0;
+  double* part[2];
+  double* norms;
+  int64_t Kp;
+  const double* sig;
+  const int* r_in;
+  int mode, kind;
+  double m, n, ksamp;
+  double* alpha;
+  double* beta;
+  int* newpos;
+  float* s_out;
+  int* r_out;
+  int* r_out2;
+  int* flags;
+  unsigned* bar;
+};
+
+__global__ void __launch_bounds__(256) embed_fused_kernel(EmbedFused a) {
+  __shared__ double s_red[256];
+  __shared__ double s_scale[256];
+  __shared__ int s_pos[256];
+  __shared__ int warp_cnt[8];
+  __shared__ int s_total;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, tx = tid & 15, ty = tid >> 4;
+  const int k = a.k;
+  const int side = static_cast<int64_t>(blockIdx.x) < a.tiles0 ? 0 : 1;
+  const int64_t tl = side ? static_cast<int64_t>(blockIdx.x) - a.tiles0 : static_cast<int64_t>(blockIdx.x);
+  const int64_t bx = tl / a.gy;
+  const int by = static_cast<int>(tl - bx * a.gy);
+  const int r = *a.r_in;  // read before CTA 0 rewrites the slot (after the second barrier)
+  float acc[4][4];
+  if (side == 0) gemm_tile<false>(a.X[0], a.ldx[0], a.N[0], k, a.B[0], a.ldb, bx, by, acc, a.part[0], a.Kp);
+  else gemm_tile<true>(a.X[1], a.ldx[1], a.N[1], k, a.B[1], a.ldb, bx, by, acc, a.part[1], a.Kp);
+  unsigned gen = 0;
+  grid_barrier(a.bar, gen);
+  for (int cc = blockIdx.x; cc < 2 * k; cc += gridDim.x) {  // column norms, fixed order
+    const int sd = cc / k, c = cc - sd * k;
+    const int64_t ntiles = ceil_div(a.N[sd], kGemmBM);
+    double acc2 = 0;
+    for (int64_t t = tid; t < ntiles; t += blockDim.x) acc2 += __ldcg(a.part[sd] + t * a.Kp + c);
+    s_red[tid] = acc2;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (tid < w) s_red[tid] += s_red[tid + w];
+      __syncthreads();
+    }
+    if (tid == 0) a.norms[sd * a.Kp + c] = s_red[0];
+    __syncthreads();
+  }
+  grid_barrier(a.bar, gen);
+  // scales of the sketching routine (embed_finalize_kernel), component c = tid
+  bool keep = false;
+  double sv = 0, al = 0, be = 0;
+  if (tid < k) {
+    const double Nc = sqrt(__ldcg(a.norms + tid)), Nr = sqrt(__ldcg(a.norms + a.Kp + tid));
+    keep = tid < r && Nc > 0 && Nr > 0;
+    if (keep) {
+      const double sg = __ldcg(a.sig + tid);
+      sv = (a.mode == CABS_STABILIZED) ? sg * sqrt(a.m * a.n) / a.ksamp : Nc * Nr / sg;
+      if (a.kind == 0) {
+        const double rs = sqrt(sv);
+        al = rs / Nc;
+        be = rs / Nr;
+      } else {
+        al = 1.0 / Nc;
+        be = 1.0 / Nr;
+      }
+    }
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  if (lane == 0) warp_cnt[warp] = __popc(bal);
+  __syncthreads();
+  if (tid == 0) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) { const int x = warp_cnt[w]; warp_cnt[w] = t; t += x; }
+    s_total = t;
+  }
+  __syncthreads();
+  const int pos = warp_cnt[warp] + __popc(bal & ((1u << lane) - 1u));
+  s_scale[tid] = side ? be : al;
+  s_pos[tid] = keep ? pos : -1;
+  __syncthreads();
+  const int reff = s_total;
+  if (blockIdx.x == 0) {
+    if (tid < k) {
+      a.newpos[tid] = keep ? pos : -1;
+      a.alpha[tid] = al;
+      a.beta[tid] = be;
+      if (a.s_out) a.s_out[tid] = 0.f;
+    }
+    __syncthreads();
+    if (keep && a.s_out) a.s_out[pos] = static_cast<float>(sv);
+    if (tid == 0) {
+      if (a.r_out) *a.r_out = reff;
+      if (a.r_out2) *a.r_out2 = reff;
+      a.flags[0] = reff;
+      a.flags[1] = 1;
+    }
+  }
+  // this tile of the output: kept columns scaled into their compacted positions, zeros in
+  // [r_eff, ldy) (the last column tile covers the padding up to ldy)
+  float* Y = a.Y[side];
+  const int64_t ldy = a.ldy[side], N = a.N[side];
+  const int c0 = by * kGemmBN;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t p = bx * kGemmBM + ty * 4 + u;
+    if (p >= N) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int c = c0 + tx * 4 + v;
+      if (c < k && s_pos[c] >= 0) Y[p * ldy + s_pos[c]] = static_cast<float>(static_cast<double>(acc[u][v]) * s_scale[c]);
+    }
+  }
+  const int q0 = c0 > reff ? c0 : reff;
+  const int64_t q1 = by == a.gy - 1 ? ldy : c0 + kGemmBN;
+  for (int64_t q = q0 + tx; q < q1; q += 16)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t p = bx * kGemmBM + ty * 4 + u;
+      if (p < N) Y[p * ldy + q] = 0.f;
+    }
+}
+
+bool launch_embed_fused(int64_t m_loc, int64_t n_sl, int k, const float* C, int64_t ldc, const float* R_slice,
+                        int64_t ldr, float* Y1, int64_t ld1, float* Y2, int64_t ld2, int mode, double m, double n,
+                        double ksamp, int kind, float* s_out, int* r_user, void* ws, const Ws& L, cudaStream_t st) {
+  if (k > 256 || m_loc < 1 || n_sl < 1) return false;
+  const int gy = static_cast<int>(ceil_div(k, kGemmBN));
+  const int64_t tiles0 = ceil_div(m_loc, kGemmBM) * gy, tiles1 = ceil_div(n_sl, kGemmBM) * gy;
+  const int64_t G = tiles0 + tiles1;
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, embed_fused_kernel, 256, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (G > (int64_t)per * nsm || G > 0x7fffffff) return false;
+  EmbedFused a{};
+  a.X[0] = C; a.ldx[0] = ldc; a.N[0] = m_loc;
+  a.X[1] = R_slice; a.ldx[1] = ldr; a.N[1] = n_sl;
+  a.B[0] = wsp<float>(ws, L.vw32); a.B[1] = wsp<float>(ws, L.uw32); a.ldb = L.Kp;
+  a.Y[0] = Y1; a.ldy[0] = ld1; a.Y[1] = Y2; a.ldy[1] = ld2;
+  a.k = k; a.gy = gy; a.tiles0 = tiles0;
+  double* part = wsp<double>(ws, L.norm_part);
+  a.part[0] = part; a.part[1] = part + L.npt * L.Kp;
+  a.norms = wsp<double>(ws, L.norms); a.Kp = L.Kp;
+  double* sc = wsp<double>(ws, L.scales);
+  int* scal = wsp<int>(ws, L.scal);
+  a.sig = wsp<double>(ws, L.sig64); a.r_in = scal + SCAL_R_TMP;
+  a.mode = mode; a.kind = kind; a.m = m; a.n = n; a.ksamp = ksamp;
+  a.alpha = sc; a.beta = sc + L.Kp;
+  a.newpos = reinterpret_cast<int*>(sc + 2 * L.Kp);
+  a.flags = a.newpos + L.Kp;
+  a.s_out = s_out; a.r_out = scal + SCAL_R_TMP; a.r_out2 = r_user;
+  a.bar = reinterpret_cast<unsigned*>(scal + SCAL_EBAR);
+  if (cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st) != cudaSuccess) return false;
+  void* args[] = {&a};
+  note_launch();
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(embed_fused_kernel), dim3(static_cast<unsigned>(G)),
+                                     dim3(256), args, 0, st) == cudaSuccess;
 }
 
 }  // namespace cabsk

@@ -31,6 +31,9 @@ int launch_embed_products(int64_t m_loc, int64_t n_sl, int k, const float* C, in
 int launch_embed_finalize(int k, int mode, double m, double n, double ksamp, int kind, float* s_out, int* r_user,
                           void* ws, const Ws& L, cudaStream_t st);
 int launch_scale_compact(float* Y, int64_t ldy, int64_t N, int k, int which, void* ws, const Ws& L, cudaStream_t st);
+bool launch_embed_fused(int64_t m_loc, int64_t n_sl, int k, const float* C, int64_t ldc, const float* R_slice,
+                        int64_t ldr, float* Y1, int64_t ld1, float* Y2, int64_t ld2, int mode, double m, double n,
+                        double ksamp, int kind, float* s_out, int* r_user, void* ws, const Ws& L, cudaStream_t st);
 
 // kmeans.cu
 struct KmWeightJob {
