@@ -12,13 +12,32 @@ constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;
 // Y[p, c] = sum_i X(p, i) B[i, c];  X(p, i) = X[p*ldx + i] (row-major C) or
 // X[i*ldx + p] (TRANS: rows of R, i.e. R^T).  FP32 FFMA, ascending i.  Epilogue:
 // per-tile FP64 column sums of squares -> norm_part[tile, c] (fixed order).
+#ifdef CABS_PROFILE_EMBED
+__device__ long long g_emb_tl[2][8];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define ETL(i) do { if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) \
+                      g_emb_tl[blockIdx.x == 0 ? 0 : 1][i] = gtimer(); } while (0)
+#else
+#define ETL(i) do { } while (0)
+#endif
+struct __align__(16) GemmSmem {
+  float Xs[64][kGemmBM + 4];
+  float Bs[64][kGemmBN + 4];
+  double red[16][kGemmBN];
+};
+
 template <bool TRANS>
 __device__ __forceinline__ void gemm_tile(const float* __restrict__ X, int64_t ldx, int64_t N, int k,
                                           const float* __restrict__ B, int64_t ldb, int64_t bx, int by,
-                                          float (&acc)[4][4], double* __restrict__ norm_part, int64_t ldn) {
-  __shared__ float Xs[kGemmBK][kGemmBM + 4];
-  __shared__ float Bs[kGemmBK][kGemmBN + 4];
-  __shared__ double red[16][kGemmBN];
+                                          float (&acc)[4][4], double* __restrict__ norm_part, int64_t ldn,
+                                          GemmSmem& sm) {
+  auto& Xs = sm.Xs;
+  auto& Bs = sm.Bs;
+  auto& red = sm.red;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int64_t p0 = bx * kGemmBM;
   const int c0 = by * kGemmBN;
@@ -91,13 +110,118 @@ __device__ __forceinline__ void gemm_tile(const float* __restrict__ X, int64_t l
   }
 }
 
+// k <= 64: the whole X tile (64 points x k) and B (k x 64) staged at once (every load in
+// flight together, one barrier), then the same FP32 FFMA chain in ascending i.
+template <bool TRANS>
+__device__ __forceinline__ void gemm_tile_k64(const float* __restrict__ X, int64_t ldx, int64_t N, int k,
+                                              const float* __restrict__ B, int64_t ldb, int64_t bx, int by,
+                                              float (&acc)[4][4], double* __restrict__ norm_part, int64_t ldn,
+                                              GemmSmem& sm) {
+  auto& Xs = sm.Xs;
+  auto& Bs = sm.Bs;
+  auto& red = sm.red;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t p0 = bx * kGemmBM;
+  const int c0 = by * kGemmBN;
+  // float4 loads (ldx, ldb multiples of 4, 16-byte aligned bases: checked by the launcher)
+  if (!TRANS) {  // X row-major: row p, dims i4..i4+3
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;  // 64 rows x 16 quads
+      const int pp = e >> 4, i4 = (e & 15) * 4;
+      const int64_t p = p0 + pp;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p < N && i4 < k) v = __ldg(reinterpret_cast<const float4*>(X + p * ldx + i4));
+      Xs[i4][pp] = i4 < k ? v.x : 0.f;
+      Xs[i4 + 1][pp] = i4 + 1 < k ? v.y : 0.f;
+      Xs[i4 + 2][pp] = i4 + 2 < k ? v.z : 0.f;
+      Xs[i4 + 3][pp] = i4 + 3 < k ? v.w : 0.f;
+    }
+  } else {  // X = R^T: row i of R, points pp..pp+3
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;  // 64 dims x 16 quads of points
+      const int ii = e >> 4, pp = (e & 15) * 4;
+      const int64_t p = p0 + pp;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ii < k) {
+        if (p + 3 < N) {
+          v = __ldg(reinterpret_cast<const float4*>(X + (int64_t)ii * ldx + p));
+        } else {
+          if (p < N) v.x = __ldg(X + (int64_t)ii * ldx + p);
+          if (p + 1 < N) v.y = __ldg(X + (int64_t)ii * ldx + p + 1);
+          if (p + 2 < N) v.z = __ldg(X + (int64_t)ii * ldx + p + 2);
+        }
+      }
+      *reinterpret_cast<float4*>(&Xs[ii][pp]) = v;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = tid + 256 * q;
+    const int ii = e >> 4, cc = (e & 15) * 4;
+    const int c = c0 + cc;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ii < k) {
+      if (c + 3 < k) {
+        v = __ldg(reinterpret_cast<const float4*>(B + (int64_t)ii * ldb + c));
+      } else {
+        if (c < k) v.x = __ldg(B + (int64_t)ii * ldb + c);
+        if (c + 1 < k) v.y = __ldg(B + (int64_t)ii * ldb + c + 1);
+        if (c + 2 < k) v.z = __ldg(B + (int64_t)ii * ldb + c + 2);
+      }
+    }
+    *reinterpret_cast<float4*>(&Bs[ii][cc]) = v;
+  }
+  __syncthreads();
+  ETL(6);
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
+#pragma unroll 8
+  for (int ii = 0; ii < k; ++ii) {
+    float a[4], b[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      a[q] = Xs[ii][ty * 4 + q];
+      b[q] = Bs[ii][tx * 4 + q];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]);
+  }
+  double ss[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t p = p0 + ty * 4 + u;
+    if (p >= N) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int c = c0 + tx * 4 + v;
+      if (c < k) ss[v] += static_cast<double>(acc[u][v]) * static_cast<double>(acc[u][v]);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v) red[ty][tx * 4 + v] = ss[v];
+  __syncthreads();
+  if (tid < kGemmBN) {
+    double s2 = 0;
+    for (int t = 0; t < 16; ++t) s2 += red[t][tid];
+    const int c = c0 + tid;
+    if (c < k) norm_part[bx * ldn + c] = s2;
+  }
+}
+
 template <bool TRANS>
 __global__ void __launch_bounds__(256) embed_gemm_kernel(const float* __restrict__ X, int64_t ldx, int64_t N, int k,
                                                          const float* __restrict__ B, int64_t ldb,
                                                          float* __restrict__ Y, int64_t ldy,
                                                          double* __restrict__ norm_part, int64_t ldn) {
+  __shared__ GemmSmem sm;
   float acc[4][4];
-  gemm_tile<TRANS>(X, ldx, N, k, B, ldb, blockIdx.x, blockIdx.y, acc, norm_part, ldn);
+  gemm_tile<TRANS>(X, ldx, N, k, B, ldb, blockIdx.x, blockIdx.y, acc, norm_part, ldn, sm);
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -346,7 +470,6 @@ struct EmbedFused {
 };
 
 __global__ void __launch_bounds__(256) embed_fused_kernel(EmbedFused a) {
-  __shared__ double s_red[256];
   __shared__ double s_scale[256];
   __shared__ int s_pos[256];
   __shared__ int warp_cnt[8];
@@ -357,12 +480,22 @@ __global__ void __launch_bounds__(256) embed_fused_kernel(EmbedFused a) {
   const int64_t tl = side ? static_cast<int64_t>(blockIdx.x) - a.tiles0 : static_cast<int64_t>(blockIdx.x);
   const int64_t bx = tl / a.gy;
   const int by = static_cast<int>(tl - bx * a.gy);
+  ETL(0);
   const int r = *a.r_in;  // read before CTA 0 rewrites the slot (after the second barrier)
   float acc[4][4];
-  if (side == 0) gemm_tile<false>(a.X[0], a.ldx[0], a.N[0], k, a.B[0], a.ldb, bx, by, acc, a.part[0], a.Kp);
-  else gemm_tile<true>(a.X[1], a.ldx[1], a.N[1], k, a.B[1], a.ldb, bx, by, acc, a.part[1], a.Kp);
+  __shared__ GemmSmem sm;
+  if (k <= 64) {
+    if (side == 0) gemm_tile_k64<false>(a.X[0], a.ldx[0], a.N[0], k, a.B[0], a.ldb, bx, by, acc, a.part[0], a.Kp, sm);
+    else gemm_tile_k64<true>(a.X[1], a.ldx[1], a.N[1], k, a.B[1], a.ldb, bx, by, acc, a.part[1], a.Kp, sm);
+  } else {
+    if (side == 0) gemm_tile<false>(a.X[0], a.ldx[0], a.N[0], k, a.B[0], a.ldb, bx, by, acc, a.part[0], a.Kp, sm);
+    else gemm_tile<true>(a.X[1], a.ldx[1], a.N[1], k, a.B[1], a.ldb, bx, by, acc, a.part[1], a.Kp, sm);
+  }
   unsigned gen = 0;
+  ETL(1);
   grid_barrier(a.bar, gen);
+  ETL(2);
+  double* s_red = &sm.red[0][0];  // the tile is done with it
   for (int cc = blockIdx.x; cc < 2 * k; cc += gridDim.x) {  // column norms, fixed order
     const int sd = cc / k, c = cc - sd * k;
     const int64_t ntiles = ceil_div(a.N[sd], kGemmBM);
@@ -377,7 +510,9 @@ __global__ void __launch_bounds__(256) embed_fused_kernel(EmbedFused a) {
     if (tid == 0) a.norms[sd * a.Kp + c] = s_red[0];
     __syncthreads();
   }
+  ETL(3);
   grid_barrier(a.bar, gen);
+  ETL(4);
   // scales of the sketching routine (embed_finalize_kernel), component c = tid
   bool keep = false;
   double sv = 0, al = 0, be = 0;
@@ -432,30 +567,66 @@ __global__ void __launch_bounds__(256) embed_fused_kernel(EmbedFused a) {
   float* Y = a.Y[side];
   const int64_t ldy = a.ldy[side], N = a.N[side];
   const int c0 = by * kGemmBN;
+  if (a.gy == 1 && ldy <= kGemmBN + 4 && (ldy & 3) == 0) {
+    // whole rows in this tile: stage the compacted, scaled rows in shared memory, then write
+    // each row [0, ldy) with coalesced 16-byte stores
+    __syncthreads();
+    float (*T)[kGemmBM + 4] = sm.Xs;  // [row][col]
+    for (int e = tid; e < kGemmBM * (kGemmBN + 4); e += blockDim.x) (&T[0][0])[e] = 0.f;
+    __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int64_t p = bx * kGemmBM + ty * 4 + u;
-    if (p >= N) continue;
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int c = c0 + tx * 4 + v;
-      if (c < k && s_pos[c] >= 0) Y[p * ldy + s_pos[c]] = static_cast<float>(static_cast<double>(acc[u][v]) * s_scale[c]);
+      for (int v = 0; v < 4; ++v) {
+        const int c = tx * 4 + v;
+        if (c < k && s_pos[c] >= 0) T[ty * 4 + u][s_pos[c]] = static_cast<float>(static_cast<double>(acc[u][v]) * s_scale[c]);
+      }
+    __syncthreads();
+    const int q4 = static_cast<int>(ldy >> 2);
+    for (int e = tid; e < kGemmBM * q4; e += blockDim.x) {
+      const int row = e / q4, c4 = (e - row * q4) * 4;
+      const int64_t p = bx * kGemmBM + row;
+      if (p < N) *reinterpret_cast<float4*>(Y + p * ldy + c4) = *reinterpret_cast<const float4*>(&T[row][c4]);
     }
-  }
-  const int q0 = c0 > reff ? c0 : reff;
-  const int64_t q1 = by == a.gy - 1 ? ldy : c0 + kGemmBN;
-  for (int64_t q = q0 + tx; q < q1; q += 16)
+  } else {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t p = bx * kGemmBM + ty * 4 + u;
-      if (p < N) Y[p * ldy + q] = 0.f;
+      if (p >= N) continue;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int c = c0 + tx * 4 + v;
+        if (c < k && s_pos[c] >= 0)
+          Y[p * ldy + s_pos[c]] = static_cast<float>(static_cast<double>(acc[u][v]) * s_scale[c]);
+      }
     }
+    const int q0 = c0 > reff ? c0 : reff;
+    const int64_t q1 = by == a.gy - 1 ? ldy : c0 + kGemmBN;
+    for (int64_t q = q0 + tx; q < q1; q += 16)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t p = bx * kGemmBM + ty * 4 + u;
+        if (p < N) Y[p * ldy + q] = 0.f;
+      }
+  }
+  ETL(5);
+}
+void embed_debug_timeline(long long* out) {
+#ifdef CABS_PROFILE_EMBED
+  cudaMemcpyFromSymbol(out, g_emb_tl, sizeof(long long) * 16);
+#else
+  for (int i = 0; i < 16; ++i) out[i] = 0;
+#endif
 }
 
 bool launch_embed_fused(int64_t m_loc, int64_t n_sl, int k, const float* C, int64_t ldc, const float* R_slice,
                         int64_t ldr, float* Y1, int64_t ld1, float* Y2, int64_t ld2, int mode, double m, double n,
                         double ksamp, int kind, float* s_out, int* r_user, void* ws, const Ws& L, cudaStream_t st) {
   if (k > 256 || m_loc < 1 || n_sl < 1) return false;
+  if ((ldc & 3) || (ldr & 3) || (L.Kp & 3) || (reinterpret_cast<uintptr_t>(C) & 15) ||
+      (reinterpret_cast<uintptr_t>(R_slice) & 15) || (reinterpret_cast<uintptr_t>(Y1) & 15) ||
+      (reinterpret_cast<uintptr_t>(Y2) & 15))
+    return false;
   const int gy = static_cast<int>(ceil_div(k, kGemmBN));
   const int64_t tiles0 = ceil_div(m_loc, kGemmBM) * gy, tiles1 = ceil_div(n_sl, kGemmBM) * gy;
   const int64_t G = tiles0 + tiles1;
