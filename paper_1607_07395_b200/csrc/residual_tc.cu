@@ -13,10 +13,12 @@
 //            so every MMA reads only its 128 x 8 G slice from shared memory (an SS MMA
 //            would re-read 4 KB of F per instruction and saturate shared memory).
 //            Per 8-wide k step: D += Fh Gh^T + Fh Gl^T + Fl Gh^T (TMEM, 2 stages).
-//   warps 2-5 epilogue: split F diag(s) rows into TF32 hi/lo and write them into TMEM
-//            one band ahead; per tile, tcgen05.ld the accumulator row (lane = row),
-//            read the A row from the 128B-swizzled smem box, accumulate (a - a~)^2
-//            and a^2 in FP32 per tile, FP64 across tiles.
+//   warps 2-5 epilogue (group 0): split F diag(s) rows into TF32 hi/lo and write them into
+//            TMEM one band ahead; per tile, tcgen05.ld the accumulator row (lane = row) for
+//            columns [0, 64), read the A row from the 128B-swizzled smem boxes, accumulate
+//            (a - a~)^2 and a^2 in FP32 per tile, FP64 across tiles.
+//   warps 7-10 epilogue (group 1): the same for columns [64, 128) (two warps per TMEM lane
+//            quarter: the epilogue, which bounds the kernel otherwise, runs at twice the rate).
 // Tile order is row-band major over a static contiguous tile range per CTA; fixed-order
 // block and grid reductions: bit-reproducible.  Requires ncomp <= 64.
 #include "common.cuh"
@@ -29,7 +31,11 @@ constexpr int kTcBM = 128, kTcBN = 128;            // N = 128: a full-rate tcgen
                                                     // bound by a ~47-cycle per-instruction floor)
 constexpr int kAS = 6, kGS = 2, kCS = 2;            // A quarter-tile / G tile / TMEM accumulator stages
 constexpr int kAQ = kTcBN / 32;                     // A boxes (128 x 32) per tile
-constexpr int kTcThreads = 224;                     // 0 TMA (A), 1 MMA, 2-5 epilogue, 6 TMA (G)
+constexpr int kHalfAQ = kAQ / 2;                    // boxes per epilogue group and tile
+constexpr int kTcThreads = 352;                     // 0 TMA (A), 1 MMA, 2-5 + 7-10 epilogue, 6 TMA (G)
+constexpr int kEpiWarps = 8;
+constexpr int kAR = kAS / 2;                       // A ring slots per epilogue group (its own ring: a
+                                                    // group never waits on a slot phase of the other)
 constexpr int kKp = 64;                             // K padded (two 32-float swizzle atoms)
 constexpr uint32_t kGAtomBytes = kTcBN * 128;      // 16 KB
 constexpr uint32_t kABoxBytes = kTcBM * 128;       // 16 KB: 128 rows x 32 floats = a quarter A tile
@@ -46,7 +52,7 @@ struct TcSmem {
   uint64_t a_full[kAS], a_empty[kAS];
   uint64_t acc_full[kCS], acc_empty[kCS];
   uint32_t tmem_base;
-  double red[2][4];
+  double red[2][kEpiWarps];
 };
 
 #ifdef CABS_PROFILE_RES
@@ -148,7 +154,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     for (int b = 0; b < 2; ++b) { tc::mbar_init(&S.f_ready[b], 4); tc::mbar_init(&S.f_free[b], 1); }
     for (int s = 0; s < kGS; ++s) { tc::mbar_init(&S.g_full[s], 1); tc::mbar_init(&S.g_empty[s], 1); }
     for (int s = 0; s < kAS; ++s) { tc::mbar_init(&S.a_full[s], 1); tc::mbar_init(&S.a_empty[s], 4); }
-    for (int s = 0; s < kCS; ++s) { tc::mbar_init(&S.acc_full[s], 1); tc::mbar_init(&S.acc_empty[s], 4); }
+    for (int s = 0; s < kCS; ++s) { tc::mbar_init(&S.acc_full[s], 1); tc::mbar_init(&S.acc_empty[s], kEpiWarps); }
     tc::mbar_fence_init();
   }
   if (warp == 1) tc::tmem_alloc(&S.tmem_base, kTmemCols);
@@ -168,9 +174,11 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         const int64_t rb = t / ntc, cb = t % ntc;
         // A (the HBM stream the kernel is bound by): kAQ boxes of 128 x 32 per tile
         for (int h = 0; h < kAQ; ++h) {
-          const int64_t ia = kAQ * i + h;
-          const int sa = static_cast<int>(ia % kAS);
-          if (ia >= kAS) RES_WAIT(1, tc::mbar_wait(&S.a_empty[sa], ring_parity(ia - kAS, kAS)));
+          // box h of the tile goes to the ring of the epilogue group reading it (columns
+          // [0, 64) group 0, [64, 128) group 1); li = its index within that ring's sequence
+          const int64_t li = kHalfAQ * i + (h % kHalfAQ);
+          const int sa = (h / kHalfAQ) * kAR + static_cast<int>(li % kAR);
+          if (li >= kAR) RES_WAIT(1, tc::mbar_wait(&S.a_empty[sa], ring_parity(li - kAR, kAR)));
           tc::mbar_expect_tx(&S.a_full[sa], kABoxBytes);
           tc::tma_load_2d(S.a[sa], &tmA, static_cast<int>(cb * kTcBN + 32 * h), static_cast<int>(rb * kTcBM),
                           &S.a_full[sa]);
@@ -235,17 +243,22 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2-5)
+    // ------------------------------------------------------------ epilogue (warps 2-5, 7-10)
     const int q = warp & 3;           // TMEM lane quarter this warp may access
+    const int eg = warp >= 7 ? 1 : 0; // column half of the tile (A boxes 2 eg, 2 eg + 1)
+    constexpr int kHalf = kAQ / 2;
+    {
     const int row = q * 32 + lane;    // row within the 128-row tile
-    // F of the first two bands, then one band ahead of the MMA
-    load_f_band(fa, m, rb0, q, lane, tmem, 0, &S.f_ready[0]);
-    if (nbands > 1) load_f_band(fa, m, rb0 + 1, q, lane, tmem, 1, &S.f_ready[1]);
+    // F of the first two bands, then one band ahead of the MMA (group 0 only)
+    if (eg == 0) {
+      load_f_band(fa, m, rb0, q, lane, tmem, 0, &S.f_ready[0]);
+      if (nbands > 1) load_f_band(fa, m, rb0 + 1, q, lane, tmem, 1, &S.f_ready[1]);
+    }
     double r2 = 0.0, a2 = 0.0;
     int64_t prev_rb = rb0;
     for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
       const int64_t rb = t / ntc;
-      if (rb != prev_rb) {  // entering band j = rb - rb0: stage band j + 1 into the buffer band j - 1 used
+      if (rb != prev_rb && eg == 0) {  // entering band j = rb - rb0: stage band j + 1 into the buffer band j - 1 used
         prev_rb = rb;
         const int64_t j = rb - rb0;
         if (j + 1 < nbands) {
@@ -261,12 +274,13 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(sc * kTcBN);
       float tr0 = 0.f, ta0 = 0.f, tr1 = 0.f, ta1 = 0.f;
 #pragma unroll
-      for (int h = 0; h < kAQ; ++h) {
+      for (int hh = 0; hh < kHalf; ++hh) {
+        const int h = kHalf * eg + hh;
         // A row from a 128B-swizzled box (16-byte chunk c of row r is at chunk c ^ (r & 7));
-        // the box slot is released as soon as its values are in registers
-        const int64_t ia = kAQ * i + h;
-        const int sa = static_cast<int>(ia % kAS);
-        RES_WAIT(10, tc::mbar_wait(&S.a_full[sa], ring_parity(ia, kAS)));
+        // the box slot (in this group's ring) is released as soon as its values are in registers
+        const int64_t li = kHalfAQ * i + hh;
+        const int sa = eg * kAR + static_cast<int>(li % kAR);
+        RES_WAIT(10, tc::mbar_wait(&S.a_full[sa], ring_parity(li, kAR)));
         float av[32];
         const uint8_t* arow = S.a[sa] + row * 128;
 #pragma unroll
@@ -278,7 +292,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         if (lane == 0) tc::mbar_arrive(&S.a_empty[sa]);
         float v[32];
         tc::tmem_ld32(tbase + 32 * h, v);
-        if (h == kAQ - 1) {
+        if (hh == kHalf - 1) {
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);
@@ -298,8 +312,9 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     r2 = warp_sum_d(r2);
     a2 = warp_sum_d(a2);
     if (lane == 0) {
-      S.red[0][q] = r2;
-      S.red[1][q] = a2;
+      S.red[0][q + 4 * eg] = r2;
+      S.red[1][q + 4 * eg] = a2;
+    }
     }
   }
 #ifdef CABS_PROFILE_RES
@@ -316,8 +331,13 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     tc::tmem_dealloc(tmem, kTmemCols);
   }
   if (threadIdx.x == 0) {
-    part[2 * blockIdx.x] = ((S.red[0][0] + S.red[0][1]) + S.red[0][2]) + S.red[0][3];
-    part[2 * blockIdx.x + 1] = ((S.red[1][0] + S.red[1][1]) + S.red[1][2]) + S.red[1][3];
+    double r2 = 0.0, a2 = 0.0;
+    for (int e = 0; e < kEpiWarps; ++e) {  // fixed order
+      r2 += S.red[0][e];
+      a2 += S.red[1][e];
+    }
+    part[2 * blockIdx.x] = r2;
+    part[2 * blockIdx.x + 1] = a2;
   }
 }
 
