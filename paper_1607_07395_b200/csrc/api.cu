@@ -91,6 +91,9 @@ int32_t cabs_debug_counters(int64_t* out, int32_t n) {
 #ifdef CABS_PROFILE_EMBED
   if (n >= 16) embed_debug_timeline(reinterpret_cast<long long*>(out));
 #endif
+#ifdef CABS_PROFILE_SNAP
+  if (n >= 4) snap_debug_counters(reinterpret_cast<long long*>(out));
+#endif
   if (n > 16) lloyd_debug_timeline(reinterpret_cast<long long*>(out) + 16, n - 16);
   return CABS_OK;
 }

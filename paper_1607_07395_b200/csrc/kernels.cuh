@@ -91,6 +91,7 @@ struct LloydJob {
 bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long long* prof, cudaStream_t st);
 void lloyd_debug_timeline(long long* out, int n);
 void embed_debug_timeline(long long* out);
+void snap_debug_counters(long long* out);
 
 // select.cu
 void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t row_off, int T, int nseg, int slot0,

@@ -172,6 +172,9 @@ __device__ __forceinline__ void taken_put(int64_t* tab, int64_t x) {
   tab[h] = x;
 }
 
+#ifdef CABS_PROFILE_SNAP
+__device__ unsigned long long g_snap_prof[4];  // rescans, greedy-pass cycles, rescan cycles, total cycles
+#endif
 __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, const int64_t* cand_i, int k2, int T,
                                                           const double* __restrict__ cluster_w,
                                                           const float* __restrict__ D, int64_t ldd, int64_t N,
@@ -217,33 +220,48 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
   }
   if (tid == 0) s_next = 0;
   __syncthreads();
+#ifdef CABS_PROFILE_SNAP
+  long long tp0 = clock64();
+#endif
   for (;;) {
-    if (tid == 0) {
-      s_rescan = -1;
+    if (tid < 32) {  // warp 0: the greedy pass, lane t checks candidate t of the current centre
+      const int lane = tid;
+      if (lane == 0) s_rescan = -1;
       int o = s_next;
       for (; o < k2; ++o) {
         const int j = order[o];
-        float d1 = FLT_MAX, d2 = FLT_MAX;
-        int64_t i1 = -1, i2 = -1;
-        for (int t = 0; t < T; ++t) {
-          const int64_t ci = cand_i[(int64_t)j * T + t];
-          if (ci < 0 || taken_has(tab, ci)) continue;
-          if (i1 < 0) { i1 = ci; d1 = cand_d[(int64_t)j * T + t]; }
-          else { i2 = ci; d2 = cand_d[(int64_t)j * T + t]; break; }
+        const int64_t ci = lane < T ? cand_i[(int64_t)j * T + lane] : -1;
+        const bool ok = ci >= 0 && !taken_has(tab, ci);
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        const int t1 = m ? __ffs(m) - 1 : -1;
+        const unsigned m2 = m & (m - 1);
+        const int t2 = m2 ? __ffs(m2) - 1 : -1;
+        int64_t i1 = __shfl_sync(0xffffffffu, ci, t1 < 0 ? 0 : t1);
+        int64_t i2 = __shfl_sync(0xffffffffu, ci, t2 < 0 ? 0 : t2);
+        if (t1 < 0) i1 = -1;
+        if (t2 < 0) i2 = -1;
+        if (i2 < 0 && can_rescan) {  // best or runner-up not resolved from the list
+          if (lane == 0) s_rescan = j;
+          break;
         }
-        if (i2 < 0) {  // best or runner-up not resolved from the list
-          if (can_rescan) { s_rescan = j; break; }
+        if (lane == 0) {
+          float d1 = i1 >= 0 ? cand_d[(int64_t)j * T + t1] : FLT_MAX;
+          const float d2 = i2 >= 0 ? cand_d[(int64_t)j * T + t2] : FLT_MAX;
           if (i1 < 0) { set_status(ws, CABS_DEV_SNAP_EXHAUSTED); i1 = 0; d1 = 0.f; }
+          taken_put(tab, i1);
+          reps[j] = i1;
+          if (rep_of_centre) rep_of_centre[j] = i1;
+          if (gap) gap[j] = (i2 < 0) ? FLT_MAX : (d2 > 0.f ? (d2 - d1) / d2 : 0.f);
         }
-        taken_put(tab, i1);
-        reps[j] = i1;
-        rep_of_centre ? (void)(rep_of_centre[j] = i1) : (void)0;
-        if (gap) gap[j] = (i2 < 0) ? FLT_MAX : (d2 > 0.f ? (d2 - d1) / d2 : 0.f);
+        __syncwarp();  // the new entry of the taken set is visible to the next centre's probes
       }
-      s_next = o;
+      if (lane == 0) s_next = o;
     }
     __syncthreads();
     const int j = s_rescan;
+#ifdef CABS_PROFILE_SNAP
+    if (tid == 0) { atomicAdd(&g_snap_prof[1], static_cast<unsigned long long>(clock64() - tp0)); tp0 = clock64(); if (j >= 0) atomicAdd(&g_snap_prof[0], 1ull); }
+#endif
     if (j < 0) break;
     // block-wide rescan of D[j, :] for the best and runner-up untaken points
     float b1 = FLT_MAX, b2 = FLT_MAX;
@@ -256,15 +274,30 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
       if (lex_less(v, gi, b1, i1)) { b2 = b1; i2 = i1; b1 = v; i1 = gi; }
       else if (lex_less(v, gi, b2, i2)) { b2 = v; i2 = gi; }
     }
-    // reduce (best, runner-up) pairs: serial merge by thread 0 in fixed order
-    rd[tid] = b1; ri[tid] = i1; rs[tid] = b2;
+    // reduce the (best, runner-up) pairs: warp butterflies, then the 8 warp results; the
+    // lexicographic (distance, index) order is total, so the top two are unique and the
+    // merge order does not matter
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob1 = __shfl_xor_sync(0xffffffffu, b1, o), ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
+      const int64_t oi1 = __shfl_xor_sync(0xffffffffu, i1, o), oi2 = __shfl_xor_sync(0xffffffffu, i2, o);
+      if (lex_less(ob1, oi1, b1, i1)) {  // other best wins: runner-up = min(own best, other runner-up)
+        if (lex_less(b1, i1, ob2, oi2)) { b2 = b1; i2 = i1; }
+        else { b2 = ob2; i2 = oi2; }
+        b1 = ob1; i1 = oi1;
+      } else if (lex_less(ob1, oi1, b2, i2)) {
+        b2 = ob1; i2 = oi1;
+      }
+    }
+    const int wid = tid >> 5;
+    if ((tid & 31) == 0) { rd[wid] = b1; ri[wid] = i1; rs[wid] = b2; }
     __shared__ int64_t ri2[256];
-    ri2[tid] = i2;
+    if ((tid & 31) == 0) ri2[wid] = i2;
     __syncthreads();
     if (tid == 0) {
       float B1 = FLT_MAX, B2 = FLT_MAX;
       int64_t I1 = INT64_MAX, I2 = INT64_MAX;
-      for (int t = 0; t < 256; ++t) {
+      for (int t = 0; t < static_cast<int>(blockDim.x >> 5); ++t) {
         const float cands_d[2] = {rd[t], rs[t]};
         const int64_t cands_i[2] = {ri[t], ri2[t]};
         for (int q = 0; q < 2; ++q) {
@@ -292,6 +325,14 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
     for (int q = 0; q < k2; ++q) rk += reps[q] < v;
     reps_sorted[rk] = v;
   }
+}
+
+void snap_debug_counters(long long* out) {
+#ifdef CABS_PROFILE_SNAP
+  cudaMemcpyFromSymbol(out, g_snap_prof, sizeof(long long) * 4);
+#else
+  for (int i = 0; i < 4; ++i) out[i] = 0;
+#endif
 }
 
 void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int T, const double* cluster_w,
