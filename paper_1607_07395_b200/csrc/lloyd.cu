@@ -77,7 +77,7 @@ struct LloydArgs {
   LloydProb pr[kMaxProb];
   int nprob, iters, resident;
   int g0;           // CTAs of problem 0 (the rest, gridDim.x - g0, run problem 1)
-  unsigned* gbar;   // grid barrier: monotonic arrival counter (zeroed at launch)
+  unsigned* gbar[kMaxProb];  // per-problem grid barriers: monotonic arrival counters (zeroed at launch)
   long long* prof;  // diagnostics (CABS_PROFILE_LLOYD builds): per-phase cycles of the last CTA
 };
 
@@ -550,9 +550,12 @@ __global__ void __launch_bounds__(kLT, 2) lloyd_persistent_kernel(LloydArgs a) {
     LPROF(7);
     if (tid == 0) {
       __threadfence();
-      atomicAdd(a.gbar, 1u);
-      const unsigned target = static_cast<unsigned>(G) * static_cast<unsigned>(it + 1);
-      while (ld_acquire_gpu(a.gbar) < target) __nanosleep(20);
+      // one counter per problem: the two problems never wait for each other, so the two CTAs
+      // of an SM drift out of phase and overlap their latency-bound phases
+      unsigned* bar = a.gbar[myq];
+      atomicAdd(bar, 1u);
+      const unsigned target = static_cast<unsigned>(Gb) * static_cast<unsigned>(it + 1);
+      while (ld_acquire_gpu(bar) < target) __nanosleep(20);
     }
     __syncthreads();
     LPROF(3);
@@ -701,7 +704,7 @@ bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long lo
     p.pitch = cap[q] + 1;
     p.fsum = reinterpret_cast<long long*>(base);
     unsigned* gb = reinterpret_cast<unsigned*>(p.fsum + 3 * E);
-    if (q == 0) a.gbar = gb;
+    a.gbar[q] = gb;
     p.pobj = reinterpret_cast<double*>(gb + 4);
     p.ptie = reinterpret_cast<int*>(p.pobj + (size_t)iters * G);
     if (cudaMemsetAsync(base, 0, sizeof(long long) * 3 * E + 16, st) != cudaSuccess) return false;

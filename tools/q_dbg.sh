@@ -1,4 +1,3 @@
-python -c "from paper_1607_07395_b200 import build; build.build(force=True, extra=['-DRES_G1_OFF'])" > gpurun_out/b.log 2>&1
-timeout 100 python tools/probe.py resprof > gpurun_out/res_g1off.log 2>&1
-python paper_1607_07395_b200/build.py --force > gpurun_out/b.log 2>&1
-timeout 100 python tools/probe.py resprof > gpurun_out/res_g1on.log 2>&1
+python paper_1607_07395_b200/build.py --force > gpurun_out/b.log 2>&1 || exit 1
+timeout 60 python tools/probe.py lloydpair > gpurun_out/dbg_prop.log 2>&1
+CABS_LLOYD_EVEN_SPLIT=1 timeout 60 python tools/probe.py lloydpair > gpurun_out/dbg_even.log 2>&1
