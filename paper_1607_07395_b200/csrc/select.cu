@@ -173,40 +173,70 @@ __device__ __forceinline__ void taken_put(int64_t* tab, int64_t x) {
 }
 
 #ifdef CABS_PROFILE_SNAP
-__device__ unsigned long long g_snap_prof[4];  // rescans, greedy-pass cycles, rescan cycles, total cycles
+__device__ unsigned long long g_snap_prof[4];  // rescans, greedy-pass cycles
 #endif
+// The taken set of the greedy pass: a bitmap over the local point indices when the rank owns
+// all points (single GPU, N <= kBitmapMax: one shared-memory word test per candidate), else
+// the open-addressing hash table of global indices.
+constexpr int64_t kBitmapMax = 1 << 18;
+struct TakenSet {
+  unsigned* bits;  // null: hash table
+  int64_t* tab;
+  int64_t off;
+  __device__ __forceinline__ bool has(int64_t x) const {
+    if (bits) {
+      const int64_t p = x - off;
+      return (bits[p >> 5] >> (p & 31)) & 1u;
+    }
+    return taken_has(tab, x);
+  }
+  __device__ __forceinline__ void put(int64_t x) {
+    if (bits) {
+      const int64_t p = x - off;
+      bits[p >> 5] |= 1u << (p & 31);
+    } else {
+      taken_put(tab, x);
+    }
+  }
+};
+
 __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, const int64_t* cand_i, int k2, int T,
                                                           const double* __restrict__ cluster_w,
                                                           const float* __restrict__ D, int64_t ldd, int64_t N,
                                                           int64_t row_off, bool can_rescan,
                                                           int64_t* __restrict__ rep_of_centre, float* __restrict__ gap,
                                                           int64_t* __restrict__ reps_sorted, void* ws,
-                                                          bool stage_cands) {
+                                                          bool staged, bool use_bitmap) {
   __shared__ int64_t tab[kTakenCap];
   __shared__ int order[CABS_KMAX];
   __shared__ int64_t reps[CABS_KMAX];
+  __shared__ float r_d1[CABS_KMAX], r_d2[CABS_KMAX];  // per centre: its distance, the runner-up's
+  __shared__ double s_w[CABS_KMAX];
   __shared__ int s_next;      // next position in `order` to process
   __shared__ int s_rescan;    // centre needing a rescan, or -1
-  __shared__ float rd[256], rs[256];
-  __shared__ int64_t ri[256];
+  __shared__ float rd[8], rs[8];
+  __shared__ int64_t ri[8], ri2[8];
+  // dynamic: candidates in visiting order [k2][T] (int64 | float), then the bitmap
   extern __shared__ __align__(16) unsigned char cand_smem[];
   const int tid = threadIdx.x;
-  for (int e = tid; e < kTakenCap; e += blockDim.x) tab[e] = -1;
-  // the sequential greedy pass reads candidates from shared memory when they fit
-  const bool staged = stage_cands;
-  if (staged) {
-    int64_t* si = reinterpret_cast<int64_t*>(cand_smem);
-    float* sd = reinterpret_cast<float*>(si + (size_t)k2 * T);
-    for (int e = tid; e < k2 * T; e += blockDim.x) {
-      si[e] = cand_i[e];
-      sd[e] = cand_d[e];
-    }
-    cand_i = si;
-    cand_d = sd;
+  // candidates by visiting position: staged in shared memory in that order, or (too large)
+  // read from global memory through order[]
+  int64_t* csi = reinterpret_cast<int64_t*>(cand_smem);
+  float* csd = reinterpret_cast<float*>(csi + (size_t)(staged ? k2 * T : 0));
+  auto cand_at = [&](int o, int t) -> int64_t { return staged ? csi[(int64_t)o * T + t] : cand_i[(int64_t)order[o] * T + t]; };
+  auto dist_at = [&](int o, int t) -> float { return staged ? csd[(int64_t)o * T + t] : cand_d[(int64_t)order[o] * T + t]; };
+  TakenSet taken;
+  taken.tab = tab;
+  taken.off = row_off;
+  taken.bits = nullptr;
+  if (use_bitmap) {
+    taken.bits = reinterpret_cast<unsigned*>(
+        cand_smem + (staged ? (((size_t)k2 * T * (sizeof(int64_t) + sizeof(float)) + 15) & ~size_t(15)) : 0));
+    for (int64_t e = tid; e < (N + 31) / 32; e += blockDim.x) taken.bits[e] = 0u;
+  } else {
+    for (int e = tid; e < kTakenCap; e += blockDim.x) tab[e] = -1;
   }
-  // visiting order (-omega_j, j): the weights staged in shared memory first (one global
-  // load per thread instead of a dependent L2 round trip per comparison)
-  __shared__ double s_w[CABS_KMAX];
+  // visiting order (-omega_j, j)
   for (int j = tid; j < k2; j += blockDim.x) s_w[j] = cluster_w[j];
   __syncthreads();
   for (int j = tid; j < k2; j += blockDim.x) {
@@ -218,6 +248,17 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
     }
     order[rk] = j;
   }
+  __syncthreads();
+  // candidates staged in visiting order: the greedy pass reads position o without first
+  // looking up order[o]
+  if (staged) {
+    for (int e = tid; e < k2 * T; e += blockDim.x) {
+      const int o = e / T, t = e - o * T;
+      const int j = order[o];
+      csi[e] = cand_i[(int64_t)j * T + t];
+      csd[e] = cand_d[(int64_t)j * T + t];
+    }
+  }
   if (tid == 0) s_next = 0;
   __syncthreads();
 #ifdef CABS_PROFILE_SNAP
@@ -228,32 +269,32 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
       const int lane = tid;
       if (lane == 0) s_rescan = -1;
       int o = s_next;
+      int64_t ci = (o < k2 && lane < T) ? cand_at(o, lane) : -1;
       for (; o < k2; ++o) {
-        const int j = order[o];
-        const int64_t ci = lane < T ? cand_i[(int64_t)j * T + lane] : -1;
-        const bool ok = ci >= 0 && !taken_has(tab, ci);
+        const bool ok = ci >= 0 && !taken.has(ci);
+        // prefetch the next centre's candidates (independent of the taken set)
+        const int64_t cn = (o + 1 < k2 && lane < T) ? cand_at(o + 1, lane) : -1;
         const unsigned m = __ballot_sync(0xffffffffu, ok);
         const int t1 = m ? __ffs(m) - 1 : -1;
         const unsigned m2 = m & (m - 1);
         const int t2 = m2 ? __ffs(m2) - 1 : -1;
         int64_t i1 = __shfl_sync(0xffffffffu, ci, t1 < 0 ? 0 : t1);
-        int64_t i2 = __shfl_sync(0xffffffffu, ci, t2 < 0 ? 0 : t2);
         if (t1 < 0) i1 = -1;
-        if (t2 < 0) i2 = -1;
-        if (i2 < 0 && can_rescan) {  // best or runner-up not resolved from the list
-          if (lane == 0) s_rescan = j;
+        if (t2 < 0 && can_rescan) {  // best or runner-up not resolved from the list
+          if (lane == 0) s_rescan = order[o];
           break;
         }
         if (lane == 0) {
-          float d1 = i1 >= 0 ? cand_d[(int64_t)j * T + t1] : FLT_MAX;
-          const float d2 = i2 >= 0 ? cand_d[(int64_t)j * T + t2] : FLT_MAX;
+          const int j = order[o];
+          float d1 = t1 >= 0 ? dist_at(o, t1) : FLT_MAX;
           if (i1 < 0) { set_status(ws, CABS_DEV_SNAP_EXHAUSTED); i1 = 0; d1 = 0.f; }
-          taken_put(tab, i1);
+          taken.put(i1);
           reps[j] = i1;
-          if (rep_of_centre) rep_of_centre[j] = i1;
-          if (gap) gap[j] = (i2 < 0) ? FLT_MAX : (d2 > 0.f ? (d2 - d1) / d2 : 0.f);
+          r_d1[j] = d1;
+          r_d2[j] = t2 >= 0 ? dist_at(o, t2) : FLT_MAX;
         }
         __syncwarp();  // the new entry of the taken set is visible to the next centre's probes
+        ci = cn;
       }
       if (lane == 0) s_next = o;
     }
@@ -269,7 +310,7 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
     const float* row = D + (int64_t)j * ldd;
     for (int64_t p = tid; p < N; p += blockDim.x) {
       const int64_t gi = row_off + p;
-      if (taken_has(tab, gi)) continue;
+      if (taken.has(gi)) continue;
       const float v = row[p];
       if (lex_less(v, gi, b1, i1)) { b2 = b1; i2 = i1; b1 = v; i1 = gi; }
       else if (lex_less(v, gi, b2, i2)) { b2 = v; i2 = gi; }
@@ -290,9 +331,7 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
       }
     }
     const int wid = tid >> 5;
-    if ((tid & 31) == 0) { rd[wid] = b1; ri[wid] = i1; rs[wid] = b2; }
-    __shared__ int64_t ri2[256];
-    if ((tid & 31) == 0) ri2[wid] = i2;
+    if ((tid & 31) == 0) { rd[wid] = b1; ri[wid] = i1; rs[wid] = b2; ri2[wid] = i2; }
     __syncthreads();
     if (tid == 0) {
       float B1 = FLT_MAX, B2 = FLT_MAX;
@@ -309,18 +348,22 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
         }
       }
       if (I1 == INT64_MAX) { set_status(ws, CABS_DEV_SNAP_EXHAUSTED); I1 = 0; B1 = 0.f; }
-      taken_put(tab, I1);
+      taken.put(I1);
       reps[j] = I1;
-      if (rep_of_centre) rep_of_centre[j] = I1;
-      if (gap) gap[j] = (I2 == INT64_MAX) ? FLT_MAX : (B2 > 0.f ? (B2 - B1) / B2 : 0.f);
+      r_d1[j] = B1;
+      r_d2[j] = I2 == INT64_MAX ? FLT_MAX : B2;
       s_next = s_next + 1;
     }
     __syncthreads();
   }
   __syncthreads();
-  // sorted representatives (distinct)
-  for (int j = tid; j < k2; j += blockDim.x) {
+  for (int j = tid; j < k2; j += blockDim.x) {  // outputs of every centre, and the sorted representatives
     const int64_t v = reps[j];
+    if (rep_of_centre) rep_of_centre[j] = v;
+    if (gap) {
+      const float d1 = r_d1[j], d2 = r_d2[j];
+      gap[j] = (d2 == FLT_MAX) ? FLT_MAX : (d2 > 0.f ? (d2 - d1) / d2 : 0.f);
+    }
     int rk = 0;
     for (int q = 0; q < k2; ++q) rk += reps[q] < v;
     reps_sorted[rk] = v;
@@ -344,11 +387,15 @@ void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int 
     cudaFuncSetAttribute(snap_dedupe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCap));
     attr = true;
   }
-  const size_t bytes = (size_t)k2 * T * (sizeof(int64_t) + sizeof(float));
-  const bool stage = bytes <= kCap;
+  size_t cand = (((size_t)k2 * T * (sizeof(int64_t) + sizeof(float))) + 15) & ~size_t(15);
+  const bool staged = cand <= kCap;
+  if (!staged) cand = 0;
+  const size_t bits = sizeof(unsigned) * ((N + 31) / 32);
+  const bool bitmap = can_rescan && N <= kBitmapMax && cand + bits <= kCap;
+  const size_t bytes = cand + (bitmap ? bits : 0);
   note_launch();
-  snap_dedupe_kernel<<<1, 256, stage ? bytes : 0, st>>>(cand_d, cand_i, k2, T, cluster_w, D, ldd, N, row_off, can_rescan,
-                                                        rep_of_centre, gap, reps_sorted, ws, stage);
+  snap_dedupe_kernel<<<1, 256, bytes, st>>>(cand_d, cand_i, k2, T, cluster_w, D, ldd, N, row_off, can_rescan,
+                                            rep_of_centre, gap, reps_sorted, ws, staged, bitmap);
 }
 
 }  // namespace cabsk
