@@ -8,6 +8,8 @@
 // pass in one CTA, rescanning D for a centre whose list is exhausted.
 #include <float.h>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -391,7 +393,7 @@ void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int 
   const bool staged = cand <= kCap;
   if (!staged) cand = 0;
   const size_t bits = sizeof(unsigned) * ((N + 31) / 32);
-  const bool bitmap = can_rescan && N <= kBitmapMax && cand + bits <= kCap;
+  const bool bitmap = can_rescan && N <= kBitmapMax && cand + bits <= kCap && !getenv("CABS_SNAP_HASH");
   const size_t bytes = cand + (bitmap ? bits : 0);
   note_launch();
   snap_dedupe_kernel<<<1, 256, bytes, st>>>(cand_d, cand_i, k2, T, cluster_w, D, ldd, N, row_off, can_rescan,

@@ -449,6 +449,62 @@ def test_select_pair_equals_two_single_calls(dev):
         assert np.array_equal(r.cpu().numpy(), rr) and np.array_equal(c.cpu().numpy(), cc)
 
 
+def test_select_bitmap_and_hash_taken_sets_agree(dev, monkeypatch):
+    """The snap's greedy pass gives the same representatives with the single-GPU bitmap
+    taken set and with the hash table of global indices (the multi-rank path)."""
+    d, k2, N = 20, 40, 5000
+    ld = C.cabs_padded_ld(d)
+    X = torch.zeros((N, ld), device=dev); X[:, :d] = torch.from_numpy(_clustered(N, d, 12, 41)).to(dev)
+    g = torch.Generator(device="cpu").manual_seed(9)
+    cen = torch.zeros((k2, ld), device=dev); cen[:, :d] = (0.3 * torch.randn(k2, d, generator=g)).to(dev)
+    cw = torch.rand(k2, generator=g, dtype=torch.float64).to(dev)
+    plan = _plan(N, N, max(d, k2))
+    ws = _ws(plan, dev)
+    res = []
+    for force_hash in (False, True):
+        if force_hash:
+            monkeypatch.setenv("CABS_SNAP_HASH", "1")
+        reps = torch.zeros(k2, dtype=torch.int64, device=dev)
+        roc = torch.zeros(k2, dtype=torch.int64, device=dev)
+        C.cabs_select(plan, X, N, N, 0, d, cen, k2, cw, reps, ws, rep_of_centre=roc)
+        res.append((reps.cpu().numpy(), roc.cpu().numpy()))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert len(set(res[0][0].tolist())) == k2
+
+
+@pytest.mark.parametrize("kind", ["embed", "sketch"])
+def test_fused_and_unfused_s5_identical(dev, monkeypatch, kind):
+    """The single-GPU fused S5 kernel and the multi-pass path (GEMMs, norm reduction,
+    finalize, scale / compaction) produce bit-identical outputs."""
+    m, n, k = 3000, 2000, 24
+    g = np.random.default_rng(17)
+    A = (g.standard_normal((m, 8)) @ g.standard_normal((8, n)) + 0.01 * g.standard_normal((m, n))).astype(np.float32)
+    At = torch.from_numpy(A).to(dev)
+    plan = _plan(m, n, k)
+    ws = _ws(plan, dev)
+    I = torch.from_numpy(np.sort(g.choice(m, k, replace=False)).astype(np.int64)).to(dev)
+    J = torch.from_numpy(np.sort(g.choice(n, k, replace=False)).astype(np.int64)).to(dev)
+    ld = C.cabs_padded_ld(k)
+    outs = []
+    for unfused in (False, True):
+        if unfused:
+            monkeypatch.setenv("CABS_EMBED_UNFUSED", "1")
+        P = torch.zeros((m, ld), device=dev); Q = torch.zeros((n, ld), device=dev)
+        s = torch.zeros(k, device=dev); r = torch.zeros(1, dtype=torch.int32, device=dev)
+        sig = torch.zeros(k, dtype=torch.float64, device=dev)
+        if kind == "embed":
+            Cm = torch.zeros((m, ld), device=dev); Cm[:, :k] = At[:, J]
+            Rm = At[I, :].contiguous()
+            W = torch.zeros((k, ld), device=dev); W[:, :k] = At[I][:, J]
+            C.cabs_embed(plan, k, Cm, Rm, W, C.STABILIZED, 1e-12, P, Q, s, r, ws, sigma=sig)
+        else:
+            C.cabs_sketch(plan, At, I, J, k, C.STABILIZED, 1e-12, P, s, Q, r, ws, sigma=sig)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in (P, Q, s, r)])
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+
+
 def test_embed_drops_zero_norm_component_with_compaction(dev):
     """S:244 drop rule with a hole: component 0 extrapolates to zero, component 1 is kept,
     so the kept component must be compacted to position 0 (inconsistent triple, as in the
