@@ -263,8 +263,7 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
     return arg_error("sketch: bad buffers");
   cudaStream_t st = S(stream);
   const int64_t m_loc = p.row_end - p.row_begin;
-  launch_validate_idx(Ir, k, p.m, ws, st);
-  launch_validate_idx(Ic, k, p.n, ws, st);
+  launch_validate_idx2(Ir, p.m, Ic, p.n, k, ws, st);
   float* Cb = wsp<float>(ws, L.cb);
   float* Rb = wsp<float>(ws, L.rb);
   float* Wb = wsp<float>(ws, L.wb);

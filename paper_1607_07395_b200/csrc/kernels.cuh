@@ -12,6 +12,8 @@ int launch_floyd2(int64_t N0, int32_t k0, uint32_t tag0, int64_t* out0, int64_t 
                   int64_t* out1, uint64_t seed, cudaStream_t st);
 void launch_philox_blocks(uint64_t seed, uint32_t tag, uint64_t start, int64_t count, uint32_t* out, cudaStream_t st);
 void launch_validate_idx(const int64_t* idx, int32_t k, int64_t N, void* ws, cudaStream_t st);
+void launch_validate_idx2(const int64_t* idx0, int64_t N0, const int64_t* idx1, int64_t N1, int32_t k, void* ws,
+                          cudaStream_t st);
 void launch_gather_rows(const float* A, int64_t lda, int64_t row_begin, int64_t row_end, const int64_t* I, int32_t k,
                         int64_t n, float* R, int64_t ldr, void* ws, cudaStream_t st);
 void launch_gather_cols(const float* A, int64_t lda, int64_t m_loc, const int64_t* J, int32_t k, float* C, int64_t ldc,

@@ -67,9 +67,59 @@ __global__ void __launch_bounds__(256) km_weights_kernel(KmWeightJob j0, KmWeigh
   }
 }
 
+// Constant weights (CABS_WEIGHT_CONST): w = 1, cnt += N, bounds = {max|x|, 1} -- no per-point
+// reduction; thread per 4 consecutive entries (16-byte loads when the rows allow), entries
+// beyond d masked out.  blockIdx.y: job.
+__global__ void __launch_bounds__(256) km_weights_const_kernel(KmWeightJob j0, KmWeightJob j1) {
+  const KmWeightJob j = blockIdx.y == 0 ? j0 : j1;
+  const int64_t N = j.N;
+  const int d = j.d;
+  const int q4 = (d + 3) >> 2;
+  const bool vec = (j.ldx & 3) == 0 && (reinterpret_cast<uintptr_t>(j.X) & 15) == 0;
+  float mx = 0.f;
+  const int64_t total = N * q4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = e / q4;
+    const int i = static_cast<int>(e - l * q4) * 4;
+    const float* row = j.X + l * j.ldx;
+    float4 v;
+    if (vec && i + 3 < d) {
+      v = __ldg(reinterpret_cast<const float4*>(row + i));
+    } else {
+      v.x = row[i];
+      v.y = i + 1 < d ? row[i + 1] : 0.f;
+      v.z = i + 2 < d ? row[i + 2] : 0.f;
+      v.w = i + 3 < d ? row[i + 3] : 0.f;
+    }
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < N; l += (int64_t)gridDim.x * blockDim.x)
+    j.w[l] = 1.f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __shared__ float s_mx[8];
+  if ((threadIdx.x & 31) == 0) s_mx[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) mx = fmaxf(mx, s_mx[q]);
+    atomicMax(j.bounds, __float_as_uint(mx));
+    if (blockIdx.x == 0) {
+      if (N > 0) atomicAdd(j.cnt, static_cast<int>(N));
+      atomicMax(j.bounds + 1, __float_as_uint(N > 0 ? 1.f : 0.f));
+    }
+  }
+}
+
 void launch_km_weights2(const KmWeightJob& j0, const KmWeightJob* j1, int kind, float p, cudaStream_t st) {
   int64_t N = j0.N > (j1 ? j1->N : 0) ? j0.N : j1->N;
   if (N <= 0) return;
+  if (kind == CABS_WEIGHT_CONST) {
+    int64_t blocks = ceil_div(N * 16, 256);
+    if (blocks > 2 * kNumSM) blocks = 2 * kNumSM;
+    note_launch();
+    km_weights_const_kernel<<<dim3(static_cast<unsigned>(blocks), j1 ? 2 : 1), 256, 0, st>>>(j0, j1 ? *j1 : j0);
+    return;
+  }
   int64_t blocks = ceil_div(N, 8);
   if (blocks > 2 * kNumSM) blocks = 2 * kNumSM;
   note_launch();
