@@ -65,8 +65,11 @@ def test_philox_blocks_match_oracle(dev):
 
 @pytest.mark.parametrize("N,k,seed,tag", [(5, 5, 0, 1), (100, 10, 7, 1), (20000, 50, 0, 1), (10000, 50, 0, 2),
                                           (2_000_000, 300, 3, 4), (1000, 1, 9, 3), (1024, 1024, 11, 2),
-                                          (4_000_000_000, 200, 5, 1)])
+                                          (4_000_000_000, 200, 5, 1), (4_000_000_000, 60, 6, 1),
+                                          (3_000_000_000, 33, 2, 5), (64, 64, 1, 1), (1000, 63, 4, 2)])
 def test_uniform_indices_bit_exact(dev, N, k, seed, tag):
+    """Floyd sampling equals the oracle's; k <= 64 runs the parallel-draw fast path, and the
+    huge-N cases make Lemire rejections likely (the fast path's fallback)."""
     out = torch.zeros(k, dtype=torch.int64, device=dev)
     C.cabs_uniform_indices(N, k, seed, tag, out)
     assert np.array_equal(out.cpu().numpy(), rng.floyd(N, k, seed, tag))
