@@ -37,30 +37,35 @@ __device__ __forceinline__ void km_tile_block(const float* __restrict__ X, int64
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+  // stage i0 + kTileD is loaded into registers while stage i0 is computed from shared memory
+  const int pp = tid >> 2, ii = (tid & 3) * 4;
+  const int64_t p = p0 + pp;
+  const int jr = j0 + pp;
+  float xr[4], cr[4];
+  auto load_stage = [&](int i0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + ii + q;
+      xr[q] = (p < N && i < d) ? __ldg(X + p * ldx + i) : 0.f;
+      cr[q] = (jr < k2 && i < d) ? ld_centre<COHERENT>(centres + (int64_t)jr * ldc + i) : 0.f;
+    }
+  };
+  load_stage(0);
   for (int i0 = 0; i0 < d; i0 += kTileD) {
-    {
-      const int pp = tid >> 2, ii = (tid & 3) * 4;
-      const int64_t p = p0 + pp;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = i0 + ii + q;
-        sm.Xs[ii + q][pp] = (p < N && i < d) ? __ldg(X + p * ldx + i) : 0.f;
-      }
-      const int j = j0 + pp;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = i0 + ii + q;
-        sm.Cs[ii + q][pp] = (j < k2 && i < d) ? ld_centre<COHERENT>(centres + (int64_t)j * ldc + i) : 0.f;
-      }
+    for (int q = 0; q < 4; ++q) {
+      sm.Xs[ii + q][pp] = xr[q];
+      sm.Cs[ii + q][pp] = cr[q];
     }
     __syncthreads();
+    if (i0 + kTileD < d) load_stage(i0 + kTileD);
 #pragma unroll
-    for (int ii = 0; ii < kTileD; ++ii) {
+    for (int ii2 = 0; ii2 < kTileD; ++ii2) {
       float x[4], c[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) x[a] = sm.Xs[ii][tp + 16 * a];
+      for (int a = 0; a < 4; ++a) x[a] = sm.Xs[ii2][tp + 16 * a];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) c[b] = sm.Cs[ii][tc + 16 * b];
+      for (int b = 0; b < 4; ++b) c[b] = sm.Cs[ii2][tc + 16 * b];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll

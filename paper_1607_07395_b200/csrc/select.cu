@@ -34,8 +34,19 @@ __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict_
 #pragma unroll
   for (int q = 0; q < T; ++q) { ld[q] = FLT_MAX; li[q] = INT64_MAX; }
   const float* row = D + (int64_t)j * ldd;
-  for (int64_t p = pbeg + tid; p < pend; p += blockDim.x) {
-    const float v = row[p];
+  constexpr int kU = 8;  // distances loaded per batch (independent loads in flight)
+  for (int64_t p0 = pbeg + tid; p0 < pend; p0 += kU * (int64_t)blockDim.x) {
+    float vb[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t p = p0 + (int64_t)u * blockDim.x;
+      vb[u] = p < pend ? __ldg(row + p) : FLT_MAX;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+    const int64_t p = p0 + (int64_t)u * blockDim.x;
+    if (p >= pend) break;
+    const float v = vb[u];
     const int64_t gi = row_off + p;
     if (lex_less(v, gi, ld[T - 1], li[T - 1])) {
       // insertion into the sorted list (compile-time indices only)
@@ -52,6 +63,7 @@ __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict_
           ci = ti;
         }
       }
+    }
     }
   }
   // merge: T rounds of block-wide lexicographic argmin over the list heads
