@@ -73,6 +73,35 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_
       : "memory");
 }
 
+// 32 lanes x 32 columns of 32-bit TMEM -> registers, WITHOUT the wait (the caller issues
+// tcgen05.wait::ld once for a batch of loads)
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// after tcgen05.wait::ld: ties the registers of a no-wait load to this point (volatile asm
+// order), so no use can be scheduled before the wait
+__device__ __forceinline__ void tmem_regs_fence(float (&v)[32]) {
+  asm volatile(""
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
+                 "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
+                 "+f"(v[15]), "+f"(v[16]), "+f"(v[17]), "+f"(v[18]), "+f"(v[19]), "+f"(v[20]), "+f"(v[21]),
+                 "+f"(v[22]), "+f"(v[23]), "+f"(v[24]), "+f"(v[25]), "+f"(v[26]), "+f"(v[27]), "+f"(v[28]),
+                 "+f"(v[29]), "+f"(v[30]), "+f"(v[31]));
+}
+
 // 32 lanes x 32 columns: registers -> TMEM (this warp's lane quarter)
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
   asm volatile(
@@ -273,39 +302,47 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       tc::fence_after_sync();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(sc * kTcBN);
       float tr0 = 0.f, ta0 = 0.f, tr1 = 0.f, ta1 = 0.f;
+      // both A boxes of this group (rows from 128B-swizzled boxes: 16-byte chunk c of row r is
+      // at chunk c ^ (r & 7)), released as soon as their values are in registers; then both
+      // 32-column halves of the accumulator in one TMEM load batch (one wait)
+      float av[kHalf][32];
 #pragma unroll
       for (int hh = 0; hh < kHalf; ++hh) {
-        const int h = kHalf * eg + hh;
-        // A row from a 128B-swizzled box (16-byte chunk c of row r is at chunk c ^ (r & 7));
-        // the box slot (in this group's ring) is released as soon as its values are in registers
         const int64_t li = kHalfAQ * i + hh;
         const int sa = eg * kAR + static_cast<int>(li % kAR);
         RES_WAIT(10, tc::mbar_wait(&S.a_full[sa], ring_parity(li, kAR)));
-        float av[32];
         const uint8_t* arow = S.a[sa] + row * 128;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const float4 a4 = *reinterpret_cast<const float4*>(arow + ((c ^ (row & 7)) << 4));
-          av[4 * c] = a4.x; av[4 * c + 1] = a4.y; av[4 * c + 2] = a4.z; av[4 * c + 3] = a4.w;
-        }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&S.a_empty[sa]);
-        float v[32];
-        tc::tmem_ld32(tbase + 32 * h, v);
-        if (hh == kHalf - 1) {
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);
-        }
-#pragma unroll
-        for (int x = 0; x < 32; x += 2) {
-          const float e0 = av[x] - v[x], e1 = av[x + 1] - v[x + 1];
-          tr0 = fmaf(e0, e0, tr0);
-          ta0 = fmaf(av[x], av[x], ta0);
-          tr1 = fmaf(e1, e1, tr1);
-          ta1 = fmaf(av[x + 1], av[x + 1], ta1);
+          av[hh][4 * c] = a4.x; av[hh][4 * c + 1] = a4.y; av[hh][4 * c + 2] = a4.z; av[hh][4 * c + 3] = a4.w;
         }
       }
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int hh = 0; hh < kHalf; ++hh)
+          tc::mbar_arrive(&S.a_empty[eg * kAR + static_cast<int>((kHalfAQ * i + hh) % kAR)]);
+      }
+      float v[kHalf][32];
+#pragma unroll
+      for (int hh = 0; hh < kHalf; ++hh) tmem_ld32_nowait(tbase + 32 * (kHalf * eg + hh), v[hh]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int hh = 0; hh < kHalf; ++hh) tmem_regs_fence(v[hh]);
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);
+#pragma unroll
+      for (int hh = 0; hh < kHalf; ++hh)
+#pragma unroll
+        for (int x = 0; x < 32; x += 2) {
+          const float e0 = av[hh][x] - v[hh][x], e1 = av[hh][x + 1] - v[hh][x + 1];
+          tr0 = fmaf(e0, e0, tr0);
+          ta0 = fmaf(av[hh][x], av[hh][x], ta0);
+          tr1 = fmaf(e1, e1, tr1);
+          ta1 = fmaf(av[hh][x + 1], av[hh][x + 1], ta1);
+        }
       r2 += static_cast<double>(tr0 + tr1);
       a2 += static_cast<double>(ta0 + ta1);
     }
