@@ -91,8 +91,9 @@ __host__ __device__ inline LloydSmem lloyd_smem(int d, int k2, int pitch, size_t
   LloydSmem L;
   size_t o = base;
   auto take = [&](size_t b) { size_t r = o; o += (b + 15) & ~size_t(15); return r; };
-  L.cs = take(sizeof(float) * round_up(k2, kLC) * d);
-  L.xs = take(sizeof(float) * (size_t)d * pitch);
+  const int d2 = (d + 1) >> 1;  // dimension pairs (an odd d gets a zero dimension)
+  L.cs = take(sizeof(float) * round_up(k2, kLC) * 2 * d2);
+  L.xs = take(sizeof(float) * (size_t)2 * d2 * pitch);
   L.wsc = take(sizeof(double) * (size_t)pitch);
   L.iw = take(sizeof(long long) * (size_t)pitch);
   L.wts = take(sizeof(float) * (size_t)pitch);
@@ -105,9 +106,9 @@ __host__ __device__ inline LloydSmem lloyd_smem(int d, int k2, int pitch, size_t
 // centre j, dimension i -> float index of the pair layout [j/64][i][q][ct][half] with
 // jj = j % 64 = 32 q + 16 half + ct: thread ct of the distance loop reads (c_{ct+32q},
 // c_{ct+32q+16}), q < 2, as two 8-byte words per dimension.
-__device__ __forceinline__ int cpair_idx(int j, int i, int d) {
+__device__ __forceinline__ int cpair_idx(int j, int i, int d2) {
   const int jj = j & 63;
-  return ((((j >> 6) * d + i) * 2 + (jj >> 5)) * 16 + (jj & 15)) * 2 + ((jj >> 4) & 1);
+  return (((((j >> 6) * d2 + (i >> 1)) * 2 + (jj >> 5)) * 16 + (jj & 15)) * 2 + (i & 1)) * 2 + ((jj >> 4) & 1);
 }
 
 __device__ __forceinline__ unsigned long long f2_dup(float x) {
@@ -149,10 +150,10 @@ __device__ __forceinline__ ProbSmem prob_smem(unsigned char* dyn, const LloydSme
 // chunk of np <= cap points -> x [i][pitch], w 2^S, llrint(w 2^Sw), w (zeros beyond)
 __device__ __forceinline__ void stage_chunk(const LloydProb& pr, int64_t p0, int np, const ProbSmem& S, double scale,
                                             double scale_w) {
-  const int d = pr.d, P = pr.pitch, cap = pr.cap;
-  for (int e = threadIdx.x; e < cap * d; e += blockDim.x) {
-    const int pp = e / d, i = e - pp * d;
-    S.xs[i * P + pp] = pp < np ? __ldg(pr.X + (p0 + pp) * pr.ldx + i) : 0.f;
+  const int d = pr.d, P = pr.pitch, cap = pr.cap, dd = 2 * ((d + 1) >> 1);
+  for (int e = threadIdx.x; e < cap * dd; e += blockDim.x) {
+    const int pp = e / dd, i = e - pp * dd;
+    S.xs[((i >> 1) * P + pp) * 2 + (i & 1)] = (pp < np && i < d) ? __ldg(pr.X + (p0 + pp) * pr.ldx + i) : 0.f;
   }
   for (int pp = threadIdx.x; pp < cap; pp += blockDim.x) {
     const float w = pp < np ? pr.w[p0 + pp] : 0.f;
@@ -186,8 +187,8 @@ __device__ __forceinline__ void accumulate_owned(const int* lab, int np, const P
           const int p = 32 * t + __ffs(m) - 1;
           m &= m - 1;
           const double ws = S.wsc[p];
-          if (ia < d) sa += fx_prod_magic(ws, S.xs[ia * P + p]);
-          if (ib < d) sb += fx_prod_magic(ws, S.xs[ib * P + p]);
+          if (ia < d) sa += fx_prod_magic(ws, S.xs[((ia >> 1) * P + p) * 2 + (ia & 1)]);
+          if (ib < d) sb += fx_prod_magic(ws, S.xs[((ib >> 1) * P + p) * 2 + (ib & 1)]);
           sw += S.iw[p];
         }
       }
@@ -201,35 +202,39 @@ __device__ __forceinline__ void accumulate_owned(const int* lab, int np, const P
 // One block of centres jc + 16 v, v < NV (jc = j0 + ct), against the points pt + 16 u: pairs
 // (v, v + 1) in one FFMA2 lane pair, an odd last centre in scalar FP32 (the same IEEE ops).
 template <int NA, int NV>
-__device__ __forceinline__ void dist_block(const float* __restrict__ xq, int P, const unsigned long long* cq, int d,
+__device__ __forceinline__ void dist_block(const float2* __restrict__ xq, int P, const ulonglong2* cq, int d2,
                                            int jc, int k2, float* bd, float* sd, int* bj) {
   unsigned long long acc0[NA], acc1[NA];
   float accs[NA];
 #pragma unroll
   for (int u = 0; u < NA; ++u) { acc0[u] = 0ull; acc1[u] = 0ull; accs[u] = 0.f; }
-#pragma unroll 2
-  for (int i = 0; i < d; ++i) {
-    const unsigned long long c0 = cq[i * 32];
-    const unsigned long long c1 = NV >= 3 ? cq[i * 32 + 16] : 0ull;
-    float x[NA];
+  for (int i2 = 0; i2 < d2; ++i2) {  // dimensions 2 i2, 2 i2 + 1: one 8-byte x load, one 16-byte centre load
+    const ulonglong2 c0 = cq[i2 * 32];
+    const ulonglong2 c1 = NV >= 3 ? cq[i2 * 32 + 16] : make_ulonglong2(0ull, 0ull);
+    float2 x2[NA];
 #pragma unroll
-    for (int u = 0; u < NA; ++u) x[u] = xq[i * P + 16 * u];
+    for (int u = 0; u < NA; ++u) x2[u] = xq[i2 * P + 16 * u];
 #pragma unroll
-    for (int u = 0; u < NA; ++u) {
-      if (NV >= 2) {
-        const unsigned long long xx = f2_dup(x[u]);
-        const unsigned long long df0 = f2_sub(xx, c0);
-        acc0[u] = f2_fma(df0, df0, acc0[u]);
-        if (NV == 4) {
-          const unsigned long long df1 = f2_sub(xx, c1);
-          acc1[u] = f2_fma(df1, df1, acc1[u]);
-        } else if (NV == 3) {
-          const float df = x[u] - f2_lo(c1);
+    for (int h = 0; h < 2; ++h) {  // the sums stay in dimension order
+      const unsigned long long cc0 = h ? c0.y : c0.x, cc1 = h ? c1.y : c1.x;
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        const float xv = h ? x2[u].y : x2[u].x;
+        if (NV >= 2) {
+          const unsigned long long xx = f2_dup(xv);
+          const unsigned long long df0 = f2_sub(xx, cc0);
+          acc0[u] = f2_fma(df0, df0, acc0[u]);
+          if (NV == 4) {
+            const unsigned long long df1 = f2_sub(xx, cc1);
+            acc1[u] = f2_fma(df1, df1, acc1[u]);
+          } else if (NV == 3) {
+            const float df = xv - f2_lo(cc1);
+            accs[u] = fmaf(df, df, accs[u]);
+          }
+        } else {
+          const float df = xv - f2_lo(cc0);
           accs[u] = fmaf(df, df, accs[u]);
         }
-      } else {
-        const float df = x[u] - f2_lo(c0);
-        accs[u] = fmaf(df, df, accs[u]);
       }
     }
   }
@@ -262,17 +267,18 @@ __device__ __forceinline__ void dist_rows(const float* __restrict__ xs, int P, c
   int bj[NA];
 #pragma unroll
   for (int q = 0; q < NA; ++q) { bd[q] = FLT_MAX; sd[q] = FLT_MAX; bj[q] = 0x7fffffff; }
-  const float* xq = xs + pt;
+  const float2* xq = reinterpret_cast<const float2*>(xs) + pt;
+  const int d2 = (d + 1) >> 1;
   for (int j0 = 0; j0 < k2; j0 += kLC) {
     // centres ct + 16 v (v < nv) of the block hold real centres for this warp (its two ct are
     // 2 warp and 2 warp + 1): the padding of the last block costs no arithmetic
     const int rem = k2 - j0 - 2 * warp;
     const int nv = rem <= 0 ? 0 : (rem >= 64 ? 4 : (rem + 15) >> 4);
-    const unsigned long long* cq = reinterpret_cast<const unsigned long long*>(cs) + (size_t)(j0 >> 6) * d * 32 + ct;
-    if (nv == 4) dist_block<NA, 4>(xq, P, cq, d, j0 + ct, k2, bd, sd, bj);
-    else if (nv == 3) dist_block<NA, 3>(xq, P, cq, d, j0 + ct, k2, bd, sd, bj);
-    else if (nv == 2) dist_block<NA, 2>(xq, P, cq, d, j0 + ct, k2, bd, sd, bj);
-    else if (nv == 1) dist_block<NA, 1>(xq, P, cq, d, j0 + ct, k2, bd, sd, bj);
+    const ulonglong2* cq = reinterpret_cast<const ulonglong2*>(cs) + (size_t)(j0 >> 6) * d2 * 32 + ct;
+    if (nv == 4) dist_block<NA, 4>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj);
+    else if (nv == 3) dist_block<NA, 3>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj);
+    else if (nv == 2) dist_block<NA, 2>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj);
+    else if (nv == 1) dist_block<NA, 1>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj);
   }
   // merge the two centre lanes of this warp (lanes l and l ^ 16 hold the same points)
 #pragma unroll
@@ -356,9 +362,10 @@ __global__ void __launch_bounds__(kLT, 2) lloyd_persistent_kernel(LloydArgs a) {
     const ProbSmem S = prob_smem(dyn, Ls[q]);
     if (a.resident) stage_chunk(pr, pbeg[q], static_cast<int>(pend[q] - pbeg[q]), S, scale[q], scale_w[q]);
     const int k2p = static_cast<int>(round_up(pr.k2, kLC));
-    for (int e = tid; e < k2p * pr.d; e += blockDim.x) {
-      const int j = e / pr.d, i = e - j * pr.d;
-      S.cs[cpair_idx(j, i, pr.d)] = j < pr.k2 ? __ldcg(pr.centres + (int64_t)j * pr.ldc + i) : 0.f;
+    const int dd = 2 * ((pr.d + 1) >> 1);
+    for (int e = tid; e < k2p * dd; e += blockDim.x) {  // padding centres and the padding dimension = 0
+      const int j = e / dd, i = e - j * dd;
+      S.cs[cpair_idx(j, i, dd >> 1)] = (j < pr.k2 && i < pr.d) ? __ldcg(pr.centres + (int64_t)j * pr.ldc + i) : 0.f;
     }
   }
 
@@ -432,7 +439,8 @@ __global__ void __launch_bounds__(kLT, 2) lloyd_persistent_kernel(LloydArgs a) {
           if (rw > 0) {
 #pragma unroll 4
             for (int i = tid >> 6; i < d; i += kLT / 64)
-              S.cs[cpair_idx(j, i, d)] = static_cast<float>((static_cast<double>(S.part[j * d + i]) * inv_scale) * rw);
+              S.cs[cpair_idx(j, i, (d + 1) >> 1)] =
+                  static_cast<float>((static_cast<double>(S.part[j * d + i]) * inv_scale) * rw);
           }
         }
         // zero this CTA's share of the slot the next iteration accumulates into (last read
@@ -581,7 +589,7 @@ __global__ void __launch_bounds__(kLT, 2) lloyd_persistent_kernel(LloydArgs a) {
         pr.centres[(int64_t)j * pr.ldc + i] =
             wj > 0 ? static_cast<float>((static_cast<double>(__ldcg(fs_last + e)) * inv_scale) *
                                         (1.0 / (static_cast<double>(wj) * inv_scale_w)))
-                   : S.cs[cpair_idx(j, i, d)];
+                   : S.cs[cpair_idx(j, i, (d + 1) >> 1)];
       }
       for (int j = tid; j < k2; j += blockDim.x)
         pr.cluster_w[j] = static_cast<double>(__ldcg(fs_last + nsum + j)) / scale_w[q];
