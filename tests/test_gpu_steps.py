@@ -359,10 +359,13 @@ def test_residual_exact_factorisation_is_small(dev):
     assert out[0].item() == 0.0 and out[1].item() == float(np.sum(A.astype(np.float64) ** 2))
 
 
-def test_kmeans_persistent_and_loop_paths_agree(dev, monkeypatch):
+@pytest.mark.parametrize("N,d,k2", [(20000, 50, 50), (7001, 33, 19), (60000, 21, 70), (3000, 7, 5)])
+def test_kmeans_persistent_and_loop_paths_agree(dev, monkeypatch, N, d, k2):
     """The single-GPU persistent Lloyd kernel and the per-iteration kernels (multi-GPU path)
-    compute the same thing; only the CTA partition of the FP32 partial sums differs."""
-    N, d, k2, iters = 20000, 50, 50, 8
+    compute the same thing; only the CTA partition of the FP32 partial sums differs.  Cases:
+    the c2 shape, an odd dimension (zero-padded dimension pair) with k2 below one centre
+    block, more points than the CTAs hold (streamed chunks) with two centre blocks, tiny."""
+    iters = 8
     X = _clustered(N, d, 30, 11)
     ld = C.cabs_padded_ld(d)
     Xt = torch.zeros((N, ld), device=dev); Xt[:, :d] = torch.from_numpy(X).to(dev)
