@@ -152,6 +152,16 @@ int32_t cabs_embed(const cabs_plan* plan, int32_t k, const float* C, int64_t ldc
                    int32_t* r, double* sigma, void* ws, size_t ws_bytes,
                    const cabs_comm* comm, void* stream);
 
+/* S1-S5 in one call: exactly cabs_pilot followed by cabs_embed on its outputs (same
+ * arguments, same results).  On one GPU the SVD of W = A(I,J) (gathered first, straight
+ * from A) runs on the library's side stream while C and R are gathered on `stream`, so the
+ * two 2-SM and HBM-bound steps overlap; with a communicator it is the two calls in order. */
+int32_t cabs_pilot_embed(const cabs_plan* plan, const cabs_source* src, int32_t k, uint64_t seed,
+                         int64_t* I, int64_t* J, float* C, int64_t ldc, float* R, int64_t ldr,
+                         float* W, int64_t ldw, int32_t mode, double tol, float* P, int64_t ldp,
+                         float* Q, int64_t ldq, float* s, int32_t* r, double* sigma, void* ws,
+                         size_t ws_bytes, const cabs_comm* comm, void* stream);
+
 /* ---------------------------------------------------------------- S6-S7 k-means
  * Weighted Lloyd k-means (Eq. 6; c iterations) on the rows of
  * X (n_loc local rows of n_glob, global index = row_off + local, d columns, ldx).

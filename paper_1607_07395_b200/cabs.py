@@ -94,6 +94,9 @@ _SIGS = {
     "cabs_device_status": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_u32)]),
     "cabs_pilot": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_i32, c_u64, c_vp, c_vp,
                            c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_pilot_embed": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_i32, c_u64, c_vp, c_vp,
+                                 c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i32, c_f64, c_vp, c_i64, c_vp, c_i64,
+                                 c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_embed": (c_i32, [ctypes.POINTER(Plan), c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i32,
                            c_f64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_sz,
                            ctypes.POINTER(Comm), c_vp]),
@@ -217,6 +220,15 @@ def cabs_pilot(plan, A, k, seed, I, J, C, R, W, ws, comm=None, stream=None):
     _check(load().cabs_pilot(ctypes.byref(plan), ctypes.byref(src), int(k), int(seed), _p(I), _p(J),
                              _p(C), _ld(C), _p(R), _ld(R), _p(W), _ld(W), _p(ws), ws.numel(),
                              _comm(comm), _stream(stream)), "cabs_pilot")
+
+
+def cabs_pilot_embed(plan, A, k, seed, I, J, C, R, W, mode, tol, P, Q, s, r, ws, sigma=None, comm=None,
+                     stream=None):
+    src = Source(A.data_ptr(), _ld(A))
+    _check(load().cabs_pilot_embed(ctypes.byref(plan), ctypes.byref(src), int(k), int(seed), _p(I), _p(J),
+                                   _p(C), _ld(C), _p(R), _ld(R), _p(W), _ld(W), int(mode), float(tol),
+                                   _p(P), _ld(P), _p(Q), _ld(Q), _p(s), _p(r), _p(sigma), _p(ws), ws.numel(),
+                                   _comm(comm), _stream(stream)), "cabs_pilot_embed")
 
 
 def cabs_embed(plan, k, C, R, W, mode, tol, P, Q, s, r, ws, sigma=None, comm=None, stream=None):

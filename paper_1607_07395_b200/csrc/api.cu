@@ -250,6 +250,47 @@ int32_t cabs_embed(const cabs_plan* plan, int32_t k, const float* C, int64_t ldc
   return embed_core(*plan, L, k, C, ldc, R, ldr, W, ldw, mode, tol, P, ldp, Q, ldq, s, r, sigma, 0, ws, comm, stream);
 }
 
+int32_t cabs_pilot_embed(const cabs_plan* plan, const cabs_source* src, int32_t k, uint64_t seed, int64_t* I,
+                         int64_t* J, float* C, int64_t ldc, float* R, int64_t ldr, float* W, int64_t ldw, int32_t mode,
+                         double tol, float* P, int64_t ldp, float* Q, int64_t ldq, float* s, int32_t* r,
+                         double* sigma, void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream) {
+  if (multi(comm)) {
+    CABS_TRY(cabs_pilot(plan, src, k, seed, I, J, C, ldc, R, ldr, W, ldw, ws, ws_bytes, comm, stream));
+    return cabs_embed(plan, k, C, ldc, R, ldr, W, ldw, mode, tol, P, ldp, Q, ldq, s, r, sigma, ws, ws_bytes, comm,
+                      stream);
+  }
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  const cabs_plan& p = *plan;
+  if (k < 1 || k > p.kmax || k > p.m || k > p.n) return arg_error("pilot: need 1 <= k <= min(m, n, kmax)");
+  if (!src || !src->a || src->lda < p.n) return arg_error("pilot: bad source");
+  if (!I || !J || !C || !R || !W || ldc < k || ldr < p.n || ldw < k) return arg_error("pilot: bad output buffers");
+  if (p.m >= 0xFFFFFFFFll || p.n >= 0xFFFFFFFFll) return arg_error("pilot: dims must be < 2^32 - 1");
+  if (mode != CABS_STABILIZED && mode != CABS_PSEUDO_SKELETON) return arg_error("embed: bad mode");
+  if (!P || !Q || !s || ldp < k || ldq < k) return arg_error("embed: bad buffers");
+  cudaStream_t st = S(stream);
+  const int64_t m_loc = p.row_end - p.row_begin;
+  launch_floyd2(p.m, k, 1u, I, p.n, k, 2u, J, seed, st);  // tags ROWS_PILOT = 1, COLS_PILOT = 2
+  CABS_LAUNCH_CHECK("floyd");
+  // W = A(I, J) first, its SVD on the side stream while C and R are gathered here
+  launch_gather_w_direct(src->a, src->lda, p.row_begin, I, J, k, W, ldw, st);
+  CABS_LAUNCH_CHECK("gather_w_direct");
+  SideStream* ss = nullptr;
+  CABS_TRY(side_stream(&ss));
+  CABS_CUDA_TRY(cudaEventRecord(ss->fork, st));
+  CABS_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+  launch_svd(k, W, ldw, tol, ws, L, sigma, nullptr, nullptr, nullptr, ss->s);
+  CABS_LAUNCH_CHECK("svd");
+  launch_gather_cols(src->a, src->lda, m_loc, J, k, C, ldc, ws, st);
+  launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, I, k, p.n, R, ldr, ws, st);
+  CABS_LAUNCH_CHECK("pilot gathers");
+  CABS_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
+  CABS_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));
+  return embed_core(p, L, k, C, ldc, R, ldr, W, ldw, mode, tol, P, ldp, Q, ldq, s, r, sigma, 0, ws, comm, stream,
+                    true);
+}
+
 int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t* Ir, const int64_t* Ic, int32_t k,
                     int32_t mode, double tol, float* U, int64_t ldu, float* s, float* V, int64_t ldv, int32_t* r,
                     double* sigma, void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream) {

@@ -34,7 +34,7 @@ class CabsConfig:
     weight_p: float = 2.0
 
 
-STEPS = ("pilot", "embed", "kmeans", "select", "sketch", "residual")
+STEPS = ("pilot_embed", "kmeans", "select", "sketch", "residual")
 
 
 class CabsPipeline:
@@ -80,6 +80,12 @@ class CabsPipeline:
         c, p = self.cfg, self.plan
         C.cabs_pilot(p, self.A, c.k1, c.seed, self.I, self.J, self.Cm, self.R, self.W, self.ws, self.comm)
 
+    def pilot_embed(self):
+        """S1-S5 in one library call (single GPU: the SVD of W overlaps the C / R gathers)."""
+        c, p = self.cfg, self.plan
+        C.cabs_pilot_embed(p, self.A, c.k1, c.seed, self.I, self.J, self.Cm, self.R, self.W, c.mode, c.tol,
+                           self.P, self.Q, self.s1, self.r1, self.ws, sigma=self.sigma1, comm=self.comm)
+
     def embed(self):
         c, p = self.cfg, self.plan
         C.cabs_embed(p, c.k1, self.Cm, self.R, self.W, c.mode, c.tol, self.P, self.Q, self.s1, self.r1,
@@ -122,19 +128,17 @@ class CabsPipeline:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(STEPS) + 1)] if timed else None
         if timed:
             ev[0].record()
-        self.pilot()
+        self.pilot_embed()
         timed and ev[1].record()
-        self.embed()
-        timed and ev[2].record()
         self.kmeans(init_rows, init_cols)
-        timed and ev[3].record()
+        timed and ev[2].record()
         self.select()
-        timed and ev[4].record()
+        timed and ev[3].record()
         self.sketch()
-        timed and ev[5].record()
+        timed and ev[4].record()
         if with_residual:
             self.residual()
-        timed and ev[6].record()
+        timed and ev[5].record()
         self.events = ev
         return ev
 

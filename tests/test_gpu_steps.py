@@ -511,6 +511,34 @@ def test_fused_and_unfused_s5_identical(dev, monkeypatch, kind):
         assert np.array_equal(a, b)
 
 
+def test_pilot_embed_equals_pilot_then_embed(dev):
+    """cabs_pilot_embed (SVD of W on the side stream during the C / R gathers) gives exactly
+    the outputs of cabs_pilot followed by cabs_embed."""
+    m, n, k = 3000, 2000, 24
+    g = np.random.default_rng(23)
+    A = (g.standard_normal((m, 6)) @ g.standard_normal((6, n)) + 0.01 * g.standard_normal((m, n))).astype(np.float32)
+    At = torch.from_numpy(A).to(dev)
+    plan = _plan(m, n, k)
+    ws = _ws(plan, dev)
+    ld = C.cabs_padded_ld(k)
+    outs = []
+    for fused in (False, True):
+        I = torch.zeros(k, dtype=torch.int64, device=dev); J = torch.zeros(k, dtype=torch.int64, device=dev)
+        Cm = torch.zeros((m, ld), device=dev); R = torch.zeros((k, n), device=dev); W = torch.zeros((k, ld), device=dev)
+        P = torch.zeros((m, ld), device=dev); Q = torch.zeros((n, ld), device=dev)
+        s = torch.zeros(k, device=dev); r = torch.zeros(1, dtype=torch.int32, device=dev)
+        sig = torch.zeros(k, dtype=torch.float64, device=dev)
+        if fused:
+            C.cabs_pilot_embed(plan, At, k, 7, I, J, Cm, R, W, C.STABILIZED, 1e-12, P, Q, s, r, ws, sigma=sig)
+        else:
+            C.cabs_pilot(plan, At, k, 7, I, J, Cm, R, W, ws)
+            C.cabs_embed(plan, k, Cm, R, W, C.STABILIZED, 1e-12, P, Q, s, r, ws, sigma=sig)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in (I, J, Cm, R, W, P, Q, s, r, sig)])
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+
+
 def test_embed_drops_zero_norm_component_with_compaction(dev):
     """S:244 drop rule with a hole: component 0 extrapolates to zero, component 1 is kept,
     so the kept component must be compacted to position 0 (inconsistent triple, as in the
