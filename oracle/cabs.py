@@ -11,7 +11,8 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
 reference leg may import this module.  It shares no code with the CUDA path.
 
 Parity status per function:
-  gather, svd_w, sketch, embeddings, lloyd, snap, residual, cabs_run: pinned
+  gather, svd_w, sketch, embeddings, lloyd, snap, residual, cabs_run,
+  row_sq_norms, hard_threshold_select, hard_threshold_followup: pinned
   (tests/test_oracle_*.py).  residual_sampled (implicit source): parity unpinned
   beyond self-consistency (not on the round-1 path).
 """
@@ -319,6 +320,37 @@ def snap(X, centres, cluster_w):
 
 
 # --------------------------------------------------------------------------
+# Hard-threshold follow-up (P:312 variant (f))
+# --------------------------------------------------------------------------
+def row_sq_norms(X):
+    """||X_l||^2 per row, accumulated in float64 over the columns IN ORDER (Z26: the
+    ranking key of the hard threshold; with float32 inputs every square is exact in
+    float64, so the value is fixed by this summation order)."""
+    X = np.asarray(X, np.float64)
+    acc = np.zeros(X.shape[0])
+    for i in range(X.shape[1]):
+        acc = acc + X[:, i] * X[:, i]
+    return acc
+
+
+def hard_threshold_select(w, k):
+    """P:312 (f) "top-k samples with largest weighting coefficients (Eq. 6)", S:182-186:
+    the indices of the k largest w_l, ties to the lowest index, returned ascending."""
+    w = np.asarray(w, np.float64)
+    if not (1 <= k <= w.shape[0]):
+        raise ValueError("need 1 <= k <= len(w)")
+    order = sorted(range(w.shape[0]), key=lambda l: (-float(w[l]), l))
+    return np.sort(np.array(order[:k], dtype=np.int64))
+
+
+def hard_threshold_followup(X, k):
+    """Follow-up indices of variant (f) on an embedding X: the weighting coefficient
+    Upsilon(||X_l||) is monotone in ||X_l|| (Eq. 6; power Upsilon, p > 0), so its top-k is
+    the top-k of ||X_l||^2 (Z26)."""
+    return hard_threshold_select(row_sq_norms(X), k)
+
+
+# --------------------------------------------------------------------------
 # Residual  ||A - U diag(s) V^T||_F  (P:313) -- the evaluation step
 # --------------------------------------------------------------------------
 def residual(A, F, G, s=None, block=2048):
@@ -368,8 +400,9 @@ class CabsResult:
 
 def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
              weight_kind=WEIGHT_CONST, weight_p=2.0, I=None, J=None,
-             init_rows=None, init_cols=None, with_residual=True):
-    """Algorithm 2 plus the evaluation residual."""
+             init_rows=None, init_cols=None, with_residual=True, followup="kmeans"):
+    """Algorithm 2 plus the evaluation residual.  followup="hard"
+    replaces step 3 by the hard-threshold variant (f) of P:312 (km_* / snap_* are None)."""
     m, n = A.shape
     if not (1 <= k1 <= min(m, n)) or not (1 <= k2 <= min(m, n)):
         raise ValueError("need 1 <= k1, k2 <= min(m, n)")  # S:346
@@ -382,6 +415,17 @@ def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
     # step 2: pilot sketching, P = U S^1/2, Q = V S^1/2
     pilot = sketch(C, R, W, m, n, k1, mode, tol)
     P, Q = embeddings(pilot)
+    if followup == "hard":  # P:312 (f): top-k2 weighting coefficients on each side
+        Ib, Jb = hard_threshold_followup(P, k2), hard_threshold_followup(Q, k2)
+        Cb, Rb, Wb = gather(A, Ib, Jb)
+        follow = sketch(Cb, Rb, Wb, m, n, k2, mode, tol)
+        res = CabsResult(I=I, J=J, pilot=pilot, P=P, Q=Q, km_rows=None, km_cols=None,
+                         snap_rows=None, snap_cols=None, Ibar=Ib, Jbar=Jb, follow=follow)
+        if with_residual:
+            res.resid_sq, res.a_sq = residual(A, follow.U, follow.V, follow.s)
+        return res
+    if followup != "kmeans":
+        raise ValueError("followup must be 'kmeans' or 'hard'")
     # step 3: weighted k-means on P and Q, snap to in-sample points
     km_r = lloyd(P, k2, iters, weights(P, weight_kind, weight_p), init_idx=init_rows,
                  seed=seed, tag=rng.TAG_INIT_ROWS)
