@@ -304,6 +304,50 @@ def main():
         e2e = {"value": (cfg.m + cfg.n) / (e2e_t / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t}
 
+    # ---- the paper's follow-up variant (f) (hard threshold) on the same
+    # matrix: S6-S8 replaced by cabs_hard_select_pair; timed the same way (graph on one GPU)
+    variants = {}
+    hpipe = CabsPipeline(A, cfg.m, cfg.n, CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, followup="hard"),
+                         rank, world, comm=comm, plan=plan)
+    for _ in range(args.warmup):
+        hpipe.run()
+    hper = {}
+    for _ in range(min(args.steps, 3)):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        hpipe.run(timed=True)
+        for k_, v in hpipe.step_ms().items():
+            hper.setdefault(k_, []).append(v)
+    hgraph = None
+    if world == 1 and not args.eager:
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            hpipe.run()
+            hgraph, _ = hpipe.capture(stream=cap)
+        stream.wait_stream(cap)
+        torch.cuda.synchronize()
+    h_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        hgraph.replay() if hgraph is not None else hpipe.run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        h_ms.append(e0.elapsed_time(e1))
+    h_t = allreduce_max(sum(h_ms), world) / args.steps
+    hres = hpipe.results()
+    variants["hard_threshold"] = {
+        "followup": "P:312 variant (f): top-k2 weighting coefficients (cabs_hard_select_pair)",
+        "value": (cfg.m + cfg.n) / (h_t / 1e3), "unit": UNIT, "ms_per_step": h_t,
+        "breakdown_ms": {k_: allreduce_max(statistics.mean(v), world) for k_, v in hper.items()},
+        "rel_err_followup": math.sqrt(max(hres["resid_sq"], 0) / hres["a_sq"])}
+    del hpipe, hgraph
+
     if rank != 0:
         return 0
     peaks, peak_src = load_peaks()
@@ -360,6 +404,7 @@ def main():
         "quality": {"rel_err_followup": math.sqrt(max(res["resid_sq"], 0) / res["a_sq"]),
                     "near_ties_rows": int(res["tie_r"].sum()), "near_ties_cols": int(res["tie_c"].sum())},
     }
+    line["variants"] = variants
     if e2e:
         line["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1:

@@ -243,6 +243,38 @@ typedef struct cabs_sel_problem {
 int32_t cabs_select_pair(const cabs_plan* plan, const cabs_sel_problem* a, const cabs_sel_problem* b,
                          void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream);
 
+/* ---------------------------------------------------------------- S8' hard threshold
+ * The paper's follow-up variant (f) ("top-k samples with largest weighting
+ * coefficients (Equation eq:wkmeans)"), replacing S6-S8: the k2 points of
+ * the embedding X (n_loc local rows of n_glob, global index = row_off + local, d columns,
+ * ldx) with the largest Upsilon(||X_l||).  Upsilon is monotone, so the key is ||X_l||^2,
+ * the FP64 sum of the exact squares of the FP32 entries in column order (Z26);
+ * ties -> lowest global index.  Outputs: reps (device int64[k2], ascending: the follow-up
+ * index set), keys (device double[n_loc] or NULL: the local keys).  Multi-rank: one
+ * sum-allreduce of 2 * nranks * k2 doubles; every rank receives the same reps.
+ * Errors: k2 < 1, k2 > kmax or k2 > n_glob, bad dims -> INVALID_ARG; a non-finite key sets
+ * CABS_DEV_NONFINITE (NaN keys rank below every finite key). */
+int32_t cabs_hard_select(const cabs_plan* plan, const float* X, int64_t ldx, int64_t n_loc,
+                         int64_t n_glob, int64_t row_off, int32_t d, int32_t k2, int64_t* reps,
+                         double* keys, void* ws, size_t ws_bytes, const cabs_comm* comm,
+                         void* stream);
+
+/* One side of cabs_hard_select_pair: the arguments of cabs_hard_select. */
+typedef struct cabs_hard_problem {
+  const float* X;               /* device n_loc x ldx */
+  int64_t ldx, n_loc, n_glob, row_off;
+  int32_t d, k2;
+  int64_t* reps;                /* device int64[k2] (out, ascending) */
+  double* keys;                 /* device double[n_loc] (out) or NULL */
+} cabs_hard_problem;
+
+/* Variant (f) for BOTH sides: exactly cabs_hard_select(a) and cabs_hard_select(b) (same
+ * results); on a single GPU the two sides share one key launch and one top-k launch (one
+ * CTA per side).  Multi-rank runs them one after the other.  Errors as cabs_hard_select. */
+int32_t cabs_hard_select_pair(const cabs_plan* plan, const cabs_hard_problem* a,
+                              const cabs_hard_problem* b, void* ws, size_t ws_bytes,
+                              const cabs_comm* comm, void* stream);
+
 /* ---------------------------------------------------------------- S9 sketch
  * Follow-up sketching, or a sketch from any given index sets:
  * gathers Cbar = A(:,Ic), Rbar = A(Ir,:), Wbar = A(Ir,Ic) (Ir, Ic: device int64[k],

@@ -82,6 +82,12 @@ class SelProblem(ctypes.Structure):
                 ("reps", c_vp), ("rep_of_centre", c_vp), ("gap", c_vp)]
 
 
+class HardProblem(ctypes.Structure):
+    """cabs_hard_problem: one side (rows or columns) of cabs_hard_select_pair."""
+    _fields_ = [("X", c_vp), ("ldx", c_i64), ("n_loc", c_i64), ("n_glob", c_i64), ("row_off", c_i64),
+                ("d", c_i32), ("k2", c_i32), ("reps", c_vp), ("keys", c_vp)]
+
+
 _SIGS = {
     "cabs_status_string": (ctypes.c_char_p, [c_i32]),
     "cabs_last_error_string": (ctypes.c_char_p, []),
@@ -109,6 +115,10 @@ _SIGS = {
                             c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_select_pair": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(SelProblem), ctypes.POINTER(SelProblem), c_vp,
                                  c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_hard_select": (c_i32, [ctypes.POINTER(Plan), c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_vp,
+                                 c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_hard_select_pair": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(HardProblem),
+                                      ctypes.POINTER(HardProblem), c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_sketch": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_vp, c_vp, c_i32, c_i32, c_f64,
                             c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz,
                             ctypes.POINTER(Comm), c_vp]),
@@ -282,6 +292,24 @@ def sel_problem(X, n_loc, n_glob, row_off, d, centres, k2, cluster_w, reps, rep_
 def cabs_select_pair(plan, a, b, ws, comm=None, stream=None):
     _check(load().cabs_select_pair(ctypes.byref(plan), ctypes.byref(a), ctypes.byref(b), _p(ws), ws.numel(),
                                    _comm(comm), _stream(stream)), "cabs_select_pair")
+
+
+def cabs_hard_select(plan, X, n_loc, n_glob, row_off, d, k2, reps, ws, keys=None, comm=None, stream=None):
+    _check(load().cabs_hard_select(ctypes.byref(plan), _p(X), _ld(X), int(n_loc), int(n_glob), int(row_off),
+                                   int(d), int(k2), _p(reps), _p(keys), _p(ws), ws.numel(), _comm(comm),
+                                   _stream(stream)), "cabs_hard_select")
+
+
+def hard_problem(X, n_loc, n_glob, row_off, d, k2, reps, keys=None):
+    """Describe one side of cabs_hard_select_pair (tensors must outlive the call)."""
+    def ptr(t):
+        return None if t is None else t.data_ptr()
+    return HardProblem(ptr(X), _ld(X), int(n_loc), int(n_glob), int(row_off), int(d), int(k2), ptr(reps), ptr(keys))
+
+
+def cabs_hard_select_pair(plan, a, b, ws, comm=None, stream=None):
+    _check(load().cabs_hard_select_pair(ctypes.byref(plan), ctypes.byref(a), ctypes.byref(b), _p(ws), ws.numel(),
+                                        _comm(comm), _stream(stream)), "cabs_hard_select_pair")
 
 
 def cabs_sketch(plan, A, Ir, Ic, k, mode, tol, U, s, V, r, ws, sigma=None, comm=None, stream=None):

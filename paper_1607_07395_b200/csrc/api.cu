@@ -588,6 +588,103 @@ int32_t cabs_select_pair(const cabs_plan* plan, const cabs_sel_problem* a, const
   return ra != CABS_OK ? ra : rb;
 }
 
+// ---------------------------------------------------------------- S8' hard threshold (P:312 (f))
+static int32_t hard_check(const cabs_plan* plan, const Ws& L, const cabs_hard_problem& p) {
+  if (p.k2 < 1 || p.k2 > plan->kmax || p.k2 > p.n_glob) return arg_error("hard_select: bad k2");
+  if (p.d < 1 || p.ldx < p.d || p.n_loc < 0 || p.n_loc > L.Nmax || p.row_off < 0 || p.row_off + p.n_loc > p.n_glob)
+    return arg_error("hard_select: bad dims");
+  if (!p.reps || (p.n_loc > 0 && !p.X)) return arg_error("hard_select: bad buffers");
+  return CABS_OK;
+}
+
+static cabsk::HardSide hard_side(const cabs_hard_problem& p) {
+  cabsk::HardSide h{};
+  h.X = p.X;
+  h.ldx = p.ldx;
+  h.N = p.n_loc;
+  h.d = p.d;
+  h.key = p.keys;  // NULL: keys are not stored
+  h.ks = 1;
+  h.off = p.row_off;
+  h.k = p.k2;
+  return h;
+}
+
+// top-k over the (key, index) candidate pairs at c (n candidates)
+static cabsk::HardSide hard_merge_side(double* c, int64_t n, int k, int64_t* out, double* slot) {
+  cabsk::HardSide h{};
+  h.key = c;
+  h.ks = 2;
+  h.cidx = c + 1;
+  h.N = n;
+  h.k = k;
+  h.out = out;
+  h.slot = slot;
+  return h;
+}
+
+// nprob problems (1 or 2); single GPU: one key + local top-k launch and one merge launch
+static int32_t hard_run(const cabs_hard_problem* const* pr, int nprob, void* ws, const Ws& L, const cabs_comm* comm,
+                        void* stream) {
+  cudaStream_t st = S(stream);
+  double* cand = wsp<double>(ws, L.hcand);
+  if (!multi(comm)) {
+    cabsk::HardArgs a{}, m{};
+    for (int q = 0; q < nprob; ++q) {
+      const cabs_hard_problem& p = *pr[q];
+      a.s[q] = hard_side(p);
+      m.s[q] = hard_merge_side(cand + q * L.hcand_side, hard_local_blocks(p.n_loc) * p.k2, p.k2, p.reps, nullptr);
+    }
+    launch_hard_local(a, nprob, cand, L.hcand_side, ws, st);
+    launch_hard_topk(m, nprob, st);
+    CABS_LAUNCH_CHECK("hard_select");
+    return CABS_OK;
+  }
+  // multi-rank, one problem after the other: this rank's winners go to its slot of a zeroed
+  // [nranks][k2] (key, index) buffer, one sum-allreduce, then the top-k2 of those candidates
+  double* all = wsp<double>(ws, L.cand_all);
+  for (int q = 0; q < nprob; ++q) {
+    const cabs_hard_problem& p = *pr[q];
+    const int64_t nall = 2LL * comm->nranks * p.k2;
+    CABS_CUDA_TRY(cudaMemsetAsync(all, 0, sizeof(double) * nall, st));
+    cabsk::HardArgs a{}, m{}, f{};
+    a.s[0] = hard_side(p);
+    m.s[0] = hard_merge_side(cand, hard_local_blocks(p.n_loc) * p.k2, p.k2, nullptr, all + 2LL * comm->rank * p.k2);
+    launch_hard_local(a, 1, cand, L.hcand_side, ws, st);
+    launch_hard_topk(m, 1, st);
+    CABS_LAUNCH_CHECK("hard_select local");
+    CABS_TRY(comm_f64(comm, all, nall, stream));
+    f.s[0] = hard_merge_side(all, (int64_t)comm->nranks * p.k2, p.k2, p.reps, nullptr);
+    launch_hard_topk(f, 1, st);
+    CABS_LAUNCH_CHECK("hard_select merge");
+  }
+  return CABS_OK;
+}
+
+int32_t cabs_hard_select(const cabs_plan* plan, const float* X, int64_t ldx, int64_t n_loc, int64_t n_glob,
+                         int64_t row_off, int32_t d, int32_t k2, int64_t* reps, double* keys, void* ws,
+                         size_t ws_bytes, const cabs_comm* comm, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  const cabs_hard_problem p{X, ldx, n_loc, n_glob, row_off, d, k2, reps, keys};
+  CABS_TRY(hard_check(plan, L, p));
+  const cabs_hard_problem* pr[1] = {&p};
+  return hard_run(pr, 1, ws, L, comm, stream);
+}
+
+int32_t cabs_hard_select_pair(const cabs_plan* plan, const cabs_hard_problem* a, const cabs_hard_problem* b, void* ws,
+                              size_t ws_bytes, const cabs_comm* comm, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  if (!a || !b) return arg_error("hard_select_pair: null problem");
+  CABS_TRY(hard_check(plan, L, *a));
+  CABS_TRY(hard_check(plan, L, *b));
+  const cabs_hard_problem* pr[2] = {a, b};
+  return hard_run(pr, 2, ws, L, comm, stream);
+}
+
 // ---------------------------------------------------------------- S10
 int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float* F, int64_t ldf, const float* s,
                       const float* G, int64_t ldg, int32_t ncomp, double* out, void* ws, size_t ws_bytes,

@@ -17,6 +17,7 @@ constexpr int kAssignGrid = 4 * kNumSM;
 constexpr int kResGrid = 8 * kNumSM;  // persistent residual CTAs (upper bound)
 constexpr int kNormTile = 64;         // points per embed-GEMM tile (norm partial rows)
 constexpr int kKmItersCap = 256;      // Lloyd iterations the persistent kernel's scratch covers
+constexpr int kHardLocalRows = 2048;  // rows per CTA of the hard-threshold key + local top-k kernel
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
@@ -30,9 +31,10 @@ struct Ws {
   size_t km_scr_bytes;                                     // per problem
   size_t dist, cand_d, cand_i, cand_all;  // snap scratch of problem slot 0 ...
   size_t dist2, cand_d2, cand_i2, cand_all2;  // ... and slot 1 (cabs_select_pair)
-  size_t idx;
+  size_t hcand, idx;
   size_t cb, rb, wb;
   size_t res_part, res_split;  // res_split: G_hi, G_lo (n x 64 each)
+  size_t hcand_side;
   size_t total;
   // dims
   int64_t K, Kp, m_loc, n_sl, Nmax, n, ldrb, npt;
@@ -87,6 +89,9 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.cand_d2 = take(sizeof(float) * K * kSnapTMulti);
   w.cand_i2 = take(sizeof(int64_t) * K * kSnapTMulti);
   w.cand_all2 = take(sizeof(double) * 2 * nr * kSnapSeg * K * kSnapTMulti);
+  // hard threshold: (key, index) candidates of every 2048-row CTA, both sides of a pair
+  w.hcand_side = 2 * ceil_div(w.Nmax, kHardLocalRows) * K;  // doubles per side
+  w.hcand = take(sizeof(double) * 2 * w.hcand_side);
   w.idx = take(sizeof(int64_t) * 8 * Kp);
   w.cb = take(sizeof(float) * (w.m_loc > 0 ? w.m_loc : 1) * Kp);
   w.rb = take(sizeof(float) * K * w.ldrb);

@@ -103,6 +103,27 @@ void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int 
                         const float* D, int64_t ldd, int64_t N, int64_t row_off, bool can_rescan,
                         int64_t* rep_of_centre, float* gap, int64_t* reps_sorted, void* ws, cudaStream_t st);
 
+// hard.cu -- one side (rows or columns) of the hard-threshold selection; up to two per launch
+struct HardSide {
+  const float* X;      // keys kernel: N x d embedding (ldx)
+  int64_t ldx, N;      // N: points (keys kernel) / candidates (top-k kernel)
+  int d;
+  double* key;         // keys kernel output; top-k input key[l * ks]
+  int64_t ks;
+  const double* cidx;  // top-k: candidate indices at cidx[l * ks], or NULL (index = off + l)
+  int64_t off;
+  int64_t* out;        // top-k: winners ascending (or NULL)
+  double* slot;        // top-k: (key, index) pairs of the winners, (-1, -1) padding (or NULL)
+  int k;               // top-k: winners wanted (min(k, N) taken)
+};
+struct HardArgs {
+  HardSide s[2];
+  int nb0;  // local kernel: blocks of side 0 (set by the launcher)
+};
+int64_t hard_local_blocks(int64_t N);
+void launch_hard_local(const HardArgs& a, int nside, double* cand, int64_t side_stride, void* ws, cudaStream_t st);
+void launch_hard_topk(const HardArgs& a, int nside, cudaStream_t st);
+
 // residual.cu
 int launch_residual(const float* A, int64_t lda, int64_t m_loc, int64_t n, const float* F, int64_t ldf, const float* s,
                     const float* G, int64_t ldg, int ncomp, double* part, double* out, cudaStream_t st);

@@ -7,6 +7,8 @@ entry points of libcabs.so in order on one stream:
   S4-S5 cabs_embed    pilot sketch -> embeddings P, Q
   S6-S7 cabs_kmeans_pair  weighted Lloyd on P (rows) and on Q (columns), one kernel  (Eq. 6)
   S8    cabs_select_pair   snap centres to in-sample rows / columns
+  (f)   cabs_hard_select   instead of S6-S8 when cfg.followup == "hard": top-k2 weighting
+                           coefficients per side (P:312 variant (f))
   S9    cabs_sketch   follow-up gathers + sketch -> Ubar, sbar, Vbar
   S10   cabs_residual ||A - Ubar diag(sbar) Vbar^T||_F^2, ||A||_F^2
 
@@ -32,9 +34,11 @@ class CabsConfig:
     tol: float = 1e-12
     weight_kind: int = C.WEIGHT_CONST
     weight_p: float = 2.0
+    followup: str = "kmeans"  # "kmeans" (Alg. 2 step 3) or "hard" (P:312 variant (f))
 
 
 STEPS = ("pilot_embed", "kmeans", "select", "sketch", "residual")
+STEPS_HARD = ("pilot_embed", "hard_select", "sketch", "residual")
 
 
 class CabsPipeline:
@@ -109,6 +113,13 @@ class CabsPipeline:
                              rep_of_centre=self.rep_c, gap=self.gap_c)
         C.cabs_select_pair(p, rows, cols, self.ws, comm=self.comm)
 
+    def hard_select(self):
+        """P:312 variant (f): the k2 rows / columns with the largest weighting coefficients."""
+        c, p = self.cfg, self.plan
+        rows = C.hard_problem(self.P, p.m_loc, p.m, p.row_begin, c.k1, c.k2, self.Ib)
+        cols = C.hard_problem(self.Q, p.n_sl, p.n, p.col_begin, c.k1, c.k2, self.Jb)
+        C.cabs_hard_select_pair(p, rows, cols, self.ws, comm=self.comm)
+
     def sketch(self):
         c, p = self.cfg, self.plan
         C.cabs_sketch(p, self.A, self.Ib, self.Jb, c.k2, c.mode, c.tol, self.U, self.s2, self.V, self.r2,
@@ -125,20 +136,29 @@ class CabsPipeline:
     # ------------------------------------------------------------------ whole path
     def run(self, with_residual=True, timed=False, init_rows=None, init_cols=None):
         """One pass of the hot path, stream-ordered; returns per-step CUDA events if timed."""
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(STEPS) + 1)] if timed else None
+        hard = self.cfg.followup == "hard"
+        if self.cfg.followup not in ("kmeans", "hard"):
+            raise ValueError("followup must be 'kmeans' or 'hard'")
+        steps = STEPS_HARD if hard else STEPS
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(steps) + 1)] if timed else None
+        e = iter(ev[1:]) if timed else None
         if timed:
             ev[0].record()
         self.pilot_embed()
-        timed and ev[1].record()
-        self.kmeans(init_rows, init_cols)
-        timed and ev[2].record()
-        self.select()
-        timed and ev[3].record()
+        timed and next(e).record()
+        if hard:
+            self.hard_select()
+            timed and next(e).record()
+        else:
+            self.kmeans(init_rows, init_cols)
+            timed and next(e).record()
+            self.select()
+            timed and next(e).record()
         self.sketch()
-        timed and ev[4].record()
+        timed and next(e).record()
         if with_residual:
             self.residual()
-        timed and ev[5].record()
+        timed and next(e).record()
         self.events = ev
         return ev
 
@@ -159,7 +179,8 @@ class CabsPipeline:
         """Per-step milliseconds of the last timed run (synchronises)."""
         ev = self.events
         torch.cuda.synchronize()
-        return {s: ev[i].elapsed_time(ev[i + 1]) for i, s in enumerate(STEPS)}
+        steps = STEPS_HARD if self.cfg.followup == "hard" else STEPS
+        return {s: ev[i].elapsed_time(ev[i + 1]) for i, s in enumerate(steps)}
 
     def results(self):
         """Host copies of everything the parity tests compare."""
