@@ -201,6 +201,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the variant (f) timing")
     ap.add_argument("--eager", action="store_true", help="time stream-ordered launches instead of the CUDA graph")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -307,19 +308,19 @@ def main():
     # ---- the paper's follow-up variant (f) (hard threshold) on the same
     # matrix: S6-S8 replaced by cabs_hard_select_pair; timed the same way (graph on one GPU)
     variants = {}
-    hpipe = CabsPipeline(A, cfg.m, cfg.n, CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, followup="hard"),
+    hpipe = None if args.no_variants else CabsPipeline(A, cfg.m, cfg.n, CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, followup="hard"),
                          rank, world, comm=comm, plan=plan)
-    for _ in range(args.warmup):
+    for _ in range(args.warmup if hpipe else 0):
         hpipe.run()
     hper = {}
-    for _ in range(min(args.steps, 3)):
+    for _ in range(min(args.steps, 3) if hpipe else 0):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         hpipe.run(timed=True)
         for k_, v in hpipe.step_ms().items():
             hper.setdefault(k_, []).append(v)
     hgraph = None
-    if world == 1 and not args.eager:
+    if hpipe and world == 1 and not args.eager:
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)
         with torch.cuda.stream(cap):
@@ -328,7 +329,7 @@ def main():
         stream.wait_stream(cap)
         torch.cuda.synchronize()
     h_ms = []
-    for _ in range(args.steps):
+    for _ in range(args.steps if hpipe else 0):
         flush.fill_(1.0)
         barrier(world)
         torch.cuda.synchronize()
@@ -339,13 +340,14 @@ def main():
         torch.cuda.synchronize()
         barrier(world)
         h_ms.append(e0.elapsed_time(e1))
-    h_t = allreduce_max(sum(h_ms), world) / args.steps
-    hres = hpipe.results()
-    variants["hard_threshold"] = {
-        "followup": "P:312 variant (f): top-k2 weighting coefficients (cabs_hard_select_pair)",
-        "value": (cfg.m + cfg.n) / (h_t / 1e3), "unit": UNIT, "ms_per_step": h_t,
-        "breakdown_ms": {k_: allreduce_max(statistics.mean(v), world) for k_, v in hper.items()},
-        "rel_err_followup": math.sqrt(max(hres["resid_sq"], 0) / hres["a_sq"])}
+    if hpipe:
+        h_t = allreduce_max(sum(h_ms), world) / args.steps
+        hres = hpipe.results()
+        variants["hard_threshold"] = {
+            "followup": "P:312 variant (f): top-k2 weighting coefficients (cabs_hard_select_pair)",
+            "value": (cfg.m + cfg.n) / (h_t / 1e3), "unit": UNIT, "ms_per_step": h_t,
+            "breakdown_ms": {k_: allreduce_max(statistics.mean(v), world) for k_, v in hper.items()},
+            "rel_err_followup": math.sqrt(max(hres["resid_sq"], 0) / hres["a_sq"])}
     del hpipe, hgraph
 
     if rank != 0:
