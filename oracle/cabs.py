@@ -12,7 +12,8 @@ reference leg may import this module.  It shares no code with the CUDA path.
 
 Parity status per function:
   gather, svd_w, sketch, embeddings, lloyd, snap, residual, cabs_run,
-  row_sq_norms, hard_threshold_select, hard_threshold_followup: pinned
+  row_sq_norms, hard_threshold_select, hard_threshold_followup, orthogonalize,
+  leverage_scores, leverage_sample: pinned
   (tests/test_oracle_*.py).  residual_sampled (implicit source): parity unpinned
   beyond self-consistency (not on the round-1 path).
 """
@@ -351,6 +352,43 @@ def hard_threshold_followup(X, k):
 
 
 # --------------------------------------------------------------------------
+# Orthogonalization (Supp. section 3) and the leverage-score follow-up
+# (P:312 variant (e))
+# --------------------------------------------------------------------------
+def orthogonalize(U, s, V):
+    """Supp. section 3, step by step: U = U0 S0 V0^T (thin SVD); then
+    S0 V0^T diag(s) V^T = U1 S1 V1^T; the result is (U0 U1, S1, V1), i.e. A ~ (U0 U1) S1 V1^T.
+    Components with S1 <= tol * S1_max (Z4's rule) are dropped (a rank-deficient input)."""
+    U = np.asarray(U, np.float64)
+    V = np.asarray(V, np.float64)
+    s = np.asarray(s, np.float64)
+    U0, S0, V0t = np.linalg.svd(U, full_matrices=False)
+    B = (S0[:, None] * V0t) @ (s[:, None] * V.T)
+    U1, S1, V1t = np.linalg.svd(B, full_matrices=False)
+    keep = S1 > DEFAULT_TOL * S1[0] if S1.size and S1[0] > 0 else np.zeros(S1.size, dtype=bool)
+    return U0 @ U1[:, keep], S1[keep], V1t[keep].T
+
+
+def leverage_scores(F):
+    """Approximate leverage scores l_i = ||F_i||^2 / r of a factor with orthonormal columns
+    (P:312 (e)); r = number of columns.  ||F_i||^2 as in row_sq_norms."""
+    F = np.asarray(F, np.float64)
+    return row_sq_norms(F) / F.shape[1]
+
+
+def leverage_sample(F, k, seed, tag):
+    """k distinct indices drawn without replacement with probability proportional to the
+    leverage scores, as Efraimidis-Spirakis keys: point l gets the key
+    l_l / (-log u_l) with u_l = rng.uniform01(seed, tag, l) (the ranking of u^(1/l_l)); the k
+    largest keys win (ties -> lowest index), returned ascending (Z27)."""
+    w = leverage_scores(F)
+    if not (1 <= k <= int(np.count_nonzero(w))):
+        raise ValueError("need 1 <= k <= number of nonzero leverage scores")
+    u = rng.uniform01(seed, tag, np.arange(w.shape[0]))
+    return hard_threshold_select(w / -np.log(u), k)
+
+
+# --------------------------------------------------------------------------
 # Residual  ||A - U diag(s) V^T||_F  (P:313) -- the evaluation step
 # --------------------------------------------------------------------------
 def residual(A, F, G, s=None, block=2048):
@@ -401,8 +439,8 @@ class CabsResult:
 def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
              weight_kind=WEIGHT_CONST, weight_p=2.0, I=None, J=None,
              init_rows=None, init_cols=None, with_residual=True, followup="kmeans"):
-    """Algorithm 2 plus the evaluation residual.  followup="hard"
-    replaces step 3 by the hard-threshold variant (f) of P:312 (km_* / snap_* are None)."""
+    """Algorithm 2 plus the evaluation residual.  followup="hard" /
+    "leverage" replaces step 3 by the paper's variant (f) / (e) of P:312 (km_* / snap_* are None)."""
     m, n = A.shape
     if not (1 <= k1 <= min(m, n)) or not (1 <= k2 <= min(m, n)):
         raise ValueError("need 1 <= k1, k2 <= min(m, n)")  # S:346
@@ -424,8 +462,19 @@ def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
         if with_residual:
             res.resid_sq, res.a_sq = residual(A, follow.U, follow.V, follow.s)
         return res
+    if followup == "leverage":  # P:312 (e): orthogonalize the pilot (Supp. 3), sample by leverage
+        Uo, so, Vo = orthogonalize(pilot.U, pilot.s, pilot.V)
+        Ib = leverage_sample(Uo, k2, seed, rng.TAG_LEVERAGE_ROWS)
+        Jb = leverage_sample(Vo, k2, seed, rng.TAG_LEVERAGE_COLS)
+        Cb, Rb, Wb = gather(A, Ib, Jb)
+        follow = sketch(Cb, Rb, Wb, m, n, k2, mode, tol)
+        res = CabsResult(I=I, J=J, pilot=pilot, P=P, Q=Q, km_rows=None, km_cols=None,
+                         snap_rows=None, snap_cols=None, Ibar=Ib, Jbar=Jb, follow=follow)
+        if with_residual:
+            res.resid_sq, res.a_sq = residual(A, follow.U, follow.V, follow.s)
+        return res
     if followup != "kmeans":
-        raise ValueError("followup must be 'kmeans' or 'hard'")
+        raise ValueError("followup must be 'kmeans', 'hard' or 'leverage'")
     # step 3: weighted k-means on P and Q, snap to in-sample points
     km_r = lloyd(P, k2, iters, weights(P, weight_kind, weight_p), init_idx=init_rows,
                  seed=seed, tag=rng.TAG_INIT_ROWS)

@@ -30,6 +30,8 @@ TAG_PILOT_COLS = 2
 TAG_INIT_ROWS = 3
 TAG_INIT_COLS = 4
 TAG_RESIDUAL_PAIRS = 5
+TAG_LEVERAGE_ROWS = 6
+TAG_LEVERAGE_COLS = 7
 
 
 def philox4x32_10(ctr, key):
@@ -133,3 +135,17 @@ def floyd(N: int, k: int, seed: int, tag: int) -> np.ndarray:
         t = bounded(stream, j + 1)
         chosen.add(j if t in chosen else t)
     return np.array(sorted(chosen), dtype=np.int64)
+
+
+def uniform01(seed: int, tag: int, idx) -> np.ndarray:
+    """Per-point uniform in (0, 1): Philox block of counter
+    (idx mod 2^32, idx >> 32, tag, 1) -> words w0, w1; u = ((w0 >> 5) 2^26 + (w1 >> 6) + 1/2) 2^-53
+    (53 random bits, exact in float64, never 0 or 1).  Counter word 3 = 1 keeps these blocks
+    apart from the sequential word stream (word 3 = 0)."""
+    idx = np.asarray(idx, dtype=np.uint64)
+    k0, k1 = seed_key(seed)
+    w0, w1, _, _ = philox4x32_10_np(idx & np.uint64(M32), idx >> np.uint64(32), np.uint64(int(tag) & M32),
+                                     np.uint64(1), k0, k1)
+    a = (w0 >> np.uint64(5)).astype(np.float64)
+    b = (w1 >> np.uint64(6)).astype(np.float64)
+    return (a * 67108864.0 + b + 0.5) * 2.0 ** -53
