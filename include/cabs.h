@@ -69,6 +69,7 @@ typedef enum {
 #define CABS_DEV_SNAP_EXHAUSTED 0x8u /* multi-GPU snap ran out of candidates */
 #define CABS_DEV_TOO_FEW_POINTS 0x10u /* fewer than k2 points with nonzero weight */
 #define CABS_DEV_SVD_NOCONV 0x20u    /* Jacobi SVD hit its sweep cap */
+#define CABS_DEV_ORTH_RANK 0x40u     /* cabs_orthogonalize: a factor is rank-deficient (Cholesky pivot <= 0) */
 
 typedef enum {
   CABS_STABILIZED = 0,     /* the paper's routine: U = C V_w N_c^-1, V = R^T U_w N_r^-1,
@@ -274,6 +275,41 @@ typedef struct cabs_hard_problem {
 int32_t cabs_hard_select_pair(const cabs_plan* plan, const cabs_hard_problem* a,
                               const cabs_hard_problem* b, void* ws, size_t ws_bytes,
                               const cabs_comm* comm, void* stream);
+
+/* ---------------------------------------------------------------- variant (e): leverage
+ * Orthogonalization of a sketch (Supp. section 3): given A ~ U diag(s) V^T
+ * (U: this rank's m_loc x r rows, ldu; V: this rank's column slice, n_sl x r, ldv; s:
+ * device float[r] or NULL = ones), writes the thin SVD of that product, A ~ Uo diag(so)
+ * Vo^T with orthonormal Uo, Vo (the paper's (U0 U1, S1, V1), unique up to signs; canonical
+ * signs as Z5), so descending, components with so_j <= 1e-12 so_1 dropped (zero columns,
+ * r_out = kept count).  Computed as Gram matrices (one allreduce of 2 x 64 x 64 doubles
+ * across ranks), FP64 Cholesky, the FP64 Jacobi SVD of the r x r core, and one pass over U
+ * and V.  Errors: r < 1, r > 64 or r > kmax, ld < r -> INVALID_ARG; all-zero columns (the zero
+ * padding beyond a truncated rank) drop out; a numerically rank-deficient U or V (negative
+ * Cholesky pivot) sets CABS_DEV_ORTH_RANK.  sigma: device double[r] or NULL.  Uo may not alias U. */
+int32_t cabs_orthogonalize(const cabs_plan* plan, int32_t r, const float* U, int64_t ldu,
+                           const float* s, const float* V, int64_t ldv, float* Uo, int64_t lduo,
+                           float* so, float* Vo, int64_t ldvo, int32_t* r_out, double* sigma,
+                           void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream);
+
+/* Leverage-score follow-up (P:312 variant (e); Z27): k2 distinct
+ * points of the orthonormal factor F (n_loc local rows of n_glob, global index = row_off +
+ * local, r columns, ldf) drawn without replacement with probability proportional to the
+ * scores l = ||F_l||^2 / r: the k2 largest Efraimidis-Spirakis keys l / (-log u_l), u_l the
+ * per-point Philox uniform of (seed, tag, global index); ties ->
+ * lowest index; reps ascending; keys (double[n_loc] or NULL) receives the keys.  Errors and
+ * multi-rank behaviour as cabs_hard_select. */
+int32_t cabs_leverage_select(const cabs_plan* plan, const float* F, int64_t ldf, int64_t n_loc,
+                             int64_t n_glob, int64_t row_off, int32_t r, int32_t k2, uint64_t seed,
+                             uint32_t tag, int64_t* reps, double* keys, void* ws, size_t ws_bytes,
+                             const cabs_comm* comm, void* stream);
+
+/* Both sides at once (a: rows with tag_a, b: columns with tag_b; the d field of each
+ * problem is its r): one key launch and one merge launch on a single GPU. */
+int32_t cabs_leverage_select_pair(const cabs_plan* plan, const cabs_hard_problem* a,
+                                  const cabs_hard_problem* b, uint64_t seed, uint32_t tag_a,
+                                  uint32_t tag_b, void* ws, size_t ws_bytes, const cabs_comm* comm,
+                                  void* stream);
 
 /* ---------------------------------------------------------------- S9 sketch
  * Follow-up sketching, or a sketch from any given index sets:

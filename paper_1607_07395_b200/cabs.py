@@ -35,6 +35,7 @@ DEV_TOO_FEW_POINTS = 0x10
 DEV_SVD_NOCONV = 0x20
 
 TAG_PILOT_ROWS, TAG_PILOT_COLS, TAG_INIT_ROWS, TAG_INIT_COLS = 1, 2, 3, 4
+TAG_LEVERAGE_ROWS, TAG_LEVERAGE_COLS = 6, 7
 
 
 class CabsError(RuntimeError):
@@ -119,6 +120,13 @@ _SIGS = {
                                  c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_hard_select_pair": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(HardProblem),
                                       ctypes.POINTER(HardProblem), c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_orthogonalize": (c_i32, [ctypes.POINTER(Plan), c_i32, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
+                                   c_vp, c_i64, c_vp, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_leverage_select": (c_i32, [ctypes.POINTER(Plan), c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_u64,
+                                     c_u32, c_vp, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_leverage_select_pair": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(HardProblem),
+                                          ctypes.POINTER(HardProblem), c_u64, c_u32, c_u32, c_vp, c_sz,
+                                          ctypes.POINTER(Comm), c_vp]),
     "cabs_sketch": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_vp, c_vp, c_i32, c_i32, c_f64,
                             c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz,
                             ctypes.POINTER(Comm), c_vp]),
@@ -310,6 +318,25 @@ def hard_problem(X, n_loc, n_glob, row_off, d, k2, reps, keys=None):
 def cabs_hard_select_pair(plan, a, b, ws, comm=None, stream=None):
     _check(load().cabs_hard_select_pair(ctypes.byref(plan), ctypes.byref(a), ctypes.byref(b), _p(ws), ws.numel(),
                                         _comm(comm), _stream(stream)), "cabs_hard_select_pair")
+
+
+def cabs_orthogonalize(plan, r, U, s, V, Uo, so, Vo, ws, r_out=None, sigma=None, comm=None, stream=None):
+    _check(load().cabs_orthogonalize(ctypes.byref(plan), int(r), _p(U), _ld(U), _p(s), _p(V), _ld(V), _p(Uo), _ld(Uo),
+                                     _p(so), _p(Vo), _ld(Vo), _p(r_out), _p(sigma), _p(ws), ws.numel(), _comm(comm),
+                                     _stream(stream)), "cabs_orthogonalize")
+
+
+def cabs_leverage_select(plan, F, n_loc, n_glob, row_off, r, k2, seed, tag, reps, ws, keys=None, comm=None,
+                         stream=None):
+    _check(load().cabs_leverage_select(ctypes.byref(plan), _p(F), _ld(F), int(n_loc), int(n_glob), int(row_off),
+                                       int(r), int(k2), int(seed), int(tag), _p(reps), _p(keys), _p(ws), ws.numel(),
+                                       _comm(comm), _stream(stream)), "cabs_leverage_select")
+
+
+def cabs_leverage_select_pair(plan, a, b, seed, tag_a, tag_b, ws, comm=None, stream=None):
+    _check(load().cabs_leverage_select_pair(ctypes.byref(plan), ctypes.byref(a), ctypes.byref(b), int(seed),
+                                            int(tag_a), int(tag_b), _p(ws), ws.numel(), _comm(comm),
+                                            _stream(stream)), "cabs_leverage_select_pair")
 
 
 def cabs_sketch(plan, A, Ir, Ic, k, mode, tol, U, s, V, r, ws, sigma=None, comm=None, stream=None):

@@ -625,14 +625,20 @@ static cabsk::HardSide hard_merge_side(double* c, int64_t n, int k, int64_t* out
 
 // nprob problems (1 or 2); single GPU: one key + local top-k launch and one merge launch
 static int32_t hard_run(const cabs_hard_problem* const* pr, int nprob, void* ws, const Ws& L, const cabs_comm* comm,
-                        void* stream) {
+                        void* stream, int mode = 0, uint64_t seed = 0, const uint32_t* tags = nullptr) {
   cudaStream_t st = S(stream);
+  auto keyed = [&](cabsk::HardSide h, int q) {  // the key of the local kernel: (f) or leverage (e)
+    h.mode = mode;
+    h.seed = seed;
+    h.tag = tags ? tags[q] : 0u;
+    return h;
+  };
   double* cand = wsp<double>(ws, L.hcand);
   if (!multi(comm)) {
     cabsk::HardArgs a{}, m{};
     for (int q = 0; q < nprob; ++q) {
       const cabs_hard_problem& p = *pr[q];
-      a.s[q] = hard_side(p);
+      a.s[q] = keyed(hard_side(p), q);
       m.s[q] = hard_merge_side(cand + q * L.hcand_side, hard_local_blocks(p.n_loc) * p.k2, p.k2, p.reps, nullptr);
     }
     launch_hard_local(a, nprob, cand, L.hcand_side, ws, st);
@@ -648,7 +654,7 @@ static int32_t hard_run(const cabs_hard_problem* const* pr, int nprob, void* ws,
     const int64_t nall = 2LL * comm->nranks * p.k2;
     CABS_CUDA_TRY(cudaMemsetAsync(all, 0, sizeof(double) * nall, st));
     cabsk::HardArgs a{}, m{}, f{};
-    a.s[0] = hard_side(p);
+    a.s[0] = keyed(hard_side(p), q);
     m.s[0] = hard_merge_side(cand, hard_local_blocks(p.n_loc) * p.k2, p.k2, nullptr, all + 2LL * comm->rank * p.k2);
     launch_hard_local(a, 1, cand, L.hcand_side, ws, st);
     launch_hard_topk(m, 1, st);
@@ -683,6 +689,78 @@ int32_t cabs_hard_select_pair(const cabs_plan* plan, const cabs_hard_problem* a,
   CABS_TRY(hard_check(plan, L, *b));
   const cabs_hard_problem* pr[2] = {a, b};
   return hard_run(pr, 2, ws, L, comm, stream);
+}
+
+// ---------------------------------------------------------------- variant (e): Supp. 3 + leverage
+int32_t cabs_orthogonalize(const cabs_plan* plan, int32_t r, const float* U, int64_t ldu, const float* s,
+                           const float* V, int64_t ldv, float* Uo, int64_t lduo, float* so, float* Vo, int64_t ldvo,
+                           int32_t* r_out, double* sigma, void* ws, size_t ws_bytes, const cabs_comm* comm,
+                           void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  const cabs_plan& p = *plan;
+  const int64_t m_loc = p.row_end - p.row_begin, n_sl = p.col_end - p.col_begin;
+  if (r < 1 || r > 64 || r > p.kmax) return arg_error("orthogonalize: need 1 <= r <= min(64, kmax)");
+  if (ldu < r || ldv < r || lduo < r || ldvo < r) return arg_error("orthogonalize: bad leading dimensions");
+  if ((m_loc > 0 && (!U || !Uo)) || (n_sl > 0 && (!V || !Vo)) || !so) return arg_error("orthogonalize: bad buffers");
+  cudaStream_t st = S(stream);
+  unsigned char* o = static_cast<unsigned char*>(ws) + L.orth;
+  cabsk::OrthArgs a{};
+  a.U = U; a.ldu = ldu; a.nu = m_loc;
+  a.V = V; a.ldv = ldv; a.nv = n_sl;
+  a.r = r; a.s = s;
+  a.part = wsp<double>(ws, L.orth_part);
+  a.nblk = orth_gram_blocks(m_loc, n_sl);
+  a.gram = reinterpret_cast<double*>(o);
+  a.UK = a.gram + 2 * 64 * 64;
+  a.VK = a.UK + 64 * 64;
+  a.sig = sigma ? sigma : a.VK + 64 * 64;
+  a.r_svd = reinterpret_cast<int*>(a.VK + 64 * 64 + 64);
+  a.kp = L.Kp;
+  a.K = reinterpret_cast<float*>(o + sizeof(double) * (4 * 64 * 64 + 64) + 256);
+  a.TU = a.K + 64 * L.Kp;
+  a.TV = a.TU + 64 * L.Kp;
+  a.s_out = so; a.r_out = r_out;
+  a.Uo = Uo; a.lduo = lduo; a.Vo = Vo; a.ldvo = ldvo;
+  launch_orth_gram(a, st);
+  CABS_LAUNCH_CHECK("orth_gram");
+  CABS_TRY(comm_f64(comm, a.gram, 2 * 64 * 64, stream));
+  launch_orth_core(a, ws, st);
+  CABS_LAUNCH_CHECK("orth_core");
+  launch_svd(r, a.K, a.kp, 1e-12, ws, L, a.sig, a.UK, a.VK, a.r_svd, st);
+  CABS_LAUNCH_CHECK("orth_svd");
+  launch_orth_finish(a, st);
+  CABS_LAUNCH_CHECK("orth_finish");
+  return CABS_OK;
+}
+
+static int32_t lev_run(const cabs_plan* plan, const cabs_hard_problem* const* pr, const uint32_t* tags, int nprob,
+                       uint64_t seed, void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  for (int q = 0; q < nprob; ++q) {
+    if (!pr[q]) return arg_error("leverage_select: null problem");
+    CABS_TRY(hard_check(plan, L, *pr[q]));
+  }
+  return hard_run(pr, nprob, ws, L, comm, stream, 1, seed, tags);
+}
+
+int32_t cabs_leverage_select(const cabs_plan* plan, const float* F, int64_t ldf, int64_t n_loc, int64_t n_glob,
+                             int64_t row_off, int32_t r, int32_t k2, uint64_t seed, uint32_t tag, int64_t* reps,
+                             double* keys, void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream) {
+  const cabs_hard_problem p{F, ldf, n_loc, n_glob, row_off, r, k2, reps, keys};
+  const cabs_hard_problem* pr[1] = {&p};
+  return lev_run(plan, pr, &tag, 1, seed, ws, ws_bytes, comm, stream);
+}
+
+int32_t cabs_leverage_select_pair(const cabs_plan* plan, const cabs_hard_problem* a, const cabs_hard_problem* b,
+                                  uint64_t seed, uint32_t tag_a, uint32_t tag_b, void* ws, size_t ws_bytes,
+                                  const cabs_comm* comm, void* stream) {
+  const cabs_hard_problem* pr[2] = {a, b};
+  const uint32_t tags[2] = {tag_a, tag_b};
+  return lev_run(plan, pr, tags, 2, seed, ws, ws_bytes, comm, stream);
 }
 
 // ---------------------------------------------------------------- S10

@@ -17,6 +17,7 @@ constexpr int kAssignGrid = 4 * kNumSM;
 constexpr int kResGrid = 8 * kNumSM;  // persistent residual CTAs (upper bound)
 constexpr int kNormTile = 64;         // points per embed-GEMM tile (norm partial rows)
 constexpr int kKmItersCap = 256;      // Lloyd iterations the persistent kernel's scratch covers
+constexpr int kOrthMaxBlocks = 64;    // Gram-partial CTAs per side (cabs_orthogonalize)
 constexpr int kHardLocalRows = 2048;  // rows per CTA of the hard-threshold key + local top-k kernel
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -35,6 +36,7 @@ struct Ws {
   size_t cb, rb, wb;
   size_t res_part, res_split;  // res_split: G_hi, G_lo (n x 64 each)
   size_t hcand_side;
+  size_t orth_part, orth;  // cabs_orthogonalize: Gram partials | gram, U_K, V_K, sigma, r, K, T_U, T_V
   size_t total;
   // dims
   int64_t K, Kp, m_loc, n_sl, Nmax, n, ldrb, npt;
@@ -92,6 +94,8 @@ inline Ws ws_layout(const cabs_plan& p) {
   // hard threshold: (key, index) candidates of every 2048-row CTA, both sides of a pair
   w.hcand_side = 2 * ceil_div(w.Nmax, kHardLocalRows) * K;  // doubles per side
   w.hcand = take(sizeof(double) * 2 * w.hcand_side);
+  w.orth_part = take(sizeof(double) * 2 * kOrthMaxBlocks * 64 * 64);
+  w.orth = take(sizeof(double) * (4 * 64 * 64 + 64) + 256 + sizeof(float) * 3 * 64 * Kp);
   w.idx = take(sizeof(int64_t) * 8 * Kp);
   w.cb = take(sizeof(float) * (w.m_loc > 0 ? w.m_loc : 1) * Kp);
   w.rb = take(sizeof(float) * K * w.ldrb);

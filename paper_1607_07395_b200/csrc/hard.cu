@@ -20,6 +20,7 @@
 // key -1 and never win).
 #include "common.cuh"
 #include "kernels.cuh"
+#include "philox.cuh"
 
 namespace cabsk {
 
@@ -251,6 +252,14 @@ __global__ void __launch_bounds__(kHtThreads, 1) hard_local_kernel(HardArgs a, d
     const bool valid = lane < nrow;
     if (valid) {
       if (!isfinite(acc)) set_status(ws, CABS_DEV_NONFINITE);
+      if (h.mode == 1) {  // Efraimidis-Spirakis key (l / r) / (-log u) of the leverage score (Z27)
+        const uint64_t gi = static_cast<uint64_t>(h.off + r0 + rb + lane);
+        const uint4 w4 = philox4x32_10(make_uint4(static_cast<uint32_t>(gi), static_cast<uint32_t>(gi >> 32), h.tag, 1u),
+                                       seed_key(h.seed));
+        const double u = (static_cast<double>(w4.x >> 5) * 67108864.0 + static_cast<double>(w4.y >> 6) + 0.5) *
+                         1.1102230246251565e-16;  // 2^-53
+        acc = (acc / static_cast<double>(d)) / -log(u);
+      }
       if (h.key) h.key[r0 + rb + lane] = acc;
     }
     s_u[rb + lane] = valid ? hard_ukey(acc) : 0ull;

@@ -115,6 +115,9 @@ struct HardSide {
   int64_t* out;        // top-k: winners ascending (or NULL)
   double* slot;        // top-k: (key, index) pairs of the winners, (-1, -1) padding (or NULL)
   int k;               // top-k: winners wanted (min(k, N) taken)
+  int mode;            // local kernel: 0 = key ||X_l||^2 (variant (f)); 1 = leverage ES key
+  uint64_t seed;       // mode 1: Philox seed / tag of the per-point uniforms
+  uint32_t tag;
 };
 struct HardArgs {
   HardSide s[2];
@@ -123,6 +126,37 @@ struct HardArgs {
 int64_t hard_local_blocks(int64_t N);
 void launch_hard_local(const HardArgs& a, int nside, double* cand, int64_t side_stride, void* ws, cudaStream_t st);
 void launch_hard_topk(const HardArgs& a, int nside, cudaStream_t st);
+
+// orth.cu -- orthogonalization of a sketch (Supp. 3), r <= 64
+struct OrthArgs {
+  const float* U;  // nu x r (ldu), this rank's rows
+  int64_t ldu, nu;
+  const float* V;  // nv x r (ldv), this rank's column slice
+  int64_t ldv, nv;
+  int r;
+  const float* s;  // float[r] or NULL (ones)
+  double* part;    // [2][nblk][r*r] Gram partials
+  int nblk;
+  double* gram;    // [2][64*64]: G_U, G_V -> R_U, R_V (ld 64)
+  float* K;        // r x kp core (FP32, input of the Jacobi SVD)
+  int64_t kp;
+  double* UK;      // r x r (ld r), from the SVD
+  double* VK;
+  double* sig;     // SVD singular values
+  int* r_svd;      // SVD rank
+  float* TU;       // r x kp
+  float* TV;
+  float* s_out;    // float[r]
+  int* r_out;      // or NULL
+  float* Uo;
+  int64_t lduo;
+  float* Vo;
+  int64_t ldvo;
+};
+int orth_gram_blocks(int64_t nu, int64_t nv);
+void launch_orth_gram(OrthArgs& a, cudaStream_t st);
+void launch_orth_core(const OrthArgs& a, void* ws, cudaStream_t st);
+void launch_orth_finish(const OrthArgs& a, cudaStream_t st);
 
 // residual.cu
 int launch_residual(const float* A, int64_t lda, int64_t m_loc, int64_t n, const float* F, int64_t ldf, const float* s,

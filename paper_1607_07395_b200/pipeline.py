@@ -34,11 +34,12 @@ class CabsConfig:
     tol: float = 1e-12
     weight_kind: int = C.WEIGHT_CONST
     weight_p: float = 2.0
-    followup: str = "kmeans"  # "kmeans" (Alg. 2 step 3) or "hard" (P:312 variant (f))
+    followup: str = "kmeans"  # "kmeans" (Alg. 2 step 3), "hard" / "leverage" (P:312 variants (f) / (e))
 
 
 STEPS = ("pilot_embed", "kmeans", "select", "sketch", "residual")
 STEPS_HARD = ("pilot_embed", "hard_select", "sketch", "residual")
+STEPS_LEVERAGE = ("pilot_embed", "orthogonalize", "leverage_select", "sketch", "residual")
 
 
 class CabsPipeline:
@@ -120,6 +121,28 @@ class CabsPipeline:
         cols = C.hard_problem(self.Q, p.n_sl, p.n, p.col_begin, c.k1, c.k2, self.Jb)
         C.cabs_hard_select_pair(p, rows, cols, self.ws, comm=self.comm)
 
+    def orthogonalize(self):
+        """Supp. 3 on the pilot: P Q^T = U diag(s) V^T, so the orthogonalized factors of
+        (P, ones, Q) are those of the pilot sketch."""
+        c, p = self.cfg, self.plan
+        if not hasattr(self, "Uo"):
+            l1 = self.P.shape[1]
+            dev = self.device
+            self.Uo = torch.zeros((self.P.shape[0], l1), device=dev)
+            self.Vo = torch.zeros((self.Q.shape[0], l1), device=dev)
+            self.so = torch.zeros(c.k1, device=dev)
+            self.ro = torch.zeros(1, dtype=torch.int32, device=dev)
+        C.cabs_orthogonalize(p, c.k1, self.P, None, self.Q, self.Uo, self.so, self.Vo, self.ws, r_out=self.ro,
+                             comm=self.comm)
+
+    def leverage_select(self):
+        """P:312 variant (e): k2 rows / columns sampled by the leverage scores of Uo / Vo."""
+        c, p = self.cfg, self.plan
+        rows = C.hard_problem(self.Uo, p.m_loc, p.m, p.row_begin, c.k1, c.k2, self.Ib)
+        cols = C.hard_problem(self.Vo, p.n_sl, p.n, p.col_begin, c.k1, c.k2, self.Jb)
+        C.cabs_leverage_select_pair(p, rows, cols, c.seed, C.TAG_LEVERAGE_ROWS, C.TAG_LEVERAGE_COLS, self.ws,
+                                    comm=self.comm)
+
     def sketch(self):
         c, p = self.cfg, self.plan
         C.cabs_sketch(p, self.A, self.Ib, self.Jb, c.k2, c.mode, c.tol, self.U, self.s2, self.V, self.r2,
@@ -136,18 +159,23 @@ class CabsPipeline:
     # ------------------------------------------------------------------ whole path
     def run(self, with_residual=True, timed=False, init_rows=None, init_cols=None):
         """One pass of the hot path, stream-ordered; returns per-step CUDA events if timed."""
-        hard = self.cfg.followup == "hard"
-        if self.cfg.followup not in ("kmeans", "hard"):
-            raise ValueError("followup must be 'kmeans' or 'hard'")
-        steps = STEPS_HARD if hard else STEPS
+        fu = self.cfg.followup
+        if fu not in ("kmeans", "hard", "leverage"):
+            raise ValueError("followup must be 'kmeans', 'hard' or 'leverage'")
+        steps = {"kmeans": STEPS, "hard": STEPS_HARD, "leverage": STEPS_LEVERAGE}[fu]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(steps) + 1)] if timed else None
         e = iter(ev[1:]) if timed else None
         if timed:
             ev[0].record()
         self.pilot_embed()
         timed and next(e).record()
-        if hard:
+        if fu == "hard":
             self.hard_select()
+            timed and next(e).record()
+        elif fu == "leverage":
+            self.orthogonalize()
+            timed and next(e).record()
+            self.leverage_select()
             timed and next(e).record()
         else:
             self.kmeans(init_rows, init_cols)
@@ -179,7 +207,7 @@ class CabsPipeline:
         """Per-step milliseconds of the last timed run (synchronises)."""
         ev = self.events
         torch.cuda.synchronize()
-        steps = STEPS_HARD if self.cfg.followup == "hard" else STEPS
+        steps = {"kmeans": STEPS, "hard": STEPS_HARD, "leverage": STEPS_LEVERAGE}[self.cfg.followup]
         return {s: ev[i].elapsed_time(ev[i + 1]) for i, s in enumerate(steps)}
 
     def results(self):
