@@ -192,6 +192,48 @@ def oracle_cpu_baseline(cfg, A_cpu):
 
 
 # ---------------------------------------------------------------------- our arm
+def time_variant(args, cfg, A, plan, rank, world, comm, flush, stream, followup, desc):
+    """One of the paper's follow-up variants on the same matrix, timed like the main step."""
+    from paper_1607_07395_b200.pipeline import CabsConfig, CabsPipeline
+    vp = CabsPipeline(A, cfg.m, cfg.n, CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, followup=followup),
+                      rank, world, comm=comm, plan=plan)
+    for _ in range(args.warmup):
+        vp.run()
+    per = {}
+    for _ in range(min(args.steps, 3)):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        vp.run(timed=True)
+        for k_, v in vp.step_ms().items():
+            per.setdefault(k_, []).append(v)
+    graph = None
+    if world == 1 and not args.eager:
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            vp.run()
+            graph, _ = vp.capture(stream=cap)
+        stream.wait_stream(cap)
+        torch.cuda.synchronize()
+    ms = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        graph.replay() if graph is not None else vp.run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        ms.append(e0.elapsed_time(e1))
+    t = allreduce_max(sum(ms), world) / args.steps
+    res = vp.results()
+    return {"followup": desc, "value": (cfg.m + cfg.n) / (t / 1e3), "unit": UNIT, "ms_per_step": t,
+            "breakdown_ms": {k_: allreduce_max(statistics.mean(v), world) for k_, v in per.items()},
+            "rel_err_followup": math.sqrt(max(res["resid_sq"], 0) / res["a_sq"])}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -308,47 +350,13 @@ def main():
     # ---- the paper's follow-up variant (f) (hard threshold) on the same
     # matrix: S6-S8 replaced by cabs_hard_select_pair; timed the same way (graph on one GPU)
     variants = {}
-    hpipe = None if args.no_variants else CabsPipeline(A, cfg.m, cfg.n, CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, followup="hard"),
-                         rank, world, comm=comm, plan=plan)
-    for _ in range(args.warmup if hpipe else 0):
-        hpipe.run()
-    hper = {}
-    for _ in range(min(args.steps, 3) if hpipe else 0):
-        flush.fill_(1.0)
-        torch.cuda.synchronize()
-        hpipe.run(timed=True)
-        for k_, v in hpipe.step_ms().items():
-            hper.setdefault(k_, []).append(v)
-    hgraph = None
-    if hpipe and world == 1 and not args.eager:
-        cap = torch.cuda.Stream()
-        cap.wait_stream(stream)
-        with torch.cuda.stream(cap):
-            hpipe.run()
-            hgraph, _ = hpipe.capture(stream=cap)
-        stream.wait_stream(cap)
-        torch.cuda.synchronize()
-    h_ms = []
-    for _ in range(args.steps if hpipe else 0):
-        flush.fill_(1.0)
-        barrier(world)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        hgraph.replay() if hgraph is not None else hpipe.run()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier(world)
-        h_ms.append(e0.elapsed_time(e1))
-    if hpipe:
-        h_t = allreduce_max(sum(h_ms), world) / args.steps
-        hres = hpipe.results()
-        variants["hard_threshold"] = {
-            "followup": "P:312 variant (f): top-k2 weighting coefficients (cabs_hard_select_pair)",
-            "value": (cfg.m + cfg.n) / (h_t / 1e3), "unit": UNIT, "ms_per_step": h_t,
-            "breakdown_ms": {k_: allreduce_max(statistics.mean(v), world) for k_, v in hper.items()},
-            "rel_err_followup": math.sqrt(max(hres["resid_sq"], 0) / hres["a_sq"])}
-    del hpipe, hgraph
+    for fu_name, fu, fu_desc in (("hard_threshold", "hard", "P:312 variant (f): top-k2 weighting coefficients "
+                                  "(cabs_hard_select_pair)"),
+                                 ("leverage", "leverage", "P:312 variant (e): Supp. 3 orthogonalization + leverage-"
+                                  "score sampling (cabs_orthogonalize, cabs_leverage_select_pair)")):
+        if args.no_variants:
+            break
+        variants[fu_name] = time_variant(args, cfg, A, plan, rank, world, comm, flush, stream, fu, fu_desc)
 
     if rank != 0:
         return 0

@@ -17,7 +17,7 @@ constexpr int kAssignGrid = 4 * kNumSM;
 constexpr int kResGrid = 8 * kNumSM;  // persistent residual CTAs (upper bound)
 constexpr int kNormTile = 64;         // points per embed-GEMM tile (norm partial rows)
 constexpr int kKmItersCap = 256;      // Lloyd iterations the persistent kernel's scratch covers
-constexpr int kOrthMaxBlocks = 64;    // Gram-partial CTAs per side (cabs_orthogonalize)
+constexpr int kOrthMaxBlocks = 148;   // Gram-partial CTAs per side (cabs_orthogonalize)
 constexpr int kHardLocalRows = 2048;  // rows per CTA of the hard-threshold key + local top-k kernel
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

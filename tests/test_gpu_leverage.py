@@ -152,3 +152,51 @@ def test_e2e_leverage_followup(dev, name, m, n, k, seed):
         a = math.sqrt(ref.a_sq)
         rg, ro = math.sqrt(max(g["resid_sq"], 0)), math.sqrt(ref.resid_sq)
         assert abs(rg - ro) <= 1e-4 * ro + 1e-6 * a, (rg, ro)
+
+
+def test_orthogonalize_two_ranks_match_one(dev):
+    """Row-sharded U and column-sliced V on two ranks (host-rendezvous allreduce, see
+    test_gpu_hard): every rank's rows of Uo / Vo equal the single-rank result."""
+    import threading
+    from paper_1607_07395_b200.dist import make_plan
+    from tests.test_gpu_hard import _HostRendezvousComm
+    g = np.random.default_rng(21)
+    m, n, r = 3001, 1999, 12
+    U = g.standard_normal((m, r)).astype(np.float32)
+    V = g.standard_normal((n, r)).astype(np.float32)
+    s = torch.from_numpy(g.uniform(0.5, 2.0, r).astype(np.float32)).to(dev)
+    ld = C.cabs_padded_ld(r)
+    plan1 = make_plan(m, n, 64)
+    ws1 = torch.zeros(C.cabs_workspace_bytes(plan1), dtype=torch.uint8, device=dev)
+    Uo1, Vo1, so1 = torch.zeros((m, ld), device=dev), torch.zeros((n, ld), device=dev), torch.zeros(r, device=dev)
+    C.cabs_orthogonalize(plan1, r, _pad(dev, U, ld), s, _pad(dev, V, ld), Uo1, so1, Vo1, ws1)
+    torch.cuda.synchronize()
+    rc = _HostRendezvousComm(2, dev)
+    out, errs = [None, None], []
+
+    def rank_main(k):
+        try:
+            p = make_plan(m, n, 64, k, 2)
+            ws = torch.zeros(C.cabs_workspace_bytes(p), dtype=torch.uint8, device=dev)
+            Ul, Vl = _pad(dev, U[p.row_begin:p.row_end], ld), _pad(dev, V[p.col_begin:p.col_end], ld)
+            Uo, Vo = torch.zeros((max(p.m_loc, 1), ld), device=dev), torch.zeros((max(p.n_sl, 1), ld), device=dev)
+            so = torch.zeros(r, device=dev)
+            st = torch.cuda.Stream(device=dev)
+            with torch.cuda.stream(st):
+                C.cabs_orthogonalize(p, r, Ul, s, Vl, Uo, so, Vo, ws, comm=rc.comms[k], stream=st)
+            st.synchronize()
+            out[k] = (p, Uo.cpu(), Vo.cpu(), so.cpu())
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=rank_main, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    for p, Uo, Vo, so in out:
+        assert torch.allclose(so, so1.cpu(), rtol=1e-6)
+        # the Gram sums differ only in association across ranks: agreement to FP32 rounding
+        assert torch.allclose(Uo[:p.m_loc], Uo1.cpu()[p.row_begin:p.row_end], atol=1e-5)
+        assert torch.allclose(Vo[:p.n_sl], Vo1.cpu()[p.col_begin:p.col_end], atol=1e-5)
