@@ -16,6 +16,13 @@
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
 
+#ifndef CABS_SVD_TSTOP
+// Stop after a sweep whose rotations all had |t| below this: Jacobi converges quadratically,
+// so the next sweep would rotate by O(t^2) ~ 1e-12 -- U_w, V_w are then orthonormal to
+// ~1e-12 (measured <= 1e-12, tools/probe.py svd), five orders below the resolution of their
+// FP32 consumers; sigma errors are second order (~1e-15).  1e-8 costs one more sweep.
+#define CABS_SVD_TSTOP 1e-6
+#endif
 namespace cabsk {
 
 constexpr int kSvdThreads = 1024;
@@ -743,7 +750,7 @@ svd_split_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, do
       rotated = __syncthreads_or(rotated);
       // quadratic convergence: after a sweep whose rotations all had |t| < 1e-8 the next
       // sweep's would be below the rotation threshold (|t| ~ 1e-16), so it is not run
-      const int small = __syncthreads_and(tmax < 1e-8);
+      const int small = __syncthreads_and(tmax < CABS_SVD_TSTOP);
       last = !rotated || small || sweep + 1 >= kSvdMaxSweeps;
       if (tid == 0) {
         dsmem_st_s32(last_remote + 4 * sp, last ? 1 : 0);
@@ -1098,7 +1105,7 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
       if ((gl & 1) == 0 && live)  // the scales the sweep ended with, for CTA 1's V columns
         dsmem_st_f64(dvs_remote + static_cast<uint32_t>((sp * n4 + 4 * g + own) * 8), od);
       rotated = __syncthreads_or(rotated);
-      const int small = __syncthreads_and(tmax < 1e-8);
+      const int small = __syncthreads_and(tmax < CABS_SVD_TSTOP);
       last = !rotated || small || sweep + 1 >= kSvdMaxSweeps;
       if (tid == 0) {
         dsmem_st_s32(last_remote + 4 * sp, last ? 1 : 0);
