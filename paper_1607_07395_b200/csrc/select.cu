@@ -190,24 +190,20 @@ __device__ __forceinline__ void taken_put(int64_t* tab, int64_t x) {
 __device__ unsigned long long g_snap_prof[4];  // rescans, greedy-pass cycles
 #endif
 // The taken set of the greedy pass: a bitmap over the local point indices when the rank owns
-// all points (single GPU, N <= kBitmapMax: one shared-memory word test per candidate), else
+// all points (single GPU, N <= kBitmapMax and fits shared memory: one byte per point, one load per candidate), else
 // the open-addressing hash table of global indices.
 constexpr int64_t kBitmapMax = 1 << 18;
 struct TakenSet {
-  unsigned* bits;  // null: hash table
+  unsigned char* bits;  // one byte per local point (a put is one plain store); null: hash table
   int64_t* tab;
   int64_t off;
   __device__ __forceinline__ bool has(int64_t x) const {
-    if (bits) {
-      const int64_t p = x - off;
-      return (bits[p >> 5] >> (p & 31)) & 1u;
-    }
+    if (bits) return bits[x - off] != 0;
     return taken_has(tab, x);
   }
   __device__ __forceinline__ void put(int64_t x) {
     if (bits) {
-      const int64_t p = x - off;
-      bits[p >> 5] |= 1u << (p & 31);
+      bits[x - off] = 1;
     } else {
       taken_put(tab, x);
     }
@@ -230,6 +226,7 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
   __shared__ int s_rescan;    // centre needing a rescan, or -1
   __shared__ float rd[8], rs[8];
   __shared__ int64_t ri[8], ri2[8];
+  __shared__ unsigned char s_t1[CABS_KMAX], s_t2[CABS_KMAX];  // fast path: chosen candidate slots
   // dynamic: candidates in visiting order [k2][T] (int64 | float), then the bitmap
   extern __shared__ __align__(16) unsigned char cand_smem[];
   const int tid = threadIdx.x;
@@ -244,9 +241,9 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
   taken.off = row_off;
   taken.bits = nullptr;
   if (use_bitmap) {
-    taken.bits = reinterpret_cast<unsigned*>(
-        cand_smem + (staged ? (((size_t)k2 * T * (sizeof(int64_t) + sizeof(float)) + 15) & ~size_t(15)) : 0));
-    for (int64_t e = tid; e < (N + 31) / 32; e += blockDim.x) taken.bits[e] = 0u;
+    taken.bits = cand_smem + (staged ? (((size_t)k2 * T * (sizeof(int64_t) + sizeof(float)) + 15) & ~size_t(15)) : 0);
+    unsigned* w32 = reinterpret_cast<unsigned*>(taken.bits);
+    for (int64_t e = tid; e < (N + 3) / 4; e += blockDim.x) w32[e] = 0u;
   } else {
     for (int e = tid; e < kTakenCap; e += blockDim.x) tab[e] = -1;
   }
@@ -282,33 +279,64 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
     if (tid < 32) {  // warp 0: the greedy pass, lane t checks candidate t of the current centre
       const int lane = tid;
       if (lane == 0) s_rescan = -1;
-      int o = s_next;
+      const int o0 = s_next;
+      int o = o0;
       int64_t ci = (o < k2 && lane < T) ? cand_at(o, lane) : -1;
-      for (; o < k2; ++o) {
-        const bool ok = ci >= 0 && !taken.has(ci);
-        // prefetch the next centre's candidates (independent of the taken set)
-        const int64_t cn = (o + 1 < k2 && lane < T) ? cand_at(o + 1, lane) : -1;
-        const unsigned m = __ballot_sync(0xffffffffu, ok);
-        const int t1 = m ? __ffs(m) - 1 : -1;
-        const unsigned m2 = m & (m - 1);
-        const int t2 = m2 ? __ffs(m2) - 1 : -1;
-        int64_t i1 = __shfl_sync(0xffffffffu, ci, t1 < 0 ? 0 : t1);
-        if (t1 < 0) i1 = -1;
-        if (t2 < 0 && can_rescan) {  // best or runner-up not resolved from the list
-          if (lane == 0) s_rescan = order[o];
-          break;
+      if (staged && taken.bits) {
+        // fast path: the only loop-carried dependency is the taken set, so the chain per centre
+        // is probe -> ballot -> the winning lane's one-byte store -> __syncwarp; the choices
+        // (t1, t2 per visiting position) are turned into outputs after the pass
+        for (; o < k2; ++o) {
+          const bool ok = ci >= 0 && !taken.has(ci);
+          const int64_t cn = (o + 1 < k2 && lane < T) ? cand_at(o + 1, lane) : -1;
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          const unsigned m2 = m & (m - 1);
+          if (m2 == 0u) {  // best or runner-up not resolved from the list (can_rescan holds here)
+            if (lane == 0) s_rescan = order[o];
+            break;
+          }
+          if (lane == __ffs(m) - 1) taken.put(ci);
+          if (lane == 0) {
+            s_t1[o] = static_cast<unsigned char>(__ffs(m) - 1);
+            s_t2[o] = static_cast<unsigned char>(__ffs(m2) - 1);
+          }
+          __syncwarp();  // the new entry of the taken set is visible to the next centre's probes
+          ci = cn;
         }
-        if (lane == 0) {
-          const int j = order[o];
-          float d1 = t1 >= 0 ? dist_at(o, t1) : FLT_MAX;
-          if (i1 < 0) { set_status(ws, CABS_DEV_SNAP_EXHAUSTED); i1 = 0; d1 = 0.f; }
-          taken.put(i1);
-          reps[j] = i1;
-          r_d1[j] = d1;
-          r_d2[j] = t2 >= 0 ? dist_at(o, t2) : FLT_MAX;
+        __syncwarp();
+        for (int q = o0 + lane; q < o; q += 32) {
+          const int j = order[q], t1 = s_t1[q], t2 = s_t2[q];
+          reps[j] = cand_at(q, t1);
+          r_d1[j] = dist_at(q, t1);
+          r_d2[j] = dist_at(q, t2);
         }
-        __syncwarp();  // the new entry of the taken set is visible to the next centre's probes
-        ci = cn;
+      } else {
+        for (; o < k2; ++o) {
+          const bool ok = ci >= 0 && !taken.has(ci);
+          // prefetch the next centre's candidates (independent of the taken set)
+          const int64_t cn = (o + 1 < k2 && lane < T) ? cand_at(o + 1, lane) : -1;
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          const int t1 = m ? __ffs(m) - 1 : -1;
+          const unsigned m2 = m & (m - 1);
+          const int t2 = m2 ? __ffs(m2) - 1 : -1;
+          int64_t i1 = __shfl_sync(0xffffffffu, ci, t1 < 0 ? 0 : t1);
+          if (t1 < 0) i1 = -1;
+          if (t2 < 0 && can_rescan) {  // best or runner-up not resolved from the list
+            if (lane == 0) s_rescan = order[o];
+            break;
+          }
+          if (lane == 0) {
+            const int j = order[o];
+            float d1 = t1 >= 0 ? dist_at(o, t1) : FLT_MAX;
+            if (i1 < 0) { set_status(ws, CABS_DEV_SNAP_EXHAUSTED); i1 = 0; d1 = 0.f; }
+            taken.put(i1);
+            reps[j] = i1;
+            r_d1[j] = d1;
+            r_d2[j] = t2 >= 0 ? dist_at(o, t2) : FLT_MAX;
+          }
+          __syncwarp();  // the new entry of the taken set is visible to the next centre's probes
+          ci = cn;
+        }
       }
       if (lane == 0) s_next = o;
     }
@@ -404,7 +432,7 @@ void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int 
   size_t cand = (((size_t)k2 * T * (sizeof(int64_t) + sizeof(float))) + 15) & ~size_t(15);
   const bool staged = cand <= kCap;
   if (!staged) cand = 0;
-  const size_t bits = sizeof(unsigned) * ((N + 31) / 32);
+  const size_t bits = ((N + 15) / 16) * 16;  // one byte per point
   const bool bitmap = can_rescan && N <= kBitmapMax && cand + bits <= kCap && !getenv("CABS_SNAP_HASH");
   const size_t bytes = cand + (bitmap ? bits : 0);
   note_launch();
