@@ -25,7 +25,6 @@ __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict_
                                                         double* __restrict__ all) {
   __shared__ float hd[256];
   __shared__ int64_t hi[256];
-  __shared__ int s_win;
   const int j = blockIdx.x, tid = threadIdx.x;
   const int64_t seg = ceil_div(N, gridDim.y);
   const int64_t pbeg = blockIdx.y * seg, pend = pbeg + seg < N ? pbeg + seg : N;
@@ -66,40 +65,68 @@ __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict_
     }
     }
   }
-  // merge: T rounds of block-wide lexicographic argmin over the list heads
+  // merge, two levels: T rounds of warp argmin over the lanes' list heads (shuffles only) give
+  // each warp its sorted top T (lane r keeps the r-th); then one warp takes the top T of the
+  // 8 warps' lists the same way, each lane holding 8T / 32 of those entries
+  const int lane = tid & 31, wid = tid >> 5;
   int head = 0;
+  float wd_ = FLT_MAX;
+  int64_t wi_ = INT64_MAX;
   for (int round = 0; round < T; ++round) {
-    float d0 = FLT_MAX;
-    int64_t i0 = INT64_MAX;
+    float bd = FLT_MAX;
+    int64_t bi = INT64_MAX;
 #pragma unroll
     for (int q = 0; q < T; ++q)
-      if (q == head) { d0 = ld[q]; i0 = li[q]; }
-    hd[tid] = d0;
-    hi[tid] = i0;
-    __syncthreads();
-    if (tid < 32) {
+      if (q == head) { bd = ld[q]; bi = li[q]; }
+    int bt = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+      if (lex_less(od, oi, bd, bi)) { bd = od; bi = oi; bt = ot; }
+    }
+    if (lane == bt) ++head;
+    if (lane == round) { wd_ = bd; wi_ = bi; }
+  }
+  if (lane < T) {
+    hd[wid * T + lane] = wd_;
+    hi[wid * T + lane] = wi_;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    constexpr int kE = 8 * T / 32;  // entries per lane
+    float ed[kE];
+    int64_t ei[kE];
+#pragma unroll
+    for (int q = 0; q < kE; ++q) { ed[q] = hd[q * 32 + lane]; ei[q] = hi[q * 32 + lane]; }
+    for (int round = 0; round < T; ++round) {
       float bd = FLT_MAX;
       int64_t bi = INT64_MAX;
-      int bt = 0;
-      for (int t = tid; t < 256; t += 32)
-        if (lex_less(hd[t], hi[t], bd, bi)) { bd = hd[t]; bi = hi[t]; bt = t; }
+      int bq = 0;
+#pragma unroll
+      for (int q = 0; q < kE; ++q)
+        if (lex_less(ed[q], ei[q], bd, bi)) { bd = ed[q]; bi = ei[q]; bq = q; }
+      int bt = lane;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        float od = __shfl_xor_sync(0xffffffffu, bd, o);
-        int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+        const float od = __shfl_xor_sync(0xffffffffu, bd, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
         if (lex_less(od, oi, bd, bi)) { bd = od; bi = oi; bt = ot; }
       }
-      if (tid == 0) {
-        const int64_t e = ((((int64_t)slot0 + blockIdx.y) * k2 + j) * T + round) * 2;
-        all[e] = static_cast<double>(bd);
-        all[e + 1] = bi == INT64_MAX ? -1.0 : static_cast<double>(bi);
-        s_win = bt;
+      if (lane == bt) {
+#pragma unroll
+        for (int q = 0; q < kE; ++q)
+          if (q == bq) { ed[q] = FLT_MAX; ei[q] = INT64_MAX; }
       }
+      if (lane == round) { wd_ = bd; wi_ = bi; }
     }
-    __syncthreads();
-    if (tid == s_win) ++head;
-    __syncthreads();
+    if (lane < T) {
+      const int64_t e = ((((int64_t)slot0 + blockIdx.y) * k2 + j) * T + lane) * 2;
+      all[e] = static_cast<double>(wd_);
+      all[e + 1] = wi_ == INT64_MAX ? -1.0 : static_cast<double>(wi_);
+    }
   }
 }
 
