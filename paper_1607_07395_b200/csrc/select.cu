@@ -19,19 +19,24 @@ namespace cabsk {
 // grid (k2, S): block (j, s) keeps the T nearest (d, index) of centre j among points of
 // segment s and writes them as list (slot0 + s) of the packed candidate array
 // all[list][k2][T][{d, idx}] (doubles; idx < 2^53 exact).  Empty entries: idx = -1.
+// (d, local index) packed as one 64-bit key: d >= 0, so its FP32 bit pattern orders like d,
+// and the low word breaks ties by index -- the lexicographic (d, idx) order is the integer
+// order of the key, and a sorted-list insertion is a chain of 64-bit min / max.
+__device__ __forceinline__ uint64_t snap_key(float d, int64_t p) {
+  return (static_cast<uint64_t>(__float_as_uint(d)) << 32) | static_cast<uint32_t>(p);
+}
+
 template <int T>
 __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict__ D, int64_t ldd, int64_t N,
                                                         int64_t row_off, int k2, int slot0,
                                                         double* __restrict__ all) {
-  __shared__ float hd[256];
-  __shared__ int64_t hi[256];
+  __shared__ uint64_t hk[256];
   const int j = blockIdx.x, tid = threadIdx.x;
   const int64_t seg = ceil_div(N, gridDim.y);
   const int64_t pbeg = blockIdx.y * seg, pend = pbeg + seg < N ? pbeg + seg : N;
-  float ld[T];
-  int64_t li[T];
+  uint64_t lk[T];
 #pragma unroll
-  for (int q = 0; q < T; ++q) { ld[q] = FLT_MAX; li[q] = INT64_MAX; }
+  for (int q = 0; q < T; ++q) lk[q] = ~0ull;
   const float* row = D + (int64_t)j * ldd;
   constexpr int kU = 8;  // distances loaded per batch (independent loads in flight)
   for (int64_t p0 = pbeg + tid; p0 < pend; p0 += kU * (int64_t)blockDim.x) {
@@ -39,30 +44,20 @@ __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict_
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int64_t p = p0 + (int64_t)u * blockDim.x;
-      vb[u] = p < pend ? __ldg(row + p) : FLT_MAX;
+      vb[u] = p < pend ? __ldg(row + p) : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-    const int64_t p = p0 + (int64_t)u * blockDim.x;
-    if (p >= pend) break;
-    const float v = vb[u];
-    const int64_t gi = row_off + p;
-    if (lex_less(v, gi, ld[T - 1], li[T - 1])) {
-      // insertion into the sorted list (compile-time indices only)
-      float cv = v;
-      int64_t ci = gi;
+      const int64_t p = p0 + (int64_t)u * blockDim.x;
+      uint64_t c = p < pend ? snap_key(vb[u], p) : ~0ull;
+      if (c < lk[T - 1]) {  // insertion into the sorted list
 #pragma unroll
-      for (int q = 0; q < T; ++q) {
-        if (lex_less(cv, ci, ld[q], li[q])) {
-          float td = ld[q];
-          int64_t ti = li[q];
-          ld[q] = cv;
-          li[q] = ci;
-          cv = td;
-          ci = ti;
+        for (int q = 0; q < T; ++q) {
+          const uint64_t lo = c < lk[q] ? c : lk[q];
+          c = c < lk[q] ? lk[q] : c;
+          lk[q] = lo;
         }
       }
-    }
     }
   }
   // merge, two levels: T rounds of warp argmin over the lanes' list heads (shuffles only) give
@@ -70,62 +65,50 @@ __global__ void __launch_bounds__(256) snap_topT_kernel(const float* __restrict_
   // 8 warps' lists the same way, each lane holding 8T / 32 of those entries
   const int lane = tid & 31, wid = tid >> 5;
   int head = 0;
-  float wd_ = FLT_MAX;
-  int64_t wi_ = INT64_MAX;
+  uint64_t mine = ~0ull;
   for (int round = 0; round < T; ++round) {
-    float bd = FLT_MAX;
-    int64_t bi = INT64_MAX;
+    uint64_t b = ~0ull;
 #pragma unroll
     for (int q = 0; q < T; ++q)
-      if (q == head) { bd = ld[q]; bi = li[q]; }
-    int bt = lane;
+      if (q == head) b = lk[q];
+    const uint64_t own = b;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const float od = __shfl_xor_sync(0xffffffffu, bd, o);
-      const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
-      if (lex_less(od, oi, bd, bi)) { bd = od; bi = oi; bt = ot; }
+      const uint64_t ob = __shfl_xor_sync(0xffffffffu, b, o);
+      b = ob < b ? ob : b;
     }
-    if (lane == bt) ++head;
-    if (lane == round) { wd_ = bd; wi_ = bi; }
+    if (own == b && b != ~0ull) ++head;  // keys are unique: exactly one lane owns the winner
+    if (lane == round) mine = b;
   }
-  if (lane < T) {
-    hd[wid * T + lane] = wd_;
-    hi[wid * T + lane] = wi_;
-  }
+  if (lane < T) hk[wid * T + lane] = mine;
   __syncthreads();
   if (wid == 0) {
     constexpr int kE = 8 * T / 32;  // entries per lane
-    float ed[kE];
-    int64_t ei[kE];
+    uint64_t e[kE];
 #pragma unroll
-    for (int q = 0; q < kE; ++q) { ed[q] = hd[q * 32 + lane]; ei[q] = hi[q * 32 + lane]; }
+    for (int q = 0; q < kE; ++q) e[q] = hk[q * 32 + lane];
     for (int round = 0; round < T; ++round) {
-      float bd = FLT_MAX;
-      int64_t bi = INT64_MAX;
-      int bq = 0;
+      uint64_t b = ~0ull;
 #pragma unroll
-      for (int q = 0; q < kE; ++q)
-        if (lex_less(ed[q], ei[q], bd, bi)) { bd = ed[q]; bi = ei[q]; bq = q; }
-      int bt = lane;
+      for (int q = 0; q < kE; ++q) b = e[q] < b ? e[q] : b;
+      const uint64_t own = b;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const float od = __shfl_xor_sync(0xffffffffu, bd, o);
-        const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
-        if (lex_less(od, oi, bd, bi)) { bd = od; bi = oi; bt = ot; }
+        const uint64_t ob = __shfl_xor_sync(0xffffffffu, b, o);
+        b = ob < b ? ob : b;
       }
-      if (lane == bt) {
+      if (own == b && b != ~0ull) {
 #pragma unroll
         for (int q = 0; q < kE; ++q)
-          if (q == bq) { ed[q] = FLT_MAX; ei[q] = INT64_MAX; }
+          if (e[q] == b) e[q] = ~0ull;
       }
-      if (lane == round) { wd_ = bd; wi_ = bi; }
+      if (lane == round) mine = b;
     }
     if (lane < T) {
-      const int64_t e = ((((int64_t)slot0 + blockIdx.y) * k2 + j) * T + lane) * 2;
-      all[e] = static_cast<double>(wd_);
-      all[e + 1] = wi_ == INT64_MAX ? -1.0 : static_cast<double>(wi_);
+      const int64_t o = ((((int64_t)slot0 + blockIdx.y) * k2 + j) * T + lane) * 2;
+      const bool empty = mine == ~0ull;
+      all[o] = empty ? static_cast<double>(FLT_MAX) : static_cast<double>(__uint_as_float(static_cast<uint32_t>(mine >> 32)));
+      all[o + 1] = empty ? -1.0 : static_cast<double>(row_off + static_cast<int64_t>(static_cast<uint32_t>(mine)));
     }
   }
 }
