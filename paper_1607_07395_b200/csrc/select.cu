@@ -135,6 +135,43 @@ __global__ void __launch_bounds__(128) snap_merge_kernel(const double* __restric
   const int j = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (j >= k2) return;
   const int ne = nlists * T;
+  if (ne <= 64) {  // every entry loaded once into registers (two per lane), then T warp argmins
+    float ed[2];
+    int64_t ei[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h;
+      ed[h] = FLT_MAX;
+      ei[h] = INT64_MAX;
+      if (e < ne) {
+        const int r = e / T, q = e - r * T;
+        const int64_t off = (((int64_t)r * k2 + j) * T + q) * 2;
+        const int64_t i = static_cast<int64_t>(all[off + 1]);
+        if (i >= 0) { ed[h] = static_cast<float>(all[off]); ei[h] = i; }
+      }
+    }
+    for (int t = 0; t < T; ++t) {
+      const bool first = lex_less(ed[0], ei[0], ed[1], ei[1]);
+      float bd = first ? ed[0] : ed[1];
+      int64_t bi = first ? ei[0] : ei[1];
+      const int64_t own = bi;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float od = __shfl_xor_sync(0xffffffffu, bd, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (lex_less(od, oi, bd, bi)) { bd = od; bi = oi; }
+      }
+      if (bi != INT64_MAX && own == bi) {  // (d, idx) pairs are unique: the owner drops it
+        if (first) { ed[0] = FLT_MAX; ei[0] = INT64_MAX; }
+        else { ed[1] = FLT_MAX; ei[1] = INT64_MAX; }
+      }
+      if (lane == 0) {
+        cand_d[(int64_t)j * T + t] = bi == INT64_MAX ? FLT_MAX : bd;
+        cand_i[(int64_t)j * T + t] = bi == INT64_MAX ? -1 : bi;
+      }
+    }
+    return;
+  }
   float pd = -FLT_MAX;
   int64_t pi = -1;  // previous winner
   for (int t = 0; t < T; ++t) {
