@@ -469,13 +469,19 @@ int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const 
   CABS_TRY(km_check(plan, L, *b, iters, weight_kind));
   const KmSlot ka = km_slot(ws, L, 0), kb = km_slot(ws, L, 1);
   if (!multi(comm)) {
-    // both sides' weights, Floyd initialisations and initial centres in one launch each
+    // both sides' weights, Floyd initialisations and initial centres in one launch each; the
+    // weights (independent of the initialisation) run on the side stream meanwhile
     cudaStream_t st = S(stream);
-    CABS_CUDA_TRY(cudaMemsetAsync(ka.cnt, 0, sizeof(int) * 20, st));  // slot 0 [0, 4), slot 1 [16, 20)
+    SideStream* ss = nullptr;
+    CABS_TRY(side_stream(&ss));
+    CABS_CUDA_TRY(cudaEventRecord(ss->fork, st));
+    CABS_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+    CABS_CUDA_TRY(cudaMemsetAsync(ka.cnt, 0, sizeof(int) * 20, ss->s));  // slot 0 [0, 4), slot 1 [16, 20)
     const KmWeightJob wa{a->X, a->ldx, a->n_loc, a->d, ka.w, ka.cnt, ka.bounds};
     const KmWeightJob wb{b->X, b->ldx, b->n_loc, b->d, kb.w, kb.cnt, kb.bounds};
-    launch_km_weights2(wa, &wb, weight_kind, weight_p, st);
+    launch_km_weights2(wa, &wb, weight_kind, weight_p, ss->s);
     CABS_LAUNCH_CHECK("km_weights");
+    CABS_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
     const bool fa = !a->init_idx && !a->init_centres, fb = !b->init_idx && !b->init_centres;
     if (fa || fb) {
       launch_floyd2(a->n_glob, fa ? a->k2 : 0, static_cast<uint32_t>(a->tag), fa ? ka.idx : nullptr, b->n_glob,
@@ -488,6 +494,7 @@ int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const 
                        b->init_centres, b->ldc, b->centres, b->ldc};
     launch_km_init2(ia, &ib, st);
     CABS_LAUNCH_CHECK("km_init");
+    CABS_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));
   } else {
     CABS_TRY(km_prepare(*a, weight_kind, weight_p, seed, ka, comm, stream));
     CABS_TRY(km_prepare(*b, weight_kind, weight_p, seed, kb, comm, stream));
