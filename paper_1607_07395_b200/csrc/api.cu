@@ -274,7 +274,7 @@ int32_t cabs_pilot_embed(const cabs_plan* plan, const cabs_source* src, int32_t 
   launch_floyd2(p.m, k, 1u, I, p.n, k, 2u, J, seed, st);  // tags ROWS_PILOT = 1, COLS_PILOT = 2
   CABS_LAUNCH_CHECK("floyd");
   // W = A(I, J) first, its SVD on the side stream while C and R are gathered here
-  launch_gather_w_direct(src->a, src->lda, p.row_begin, I, J, k, W, ldw, st);
+  launch_gather_w_direct(src->a, src->lda, p.row_begin, m_loc, p.n, I, J, k, W, ldw, st);
   CABS_LAUNCH_CHECK("gather_w_direct");
   SideStream* ss = nullptr;
   CABS_TRY(side_stream(&ss));
@@ -304,21 +304,21 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
     return arg_error("sketch: bad buffers");
   cudaStream_t st = S(stream);
   const int64_t m_loc = p.row_end - p.row_begin;
-  launch_validate_idx2(Ir, p.m, Ic, p.n, k, ws, st);
   float* Cb = wsp<float>(ws, L.cb);
   float* Rb = wsp<float>(ws, L.rb);
   float* Wb = wsp<float>(ws, L.wb);
   if (!multi(comm)) {
-    // single GPU: W = A(Ir, Ic) first, its SVD on the side stream (2 SMs) while the large C
-    // and R gathers run on the caller's stream, then join
-    launch_gather_w_direct(src->a, src->lda, p.row_begin, Ir, Ic, k, Wb, L.Kp, st);
-    CABS_LAUNCH_CHECK("gather_w_direct");
+    // single GPU: W = A(Ir, Ic) and its SVD (2 SMs) on the side stream, the index check and
+    // the large C and R gathers on the caller's stream meanwhile, then join
     SideStream* ss = nullptr;
     CABS_TRY(side_stream(&ss));
     CABS_CUDA_TRY(cudaEventRecord(ss->fork, st));
     CABS_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+    launch_gather_w_direct(src->a, src->lda, p.row_begin, m_loc, p.n, Ir, Ic, k, Wb, L.Kp, ss->s);
+    CABS_LAUNCH_CHECK("gather_w_direct");
     launch_svd(k, Wb, L.Kp, tol, ws, L, sigma, nullptr, nullptr, nullptr, ss->s);
     CABS_LAUNCH_CHECK("svd");
+    launch_validate_idx2(Ir, p.m, Ic, p.n, k, ws, st);
     launch_gather_cols(src->a, src->lda, m_loc, Ic, k, Cb, L.Kp, ws, st);
     launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, Ir, k, p.n, Rb, L.ldrb, ws, st);
     CABS_LAUNCH_CHECK("sketch gathers");
@@ -327,6 +327,7 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
     return embed_core(p, L, k, Cb, L.Kp, Rb, L.ldrb, Wb, L.Kp, mode, tol, U, ldu, V, ldv, s, r, sigma, 1, ws, comm,
                       stream, true);
   }
+  launch_validate_idx2(Ir, p.m, Ic, p.n, k, ws, st);
   launch_gather_cols(src->a, src->lda, m_loc, Ic, k, Cb, L.Kp, ws, st);
   if (multi(comm)) CABS_CUDA_TRY(cudaMemsetAsync(Rb, 0, sizeof(float) * L.ldrb * k, st));
   launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, Ir, k, p.n, Rb, L.ldrb, ws, st);

@@ -19,8 +19,8 @@ void launch_gather_rows(const float* A, int64_t lda, int64_t row_begin, int64_t 
 void launch_gather_cols(const float* A, int64_t lda, int64_t m_loc, const int64_t* J, int32_t k, float* C, int64_t ldc,
                         void* ws, cudaStream_t st);
 void launch_gather_w(const float* R, int64_t ldr, const int64_t* J, int32_t k, float* W, int64_t ldw, cudaStream_t st);
-void launch_gather_w_direct(const float* A, int64_t lda, int64_t row_begin, const int64_t* I, const int64_t* J,
-                            int32_t k, float* W, int64_t ldw, cudaStream_t st);
+void launch_gather_w_direct(const float* A, int64_t lda, int64_t row_begin, int64_t m_loc, int64_t n,
+                            const int64_t* I, const int64_t* J, int32_t k, float* W, int64_t ldw, cudaStream_t st);
 
 // svd.cu
 int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const Ws& L, double* sigma_user, double* Uw64,
