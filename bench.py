@@ -6,8 +6,8 @@
 A step is one pass of the whole hot path -- pilot sampling + gathers, pilot
 sketch + embeddings, weighted Lloyd k-means on both sides, snap, follow-up
 gathers + sketch, and the fused residual -- over the synthetic matrix of
-BASELINE.json configs[1] (c2, 20000 x 10000, k1 = k2 = 50, 20 Lloyd iterations)
-held in HBM.  Timing: W untimed warm-ups, then K steps, each bracketed by a
+BASELINE.json configs[2] (c3, 100000 x 50000 = 20 GB, k1 = k2 = 100, 25 Lloyd iterations:
+the largest configuration that fits one GPU; c4 is a 2/4/8-GPU config) held in HBM.  Timing: W untimed warm-ups, then K steps, each bracketed by a
 barrier + cuda.synchronize on both sides and timed with CUDA events on the
 launching stream; the L2 is flushed (256 MiB write) before every timed step;
 max over ranks.  N > 1: one process per GPU (torchrun), A row-sharded, NCCL.
@@ -29,13 +29,15 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from workloads import CHUNK, CONFIGS, Generator  # noqa: E402
 
 METRIC = "CABS sketch wall time & k-means pts/s at 1/2/4/8 GPU; HBM GB/s vs peak"
 UNIT = "rows+cols/s"
-BASE_CFG = {1: "c2"}  # BASELINE.json configs[1]
+BASE_CFG = {1: "c3"}  # BASELINE.json configs[2]: the largest single-GPU configuration
+CFG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
 
 
 def load_peaks():
@@ -144,51 +146,167 @@ def allreduce_max(x, world):
 
 
 # ---------------------------------------------------------------------- reference arm (the oracle)
+def oracle_sample(cfg):
+    """The bounded sample of a config the oracle is timed on (10-30 s of host CPU per step):
+    the leading ms x ns block of the same matrix, same k1, k2 and Lloyd iterations."""
+    ms, ns = {"c1": (2000, 1500), "c2": (8000, 4000), "c3": (6000, 3000), "c4": (6000, 3000)}[cfg.name]
+    return min(ms, cfg.m), min(ns, cfg.n)
+
+
 def run_reference(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import numpy as np
     from oracle import cabs as O
-    from workloads import make_A
+    from workloads import Generator
     cores = len(os.sched_getaffinity(0))
-    A = make_A(cfg, device="cpu").numpy()
-    budget = 240.0
+    ms, ns = oracle_sample(cfg)
+    A = Generator(cfg, device="cpu").rows(0, ms)[:, :ns].numpy().copy()
+    k1, k2 = min(cfg.k1, ms, ns), min(cfg.k2, ms, ns)
     times = []
-    t_start = time.time()
     for i in range(args.warmup + args.steps):
         if i < args.warmup:  # warm-up: a small sample (page-in, BLAS init)
-            O.cabs_run(A[:2000], min(cfg.k1, 20), min(cfg.k2, 20), 2, seed=cfg.seed)
+            O.cabs_run(A[:1000, :800], min(k1, 20), min(k2, 20), 2, seed=cfg.seed)
             continue
         t0 = time.perf_counter()
-        O.cabs_run(A, cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed)
+        O.cabs_run(A, k1, k2, cfg.iters, seed=cfg.seed)
         times.append(time.perf_counter() - t0)
-        if time.time() - t_start > budget:
-            break
     t = statistics.mean(times)
-    v = (cfg.m + cfg.n) / t
+    v = (ms + ns) / t
+    sample = (f"leading {ms} x {ns} block of {cfg.name} (same recipe, k1={k1}, k2={k2}, {cfg.iters} Lloyd "
+              f"iterations), full S1-S10 of the FP64 NumPy oracle per step")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.note}", "m": cfg.m, "n": cfg.n, "k1": cfg.k1, "k2": cfg.k2,
-                       "iters": cfg.iters},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"full {cfg.name} step S1-S10 (FP64 NumPy oracle), {len(times)} step(s)"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} = BASELINE.json configs[{CFG_INDEX[cfg.name]}]: {cfg.note}",
+                       "m": cfg.m, "n": cfg.n, "k1": cfg.k1, "k2": cfg.k2, "iters": cfg.iters},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
 
-def oracle_cpu_baseline(cfg, A_cpu):
-    """The oracle as it stands, on the host cores, on a bounded sample (one full step)."""
+def oracle_cpu_baseline(cfg, A_host):
+    """The oracle as it stands, on the host cores, on a bounded sample of the workload."""
     from oracle import cabs as O
     cores = len(os.sched_getaffinity(0))
+    ms, ns = oracle_sample(cfg)
+    A = np.ascontiguousarray(A_host[:ms, :ns])
+    k1, k2 = min(cfg.k1, ms, ns), min(cfg.k2, ms, ns)
     t0 = time.perf_counter()
-    O.cabs_run(A_cpu, cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed)
+    O.cabs_run(A, k1, k2, cfg.iters, seed=cfg.seed)
     t = time.perf_counter() - t0
-    return {"value": (cfg.m + cfg.n) / t, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"one full {cfg.name} step S1-S10 of the FP64 NumPy oracle ({t:.1f} s)"}
+    return {"value": (ms + ns) / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"leading {ms} x {ns} block of {cfg.name} (k1={k1}, k2={k2}, {cfg.iters} Lloyd iterations), "
+                      f"one full S1-S10 step of the FP64 NumPy oracle ({t:.1f} s)"}
+
+
+def parity_block(cfg, A_host, pipe, res, plan, dev, row_sample=2048):
+    """Full-size parity of this bench run against the FP64 oracle, teacher-forced where the full
+    oracle would take minutes.  Every comparison is on the SAME A:
+      S1  pilot indices bit-exact (oracle Philox/Lemire/Floyd);  S2/S3 gathers bit-exact;
+      S4-S5  the oracle's sketch of the gathered C, R, W -> r exact, P, Q within 1e-4;
+      S7  every GPU centre = weighted mean of its GPU cluster (FP64 on the GPU's embedding), 1e-5;
+      S6  objective non-increasing (1e-6 relative);
+      S8  the oracle's snap of the GPU's final centres on the GPU's embedding -> representatives
+          bit-exact, or the first divergence in visiting order is a near tie (gap < 1e-5);
+      S9  the oracle's sketch from the GPU's follow-up indices -> r exact, U, V, s within 1e-4;
+      S10 the GPU residual of a sampled row block vs the oracle's on the same rows and factors."""
+    from oracle import cabs as O
+    from oracle import rng
+    from paper_1607_07395_b200 import cabs as C
+    from paper_1607_07395_b200.dist import make_plan
+    out = {"kind": "full-size, teacher-forced per step (the full FP64 Lloyd loop on 1.5e5 points is minutes)"}
+    t0 = time.perf_counter()
+    m, n, k1, k2 = cfg.m, cfg.n, cfg.k1, cfg.k2
+    I, J = res["I"].numpy(), res["J"].numpy()
+    out["S1_pilot_indices_exact"] = bool(np.array_equal(I, rng.floyd(m, k1, cfg.seed, rng.TAG_PILOT_ROWS)) and
+                                         np.array_equal(J, rng.floyd(n, k1, cfg.seed, rng.TAG_PILOT_COLS)))
+    Cg, Rg, Wg = res["C"].numpy()[:, :k1], res["R"].numpy()[:, :n], res["W"].numpy()[:, :k1]
+    Co, Ro, Wo = O.gather(A_host, I, J)
+    out["S2_S3_gathers_exact"] = bool(np.array_equal(Cg, Co) and np.array_equal(Rg, Ro) and np.array_equal(Wg, Wo))
+
+    def fro(a, b):
+        nb = np.linalg.norm(b)
+        return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+    def aligned(X, Xr):
+        X = np.array(X, np.float64, copy=True)
+        for c in range(min(X.shape[1], Xr.shape[1])):
+            if np.dot(X[:, c], Xr[:, c]) < 0:
+                X[:, c] = -X[:, c]
+        return X
+
+    sk = O.sketch(Co, Ro, Wo, m, n, k1)
+    Po, Qo = O.embeddings(sk)
+    r1 = res["r1"]
+    Pg = res["P"].numpy()[:, :r1].astype(np.float64)
+    Qg = res["Q"].numpy()[:, :r1].astype(np.float64)
+    e_p = fro(aligned(Pg, Po), Po) if r1 == sk.r else float("inf")
+    e_q = fro(aligned(Qg, Qo), Qo) if r1 == sk.r else float("inf")
+    out["S4_S5"] = {"r_gpu": r1, "r_oracle": int(sk.r), "P_rel_fro": e_p, "Q_rel_fro": e_q,
+                    "ok": bool(r1 == sk.r and e_p < 1e-4 and e_q < 1e-4)}
+    s78 = {}
+    for side, X, cen, lab, cw, obj, reps, rep_of in (
+            ("rows", Pg, res["cen_r"], res["lab_r"], res["cw_r"], res["obj_r"], res["Ib"], res["rep_r"]),
+            ("cols", Qg, res["cen_c"], res["lab_c"], res["cw_c"], res["obj_c"], res["Jb"], res["rep_c"])):
+        cen = cen.numpy()[:, :r1].astype(np.float64)
+        lab = lab.numpy()[:X.shape[0]].astype(np.int64)
+        cwv = cw.numpy()
+        sums = np.zeros_like(cen)
+        np.add.at(sums, lab, X)
+        cnt = np.bincount(lab, minlength=k2).astype(np.float64)
+        nz = cnt > 0
+        e_c = fro(cen[nz], sums[nz] / cnt[nz, None])
+        ob = obj.numpy()
+        mono = bool(np.all(ob[1:] <= ob[:-1] * (1 + 1e-6) + 1e-30))
+        sn = O.snap(X, cen, cwv)
+        g_rep = rep_of.numpy()
+        first = None
+        for j in sn.order:
+            if g_rep[j] != sn.rep_of_centre[j]:
+                first = int(j)
+                break
+        ok_snap = first is None or float(sn.gap[first]) < 1e-5
+        s78[side] = {"centres_vs_cluster_means_rel": e_c, "objective_monotone": mono,
+                     "reps_exact": bool(np.array_equal(np.sort(g_rep), reps.numpy()) and first is None),
+                     "first_divergence": None if first is None else
+                     {"centre": first, "oracle_rep": int(sn.rep_of_centre[first]), "gpu_rep": int(g_rep[first]),
+                      "oracle_gap": float(sn.gap[first])},
+                     "near_ties_gpu": int(res["tie_r" if side == "rows" else "tie_c"].sum()),
+                     "ok": bool(e_c < 1e-5 and mono and ok_snap)}
+    out["S6_S8"] = s78
+    Ib, Jb = res["Ib"].numpy(), res["Jb"].numpy()
+    Cb, Rb, Wb = O.gather(A_host, Ib, Jb)
+    fu = O.sketch(Cb, Rb, Wb, m, n, k2)
+    r2 = res["r2"]
+    Ug = res["U"].numpy()[:, :r2].astype(np.float64)
+    Vg = res["V"].numpy()[:, :r2].astype(np.float64)
+    sg = res["s2"].numpy()[:r2].astype(np.float64)
+    ok9 = r2 == fu.r
+    e_u = fro(aligned(Ug, fu.U), fu.U) if ok9 else float("inf")
+    e_v = fro(aligned(Vg, fu.V), fu.V) if ok9 else float("inf")
+    e_s = fro(sg, fu.s) if ok9 else float("inf")
+    out["S9"] = {"r_gpu": r2, "r_oracle": int(fu.r), "U_rel_fro": e_u, "V_rel_fro": e_v, "s_rel": e_s,
+                 "ok": bool(ok9 and max(e_u, e_v, e_s) < 1e-4)}
+    # S10 on a row sample: the GPU's residual of rows [r0, r0 + row_sample) vs the oracle's
+    rs = min(row_sample, m)
+    r0 = (m - rs) // 2
+    sub = make_plan(rs, n, max(k1, k2))
+    ws = torch.zeros(C.cabs_workspace_bytes(sub), dtype=torch.uint8, device=dev)
+    o = torch.zeros(2, dtype=torch.float64, device=dev)
+    C.cabs_residual(sub, pipe.A[r0:r0 + rs], pipe.U[r0:r0 + rs], pipe.s2, pipe.G, r2, o, ws)
+    og = o.cpu().numpy()
+    ro2, ao2 = O.residual(A_host[r0:r0 + rs], Ug[r0:r0 + rs], Vg, sg)
+    rg, ro, ao = math.sqrt(max(og[0], 0)), math.sqrt(ro2), math.sqrt(ao2)
+    out["S10_row_sample"] = {"rows": [r0, r0 + rs], "r_gpu": rg, "r_oracle": ro, "a_gpu": math.sqrt(og[1]),
+                             "a_oracle": ao, "ok": bool(abs(rg - ro) <= 1e-4 * ro + 1e-6 * ao and
+                                                        abs(og[1] - ao2) <= 1e-6 * ao2)}
+    out["ok"] = bool(out["S1_pilot_indices_exact"] and out["S2_S3_gathers_exact"] and out["S4_S5"]["ok"] and
+                     all(v["ok"] for v in s78.values()) and out["S9"]["ok"] and out["S10_row_sample"]["ok"])
+    out["oracle_s"] = time.perf_counter() - t0
+    return out
 
 
 # ---------------------------------------------------------------------- our arm
@@ -243,6 +361,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-size oracle parity block")
     ap.add_argument("--no-variants", action="store_true", help="skip the variant (f) timing")
     ap.add_argument("--eager", action="store_true", help="time stream-ordered launches instead of the CUDA graph")
     args = ap.parse_args()
@@ -319,6 +438,7 @@ def main():
 
     # ---- end to end: host-resident A, copied in every step; the sketch and metric read back
     e2e = None
+    A_host = None
     if not args.no_e2e:
         A_host = A.cpu().pin_memory()
         outs = [pipe.U, pipe.s2, pipe.V, pipe.Ib, pipe.Jb, pipe.out]
@@ -356,59 +476,73 @@ def main():
                                   "score sampling (cabs_orthogonalize, cabs_leverage_select_pair)")):
         if args.no_variants:
             break
+        if fu == "leverage" and cfg.k1 > C.ORTH_RMAX:
+            variants[fu_name] = {"followup": fu_desc, "skipped": f"cabs_orthogonalize supports r <= {C.ORTH_RMAX}"}
+            continue
         variants[fu_name] = time_variant(args, cfg, A, plan, rank, world, comm, flush, stream, fu, fu_desc)
 
     if rank != 0:
         return 0
     peaks, peak_src = load_peaks()
     traffic = load_traffic()
-    # ---- rooflines.  The dominant kernel of the step is the persistent
-    # Lloyd kernel (S6-S7, both sides in one launch): FP32 ALU-bound -- per (point, centre,
-    # dimension) one FADD + one FFMA (direct differences) = 3 flops in 2 FP32 lane-ops, so the
-    # attainable peak is 3/4 of the FFMA peak 148 SM x 128 lanes x 2 flops x max SM clock.
-    # Timed as the k-means phase (the launch plus the small weight / init kernels before it).
+    # ---- rooflines, algorithmic work per SURVEY.md section 8(d):
+    #   k-means (S6-S7): 2 r k2 flop per point per Lloyd pass, c passes over m + n points;
+    #   residual (S10): A once (4 m n bytes) plus the factors F (4 m k2) and G (4 n k2).
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     ffma_tf = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-    lloyd_peak = 0.75 * ffma_tf
+    tf32_tf = 0.5 * float(peaks.get("bf16_tflops", 1627.4))
     d_emb = int(pipe.r1.item())  # embedding dimension r <= k1 the k-means runs on
-    lloyd_flops = 3.0 * cfg.iters * (m_loc_rows(plan) + n_loc_cols(plan)) * cfg.k2 * d_emb
+    km_path = C.cabs_kmeans_path(cfg.k2, d_emb)
+    km_flops = 2.0 * cfg.iters * (m_loc_rows(plan) + n_loc_cols(plan)) * cfg.k2 * d_emb
     km_ms = step_mean["kmeans"]
-    lloyd = {"kernel": "lloyd_persistent_kernel (cabs_kmeans_pair: both sides, all iterations, one launch)",
-             "bound": "alu", "achieved": lloyd_flops / (km_ms / 1e3) / 1e12, "peak": lloyd_peak, "unit": "TFLOP/s",
-             "traffic": traffic_of(traffic, "lloyd"),
-             "peak_source": f"derived: 0.75 x FFMA peak (148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz = "
-                            f"{ffma_tf:.1f} TFLOP/s); direct-difference op mix FADD+FFMA",
-             "algorithmic_flops_per_launch": lloyd_flops, "launch_ms": km_ms}
-    lloyd["frac"] = lloyd["achieved"] / lloyd["peak"]
-    # the fused residual (S10), HBM-bound: it must stream A once (m*n*4 bytes) plus the factors
-    # F (m*k2*4) and G (n*k2*4).
+    if km_path == "tc":
+        km_peak, km_bound = tf32_tf / 3.0, "tensor"
+        km_src = (f"MEASURED_PEAKS bf16_tflops {peaks.get('bf16_tflops')} x 0.5 (nominal TF32:BF16) / 3 "
+                  f"(3xTF32: three MMAs per algorithmic flop)")
+        km_kernel = "lloyd_tc_kernel (cabs_kmeans_pair: tcgen05 3xTF32 cross-term + FP32 direct-difference refine)"
+    else:
+        km_peak, km_bound = ffma_tf, "alu"
+        km_src = f"derived: FFMA peak 148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz = {ffma_tf:.1f} TFLOP/s"
+        km_kernel = "lloyd_persistent_kernel (cabs_kmeans_pair: both sides, all iterations, one launch; FFMA)"
+    kmeans = {"kernel": km_kernel, "bound": km_bound, "achieved": km_flops / (km_ms / 1e3) / 1e12, "peak": km_peak,
+              "unit": "TFLOP/s", "traffic": traffic_of(traffic, f"{cfg.name}_lloyd"), "peak_source": km_src,
+              "algorithmic_flops_per_launch": km_flops, "launch_ms": km_ms,
+              "timing": "CUDA events around cabs_kmeans_pair (eager runs): the persistent kernel plus its "
+                        "weight / Floyd / init launches"}
+    kmeans["frac"] = kmeans["achieved"] / kmeans["peak"]
     m_loc = plan.row_end - plan.row_begin
     res_bytes = 4.0 * (m_loc * cfg.n + m_loc * cfg.k2 + cfg.n * cfg.k2)
     res_ms = step_mean["residual"]
     achieved = res_bytes / (res_ms / 1e3) / 1e9
     peak = float(peaks["hbm_gbs"])
-    residual = {"kernel": "residual_tc_kernel (cabs_residual: fused F diag(s) G^T - A, squared-sum)", "bound": "hbm",
+    res_tc = C.cabs_residual_path(int(pipe.r2.item())) == "tc"
+    residual = {"kernel": ("residual_tc_kernel (tcgen05 3xTF32, TMA)" if res_tc else "residual_ffma_kernel") +
+                          " (cabs_residual: fused F diag(s) G^T - A, squared-sum)", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic_of(traffic, "residual"),
-                "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
-                "algorithmic_bytes_per_launch": res_bytes, "launch_ms": res_ms}
+                "traffic": traffic_of(traffic, f"{cfg.name}_residual"),
+                "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json, copy bandwidth)",
+                "algorithmic_bytes_per_launch": res_bytes, "launch_ms": res_ms,
+                "timing": "CUDA events around cabs_residual (eager runs): G split + the fused kernel + final reduce"}
+    dominant = kmeans if km_ms >= res_ms else residual
     kmeans_pts = cfg.iters * (cfg.m + cfg.n) / (step_mean["kmeans"] / 1e3)
     sketch_ms = sum(step_mean[s] for s in STEPS if s != "residual")
+    a_gb = cfg.m * cfg.n * 4 / 1e9
     line = {
         "metric": METRIC, "value": (cfg.m + cfg.n) / (ms / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} = BASELINE.json configs[1]: {cfg.note}", "m": cfg.m, "n": cfg.n,
+        "config": {"workload": f"{cfg.name} = BASELINE.json configs[{CFG_INDEX[cfg.name]}]: {cfg.note}",
+                   "m": cfg.m, "n": cfg.n,
                    "k1": cfg.k1, "k2": cfg.k2, "iters": cfg.iters, "mode": "stabilized", "parallelism": f"rows{world}",
-                   "l2": "flushed (256 MiB write) before every timed step; A (800 MB) > L2",
+                   "l2": f"flushed (256 MiB write) before every timed step; A ({a_gb:.1f} GB) > L2",
                    "timing": "per-step CUDA events on the launching stream, barrier+sync both sides, max over ranks",
                    "launch": "one CUDA graph per step (captured S1-S10)" if graph is not None else "stream-ordered"},
         "breakdown_ms": step_mean,
         "sketch_ms": sketch_ms,
         "sketch_rows_cols_per_s": (cfg.m + cfg.n) / (sketch_ms / 1e3),
         "kmeans_pts_per_s": kmeans_pts,
-        "roofline": lloyd,
-        "rooflines": {"lloyd": lloyd, "residual": residual},
+        "roofline": dominant,
+        "rooflines": {"kmeans": kmeans, "residual": residual},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "quality": {"rel_err_followup": math.sqrt(max(res["resid_sq"], 0) / res["a_sq"]),
@@ -417,8 +551,12 @@ def main():
     line["variants"] = variants
     if e2e:
         line["e2e"] = e2e
-    if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = oracle_cpu_baseline(cfg, A.cpu().numpy())
+    if world == 1 and not (args.no_cpu_baseline and args.no_parity):
+        A_np = A_host.numpy() if A_host is not None else A.cpu().numpy()
+        if not args.no_parity:
+            line["parity"] = parity_block(cfg, A_np, pipe, res, plan, dev)
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = oracle_cpu_baseline(cfg, A_np)
     print(json.dumps(line))
     return 0
 

@@ -36,6 +36,8 @@ DEV_SVD_NOCONV = 0x20
 
 TAG_PILOT_ROWS, TAG_PILOT_COLS, TAG_INIT_ROWS, TAG_INIT_COLS = 1, 2, 3, 4
 TAG_LEVERAGE_ROWS, TAG_LEVERAGE_COLS = 6, 7
+OP_KMEANS, OP_RESIDUAL, PATH_FFMA, PATH_TC = 0, 1, 0, 1
+ORTH_RMAX = 64  # cabs_orthogonalize: largest supported r
 
 
 class CabsError(RuntimeError):
@@ -95,6 +97,7 @@ _SIGS = {
     "cabs_version": (None, [ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "cabs_padded_ld": (c_i64, [c_i32]),
     "cabs_launch_count": (c_i64, []),
+    "cabs_kernel_path": (c_i32, [c_i32, c_i32, c_i32]),
     "cabs_debug_counters": (c_i32, [ctypes.POINTER(c_i64), c_i32]),
     "cabs_workspace_bytes": (c_sz, [ctypes.POINTER(Plan)]),
     "cabs_clear_status": (c_i32, [c_vp, c_vp]),
@@ -214,6 +217,19 @@ def cabs_debug_counters(n=16):
 
 def cabs_launch_count() -> int:
     return int(load().cabs_launch_count())
+
+
+def cabs_kernel_path(op: int, k: int, d: int = 0) -> int:
+    return int(load().cabs_kernel_path(op, k, d))
+
+
+def cabs_kmeans_path(k2: int, d: int) -> str:
+    """'tc' or 'ffma': the k-means distance kernel cabs_kmeans(_pair) runs for (k2, d)."""
+    return "tc" if cabs_kernel_path(OP_KMEANS, k2, d) == PATH_TC else "ffma"
+
+
+def cabs_residual_path(ncomp: int) -> str:
+    return "tc" if cabs_kernel_path(OP_RESIDUAL, ncomp) == PATH_TC else "ffma"
 
 
 def cabs_version():

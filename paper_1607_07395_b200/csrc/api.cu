@@ -100,6 +100,13 @@ int32_t cabs_debug_counters(int64_t* out, int32_t n) {
 
 int64_t cabs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+int32_t cabs_kernel_path(int32_t op, int32_t k, int32_t d) {
+  if (op == CABS_OP_KMEANS) return kmeans_tc_selected(k, d) ? CABS_PATH_TC : CABS_PATH_FFMA;
+  if (op == CABS_OP_RESIDUAL) return (k >= 1 && k <= residual_tc_kmax() && !getenv("CABS_RESIDUAL_FFMA")) ? CABS_PATH_TC
+                                                                                                         : CABS_PATH_FFMA;
+  return -1;
+}
+
 void cabs_version(int32_t* major, int32_t* minor) {
   if (major) *major = CABS_VERSION_MAJOR;
   if (minor) *minor = CABS_VERSION_MINOR;

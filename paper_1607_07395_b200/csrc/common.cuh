@@ -34,7 +34,7 @@ struct Ws {
   size_t dist2, cand_d2, cand_i2, cand_all2;  // ... and slot 1 (cabs_select_pair)
   size_t hcand, idx;
   size_t cb, rb, wb;
-  size_t res_part, res_split;  // res_split: G_hi, G_lo (n x 64 each)
+  size_t res_part, res_split;  // res_split: G_hi, G_lo (n x round_up(ncomp, 32) each, <= 192)
   size_t hcand_side;
   size_t orth_part, orth;  // cabs_orthogonalize: Gram partials | gram, U_K, V_K, sigma, r, K, T_U, T_V
   size_t total;
@@ -101,7 +101,7 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.rb = take(sizeof(float) * K * w.ldrb);
   w.wb = take(sizeof(float) * K * Kp);
   w.res_part = take(sizeof(double) * 2 * kResGrid);
-  w.res_split = take(sizeof(float) * 2 * (size_t)p.n * 64);
+  w.res_split = take(sizeof(float) * 2 * (size_t)p.n * (Kp < 192 ? Kp : 192));  // G hi/lo, pitch round_up(ncomp, 32)
   w.total = off;
   return w;
 }

@@ -6,13 +6,14 @@
 //
 // Persistent, warp-specialised, one CTA per SM, tiles of 128 rows x 128 columns:
 //   warp 0   TMA producer of the A stream (quarter tiles of 128 x 32, 6-deep ring)
-//   warp 6   TMA producer of the G_hi/G_lo column tiles (2-deep ring), on its own
-//            thread so that a full A ring never delays the next tile's MMA operands
+//   warp 6   TMA producer of the G_hi/G_lo column tiles in 32-wide K chunks (4-deep ring of
+//            hi+lo chunk pairs), on its own thread so that a full A ring never delays the
+//            next tile's MMA operands
 //   warp 1   TMEM allocator + single-thread MMA issuer.  The row band's F_hi/F_lo
-//            live in TMEM (double-buffered across bands) and are the MMA's A operand,
+//            live in TMEM (double-buffered across bands when K <= 64) and are the MMA's A operand,
 //            so every MMA reads only its 128 x 8 G slice from shared memory (an SS MMA
 //            would re-read 4 KB of F per instruction and saturate shared memory).
-//            Per 8-wide k step: D += Fh Gh^T + Fh Gl^T + Fl Gh^T (TMEM, 2 stages).
+//            Per 8-wide k step: D += Fh Gh^T + Fh Gl^T + Fl Gh^T (TMEM, 2 stages; 1 when K > 128).
 //   warps 2-5 epilogue (group 0): split F diag(s) rows into TF32 hi/lo and write them into
 //            TMEM one band ahead; per tile, tcgen05.ld the accumulator row (lane = row) for
 //            columns [0, 64), read the A row from the 128B-swizzled smem boxes, accumulate
@@ -20,7 +21,8 @@
 //   warps 7-10 epilogue (group 1): the same for columns [64, 128) (two warps per TMEM lane
 //            quarter: the epilogue, which bounds the kernel otherwise, runs at twice the rate).
 // Tile order is row-band major over a static contiguous tile range per CTA; fixed-order
-// block and grid reductions: bit-reproducible.  Requires ncomp <= 64.
+// block and grid reductions: bit-reproducible.  ncomp <= 192 (K padded to a multiple of 32;
+// G streamed in 32-wide K chunks through a 4-deep ring; TMEM plan in tmem_plan()).
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
@@ -29,28 +31,40 @@ namespace cabsk {
 
 constexpr int kTcBM = 128, kTcBN = 128;            // N = 128: a full-rate tcgen05 shape (N <= 96 is
                                                     // bound by a ~47-cycle per-instruction floor)
-constexpr int kAS = 6, kGS = 2, kCS = 2;            // A quarter-tile / G tile / TMEM accumulator stages
+constexpr int kAS = 6, kGS = 4;                     // A quarter-tile stages / G chunk stages
 constexpr int kAQ = kTcBN / 32;                     // A boxes (128 x 32) per tile
 constexpr int kHalfAQ = kAQ / 2;                    // boxes per epilogue group and tile
 constexpr int kTcThreads = 352;                     // 0 TMA (A), 1 MMA, 2-5 + 7-10 epilogue, 6 TMA (G)
 constexpr int kEpiWarps = 8;
 constexpr int kAR = kAS / 2;                       // A ring slots per epilogue group (its own ring: a
                                                     // group never waits on a slot phase of the other)
-constexpr int kKp = 64;                             // K padded (two 32-float swizzle atoms)
-constexpr uint32_t kGAtomBytes = kTcBN * 128;      // 16 KB
+constexpr int kResKpMax = 192;                      // largest padded K (hi + lo F in TMEM + 1 acc stage)
+constexpr uint32_t kGAtomBytes = kTcBN * 128;      // 16 KB: 128 G rows x 32 floats (one K chunk)
 constexpr uint32_t kABoxBytes = kTcBM * 128;       // 16 KB: 128 rows x 32 floats = a quarter A tile
-// TMEM columns: [0, 256) accumulators (2 stages x 128); [256, 512) F buffers (2 x {hi 64 | lo 64})
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kFCol0 = kCS * kTcBN;
+
+// TMEM plan for a padded K (a multiple of 32): accumulator stages of 128 columns, then the F
+// buffers ({hi Kp | lo Kp} each).  Kp <= 64: 2 acc + 2 F (F double-buffered across bands);
+// Kp <= 128: 2 acc + 1 F; Kp <= 192: 1 acc + 1 F.
+struct TmemPlan {
+  int kp, nacc, nf;
+  __host__ __device__ uint32_t fcol0() const { return static_cast<uint32_t>(nacc * kTcBN); }
+};
+inline TmemPlan tmem_plan(int kp) {
+  TmemPlan t{kp, 2, 2};
+  if (kp > 64) t.nf = 1;
+  if (kp > 128) t.nacc = 1;
+  return t;
+}
 
 struct TcSmem {
-  uint8_t gh[kGS][2][kGAtomBytes];  // 1024-byte aligned 128B-swizzle atoms
-  uint8_t gl[kGS][2][kGAtomBytes];
+  uint8_t gh[kGS][kGAtomBytes];  // 1024-byte aligned 128B-swizzle atoms: one K chunk of a G tile
+  uint8_t gl[kGS][kGAtomBytes];
   uint8_t a[kAS][kABoxBytes];
   uint64_t f_ready[2], f_free[2];
   uint64_t g_full[kGS], g_empty[kGS];
   uint64_t a_full[kAS], a_empty[kAS];
-  uint64_t acc_full[kCS], acc_empty[kCS];
+  uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
   double red[2][kEpiWarps];
 };
@@ -115,8 +129,8 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       : "memory");
 }
 
-// Epilogue warps: row r of F diag(s), split into TF32 hi + exact lo, -> TMEM buffer fb
-// (row = lane quarter q * 32 + lane; hi in columns [0, 64), lo in [64, 128)).
+// Epilogue warps: row r of F diag(s), split into TF32 hi + exact lo, -> TMEM F buffer at
+// column fcol (row = lane quarter q * 32 + lane; hi in columns [0, Kp), lo in [Kp, 2 Kp)).
 struct FArgs {
   const float* f;
   int64_t ldf;
@@ -125,18 +139,17 @@ struct FArgs {
   bool vec;        // f and ldf 16-byte aligned
 };
 
-__device__ __forceinline__ void load_f_band(const FArgs& F, int64_t m, int64_t rb, int q, int lane, uint32_t tmem,
-                                            int fb, uint64_t* ready) {
+__device__ __forceinline__ void load_f_band(const FArgs& F, int64_t m, int64_t rb, int q, int lane, uint32_t fcol,
+                                            int kp, uint64_t* ready) {
   const int64_t r = rb * kTcBM + q * 32 + lane;
-  const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + kFCol0 + static_cast<uint32_t>(fb * 2 * kKp);
+  const uint32_t tq = fcol + (static_cast<uint32_t>(q * 32) << 16);
   const float* src = F.f + (r < m ? r : 0) * F.ldf;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {  // columns [32 half, 32 half + 32)
+  for (int a = 0; a < kp / 32; ++a) {  // K chunk [32 a, 32 a + 32)
     float x[32];
     if (F.vec) {
 #pragma unroll
       for (int c = 0; c < 32; c += 4) {
-        const int col = 32 * half + c;
+        const int col = 32 * a + c;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (r < m && col < F.ncomp) v = __ldg(reinterpret_cast<const float4*>(src + col));
         x[c] = v.x; x[c + 1] = v.y; x[c + 2] = v.z; x[c + 3] = v.w;
@@ -144,20 +157,20 @@ __device__ __forceinline__ void load_f_band(const FArgs& F, int64_t m, int64_t r
     } else {
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
-        const int col = 32 * half + c;
+        const int col = 32 * a + c;
         x[c] = (r < m && col < F.ncomp) ? __ldg(src + col) : 0.f;
       }
     }
     float hi[32], lo[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
-      const int col = 32 * half + c;
+      const int col = 32 * a + c;
       const float v = col < F.ncomp ? x[c] * (F.s ? __ldg(F.s + col) : 1.f) : 0.f;
       hi[c] = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);  // TF32 operand bits
       lo[c] = v - hi[c];                                            // exact
     }
-    tmem_st32(tq + static_cast<uint32_t>(32 * half), hi);
-    tmem_st32(tq + static_cast<uint32_t>(kKp + 32 * half), lo);
+    tmem_st32(tq + static_cast<uint32_t>(32 * a), hi);
+    tmem_st32(tq + static_cast<uint32_t>(kp + 32 * a), lo);
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   tc::fence_before_sync();
@@ -168,14 +181,15 @@ __device__ __forceinline__ void load_f_band(const FArgs& F, int64_t m, int64_t r
 __global__ void __launch_bounds__(kTcThreads, 1)
 residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmGh,
                    const __grid_constant__ CUtensorMap tmGl, const FArgs fa, int64_t m, int64_t n, int ksteps,
-                   double* __restrict__ part) {
+                   const TmemPlan tp, double* __restrict__ part, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntr = ceil_div(m, kTcBM), ntc = ceil_div(n, kTcBN);
   const int64_t T = ntr * ntc;
   const int64_t t_beg = (T * blockIdx.x) / gridDim.x, t_end = (T * (blockIdx.x + 1)) / gridDim.x;
-  const int katoms = ksteps > 4 ? 2 : 1;  // 8-wide k steps per 32-float atom = 4
+  const int nch = (ksteps + 3) / 4;  // K chunks (32 floats = 4 k steps of 8) per tile
+  const int kp = tp.kp, nacc = tp.nacc, nf = tp.nf;
   const int64_t rb0 = t_beg / ntc, nbands = (t_end - 1) / ntc - rb0 + 1;
 
   if (warp == 0 && lane == 0) {
@@ -183,7 +197,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     for (int b = 0; b < 2; ++b) { tc::mbar_init(&S.f_ready[b], 4); tc::mbar_init(&S.f_free[b], 1); }
     for (int s = 0; s < kGS; ++s) { tc::mbar_init(&S.g_full[s], 1); tc::mbar_init(&S.g_empty[s], 1); }
     for (int s = 0; s < kAS; ++s) { tc::mbar_init(&S.a_full[s], 1); tc::mbar_init(&S.a_empty[s], 4); }
-    for (int s = 0; s < kCS; ++s) { tc::mbar_init(&S.acc_full[s], 1); tc::mbar_init(&S.acc_empty[s], kEpiWarps); }
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&S.acc_full[s], 1); tc::mbar_init(&S.acc_empty[s], kEpiWarps); }
     tc::mbar_fence_init();
   }
   if (warp == 1) tc::tmem_alloc(&S.tmem_base, kTmemCols);
@@ -191,6 +205,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem_base;
+  const uint32_t fcol0 = tmem + tp.fcol0();
 #ifdef CABS_PROFILE_RES
   long long prof[16] = {0};
   const long long t_start = clock64();
@@ -199,6 +214,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      const uint64_t pol = tc::policy_evict_first();  // A is read exactly once
       for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
         const int64_t rb = t / ntc, cb = t % ntc;
         // A (the HBM stream the kernel is bound by): kAQ boxes of 128 x 32 per tile
@@ -208,24 +224,34 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           const int64_t li = kHalfAQ * i + (h % kHalfAQ);
           const int sa = (h / kHalfAQ) * kAR + static_cast<int>(li % kAR);
           if (li >= kAR) RES_WAIT(1, tc::mbar_wait(&S.a_empty[sa], ring_parity(li - kAR, kAR)));
+          if ((dbg & 4) && i > 0) {  // diagnostics: no A traffic after the first tile
+            tc::mbar_arrive(&S.a_full[sa]);
+            continue;
+          }
           tc::mbar_expect_tx(&S.a_full[sa], kABoxBytes);
-          tc::tma_load_2d(S.a[sa], &tmA, static_cast<int>(cb * kTcBN + 32 * h), static_cast<int>(rb * kTcBM),
-                          &S.a_full[sa]);
+          tc::tma_load_2d_hint(S.a[sa], &tmA, static_cast<int>(cb * kTcBN + 32 * h), static_cast<int>(rb * kTcBM),
+                               &S.a_full[sa], pol);
         }
       }
     }
   } else if (warp == 6) {
-    // ------------------------------------------------------------ TMA producer (G tiles), its own
+    // ------------------------------------------------------------ TMA producer (G chunks), its own
     // thread so that a full A ring never delays the next tile's MMA operands
     if (lane == 0) {
-      for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
+      const uint64_t pol = tc::policy_evict_last();  // G is re-read by every row band
+      int64_t j = 0;  // chunk sequence number
+      for (int64_t t = t_beg; t < t_end; ++t) {
         const int64_t cb = t % ntc;
-        const int sg = static_cast<int>(i % kGS);
-        if (i >= kGS) RES_WAIT(2, tc::mbar_wait(&S.g_empty[sg], ring_parity(i - kGS, kGS)));
-        tc::mbar_expect_tx(&S.g_full[sg], 2 * katoms * kGAtomBytes);
-        for (int a = 0; a < katoms; ++a) {
-          tc::tma_load_2d(S.gh[sg][a], &tmGh, a * 32, static_cast<int>(cb * kTcBN), &S.g_full[sg]);
-          tc::tma_load_2d(S.gl[sg][a], &tmGl, a * 32, static_cast<int>(cb * kTcBN), &S.g_full[sg]);
+        for (int c = 0; c < nch; ++c, ++j) {
+          const int sg = static_cast<int>(j % kGS);
+          if (j >= kGS) RES_WAIT(2, tc::mbar_wait(&S.g_empty[sg], ring_parity(j - kGS, kGS)));
+          if ((dbg & 2) && j >= kGS) {  // diagnostics: no G traffic after the first ring fill
+            tc::mbar_arrive(&S.g_full[sg]);
+            continue;
+          }
+          tc::mbar_expect_tx(&S.g_full[sg], 2 * kGAtomBytes);
+          tc::tma_load_2d_hint(S.gh[sg], &tmGh, c * 32, static_cast<int>(cb * kTcBN), &S.g_full[sg], pol);
+          tc::tma_load_2d_hint(S.gl[sg], &tmGl, c * 32, static_cast<int>(cb * kTcBN), &S.g_full[sg], pol);
         }
       }
     }
@@ -233,41 +259,42 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     // ------------------------------------------------------------ MMA issuer (A operand = F in TMEM)
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_tf32(kTcBM, kTcBN);
-      uint64_t dgh[kGS][2], dgl[kGS][2];
+      uint64_t dgh[kGS], dgl[kGS];
 #pragma unroll
-      for (int g = 0; g < kGS; ++g)
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          dgh[g][a] = tc::desc_sw128(tc::smem_u32(S.gh[g][a]));
-          dgl[g][a] = tc::desc_sw128(tc::smem_u32(S.gl[g][a]));
-        }
-      int64_t prev_rb = -1, band = -1;
+      for (int g = 0; g < kGS; ++g) {
+        dgh[g] = tc::desc_sw128(tc::smem_u32(S.gh[g]));
+        dgl[g] = tc::desc_sw128(tc::smem_u32(S.gl[g]));
+      }
+      int64_t prev_rb = -1, band = -1, j = 0;
       uint32_t fcol = 0;
       for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
         const int64_t rb = t / ntc;
-        const int sg = static_cast<int>(i % kGS), sc = static_cast<int>(i % kCS);
+        const int sc = static_cast<int>(i % nacc);
         if (rb != prev_rb) {
-          if (band >= 0) tc::mma_commit(&S.f_free[band & 1]);  // previous band's F no longer read
+          if (band >= 0) tc::mma_commit(&S.f_free[band % nf]);  // previous band's F no longer read
           ++band;
-          RES_WAIT(4, tc::mbar_wait(&S.f_ready[band & 1], static_cast<uint32_t>((band >> 1) & 1)));
-          fcol = tmem + kFCol0 + static_cast<uint32_t>((band & 1) * 2 * kKp);
+          RES_WAIT(4, tc::mbar_wait(&S.f_ready[band % nf], static_cast<uint32_t>((band / nf) & 1)));
+          fcol = fcol0 + static_cast<uint32_t>((band % nf) * 2 * kp);
           prev_rb = rb;
         }
-        RES_WAIT(5, tc::mbar_wait(&S.g_full[sg], ring_parity(i, kGS)));
-        if (i >= kCS) RES_WAIT(6, tc::mbar_wait(&S.acc_empty[sc], ring_parity(i - kCS, kCS)));
+        if (i >= nacc) RES_WAIT(6, tc::mbar_wait(&S.acc_empty[sc], ring_parity(i - nacc, nacc)));
         tc::fence_after_sync();
         const uint32_t d = tmem + static_cast<uint32_t>(sc * kTcBN);
-        for (int kk = 0; kk < ksteps; ++kk) {
-          const int a = kk >> 2;
-          const uint64_t off = static_cast<uint64_t>((kk & 3) * 2);
-          const uint64_t gh = (sg == 0 ? dgh[0][a] : dgh[1][a]) + off;
-          const uint64_t gl = (sg == 0 ? dgl[0][a] : dgl[1][a]) + off;
-          const uint32_t fh_t = fcol + static_cast<uint32_t>(kk * 8), fl_t = fh_t + kKp;
-          mma_tf32_ts(d, fh_t, gh, idesc, kk > 0 ? 1u : 0u);
-          mma_tf32_ts(d, fh_t, gl, idesc, 1u);
-          mma_tf32_ts(d, fl_t, gh, idesc, 1u);
+        for (int c = 0; c < nch; ++c, ++j) {
+          const int sg = static_cast<int>(j % kGS);
+          RES_WAIT(5, tc::mbar_wait(&S.g_full[sg], ring_parity(j, kGS)));
+          tc::fence_after_sync();
+          const int kk1 = (4 * c + 4 < ksteps) ? 4 * c + 4 : ksteps;
+          for (int kk = 4 * c; kk < kk1; ++kk) {
+            const uint64_t off = static_cast<uint64_t>((kk & 3) * 2);  // 32 B per k step, in 16-byte units
+            const uint32_t fh_t = fcol + static_cast<uint32_t>(kk * 8), fl_t = fh_t + static_cast<uint32_t>(kp);
+            mma_tf32_ts(d, fh_t, dgh[sg] + off, idesc, kk > 0 ? 1u : 0u);
+            if (dbg & 8) continue;  // diagnostics: 1xTF32
+            mma_tf32_ts(d, fh_t, dgl[sg] + off, idesc, 1u);
+            mma_tf32_ts(d, fl_t, dgh[sg] + off, idesc, 1u);
+          }
+          tc::mma_commit(&S.g_empty[sg]);
         }
-        tc::mma_commit(&S.g_empty[sg]);
         tc::mma_commit(&S.acc_full[sc]);
       }
     }
@@ -278,27 +305,28 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     constexpr int kHalf = kAQ / 2;
     {
     const int row = q * 32 + lane;    // row within the 128-row tile
-    // F of the first two bands, then one band ahead of the MMA (group 0 only)
+    // F of the first band(s) (group 0 only): nf = 2 stages band j + 1 while band j runs; nf = 1
+    // loads band j + 1 once the MMA has released band j (at the band's last tile)
     if (eg == 0) {
-      load_f_band(fa, m, rb0, q, lane, tmem, 0, &S.f_ready[0]);
-      if (nbands > 1) load_f_band(fa, m, rb0 + 1, q, lane, tmem, 1, &S.f_ready[1]);
+      load_f_band(fa, m, rb0, q, lane, fcol0, kp, &S.f_ready[0]);
+      if (nf == 2 && nbands > 1) load_f_band(fa, m, rb0 + 1, q, lane, fcol0 + 2 * kp, kp, &S.f_ready[1]);
     }
     double r2 = 0.0, a2 = 0.0;
     int64_t prev_rb = rb0;
     for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
       const int64_t rb = t / ntc;
-      if (rb != prev_rb && eg == 0) {  // entering band j = rb - rb0: stage band j + 1 into the buffer band j - 1 used
+      if (nf == 2 && rb != prev_rb && eg == 0) {  // entering band j: stage band j + 1 into band j - 1's buffer
         prev_rb = rb;
-        const int64_t j = rb - rb0;
-        if (j + 1 < nbands) {
-          const int fb = static_cast<int>((j + 1) & 1);
-          tc::mbar_wait(&S.f_free[fb], static_cast<uint32_t>(((j - 1) >> 1) & 1));
+        const int64_t jb = rb - rb0;
+        if (jb + 1 < nbands) {
+          const int fb = static_cast<int>((jb + 1) & 1);
+          tc::mbar_wait(&S.f_free[fb], static_cast<uint32_t>(((jb - 1) >> 1) & 1));
           tc::fence_after_sync();
-          load_f_band(fa, m, rb + 1, q, lane, tmem, fb, &S.f_ready[fb]);
+          load_f_band(fa, m, rb + 1, q, lane, fcol0 + static_cast<uint32_t>(fb * 2 * kp), kp, &S.f_ready[fb]);
         }
       }
-      const int sc = static_cast<int>(i % kCS);
-      RES_WAIT(11, tc::mbar_wait(&S.acc_full[sc], ring_parity(i, kCS)));
+      const int sc = static_cast<int>(i % nacc);
+      RES_WAIT(11, tc::mbar_wait(&S.acc_full[sc], ring_parity(i, nacc)));
       tc::fence_after_sync();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(sc * kTcBN);
       float tr0 = 0.f, ta0 = 0.f, tr1 = 0.f, ta1 = 0.f;
@@ -324,6 +352,12 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         for (int hh = 0; hh < kHalf; ++hh)
           tc::mbar_arrive(&S.a_empty[eg * kAR + static_cast<int>((kHalfAQ * i + hh) % kAR)]);
       }
+      if (dbg & 1) {  // diagnostics: no TMEM loads / arithmetic in the epilogue
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);
+        continue;
+      }
       float v[kHalf][32];
 #pragma unroll
       for (int hh = 0; hh < kHalf; ++hh) tmem_ld32_nowait(tbase + 32 * (kHalf * eg + hh), v[hh]);
@@ -333,6 +367,14 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);
+      // nf = 1: the band's last tile is in registers; the MMA released the F buffer when it
+      // finished this tile (f_free commits after the tile's MMAs): load the next band now
+      if (nf == 1 && eg == 0 && t + 1 < t_end && (t + 1) / ntc != rb) {
+        const int64_t jb = rb - rb0;
+        tc::mbar_wait(&S.f_free[0], static_cast<uint32_t>(jb & 1));
+        tc::fence_after_sync();
+        load_f_band(fa, m, rb + 1, q, lane, fcol0, kp, &S.f_ready[0]);
+      }
 #pragma unroll
       for (int hh = 0; hh < kHalf; ++hh)
 #pragma unroll
@@ -378,16 +420,19 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   }
 }
 
-// G_hi = tf32(G), G_lo = G - G_hi (exact), zero-padded to kKp columns; 4 rows x 64 columns per
-// 256-thread block iteration (the F side is split on the fly by the epilogue warps).
+// G_hi = tf32(G), G_lo = G - G_hi (exact), zero-padded to kp columns (row pitch kp); one row per
+// 32-lane group, 8 groups per 256-thread block iteration (the F side is split on the fly by
+// the epilogue warps).
 __global__ void __launch_bounds__(256) split_g_kernel(const float* __restrict__ G, int64_t ldg, int64_t rows, int ncomp,
-                                                      float* __restrict__ hi, float* __restrict__ lo) {
-  const int c = threadIdx.x & (kKp - 1);
-  for (int64_t r = blockIdx.x * 4LL + (threadIdx.x >> 6); r < rows; r += gridDim.x * 4LL) {
-    const float x = c < ncomp ? __ldg(G + r * ldg + c) : 0.f;
-    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-    hi[r * kKp + c] = h;
-    lo[r * kKp + c] = x - h;
+                                                      int kp, float* __restrict__ hi, float* __restrict__ lo) {
+  const int l = threadIdx.x & 31;
+  for (int64_t r = blockIdx.x * 8LL + (threadIdx.x >> 5); r < rows; r += gridDim.x * 8LL) {
+    for (int c = l; c < kp; c += 32) {
+      const float x = c < ncomp ? __ldg(G + r * ldg + c) : 0.f;
+      const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+      hi[r * kp + c] = h;
+      lo[r * kp + c] = x - h;
+    }
   }
 }
 
@@ -429,8 +474,10 @@ void residual_debug_counters(long long* out, int n) {
 #endif
 }
 
+int residual_tc_kmax() { return kResKpMax; }
+
 bool residual_tc_supported(const float* A, int64_t lda, int64_t m_loc, int64_t n, int ncomp) {
-  if (ncomp < 1 || ncomp > kKp || m_loc < 1 || n < 1) return false;
+  if (ncomp < 1 || ncomp > kResKpMax || m_loc < 1 || n < 1) return false;
   if ((lda % 4) != 0 || (reinterpret_cast<uintptr_t>(A) & 15) != 0) return false;
   if (m_loc > 0x7fffffff || n > 0x7fffffff) return false;
   if (getenv("CABS_RESIDUAL_FFMA")) return false;
@@ -440,11 +487,12 @@ bool residual_tc_supported(const float* A, int64_t lda, int64_t m_loc, int64_t n
 int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, const float* F, int64_t ldf,
                        const float* s, const float* G, int64_t ldg, int ncomp, float* split, double* part, double* out,
                        cudaStream_t st) {
-  const int kp = kKp;
+  const int kp = static_cast<int>(round_up(ncomp, 32));
+  const TmemPlan tp = tmem_plan(kp);
   float* gh = split;
   float* gl = gh + n * kp;
   note_launch();
-  split_g_kernel<<<4 * kNumSM, 256, 0, st>>>(G, ldg, n, ncomp, gh, gl);
+  split_g_kernel<<<4 * kNumSM, 256, 0, st>>>(G, ldg, n, ncomp, kp, gh, gl);
   FArgs fa{F, ldf, s, ncomp, (reinterpret_cast<uintptr_t>(F) & 15) == 0 && (ldf % 4) == 0};
   CUtensorMap tA, tGh, tGl;
   if (!make_map(&tA, A, n, m_loc, lda, kTcBM) || !make_map(&tGh, gh, kp, n, kp, kTcBN) ||
@@ -463,7 +511,12 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
   int64_t g = T < nsm ? T : nsm;
   const int ksteps = static_cast<int>(ceil_div(ncomp, 8));
   note_launch();
-  residual_tc_kernel<<<static_cast<unsigned>(g), kTcThreads, smem, st>>>(tA, tGh, tGl, fa, m_loc, n, ksteps, part);
+  int dbg = 0;
+#ifdef CABS_PROFILE_RES
+  if (const char* e = getenv("CABS_RES_DBG")) dbg = atoi(e);
+#endif
+  residual_tc_kernel<<<static_cast<unsigned>(g), kTcThreads, smem, st>>>(tA, tGh, tGl, fa, m_loc, n, ksteps, tp, part,
+                                                                          dbg);
   launch_residual_final(part, static_cast<int>(g), out, st);
   return 0;
 }

@@ -322,7 +322,9 @@ def test_sketch_flags_bad_indices(dev):
 
 # ------------------------------------------------------------------ S10 residual
 @pytest.mark.parametrize("m,n,k,use_s", [(2000, 1500, 20, True), (1000, 777, 50, False), (129, 257, 7, True),
-                                         (4096, 2048, 100, True), (300, 200, 1, False)])
+                                         (4096, 2048, 100, True), (300, 200, 1, False), (8000, 1000, 128, True),
+                                         (2600, 1900, 192, True), (5000, 3001, 160, False), (1500, 1300, 200, True),
+                                         (1000, 700, 300, False)])
 def test_residual_matches_oracle(dev, m, n, k, use_s):
     A, T = _A(m, n, m + k, dev, r=k)
     g = np.random.default_rng(k)
@@ -343,9 +345,10 @@ def test_residual_matches_oracle(dev, m, n, k, use_s):
     assert abs(math.sqrt(o[0]) - math.sqrt(r2)) <= 1e-4 * math.sqrt(r2) + 1e-6 * math.sqrt(a2)
 
 
-def test_residual_exact_factorisation_is_small(dev):
+@pytest.mark.parametrize("k", [16, 120, 190])
+def test_residual_exact_factorisation_is_small(dev, k):
     # A = F G^T exactly representable: residual at the FP32 rounding floor, far below ||A||
-    m, n, k = 1024, 768, 16
+    m, n = 1024, 768
     g = np.random.default_rng(0)
     F = g.integers(-3, 4, (m, k)).astype(np.float32)
     G = g.integers(-3, 4, (n, k)).astype(np.float32)
@@ -353,8 +356,9 @@ def test_residual_exact_factorisation_is_small(dev):
     plan = _plan(m, n, k)
     ws = _ws(plan, dev)
     out = torch.zeros(2, dtype=torch.float64, device=dev)
-    Ft = torch.zeros((m, 32), device=dev); Ft[:, :k] = torch.from_numpy(F).to(dev)
-    Gt = torch.zeros((n, 32), device=dev); Gt[:, :k] = torch.from_numpy(G).to(dev)
+    ld = C.cabs_padded_ld(k)
+    Ft = torch.zeros((m, ld), device=dev); Ft[:, :k] = torch.from_numpy(F).to(dev)
+    Gt = torch.zeros((n, ld), device=dev); Gt[:, :k] = torch.from_numpy(G).to(dev)
     C.cabs_residual(plan, torch.from_numpy(A).to(dev), Ft, None, Gt, k, out, ws)
     assert out[0].item() == 0.0 and out[1].item() == float(np.sum(A.astype(np.float64) ** 2))
 
