@@ -83,8 +83,7 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 
 // 32 lanes x 32 columns of 32-bit TMEM -> registers, WITHOUT the wait (the caller issues
@@ -139,9 +138,10 @@ struct FArgs {
   bool vec;        // f and ldf 16-byte aligned
 };
 
-__device__ __forceinline__ void load_f_band(const FArgs& F, int64_t m, int64_t rb, int q, int lane, uint32_t fcol,
-                                            int kp, uint64_t* ready) {
-  const int64_t r = rb * kTcBM + q * 32 + lane;
+template <bool PAIR = false>
+__device__ __forceinline__ void load_f_rows(const FArgs& F, int64_t m, int64_t r0, int q, int lane, uint32_t fcol,
+                                            int kp, uint64_t* ready, uint32_t ready_cluster = 0) {
+  const int64_t r = r0 + q * 32 + lane;
   const uint32_t tq = fcol + (static_cast<uint32_t>(q * 32) << 16);
   const float* src = F.f + (r < m ? r : 0) * F.ldf;
   for (int a = 0; a < kp / 32; ++a) {  // K chunk [32 a, 32 a + 32)
@@ -175,7 +175,15 @@ __device__ __forceinline__ void load_f_band(const FArgs& F, int64_t m, int64_t r
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   tc::fence_before_sync();
   __syncwarp();
-  if (lane == 0) tc::mbar_arrive(ready);
+  if (lane == 0) {
+    if (PAIR) tc::mbar_arrive_cluster(ready_cluster);
+    else tc::mbar_arrive(ready);
+  }
+}
+
+__device__ __forceinline__ void load_f_band(const FArgs& F, int64_t m, int64_t rb, int q, int lane, uint32_t fcol,
+                                            int kp, uint64_t* ready) {
+  load_f_rows<false>(F, m, rb * kTcBM, q, lane, fcol, kp, ready);
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -256,22 +264,23 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (A operand = F in TMEM)
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (A operand = F in TMEM).
+    // The whole warp runs the (warp-uniform) loop so that the operand arithmetic stays in the
+    // uniform datapath; one elected lane issues the MMAs and their commits (a lane-0-only loop
+    // feeds the tensor pipe at ~1/2 rate: tools/ubench_issue2.cu).
+    {
       constexpr uint32_t idesc = tc::idesc_tf32(kTcBM, kTcBN);
-      uint64_t dgh[kGS], dgl[kGS];
-#pragma unroll
-      for (int g = 0; g < kGS; ++g) {
-        dgh[g] = tc::desc_sw128(tc::smem_u32(S.gh[g]));
-        dgl[g] = tc::desc_sw128(tc::smem_u32(S.gl[g]));
-      }
+      // slot descriptors by arithmetic (the start-address field is addr >> 4): a descriptor array
+      // indexed by the runtime slot would live in local memory
+      const uint64_t dgh0 = tc::desc_sw128(tc::smem_u32(S.gh[0])), dgl0 = tc::desc_sw128(tc::smem_u32(S.gl[0]));
       int64_t prev_rb = -1, band = -1, j = 0;
       uint32_t fcol = 0;
       for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
         const int64_t rb = t / ntc;
         const int sc = static_cast<int>(i % nacc);
         if (rb != prev_rb) {
-          if (band >= 0) tc::mma_commit(&S.f_free[band % nf]);  // previous band's F no longer read
+          if (band >= 0 && tc::elect_one()) tc::mma_commit(&S.f_free[band % nf]);  // previous band's F no longer read
+          __syncwarp();
           ++band;
           RES_WAIT(4, tc::mbar_wait(&S.f_ready[band % nf], static_cast<uint32_t>((band / nf) & 1)));
           fcol = fcol0 + static_cast<uint32_t>((band % nf) * 2 * kp);
@@ -284,18 +293,28 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           const int sg = static_cast<int>(j % kGS);
           RES_WAIT(5, tc::mbar_wait(&S.g_full[sg], ring_parity(j, kGS)));
           tc::fence_after_sync();
-          const int kk1 = (4 * c + 4 < ksteps) ? 4 * c + 4 : ksteps;
-          for (int kk = 4 * c; kk < kk1; ++kk) {
-            const uint64_t off = static_cast<uint64_t>((kk & 3) * 2);  // 32 B per k step, in 16-byte units
-            const uint32_t fh_t = fcol + static_cast<uint32_t>(kk * 8), fl_t = fh_t + static_cast<uint32_t>(kp);
-            mma_tf32_ts(d, fh_t, dgh[sg] + off, idesc, kk > 0 ? 1u : 0u);
-            if (dbg & 8) continue;  // diagnostics: 1xTF32
-            mma_tf32_ts(d, fh_t, dgl[sg] + off, idesc, 1u);
-            mma_tf32_ts(d, fl_t, dgh[sg] + off, idesc, 1u);
+          const uint64_t slot = static_cast<uint64_t>(sg) * (kGAtomBytes >> 4);
+          const uint64_t bh = dgh0 + slot, bl = dgl0 + slot;  // + 2 per 8-wide k step (32 B in 16-byte units)
+          const uint32_t fh0 = fcol + static_cast<uint32_t>(32 * c);
+          const int nk = ksteps - 4 * c < 4 ? ksteps - 4 * c : 4;
+          if (tc::elect_one()) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (q < nk) {
+                const uint32_t fh = fh0 + static_cast<uint32_t>(8 * q);
+                mma_tf32_ts(d, fh, bh + 2 * q, idesc, (c | q) ? 1u : 0u);
+                if (!(dbg & 8)) {
+                  mma_tf32_ts(d, fh, bl + 2 * q, idesc, 1u);
+                  mma_tf32_ts(d, fh + static_cast<uint32_t>(kp), bh + 2 * q, idesc, 1u);
+                }
+              }
+            }
+            tc::mma_commit(&S.g_empty[sg]);
           }
-          tc::mma_commit(&S.g_empty[sg]);
+          __syncwarp();
         }
-        tc::mma_commit(&S.acc_full[sc]);
+        if (tc::elect_one()) tc::mma_commit(&S.acc_full[sc]);
+        __syncwarp();
       }
     }
   } else {
@@ -330,43 +349,44 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       tc::fence_after_sync();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(sc * kTcBN);
       float tr0 = 0.f, ta0 = 0.f, tr1 = 0.f, ta1 = 0.f;
-      // both A boxes of this group (rows from 128B-swizzled boxes: 16-byte chunk c of row r is
-      // at chunk c ^ (r & 7)), released as soon as their values are in registers; then both
-      // 32-column halves of the accumulator in one TMEM load batch (one wait)
-      float av[kHalf][32];
+      // the group's two 32-column halves one after the other (register budget): the A box
+      // (rows of a 128B-swizzled box: 16-byte chunk c of row r is at chunk c ^ (r & 7)),
+      // released once in registers, and the matching 32 accumulator columns
 #pragma unroll
       for (int hh = 0; hh < kHalf; ++hh) {
         const int64_t li = kHalfAQ * i + hh;
         const int sa = eg * kAR + static_cast<int>(li % kAR);
+        float av[32], v[32];
+        tmem_ld32_nowait(tbase + 32 * (kHalf * eg + hh), v);
         RES_WAIT(10, tc::mbar_wait(&S.a_full[sa], ring_parity(li, kAR)));
         const uint8_t* arow = S.a[sa] + row * 128;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const float4 a4 = *reinterpret_cast<const float4*>(arow + ((c ^ (row & 7)) << 4));
-          av[hh][4 * c] = a4.x; av[hh][4 * c + 1] = a4.y; av[hh][4 * c + 2] = a4.z; av[hh][4 * c + 3] = a4.w;
+          av[4 * c] = a4.x; av[4 * c + 1] = a4.y; av[4 * c + 2] = a4.z; av[4 * c + 3] = a4.w;
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.a_empty[sa]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tmem_regs_fence(v);
+        if (dbg & 1) {
+#pragma unroll
+          for (int x = 0; x < 32; ++x) v[x] = 0.f;
+        }
+        if (hh == kHalf - 1) {  // the accumulator stage is in registers: release it
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);
+        }
+#pragma unroll
+        for (int x = 0; x < 32; x += 2) {
+          const float e0 = av[x] - v[x], e1 = av[x + 1] - v[x + 1];
+          tr0 = fmaf(e0, e0, tr0);
+          ta0 = fmaf(av[x], av[x], ta0);
+          tr1 = fmaf(e1, e1, tr1);
+          ta1 = fmaf(av[x + 1], av[x + 1], ta1);
         }
       }
-      __syncwarp();
-      if (lane == 0) {
-#pragma unroll
-        for (int hh = 0; hh < kHalf; ++hh)
-          tc::mbar_arrive(&S.a_empty[eg * kAR + static_cast<int>((kHalfAQ * i + hh) % kAR)]);
-      }
-      if (dbg & 1) {  // diagnostics: no TMEM loads / arithmetic in the epilogue
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);
-        continue;
-      }
-      float v[kHalf][32];
-#pragma unroll
-      for (int hh = 0; hh < kHalf; ++hh) tmem_ld32_nowait(tbase + 32 * (kHalf * eg + hh), v[hh]);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int hh = 0; hh < kHalf; ++hh) tmem_regs_fence(v[hh]);
-      tc::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);
       // nf = 1: the band's last tile is in registers; the MMA released the F buffer when it
       // finished this tile (f_free commits after the tile's MMAs): load the next band now
       if (nf == 1 && eg == 0 && t + 1 < t_end && (t + 1) / ntc != rb) {
@@ -375,16 +395,6 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         tc::fence_after_sync();
         load_f_band(fa, m, rb + 1, q, lane, fcol0, kp, &S.f_ready[0]);
       }
-#pragma unroll
-      for (int hh = 0; hh < kHalf; ++hh)
-#pragma unroll
-        for (int x = 0; x < 32; x += 2) {
-          const float e0 = av[hh][x] - v[hh][x], e1 = av[hh][x + 1] - v[hh][x + 1];
-          tr0 = fmaf(e0, e0, tr0);
-          ta0 = fmaf(av[hh][x], av[hh][x], ta0);
-          tr1 = fmaf(e1, e1, tr1);
-          ta1 = fmaf(av[hh][x + 1], av[hh][x + 1], ta1);
-        }
       r2 += static_cast<double>(tr0 + tr1);
       a2 += static_cast<double>(ta0 + ta1);
     }
@@ -412,6 +422,245 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   if (threadIdx.x == 0) {
     double r2 = 0.0, a2 = 0.0;
     for (int e = 0; e < kEpiWarps; ++e) {  // fixed order
+      r2 += S.red[0][e];
+      a2 += S.red[1][e];
+    }
+    part[2 * blockIdx.x] = r2;
+    part[2 * blockIdx.x + 1] = a2;
+  }
+}
+
+// ---------------------------------------------------------------- CTA-pair variant (default)
+// The same pipeline over a CTA pair (cta_group::2): a tile is 256 rows x 128 columns, the
+// leader's MMA (M = 256) takes rows 0-127 of F from the leader's TMEM and rows 128-255 from
+// the peer's, and each CTA holds only HALF of the G tile (64 of its 128 rows) in its shared
+// memory.  Per output element the G bytes streamed from L2 and read by the tensor core halve,
+// which is what bounds the single-CTA kernel once K grows past ~32.  Each CTA streams and
+// reduces its own 128 rows of A.  Barriers the leader's MMA waits on (f_ready, g_full,
+// acc_empty) live in the leader and receive the peer's arrivals (remote arrive / cta_group::2
+// TMA); the MMA's commits are multicast to both CTAs.
+constexpr int kGS2 = 8;                             // G half-chunk stages
+constexpr uint32_t kGHalfBytes = (kTcBN / 2) * 128;  // 8 KB: 64 G rows x 32 floats
+
+struct Tc2Smem {
+  uint8_t gh[kGS2][kGHalfBytes];  // 1024-byte aligned 128B-swizzle atoms (64 rows)
+  uint8_t gl[kGS2][kGHalfBytes];
+  uint8_t a[kAS][kABoxBytes];
+  uint64_t f_ready[2], f_free[2];
+  uint64_t g_full[kGS2], g_empty[kGS2];
+  uint64_t a_full[kAS], a_empty[kAS];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+  double red[2][kEpiWarps];
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1) __cluster_dims__(2, 1, 1)
+residual_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmGh,
+                    const __grid_constant__ CUtensorMap tmGl, const FArgs fa, int64_t m, int64_t n, int ksteps,
+                    const TmemPlan tp, double* __restrict__ part) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Tc2Smem& S = *reinterpret_cast<Tc2Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cr = tc::cluster_rank();  // 0 = leader (issues the MMAs)
+  const int64_t pair = blockIdx.x >> 1, npair = gridDim.x >> 1;
+  constexpr int kPM = 2 * kTcBM;  // rows per pair tile
+  const int64_t ntr = ceil_div(m, kPM), ntc = ceil_div(n, kTcBN);
+  const int64_t T = ntr * ntc;
+  const int64_t t_beg = (T * pair) / npair, t_end = (T * (pair + 1)) / npair;
+  const int nch = (ksteps + 3) / 4;
+  const int kp = tp.kp, nacc = tp.nacc, nf = tp.nf;
+  const int64_t rb0 = t_beg / ntc, nbands = (t_end - 1) / ntc - rb0 + 1;
+  const int64_t my_row0 = static_cast<int64_t>(cr) * kTcBM;  // this CTA's rows within a pair tile
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmA); tc::tma_prefetch(&tmGh); tc::tma_prefetch(&tmGl);
+    for (int b = 0; b < 2; ++b) { tc::mbar_init(&S.f_ready[b], 8); tc::mbar_init(&S.f_free[b], 1); }
+    for (int s = 0; s < kGS2; ++s) { tc::mbar_init(&S.g_full[s], 1); tc::mbar_init(&S.g_empty[s], 1); }
+    for (int s = 0; s < kAS; ++s) { tc::mbar_init(&S.a_full[s], 1); tc::mbar_init(&S.a_empty[s], 4); }
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&S.acc_full[s], 1); tc::mbar_init(&S.acc_empty[s], 2 * kEpiWarps); }
+    tc::mbar_fence_init();
+  }
+  if (warp == 1) tc::tmem_alloc_pair(&S.tmem_base, kTmemCols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::fence_after_sync();
+  const uint32_t tmem = S.tmem_base;
+  const uint32_t fcol0 = tmem + tp.fcol0();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer of this CTA's A rows
+    if (lane == 0) {
+      const uint64_t pol = tc::policy_evict_first();
+      for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
+        const int64_t rb = t / ntc, cb = t % ntc;
+        for (int h = 0; h < kAQ; ++h) {
+          const int64_t li = kHalfAQ * i + (h % kHalfAQ);
+          const int sa = (h / kHalfAQ) * kAR + static_cast<int>(li % kAR);
+          if (li >= kAR) tc::mbar_wait(&S.a_empty[sa], ring_parity(li - kAR, kAR));
+          tc::mbar_expect_tx(&S.a_full[sa], kABoxBytes);
+          tc::tma_load_2d_hint(S.a[sa], &tmA, static_cast<int>(cb * kTcBN + 32 * h),
+                               static_cast<int>(rb * kPM + my_row0), &S.a_full[sa], pol);
+        }
+      }
+    }
+  } else if (warp == 6) {
+    // ------------------------------------------------------------ TMA producer of this CTA's half of G
+    if (lane == 0) {
+      const uint64_t pol = tc::policy_evict_last();
+      int64_t j = 0;
+      for (int64_t t = t_beg; t < t_end; ++t) {
+        const int64_t cb = t % ntc;
+        for (int c = 0; c < nch; ++c, ++j) {
+          const int sg = static_cast<int>(j % kGS2);
+          if (j >= kGS2) tc::mbar_wait(&S.g_empty[sg], ring_parity(j - kGS2, kGS2));
+          if (cr == 0) tc::mbar_expect_tx(&S.g_full[sg], 2 * 2 * kGHalfBytes);  // both halves land on the leader's barrier
+          const uint32_t bar = tc::mapa(&S.g_full[sg], 0);
+          const int y = static_cast<int>(cb * kTcBN + cr * (kTcBN / 2));
+          tc::tma_load_2d_pair(S.gh[sg], &tmGh, c * 32, y, bar, pol);
+          tc::tma_load_2d_pair(S.gl[sg], &tmGl, c * 32, y, bar, pol);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only; whole warp,
+    // one elected lane issues: see the single-CTA kernel)
+    if (cr == 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(kPM, kTcBN);
+      const uint64_t dgh0 = tc::desc_sw128(tc::smem_u32(S.gh[0])), dgl0 = tc::desc_sw128(tc::smem_u32(S.gl[0]));
+      int64_t prev_rb = -1, band = -1, j = 0;
+      uint32_t fcol = 0;
+      for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
+        const int64_t rb = t / ntc;
+        const int sc = static_cast<int>(i % nacc);
+        if (rb != prev_rb) {
+          if (band >= 0 && tc::elect_one()) tc::mma_commit_pair(&S.f_free[band % nf], 3);
+          __syncwarp();
+          ++band;
+          tc::mbar_wait_acq_cluster(&S.f_ready[band % nf], static_cast<uint32_t>((band / nf) & 1));
+          fcol = fcol0 + static_cast<uint32_t>((band % nf) * 2 * kp);
+          prev_rb = rb;
+        }
+        if (i >= nacc) tc::mbar_wait_acq_cluster(&S.acc_empty[sc], ring_parity(i - nacc, nacc));
+        tc::fence_after_sync();
+        const uint32_t d = tmem + static_cast<uint32_t>(sc * kTcBN);
+        for (int c = 0; c < nch; ++c, ++j) {
+          const int sg = static_cast<int>(j % kGS2);
+          tc::mbar_wait(&S.g_full[sg], ring_parity(j, kGS2));
+          tc::fence_after_sync();
+          const uint64_t slot = static_cast<uint64_t>(sg) * (kGHalfBytes >> 4);
+          const uint64_t bh = dgh0 + slot, bl = dgl0 + slot;
+          const uint32_t fh0 = fcol + static_cast<uint32_t>(32 * c);
+          const int nk = ksteps - 4 * c < 4 ? ksteps - 4 * c : 4;
+          if (tc::elect_one()) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (q < nk) {
+                const uint32_t fh = fh0 + static_cast<uint32_t>(8 * q);
+                tc::mma_tf32_ts_pair(d, fh, bh + 2 * q, idesc, (c | q) ? 1u : 0u);
+                tc::mma_tf32_ts_pair(d, fh, bl + 2 * q, idesc, 1u);
+                tc::mma_tf32_ts_pair(d, fh + static_cast<uint32_t>(kp), bh + 2 * q, idesc, 1u);
+              }
+            }
+            tc::mma_commit_pair(&S.g_empty[sg], 3);
+          }
+          __syncwarp();
+        }
+        if (tc::elect_one()) tc::mma_commit_pair(&S.acc_full[sc], 3);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2-5, 7-10), both CTAs
+    const int q = warp & 3;
+    const int eg = warp >= 7 ? 1 : 0;
+    constexpr int kHalf = kAQ / 2;
+    const int row = q * 32 + lane;
+    const uint32_t f_ready_l0 = tc::mapa(&S.f_ready[0], 0), acc_empty_l0 = tc::mapa(&S.acc_empty[0], 0);
+    auto f_ready_l = [&](int b) { return f_ready_l0 + 8u * static_cast<uint32_t>(b); };  // adjacent uint64 barriers
+    auto acc_empty_l = [&](int b) { return acc_empty_l0 + 8u * static_cast<uint32_t>(b); };
+    if (eg == 0) {
+      load_f_rows<true>(fa, m, rb0 * kPM + my_row0, q, lane, fcol0, kp, nullptr, f_ready_l(0));
+      if (nf == 2 && nbands > 1)
+        load_f_rows<true>(fa, m, (rb0 + 1) * kPM + my_row0, q, lane, fcol0 + 2 * kp, kp, nullptr, f_ready_l(1));
+    }
+    double r2 = 0.0, a2 = 0.0;
+    int64_t prev_rb = rb0;
+    for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
+      const int64_t rb = t / ntc;
+      if (nf == 2 && rb != prev_rb && eg == 0) {
+        prev_rb = rb;
+        const int64_t jb = rb - rb0;
+        if (jb + 1 < nbands) {
+          const int fb = static_cast<int>((jb + 1) & 1);
+          tc::mbar_wait(&S.f_free[fb], static_cast<uint32_t>(((jb - 1) >> 1) & 1));
+          tc::fence_after_sync();
+          load_f_rows<true>(fa, m, (rb + 1) * kPM + my_row0, q, lane, fcol0 + static_cast<uint32_t>(fb * 2 * kp), kp,
+                            nullptr, f_ready_l(fb));
+        }
+      }
+      const int sc = static_cast<int>(i % nacc);
+      tc::mbar_wait(&S.acc_full[sc], ring_parity(i, nacc));
+      tc::fence_after_sync();
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(sc * kTcBN);
+      float tr0 = 0.f, ta0 = 0.f, tr1 = 0.f, ta1 = 0.f;
+#pragma unroll
+      for (int hh = 0; hh < kHalf; ++hh) {
+        const int64_t li = kHalfAQ * i + hh;
+        const int sa = eg * kAR + static_cast<int>(li % kAR);
+        float av[32], v[32];
+        tmem_ld32_nowait(tbase + 32 * (kHalf * eg + hh), v);
+        tc::mbar_wait(&S.a_full[sa], ring_parity(li, kAR));
+        const uint8_t* arow = S.a[sa] + row * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 a4 = *reinterpret_cast<const float4*>(arow + ((c ^ (row & 7)) << 4));
+          av[4 * c] = a4.x; av[4 * c + 1] = a4.y; av[4 * c + 2] = a4.z; av[4 * c + 3] = a4.w;
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.a_empty[sa]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tmem_regs_fence(v);
+        if (hh == kHalf - 1) {
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_cluster(acc_empty_l(sc));
+        }
+#pragma unroll
+        for (int x = 0; x < 32; x += 2) {
+          const float e0 = av[x] - v[x], e1 = av[x + 1] - v[x + 1];
+          tr0 = fmaf(e0, e0, tr0);
+          ta0 = fmaf(av[x], av[x], ta0);
+          tr1 = fmaf(e1, e1, tr1);
+          ta1 = fmaf(av[x + 1], av[x + 1], ta1);
+        }
+      }
+      if (nf == 1 && eg == 0 && t + 1 < t_end && (t + 1) / ntc != rb) {
+        const int64_t jb = rb - rb0;
+        tc::mbar_wait(&S.f_free[0], static_cast<uint32_t>(jb & 1));
+        tc::fence_after_sync();
+        load_f_rows<true>(fa, m, (rb + 1) * kPM + my_row0, q, lane, fcol0, kp, nullptr, f_ready_l(0));
+      }
+      r2 += static_cast<double>(tr0 + tr1);
+      a2 += static_cast<double>(ta0 + ta1);
+    }
+    r2 = warp_sum_d(r2);
+    a2 = warp_sum_d(a2);
+    if (lane == 0) {
+      S.red[0][q + 4 * eg] = r2;
+      S.red[1][q + 4 * eg] = a2;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();  // the leader's last MMAs (which read this CTA's TMEM) are complete
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc_pair(tmem, kTmemCols);
+  }
+  if (threadIdx.x == 0) {
+    double r2 = 0.0, a2 = 0.0;
+    for (int e = 0; e < kEpiWarps; ++e) {
       r2 += S.red[0][e];
       a2 += S.red[1][e];
     }
@@ -504,10 +753,28 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
     cudaFuncSetAttribute(residual_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  const int64_t T = ceil_div(m_loc, kTcBM) * ceil_div(n, kTcBN);
   int dev = 0, nsm = kNumSM;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (!getenv("CABS_RESIDUAL_1SM")) {  // CTA-pair kernel (default)
+    CUtensorMap tGh2, tGl2;
+    if (!make_map(&tGh2, gh, kp, n, kp, kTcBN / 2) || !make_map(&tGl2, gl, kp, n, kp, kTcBN / 2)) return -1;
+    static bool attr2 = false;
+    const size_t smem2 = sizeof(Tc2Smem) + 1024;
+    if (!attr2) {
+      cudaFuncSetAttribute(residual_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
+      attr2 = true;
+    }
+    const int64_t T2 = ceil_div(m_loc, 2 * kTcBM) * ceil_div(n, kTcBN);
+    const int64_t np = T2 < nsm / 2 ? T2 : nsm / 2;
+    const int ksteps2 = static_cast<int>(ceil_div(ncomp, 8));
+    note_launch();
+    residual_tc2_kernel<<<static_cast<unsigned>(2 * np), kTcThreads, smem2, st>>>(tA, tGh2, tGl2, fa, m_loc, n, ksteps2,
+                                                                                 tp, part);
+    launch_residual_final(part, static_cast<int>(2 * np), out, st);
+    return 0;
+  }
+  const int64_t T = ceil_div(m_loc, kTcBM) * ceil_div(n, kTcBN);
   int64_t g = T < nsm ? T : nsm;
   const int ksteps = static_cast<int>(ceil_div(ncomp, 8));
   note_launch();
