@@ -101,7 +101,8 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.rb = take(sizeof(float) * K * w.ldrb);
   w.wb = take(sizeof(float) * K * Kp);
   w.res_part = take(sizeof(double) * 2 * kResGrid);
-  w.res_split = take(sizeof(float) * 2 * (size_t)p.n * (Kp < 192 ? Kp : 192));  // G hi/lo, pitch round_up(ncomp, 32)
+  w.res_split = take(sizeof(float) * 2 * (size_t)p.n * (Kp < 192 ? Kp : 192) + 256);  // G hi/lo (TF32: pitch round_up(K, 32) <= 192;
+                                                                                   // FP16: round_up(K, 64) <= 384 halves) + max
   w.total = off;
   return w;
 }

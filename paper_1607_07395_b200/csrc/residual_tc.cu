@@ -23,6 +23,8 @@
 // Tile order is row-band major over a static contiguous tile range per CTA; fixed-order
 // block and grid reductions: bit-reproducible.  ncomp <= 192 (K padded to a multiple of 32;
 // G streamed in 32-wide K chunks through a 4-deep ring; TMEM plan in tmem_plan()).
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
@@ -38,7 +40,9 @@ constexpr int kTcThreads = 352;                     // 0 TMA (A), 1 MMA, 2-5 + 7
 constexpr int kEpiWarps = 8;
 constexpr int kAR = kAS / 2;                       // A ring slots per epilogue group (its own ring: a
                                                     // group never waits on a slot phase of the other)
-constexpr int kResKpMax = 192;                      // largest padded K (hi + lo F in TMEM + 1 acc stage)
+constexpr int kResKpMax = 192;                      // largest padded K, 3xTF32 (hi + lo F in TMEM + 1 acc stage)
+constexpr int kResKpMaxF16 = 128;                   // ... FP16 split (two K elements per TMEM column; the
+                                                    // one-F-buffer plan for K > 128 fails parity: not used)
 constexpr uint32_t kGAtomBytes = kTcBN * 128;      // 16 KB: 128 G rows x 32 floats (one K chunk)
 constexpr uint32_t kABoxBytes = kTcBM * 128;       // 16 KB: 128 rows x 32 floats = a quarter A tile
 constexpr uint32_t kTmemCols = 512;
@@ -52,7 +56,7 @@ struct TmemPlan {
 };
 inline TmemPlan tmem_plan(int kp) {
   TmemPlan t{kp, 2, 2};
-  if (kp > 64) t.nf = 1;
+  if (kp > 64 || getenv("CABS_RES_NF1")) t.nf = 1;  // (the variable forces the 1-buffer plan: tests)
   if (kp > 128) t.nacc = 1;
   return t;
 }
@@ -84,6 +88,17 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_f16_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// instruction descriptor, kind::f16 with FP16 A and B, FP32 accumulate, both K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
 // 32 lanes x 32 columns of 32-bit TMEM -> registers, WITHOUT the wait (the caller issues
@@ -138,6 +153,51 @@ struct FArgs {
   bool vec;        // f and ldf 16-byte aligned
 };
 
+// FP16 split: power-of-two scale of row r of F diag(s) (its largest |entry| maps below 2^14, far
+// inside the FP16 range); the epilogue divides the accumulator by it again (exact).
+__device__ __forceinline__ float f_row_scale(const FArgs& F, int64_t m, int64_t r) {
+  float mx = 0.f;
+  if (r < m) {
+    const float* src = F.f + r * F.ldf;
+    for (int c = 0; c < F.ncomp; ++c) mx = fmaxf(mx, fabsf(__ldg(src + c) * (F.s ? __ldg(F.s + c) : 1.f)));
+  }
+  return mx > 0.f ? exp2f(static_cast<float>(13 - ilogbf(mx))) : 1.f;
+}
+__device__ __forceinline__ uint32_t pack_h2(__half lo16, __half hi16) {
+  return static_cast<uint32_t>(__half_as_ushort(lo16)) | (static_cast<uint32_t>(__half_as_ushort(hi16)) << 16);
+}
+
+// FP16 split of row r of F diag(s) * rs into TMEM: chunk a = K elements [64 a, 64 a + 64) as 32
+// columns of packed pairs (hi at fcol + 32 a, lo at fcol + kp + 32 a).
+__device__ __forceinline__ void load_f_rows_h(const FArgs& F, int64_t m, int64_t r0, int q, int lane, uint32_t fcol,
+                                              int kp, float rs, uint64_t* ready) {
+  const int64_t r = r0 + q * 32 + lane;
+  const uint32_t tq = fcol + (static_cast<uint32_t>(q * 32) << 16);
+  const float* src = F.f + (r < m ? r : 0) * F.ldf;
+  for (int a = 0; a < kp / 32; ++a) {
+    float hi[32], lo[32];  // packed words (bit patterns)
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      float v2[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = 64 * a + 2 * c + e;
+        v2[e] = (r < m && col < F.ncomp) ? __ldg(src + col) * (F.s ? __ldg(F.s + col) : 1.f) * rs : 0.f;
+      }
+      const __half h0 = __float2half_rn(v2[0]), h1 = __float2half_rn(v2[1]);
+      const __half l0 = __float2half_rn(v2[0] - __half2float(h0)), l1 = __float2half_rn(v2[1] - __half2float(h1));
+      hi[c] = __uint_as_float(pack_h2(h0, h1));
+      lo[c] = __uint_as_float(pack_h2(l0, l1));
+    }
+    tmem_st32(tq + static_cast<uint32_t>(32 * a), hi);
+    tmem_st32(tq + static_cast<uint32_t>(kp + 32 * a), lo);
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  tc::fence_before_sync();
+  __syncwarp();
+  if (lane == 0) tc::mbar_arrive(ready);
+}
+
 template <bool PAIR = false>
 __device__ __forceinline__ void load_f_rows(const FArgs& F, int64_t m, int64_t r0, int q, int lane, uint32_t fcol,
                                             int kp, uint64_t* ready, uint32_t ready_cluster = 0) {
@@ -186,10 +246,15 @@ __device__ __forceinline__ void load_f_band(const FArgs& F, int64_t m, int64_t r
   load_f_rows<false>(F, m, rb * kTcBM, q, lane, fcol, kp, ready);
 }
 
+// H = false: 3xTF32 (kind::tf32, K = 8 per MMA); H = true: FP16 hi/lo split (kind::f16, K = 16 per
+// MMA, half the MMAs and half the G bytes): F rows scaled by a power of two each (f_row_scale), G
+// by one global power of two (gmax_bits), both undone exactly in the epilogue.  Either way a K
+// chunk is 128 bytes of a row (32 TF32 or 64 FP16 elements) = 32 TMEM columns of F.
+template <bool H>
 __global__ void __launch_bounds__(kTcThreads, 1)
 residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmGh,
                    const __grid_constant__ CUtensorMap tmGl, const FArgs fa, int64_t m, int64_t n, int ksteps,
-                   const TmemPlan tp, double* __restrict__ part, int dbg) {
+                   const TmemPlan tp, double* __restrict__ part, const unsigned* __restrict__ gmax_bits, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -258,8 +323,9 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             continue;
           }
           tc::mbar_expect_tx(&S.g_full[sg], 2 * kGAtomBytes);
-          tc::tma_load_2d_hint(S.gh[sg], &tmGh, c * 32, static_cast<int>(cb * kTcBN), &S.g_full[sg], pol);
-          tc::tma_load_2d_hint(S.gl[sg], &tmGl, c * 32, static_cast<int>(cb * kTcBN), &S.g_full[sg], pol);
+          const int x = c * (H ? 64 : 32);  // first K element of the chunk
+          tc::tma_load_2d_hint(S.gh[sg], &tmGh, x, static_cast<int>(cb * kTcBN), &S.g_full[sg], pol);
+          tc::tma_load_2d_hint(S.gl[sg], &tmGl, x, static_cast<int>(cb * kTcBN), &S.g_full[sg], pol);
         }
       }
     }
@@ -269,7 +335,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     // uniform datapath; one elected lane issues the MMAs and their commits (a lane-0-only loop
     // feeds the tensor pipe at ~1/2 rate: tools/ubench_issue2.cu).
     {
-      constexpr uint32_t idesc = tc::idesc_tf32(kTcBM, kTcBN);
+      constexpr uint32_t idesc = H ? idesc_f16(kTcBM, kTcBN) : tc::idesc_tf32(kTcBM, kTcBN);
       // slot descriptors by arithmetic (the start-address field is addr >> 4): a descriptor array
       // indexed by the runtime slot would live in local memory
       const uint64_t dgh0 = tc::desc_sw128(tc::smem_u32(S.gh[0])), dgl0 = tc::desc_sw128(tc::smem_u32(S.gl[0]));
@@ -302,10 +368,16 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             for (int q = 0; q < 4; ++q) {
               if (q < nk) {
                 const uint32_t fh = fh0 + static_cast<uint32_t>(8 * q);
-                mma_tf32_ts(d, fh, bh + 2 * q, idesc, (c | q) ? 1u : 0u);
-                if (!(dbg & 8)) {
-                  mma_tf32_ts(d, fh, bl + 2 * q, idesc, 1u);
-                  mma_tf32_ts(d, fh + static_cast<uint32_t>(kp), bh + 2 * q, idesc, 1u);
+                if (H) {
+                  mma_f16_ts(d, fh, bh + 2 * q, idesc, (c | q) ? 1u : 0u);
+                  mma_f16_ts(d, fh, bl + 2 * q, idesc, 1u);
+                  mma_f16_ts(d, fh + static_cast<uint32_t>(kp), bh + 2 * q, idesc, 1u);
+                } else {
+                  mma_tf32_ts(d, fh, bh + 2 * q, idesc, (c | q) ? 1u : 0u);
+                  if (!(dbg & 8)) {
+                    mma_tf32_ts(d, fh, bl + 2 * q, idesc, 1u);
+                    mma_tf32_ts(d, fh + static_cast<uint32_t>(kp), bh + 2 * q, idesc, 1u);
+                  }
                 }
               }
             }
@@ -326,10 +398,22 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const int row = q * 32 + lane;    // row within the 128-row tile
     // F of the first band(s) (group 0 only): nf = 2 stages band j + 1 while band j runs; nf = 1
     // loads band j + 1 once the MMA has released band j (at the band's last tile)
-    if (eg == 0) {
-      load_f_band(fa, m, rb0, q, lane, fcol0, kp, &S.f_ready[0]);
-      if (nf == 2 && nbands > 1) load_f_band(fa, m, rb0 + 1, q, lane, fcol0 + 2 * kp, kp, &S.f_ready[1]);
+    // H: the accumulator of row r is (F diag(s))_r G^T * rs_r * gs; gs from the split kernel's max
+    float gs = 1.f;
+    if (H) {
+      const float gmx = __uint_as_float(__ldg(gmax_bits));
+      gs = gmx > 0.f ? exp2f(static_cast<float>(13 - ilogbf(gmx))) : 1.f;
     }
+    auto load_band = [&](int64_t rb, uint32_t fc, uint64_t* ready) {
+      if (H) load_f_rows_h(fa, m, rb * kTcBM, q, lane, fc, kp, f_row_scale(fa, m, rb * kTcBM + row), ready);
+      else load_f_band(fa, m, rb, q, lane, fc, kp, ready);
+    };
+    if (eg == 0) {
+      load_band(rb0, fcol0, &S.f_ready[0]);
+      if (nf == 2 && nbands > 1) load_band(rb0 + 1, fcol0 + 2 * kp, &S.f_ready[1]);
+    }
+    int64_t inv_rb = -1;
+    float inv = 1.f;
     double r2 = 0.0, a2 = 0.0;
     int64_t prev_rb = rb0;
     for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
@@ -341,8 +425,12 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           const int fb = static_cast<int>((jb + 1) & 1);
           tc::mbar_wait(&S.f_free[fb], static_cast<uint32_t>(((jb - 1) >> 1) & 1));
           tc::fence_after_sync();
-          load_f_band(fa, m, rb + 1, q, lane, fcol0 + static_cast<uint32_t>(fb * 2 * kp), kp, &S.f_ready[fb]);
+          load_band(rb + 1, fcol0 + static_cast<uint32_t>(fb * 2 * kp), &S.f_ready[fb]);
         }
+      }
+      if (H && rb != inv_rb) {
+        inv_rb = rb;
+        inv = 1.f / (f_row_scale(fa, m, rb * kTcBM + row) * gs);  // a power of two: exact
       }
       const int sc = static_cast<int>(i % nacc);
       RES_WAIT(11, tc::mbar_wait(&S.acc_full[sc], ring_parity(i, nacc)));
@@ -357,7 +445,6 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         const int64_t li = kHalfAQ * i + hh;
         const int sa = eg * kAR + static_cast<int>(li % kAR);
         float av[32], v[32];
-        tmem_ld32_nowait(tbase + 32 * (kHalf * eg + hh), v);
         RES_WAIT(10, tc::mbar_wait(&S.a_full[sa], ring_parity(li, kAR)));
         const uint8_t* arow = S.a[sa] + row * 128;
 #pragma unroll
@@ -367,11 +454,16 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&S.a_empty[sa]);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        tmem_regs_fence(v);
+        // load + wait back to back: between a no-wait tcgen05.ld and its wait the compiler may
+        // move or reuse the destination registers, which the load then overwrites asynchronously
+        tc::tmem_ld32(tbase + 32 * (kHalf * eg + hh), v);
         if (dbg & 1) {
 #pragma unroll
           for (int x = 0; x < 32; ++x) v[x] = 0.f;
+        }
+        if (H) {
+#pragma unroll
+          for (int x = 0; x < 32; ++x) v[x] *= inv;
         }
         if (hh == kHalf - 1) {  // the accumulator stage is in registers: release it
           tc::fence_before_sync();
@@ -393,7 +485,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         const int64_t jb = rb - rb0;
         tc::mbar_wait(&S.f_free[0], static_cast<uint32_t>(jb & 1));
         tc::fence_after_sync();
-        load_f_band(fa, m, rb + 1, q, lane, fcol0, kp, &S.f_ready[0]);
+        load_band(rb + 1, fcol0, &S.f_ready[0]);
       }
       r2 += static_cast<double>(tr0 + tr1);
       a2 += static_cast<double>(ta0 + ta1);
@@ -609,7 +701,6 @@ residual_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         const int64_t li = kHalfAQ * i + hh;
         const int sa = eg * kAR + static_cast<int>(li % kAR);
         float av[32], v[32];
-        tmem_ld32_nowait(tbase + 32 * (kHalf * eg + hh), v);
         tc::mbar_wait(&S.a_full[sa], ring_parity(li, kAR));
         const uint8_t* arow = S.a[sa] + row * 128;
 #pragma unroll
@@ -619,8 +710,7 @@ residual_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&S.a_empty[sa]);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        tmem_regs_fence(v);
+        tc::tmem_ld32(tbase + 32 * (kHalf * eg + hh), v);
         if (hh == kHalf - 1) {
           tc::fence_before_sync();
           __syncwarp();
@@ -685,6 +775,34 @@ __global__ void __launch_bounds__(256) split_g_kernel(const float* __restrict__ 
   }
 }
 
+// FP16 split of G: the largest |G| (as float bits; non-negative floats order as unsigned), then
+// hi = fp16(G gs), lo = fp16(G gs - hi) with gs = 2^(13 - ilogb(max)), pitch kp16 (zero padded).
+__global__ void __launch_bounds__(256) gmax_kernel(const float* __restrict__ G, int64_t ldg, int64_t rows, int ncomp,
+                                                   unsigned* __restrict__ gmax) {
+  float mx = 0.f;
+  const int l = threadIdx.x & 31;
+  for (int64_t r = blockIdx.x * 8LL + (threadIdx.x >> 5); r < rows; r += gridDim.x * 8LL)
+    for (int c = l; c < ncomp; c += 32) mx = fmaxf(mx, fabsf(__ldg(G + r * ldg + c)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (l == 0) atomicMax(gmax, __float_as_uint(mx));
+}
+__global__ void __launch_bounds__(256) split_g16_kernel(const float* __restrict__ G, int64_t ldg, int64_t rows, int ncomp,
+                                                        int kp16, const unsigned* __restrict__ gmax,
+                                                        __half* __restrict__ hi, __half* __restrict__ lo) {
+  const float gmx = __uint_as_float(*gmax);
+  const float gs = gmx > 0.f ? exp2f(static_cast<float>(13 - ilogbf(gmx))) : 1.f;
+  const int l = threadIdx.x & 31;
+  for (int64_t r = blockIdx.x * 8LL + (threadIdx.x >> 5); r < rows; r += gridDim.x * 8LL) {
+    for (int c = l; c < kp16; c += 32) {
+      const float x = c < ncomp ? __ldg(G + r * ldg + c) * gs : 0.f;
+      const __half h = __float2half_rn(x);
+      hi[r * kp16 + c] = h;
+      lo[r * kp16 + c] = __float2half_rn(x - __half2float(h));
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -703,16 +821,18 @@ static EncodeTiledFn encoder() {
 }
 
 // 2D fp32 tensor map: `cols` x `rows`, row pitch `ld` floats, box 32 x box_rows, 128B swizzle.
-static bool make_map(CUtensorMap* tm, const float* base, int64_t cols, int64_t rows, int64_t ld, uint32_t box_rows) {
+static bool make_map(CUtensorMap* tm, const void* base, int64_t cols, int64_t rows, int64_t ld, uint32_t box_rows,
+                     bool f16 = false) {
   EncodeTiledFn enc = encoder();
   if (!enc) return false;
+  const size_t es = f16 ? 2 : 4;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
-  cuuint32_t box[2] = {32, box_rows};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * es};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), box_rows};  // one 128-byte swizzle row
   cuuint32_t estr[2] = {1, 1};
-  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return enc(tm, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
+             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 void residual_debug_counters(long long* out, int n) {
@@ -726,7 +846,7 @@ void residual_debug_counters(long long* out, int n) {
 int residual_tc_kmax() { return kResKpMax; }
 
 bool residual_tc_supported(const float* A, int64_t lda, int64_t m_loc, int64_t n, int ncomp) {
-  if (ncomp < 1 || ncomp > kResKpMax || m_loc < 1 || n < 1) return false;
+  if (ncomp < 1 || ncomp > residual_tc_kmax() || m_loc < 1 || n < 1) return false;
   if ((lda % 4) != 0 || (reinterpret_cast<uintptr_t>(A) & 15) != 0) return false;
   if (m_loc > 0x7fffffff || n > 0x7fffffff) return false;
   if (getenv("CABS_RESIDUAL_FFMA")) return false;
@@ -736,13 +856,47 @@ bool residual_tc_supported(const float* A, int64_t lda, int64_t m_loc, int64_t n
 int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, const float* F, int64_t ldf,
                        const float* s, const float* G, int64_t ldg, int ncomp, float* split, double* part, double* out,
                        cudaStream_t st) {
+  int dev = 0, nsm = kNumSM;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  FArgs fa{F, ldf, s, ncomp, (reinterpret_cast<uintptr_t>(F) & 15) == 0 && (ldf % 4) == 0};
+  if (!getenv("CABS_RESIDUAL_TF32") && ncomp <= kResKpMaxF16) {
+    // FP16 hi/lo split (default): K in chunks of 64, 16 per MMA
+    const int kp16 = static_cast<int>(round_up(ncomp, 64));
+    const TmemPlan tp = tmem_plan(kp16 / 2);
+    __half* gh = reinterpret_cast<__half*>(split);
+    __half* gl = gh + n * kp16;
+    unsigned* gmax = reinterpret_cast<unsigned*>(gl + n * kp16);
+    cudaMemsetAsync(gmax, 0, sizeof(unsigned), st);
+    note_launch();
+    gmax_kernel<<<4 * kNumSM, 256, 0, st>>>(G, ldg, n, ncomp, gmax);
+    note_launch();
+    split_g16_kernel<<<4 * kNumSM, 256, 0, st>>>(G, ldg, n, ncomp, kp16, gmax, gh, gl);
+    CUtensorMap tA, tGh, tGl;
+    if (!make_map(&tA, A, n, m_loc, lda, kTcBM) || !make_map(&tGh, gh, kp16, n, kp16, kTcBN, true) ||
+        !make_map(&tGl, gl, kp16, n, kp16, kTcBN, true))
+      return -1;
+    static bool attr16 = false;
+    const size_t smem = sizeof(TcSmem) + 1024;
+    if (!attr16) {
+      cudaFuncSetAttribute(residual_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      attr16 = true;
+    }
+    const int64_t T = ceil_div(m_loc, kTcBM) * ceil_div(n, kTcBN);
+    const int64_t g = T < nsm ? T : nsm;
+    const int ksteps = static_cast<int>(ceil_div(ncomp, 16));
+    note_launch();
+    residual_tc_kernel<true><<<static_cast<unsigned>(g), kTcThreads, smem, st>>>(tA, tGh, tGl, fa, m_loc, n, ksteps, tp,
+                                                                                part, gmax, 0);
+    launch_residual_final(part, static_cast<int>(g), out, st);
+    return 0;
+  }
   const int kp = static_cast<int>(round_up(ncomp, 32));
   const TmemPlan tp = tmem_plan(kp);
   float* gh = split;
   float* gl = gh + n * kp;
   note_launch();
   split_g_kernel<<<4 * kNumSM, 256, 0, st>>>(G, ldg, n, ncomp, kp, gh, gl);
-  FArgs fa{F, ldf, s, ncomp, (reinterpret_cast<uintptr_t>(F) & 15) == 0 && (ldf % 4) == 0};
   CUtensorMap tA, tGh, tGl;
   if (!make_map(&tA, A, n, m_loc, lda, kTcBM) || !make_map(&tGh, gh, kp, n, kp, kTcBN) ||
       !make_map(&tGl, gl, kp, n, kp, kTcBN))
@@ -750,13 +904,10 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
   static bool attr = false;
   const size_t smem = sizeof(TcSmem) + 1024;
   if (!attr) {
-    cudaFuncSetAttribute(residual_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(residual_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  int dev = 0, nsm = kNumSM;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (!getenv("CABS_RESIDUAL_1SM")) {  // CTA-pair kernel (default)
+  if (getenv("CABS_RESIDUAL_PAIR")) {  // 3xTF32 CTA-pair kernel
     CUtensorMap tGh2, tGl2;
     if (!make_map(&tGh2, gh, kp, n, kp, kTcBN / 2) || !make_map(&tGl2, gl, kp, n, kp, kTcBN / 2)) return -1;
     static bool attr2 = false;
@@ -782,8 +933,8 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
 #ifdef CABS_PROFILE_RES
   if (const char* e = getenv("CABS_RES_DBG")) dbg = atoi(e);
 #endif
-  residual_tc_kernel<<<static_cast<unsigned>(g), kTcThreads, smem, st>>>(tA, tGh, tGl, fa, m_loc, n, ksteps, tp, part,
-                                                                          dbg);
+  residual_tc_kernel<false><<<static_cast<unsigned>(g), kTcThreads, smem, st>>>(tA, tGh, tGl, fa, m_loc, n, ksteps, tp,
+                                                                                 part, nullptr, dbg);
   launch_residual_final(part, static_cast<int>(g), out, st);
   return 0;
 }
