@@ -94,7 +94,11 @@ int32_t cabs_debug_counters(int64_t* out, int32_t n) {
 #ifdef CABS_PROFILE_SNAP
   if (n >= 4) snap_debug_counters(reinterpret_cast<long long*>(out));
 #endif
+#ifdef CABS_PROFILE_KTC
+  if (n > 16) ktc_debug_timeline(reinterpret_cast<long long*>(out) + 16, n - 16);
+#else
   if (n > 16) lloyd_debug_timeline(reinterpret_cast<long long*>(out) + 16, n - 16);
+#endif
   return CABS_OK;
 }
 
@@ -457,6 +461,14 @@ int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   CABS_TRY(km_prepare(p, weight_kind, weight_p, seed, k, comm, stream));
   if (km_persistent_allowed(comm) && n_loc > 0) {
     const LloydJob j = km_job(p, k);
+    if (kmeans_tc_selected(k2, d)) {
+      if (launch_lloyd_tc(&j, 1, iters, nullptr, nullptr, S(stream))) {
+        CABS_LAUNCH_CHECK("lloyd_tc");
+        return CABS_OK;
+      }
+      if (getenv("CABS_KMEANS_REQUIRE_TC")) return arg_error("kmeans: tensor-core kernel not launched");
+    }
+    cudaGetLastError();
     if (launch_lloyd_persistent(&j, 1, iters, reinterpret_cast<long long*>(ws) + 8, S(stream))) {
       CABS_LAUNCH_CHECK("lloyd_persistent");
       return CABS_OK;
@@ -509,6 +521,14 @@ int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const 
   }
   if (km_persistent_allowed(comm) && a->n_loc > 0 && b->n_loc > 0) {
     const LloydJob j[2] = {km_job(*a, ka), km_job(*b, kb)};
+    if (kmeans_tc_selected(a->k2, a->d) && kmeans_tc_selected(b->k2, b->d)) {
+      if (launch_lloyd_tc(j, 2, iters, nullptr, nullptr, S(stream))) {
+        CABS_LAUNCH_CHECK("lloyd_tc");
+        return CABS_OK;
+      }
+      if (getenv("CABS_KMEANS_REQUIRE_TC")) return arg_error("kmeans_pair: tensor-core kernel not launched");
+    }
+    cudaGetLastError();
     if (launch_lloyd_persistent(j, 2, iters, reinterpret_cast<long long*>(ws) + 8, S(stream))) {
       CABS_LAUNCH_CHECK("lloyd_persistent");
       return CABS_OK;

@@ -91,6 +91,12 @@ struct LloydJob {
   size_t scratch_bytes;
 };
 bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long long* prof, cudaStream_t st);
+// lloyd_tc.cu: the same loop with the distance cross-term on the tensor cores (d, k2 <= 128);
+// tie_logs[q] (or NULL): near-tie log of problem q, [0] = count, then (iteration, point, j1, j2,
+// gap bits) per entry, up to tie_caps[q] entries.  False -> not applicable.
+void ktc_debug_timeline(long long* out, int n);
+bool launch_lloyd_tc(const LloydJob* jobs, int njobs, int iters, int* const* tie_logs, const int* tie_caps,
+                     cudaStream_t st);
 void lloyd_debug_timeline(long long* out, int n);
 void embed_debug_timeline(long long* out);
 void snap_debug_counters(long long* out);

@@ -721,6 +721,4 @@ bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long lo
   return cudaLaunchKernelEx(&cfg, lloyd_persistent_kernel, a) == cudaSuccess;
 }
 
-bool kmeans_tc_selected(int, int) { return false; }
-
 }  // namespace cabsk

@@ -567,3 +567,38 @@ def test_embed_drops_zero_norm_component_with_compaction(dev):
     assert rel_fro(align_signs(Q.cpu().numpy()[:, :1], Qr), Qr) < 1e-6
     assert np.all(P.cpu().numpy()[:, 1:] == 0) and np.all(Q.cpu().numpy()[:, 1:] == 0)
     assert abs(s[0].item() - sk.s[0]) < 1e-6 * sk.s[0] and s[1].item() == 0.0
+
+
+@pytest.mark.parametrize("N,d,k2,ncl,iters", [(50000, 100, 100, 64, 6), (30000, 50, 50, 30, 8), (7001, 33, 19, 30, 5),
+                                              (12000, 96, 112, 90, 4), (3000, 20, 20, 10, 10), (5000, 7, 5, 4, 6)])
+def test_kmeans_tensor_core_and_ffma_paths_agree(dev, monkeypatch, N, d, k2, ncl, iters):
+    """The tensor-core Lloyd kernel (FP16-split cross-term prunes the centres, then the
+    candidates' FP32 direct-difference distances decide) and the FFMA kernel (direct
+    differences against every centre) take the same decisions: labels, exact-integer centres,
+    cluster weights and near-tie counts bit for bit; the objective is the same FP64 sum of
+    the same FP32 terms over another CTA partition.  Cases: the c3 shape (tight clusters, more
+    centres than clusters -> near-equal candidates), c2, odd d, a near-limit shape, c1, tiny."""
+    X = _clustered(N, d, ncl, N + d, spread=0.02)
+    ld = C.cabs_padded_ld(d)
+    Xt = torch.zeros((N, ld), device=dev); Xt[:, :d] = torch.from_numpy(X).to(dev)
+    plan = _plan(N, N, max(d, k2))
+    ws = _ws(plan, dev)
+    monkeypatch.setenv("CABS_KMEANS_TC", "1")  # wherever the tensor-core kernel applies
+    assert C.cabs_kmeans_path(k2, d) == "tc"
+    outs = []
+    monkeypatch.setenv("CABS_KMEANS_REQUIRE_TC", "1")  # the library errors if the TC kernel is not launched
+    for ffma in ("", "1"):
+        if ffma:
+            monkeypatch.setenv("CABS_KMEANS_FFMA", "1")
+        cen = torch.zeros((k2, ld), device=dev)
+        lab = torch.zeros(N, dtype=torch.int32, device=dev)
+        cw = torch.zeros(k2, dtype=torch.float64, device=dev)
+        obj = torch.zeros(iters, dtype=torch.float64, device=dev)
+        ties = torch.zeros(iters, dtype=torch.int32, device=dev)
+        C.cabs_kmeans(plan, Xt, N, N, 0, d, k2, iters, C.WEIGHT_CONST, 2.0, 3, C.TAG_INIT_ROWS, cen, lab, cw, obj, ws,
+                      near_ties=ties)
+        outs.append([t.cpu().numpy() for t in (cen, lab, cw, obj, ties)])
+    (c1, l1, w1, o1, t1), (c2, l2, w2, o2, t2) = outs
+    assert np.array_equal(l1, l2), f"{np.count_nonzero(l1 != l2)} labels differ"
+    assert np.array_equal(c1, c2) and np.array_equal(w1, w2) and np.array_equal(t1, t2)
+    assert np.allclose(o1, o2, rtol=1e-12)
