@@ -26,6 +26,10 @@ void launch_gather_w_direct(const float* A, int64_t lda, int64_t row_begin, int6
 int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const Ws& L, double* sigma_user, double* Uw64,
                double* Vw64, int* r_user, cudaStream_t st);
 
+// svd_cluster.cu: k in (1, 320] on a cluster of ceil(k / 32) CTAs (false: not launched)
+bool launch_svd_cluster(int k, const float* W, int64_t ldw, double tol, double* sig, double* Uw64, double* Vw64,
+                        float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st);
+
 // embed.cu
 int launch_embed_products(int64_t m_loc, int64_t n_sl, int k, const float* C, int64_t ldc, const float* R_slice,
                           int64_t ldr, float* Yc, int64_t ldyc, float* Yr, int64_t ldyr, void* ws, const Ws& L,

@@ -1436,6 +1436,9 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
     else if (k <= 32) launch_systolic<4, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
     else if (k <= 52) launch_systolic<4, 13>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
     else launch_systolic<4, 16>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+  } else if (k <= 320 && !getenv("CABS_SVD_ONE_CTA") &&
+             launch_svd_cluster(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st)) {
+    // k > 64: block Jacobi over a thread-block cluster (svd_cluster.cu)
   } else {
     static bool attr_set = false;
     if (!attr_set) {
