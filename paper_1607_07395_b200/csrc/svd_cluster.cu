@@ -79,36 +79,39 @@ __device__ __forceinline__ void sc_cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-// One warp rotates the column pair (p, q) of the CTA's 2w local columns, A and V: lanes hold
-// rows lane + 32 e.  Column j of the CTA lives at col(j) (A) and col(j) + kp (V).
+// Squared norm of a column (warp, fixed-order tree)
 template <int EPL>
-__device__ __forceinline__ void sc_rotate(double* cp, double* cq, int kp, double tol2, int lane, bool& rotated,
-                                          double& tmax) {
+__device__ __forceinline__ double sc_norm2(const double* cp, int lane) {
+  double a0 = 0, a1 = 0;
+#pragma unroll
+  for (int e = 0; e < EPL; e += 2) {
+    a0 = fma(cp[lane + 32 * e], cp[lane + 32 * e], a0);
+    if (e + 1 < EPL) a1 = fma(cp[lane + 32 * (e + 1)], cp[lane + 32 * (e + 1)], a1);
+  }
+  return warp_sum_d(a0 + a1);
+}
+
+// One warp rotates the column pair (p, q) of the CTA's 2w local columns, A and V: lanes hold
+// rows lane + 32 e.  Column j lives at col(j) (A) and col(j) + kp (V); its squared norm is
+// cached in *np / *nq (exact at every block round start, then updated by the rotation's exact
+// 2 x 2 formula: x.x -= t g, y.y += t g), so only x.y is reduced across the warp.
+template <int EPL>
+__device__ __forceinline__ void sc_rotate(double* cp, double* cq, double* np, double* nq, int kp, double tol2,
+                                          int lane, bool& rotated, double& tmax) {
   double x[EPL], y[EPL];
 #pragma unroll
   for (int e = 0; e < EPL; ++e) {
     x[e] = cp[lane + 32 * e];
     y[e] = cq[lane + 32 * e];
   }
-  double al0 = 0, be0 = 0, ga0 = 0, al1 = 0, be1 = 0, ga1 = 0;
+  double ga0 = 0, ga1 = 0;
 #pragma unroll
   for (int e = 0; e < EPL; e += 2) {
-    al0 = fma(x[e], x[e], al0);
-    be0 = fma(y[e], y[e], be0);
     ga0 = fma(x[e], y[e], ga0);
-    if (e + 1 < EPL) {
-      al1 = fma(x[e + 1], x[e + 1], al1);
-      be1 = fma(y[e + 1], y[e + 1], be1);
-      ga1 = fma(x[e + 1], y[e + 1], ga1);
-    }
+    if (e + 1 < EPL) ga1 = fma(x[e + 1], y[e + 1], ga1);
   }
-  double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    al += __shfl_xor_sync(0xffffffffu, al, o);
-    be += __shfl_xor_sync(0xffffffffu, be, o);
-    ga += __shfl_xor_sync(0xffffffffu, ga, o);
-  }
+  const double ga = warp_sum_d(ga0 + ga1);
+  const double al = *np, be = *nq;
   double c, s;
   const double t = sc_angle(al, be, ga, tol2, c, s);
   if (t != 0.0) {
@@ -126,6 +129,11 @@ __device__ __forceinline__ void sc_rotate(double* cp, double* cq, int kp, double
       const double a = vp[lane + 32 * e], b = vq[lane + 32 * e];
       vp[lane + 32 * e] = c * a - s * b;
       vq[lane + 32 * e] = s * a + c * b;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      *np = fma(-t, ga, al);
+      *nq = fma(t, ga, be);
     }
   }
 }
@@ -148,14 +156,25 @@ svd_cluster_kernel(int k, int w, const float* __restrict__ W, int64_t ldw, doubl
   __shared__ int s_perm[kScKmax];
   __shared__ int s_flag[2];          // CTA 0: [rotated any, all |t| small] of the sweep
   __shared__ int s_r, s_last;
+  __shared__ double s_nrm[32];       // cached squared norms of the 2w local columns
   constexpr int kp = 32 * EPL;       // padded column length
+  constexpr bool DB = EPL <= 5;      // double-buffered block storage (seat changes without staging)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t cr, P;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(P));
   const int nb = 2 * static_cast<int>(P);
   // local column j (0 <= j < 2w): slot j / w, column j % w; storage [j][A kp | V kp]
-  auto col = [&](int j) { return sm + (size_t)j * 2 * kp; };
+  int buf = 0;
+  const size_t bufsz = (size_t)2 * w * 2 * kp;
+  auto col = [&](int j) { return sm + buf * bufsz + (size_t)j * 2 * kp; };
+  auto refresh_norms = [&]() {  // exact squared norms of the local columns
+    for (int j = warp; j < 2 * w; j += kScThreads / 32) {
+      const double n2 = sc_norm2<EPL>(col(j), lane);
+      if (lane == 0) s_nrm[j] = n2;
+    }
+    __syncthreads();
+  };
   // block ids of the two slots (the tournament moves them); global column = blk * w + local
   int blk[2] = {static_cast<int>(cr), nb - 1 - static_cast<int>(cr)};
 
@@ -191,13 +210,16 @@ svd_cluster_kernel(int k, int w, const float* __restrict__ W, int64_t ldw, doubl
     bool rotated = false;
     double tmax = 0.0;
     // (1) pairs inside each block: round-robin on w (padded to even) players, both slots at once
+    refresh_norms();
     {
       const int wp = (w + 1) & ~1;
       for (int r = 0; r < wp - 1; ++r) {
         if (warp < wp) {  // warps [0, wp/2): slot 0, [wp/2, wp): slot 1
           const int half = wp / 2, sl = warp / half, pi = warp % half;
           int p = sc_rr(pi, r, wp), q = sc_rr(wp - 1 - pi, r, wp);
-          if (p < w && q < w) sc_rotate<EPL>(col(sl * w + p), col(sl * w + q), kp, tol2, lane, rotated, tmax);
+          if (p < w && q < w)
+            sc_rotate<EPL>(col(sl * w + p), col(sl * w + q), &s_nrm[sl * w + p], &s_nrm[sl * w + q], kp, tol2, lane,
+                           rotated, tmax);
         }
         __syncthreads();
       }
@@ -205,10 +227,11 @@ svd_cluster_kernel(int k, int w, const float* __restrict__ W, int64_t ldw, doubl
     SC_PROF(0);
     // (2) block rounds: cross pairs, then a seat change
     for (int br = 0; br < nb - 1; ++br) {
+      if (br > 0) refresh_norms();  // the blocks moved
       for (int s = 0; s < w; ++s) {
         if (warp < w) {
           const int i = warp, jq = (warp + s) % w;
-          sc_rotate<EPL>(col(i), col(w + jq), kp, tol2, lane, rotated, tmax);
+          sc_rotate<EPL>(col(i), col(w + jq), &s_nrm[i], &s_nrm[w + jq], kp, tol2, lane, rotated, tmax);
         }
         __syncthreads();
       }
@@ -224,30 +247,46 @@ svd_cluster_kernel(int k, int w, const float* __restrict__ W, int64_t ldw, doubl
         dst[1] = c == 0 ? 1 : c - 1;
         dsl[1] = c == 0 ? 0 : 1;
         sc_cluster_sync();  // every CTA is done with its blocks
-        // stage both slots through registers in two halves (A, then V), write them to the seats
-        constexpr int kPer = (16 * kScKmax + kScThreads - 1) / kScThreads;  // w * kp / threads, <= 10
-        for (int part = 0; part < 2; ++part) {
-          double v[2][kPer];
-#pragma unroll
-          for (int sl = 0; sl < 2; ++sl)
-#pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-              const int e = tid + u * kScThreads;
-              const int j = e / kp, i = e - j * kp;
-              v[sl][u] = (j < w) ? col(sl * w + j)[part * kp + i] : 0.0;
-            }
-          sc_cluster_sync();  // reads done before anyone overwrites
-#pragma unroll
+        if (DB) {
+          // straight into the destination's other buffer, 16 bytes per store
           for (int sl = 0; sl < 2; ++sl) {
-            const uint32_t base = sc_map(col(dsl[sl] * w), static_cast<uint32_t>(dst[sl]));
-#pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-              const int e = tid + u * kScThreads;
-              const int j = e / kp, i = e - j * kp;
-              if (j < w) sc_st_f64(base + static_cast<uint32_t>(((size_t)j * 2 * kp + part * kp + i) * 8), v[sl][u]);
+            const uint32_t base = sc_map(sm + (buf ^ 1) * bufsz + (size_t)dsl[sl] * w * 2 * kp,
+                                         static_cast<uint32_t>(dst[sl]));
+            const double2* src = reinterpret_cast<const double2*>(col(sl * w));
+            for (int e = tid; e < w * kp; e += kScThreads) {  // w columns x (A | V) = w * 2 kp doubles
+              const double2 v2 = src[e];
+              asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(base + 16u * e), "d"(v2.x), "d"(v2.y)
+                           : "memory");
             }
           }
           sc_cluster_sync();
+          buf ^= 1;
+        } else {
+          // stage both slots through registers in two halves (A, then V), write them to the seats
+          constexpr int kPer = (16 * kScKmax + kScThreads - 1) / kScThreads;  // w * kp / threads, <= 10
+          for (int part = 0; part < 2; ++part) {
+            double v[2][kPer];
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+              for (int u = 0; u < kPer; ++u) {
+                const int e = tid + u * kScThreads;
+                const int j = e / kp, i = e - j * kp;
+                v[sl][u] = (j < w) ? col(sl * w + j)[part * kp + i] : 0.0;
+              }
+            sc_cluster_sync();  // reads done before anyone overwrites
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+              const uint32_t base = sc_map(col(dsl[sl] * w), static_cast<uint32_t>(dst[sl]));
+#pragma unroll
+              for (int u = 0; u < kPer; ++u) {
+                const int e = tid + u * kScThreads;
+                const int j = e / kp, i = e - j * kp;
+                if (j < w) sc_st_f64(base + static_cast<uint32_t>(((size_t)j * 2 * kp + part * kp + i) * 8), v[sl][u]);
+              }
+            }
+            sc_cluster_sync();
+          }
         }
         // the tournament is deterministic: the seats' blocks from the number of seat changes
         const int rd = sweep * (nb - 1) + br + 1;  // seat changes so far
@@ -378,7 +417,7 @@ template <int EPL>
 static bool launch_sc(int k, int w, int P, const float* W, int64_t ldw, double tol, double* sig, double* Uw64,
                       double* Vw64, float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws,
                       cudaStream_t st) {
-  const size_t smem = sizeof(double) * 2 * (size_t)w * 2 * 32 * EPL;
+  const size_t smem = sizeof(double) * 2 * (size_t)w * 2 * 32 * EPL * (EPL <= 5 ? 2 : 1);
   auto kern = svd_cluster_kernel<EPL>;
   static bool attr = false;
   if (!attr) {
@@ -413,6 +452,7 @@ bool launch_svd_cluster(int k, const float* W, int64_t ldw, double tol, double* 
   const int epl = static_cast<int>(ceil_div(k, 32));
   bool ok;
   if (epl <= 4) ok = launch_sc<4>(k, w, P, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
+  else if (epl <= 5) ok = launch_sc<5>(k, w, P, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
   else if (epl <= 7) ok = launch_sc<7>(k, w, P, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
   else ok = launch_sc<10>(k, w, P, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
   if (!ok) cudaGetLastError();

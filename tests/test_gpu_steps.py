@@ -125,17 +125,21 @@ def test_pilot_invalid_k(dev):
 
 
 # ------------------------------------------------------------------ S4 SVD
-_SVD_KERNELS = {"quad": None, "split": "CABS_SVD_SPLIT", "one_sm": "CABS_SVD_ONE_SM", "smem": "CABS_SVD_SMEM"}
+_SVD_KERNELS = {"default": None, "split": "CABS_SVD_SPLIT", "one_sm": "CABS_SVD_ONE_SM", "smem": "CABS_SVD_SMEM",
+                "one_cta": "CABS_SVD_ONE_CTA"}
 
 
-@pytest.mark.parametrize("kernel", ["quad", "split", "one_sm", "smem"])
-@pytest.mark.parametrize("k,rank", [(20, 20), (50, 50), (64, 40), (100, 100), (112, 60), (150, 150), (7, 3),
-                                    (1, 1)])
+@pytest.mark.parametrize("kernel", ["default", "split", "one_sm", "smem", "one_cta"])
+@pytest.mark.parametrize("k,rank", [(20, 20), (50, 50), (64, 40), (65, 65), (100, 100), (112, 60), (150, 150),
+                                    (200, 200), (256, 130), (300, 300), (7, 3), (1, 1)])
 def test_svd_matches_lapack(dev, k, rank, kernel, monkeypatch):
-    """Every SVD kernel variant (k <= 64: the default 4-columns-per-slot cluster pair, the
-    2-column pair, the one-SM systolic and the shared-memory kernels; selected per call)."""
-    if kernel != "quad" and k > 64:
-        pytest.skip("one kernel beyond k = 64")
+    """Every SVD kernel variant: k <= 64 the default 4-columns-per-slot cluster pair, the
+    2-column pair, the one-SM systolic and the shared-memory kernels; k > 64 the default
+    block Jacobi over a thread-block cluster (svd_cluster.cu) and the single-CTA kernel."""
+    if kernel in ("split", "one_sm") and k > 64:
+        pytest.skip("k <= 64 variant")
+    if kernel == "one_cta" and not (64 < k <= 150):
+        pytest.skip("k > 64 variant (slow beyond 150)")
     if _SVD_KERNELS[kernel]:
         monkeypatch.setenv(_SVD_KERNELS[kernel], "1")
     g = np.random.default_rng(k * 7 + rank)
