@@ -185,14 +185,18 @@ int32_t cabs_pilot_embed(const cabs_plan* plan, const cabs_source* src, int32_t 
  * Outputs: centres (k2 x ldc, after the last update), labels (int32[n_loc], last
  * assignment), cluster_w (double[k2], weights of the last assignment),
  * objective (double[iters]), near_ties (int32[iters] or NULL: points whose
- * FP32 relative gap (d2-d1)/d2 < 1e-5, north_star near-tie rule). */
+ * FP32 relative gap (d2-d1)/d2 < 1e-5, north_star near-tie rule), tie_log (int32[1 + 5
+ * tie_log_cap] or NULL: the near-tie log the north_star asks for -- tie_log[0] = number of
+ * near ties seen (all iterations, this rank's points), then per entry (iteration, global point
+ * index, nearest centre, runner-up centre, relative gap as FP32 bits); entries beyond
+ * tie_log_cap are counted but not stored; order of entries unspecified). */
 int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t n_loc,
                     int64_t n_glob, int64_t row_off, int32_t d, int32_t k2, int32_t iters,
                     int32_t weight_kind, float weight_p, uint64_t seed, int32_t tag,
                     const int64_t* init_idx, const float* init_centres, float* centres,
                     int64_t ldc, int32_t* labels, double* cluster_w, double* objective,
-                    int32_t* near_ties, void* ws, size_t ws_bytes, const cabs_comm* comm,
-                    void* stream);
+                    int32_t* near_ties, int32_t* tie_log, int32_t tie_log_cap, void* ws,
+                    size_t ws_bytes, const cabs_comm* comm, void* stream);
 
 /* One k-means problem of cabs_kmeans_pair: the arguments of cabs_kmeans that differ
  * between the row side (X = P, rows of A) and the column side (X = Q, columns of A). */
@@ -208,6 +212,8 @@ typedef struct cabs_km_problem {
   double* cluster_w;            /* device double[k2] (out) */
   double* objective;            /* device double[iters] (out) */
   int32_t* near_ties;           /* device int32[iters] (out) or NULL */
+  int32_t* tie_log;             /* device int32[1 + 5 tie_log_cap] (out) or NULL: see cabs_kmeans */
+  int32_t tie_log_cap;
 } cabs_km_problem;
 
 /* Alg. 2 steps 6-7 for BOTH sides at once: exactly cabs_kmeans(a) and cabs_kmeans(b) with

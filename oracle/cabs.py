@@ -11,11 +11,9 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
 reference leg may import this module.  It shares no code with the CUDA path.
 
 Parity status per function:
-  gather, svd_w, sketch, embeddings, lloyd, snap, residual, cabs_run,
+  gather, svd_w, sketch, embeddings, argmin_with_gap, lloyd, snap, residual, cabs_run,
   row_sq_norms, hard_threshold_select, hard_threshold_followup, orthogonalize,
-  leverage_scores, leverage_sample: pinned
-  (tests/test_oracle_*.py).  residual_sampled (implicit source): parity unpinned
-  beyond self-consistency (not on the round-1 path).
+  leverage_scores, leverage_sample: pinned (tests/test_oracle_*.py).
 """
 from __future__ import annotations
 

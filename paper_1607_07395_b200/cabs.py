@@ -75,7 +75,7 @@ class KmProblem(ctypes.Structure):
     _fields_ = [("X", c_vp), ("ldx", c_i64), ("n_loc", c_i64), ("n_glob", c_i64), ("row_off", c_i64),
                 ("d", c_i32), ("k2", c_i32), ("tag", c_i32), ("init_idx", c_vp), ("init_centres", c_vp),
                 ("centres", c_vp), ("ldc", c_i64), ("labels", c_vp), ("cluster_w", c_vp), ("objective", c_vp),
-                ("near_ties", c_vp)]
+                ("near_ties", c_vp), ("tie_log", c_vp), ("tie_log_cap", c_i32)]
 
 
 class SelProblem(ctypes.Structure):
@@ -112,7 +112,7 @@ _SIGS = {
                            ctypes.POINTER(Comm), c_vp]),
     "cabs_kmeans": (c_i32, [ctypes.POINTER(Plan), c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32,
                             c_i32, c_f32, c_u64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,
-                            c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+                            c_vp, c_i32, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_kmeans_pair": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(KmProblem), ctypes.POINTER(KmProblem), c_i32,
                                  c_i32, c_f32, c_u64, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_select": (c_i32, [ctypes.POINTER(Plan), c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_vp, c_i64,
@@ -273,22 +273,44 @@ def cabs_embed(plan, k, C, R, W, mode, tol, P, Q, s, r, ws, sigma=None, comm=Non
 
 def cabs_kmeans(plan, X, n_loc, n_glob, row_off, d, k2, iters, weight_kind, weight_p, seed, tag,
                 centres, labels, cluster_w, objective, ws, near_ties=None, init_idx=None,
-                init_centres=None, comm=None, stream=None):
+                init_centres=None, comm=None, stream=None, tie_log=None):
     _check(load().cabs_kmeans(ctypes.byref(plan), _p(X), _ld(X), int(n_loc), int(n_glob), int(row_off),
                               int(d), int(k2), int(iters), int(weight_kind), float(weight_p), int(seed),
                               int(tag), _p(init_idx), _p(init_centres), _p(centres), _ld(centres),
-                              _p(labels), _p(cluster_w), _p(objective), _p(near_ties), _p(ws), ws.numel(),
-                              _comm(comm), _stream(stream)), "cabs_kmeans")
+                              _p(labels), _p(cluster_w), _p(objective), _p(near_ties), _p(tie_log),
+                              tie_log_cap(tie_log), _p(ws), ws.numel(), _comm(comm), _stream(stream)), "cabs_kmeans")
+
+
+def tie_log_cap(tie_log):
+    """Entries a near-tie log buffer holds (int32[1 + 5 cap])."""
+    return 0 if tie_log is None else (tie_log.numel() - 1) // 5
+
+
+def new_tie_log(cap, device):
+    return torch.zeros(1 + 5 * cap, dtype=torch.int32, device=device)
+
+
+def read_tie_log(tie_log):
+    """Host list of (iteration, point, nearest centre, runner-up centre, relative gap) and the
+    total count of near ties seen (which may exceed the stored entries)."""
+    import struct
+    v = tie_log.cpu().tolist()
+    n = min(v[0], tie_log_cap(tie_log))
+    out = []
+    for q in range(n):
+        it, p, j1, j2, gb = v[1 + 5 * q:6 + 5 * q]
+        out.append((it, p, j1, j2, struct.unpack("<f", struct.pack("<i", gb))[0]))
+    return sorted(out), v[0]
 
 
 def km_problem(X, n_loc, n_glob, row_off, d, k2, tag, centres, labels, cluster_w, objective, near_ties=None,
-               init_idx=None, init_centres=None):
+               init_idx=None, init_centres=None, tie_log=None):
     """Describe one side of cabs_kmeans_pair (tensors must outlive the call)."""
     def ptr(t):
         return None if t is None else t.data_ptr()
     return KmProblem(ptr(X), _ld(X), int(n_loc), int(n_glob), int(row_off), int(d), int(k2), int(tag), ptr(init_idx),
                      ptr(init_centres), ptr(centres), _ld(centres), ptr(labels), ptr(cluster_w), ptr(objective),
-                     ptr(near_ties))
+                     ptr(near_ties), ptr(tie_log), tie_log_cap(tie_log))
 
 
 def cabs_kmeans_pair(plan, a, b, iters, weight_kind, weight_p, seed, ws, comm=None, stream=None):

@@ -408,6 +408,7 @@ static LloydJob km_job(const cabs_km_problem& p, const KmSlot& k) {
   j.X = p.X; j.ldx = p.ldx; j.N = p.n_loc; j.d = p.d; j.k2 = p.k2; j.w = k.w; j.bounds = k.bounds;
   j.centres = p.centres; j.ldc = p.ldc; j.labels = p.labels; j.objective = p.objective; j.near_ties = p.near_ties;
   j.cluster_w = p.cluster_w; j.scratch = k.scr; j.scratch_bytes = k.scr_bytes;
+  j.tie_log = p.tie_log; j.tie_cap = p.tie_log_cap; j.row_off = p.row_off;
   return j;
 }
 
@@ -430,7 +431,7 @@ static int32_t km_loop(const cabs_km_problem& p, int32_t iters, const KmSlot& k,
     int ga = 1;
     if (p.n_loc > 0) {
       launch_km_assign(p.X, p.ldx, p.n_loc, d, p.centres, p.ldc, k2, k.w, p.labels, wsp<double>(ws, L.km_pobj),
-                       wsp<int>(ws, L.km_ptie), &ga, st);
+                       wsp<int>(ws, L.km_ptie), &ga, st, p.tie_log, p.tie_log_cap, t, p.row_off);
       launch_km_accum(p.X, p.ldx, p.n_loc, d, p.labels, k.w, k.bounds, fsum, fwt, st);
       CABS_LAUNCH_CHECK("km_assign/accum");
       launch_km_reduce(fsum, fwt, k.bounds, p.n_loc, k2, d, wsp<double>(ws, L.km_pobj), wsp<int>(ws, L.km_ptie), ga,
@@ -449,20 +450,21 @@ static int32_t km_loop(const cabs_km_problem& p, int32_t iters, const KmSlot& k,
 int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t n_loc, int64_t n_glob, int64_t row_off,
                     int32_t d, int32_t k2, int32_t iters, int32_t weight_kind, float weight_p, uint64_t seed,
                     int32_t tag, const int64_t* init_idx, const float* init_centres, float* centres, int64_t ldc,
-                    int32_t* labels, double* cluster_w, double* objective, int32_t* near_ties, void* ws,
-                    size_t ws_bytes, const cabs_comm* comm, void* stream) {
+                    int32_t* labels, double* cluster_w, double* objective, int32_t* near_ties, int32_t* tie_log,
+                    int32_t tie_log_cap, void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream) {
   CABS_TRY(check_plan(plan));
   Ws L;
   CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
   const cabs_km_problem p{X, ldx, n_loc, n_glob, row_off, d, k2, tag, init_idx, init_centres, centres, ldc,
-                          labels, cluster_w, objective, near_ties};
+                          labels, cluster_w, objective, near_ties, tie_log, tie_log_cap};
   CABS_TRY(km_check(plan, L, p, iters, weight_kind));
+  if (tie_log) CABS_CUDA_TRY(cudaMemsetAsync(tie_log, 0, sizeof(int32_t), S(stream)));
   const KmSlot k = km_slot(ws, L, 0);
   CABS_TRY(km_prepare(p, weight_kind, weight_p, seed, k, comm, stream));
   if (km_persistent_allowed(comm) && n_loc > 0) {
     const LloydJob j = km_job(p, k);
     if (kmeans_tc_selected(k2, d)) {
-      if (launch_lloyd_tc(&j, 1, iters, nullptr, nullptr, S(stream))) {
+      if (launch_lloyd_tc(&j, 1, iters, S(stream))) {
         CABS_LAUNCH_CHECK("lloyd_tc");
         return CABS_OK;
       }
@@ -487,6 +489,8 @@ int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const 
   if (!a || !b) return arg_error("kmeans_pair: null problem");
   CABS_TRY(km_check(plan, L, *a, iters, weight_kind));
   CABS_TRY(km_check(plan, L, *b, iters, weight_kind));
+  if (a->tie_log) CABS_CUDA_TRY(cudaMemsetAsync(a->tie_log, 0, sizeof(int32_t), S(stream)));
+  if (b->tie_log) CABS_CUDA_TRY(cudaMemsetAsync(b->tie_log, 0, sizeof(int32_t), S(stream)));
   const KmSlot ka = km_slot(ws, L, 0), kb = km_slot(ws, L, 1);
   if (!multi(comm)) {
     // both sides' weights, Floyd initialisations and initial centres in one launch each; the
@@ -522,7 +526,7 @@ int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const 
   if (km_persistent_allowed(comm) && a->n_loc > 0 && b->n_loc > 0) {
     const LloydJob j[2] = {km_job(*a, ka), km_job(*b, kb)};
     if (kmeans_tc_selected(a->k2, a->d) && kmeans_tc_selected(b->k2, b->d)) {
-      if (launch_lloyd_tc(j, 2, iters, nullptr, nullptr, S(stream))) {
+      if (launch_lloyd_tc(j, 2, iters, S(stream))) {
         CABS_LAUNCH_CHECK("lloyd_tc");
         return CABS_OK;
       }

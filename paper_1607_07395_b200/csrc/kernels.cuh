@@ -67,7 +67,8 @@ void launch_km_weights(const float* X, int64_t ldx, int64_t N, int d, int kind, 
 void launch_km_init(const float* X, int64_t ldx, int64_t n_loc, int64_t row_off, int d, int k2, const int64_t* idx,
                     const float* init_c, int64_t ldic, float* centres, int64_t ldc, cudaStream_t st);
 void launch_km_assign(const float* X, int64_t ldx, int64_t N, int d, const float* centres, int64_t ldc, int k2,
-                      const float* w, int* labels, double* pobj, int* ptie, int* grid_out, cudaStream_t st);
+                      const float* w, int* labels, double* pobj, int* ptie, int* grid_out, cudaStream_t st,
+                      int* tie_log = nullptr, int tie_cap = 0, int it = 0, int64_t row_off = 0);
 void launch_km_distmat(const float* X, int64_t ldx, int64_t N, int d, const float* centres, int64_t ldc, int k2,
                        float* D, int64_t ldd, cudaStream_t st);
 void launch_km_accum(const float* X, int64_t ldx, int64_t N, int d, const int* labels, const float* w,
@@ -93,14 +94,15 @@ struct LloydJob {
   double* cluster_w;
   void* scratch;
   size_t scratch_bytes;
+  int* tie_log;      // near-tie log or null (km_tile.cuh: km_log_tie)
+  int tie_cap;
+  int64_t row_off;   // global index of local point 0
 };
 bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long long* prof, cudaStream_t st);
 // lloyd_tc.cu: the same loop with the distance cross-term on the tensor cores (d, k2 <= 128);
-// tie_logs[q] (or NULL): near-tie log of problem q, [0] = count, then (iteration, point, j1, j2,
-// gap bits) per entry, up to tie_caps[q] entries.  False -> not applicable.
+// the jobs' near-tie logs as km_log_tie.  False -> not applicable.
 void ktc_debug_timeline(long long* out, int n);
-bool launch_lloyd_tc(const LloydJob* jobs, int njobs, int iters, int* const* tie_logs, const int* tie_caps,
-                     cudaStream_t st);
+bool launch_lloyd_tc(const LloydJob* jobs, int njobs, int iters, cudaStream_t st);
 void lloyd_debug_timeline(long long* out, int n);
 void embed_debug_timeline(long long* out);
 void snap_debug_counters(long long* out);

@@ -11,12 +11,28 @@ namespace cabsk {
 constexpr int kTileP = 64, kTileC = 64, kTileD = 16;
 constexpr float kNearTie = 1e-5f;  // north_star near-tie rule: relative gap (d2 - d1)/d2 < 1e-5
 
+// one entry of a near-tie log (int32 [0] = count of near ties seen, then per entry: iteration,
+// global point index, nearest centre, runner-up centre, relative gap (FP32 bits)); entries past
+// cap are counted, not stored
+__device__ __forceinline__ void km_log_tie(int* log, int cap, int it, int64_t p, int j1, int j2, float d1, float d2) {
+  const int slot = atomicAdd(log, 1);
+  if (slot < cap) {
+    int* e = log + 1 + 5 * slot;
+    e[0] = it;
+    e[1] = static_cast<int>(p);
+    e[2] = j1;
+    e[3] = j2;
+    e[4] = __float_as_int(d2 > 0.f ? (d2 - d1) / d2 : 0.f);
+  }
+}
+
 struct KmTileSmem {
   float Xs[kTileD][kTileP + 4];
   float Cs[kTileD][kTileC + 4];
   float sb_d[16][kTileP + 1];
   int sb_j[16][kTileP + 1];
   float ss_d[16][kTileP + 1];
+  int ss_j[16][kTileP + 1];
 };
 
 // centres may be rewritten by other CTAs inside a persistent kernel: COHERENT loads
@@ -83,12 +99,12 @@ __device__ __forceinline__ void km_tile_block(const float* __restrict__ X, int64
 template <bool COHERENT>
 __device__ __forceinline__ void km_tile_argmin(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
                                                const float* __restrict__ centres, int64_t ldc, int k2, int64_t p0,
-                                               KmTileSmem& sm, int* lab_s, float* d1_s, float* d2_s) {
+                                               KmTileSmem& sm, int* lab_s, float* d1_s, float* d2_s, int* j2_s) {
   const int tid = threadIdx.x, tp = tid & 15, tc = tid >> 4;
   float bd[4], sd[4];
-  int bj[4];
+  int bj[4], sj[4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a) { bd[a] = FLT_MAX; sd[a] = FLT_MAX; bj[a] = 0x7fffffff; }
+  for (int a = 0; a < 4; ++a) { bd[a] = FLT_MAX; sd[a] = FLT_MAX; bj[a] = 0x7fffffff; sj[a] = -1; }
   for (int j0 = 0; j0 < k2; j0 += kTileC) {
     float acc[4][4];
     km_tile_block<COHERENT>(X, ldx, N, d, centres, ldc, k2, p0, j0, sm, acc);
@@ -101,10 +117,12 @@ __device__ __forceinline__ void km_tile_argmin(const float* __restrict__ X, int6
         const float v = acc[a][b];
         if (v < bd[a] || (v == bd[a] && j < bj[a])) {
           sd[a] = bd[a];
+          sj[a] = bj[a];
           bd[a] = v;
           bj[a] = j;
-        } else {
-          sd[a] = fminf(sd[a], v);
+        } else if (v < sd[a]) {
+          sd[a] = v;
+          sj[a] = j;
         }
       }
     }
@@ -114,25 +132,28 @@ __device__ __forceinline__ void km_tile_argmin(const float* __restrict__ X, int6
     sm.sb_d[tc][tp + 16 * a] = bd[a];
     sm.sb_j[tc][tp + 16 * a] = bj[a];
     sm.ss_d[tc][tp + 16 * a] = sd[a];
+    sm.ss_j[tc][tp + 16 * a] = sj[a];
   }
   __syncthreads();
   if (tid < kTileP) {
     float B = sm.sb_d[0][tid], S = sm.ss_d[0][tid];
-    int Bj = sm.sb_j[0][tid];
+    int Bj = sm.sb_j[0][tid], Sj = sm.ss_j[0][tid];
     for (int t = 1; t < 16; ++t) {
       const float b2 = sm.sb_d[t][tid], s2 = sm.ss_d[t][tid];
-      const int j2 = sm.sb_j[t][tid];
+      const int j2 = sm.sb_j[t][tid], sj2 = sm.ss_j[t][tid];
       if (b2 < B || (b2 == B && j2 < Bj)) {
-        S = fminf(fminf(S, s2), B);
+        if (B < s2) { S = B; Sj = Bj; } else { S = s2; Sj = sj2; }
         B = b2;
         Bj = j2;
       } else {
-        S = fminf(fminf(S, s2), b2);
+        if (b2 < S) { S = b2; Sj = j2; }
+        if (s2 < S) { S = s2; Sj = sj2; }
       }
     }
     lab_s[tid] = Bj;
     d1_s[tid] = B;
     d2_s[tid] = S;
+    if (j2_s) j2_s[tid] = Sj;
   }
   __syncthreads();
 }

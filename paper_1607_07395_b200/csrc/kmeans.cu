@@ -170,9 +170,10 @@ __global__ void __launch_bounds__(256) km_assign_kernel(const float* __restrict_
                                                         const float* __restrict__ centres, int64_t ldc, int k2,
                                                         const float* __restrict__ w, int* __restrict__ labels,
                                                         double* __restrict__ pobj, int* __restrict__ ptie,
-                                                        float* __restrict__ D, int64_t ldd) {
+                                                        float* __restrict__ D, int64_t ldd, int* tie_log, int tie_cap,
+                                                        int it, int64_t row_off) {
   __shared__ KmTileSmem sm;
-  __shared__ int lab_s[kTileP];
+  __shared__ int lab_s[kTileP], j2_s[kTileP];
   __shared__ float d1_s[kTileP], d2_s[kTileP];
   __shared__ double s_red[8];
   __shared__ int s_tie[8];
@@ -185,14 +186,16 @@ __global__ void __launch_bounds__(256) km_assign_kernel(const float* __restrict_
     if (DISTMAT) {
       km_tile_distmat(X, ldx, N, d, centres, ldc, k2, p0, sm, D, ldd);
     } else {
-      km_tile_argmin<false>(X, ldx, N, d, centres, ldc, k2, p0, sm, lab_s, d1_s, d2_s);
+      km_tile_argmin<false>(X, ldx, N, d, centres, ldc, k2, p0, sm, lab_s, d1_s, d2_s, j2_s);
       if (tid < kTileP) {
         const int64_t p = p0 + tid;
         if (p < N) {
           const float B = d1_s[tid], S = d2_s[tid];
           labels[p] = lab_s[tid];
           obj += static_cast<double>(w[p]) * static_cast<double>(B);
-          ties += (S - B) < kNearTie * S;
+          const bool tie = (S - B) < kNearTie * S;
+          ties += tie;
+          if (tie && tie_log) km_log_tie(tie_log, tie_cap, it, row_off + p, lab_s[tid], j2_s[tid], B, S);
         }
       }
       __syncthreads();
@@ -225,11 +228,13 @@ static int assign_grid(int64_t N) {
 }
 
 void launch_km_assign(const float* X, int64_t ldx, int64_t N, int d, const float* centres, int64_t ldc, int k2,
-                      const float* w, int* labels, double* pobj, int* ptie, int* grid_out, cudaStream_t st) {
+                      const float* w, int* labels, double* pobj, int* ptie, int* grid_out, cudaStream_t st,
+                      int* tie_log, int tie_cap, int it, int64_t row_off) {
   const int g = assign_grid(N);
   *grid_out = g;
   note_launch();
-  km_assign_kernel<false><<<g, 256, 0, st>>>(X, ldx, N, d, centres, ldc, k2, w, labels, pobj, ptie, nullptr, 0);
+  km_assign_kernel<false><<<g, 256, 0, st>>>(X, ldx, N, d, centres, ldc, k2, w, labels, pobj, ptie, nullptr, 0, tie_log,
+                                             tie_cap, it, row_off);
 }
 
 void launch_km_distmat(const float* X, int64_t ldx, int64_t N, int d, const float* centres, int64_t ldc, int k2,
@@ -237,7 +242,8 @@ void launch_km_distmat(const float* X, int64_t ldx, int64_t N, int d, const floa
   if (N <= 0) return;
   const int g = assign_grid(N);
   note_launch();
-  km_assign_kernel<true><<<g, 256, 0, st>>>(X, ldx, N, d, centres, ldc, k2, nullptr, nullptr, nullptr, nullptr, D, ldd);
+  km_assign_kernel<true><<<g, 256, 0, st>>>(X, ldx, N, d, centres, ldc, k2, nullptr, nullptr, nullptr, nullptr, D, ldd,
+                                            nullptr, 0, 0, 0);
 }
 
 // ---------------------------------------------------------------- accumulate

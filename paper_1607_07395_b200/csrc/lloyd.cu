@@ -69,6 +69,9 @@ struct LloydProb {
   const unsigned* bounds;  // [2] max|x|, max w (km_weights)
   double* pobj;            // [iters][G]
   int* ptie;               // [iters][G]
+  int* tie_log;            // near-tie log ([0] count, then 5 ints per entry) or null
+  int tie_cap;
+  int64_t row_off;         // global index of local point 0 (for the log)
   int cap;                 // points per chunk (multiple of 16, <= kLP): all of the CTA's when resident
   int pitch;               // cap + 1: odd, so a warp reading one point's dimensions is conflict-free
 };
@@ -203,7 +206,7 @@ __device__ __forceinline__ void accumulate_owned(const int* lab, int np, const P
 // (v, v + 1) in one FFMA2 lane pair, an odd last centre in scalar FP32 (the same IEEE ops).
 template <int NA, int NV>
 __device__ __forceinline__ void dist_block(const float2* __restrict__ xq, int P, const ulonglong2* cq, int d2,
-                                           int jc, int k2, float* bd, float* sd, int* bj) {
+                                           int jc, int k2, float* bd, float* sd, int* bj, int* sj) {
   unsigned long long acc0[NA], acc1[NA];
   float accs[NA];
 #pragma unroll
@@ -250,9 +253,21 @@ __device__ __forceinline__ void dist_block(const float2* __restrict__ xq, int P,
       else if (v == 1) val = f2_hi(acc0[u]);
       else if (v == 2) val = NV == 3 ? accs[u] : f2_lo(acc1[u]);
       else val = f2_hi(acc1[u]);
-      if (val < bd[u] || (val == bd[u] && j < bj[u])) { sd[u] = bd[u]; bd[u] = val; bj[u] = j; }
-      else sd[u] = fminf(sd[u], val);
+      if (val < bd[u] || (val == bd[u] && j < bj[u])) { sd[u] = bd[u]; sj[u] = bj[u]; bd[u] = val; bj[u] = j; }
+      else if (val < sd[u]) { sd[u] = val; sj[u] = j; }
     }
+  }
+}
+
+// merge (b2, j2, s2, sj2) into the running (best, index, runner-up, index); lowest index on ties
+__device__ __forceinline__ void merge_best2(float& bd, int& bj, float& sd, int& sj, float b2, int j2, float s2,
+                                            int sj2) {
+  if (b2 < bd || (b2 == bd && j2 < bj)) {
+    if (bd < s2) { sd = bd; sj = bj; } else { sd = s2; sj = sj2; }
+    bd = b2; bj = j2;
+  } else {
+    if (b2 < sd) { sd = b2; sj = j2; }
+    if (s2 < sd) { sd = s2; sj = sj2; }
   }
 }
 
@@ -262,11 +277,11 @@ __device__ __forceinline__ void dist_block(const float2* __restrict__ xq, int P,
 template <int NA>
 __device__ __forceinline__ void dist_rows(const float* __restrict__ xs, int P, const float* cs, int d, int k2, int pt,
                                           int ct, int lane, int warp, float (*sb_d)[kLP], int (*sb_j)[kLP],
-                                          float (*ss_d)[kLP]) {
+                                          float (*ss_d)[kLP], int (*ss_j)[kLP]) {
   float bd[NA], sd[NA];
-  int bj[NA];
+  int bj[NA], sj[NA];
 #pragma unroll
-  for (int q = 0; q < NA; ++q) { bd[q] = FLT_MAX; sd[q] = FLT_MAX; bj[q] = 0x7fffffff; }
+  for (int q = 0; q < NA; ++q) { bd[q] = FLT_MAX; sd[q] = FLT_MAX; bj[q] = 0x7fffffff; sj[q] = -1; }
   const float2* xq = reinterpret_cast<const float2*>(xs) + pt;
   const int d2 = (d + 1) >> 1;
   for (int j0 = 0; j0 < k2; j0 += kLC) {
@@ -275,18 +290,17 @@ __device__ __forceinline__ void dist_rows(const float* __restrict__ xs, int P, c
     const int rem = k2 - j0 - 2 * warp;
     const int nv = rem <= 0 ? 0 : (rem >= 64 ? 4 : (rem + 15) >> 4);
     const ulonglong2* cq = reinterpret_cast<const ulonglong2*>(cs) + (size_t)(j0 >> 6) * d2 * 32 + ct;
-    if (nv == 4) dist_block<NA, 4>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj);
-    else if (nv == 3) dist_block<NA, 3>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj);
-    else if (nv == 2) dist_block<NA, 2>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj);
-    else if (nv == 1) dist_block<NA, 1>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj);
+    if (nv == 4) dist_block<NA, 4>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj, sj);
+    else if (nv == 3) dist_block<NA, 3>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj, sj);
+    else if (nv == 2) dist_block<NA, 2>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj, sj);
+    else if (nv == 1) dist_block<NA, 1>(xq, P, cq, d2, j0 + ct, k2, bd, sd, bj, sj);
   }
   // merge the two centre lanes of this warp (lanes l and l ^ 16 hold the same points)
 #pragma unroll
   for (int u = 0; u < NA; ++u) {
     const float b2 = __shfl_xor_sync(0xffffffffu, bd[u], 16), s2 = __shfl_xor_sync(0xffffffffu, sd[u], 16);
-    const int j2 = __shfl_xor_sync(0xffffffffu, bj[u], 16);
-    if (b2 < bd[u] || (b2 == bd[u] && j2 < bj[u])) { sd[u] = fminf(fminf(sd[u], s2), bd[u]); bd[u] = b2; bj[u] = j2; }
-    else sd[u] = fminf(fminf(sd[u], s2), b2);
+    const int j2 = __shfl_xor_sync(0xffffffffu, bj[u], 16), sj2 = __shfl_xor_sync(0xffffffffu, sj[u], 16);
+    merge_best2(bd[u], bj[u], sd[u], sj[u], b2, j2, s2, sj2);
   }
   if (lane < 16) {
 #pragma unroll
@@ -294,6 +308,7 @@ __device__ __forceinline__ void dist_rows(const float* __restrict__ xs, int P, c
       sb_d[warp][pt + 16 * u] = bd[u];
       sb_j[warp][pt + 16 * u] = bj[u];
       ss_d[warp][pt + 16 * u] = sd[u];
+      ss_j[warp][pt + 16 * u] = sj[u];
     }
   }
 }
@@ -314,6 +329,7 @@ __global__ void __launch_bounds__(kLT, 2) lloyd_persistent_kernel(LloydArgs a) {
   __shared__ float sb_d[8][kLP];  // per point: best / runner-up of each warp's two centre lanes
   __shared__ int sb_j[8][kLP];
   __shared__ float ss_d[8][kLP];
+  __shared__ int ss_j[8][kLP];
   __shared__ int lab_s[kLP];
   __shared__ double s_red[kMaxProb][kLT / 32];
   __shared__ int s_tie[kMaxProb][kLT / 32];
@@ -480,24 +496,21 @@ __global__ void __launch_bounds__(kLT, 2) lloyd_persistent_kernel(LloydArgs a) {
         // distances: rows u < ceil(np / 16)
         {
           const int na = (np + 15) >> 4;
-          if (na <= 3) dist_rows<3>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
-          else if (na <= 5) dist_rows<5>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
-          else dist_rows<7>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d);
+          if (na <= 3) dist_rows<3>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d, ss_j);
+          else if (na <= 5) dist_rows<5>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d, ss_j);
+          else dist_rows<7>(S.xs, pr.pitch, S.cs, d, k2, pt, ct, lane, warp, sb_d, sb_j, ss_d, ss_j);
         }
         __syncthreads();
         for (int p = tid; p < np; p += kLT) {  // merge the 8 warps (lowest index on ties)
           float B = sb_d[0][p], Sd = ss_d[0][p];
-          int Bj = sb_j[0][p];
-          for (int t = 1; t < kLT / 32; ++t) {
-            const float b2 = sb_d[t][p], s2 = ss_d[t][p];
-            const int j2 = sb_j[t][p];
-            if (b2 < B || (b2 == B && j2 < Bj)) { Sd = fminf(fminf(Sd, s2), B); B = b2; Bj = j2; }
-            else Sd = fminf(fminf(Sd, s2), b2);
-          }
+          int Bj = sb_j[0][p], Sj = ss_j[0][p];
+          for (int t = 1; t < kLT / 32; ++t) merge_best2(B, Bj, Sd, Sj, sb_d[t][p], sb_j[t][p], ss_d[t][p], ss_j[t][p]);
           lab_s[p] = Bj;
           pr.labels[p0 + p] = Bj;
           obj += static_cast<double>(S.wts[p]) * static_cast<double>(B);
-          ties += (Sd - B) < kNearTie * Sd;
+          const bool tie = (Sd - B) < kNearTie * Sd;
+          ties += tie;
+          if (tie && pr.tie_log) km_log_tie(pr.tie_log, pr.tie_cap, it, pr.row_off + p0 + p, Bj, Sj, B, Sd);
         }
         __syncthreads();
         LPROF(1);
@@ -709,6 +722,7 @@ bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long lo
     p.X = j.X; p.ldx = j.ldx; p.N = j.N; p.d = j.d; p.k2 = j.k2; p.w = j.w;
     p.centres = j.centres; p.ldc = j.ldc; p.labels = j.labels; p.objective = j.objective;
     p.near_ties = j.near_ties; p.cluster_w = j.cluster_w; p.bounds = j.bounds; p.cap = cap[q];
+    p.tie_log = j.tie_log; p.tie_cap = j.tie_cap; p.row_off = j.row_off;
     p.pitch = cap[q] + 1;
     p.fsum = reinterpret_cast<long long*>(base);
     unsigned* gb = reinterpret_cast<unsigned*>(p.fsum + 3 * E);

@@ -93,6 +93,7 @@ struct KtcProb {
   int* ptie;        // [iters][Gq]
   int* tie_log;     // [1 + 5 cap] or null
   int tie_cap;
+  int64_t row_off;  // global index of local point 0
 };
 
 struct KtcArgs {
@@ -562,14 +563,7 @@ lloyd_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant_
           obj += static_cast<double>(__ldg(pr.w + p)) * static_cast<double>(bd);
           const bool tie = (sd - bd) < kNearTie * sd;
           ties += tie;
-          if (tie && pr.tie_log) {
-            const int slot = atomicAdd(pr.tie_log, 1);
-            if (slot < pr.tie_cap) {
-              int* e = pr.tie_log + 1 + 5 * slot;
-              e[0] = it; e[1] = static_cast<int>(p); e[2] = bj; e[3] = sj;
-              e[4] = __float_as_int((sd - bd) / sd);
-            }
-          }
+          if (tie && pr.tie_log) km_log_tie(pr.tie_log, pr.tie_cap, it, pr.row_off + p, bj, sj, bd, sd);
         }
         // tile done: xs and the masks may be rewritten (every warp of 2-9 arrives and waits)
         __syncwarp();
@@ -770,8 +764,7 @@ bool kmeans_tc_selected(int k2, int d) {
   return a.total + 1024 <= kKtcSmemCap && encoder_k() != nullptr;
 }
 
-bool launch_lloyd_tc(const LloydJob* jobs, int njobs, int iters, int* const* tie_logs, const int* tie_caps,
-                     cudaStream_t st) {
+bool launch_lloyd_tc(const LloydJob* jobs, int njobs, int iters, cudaStream_t st) {
   if (njobs < 1 || njobs > 2) return false;
   int dmax = 0, k2max = 0;
   for (int q = 0; q < njobs; ++q) {
@@ -862,10 +855,10 @@ bool launch_lloyd_tc(const LloydJob* jobs, int njobs, int iters, int* const* tie
     a.gbar[q] = gb;
     p.pobj = reinterpret_cast<double*>(gb + 4);
     p.ptie = reinterpret_cast<int*>(p.pobj + (size_t)iters * Gt);
-    p.tie_log = tie_logs ? tie_logs[q] : nullptr;
-    p.tie_cap = tie_caps ? tie_caps[q] : 0;
+    p.tie_log = j.tie_log;
+    p.tie_cap = j.tie_cap;
+    p.row_off = j.row_off;
     if (cudaMemsetAsync(base, 0, sizeof(long long) * 3 * E + 16, st) != cudaSuccess) return false;
-    if (p.tie_log && cudaMemsetAsync(p.tie_log, 0, sizeof(int), st) != cudaSuccess) return false;
   }
   if (njobs == 1) tm[1] = tm[0];
   cfg.gridDim = dim3(static_cast<unsigned>(Gt));

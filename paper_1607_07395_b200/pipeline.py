@@ -38,6 +38,7 @@ class CabsConfig:
 
 
 STEPS = ("pilot_embed", "kmeans", "select", "sketch", "residual")
+TIE_LOG_CAP = 4096  # near-tie log entries kept per side and run
 STEPS_HARD = ("pilot_embed", "hard_select", "sketch", "residual")
 STEPS_LEVERAGE = ("pilot_embed", "orthogonalize", "leverage_select", "sketch", "residual")
 
@@ -71,6 +72,8 @@ class CabsPipeline:
         self.cw_r, self.cw_c = z(k2, dt=f64), z(k2, dt=f64)
         self.obj_r, self.obj_c = z(cfg.iters, dt=f64), z(cfg.iters, dt=f64)
         self.tie_r, self.tie_c = z(cfg.iters, dt=i32), z(cfg.iters, dt=i32)
+        # near-tie logs (north_star: "near-tie argmins ... must be logged"): C.read_tie_log
+        self.tlog_r, self.tlog_c = C.new_tie_log(TIE_LOG_CAP, dev), C.new_tie_log(TIE_LOG_CAP, dev)
         self.Ib, self.Jb = z(k2, dt=i64), z(k2, dt=i64)
         self.rep_r, self.rep_c = z(k2, dt=i64), z(k2, dt=i64)
         self.gap_r, self.gap_c = z(k2), z(k2)
@@ -100,9 +103,9 @@ class CabsPipeline:
         c, p = self.cfg, self.plan
         # both sides in one call: one persistent kernel serves the two problems (single GPU)
         rows = C.km_problem(self.P, p.m_loc, p.m, p.row_begin, c.k1, c.k2, C.TAG_INIT_ROWS, self.cen_r, self.lab_r,
-                            self.cw_r, self.obj_r, near_ties=self.tie_r, init_idx=init_rows)
+                            self.cw_r, self.obj_r, near_ties=self.tie_r, init_idx=init_rows, tie_log=self.tlog_r)
         cols = C.km_problem(self.Q, p.n_sl, p.n, p.col_begin, c.k1, c.k2, C.TAG_INIT_COLS, self.cen_c, self.lab_c,
-                            self.cw_c, self.obj_c, near_ties=self.tie_c, init_idx=init_cols)
+                            self.cw_c, self.obj_c, near_ties=self.tie_c, init_idx=init_cols, tie_log=self.tlog_c)
         C.cabs_kmeans_pair(p, rows, cols, c.iters, c.weight_kind, c.weight_p, c.seed, self.ws, comm=self.comm)
 
     def select(self):
@@ -223,4 +226,5 @@ class CabsPipeline:
                     tie_c=cpu(self.tie_c), Ib=cpu(self.Ib), Jb=cpu(self.Jb), rep_r=cpu(self.rep_r),
                     rep_c=cpu(self.rep_c), gap_r=cpu(self.gap_r), gap_c=cpu(self.gap_c),
                     r2=r2, U=cpu(self.U), V=cpu(self.V), s2=cpu(self.s2), sigma2=cpu(self.sigma2),
-                    resid_sq=float(self.out[0]), a_sq=float(self.out[1]))
+                    resid_sq=float(self.out[0]), a_sq=float(self.out[1]),
+                    tie_log_r=C.read_tie_log(self.tlog_r), tie_log_c=C.read_tie_log(self.tlog_c))

@@ -167,3 +167,27 @@ def test_snap_over_all_points_not_members():
     X = np.array([[0.0], [0.9], [2.0]])
     sn = O.snap(X, np.array([[1.0], [2.0]]), np.array([1.0, 1.0]))
     assert sn.rep_of_centre.tolist() == [1, 2]
+
+
+def test_argmin_with_gap_closed_form():
+    """The gap that decides which GPU/oracle label flips are excused (Z18): lowest-index argmin,
+    relative gap (d2 - d1) / d2 to the runner-up, 0 for an exact tie, 0 when d2 = 0, inf with
+    one centre; checked on distances with known values, and on points against centres at known
+    positions (x = 0 against centres at 1 and 3 -> d = 1, 9 -> gap 8/9)."""
+    D = np.array([[1.0, 4.0, 9.0],   # unique minimum: gap (4 - 1) / 4
+                  [2.0, 2.0, 5.0],   # exact tie -> lowest index, gap 0
+                  [7.0, 3.0, 3.5],   # minimum in the middle: gap (3.5 - 3) / 3.5
+                  [0.0, 0.0, 1.0],   # d2 = 0 -> gap 0
+                  [5.0, 0.0, 5.0]])  # zero distance, runner-up 5: gap 1
+    lab, d1, gap = O.argmin_with_gap(D)
+    assert lab.tolist() == [0, 0, 1, 0, 1]
+    assert d1.tolist() == [1.0, 2.0, 3.0, 0.0, 0.0]
+    assert np.allclose(gap, [0.75, 0.0, 0.5 / 3.5, 0.0, 1.0], rtol=0, atol=1e-15)
+    lab1, _, gap1 = O.argmin_with_gap(np.array([[2.0], [0.5]]))
+    assert lab1.tolist() == [0, 0] and np.all(np.isinf(gap1))
+    X = np.array([[0.0], [2.0], [2.9]])
+    cen = np.array([[1.0], [3.0]])
+    lab2, d12, gap2 = O.argmin_with_gap(O.sq_dist_all(X, cen))
+    assert lab2.tolist() == [0, 0, 1]  # x = 2 is equidistant: lowest index
+    assert np.allclose(d12, [1.0, 1.0, 0.01], rtol=0, atol=1e-12)
+    assert np.allclose(gap2, [8.0 / 9.0, 0.0, (3.61 - 0.01) / 3.61], rtol=0, atol=1e-12)
