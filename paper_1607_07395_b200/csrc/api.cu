@@ -169,8 +169,10 @@ struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
+// Per host thread (thread_local): a caller's event record + stream wait cannot interleave with
+// another thread's, so distinct (workspace, stream) pairs stay reentrant across threads.
 static int32_t side_stream(SideStream** out) {
-  static SideStream side[64];
+  static thread_local SideStream side[64];
   int dev = 0;
   CABS_CUDA_TRY(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return arg_error("device index out of range");
@@ -193,20 +195,20 @@ int32_t cabs_pilot(const cabs_plan* plan, const cabs_source* src, int32_t k, uin
   CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
   const cabs_plan& p = *plan;
   if (k < 1 || k > p.kmax || k > p.m || k > p.n) return arg_error("pilot: need 1 <= k <= min(m, n, kmax)");
-  if (!src || !src->a || src->lda < p.n) return arg_error("pilot: bad source");
+  if (!src || (p.row_end > p.row_begin && !src->a) || src->lda < p.n) return arg_error("pilot: bad source");
   if (!I || !J || !C || !R || !W || ldc < k || ldr < p.n || ldw < k) return arg_error("pilot: bad output buffers");
   if (p.m >= 0xFFFFFFFFll || p.n >= 0xFFFFFFFFll) return arg_error("pilot: dims must be < 2^32 - 1");
   cudaStream_t st = S(stream);
   const int64_t m_loc = p.row_end - p.row_begin;
   launch_floyd2(p.m, k, 1u, I, p.n, k, 2u, J, seed, st);  // tags ROWS_PILOT = 1, COLS_PILOT = 2
   CABS_LAUNCH_CHECK("floyd");
-  launch_gather_cols(src->a, src->lda, m_loc, J, k, C, ldc, ws, st);
+  launch_gather_cols(src->a, src->lda, m_loc, p.n, J, k, C, ldc, ws, st);
   CABS_LAUNCH_CHECK("gather_cols");
-  if (multi(comm)) CABS_CUDA_TRY(cudaMemsetAsync(R, 0, sizeof(float) * ldr * k, st));
+  if (multi(comm)) launch_fill_neg_zero(R, ldr * (int64_t)k, st);  // -0.0: the allreduce is then bit-exact
   launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, I, k, p.n, R, ldr, ws, st);
   CABS_LAUNCH_CHECK("gather_rows");
   CABS_TRY(comm_f32(comm, R, ldr * (int64_t)k, stream));
-  launch_gather_w(R, ldr, J, k, W, ldw, st);
+  launch_gather_w(R, ldr, p.n, J, k, W, ldw, st);
   CABS_LAUNCH_CHECK("gather_w");
   return CABS_OK;
 }
@@ -275,7 +277,7 @@ int32_t cabs_pilot_embed(const cabs_plan* plan, const cabs_source* src, int32_t 
   CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
   const cabs_plan& p = *plan;
   if (k < 1 || k > p.kmax || k > p.m || k > p.n) return arg_error("pilot: need 1 <= k <= min(m, n, kmax)");
-  if (!src || !src->a || src->lda < p.n) return arg_error("pilot: bad source");
+  if (!src || (p.row_end > p.row_begin && !src->a) || src->lda < p.n) return arg_error("pilot: bad source");
   if (!I || !J || !C || !R || !W || ldc < k || ldr < p.n || ldw < k) return arg_error("pilot: bad output buffers");
   if (p.m >= 0xFFFFFFFFll || p.n >= 0xFFFFFFFFll) return arg_error("pilot: dims must be < 2^32 - 1");
   if (mode != CABS_STABILIZED && mode != CABS_PSEUDO_SKELETON) return arg_error("embed: bad mode");
@@ -293,7 +295,7 @@ int32_t cabs_pilot_embed(const cabs_plan* plan, const cabs_source* src, int32_t 
   CABS_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
   launch_svd(k, W, ldw, tol, ws, L, sigma, nullptr, nullptr, nullptr, ss->s);
   CABS_LAUNCH_CHECK("svd");
-  launch_gather_cols(src->a, src->lda, m_loc, J, k, C, ldc, ws, st);
+  launch_gather_cols(src->a, src->lda, m_loc, p.n, J, k, C, ldc, ws, st);
   launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, I, k, p.n, R, ldr, ws, st);
   CABS_LAUNCH_CHECK("pilot gathers");
   CABS_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
@@ -311,7 +313,7 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
   const cabs_plan& p = *plan;
   if (k < 1 || k > p.kmax || k > p.m || k > p.n) return arg_error("sketch: need 1 <= k <= min(m, n, kmax)");
   if (mode != CABS_STABILIZED && mode != CABS_PSEUDO_SKELETON) return arg_error("sketch: bad mode");
-  if (!src || !src->a || src->lda < p.n || !Ir || !Ic || !U || !V || !s || ldu < k || ldv < k)
+  if (!src || (p.row_end > p.row_begin && !src->a) || src->lda < p.n || !Ir || !Ic || !U || !V || !s || ldu < k || ldv < k)
     return arg_error("sketch: bad buffers");
   cudaStream_t st = S(stream);
   const int64_t m_loc = p.row_end - p.row_begin;
@@ -330,7 +332,7 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
     launch_svd(k, Wb, L.Kp, tol, ws, L, sigma, nullptr, nullptr, nullptr, ss->s);
     CABS_LAUNCH_CHECK("svd");
     launch_validate_idx2(Ir, p.m, Ic, p.n, k, ws, st);
-    launch_gather_cols(src->a, src->lda, m_loc, Ic, k, Cb, L.Kp, ws, st);
+    launch_gather_cols(src->a, src->lda, m_loc, p.n, Ic, k, Cb, L.Kp, ws, st);
     launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, Ir, k, p.n, Rb, L.ldrb, ws, st);
     CABS_LAUNCH_CHECK("sketch gathers");
     CABS_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
@@ -339,12 +341,12 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
                       stream, true);
   }
   launch_validate_idx2(Ir, p.m, Ic, p.n, k, ws, st);
-  launch_gather_cols(src->a, src->lda, m_loc, Ic, k, Cb, L.Kp, ws, st);
-  if (multi(comm)) CABS_CUDA_TRY(cudaMemsetAsync(Rb, 0, sizeof(float) * L.ldrb * k, st));
+  launch_gather_cols(src->a, src->lda, m_loc, p.n, Ic, k, Cb, L.Kp, ws, st);
+  if (multi(comm)) launch_fill_neg_zero(Rb, L.ldrb * (int64_t)k, st);
   launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, Ir, k, p.n, Rb, L.ldrb, ws, st);
   CABS_LAUNCH_CHECK("sketch gathers");
   CABS_TRY(comm_f32(comm, Rb, L.ldrb * (int64_t)k, stream));
-  launch_gather_w(Rb, L.ldrb, Ic, k, Wb, L.Kp, st);
+  launch_gather_w(Rb, L.ldrb, p.n, Ic, k, Wb, L.Kp, st);
   CABS_LAUNCH_CHECK("gather_w");
   return embed_core(p, L, k, Cb, L.Kp, Rb, L.ldrb, Wb, L.Kp, mode, tol, U, ldu, V, ldv, s, r, sigma, 1, ws, comm,
                     stream);
@@ -417,32 +419,48 @@ static bool km_persistent_allowed(const cabs_comm* comm) {
   return !(path && strcmp(path, "loop") == 0) && !multi(comm);
 }
 
-// per-iteration kernels (multi-rank, or when the persistent kernel does not apply)
-static int32_t km_loop(const cabs_km_problem& p, int32_t iters, const KmSlot& k, void* ws, const Ws& L,
-                       const cabs_comm* comm, void* stream) {
+// per-iteration kernels (multi-rank, or when the persistent kernel does not apply) for np <= 2
+// problems: each iteration reduces every problem's sums into its part of ONE payload, so a
+// pair costs one collective per iteration, not two
+static int32_t km_loop(const cabs_km_problem* const* pp, const KmSlot* const* kk, int np, int32_t iters, void* ws,
+                       const Ws& L, const cabs_comm* comm, void* stream) {
   cudaStream_t st = S(stream);
-  const int k2 = p.k2, d = p.d;
-  double* red = wsp<double>(ws, L.km_red);
-  const int64_t payload = (int64_t)k2 * d + k2 + 2;
-  long long* fsum = static_cast<long long*>(k.scr);  // exact int64 sums (km_fixed.cuh), re-zeroed by km_reduce
-  long long* fwt = fsum + (int64_t)k2 * d;
-  CABS_CUDA_TRY(cudaMemsetAsync(fsum, 0, sizeof(long long) * ((int64_t)k2 * d + k2), st));
+  double* red[2];
+  int64_t payload[2], total = 0;
+  for (int q = 0; q < np; ++q) {
+    const cabs_km_problem& p = *pp[q];
+    red[q] = wsp<double>(ws, L.km_red) + total;
+    payload[q] = (int64_t)p.k2 * p.d + p.k2 + 2;
+    total += payload[q];
+    long long* fsum = static_cast<long long*>(kk[q]->scr);  // exact int64 sums (km_fixed.cuh), re-zeroed by km_reduce
+    CABS_CUDA_TRY(cudaMemsetAsync(fsum, 0, sizeof(long long) * ((int64_t)p.k2 * p.d + p.k2), st));
+  }
   for (int t = 0; t < iters; ++t) {
-    int ga = 1;
-    if (p.n_loc > 0) {
-      launch_km_assign(p.X, p.ldx, p.n_loc, d, p.centres, p.ldc, k2, k.w, p.labels, wsp<double>(ws, L.km_pobj),
-                       wsp<int>(ws, L.km_ptie), &ga, st, p.tie_log, p.tie_log_cap, t, p.row_off);
-      launch_km_accum(p.X, p.ldx, p.n_loc, d, p.labels, k.w, k.bounds, fsum, fwt, st);
-      CABS_LAUNCH_CHECK("km_assign/accum");
-      launch_km_reduce(fsum, fwt, k.bounds, p.n_loc, k2, d, wsp<double>(ws, L.km_pobj), wsp<int>(ws, L.km_ptie), ga,
-                       red, st);
-    } else {
-      CABS_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(double) * payload, st));
+    for (int q = 0; q < np; ++q) {
+      const cabs_km_problem& p = *pp[q];
+      const KmSlot& k = *kk[q];
+      const int k2 = p.k2, d = p.d;
+      long long* fsum = static_cast<long long*>(k.scr);
+      long long* fwt = fsum + (int64_t)k2 * d;
+      int ga = 1;
+      if (p.n_loc > 0) {
+        launch_km_assign(p.X, p.ldx, p.n_loc, d, p.centres, p.ldc, k2, k.w, p.labels, wsp<double>(ws, L.km_pobj),
+                         wsp<int>(ws, L.km_ptie), &ga, st, p.tie_log, p.tie_log_cap, t, p.row_off);
+        launch_km_accum(p.X, p.ldx, p.n_loc, d, p.labels, k.w, k.bounds, fsum, fwt, st);
+        CABS_LAUNCH_CHECK("km_assign/accum");
+        launch_km_reduce(fsum, fwt, k.bounds, p.n_loc, k2, d, wsp<double>(ws, L.km_pobj), wsp<int>(ws, L.km_ptie),
+                         ga, red[q], st);
+      } else {
+        CABS_CUDA_TRY(cudaMemsetAsync(red[q], 0, sizeof(double) * payload[q], st));
+      }
+      CABS_LAUNCH_CHECK("km_reduce");
     }
-    CABS_LAUNCH_CHECK("km_reduce");
-    CABS_TRY(comm_f64(comm, red, payload, stream));  // ONE fused message per iteration
-    launch_km_finalize(red, k2, d, p.centres, p.ldc, p.objective, p.near_ties, p.cluster_w, t, st);
-    CABS_LAUNCH_CHECK("km_finalize");
+    CABS_TRY(comm_f64(comm, red[0], total, stream));  // ONE fused message per iteration
+    for (int q = 0; q < np; ++q) {
+      const cabs_km_problem& p = *pp[q];
+      launch_km_finalize(red[q], p.k2, p.d, p.centres, p.ldc, p.objective, p.near_ties, p.cluster_w, t, st);
+      CABS_LAUNCH_CHECK("km_finalize");
+    }
   }
   return CABS_OK;
 }
@@ -477,7 +495,9 @@ int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
     }
   }
   cudaGetLastError();  // a refused cooperative launch is not an error: use the per-iteration kernels
-  return km_loop(p, iters, k, ws, L, comm, stream);
+  const cabs_km_problem* pp = &p;
+  const KmSlot* kp = &k;
+  return km_loop(&pp, &kp, 1, iters, ws, L, comm, stream);
 }
 
 int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const cabs_km_problem* b, int32_t iters,
@@ -539,9 +559,10 @@ int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const 
     }
   }
   cudaGetLastError();
-  // one problem at a time (each may still take the single-problem persistent kernel)
   const cabs_km_problem* pp[2] = {a, b};
   const KmSlot* kk[2] = {&ka, &kb};
+  if (multi(comm)) return km_loop(pp, kk, 2, iters, ws, L, comm, stream);  // one fused payload per iteration
+  // one problem at a time (each may still take the single-problem persistent kernel)
   for (int q = 0; q < 2; ++q) {
     bool done = false;
     if (km_persistent_allowed(comm) && pp[q]->n_loc > 0) {
@@ -550,7 +571,7 @@ int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const 
       if (done) CABS_LAUNCH_CHECK("lloyd_persistent");
     }
     cudaGetLastError();
-    if (!done) CABS_TRY(km_loop(*pp[q], iters, *kk[q], ws, L, comm, stream));
+    if (!done) CABS_TRY(km_loop(&pp[q], &kk[q], 1, iters, ws, L, comm, stream));
   }
   return CABS_OK;
 }
@@ -564,6 +585,15 @@ static int32_t sel_check(const cabs_plan* plan, const Ws& L, const cabs_sel_prob
 }
 
 // snap of one problem with the scratch of slot q
+struct SnapComm {
+  const cabs_comm* comm;
+  void* stream;
+};
+static int snap_allreduce(double* buf, int64_t n, void* ctx) {
+  const SnapComm* c = static_cast<const SnapComm*>(ctx);
+  return comm_f64(c->comm, buf, n, c->stream) == CABS_OK ? 0 : -1;
+}
+
 static int32_t sel_run(const cabs_sel_problem& p, int q, void* ws, const Ws& L, const cabs_comm* comm, void* stream) {
   cudaStream_t st = S(stream);
   float* D = wsp<float>(ws, q ? L.dist2 : L.dist);
@@ -572,22 +602,48 @@ static int32_t sel_run(const cabs_sel_problem& p, int q, void* ws, const Ws& L, 
   double* all = wsp<double>(ws, q ? L.cand_all2 : L.cand_all);
   const bool mr = multi(comm);
   const int T = mr ? kSnapTMulti : kSnapT;
+  const int nr = mr ? comm->nranks : 1, rank = mr ? comm->rank : 0;
   launch_km_distmat(p.X, p.ldx, p.n_loc, p.d, p.centres, p.ldc, p.k2, D, L.Nmax, st);
   // per-centre top-T over S point segments in parallel; lists packed as doubles so that
-  // other ranks' slots (zeros here) are completed by ONE sum-allreduce, then merged
-  int Sg = static_cast<int>(ceil_div(p.n_loc > 0 ? p.n_loc : 1, 4096));
-  if (Sg > kSnapSeg) Sg = kSnapSeg;
-  const int nr = mr ? comm->nranks : 1;
+  // other ranks' slots (zeros here) are completed by ONE sum-allreduce, then merged.  Multi-rank:
+  // S = kSnapSeg on every rank (slot offsets must agree), and a rank without points still
+  // writes its (FLT_MAX, -1) sentinels (topT of an empty range)
+  int Sg = kSnapSeg;
+  if (!mr) {
+    Sg = static_cast<int>(ceil_div(p.n_loc > 0 ? p.n_loc : 1, 4096));
+    if (Sg > kSnapSeg) Sg = kSnapSeg;
+  }
   const int64_t nall = 2LL * nr * Sg * p.k2 * T;
   if (mr) CABS_CUDA_TRY(cudaMemsetAsync(all, 0, sizeof(double) * nall, st));
-  if (p.n_loc > 0) launch_snap_topT(D, L.Nmax, p.n_loc, p.k2, p.row_off, T, Sg, (mr ? comm->rank : 0) * Sg, all, st);
+  if (p.n_loc > 0 || mr) launch_snap_topT(D, L.Nmax, p.n_loc, p.k2, p.row_off, T, Sg, rank * Sg, all, st);
   CABS_LAUNCH_CHECK("snap distmat/topT");
   CABS_TRY(comm_f64(comm, all, nall, stream));
   launch_snap_merge(all, p.k2, T, nr * Sg, cd, ci, st);
   CABS_LAUNCH_CHECK("snap_merge");
+  int* unres = wsp<int>(ws, L.scal) + SCAL_UNRES + q;
+  if (mr) CABS_CUDA_TRY(cudaMemsetAsync(unres, 0, sizeof(int), st));
   launch_snap_dedupe(cd, ci, p.k2, T, p.cluster_w, D, L.Nmax, p.n_loc, p.row_off, !mr, p.rep_of_centre, p.gap,
-                     p.reps, ws, st);
+                     p.reps, ws, st, mr ? unres : nullptr);
   CABS_LAUNCH_CHECK("snap_dedupe");
+  // multi-rank: a centre whose best or runner-up the exchanged lists did not resolve (every rank
+  // sees the same merged lists, so all ranks agree) -> the exact pass over the ranks' rows of D
+  bool redo = getenv("CABS_SNAP_FORCE_DIST") != nullptr;
+  if (mr && !redo) {
+    int h = 0;
+    CABS_CUDA_TRY(cudaMemcpyAsync(&h, unres, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CABS_CUDA_TRY(cudaStreamSynchronize(st));
+    redo = h != 0;
+  }
+  if (redo) {
+    // scratch: the candidate array (>= 4096 K bytes, > snap_dist_bytes for any k2 <= K)
+    if (sizeof(double) * 2 * nr * kSnapSeg * L.K * kSnapTMulti < snap_dist_bytes(p.k2, nr))
+      return arg_error("select: snap scratch too small");
+    SnapComm sc{comm, stream};
+    const int rc = snap_dist_run(D, L.Nmax, p.n_loc, p.row_off, p.k2, p.cluster_w, rank, nr, all, p.rep_of_centre,
+                                 p.gap, p.reps, ws, st, snap_allreduce, &sc);
+    if (rc == -2) return CABS_ERR_COMM;
+    CABS_LAUNCH_CHECK("snap_dist");
+  }
   return CABS_OK;
 }
 
@@ -810,7 +866,7 @@ int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float
   Ws L;
   CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
   const cabs_plan& p = *plan;
-  if (!src || !src->a || src->lda < p.n || !F || !G || !out || ncomp < 0 || ldf < ncomp || ldg < ncomp)
+  if (!src || (p.row_end > p.row_begin && !src->a) || src->lda < p.n || !F || !G || !out || ncomp < 0 || ldf < ncomp || ldg < ncomp)
     return arg_error("residual: bad arguments");
   const int64_t m_loc = p.row_end - p.row_begin;
   if (residual_tc_supported(src->a, src->lda, m_loc, p.n, ncomp)) {

@@ -81,7 +81,7 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.km_scr = take(2 * w.km_scr_bytes);
   w.km_pobj = take(sizeof(double) * kAssignGrid);
   w.km_ptie = take(sizeof(int) * kAssignGrid);
-  w.km_red = take(sizeof(double) * (K * Kp + K + 2));
+  w.km_red = take(sizeof(double) * 2 * (K * Kp + K + 2));  // two problems' payloads (fused pair)
   w.km_cnt = take(sizeof(int) * 64);
   w.dist = take(sizeof(float) * K * w.Nmax);
   w.cand_d = take(sizeof(float) * K * kSnapTMulti);
@@ -113,7 +113,8 @@ inline T* wsp(void* ws, size_t off) {
 }
 
 // scalar slots inside ws.scal (ints)
-enum ScalSlot : int { SCAL_R_PILOT = 0, SCAL_R_TMP = 1, SCAL_NRANKS = 2, SCAL_EXHAUST = 3, SCAL_EBAR = 4 /* [2] */ };
+enum ScalSlot : int { SCAL_R_PILOT = 0, SCAL_R_TMP = 1, SCAL_NRANKS = 2, SCAL_EXHAUST = 3, SCAL_EBAR = 4 /* [2] */,
+                       SCAL_UNRES = 8 /* [2]: a multi-rank snap left a centre unresolved */ };
 
 __device__ inline void set_status(void* ws, uint32_t bit) {
   atomicOr(reinterpret_cast<unsigned int*>(ws), bit);

@@ -14,11 +14,12 @@ void launch_philox_blocks(uint64_t seed, uint32_t tag, uint64_t start, int64_t c
 void launch_validate_idx(const int64_t* idx, int32_t k, int64_t N, void* ws, cudaStream_t st);
 void launch_validate_idx2(const int64_t* idx0, int64_t N0, const int64_t* idx1, int64_t N1, int32_t k, void* ws,
                           cudaStream_t st);
+void launch_fill_neg_zero(float* p, int64_t n, cudaStream_t st);
 void launch_gather_rows(const float* A, int64_t lda, int64_t row_begin, int64_t row_end, const int64_t* I, int32_t k,
                         int64_t n, float* R, int64_t ldr, void* ws, cudaStream_t st);
-void launch_gather_cols(const float* A, int64_t lda, int64_t m_loc, const int64_t* J, int32_t k, float* C, int64_t ldc,
+void launch_gather_cols(const float* A, int64_t lda, int64_t m_loc, int64_t n, const int64_t* J, int32_t k, float* C, int64_t ldc,
                         void* ws, cudaStream_t st);
-void launch_gather_w(const float* R, int64_t ldr, const int64_t* J, int32_t k, float* W, int64_t ldw, cudaStream_t st);
+void launch_gather_w(const float* R, int64_t ldr, int64_t n, const int64_t* J, int32_t k, float* W, int64_t ldw, cudaStream_t st);
 void launch_gather_w_direct(const float* A, int64_t lda, int64_t row_begin, int64_t m_loc, int64_t n,
                             const int64_t* I, const int64_t* J, int32_t k, float* W, int64_t ldw, cudaStream_t st);
 
@@ -113,7 +114,14 @@ void launch_snap_topT(const float* D, int64_t ldd, int64_t N, int k2, int64_t ro
 void launch_snap_merge(const double* all, int k2, int T, int nlists, float* cand_d, int64_t* cand_i, cudaStream_t st);
 void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int T, const double* cluster_w,
                         const float* D, int64_t ldd, int64_t N, int64_t row_off, bool can_rescan,
-                        int64_t* rep_of_centre, float* gap, int64_t* reps_sorted, void* ws, cudaStream_t st);
+                        int64_t* rep_of_centre, float* gap, int64_t* reps_sorted, void* ws, cudaStream_t st,
+                        int* unresolved = nullptr);
+// multi-rank exact greedy pass (select.cu): scratch of snap_dist_bytes at buf; allreduce(buf, n, ctx)
+// sums n doubles over the ranks on st
+size_t snap_dist_bytes(int k2, int nranks);
+int snap_dist_run(const float* D, int64_t ldd, int64_t N, int64_t row_off, int k2, const double* cluster_w,
+                  int rank, int nranks, void* buf, int64_t* rep_of_centre, float* gap, int64_t* reps_sorted,
+                  void* ws, cudaStream_t st, int (*allreduce)(double*, int64_t, void*), void* ctx);
 
 // hard.cu -- one side (rows or columns) of the hard-threshold selection; up to two per launch
 struct HardSide {

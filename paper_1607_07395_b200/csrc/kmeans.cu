@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(256) km_weights_const_kernel(KmWeightJob j0, K
 }
 
 void launch_km_weights2(const KmWeightJob& j0, const KmWeightJob* j1, int kind, float p, cudaStream_t st) {
-  int64_t N = j0.N > (j1 ? j1->N : 0) ? j0.N : j1->N;
+  const int64_t N1 = j1 ? j1->N : 0;
+  const int64_t N = j0.N > N1 ? j0.N : N1;
   if (N <= 0) return;
   if (kind == CABS_WEIGHT_CONST) {
     int64_t blocks = ceil_div(N * 16, 256);
@@ -145,12 +146,14 @@ __global__ void km_init_kernel(KmInitJob j0, KmInitJob j1) {
     int64_t g = jb.idx[j] - jb.row_off;
     if (g >= 0 && g < jb.n_loc) src = jb.X + g * jb.ldx;
   }
+  // a centre another rank owns starts as -0.0 (bit-exact sum-allreduce, see fill_neg_zero_kernel)
   for (int i = threadIdx.x; i < jb.ldc; i += blockDim.x)
-    jb.centres[(int64_t)j * jb.ldc + i] = (src && i < jb.d) ? src[i] : 0.f;
+    jb.centres[(int64_t)j * jb.ldc + i] = (src && i < jb.d) ? src[i] : (i < jb.d ? -0.f : 0.f);
 }
 
 void launch_km_init2(const KmInitJob& j0, const KmInitJob* j1, cudaStream_t st) {
-  const int kx = j0.k2 > (j1 ? j1->k2 : 0) ? j0.k2 : j1->k2;
+  const int k1 = j1 ? j1->k2 : 0;
+  const int kx = j0.k2 > k1 ? j0.k2 : k1;
   note_launch();
   km_init_kernel<<<dim3(kx, j1 ? 2 : 1), 128, 0, st>>>(j0, j1 ? *j1 : j0);
 }

@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
                                                           int64_t row_off, bool can_rescan,
                                                           int64_t* __restrict__ rep_of_centre, float* __restrict__ gap,
                                                           int64_t* __restrict__ reps_sorted, void* ws,
-                                                          bool staged, bool use_bitmap) {
+                                                          bool staged, bool use_bitmap, int* unresolved) {
   __shared__ int64_t tab[kTakenCap];
   __shared__ int order[CABS_KMAX];
   __shared__ int64_t reps[CABS_KMAX];
@@ -372,6 +372,9 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
             if (lane == 0) s_rescan = order[o];
             break;
           }
+          // multi-rank: D holds only this rank's points, no rescan here; the caller redoes the
+          // pass with snap_dist_* (exact) when this flag is raised
+          if (t2 < 0 && unresolved && lane == 0) *unresolved = 1;
           if (lane == 0) {
             const int j = order[o];
             float d1 = t1 >= 0 ? dist_at(o, t1) : FLT_MAX;
@@ -469,7 +472,8 @@ void snap_debug_counters(long long* out) {
 
 void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int T, const double* cluster_w,
                         const float* D, int64_t ldd, int64_t N, int64_t row_off, bool can_rescan,
-                        int64_t* rep_of_centre, float* gap, int64_t* reps_sorted, void* ws, cudaStream_t st) {
+                        int64_t* rep_of_centre, float* gap, int64_t* reps_sorted, void* ws, cudaStream_t st,
+                        int* unresolved) {
   constexpr size_t kCap = 160 * 1024;
   static bool attr = false;
   if (!attr) {
@@ -484,7 +488,184 @@ void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int 
   const size_t bytes = cand + (bitmap ? bits : 0);
   note_launch();
   snap_dedupe_kernel<<<1, 256, bytes, st>>>(cand_d, cand_i, k2, T, cluster_w, D, ldd, N, row_off, can_rescan,
-                                            rep_of_centre, gap, reps_sorted, ws, staged, bitmap);
+                                            rep_of_centre, gap, reps_sorted, ws, staged, bitmap, unresolved);
+}
+
+// ---------------------------------------------------------------- multi-rank exact greedy pass
+// When the exchanged lists leave some centre's best or runner-up unresolved (T-1 or more of its
+// T nearest points already taken), the greedy pass of readings Z13/Z14 is redone centre by
+// centre over the whole distance matrix: every rank scans ITS rows of D[j, :] for its two
+// nearest untaken points (snap_dist_scan + snap_dist_local), the ranks' pairs meet in one
+// sum-allreduce of 4 doubles per rank (zeros elsewhere), and every rank takes the same winner
+// (snap_dist_take).  k2 small collectives: slow, exact, and only taken when needed.
+struct SnapDist {
+  int* order;       // [k2] visiting order (-omega_j, j)
+  int* count;       // [1] number of taken points
+  int64_t* taken;   // [k2] taken global indices, ascending
+  int64_t* reps;    // [k2] per centre
+  float* d1;        // [k2]
+  float* d2;        // [k2]
+  double* slots;    // [4 nranks] (d1, i1, d2, i2) per rank, empty: (FLT_MAX, -1)
+  float* bd;        // [2 G] per-block top two
+  int64_t* bi;
+};
+constexpr int kSnapDistG = 64;  // scan blocks
+
+size_t snap_dist_bytes(int k2, int nranks) {
+  return (size_t)k2 * (4 + 8 + 8 + 4 + 4) + 64 + sizeof(double) * 4 * nranks + (size_t)2 * kSnapDistG * 12 + 256;
+}
+
+static SnapDist snap_dist_carve(void* buf, int k2, int nranks) {
+  char* b = static_cast<char*>(buf);
+  SnapDist s;
+  s.slots = reinterpret_cast<double*>(b);  b += sizeof(double) * 4 * nranks;
+  s.taken = reinterpret_cast<int64_t*>(b); b += sizeof(int64_t) * k2;
+  s.reps = reinterpret_cast<int64_t*>(b);  b += sizeof(int64_t) * k2;
+  s.bi = reinterpret_cast<int64_t*>(b);    b += sizeof(int64_t) * 2 * kSnapDistG;
+  s.bd = reinterpret_cast<float*>(b);      b += sizeof(float) * 2 * kSnapDistG;
+  s.d1 = reinterpret_cast<float*>(b);      b += sizeof(float) * k2;
+  s.d2 = reinterpret_cast<float*>(b);      b += sizeof(float) * k2;
+  s.order = reinterpret_cast<int*>(b);     b += sizeof(int) * k2;
+  s.count = reinterpret_cast<int*>(b);
+  return s;
+}
+
+__global__ void __launch_bounds__(256) snap_dist_init_kernel(const double* __restrict__ cluster_w, int k2, SnapDist s) {
+  for (int j = threadIdx.x; j < k2; j += blockDim.x) {
+    const double wj = cluster_w[j];
+    int rk = 0;
+    for (int q = 0; q < k2; ++q) {
+      const double wq = cluster_w[q];
+      rk += (wq > wj) || (wq == wj && q < j);
+    }
+    s.order[rk] = j;
+  }
+  if (threadIdx.x == 0) *s.count = 0;
+}
+
+// the (best, runner-up) pair update in lexicographic (d, idx) order
+__device__ __forceinline__ void top2_push(float v, int64_t i, float& b1, int64_t& i1, float& b2, int64_t& i2) {
+  if (lex_less(v, i, b1, i1)) { b2 = b1; i2 = i1; b1 = v; i1 = i; }
+  else if (lex_less(v, i, b2, i2)) { b2 = v; i2 = i; }
+}
+
+__device__ void block_top2(float& b1, int64_t& i1, float& b2, int64_t& i2) {  // result valid in thread 0
+  __shared__ float sd[16];
+  __shared__ int64_t si[16];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob1 = __shfl_xor_sync(0xffffffffu, b1, o), ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
+    const int64_t oi1 = __shfl_xor_sync(0xffffffffu, i1, o), oi2 = __shfl_xor_sync(0xffffffffu, i2, o);
+    top2_push(ob1, oi1, b1, i1, b2, i2);
+    top2_push(ob2, oi2, b1, i1, b2, i2);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { sd[2 * w] = b1; si[2 * w] = i1; sd[2 * w + 1] = b2; si[2 * w + 1] = i2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int e = 2; e < 2 * static_cast<int>(blockDim.x >> 5); ++e) top2_push(sd[e], si[e], b1, i1, b2, i2);
+  }
+}
+
+__global__ void __launch_bounds__(256) snap_dist_scan_kernel(const float* __restrict__ D, int64_t ldd, int64_t N,
+                                                             int64_t row_off, int o, SnapDist s) {
+  __shared__ int64_t tk[CABS_KMAX];
+  const int cnt = *s.count;
+  for (int e = threadIdx.x; e < cnt; e += blockDim.x) tk[e] = s.taken[e];
+  __syncthreads();
+  const float* row = D + (int64_t)s.order[o] * ldd;
+  float b1 = FLT_MAX, b2 = FLT_MAX;
+  int64_t i1 = INT64_MAX, i2 = INT64_MAX;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gi = row_off + p;
+    int lo = 0, hi = cnt;  // binary search of the sorted taken list
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (tk[mid] < gi) lo = mid + 1; else hi = mid;
+    }
+    if (lo < cnt && tk[lo] == gi) continue;
+    top2_push(row[p], gi, b1, i1, b2, i2);
+  }
+  block_top2(b1, i1, b2, i2);
+  if (threadIdx.x == 0) {
+    s.bd[2 * blockIdx.x] = b1; s.bi[2 * blockIdx.x] = i1;
+    s.bd[2 * blockIdx.x + 1] = b2; s.bi[2 * blockIdx.x + 1] = i2;
+  }
+}
+
+__global__ void __launch_bounds__(32) snap_dist_local_kernel(int G, int rank, int nranks, SnapDist s) {
+  if (threadIdx.x != 0) return;
+  float b1 = FLT_MAX, b2 = FLT_MAX;
+  int64_t i1 = INT64_MAX, i2 = INT64_MAX;
+  for (int e = 0; e < 2 * G; ++e) top2_push(s.bd[e], s.bi[e], b1, i1, b2, i2);
+  for (int r = 0; r < nranks; ++r) {
+    double* sl = s.slots + 4 * r;
+    if (r == rank) {
+      sl[0] = i1 == INT64_MAX ? static_cast<double>(FLT_MAX) : static_cast<double>(b1);
+      sl[1] = i1 == INT64_MAX ? -1.0 : static_cast<double>(i1);
+      sl[2] = i2 == INT64_MAX ? static_cast<double>(FLT_MAX) : static_cast<double>(b2);
+      sl[3] = i2 == INT64_MAX ? -1.0 : static_cast<double>(i2);
+    } else {
+      sl[0] = sl[1] = sl[2] = sl[3] = 0.0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32) snap_dist_take_kernel(int o, int nranks, SnapDist s, void* ws) {
+  if (threadIdx.x != 0) return;
+  float b1 = FLT_MAX, b2 = FLT_MAX;
+  int64_t i1 = INT64_MAX, i2 = INT64_MAX;
+  for (int e = 0; e < 2 * nranks; ++e) {
+    const int64_t i = static_cast<int64_t>(s.slots[2 * e + 1]);
+    if (i >= 0) top2_push(static_cast<float>(s.slots[2 * e]), i, b1, i1, b2, i2);
+  }
+  const int j = s.order[o];
+  if (i1 == INT64_MAX) { set_status(ws, CABS_DEV_SNAP_EXHAUSTED); i1 = 0; b1 = 0.f; }
+  s.reps[j] = i1;
+  s.d1[j] = b1;
+  s.d2[j] = i2 == INT64_MAX ? FLT_MAX : b2;
+  int c = *s.count;  // sorted insertion
+  while (c > 0 && s.taken[c - 1] > i1) { s.taken[c] = s.taken[c - 1]; --c; }
+  s.taken[c] = i1;
+  *s.count += 1;
+}
+
+__global__ void __launch_bounds__(256) snap_dist_finish_kernel(int k2, SnapDist s, int64_t* __restrict__ rep_of_centre,
+                                                               float* __restrict__ gap, int64_t* __restrict__ reps_sorted) {
+  for (int j = threadIdx.x; j < k2; j += blockDim.x) {  // the same outputs as snap_dedupe_kernel
+    const int64_t v = s.reps[j];
+    if (rep_of_centre) rep_of_centre[j] = v;
+    if (gap) {
+      const float d1 = s.d1[j], d2 = s.d2[j];
+      gap[j] = (d2 == FLT_MAX) ? FLT_MAX : (d2 > 0.f ? (d2 - d1) / d2 : 0.f);
+    }
+    int rk = 0;
+    for (int q = 0; q < k2; ++q) rk += s.reps[q] < v;
+    reps_sorted[rk] = v;
+  }
+}
+
+int snap_dist_run(const float* D, int64_t ldd, int64_t N, int64_t row_off, int k2, const double* cluster_w,
+                  int rank, int nranks, void* buf, int64_t* rep_of_centre, float* gap, int64_t* reps_sorted,
+                  void* ws, cudaStream_t st, int (*allreduce)(double*, int64_t, void*), void* ctx) {
+  const SnapDist s = snap_dist_carve(buf, k2, nranks);
+  int G = static_cast<int>(ceil_div(N > 0 ? N : 1, 1024));
+  if (G > kSnapDistG) G = kSnapDistG;
+  note_launch();
+  snap_dist_init_kernel<<<1, 256, 0, st>>>(cluster_w, k2, s);
+  for (int o = 0; o < k2; ++o) {
+    note_launch();
+    snap_dist_scan_kernel<<<G, 256, 0, st>>>(D, ldd, N, row_off, o, s);
+    note_launch();
+    snap_dist_local_kernel<<<1, 32, 0, st>>>(G, rank, nranks, s);
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    if (allreduce && allreduce(s.slots, 4LL * nranks, ctx) != 0) return -2;
+    note_launch();
+    snap_dist_take_kernel<<<1, 32, 0, st>>>(o, nranks, s, ws);
+  }
+  note_launch();
+  snap_dist_finish_kernel<<<1, 256, 0, st>>>(k2, s, rep_of_centre, gap, reps_sorted);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace cabsk

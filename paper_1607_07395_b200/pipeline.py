@@ -62,13 +62,14 @@ class CabsPipeline:
         z = lambda *s, dt=f32: torch.zeros(*s, dtype=dt, device=dev)  # noqa: E731
         self.ws = torch.zeros(C.cabs_workspace_bytes(p), dtype=torch.uint8, device=dev)
         self.I, self.J = z(k1, dt=i64), z(k1, dt=i64)
-        self.Cm = z(p.m_loc, l1)
+        ml, nl = max(p.m_loc, 1), max(p.n_sl, 1)  # a rank may own no rows / columns: keep pointers valid
+        self.Cm = z(ml, l1)
         self.R = z(k1, ldr)
         self.W = z(k1, l1)
-        self.P, self.Q = z(p.m_loc, l1), z(p.n_sl, l1)
+        self.P, self.Q = z(ml, l1), z(nl, l1)
         self.s1, self.r1, self.sigma1 = z(k1), z(1, dt=i32), z(k1, dt=f64)
         self.cen_r, self.cen_c = z(k2, l1), z(k2, l1)
-        self.lab_r, self.lab_c = z(max(p.m_loc, 1), dt=i32), z(max(p.n_sl, 1), dt=i32)
+        self.lab_r, self.lab_c = z(ml, dt=i32), z(nl, dt=i32)
         self.cw_r, self.cw_c = z(k2, dt=f64), z(k2, dt=f64)
         self.obj_r, self.obj_c = z(cfg.iters, dt=f64), z(cfg.iters, dt=f64)
         self.tie_r, self.tie_c = z(cfg.iters, dt=i32), z(cfg.iters, dt=i32)
@@ -77,7 +78,7 @@ class CabsPipeline:
         self.Ib, self.Jb = z(k2, dt=i64), z(k2, dt=i64)
         self.rep_r, self.rep_c = z(k2, dt=i64), z(k2, dt=i64)
         self.gap_r, self.gap_c = z(k2), z(k2)
-        self.U, self.V = z(p.m_loc, l2), z(p.n_sl, l2)
+        self.U, self.V = z(ml, l2), z(nl, l2)
         self.s2, self.r2, self.sigma2 = z(k2), z(1, dt=i32), z(k2, dt=f64)
         self.G = self.V if p.nranks == 1 else z(n, l2)
         self.out = z(2, dt=f64)

@@ -159,40 +159,7 @@ def test_pair_equals_two_singles(dev):
     assert np.array_equal(kb.cpu().numpy(), O.row_sq_norms(Xb[:, :d].cpu().numpy()))
 
 
-class _HostRendezvousComm:
-    """Two ranks in two host threads of one process, each on its own stream: the allreduce
-    callback synchronises its stream, meets the other rank at a host barrier and sums the two
-    buffers on the host (the kernels never wait on each other; only the host logic of the
-    multi-rank path -- slots, padding, the merge over candidates -- is exercised)."""
-
-    def __init__(self, nranks, device):
-        import threading
-        from paper_1607_07395_b200.cabs import ALLREDUCE_FN, Comm
-        from paper_1607_07395_b200.dist import tensor_from_ptr
-        self.bar = threading.Barrier(nranks)
-        self.bufs = [None] * nranks
-        self.comms, self._fns = [], []
-        for r in range(nranks):
-            def f(ptr, count, ctx, stream, r=r):
-                try:
-                    torch.cuda.ExternalStream(int(stream), device=device).synchronize() if stream else \
-                        torch.cuda.synchronize()
-                    t = tensor_from_ptr(ptr, count, torch.float64, device)
-                    self.bufs[r] = t.cpu()
-                    self.bar.wait()
-                    tot = sum(self.bufs)
-                    self.bar.wait()
-                    t.copy_(tot.to(device))
-                    torch.cuda.synchronize()
-                    return 0
-                except Exception as e:  # noqa: BLE001 -- never cross the C ABI
-                    print("rendezvous comm failed:", repr(e))
-                    return 1
-            fn = ALLREDUCE_FN(f)
-            self._fns.append(fn)
-            c = type("C", (), {})()
-            c.c = Comm(r, nranks, fn, fn, None)
-            self.comms.append(c)
+from tests.rendezvous import HostRendezvousComm as _HostRendezvousComm  # noqa: E402
 
 
 @pytest.mark.parametrize("m,k2", [(5000, 50), (30, 20), (2049, 1)])
@@ -215,6 +182,7 @@ def test_multi_rank_merge_matches_single(dev, m, k2):
             Xl[:plan.m_loc, :d] = torch.from_numpy(X[plan.row_begin:plan.row_end]).to(dev)
             reps = torch.zeros(k2, dtype=torch.int64, device=dev)
             st = torch.cuda.Stream(device=dev)
+            st.wait_stream(torch.cuda.current_stream(dev))  # inputs were written on the thread's default stream
             with torch.cuda.stream(st):
                 C.cabs_hard_select(plan, Xl, plan.m_loc, m, plan.row_begin, d, k2, reps, ws, comm=rc.comms[r],
                                    stream=st)

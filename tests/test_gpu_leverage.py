@@ -182,6 +182,7 @@ def test_orthogonalize_two_ranks_match_one(dev):
             Uo, Vo = torch.zeros((max(p.m_loc, 1), ld), device=dev), torch.zeros((max(p.n_sl, 1), ld), device=dev)
             so = torch.zeros(r, device=dev)
             st = torch.cuda.Stream(device=dev)
+            st.wait_stream(torch.cuda.current_stream(dev))  # inputs were written on the thread's default stream
             with torch.cuda.stream(st):
                 C.cabs_orthogonalize(p, r, Ul, s, Vl, Uo, so, Vo, ws, comm=rc.comms[k], stream=st)
             st.synchronize()
