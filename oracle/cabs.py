@@ -13,7 +13,7 @@ reference leg may import this module.  It shares no code with the CUDA path.
 Parity status per function:
   gather, svd_w, sketch, embeddings, argmin_with_gap, lloyd, snap, residual, cabs_run,
   row_sq_norms, hard_threshold_select, hard_threshold_followup, orthogonalize,
-  leverage_scores, leverage_sample: pinned (tests/test_oracle_*.py).
+  leverage_scores, leverage_sample, RbfSource, residual_sampled: pinned (tests/test_oracle_*.py).
 """
 from __future__ import annotations
 
@@ -46,14 +46,54 @@ def check_indices(idx, N, what="index"):
     return idx
 
 
+class RbfSource:
+    """The implicit c5 matrix (BASELINE.json configs[4]): A_ij = exp(-||x_i - y_j||^2 / (2 sigma^2)),
+    entries generated on access ("never knowing the remaining entries").
+    x (m x d), y (n x d) are the FP32 points; sigma is given (an input of the workload)."""
+
+    def __init__(self, x, y, sigma):
+        self.x = np.asarray(x, np.float64)
+        self.y = np.asarray(y, np.float64)
+        self.sigma = float(sigma)
+        self.shape = (self.x.shape[0], self.y.shape[0])
+
+    def entries(self, I, J):
+        """A[I][:, J] as float64: the definition, ||x_i - y_j||^2 summed over the d coordinates."""
+        X = self.x[np.asarray(I, np.int64)]
+        Y = self.y[np.asarray(J, np.int64)]
+        d2 = np.zeros((X.shape[0], Y.shape[0]))
+        for l in range(X.shape[1]):
+            diff = X[:, l][:, None] - Y[:, l][None, :]
+            d2 += diff * diff
+        return np.exp(-d2 / (2.0 * self.sigma ** 2))
+
+    def at(self, i, j):
+        """A_{i_t j_t} for position arrays i, j (elementwise)."""
+        X = self.x[np.asarray(i, np.int64)]
+        Y = self.y[np.asarray(j, np.int64)]
+        d2 = np.zeros(X.shape[0])
+        for l in range(X.shape[1]):  # the same coordinate order as entries()
+            diff = X[:, l] - Y[:, l]
+            d2 += diff * diff
+        return np.exp(-d2 / (2.0 * self.sigma ** 2))
+
+
+def _block(A, I, J):
+    """A[I][:, J] as float64 for a dense array or an implicit source."""
+    if isinstance(A, RbfSource):
+        return A.entries(I, J)
+    return np.asarray(A[np.ix_(I, J)], dtype=np.float64)
+
+
 def gather(A, I, J):
-    """P:195 "C = A_[:,I^c], R = A_[I^r,:], W = A_[I^r,I^c]".  Exact copies, as float64."""
+    """P:195 "C = A_[:,I^c], R = A_[I^r,:], W = A_[I^r,I^c]".  Exact copies, as float64.
+    A: dense array, or an implicit source whose entries are generated on access."""
     m, n = A.shape
     I = check_indices(I, m, "row index")
     J = check_indices(J, n, "column index")
-    C = np.asarray(A[:, J], dtype=np.float64)
-    R = np.asarray(A[I, :], dtype=np.float64)
-    W = np.asarray(A[np.ix_(I, J)], dtype=np.float64)
+    C = _block(A, np.arange(m), J)
+    R = _block(A, I, np.arange(n))
+    W = _block(A, I, J)
     return C, R, W
 
 
@@ -398,12 +438,38 @@ def residual(A, F, G, s=None, block=2048):
         F = F * np.asarray(s, np.float64)[None, :]
     r2 = 0.0
     a2 = 0.0
+    n = A.shape[1]
     for i in range(0, A.shape[0], block):
-        Ab = np.asarray(A[i:i + block], np.float64)
+        Ab = _block(A, np.arange(i, min(i + block, A.shape[0])), np.arange(n))
         E = Ab - F[i:i + block] @ G.T
         r2 += float(np.sum(E * E))
         a2 += float(np.sum(Ab * Ab))
     return r2, a2
+
+
+def residual_sampled(A, F, G, i, j, s=None, chunk=1 << 20):
+    """The P:313 error on a uniform subset of entries (BASELINE.json configs[4] "residual
+    estimated on a seeded 1e9-entry uniform subset"; reading Z23: T i.i.d. positions (i_t, j_t)).
+    Unbiased estimates of sum (A - F diag(s) G^T)^2 and sum A^2:
+        r2 = (m n / T) sum_t (A_{i_t j_t} - F_{i_t} . G_{j_t})^2,   a2 = (m n / T) sum_t A_{i_t j_t}^2."""
+    m, n = A.shape
+    i = np.asarray(i, np.int64)
+    j = np.asarray(j, np.int64)
+    T = i.shape[0]
+    F = np.asarray(F, np.float64)
+    G = np.asarray(G, np.float64)
+    if s is not None:
+        F = F * np.asarray(s, np.float64)[None, :]
+    r2 = 0.0
+    a2 = 0.0
+    for c in range(0, T, chunk):
+        ic, jc = i[c:c + chunk], j[c:c + chunk]
+        a = A.at(ic, jc) if isinstance(A, RbfSource) else np.asarray(A[ic, jc], np.float64)
+        e = a - np.sum(F[ic] * G[jc], axis=1)
+        r2 += float(np.sum(e * e))
+        a2 += float(np.sum(a * a))
+    scale = float(m) * float(n) / float(T)
+    return scale * r2, scale * a2
 
 
 def relative_error(A, F, G, s=None):
@@ -436,9 +502,11 @@ class CabsResult:
 
 def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
              weight_kind=WEIGHT_CONST, weight_p=2.0, I=None, J=None,
-             init_rows=None, init_cols=None, with_residual=True, followup="kmeans"):
+             init_rows=None, init_cols=None, with_residual=True, followup="kmeans", n_samples=0):
     """Algorithm 2 plus the evaluation residual.  followup="hard" /
-    "leverage" replaces step 3 by the paper's variant (f) / (e) of P:312 (km_* / snap_* are None)."""
+    "leverage" replaces step 3 by the paper's variant (f) / (e) of P:312 (km_* / snap_* are None).
+    A: dense array or RbfSource.  n_samples > 0: the residual is the sampled estimate on the
+    pairs rng.residual_pairs(seed, n_samples, m, n)."""
     m, n = A.shape
     if not (1 <= k1 <= min(m, n)) or not (1 <= k2 <= min(m, n)):
         raise ValueError("need 1 <= k1, k2 <= min(m, n)")  # S:346
@@ -458,7 +526,7 @@ def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
         res = CabsResult(I=I, J=J, pilot=pilot, P=P, Q=Q, km_rows=None, km_cols=None,
                          snap_rows=None, snap_cols=None, Ibar=Ib, Jbar=Jb, follow=follow)
         if with_residual:
-            res.resid_sq, res.a_sq = residual(A, follow.U, follow.V, follow.s)
+            res.resid_sq, res.a_sq = _evaluate(A, follow, seed, n_samples)
         return res
     if followup == "leverage":  # P:312 (e): orthogonalize the pilot (Supp. 3), sample by leverage
         Uo, so, Vo = orthogonalize(pilot.U, pilot.s, pilot.V)
@@ -469,7 +537,7 @@ def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
         res = CabsResult(I=I, J=J, pilot=pilot, P=P, Q=Q, km_rows=None, km_cols=None,
                          snap_rows=None, snap_cols=None, Ibar=Ib, Jbar=Jb, follow=follow)
         if with_residual:
-            res.resid_sq, res.a_sq = residual(A, follow.U, follow.V, follow.s)
+            res.resid_sq, res.a_sq = _evaluate(A, follow, seed, n_samples)
         return res
     if followup != "kmeans":
         raise ValueError("followup must be 'kmeans', 'hard' or 'leverage'")
@@ -487,5 +555,13 @@ def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
     res = CabsResult(I=I, J=J, pilot=pilot, P=P, Q=Q, km_rows=km_r, km_cols=km_c,
                      snap_rows=sn_r, snap_cols=sn_c, Ibar=Ib, Jbar=Jb, follow=follow)
     if with_residual:
-        res.resid_sq, res.a_sq = residual(A, follow.U, follow.V, follow.s)
+        res.resid_sq, res.a_sq = _evaluate(A, follow, seed, n_samples)
     return res
+
+
+def _evaluate(A, follow, seed, n_samples):
+    if n_samples > 0:
+        m, n = A.shape
+        i, j = rng.residual_pairs(seed, n_samples, m, n)
+        return residual_sampled(A, follow.U, follow.V, i, j, follow.s)
+    return residual(A, follow.U, follow.V, follow.s)

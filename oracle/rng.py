@@ -149,3 +149,42 @@ def uniform01(seed: int, tag: int, idx) -> np.ndarray:
     a = (w0 >> np.uint64(5)).astype(np.float64)
     b = (w1 >> np.uint64(6)).astype(np.float64)
     return (a * 67108864.0 + b + 0.5) * 2.0 ** -53
+
+
+def _lemire_np(x, s):
+    """Vectorised Lemire step: (accepted mask, value) for uint64 arrays of 32-bit words x."""
+    s64 = np.uint64(s)
+    prod = x * s64  # x < 2^32, s <= 2^32: exact in uint64
+    lo = prod & np.uint64(M32)
+    thresh = np.uint64(((1 << 32) - s) % s)
+    return lo >= thresh, prod >> np.uint64(32)
+
+
+def residual_pairs(seed: int, T: int, m: int, n: int, t0: int = 0):
+    """T i.i.d. uniform entry positions (i, j) in [0, m) x [0, n) for the sampled residual
+    (SURVEY.md Z17 / Z23 "uniform subset" = pairs with replacement).
+
+    Pair t (t = t0 .. t0+T-1) reads Philox blocks of counter (t mod 2^32, t >> 32, 5, a) for
+    attempts a = 0, 1, ...: i = Lemire(word 0, m), on rejection Lemire(word 1, m), then the
+    next attempt's words 0, 1; j likewise from words 2, 3.  Returns int64 arrays (i, j)."""
+    if not (1 <= m <= (1 << 32)) or not (1 <= n <= (1 << 32)):
+        raise ValueError("bounds out of range")
+    t = np.arange(t0, t0 + T, dtype=np.uint64)
+    k0, k1 = seed_key(seed)
+    out = []
+    for s, (wa, wb) in ((m, (0, 1)), (n, (2, 3))):
+        val = np.zeros(T, dtype=np.uint64)
+        todo = np.arange(T)
+        a = 0
+        while todo.size:
+            tt = t[todo]
+            words = philox4x32_10_np(tt & np.uint64(M32), tt >> np.uint64(32), np.uint64(TAG_RESIDUAL_PAIRS),
+                                     np.uint64(a), k0, k1)
+            ok0, v0 = _lemire_np(words[wa], s)
+            ok1, v1 = _lemire_np(words[wb], s)
+            done = ok0 | ok1
+            val[todo[done]] = np.where(ok0, v0, v1)[done]
+            todo = todo[~done]
+            a += 1
+        out.append(val.astype(np.int64))
+    return out[0], out[1]

@@ -7,7 +7,7 @@
   profiles/traffic.json             {"<key>": {"dram_bytes_per_launch": ..., "source": ...}}
   profiles/<tag>_bench.json         the bench line of the same session
 
-usage: python tools/summarize_profiles.py <tag> [traffic-key]
+usage: python tools/summarize_profiles.py <tag> [traffic-key-prefix, e.g. c3]
 """
 import csv
 import io
@@ -39,7 +39,7 @@ def ncu_raw(rep):
 
 def main():
     tag = sys.argv[1]
-    key = sys.argv[2] if len(sys.argv) > 2 else "residual"
+    key = sys.argv[2] if len(sys.argv) > 2 else ""  # traffic.json key prefix, e.g. "c3"
     go = os.path.join(ROOT, "gpurun_out")
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
@@ -74,6 +74,26 @@ def main():
                 if k in h:
                     i = h.index(k)
                     lines.append(f"{k:80s} {v[i]} {u[i]}")
+            # pipe utilisation (% of peak over active cycles) of every pipe that did work
+            lines.append("# pipes (pct_of_peak_sustained_active)")
+            for i, k in enumerate(h):
+                if k.startswith("sm__pipe_") and k.endswith("cycles_active.avg.pct_of_peak_sustained_active"):
+                    try:
+                        if float(v[i]) >= 0.5:
+                            lines.append(f"{k:80s} {v[i]} {u[i]}")
+                    except ValueError:
+                        pass
+            # top stall reasons (warp-cycles per issued instruction)
+            st = []
+            for i, k in enumerate(h):
+                if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+                    try:
+                        st.append((float(v[i]), k))
+                    except ValueError:
+                        pass
+            lines.append("# top stall reasons (warps per issue-active cycle)")
+            for val, k in sorted(st, reverse=True)[:8]:
+                lines.append(f"{k:80s} {val}")
             with open(os.path.join(prof, f"{tag}_{name}_ncu.txt"), "w") as f:
                 f.write("\n".join(lines) + "\n")
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -81,7 +101,8 @@ def main():
             wr = float(v[h.index("dram__bytes_write.sum")]) * scale[u[h.index("dram__bytes_write.sum")]]
             tj = os.path.join(prof, "traffic.json")
             t = json.load(open(tj)) if os.path.exists(tj) else {}
-            k = "lloyd" if "lloyd" in name else ("residual" if "residual" in name else ("svd" if "svd" in name else key))
+            k = "lloyd" if "lloyd" in name else ("residual" if "residual" in name else ("svd" if "svd" in name else name))
+            k = f"{key}_{k}" if key else k
             t[k] = {"kernel": name, "dram_bytes_per_launch": rd + wr, "source": f"profiles/{tag}_{name}_ncu.txt"}
             json.dump(t, open(tj, "w"), indent=1)
             print(open(os.path.join(prof, f"{tag}_{name}_ncu.txt")).read())

@@ -34,7 +34,7 @@ class Config:
     note: str = ""
 
 
-# BASELINE.json configs[0..3] (configs[4], the implicit RBF source, is a later row).
+# BASELINE.json configs[0..4]; c5 is the implicit RBF source (make_rbf, never materialised).
 CONFIGS = {
     "c1": Config("c1", 2000, 1500, 20, 20, 10, "gauss_factor_decay",
                  note="A = G1 diag(1/i) G2^T + 0.01 N, rank 20 (BASELINE configs[0])"),
@@ -44,7 +44,14 @@ CONFIGS = {
                  note="A_ij = <mu_c(i), nu_d(j)> + 0.05 N_ij, 64 Zipf(1.1) clusters/side (configs[2])"),
     "c4": Config("c4", 400000, 100000, 200, 200, 25, "gauss_factor",
                  note="A = G1 G2^T + 0.1 N, rank 500 (configs[3])"),
+    "c5": Config("c5", 2000000, 1000000, 300, 300, 5, "rbf_mixture",
+                 note="A_ij = exp(-|x_i - y_j|^2 / 2 sigma^2), x, y in R^16 from a 100-component "
+                      "Gaussian mixture, sigma = median pairwise distance of 1e4 pairs (configs[4], Z23)"),
 }
+
+RBF_DIM = 16
+RBF_COMPONENTS = 100
+RBF_SIGMA_PAIRS = 10000
 
 
 def _gen(device, seed: int, tag: int, idx: int = 0) -> torch.Generator:
@@ -154,3 +161,28 @@ def col_partition(n: int, rank: int, nranks: int):
     per = int(math.ceil(n / nranks))
     c0 = min(n, rank * per)
     return c0, min(n, c0 + per)
+
+
+def make_rbf(cfg: Config):
+    """Inputs of the implicit RBF source (BASELINE.json configs[4]; reading Z23): x (m x 16) and
+    y (n x 16) float32 on the CPU, independent draws from one mixture of 100 unit-covariance
+    Gaussians with means 3 N(0, I_16) and equal weights; sigma = median (mean of the two middle
+    order statistics) of |x_a - y_b| over 1e4 seeded pairs, in float64 on the float32 points.
+    The matrix itself is never formed: both sides generate entries on access."""
+    assert cfg.kind == "rbf_mixture"
+    s = cfg.seed
+    mu = 3.0 * _randn((RBF_COMPONENTS, RBF_DIM), "cpu", s, 30)
+
+    def points(count, tag):
+        comp = torch.randint(0, RBF_COMPONENTS, (count,), generator=_gen("cpu", s, tag))
+        return (mu[comp] + _randn((count, RBF_DIM), "cpu", s, tag + 1)).to(torch.float32)
+
+    x = points(cfg.m, 31)
+    y = points(cfg.n, 33)
+    a = torch.randint(0, cfg.m, (RBF_SIGMA_PAIRS,), generator=_gen("cpu", s, 35))
+    b = torch.randint(0, cfg.n, (RBF_SIGMA_PAIRS,), generator=_gen("cpu", s, 36))
+    dist = torch.sqrt(((x[a].double() - y[b].double()) ** 2).sum(1))
+    ds = torch.sort(dist).values
+    h = RBF_SIGMA_PAIRS // 2
+    sigma = float(0.5 * (ds[h - 1] + ds[h]))
+    return x, y, sigma
