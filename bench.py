@@ -32,12 +32,14 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from workloads import CHUNK, CONFIGS, Generator  # noqa: E402
+from workloads import CHUNK, CONFIGS, Generator, make_rbf  # noqa: E402
 
 METRIC = "CABS sketch wall time & k-means pts/s at 1/2/4/8 GPU; HBM GB/s vs peak"
 UNIT = "rows+cols/s"
 BASE_CFG = {1: "c3"}  # BASELINE.json configs[2]: the largest single-GPU configuration
 CFG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
+C5_SAMPLES = 10 ** 9     # BASELINE.json configs[4]: "residual estimated on a seeded 1e9-entry uniform subset"
+ORACLE_RBF_SAMPLES = 1 << 20  # the oracle's bounded c5 sample: pairs of its leading block
 
 
 def load_peaks():
@@ -149,8 +151,19 @@ def allreduce_max(x, world):
 def oracle_sample(cfg):
     """The bounded sample of a config the oracle is timed on (10-30 s of host CPU per step):
     the leading ms x ns block of the same matrix, same k1, k2 and Lloyd iterations."""
-    ms, ns = {"c1": (2000, 1500), "c2": (8000, 4000), "c3": (6000, 3000), "c4": (6000, 3000)}[cfg.name]
+    ms, ns = {"c1": (2000, 1500), "c2": (8000, 4000), "c3": (6000, 3000), "c4": (6000, 3000),
+              "c5": (6000, 4000)}[cfg.name]
     return min(ms, cfg.m), min(ns, cfg.n)
+
+
+def oracle_source(cfg, ms, ns):
+    """The oracle's matrix for the bounded sample: the leading ms x ns block (dense), or the implicit
+    source on the first ms / ns points (c5), with the residual sample size the oracle runs."""
+    from oracle import cabs as O
+    if cfg.kind == "rbf_mixture":
+        x, y, sigma = make_rbf(cfg)
+        return O.RbfSource(x[:ms].numpy(), y[:ns].numpy(), sigma), ORACLE_RBF_SAMPLES
+    return Generator(cfg, device="cpu").rows(0, ms)[:, :ns].numpy().copy(), 0
 
 
 def run_reference(args, cfg):
@@ -162,20 +175,21 @@ def run_reference(args, cfg):
     from workloads import Generator
     cores = len(os.sched_getaffinity(0))
     ms, ns = oracle_sample(cfg)
-    A = Generator(cfg, device="cpu").rows(0, ms)[:, :ns].numpy().copy()
+    A, T = oracle_source(cfg, ms, ns)
     k1, k2 = min(cfg.k1, ms, ns), min(cfg.k2, ms, ns)
     times = []
     for i in range(args.warmup + args.steps):
-        if i < args.warmup:  # warm-up: a small sample (page-in, BLAS init)
-            O.cabs_run(A[:1000, :800], min(k1, 20), min(k2, 20), 2, seed=cfg.seed)
+        if i < args.warmup:  # warm-up: a small run (page-in, BLAS init)
+            O.cabs_run(A, min(k1, 20), min(k2, 20), 2, seed=cfg.seed, n_samples=min(T, 4096))
             continue
         t0 = time.perf_counter()
-        O.cabs_run(A, k1, k2, cfg.iters, seed=cfg.seed)
+        O.cabs_run(A, k1, k2, cfg.iters, seed=cfg.seed, n_samples=T)
         times.append(time.perf_counter() - t0)
     t = statistics.mean(times)
     v = (ms + ns) / t
     sample = (f"leading {ms} x {ns} block of {cfg.name} (same recipe, k1={k1}, k2={k2}, {cfg.iters} Lloyd "
-              f"iterations), full S1-S10 of the FP64 NumPy oracle per step")
+              f"iterations{f', residual on {T} sampled entries' if T else ''}), full S1-S10 of the FP64 NumPy "
+              f"oracle per step")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -192,14 +206,18 @@ def oracle_cpu_baseline(cfg, A_host):
     from oracle import cabs as O
     cores = len(os.sched_getaffinity(0))
     ms, ns = oracle_sample(cfg)
-    A = np.ascontiguousarray(A_host[:ms, :ns])
+    if A_host is None:  # implicit source
+        A, T = oracle_source(cfg, ms, ns)
+    else:
+        A, T = np.ascontiguousarray(A_host[:ms, :ns]), 0
     k1, k2 = min(cfg.k1, ms, ns), min(cfg.k2, ms, ns)
     t0 = time.perf_counter()
-    O.cabs_run(A, k1, k2, cfg.iters, seed=cfg.seed)
+    O.cabs_run(A, k1, k2, cfg.iters, seed=cfg.seed, n_samples=T)
     t = time.perf_counter() - t0
     return {"value": (ms + ns) / t, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"leading {ms} x {ns} block of {cfg.name} (k1={k1}, k2={k2}, {cfg.iters} Lloyd iterations), "
-                      f"one full S1-S10 step of the FP64 NumPy oracle ({t:.1f} s)"}
+            "sample": f"leading {ms} x {ns} block of {cfg.name} (k1={k1}, k2={k2}, {cfg.iters} Lloyd iterations"
+                      f"{f', residual on {T} sampled entries' if T else ''}), one full S1-S10 step of the FP64 "
+                      f"NumPy oracle ({t:.1f} s)"}
 
 
 def parity_block(cfg, A_host, pipe, res, plan, dev, row_sample=2048):
@@ -309,12 +327,71 @@ def parity_block(cfg, A_host, pipe, res, plan, dev, row_sample=2048):
     return out
 
 
+def parity_block_rbf(cfg, x, y, sigma, pipe, res, plan, dev, sample=2048, pairs=1 << 20):
+    """Full-size c5 parity on samples the oracle computes one by one: S1 indices bit-exact; the
+    generated gathers (a sample of rows of C, of columns of R, all of W) within 2e-6 of the FP64
+    entries; S7 centres = cluster means, S6 objective monotone; S10 the GPU's sampled residual on
+    the first `pairs` positions vs the oracle's on the same positions with the GPU's factors."""
+    from oracle import cabs as O
+    from oracle import rng
+    from paper_1607_07395_b200 import cabs as C
+    out = {"kind": "full-size c5, per-step checks on sampled outputs (the oracle cannot form the 2e6 x 1e6 "
+                   "matrix; the whole pipeline is compared with the oracle at reduced sizes in tests/test_gpu_rbf.py)"}
+    t0 = time.perf_counter()
+    m, n, k1, k2 = cfg.m, cfg.n, cfg.k1, cfg.k2
+    osrc = O.RbfSource(x.numpy(), y.numpy(), sigma)
+    I, J = res["I"].numpy(), res["J"].numpy()
+    out["S1_pilot_indices_exact"] = bool(np.array_equal(I, rng.floyd(m, k1, cfg.seed, rng.TAG_PILOT_ROWS)) and
+                                         np.array_equal(J, rng.floyd(n, k1, cfg.seed, rng.TAG_PILOT_COLS)))
+    g = np.random.default_rng(0)
+    rows = np.sort(g.choice(m, sample, replace=False))
+    cols = np.sort(g.choice(n, sample, replace=False))
+    e_c = float(np.abs(res["C"].numpy()[rows, :k1] - osrc.entries(rows, J)).max())
+    e_r = float(np.abs(res["R"].numpy()[:, cols] - osrc.entries(I, cols)).max())
+    e_w = float(np.abs(res["W"].numpy()[:, :k1] - osrc.entries(I, J)).max())
+    out["S2_S3_generated_gathers"] = {"C_rows_sampled": sample, "R_cols_sampled": sample, "max_abs_err":
+                                      max(e_c, e_r, e_w), "ok": bool(max(e_c, e_r, e_w) < 2e-6)}
+    r1 = res["r1"]
+    s7 = {}
+    for side, X, cen, lab, obj in (("rows", res["P"], res["cen_r"], res["lab_r"], res["obj_r"]),
+                                   ("cols", res["Q"], res["cen_c"], res["lab_c"], res["obj_c"])):
+        Xn = X.numpy()[:, :r1].astype(np.float64)
+        c = cen.numpy()[:, :r1].astype(np.float64)
+        lb = lab.numpy()[:Xn.shape[0]].astype(np.int64)
+        sums = np.zeros_like(c)
+        np.add.at(sums, lb, Xn)
+        cnt = np.bincount(lb, minlength=k2).astype(np.float64)
+        nz = cnt > 0
+        err = float(np.linalg.norm(c[nz] - sums[nz] / cnt[nz, None]) / np.linalg.norm(c[nz]))
+        ob = obj.numpy()
+        mono = bool(np.all(ob[1:] <= ob[:-1] * (1 + 1e-6) + 1e-30))
+        s7[side] = {"centres_vs_cluster_means_rel": err, "objective_monotone": mono, "ok": bool(err < 1e-5 and mono)}
+    out["S6_S7"] = s7
+    r2 = res["r2"]
+    ws = pipe.ws
+    o = torch.zeros(2, dtype=torch.float64, device=dev)
+    C.cabs_residual(plan, pipe.A, pipe.U, pipe.s2, pipe.G, r2, o, ws, n_samples=pairs, seed=cfg.seed)
+    og = o.cpu().numpy()
+    pi, pj = rng.residual_pairs(cfg.seed, pairs, m, n)
+    iu, inv = np.unique(pi, return_inverse=True)
+    Fu = pipe.U[torch.from_numpy(iu).to(dev), :r2].cpu().numpy()
+    ro2, ao2 = O.residual_sampled(osrc, Fu, res["V"].numpy()[:, :r2], pi, pj, res["s2"].numpy()[:r2], f_rows=inv)
+    rg, ro, ao = math.sqrt(max(og[0], 0)), math.sqrt(ro2), math.sqrt(ao2)
+    out["S10_sampled"] = {"pairs": pairs, "r_gpu": rg, "r_oracle": ro, "a_gpu": math.sqrt(og[1]), "a_oracle": ao,
+                          "ok": bool(abs(rg - ro) <= 1e-4 * ro + 1e-6 * ao and abs(og[1] - ao2) <= 1e-6 * ao2)}
+    out["ok"] = bool(out["S1_pilot_indices_exact"] and out["S2_S3_generated_gathers"]["ok"] and
+                     all(v["ok"] for v in s7.values()) and out["S10_sampled"]["ok"])
+    out["oracle_s"] = time.perf_counter() - t0
+    return out
+
+
 # ---------------------------------------------------------------------- our arm
 def time_variant(args, cfg, A, plan, rank, world, comm, flush, stream, followup, desc):
     """One of the paper's follow-up variants on the same matrix, timed like the main step."""
     from paper_1607_07395_b200.pipeline import CabsConfig, CabsPipeline
-    vp = CabsPipeline(A, cfg.m, cfg.n, CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, followup=followup),
-                      rank, world, comm=comm, plan=plan)
+    samples = C5_SAMPLES if cfg.kind == "rbf_mixture" else 0
+    vp = CabsPipeline(A, cfg.m, cfg.n, CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, followup=followup,
+                                                  residual_samples=samples), rank, world, comm=comm, plan=plan)
     for _ in range(args.warmup):
         vp.run()
     per = {}
@@ -378,12 +455,18 @@ def main():
     torch.cuda.set_device(dev)
     C.load()
     plan = make_plan(cfg.m, cfg.n, max(cfg.k1, cfg.k2), rank, world, align=CHUNK)
-    gen = Generator(cfg, device=dev)
-    A = gen.rows(plan.row_begin, plan.row_end)
-    del gen
+    rbf = cfg.kind == "rbf_mixture"
+    if rbf:  # implicit source: the points on every rank, entries generated on access
+        xh, yh, sigma = make_rbf(cfg)
+        A = C.RbfSource(xh.to(dev), yh.to(dev), sigma)
+    else:
+        gen = Generator(cfg, device=dev)
+        A = gen.rows(plan.row_begin, plan.row_end)
+        del gen
     torch.cuda.empty_cache()
     comm = TorchComm(dev) if world > 1 else None
-    ccfg = CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed)
+    samples = C5_SAMPLES if rbf else 0
+    ccfg = CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, residual_samples=samples)
     pipe = CabsPipeline(A, cfg.m, cfg.n, ccfg, rank, world, comm=comm, plan=plan)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
@@ -440,11 +523,15 @@ def main():
     e2e = None
     A_host = None
     if not args.no_e2e:
-        A_host = A.cpu().pin_memory()
+        if rbf:  # the inputs are the points x, y
+            ins = [(A.x, xh.pin_memory()), (A.y, yh.pin_memory())]
+        else:
+            A_host = A.cpu().pin_memory()
+            ins = [(A, A_host)]
         outs = [pipe.U, pipe.s2, pipe.V, pipe.Ib, pipe.Jb, pipe.out]
         host_outs = [torch.empty_like(t, device="cpu").pin_memory() for t in outs]
         d2h = sum(t.numel() * t.element_size() for t in outs)
-        h2d = A_host.numel() * A_host.element_size()
+        h2d = sum(h.numel() * h.element_size() for _, h in ins)
         e2e_ms = []
         for _ in range(max(2, min(args.steps, 5))):
             flush.fill_(1.0)
@@ -452,7 +539,8 @@ def main():
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            pipe.A.copy_(A_host, non_blocking=True)
+            for dst, h in ins:
+                dst.copy_(h, non_blocking=True)
             if graph is not None:
                 graph.replay()
             else:
@@ -511,13 +599,19 @@ def main():
                         "weight / Floyd / init launches"}
     kmeans["frac"] = kmeans["achieved"] / kmeans["peak"]
     m_loc = plan.row_end - plan.row_begin
-    res_bytes = 4.0 * (m_loc * cfg.n + m_loc * cfg.k2 + cfg.n * cfg.k2)
+    r2n = int(pipe.r2.item())
+    if rbf:  # sampled: two random factor rows per owned pair; entries generated
+        res_bytes = 4.0 * 2 * r2n * samples * (m_loc / cfg.m)
+        res_kernel = "residual_sampled_kernel (Philox pairs, generated entries, warp dot of random factor rows)"
+    else:
+        res_bytes = 4.0 * (m_loc * cfg.n + m_loc * cfg.k2 + cfg.n * cfg.k2)
+        res_tc = C.cabs_residual_path(r2n) == "tc"
+        res_kernel = (("residual_tc_kernel (tcgen05 3xTF32, TMA)" if res_tc else "residual_ffma_kernel") +
+                      " (cabs_residual: fused F diag(s) G^T - A, squared-sum)")
     res_ms = step_mean["residual"]
     achieved = res_bytes / (res_ms / 1e3) / 1e9
     peak = float(peaks["hbm_gbs"])
-    res_tc = C.cabs_residual_path(int(pipe.r2.item())) == "tc"
-    residual = {"kernel": ("residual_tc_kernel (tcgen05 3xTF32, TMA)" if res_tc else "residual_ffma_kernel") +
-                          " (cabs_residual: fused F diag(s) G^T - A, squared-sum)", "bound": "hbm",
+    residual = {"kernel": res_kernel, "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic_of(traffic, f"{cfg.name}_residual"),
                 "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json, copy bandwidth)",
@@ -527,6 +621,9 @@ def main():
     kmeans_pts = cfg.iters * (cfg.m + cfg.n) / (step_mean["kmeans"] / 1e3)
     sketch_ms = sum(step_mean[s] for s in STEPS if s != "residual")
     a_gb = cfg.m * cfg.n * 4 / 1e9
+    l2_note = (f"flushed (256 MiB write) before every timed step; implicit A, {samples:.0e} sampled entries read "
+               f"{4.0 * 2 * r2n * samples / 1e12:.1f} TB of random factor rows (> L2)" if rbf else
+               f"flushed (256 MiB write) before every timed step; A ({a_gb:.1f} GB) > L2")
     line = {
         "metric": METRIC, "value": (cfg.m + cfg.n) / (ms / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -534,7 +631,7 @@ def main():
         "config": {"workload": f"{cfg.name} = BASELINE.json configs[{CFG_INDEX[cfg.name]}]: {cfg.note}",
                    "m": cfg.m, "n": cfg.n,
                    "k1": cfg.k1, "k2": cfg.k2, "iters": cfg.iters, "mode": "stabilized", "parallelism": f"rows{world}",
-                   "l2": f"flushed (256 MiB write) before every timed step; A ({a_gb:.1f} GB) > L2",
+                   "l2": l2_note, "residual_samples": samples or "exact",
                    "timing": "per-step CUDA events on the launching stream, barrier+sync both sides, max over ranks",
                    "launch": "one CUDA graph per step (captured S1-S10)" if graph is not None else "stream-ordered"},
         "breakdown_ms": step_mean,
@@ -552,9 +649,14 @@ def main():
     if e2e:
         line["e2e"] = e2e
     if world == 1 and not (args.no_cpu_baseline and args.no_parity):
-        A_np = A_host.numpy() if A_host is not None else A.cpu().numpy()
-        if not args.no_parity:
-            line["parity"] = parity_block(cfg, A_np, pipe, res, plan, dev)
+        if rbf:
+            A_np = None
+            if not args.no_parity:
+                line["parity"] = parity_block_rbf(cfg, xh, yh, sigma, pipe, res, plan, dev)
+        else:
+            A_np = A_host.numpy() if A_host is not None else A.cpu().numpy()
+            if not args.no_parity:
+                line["parity"] = parity_block(cfg, A_np, pipe, res, plan, dev)
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = oracle_cpu_baseline(cfg, A_np)
     print(json.dumps(line))

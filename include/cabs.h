@@ -92,10 +92,27 @@ typedef struct cabs_plan {
   int32_t rank, nranks;
 } cabs_plan;
 
-/* Dense float32 source (host struct).  Row i of the rank's block is at a + (i - row_begin)*lda. */
+/* Source of the matrix A (host struct).  A zero-initialised struct with a / lda set is dense.
+ *
+ * CABS_SOURCE_DENSE_F32: row i of the rank's block is at a + (i - row_begin)*lda (device,
+ *   (row_end - row_begin) x n, row-major, lda >= n).
+ * CABS_SOURCE_RBF_F32: the implicit matrix of BASELINE.json configs[4] (reading Z23),
+ *   A_ij = exp(-|x_i - y_j|^2 * inv_two_sigma2), generated on access in FP32 (direct
+ *   differences summed over the d coordinates in order, exp via ex2.approx) -- PAPER.md P:24
+ *   "never knowing the remaining entries".  x: device, ALL m points (m x ldx, replicated on
+ *   every rank); y: device, all n points (n x ldy); 1 <= d <= 64; inv_two_sigma2 = 1/(2 sigma^2) > 0.
+ *   No gather crosses ranks; cabs_residual needs n_samples > 0 for this kind. */
+#define CABS_SOURCE_DENSE_F32 0
+#define CABS_SOURCE_RBF_F32 1
 typedef struct cabs_source {
-  const float* a; /* device, (row_end - row_begin) x n, row-major */
-  int64_t lda;    /* >= n */
+  const float* a;         /* dense: device, (row_end - row_begin) x n, row-major */
+  int64_t lda;            /* dense: >= n */
+  int32_t kind;           /* CABS_SOURCE_* */
+  int32_t d;              /* RBF: point dimension */
+  const float* x;         /* RBF: m x ldx */
+  const float* y;         /* RBF: n x ldy */
+  int64_t ldx, ldy;       /* RBF: >= d */
+  float inv_two_sigma2;   /* RBF */
 } cabs_source;
 
 /* Collectives supplied by the caller (host struct).  Each callback sums `count`
@@ -344,17 +361,27 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
  * G^T)_ij^2 and out[1] = sum_ij A_ij^2 over the global matrix (FP64, reduced over
  * ranks).  F: this rank's m_loc x ncomp (ldf); G: all n rows x ncomp (ldg);
  * s: float[ncomp] or NULL (= ones).  The reconstruction is never materialised.
+ * n_samples = 0: the exact sums over all entries (dense source only).  n_samples = T > 0: the
+ * unbiased estimates (m n / T) sum_t (A_{i_t j_t} - F_{i_t} diag(s) G_{j_t}^T)^2 and
+ * (m n / T) sum_t A_{i_t j_t}^2 over T i.i.d. uniform positions from the Philox stream of
+ * `seed`, tag 5 (BASELINE.json configs[4] "residual estimated on a seeded 1e9-entry uniform
+ * subset"; readings Z17 / Z23; cabs_residual_pairs returns the same positions); every rank
+ * draws all T positions and adds the ones whose row it owns.
  * out: device double[2]. */
 int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float* F,
                       int64_t ldf, const float* s, const float* G, int64_t ldg, int32_t ncomp,
-                      double* out, void* ws, size_t ws_bytes, const cabs_comm* comm,
-                      void* stream);
+                      int64_t n_samples, uint64_t seed, double* out, void* ws, size_t ws_bytes,
+                      const cabs_comm* comm, void* stream);
 
 /* ---------------------------------------------------------------- test hooks
  * Building blocks exposed for step-level parity tests (same kernels as above). */
 /* Philox4x32-10 blocks: out[4*b + i] = Philox(ctr=(start+b lo, hi, tag, 0), key=seed)[i]. */
 int32_t cabs_philox_blocks(uint64_t seed, uint32_t tag, uint64_t start, int64_t count,
                            uint32_t* out, void* stream);
+/* Positions of sampled-residual pairs t0 .. t0+T-1 (the stream cabs_residual draws when
+ * n_samples > 0): device int64 i[T], j[T]. */
+int32_t cabs_residual_pairs(uint64_t seed, uint64_t t0, int64_t T, int64_t m, int64_t n, int64_t* i, int64_t* j,
+                            void* stream);
 /* Floyd sample of k distinct values in [0, N), sorted (the generator of cabs_pilot). */
 int32_t cabs_uniform_indices(int64_t N, int32_t k, uint64_t seed, uint32_t tag, int64_t* out,
                              void* stream);

@@ -447,11 +447,12 @@ def residual(A, F, G, s=None, block=2048):
     return r2, a2
 
 
-def residual_sampled(A, F, G, i, j, s=None, chunk=1 << 20):
+def residual_sampled(A, F, G, i, j, s=None, chunk=1 << 20, f_rows=None):
     """The P:313 error on a uniform subset of entries (BASELINE.json configs[4] "residual
     estimated on a seeded 1e9-entry uniform subset"; reading Z23: T i.i.d. positions (i_t, j_t)).
     Unbiased estimates of sum (A - F diag(s) G^T)^2 and sum A^2:
-        r2 = (m n / T) sum_t (A_{i_t j_t} - F_{i_t} . G_{j_t})^2,   a2 = (m n / T) sum_t A_{i_t j_t}^2."""
+        r2 = (m n / T) sum_t (A_{i_t j_t} - F_{i_t} . G_{j_t})^2,   a2 = (m n / T) sum_t A_{i_t j_t}^2.
+    f_rows: optional int array, F's row of pair t is F[f_rows[t]] (F given as the rows i_t only)."""
     m, n = A.shape
     i = np.asarray(i, np.int64)
     j = np.asarray(j, np.int64)
@@ -464,8 +465,9 @@ def residual_sampled(A, F, G, i, j, s=None, chunk=1 << 20):
     a2 = 0.0
     for c in range(0, T, chunk):
         ic, jc = i[c:c + chunk], j[c:c + chunk]
+        fc = ic if f_rows is None else np.asarray(f_rows, np.int64)[c:c + chunk]
         a = A.at(ic, jc) if isinstance(A, RbfSource) else np.asarray(A[ic, jc], np.float64)
-        e = a - np.sum(F[ic] * G[jc], axis=1)
+        e = a - np.sum(F[fc] * G[jc], axis=1)
         r2 += float(np.sum(e * e))
         a2 += float(np.sum(a * a))
     scale = float(m) * float(n) / float(T)

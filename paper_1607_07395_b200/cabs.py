@@ -58,8 +58,35 @@ class Plan(ctypes.Structure):
         return self.col_end - self.col_begin
 
 
+SOURCE_DENSE_F32 = 0
+SOURCE_RBF_F32 = 1
+
+
 class Source(ctypes.Structure):
-    _fields_ = [("a", c_vp), ("lda", c_i64)]
+    _fields_ = [("a", c_vp), ("lda", c_i64), ("kind", c_i32), ("d", c_i32), ("x", c_vp), ("y", c_vp),
+                ("ldx", c_i64), ("ldy", c_i64), ("inv_two_sigma2", c_f32)]
+
+
+class RbfSource:
+    """The implicit RBF matrix of BASELINE.json configs[4]: A_ij = exp(-|x_i - y_j|^2 / (2 sigma^2)),
+    generated on access by the library (cabs.h CABS_SOURCE_RBF_F32).  x: device float32 (m, d) with
+    ALL m points, y: device float32 (n, d); the tensors must outlive the calls."""
+
+    def __init__(self, x, y, sigma):
+        assert x.dtype == y.dtype == torch.float32 and x.is_cuda and y.is_cuda and x.shape[1] == y.shape[1]
+        self.x, self.y = x.contiguous(), y.contiguous()
+        self.sigma = float(sigma)
+        self.inv_two_sigma2 = 1.0 / (2.0 * self.sigma * self.sigma)
+        self.shape = (x.shape[0], y.shape[0])
+        self.device = x.device
+
+
+def _source(A):
+    """cabs_source for a dense row block (a torch tensor) or an RbfSource."""
+    if isinstance(A, RbfSource):
+        return Source(None, 0, SOURCE_RBF_F32, A.x.shape[1], A.x.data_ptr(), A.y.data_ptr(), A.x.stride(0),
+                      A.y.stride(0), A.inv_two_sigma2)
+    return Source(A.data_ptr(), _ld(A), SOURCE_DENSE_F32, 0, None, None, 0, 0, 0.0)
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(c_i32, c_vp, c_i64, c_vp, c_vp)
@@ -134,9 +161,10 @@ _SIGS = {
                             c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz,
                             ctypes.POINTER(Comm), c_vp]),
     "cabs_residual": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_vp, c_i64, c_vp, c_vp, c_i64,
-                              c_i32, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+                              c_i32, c_i64, c_u64, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_philox_blocks": (c_i32, [c_u64, c_u32, c_u64, c_i64, c_vp, c_vp]),
     "cabs_uniform_indices": (c_i32, [c_i64, c_i32, c_u64, c_u32, c_vp, c_vp]),
+    "cabs_residual_pairs": (c_i32, [c_u64, c_u64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "cabs_svd": (c_i32, [ctypes.POINTER(Plan), c_i32, c_vp, c_i64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp,
                          c_sz, c_vp]),
 }
@@ -250,7 +278,7 @@ def cabs_device_status(ws, stream=None) -> int:
 
 # ---------------------------------------------------------------- entry points
 def cabs_pilot(plan, A, k, seed, I, J, C, R, W, ws, comm=None, stream=None):
-    src = Source(A.data_ptr(), _ld(A))
+    src = _source(A)
     _check(load().cabs_pilot(ctypes.byref(plan), ctypes.byref(src), int(k), int(seed), _p(I), _p(J),
                              _p(C), _ld(C), _p(R), _ld(R), _p(W), _ld(W), _p(ws), ws.numel(),
                              _comm(comm), _stream(stream)), "cabs_pilot")
@@ -258,7 +286,7 @@ def cabs_pilot(plan, A, k, seed, I, J, C, R, W, ws, comm=None, stream=None):
 
 def cabs_pilot_embed(plan, A, k, seed, I, J, C, R, W, mode, tol, P, Q, s, r, ws, sigma=None, comm=None,
                      stream=None):
-    src = Source(A.data_ptr(), _ld(A))
+    src = _source(A)
     _check(load().cabs_pilot_embed(ctypes.byref(plan), ctypes.byref(src), int(k), int(seed), _p(I), _p(J),
                                    _p(C), _ld(C), _p(R), _ld(R), _p(W), _ld(W), int(mode), float(tol),
                                    _p(P), _ld(P), _p(Q), _ld(Q), _p(s), _p(r), _p(sigma), _p(ws), ws.numel(),
@@ -378,17 +406,23 @@ def cabs_leverage_select_pair(plan, a, b, seed, tag_a, tag_b, ws, comm=None, str
 
 
 def cabs_sketch(plan, A, Ir, Ic, k, mode, tol, U, s, V, r, ws, sigma=None, comm=None, stream=None):
-    src = Source(A.data_ptr(), _ld(A))
+    src = _source(A)
     _check(load().cabs_sketch(ctypes.byref(plan), ctypes.byref(src), _p(Ir), _p(Ic), int(k), int(mode),
                               float(tol), _p(U), _ld(U), _p(s), _p(V), _ld(V), _p(r), _p(sigma), _p(ws),
                               ws.numel(), _comm(comm), _stream(stream)), "cabs_sketch")
 
 
-def cabs_residual(plan, A, F, s, G, ncomp, out, ws, comm=None, stream=None):
-    src = Source(A.data_ptr(), _ld(A))
+def cabs_residual(plan, A, F, s, G, ncomp, out, ws, comm=None, stream=None, n_samples=0, seed=0):
+    """n_samples = 0: exact sums (dense A); n_samples > 0: the sampled estimate (cabs.h)."""
+    src = _source(A)
     _check(load().cabs_residual(ctypes.byref(plan), ctypes.byref(src), _p(F), _ld(F), _p(s), _p(G),
-                                _ld(G), int(ncomp), _p(out), _p(ws), ws.numel(), _comm(comm),
-                                _stream(stream)), "cabs_residual")
+                                _ld(G), int(ncomp), int(n_samples), int(seed), _p(out), _p(ws), ws.numel(),
+                                _comm(comm), _stream(stream)), "cabs_residual")
+
+
+def cabs_residual_pairs(seed, t0, T, m, n, i, j, stream=None):
+    _check(load().cabs_residual_pairs(int(seed), int(t0), int(T), int(m), int(n), _p(i), _p(j), _stream(stream)),
+           "cabs_residual_pairs")
 
 
 # ---------------------------------------------------------------- test hooks

@@ -186,6 +186,48 @@ static int32_t side_stream(SideStream** out) {
   return CABS_OK;
 }
 
+// ---------------------------------------------------------------- sources
+static bool is_rbf(const cabs_source* s) { return s->kind == CABS_SOURCE_RBF_F32; }
+static RbfSrc rbf_of(const cabs_source* s) {
+  return RbfSrc{s->x, s->y, s->ldx, s->ldy, s->d, s->inv_two_sigma2};
+}
+static int32_t check_source(const cabs_plan& p, const cabs_source* src, const char* what) {
+  if (!src) return arg_error(what);
+  if (src->kind == CABS_SOURCE_DENSE_F32) {
+    if ((p.row_end > p.row_begin && !src->a) || src->lda < p.n) return arg_error(what);
+    return CABS_OK;
+  }
+  if (src->kind == CABS_SOURCE_RBF_F32) {
+    if (!src->x || !src->y || src->d < 1 || src->d > 64 || src->ldx < src->d || src->ldy < src->d ||
+        !(src->inv_two_sigma2 > 0.f))
+      return arg_error(what);
+    return CABS_OK;
+  }
+  return arg_error(what);
+}
+// C = A(rows of this rank, J)
+static void src_cols(const cabs_plan& p, const cabs_source* src, const int64_t* J, int k, float* C, int64_t ldc,
+                     void* ws, cudaStream_t st) {
+  const int64_t m_loc = p.row_end - p.row_begin;
+  if (is_rbf(src)) launch_rbf_cols(rbf_of(src), p.row_begin, m_loc, J, k, C, ldc, st);
+  else launch_gather_cols(src->a, src->lda, m_loc, p.n, J, k, C, ldc, ws, st);
+}
+// R = A(I, :): dense -- the rows this rank owns (others: completed by the caller's allreduce);
+// implicit -- every row, on every rank
+static void src_rows(const cabs_plan& p, const cabs_source* src, const int64_t* I, int k, float* R, int64_t ldr,
+                     void* ws, cudaStream_t st) {
+  if (is_rbf(src)) launch_rbf_rows(rbf_of(src), I, k, p.n, R, ldr, st);
+  else launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, I, k, p.n, R, ldr, ws, st);
+}
+// W = A(I, J) straight from the source (single rank, or implicit)
+static void src_w(const cabs_plan& p, const cabs_source* src, const int64_t* I, const int64_t* J, int k, float* W,
+                  int64_t ldw, cudaStream_t st) {
+  if (is_rbf(src)) launch_rbf_w(rbf_of(src), I, J, k, W, ldw, st);
+  else launch_gather_w_direct(src->a, src->lda, p.row_begin, p.row_end - p.row_begin, p.n, I, J, k, W, ldw, st);
+}
+// rows of R are exchanged only for a dense source on several ranks
+static bool rows_need_comm(const cabs_source* src, const cabs_comm* comm) { return multi(comm) && !is_rbf(src); }
+
 // ---------------------------------------------------------------- S1-S3
 int32_t cabs_pilot(const cabs_plan* plan, const cabs_source* src, int32_t k, uint64_t seed, int64_t* I, int64_t* J,
                    float* C, int64_t ldc, float* R, int64_t ldr, float* W, int64_t ldw, void* ws, size_t ws_bytes,
@@ -195,19 +237,19 @@ int32_t cabs_pilot(const cabs_plan* plan, const cabs_source* src, int32_t k, uin
   CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
   const cabs_plan& p = *plan;
   if (k < 1 || k > p.kmax || k > p.m || k > p.n) return arg_error("pilot: need 1 <= k <= min(m, n, kmax)");
-  if (!src || (p.row_end > p.row_begin && !src->a) || src->lda < p.n) return arg_error("pilot: bad source");
+  CABS_TRY(check_source(p, src, "pilot: bad source"));
   if (!I || !J || !C || !R || !W || ldc < k || ldr < p.n || ldw < k) return arg_error("pilot: bad output buffers");
   if (p.m >= 0xFFFFFFFFll || p.n >= 0xFFFFFFFFll) return arg_error("pilot: dims must be < 2^32 - 1");
   cudaStream_t st = S(stream);
-  const int64_t m_loc = p.row_end - p.row_begin;
   launch_floyd2(p.m, k, 1u, I, p.n, k, 2u, J, seed, st);  // tags ROWS_PILOT = 1, COLS_PILOT = 2
   CABS_LAUNCH_CHECK("floyd");
-  launch_gather_cols(src->a, src->lda, m_loc, p.n, J, k, C, ldc, ws, st);
+  src_cols(p, src, J, k, C, ldc, ws, st);
   CABS_LAUNCH_CHECK("gather_cols");
-  if (multi(comm)) launch_fill_neg_zero(R, ldr * (int64_t)k, st);  // -0.0: the allreduce is then bit-exact
-  launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, I, k, p.n, R, ldr, ws, st);
+  const bool xr = rows_need_comm(src, comm);
+  if (xr) launch_fill_neg_zero(R, ldr * (int64_t)k, st);  // -0.0: the allreduce is then bit-exact
+  src_rows(p, src, I, k, R, ldr, ws, st);
   CABS_LAUNCH_CHECK("gather_rows");
-  CABS_TRY(comm_f32(comm, R, ldr * (int64_t)k, stream));
+  if (xr) CABS_TRY(comm_f32(comm, R, ldr * (int64_t)k, stream));
   launch_gather_w(R, ldr, p.n, J, k, W, ldw, st);
   CABS_LAUNCH_CHECK("gather_w");
   return CABS_OK;
@@ -277,17 +319,16 @@ int32_t cabs_pilot_embed(const cabs_plan* plan, const cabs_source* src, int32_t 
   CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
   const cabs_plan& p = *plan;
   if (k < 1 || k > p.kmax || k > p.m || k > p.n) return arg_error("pilot: need 1 <= k <= min(m, n, kmax)");
-  if (!src || (p.row_end > p.row_begin && !src->a) || src->lda < p.n) return arg_error("pilot: bad source");
+  CABS_TRY(check_source(p, src, "pilot: bad source"));
   if (!I || !J || !C || !R || !W || ldc < k || ldr < p.n || ldw < k) return arg_error("pilot: bad output buffers");
   if (p.m >= 0xFFFFFFFFll || p.n >= 0xFFFFFFFFll) return arg_error("pilot: dims must be < 2^32 - 1");
   if (mode != CABS_STABILIZED && mode != CABS_PSEUDO_SKELETON) return arg_error("embed: bad mode");
   if (!P || !Q || !s || ldp < k || ldq < k) return arg_error("embed: bad buffers");
   cudaStream_t st = S(stream);
-  const int64_t m_loc = p.row_end - p.row_begin;
   launch_floyd2(p.m, k, 1u, I, p.n, k, 2u, J, seed, st);  // tags ROWS_PILOT = 1, COLS_PILOT = 2
   CABS_LAUNCH_CHECK("floyd");
   // W = A(I, J) first, its SVD on the side stream while C and R are gathered here
-  launch_gather_w_direct(src->a, src->lda, p.row_begin, m_loc, p.n, I, J, k, W, ldw, st);
+  src_w(p, src, I, J, k, W, ldw, st);
   CABS_LAUNCH_CHECK("gather_w_direct");
   SideStream* ss = nullptr;
   CABS_TRY(side_stream(&ss));
@@ -295,8 +336,8 @@ int32_t cabs_pilot_embed(const cabs_plan* plan, const cabs_source* src, int32_t 
   CABS_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
   launch_svd(k, W, ldw, tol, ws, L, sigma, nullptr, nullptr, nullptr, ss->s);
   CABS_LAUNCH_CHECK("svd");
-  launch_gather_cols(src->a, src->lda, m_loc, p.n, J, k, C, ldc, ws, st);
-  launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, I, k, p.n, R, ldr, ws, st);
+  src_cols(p, src, J, k, C, ldc, ws, st);
+  src_rows(p, src, I, k, R, ldr, ws, st);
   CABS_LAUNCH_CHECK("pilot gathers");
   CABS_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
   CABS_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));
@@ -313,10 +354,9 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
   const cabs_plan& p = *plan;
   if (k < 1 || k > p.kmax || k > p.m || k > p.n) return arg_error("sketch: need 1 <= k <= min(m, n, kmax)");
   if (mode != CABS_STABILIZED && mode != CABS_PSEUDO_SKELETON) return arg_error("sketch: bad mode");
-  if (!src || (p.row_end > p.row_begin && !src->a) || src->lda < p.n || !Ir || !Ic || !U || !V || !s || ldu < k || ldv < k)
-    return arg_error("sketch: bad buffers");
+  CABS_TRY(check_source(p, src, "sketch: bad source"));
+  if (!Ir || !Ic || !U || !V || !s || ldu < k || ldv < k) return arg_error("sketch: bad buffers");
   cudaStream_t st = S(stream);
-  const int64_t m_loc = p.row_end - p.row_begin;
   float* Cb = wsp<float>(ws, L.cb);
   float* Rb = wsp<float>(ws, L.rb);
   float* Wb = wsp<float>(ws, L.wb);
@@ -327,13 +367,13 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
     CABS_TRY(side_stream(&ss));
     CABS_CUDA_TRY(cudaEventRecord(ss->fork, st));
     CABS_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
-    launch_gather_w_direct(src->a, src->lda, p.row_begin, m_loc, p.n, Ir, Ic, k, Wb, L.Kp, ss->s);
+    src_w(p, src, Ir, Ic, k, Wb, L.Kp, ss->s);
     CABS_LAUNCH_CHECK("gather_w_direct");
     launch_svd(k, Wb, L.Kp, tol, ws, L, sigma, nullptr, nullptr, nullptr, ss->s);
     CABS_LAUNCH_CHECK("svd");
     launch_validate_idx2(Ir, p.m, Ic, p.n, k, ws, st);
-    launch_gather_cols(src->a, src->lda, m_loc, p.n, Ic, k, Cb, L.Kp, ws, st);
-    launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, Ir, k, p.n, Rb, L.ldrb, ws, st);
+    src_cols(p, src, Ic, k, Cb, L.Kp, ws, st);
+    src_rows(p, src, Ir, k, Rb, L.ldrb, ws, st);
     CABS_LAUNCH_CHECK("sketch gathers");
     CABS_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
     CABS_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));
@@ -341,11 +381,12 @@ int32_t cabs_sketch(const cabs_plan* plan, const cabs_source* src, const int64_t
                       stream, true);
   }
   launch_validate_idx2(Ir, p.m, Ic, p.n, k, ws, st);
-  launch_gather_cols(src->a, src->lda, m_loc, p.n, Ic, k, Cb, L.Kp, ws, st);
-  if (multi(comm)) launch_fill_neg_zero(Rb, L.ldrb * (int64_t)k, st);
-  launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, Ir, k, p.n, Rb, L.ldrb, ws, st);
+  src_cols(p, src, Ic, k, Cb, L.Kp, ws, st);
+  const bool xr = rows_need_comm(src, comm);
+  if (xr) launch_fill_neg_zero(Rb, L.ldrb * (int64_t)k, st);
+  src_rows(p, src, Ir, k, Rb, L.ldrb, ws, st);
   CABS_LAUNCH_CHECK("sketch gathers");
-  CABS_TRY(comm_f32(comm, Rb, L.ldrb * (int64_t)k, stream));
+  if (xr) CABS_TRY(comm_f32(comm, Rb, L.ldrb * (int64_t)k, stream));
   launch_gather_w(Rb, L.ldrb, p.n, Ic, k, Wb, L.Kp, st);
   CABS_LAUNCH_CHECK("gather_w");
   return embed_core(p, L, k, Cb, L.Kp, Rb, L.ldrb, Wb, L.Kp, mode, tol, U, ldu, V, ldv, s, r, sigma, 1, ws, comm,
@@ -860,15 +901,34 @@ int32_t cabs_leverage_select_pair(const cabs_plan* plan, const cabs_hard_problem
 
 // ---------------------------------------------------------------- S10
 int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float* F, int64_t ldf, const float* s,
-                      const float* G, int64_t ldg, int32_t ncomp, double* out, void* ws, size_t ws_bytes,
-                      const cabs_comm* comm, void* stream) {
+                      const float* G, int64_t ldg, int32_t ncomp, int64_t n_samples, uint64_t seed, double* out,
+                      void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream) {
   CABS_TRY(check_plan(plan));
   Ws L;
   CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
   const cabs_plan& p = *plan;
-  if (!src || (p.row_end > p.row_begin && !src->a) || src->lda < p.n || !F || !G || !out || ncomp < 0 || ldf < ncomp || ldg < ncomp)
+  CABS_TRY(check_source(p, src, "residual: bad source"));
+  if (!F || !G || !out || ncomp < 0 || ncomp > CABS_KMAX || ldf < ncomp || ldg < ncomp || n_samples < 0)
     return arg_error("residual: bad arguments");
   const int64_t m_loc = p.row_end - p.row_begin;
+  if (n_samples > 0) {  // the sampled estimate (readings Z17 / Z23)
+    if (p.m > (1ll << 32) || p.n > (1ll << 32)) return arg_error("residual: sampled dims must be <= 2^32");
+    SampArgs a{};
+    if (is_rbf(src)) a.rbf = rbf_of(src);
+    else { a.A = src->a; a.lda = src->lda; }
+    a.m = static_cast<uint64_t>(p.m);
+    a.n = static_cast<uint64_t>(p.n);
+    a.row_begin = p.row_begin;
+    a.row_end = p.row_end;
+    a.F = F; a.ldf = ldf; a.s = s; a.G = G; a.ldg = ldg; a.ncomp = ncomp;
+    a.T = n_samples;
+    a.seed = seed;
+    launch_residual_sampled(a, wsp<double>(ws, L.res_part), out, S(stream));
+    CABS_LAUNCH_CHECK("residual_sampled");
+    CABS_TRY(comm_f64(comm, out, 2, stream));
+    return CABS_OK;
+  }
+  if (is_rbf(src)) return arg_error("residual: the implicit source needs n_samples > 0");
   if (residual_tc_supported(src->a, src->lda, m_loc, p.n, ncomp)) {
     if (launch_residual_tc(src->a, src->lda, m_loc, p.n, F, ldf, s, G, ldg, ncomp, wsp<float>(ws, L.res_split),
                            wsp<double>(ws, L.res_part), out, S(stream)) != 0) {
@@ -881,6 +941,15 @@ int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float
   }
   CABS_LAUNCH_CHECK("residual");
   CABS_TRY(comm_f64(comm, out, 2, stream));
+  return CABS_OK;
+}
+
+int32_t cabs_residual_pairs(uint64_t seed, uint64_t t0, int64_t T, int64_t m, int64_t n, int64_t* i, int64_t* j,
+                            void* stream) {
+  if (T < 0 || m < 1 || n < 1 || m > (1ll << 32) || n > (1ll << 32) || (T > 0 && (!i || !j)))
+    return arg_error("residual_pairs: bad arguments");
+  launch_residual_pairs(seed, t0, T, m, n, i, j, S(stream));
+  CABS_LAUNCH_CHECK("residual_pairs");
   return CABS_OK;
 }
 

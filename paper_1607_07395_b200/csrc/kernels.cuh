@@ -194,4 +194,37 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
                        const float* s, const float* G, int64_t ldg, int ncomp, float* split, double* part, double* out,
                        cudaStream_t st);
 
+// rbf.cu: the implicit RBF source (reading Z23) and the sampled residual (Z17 / Z23)
+struct RbfSrc {
+  const float* x;  // m x ldx (all points)
+  const float* y;  // n x ldy
+  int64_t ldx, ldy;
+  int d;
+  float g;  // 1 / (2 sigma^2)
+};
+struct SampArgs {
+  const float* A;  // dense source (rbf.x == nullptr): the rank's rows
+  int64_t lda;
+  RbfSrc rbf;      // implicit source when rbf.x != nullptr
+  uint64_t m, n, thr_m, thr_n;
+  int64_t row_begin, row_end;
+  const float* F;  // m_loc x ncomp (ldf)
+  int64_t ldf;
+  const float* s;  // ncomp or null
+  const float* G;  // n x ncomp (ldg)
+  int64_t ldg;
+  int ncomp;
+  int64_t T;
+  uint64_t seed;
+};
+void launch_rbf_rows(const RbfSrc& s, const int64_t* I, int k, int64_t n, float* R, int64_t ldr, cudaStream_t st);
+void launch_rbf_cols(const RbfSrc& s, int64_t row_begin, int64_t m_loc, const int64_t* J, int k, float* C,
+                     int64_t ldc, cudaStream_t st);
+void launch_rbf_w(const RbfSrc& s, const int64_t* I, const int64_t* J, int k, float* W, int64_t ldw,
+                  cudaStream_t st);
+void launch_residual_pairs(uint64_t seed, uint64_t t0, int64_t T, int64_t m, int64_t n, int64_t* oi, int64_t* oj,
+                           cudaStream_t st);
+void launch_residual_sampled(const SampArgs& a, double* part, double* out, cudaStream_t st);
+int residual_sampled_part_doubles();
+
 }  // namespace cabsk

@@ -10,7 +10,9 @@ entry points of libcabs.so in order on one stream:
   (f)   cabs_hard_select   instead of S6-S8 when cfg.followup == "hard": top-k2 weighting
                            coefficients per side (P:312 variant (f))
   S9    cabs_sketch   follow-up gathers + sketch -> Ubar, sbar, Vbar
-  S10   cabs_residual ||A - Ubar diag(sbar) Vbar^T||_F^2, ||A||_F^2
+  S10   cabs_residual ||A - Ubar diag(sbar) Vbar^T||_F^2, ||A||_F^2, exact or sampled
+
+A is this rank's dense row block (a tensor) or a cabs.RbfSource (c5, entries generated on access).
 
 Buffers are allocated once, so repeated runs (benchmark steps) allocate nothing.
 """
@@ -35,6 +37,7 @@ class CabsConfig:
     weight_kind: int = C.WEIGHT_CONST
     weight_p: float = 2.0
     followup: str = "kmeans"  # "kmeans" (Alg. 2 step 3), "hard" / "leverage" (P:312 variants (f) / (e))
+    residual_samples: int = 0  # 0: exact residual; T > 0: sampled estimate on T Philox pairs (c5)
 
 
 STEPS = ("pilot_embed", "kmeans", "select", "sketch", "residual")
@@ -52,7 +55,10 @@ class CabsPipeline:
         self.comm = comm
         self.plan = plan if plan is not None else make_plan(m, n, max(cfg.k1, cfg.k2), rank, nranks, align)
         p = self.plan
-        assert A_local.shape[0] == p.m_loc and A_local.shape[1] >= n
+        if isinstance(A_local, C.RbfSource):  # implicit source: every rank holds all points
+            assert A_local.shape == (m, n)
+        else:
+            assert A_local.shape[0] == p.m_loc and A_local.shape[1] >= n
         dev = A_local.device
         self.device = dev
         k1, k2 = cfg.k1, cfg.k2
@@ -158,7 +164,8 @@ class CabsPipeline:
 
     def residual(self):
         c, p = self.cfg, self.plan
-        C.cabs_residual(p, self.A, self.U, self.s2, self.G, c.k2, self.out, self.ws, self.comm)
+        C.cabs_residual(p, self.A, self.U, self.s2, self.G, c.k2, self.out, self.ws, self.comm,
+                        n_samples=c.residual_samples, seed=c.seed)
 
     # ------------------------------------------------------------------ whole path
     def run(self, with_residual=True, timed=False, init_rows=None, init_cols=None):

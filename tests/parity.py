@@ -57,8 +57,10 @@ def _gpu_labels_per_iteration(C, X_dev, N, d, k2, iters, seed, tag, weight_kind=
     return out
 
 
-def check_e2e(C, O, A_host, g, ref, pipe, log_path=None, factor_tol=1e-4):
-    """Returns the divergence log; raises AssertionError on any parity failure."""
+def check_e2e(C, O, A_host, g, ref, pipe, log_path=None, factor_tol=1e-4, n_samples=0):
+    """Returns the divergence log; raises AssertionError on any parity failure.  A_host: the
+    oracle's matrix (dense array or oracle RbfSource); n_samples > 0: the residual is the
+    sampled estimate on the same Philox pairs on both sides (c5)."""
     cfg = pipe.cfg
     m, n = A_host.shape
     k1, k2, iters = cfg.k1, cfg.k2, cfg.iters
@@ -130,7 +132,7 @@ def check_e2e(C, O, A_host, g, ref, pipe, log_path=None, factor_tol=1e-4):
     C.cabs_sketch(plan, pipe.A, Ir, Ic, k2, cfg.mode, cfg.tol, U, s, V, r, ws)
     out = torch.zeros(2, dtype=torch.float64, device=dev)
     r2 = int(r.item())
-    C.cabs_residual(plan, pipe.A, U, s, V, r2, out, ws)
+    C.cabs_residual(plan, pipe.A, U, s, V, r2, out, ws, n_samples=n_samples, seed=cfg.seed)
     fu = ref.follow
     assert r2 == fu.r, ("follow-up rank", r2, fu.r)
     eU = rel_fro(align_signs(U.cpu().numpy()[:, :r2], fu.U), fu.U)

@@ -226,3 +226,47 @@ def test_sketch_out_of_range_index_sets_status(dev):
         pass
     torch.cuda.synchronize()
     assert C.cabs_device_status(ws) & C.DEV_RANGE
+
+
+def test_pipeline_rbf_two_ranks_match_one(dev):
+    """The implicit source on two ranks: every rank generates its own rows (no row exchange);
+    the pipeline with the sampled residual equals the single-rank one (P15)."""
+    from paper_1607_07395_b200.dist import make_plan
+    from paper_1607_07395_b200.pipeline import CabsConfig, CabsPipeline
+    from workloads import CONFIGS, make_rbf, scaled
+    m, n, k = 9001, 5003, 40
+    x, y, sigma = make_rbf(scaled(CONFIGS["c5"], m, n))
+    src = C.RbfSource(x.to(dev), y.to(dev), sigma)
+    cfg = CabsConfig(k, k, 4, seed=1, residual_samples=1 << 20)
+    one = CabsPipeline(src, m, n, cfg)
+    one.run()
+    g1 = one.results()
+    rc = HostRendezvousComm(2, dev)
+
+    def rank(r):
+        plan = make_plan(m, n, k, r, 2)
+        st = torch.cuda.Stream(device=dev)
+        st.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(st):
+            pipe = CabsPipeline(src, m, n, cfg, r, 2, comm=rc.comms[r], plan=plan)
+            pipe.run()
+        st.synchronize()
+        with torch.cuda.stream(st):
+            return plan, pipe.results()
+
+    outs = run_ranks(2, rank)
+    for plan, g in outs:
+        assert torch.equal(g["I"], g1["I"]) and torch.equal(g["J"], g1["J"])
+        assert torch.equal(g["R"], g1["R"]) and torch.equal(g["W"], g1["W"])
+    cat = lambda key, rows: torch.cat([g[key][:(p.m_loc if rows else p.n_sl)] for p, g in outs])  # noqa: E731
+    r1 = g1["r1"]
+    P1 = g1["P"].numpy()[:, :r1]
+    assert rel_fro(align_signs(cat("P", True).numpy()[:, :r1], P1), P1) < 1e-5
+    same = all(torch.equal(g["Ib"], g1["Ib"]) and torch.equal(g["Jb"], g1["Jb"]) for _, g in outs)
+    if not same:
+        ties = _tie_points([g1] + [g for _, g in outs], "rows") | _tie_points([g1] + [g for _, g in outs], "cols")
+        assert ties, "representatives differ without any logged near tie"
+        pytest.skip("trajectories parted at a logged near tie")
+    for _, g in outs:
+        assert abs(g["resid_sq"] - g1["resid_sq"]) <= 1e-6 * g1["a_sq"]
+        assert abs(g["a_sq"] - g1["a_sq"]) <= 1e-9 * g1["a_sq"]

@@ -135,3 +135,13 @@ def test_cabs_run_on_rbf_source_small():
     # the sampled estimate is near the dense value on this smooth matrix
     r2, a2 = O.residual(src, a.follow.U, a.follow.V, a.follow.s)
     assert abs(a.a_sq - a2) < 0.05 * a2
+
+
+def test_sampled_residual_row_remap_equals_full_factor():
+    """f_rows (F given only on the sampled rows) is a re-indexing: identical result."""
+    g = np.random.default_rng(5)
+    src = O.RbfSource(g.standard_normal((50, 16)), g.standard_normal((40, 16)), 4.0)
+    F, G, s = g.standard_normal((50, 3)), g.standard_normal((40, 3)), g.uniform(0.5, 2, 3)
+    i, j = rng.residual_pairs(3, 2000, 50, 40)
+    iu, inv = np.unique(i, return_inverse=True)
+    assert O.residual_sampled(src, F, G, i, j, s) == O.residual_sampled(src, F[iu], G, i, j, s, f_rows=inv)
