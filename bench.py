@@ -564,9 +564,6 @@ def main():
                                   "score sampling (cabs_orthogonalize, cabs_leverage_select_pair)")):
         if args.no_variants:
             break
-        if fu == "leverage" and cfg.k1 > C.ORTH_RMAX:
-            variants[fu_name] = {"followup": fu_desc, "skipped": f"cabs_orthogonalize supports r <= {C.ORTH_RMAX}"}
-            continue
         variants[fu_name] = time_variant(args, cfg, A, plan, rank, world, comm, flush, stream, fu, fu_desc)
 
     if rank != 0:

@@ -315,9 +315,9 @@ int32_t cabs_hard_select_pair(const cabs_plan* plan, const cabs_hard_problem* a,
  * device float[r] or NULL = ones), writes the thin SVD of that product, A ~ Uo diag(so)
  * Vo^T with orthonormal Uo, Vo (the paper's (U0 U1, S1, V1), unique up to signs; canonical
  * signs as Z5), so descending, components with so_j <= 1e-12 so_1 dropped (zero columns,
- * r_out = kept count).  Computed as Gram matrices (one allreduce of 2 x 64 x 64 doubles
- * across ranks), FP64 Cholesky, the FP64 Jacobi SVD of the r x r core, and one pass over U
- * and V.  Errors: r < 1, r > 64 or r > kmax, ld < r -> INVALID_ARG; all-zero columns (the zero
+ * r_out = kept count).  Computed as Gram matrices (one allreduce of 2 r^2 doubles across
+ * ranks), FP64 Cholesky, the FP64 Jacobi SVD of the r x r core, and one pass over U and V.
+ * Errors: r < 1 or r > kmax, ld < r -> INVALID_ARG; all-zero columns (the zero
  * padding beyond a truncated rank) drop out; a numerically rank-deficient U or V (negative
  * Cholesky pivot) sets CABS_DEV_ORTH_RANK.  sigma: device double[r] or NULL.  Uo may not alias U. */
 int32_t cabs_orthogonalize(const cabs_plan* plan, int32_t r, const float* U, int64_t ldu,

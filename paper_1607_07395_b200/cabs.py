@@ -37,7 +37,7 @@ DEV_SVD_NOCONV = 0x20
 TAG_PILOT_ROWS, TAG_PILOT_COLS, TAG_INIT_ROWS, TAG_INIT_COLS = 1, 2, 3, 4
 TAG_LEVERAGE_ROWS, TAG_LEVERAGE_COLS = 6, 7
 OP_KMEANS, OP_RESIDUAL, PATH_FFMA, PATH_TC = 0, 1, 0, 1
-ORTH_RMAX = 64  # cabs_orthogonalize: largest supported r
+ORTH_RMAX = 1024  # cabs_orthogonalize: largest supported r (= CABS_KMAX)
 
 
 class CabsError(RuntimeError):

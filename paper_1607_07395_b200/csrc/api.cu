@@ -837,7 +837,7 @@ int32_t cabs_orthogonalize(const cabs_plan* plan, int32_t r, const float* U, int
   CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
   const cabs_plan& p = *plan;
   const int64_t m_loc = p.row_end - p.row_begin, n_sl = p.col_end - p.col_begin;
-  if (r < 1 || r > 64 || r > p.kmax) return arg_error("orthogonalize: need 1 <= r <= min(64, kmax)");
+  if (r < 1 || r > p.kmax) return arg_error("orthogonalize: need 1 <= r <= kmax");
   if (ldu < r || ldv < r || lduo < r || ldvo < r) return arg_error("orthogonalize: bad leading dimensions");
   if ((m_loc > 0 && (!U || !Uo)) || (n_sl > 0 && (!V || !Vo)) || !so) return arg_error("orthogonalize: bad buffers");
   cudaStream_t st = S(stream);
@@ -847,21 +847,23 @@ int32_t cabs_orthogonalize(const cabs_plan* plan, int32_t r, const float* U, int
   a.V = V; a.ldv = ldv; a.nv = n_sl;
   a.r = r; a.s = s;
   a.part = wsp<double>(ws, L.orth_part);
-  a.nblk = orth_gram_blocks(m_loc, n_sl);
+  a.nblk = orth_gram_blocks(m_loc, n_sl, r);
+  // [gram: 2 r^2 | U_K: r^2 | V_K: r^2 | sigma: r | r_svd] FP64, then K, T_U, T_V (r x Kp FP32)
+  const size_t rr = static_cast<size_t>(r) * r;
   a.gram = reinterpret_cast<double*>(o);
-  a.UK = a.gram + 2 * 64 * 64;
-  a.VK = a.UK + 64 * 64;
-  a.sig = sigma ? sigma : a.VK + 64 * 64;
-  a.r_svd = reinterpret_cast<int*>(a.VK + 64 * 64 + 64);
+  a.UK = a.gram + 2 * rr;
+  a.VK = a.UK + rr;
+  a.sig = sigma ? sigma : a.VK + rr;
+  a.r_svd = reinterpret_cast<int*>(a.VK + rr + r);
   a.kp = L.Kp;
-  a.K = reinterpret_cast<float*>(o + sizeof(double) * (4 * 64 * 64 + 64) + 256);
-  a.TU = a.K + 64 * L.Kp;
-  a.TV = a.TU + 64 * L.Kp;
+  a.K = reinterpret_cast<float*>(o + sizeof(double) * (4 * rr + r) + 256);
+  a.TU = a.K + static_cast<size_t>(r) * L.Kp;
+  a.TV = a.TU + static_cast<size_t>(r) * L.Kp;
   a.s_out = so; a.r_out = r_out;
   a.Uo = Uo; a.lduo = lduo; a.Vo = Vo; a.ldvo = ldvo;
   launch_orth_gram(a, st);
   CABS_LAUNCH_CHECK("orth_gram");
-  CABS_TRY(comm_f64(comm, a.gram, 2 * 64 * 64, stream));
+  CABS_TRY(comm_f64(comm, a.gram, static_cast<int64_t>(2) * r * r, stream));
   launch_orth_core(a, ws, st);
   CABS_LAUNCH_CHECK("orth_core");
   launch_svd(r, a.K, a.kp, 1e-12, ws, L, a.sig, a.UK, a.VK, a.r_svd, st);

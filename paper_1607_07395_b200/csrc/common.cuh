@@ -94,8 +94,11 @@ inline Ws ws_layout(const cabs_plan& p) {
   // hard threshold: (key, index) candidates of every 2048-row CTA, both sides of a pair
   w.hcand_side = 2 * ceil_div(w.Nmax, kHardLocalRows) * K;  // doubles per side
   w.hcand = take(sizeof(double) * 2 * w.hcand_side);
-  w.orth_part = take(sizeof(double) * 2 * kOrthMaxBlocks * 64 * 64);
-  w.orth = take(sizeof(double) * (4 * 64 * 64 + 64) + 256 + sizeof(float) * 3 * 64 * Kp);
+  {  // cabs_orthogonalize (orth.cu): Gram partials of <= max(kOrthMaxBlocks, tile pairs) CTAs per side
+    const int64_t nt = (K + 63) / 64, np = nt * (nt + 1) / 2;
+    w.orth_part = take(sizeof(double) * 2 * (np > kOrthMaxBlocks ? np : kOrthMaxBlocks) * 64 * 64);
+  }
+  w.orth = take(sizeof(double) * (4 * K * K + K) + 256 + sizeof(float) * 3 * K * Kp);
   w.idx = take(sizeof(int64_t) * 8 * Kp);
   w.cb = take(sizeof(float) * (w.m_loc > 0 ? w.m_loc : 1) * Kp);
   w.rb = take(sizeof(float) * K * w.ldrb);

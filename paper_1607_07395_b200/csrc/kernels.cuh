@@ -147,7 +147,7 @@ int64_t hard_local_blocks(int64_t N);
 void launch_hard_local(const HardArgs& a, int nside, double* cand, int64_t side_stride, void* ws, cudaStream_t st);
 void launch_hard_topk(const HardArgs& a, int nside, cudaStream_t st);
 
-// orth.cu -- orthogonalization of a sketch (Supp. 3), r <= 64
+// orth.cu -- orthogonalization of a sketch (Supp. 3), r <= kmax
 struct OrthArgs {
   const float* U;  // nu x r (ldu), this rank's rows
   int64_t ldu, nu;
@@ -155,12 +155,12 @@ struct OrthArgs {
   int64_t ldv, nv;
   int r;
   const float* s;  // float[r] or NULL (ones)
-  double* part;    // [2][nblk][r*r] Gram partials
+  double* part;    // [2][nblk][tile pairs][64*64] Gram partials
   int nblk;
-  double* gram;    // [2][64*64]: G_U, G_V -> R_U, R_V (ld 64)
+  double* gram;    // [2][r*r]: G_U, G_V -> R_U, R_V (ld r)
   float* K;        // r x kp core (FP32, input of the Jacobi SVD)
   int64_t kp;
-  double* UK;      // r x r (ld r), from the SVD
+  double* UK;      // r x r (ld r), from the SVD; T_U in place
   double* VK;
   double* sig;     // SVD singular values
   int* r_svd;      // SVD rank
@@ -173,7 +173,7 @@ struct OrthArgs {
   float* Vo;
   int64_t ldvo;
 };
-int orth_gram_blocks(int64_t nu, int64_t nv);
+int orth_gram_blocks(int64_t nu, int64_t nv, int r);
 void launch_orth_gram(OrthArgs& a, cudaStream_t st);
 void launch_orth_core(const OrthArgs& a, void* ws, cudaStream_t st);
 void launch_orth_finish(const OrthArgs& a, cudaStream_t st);

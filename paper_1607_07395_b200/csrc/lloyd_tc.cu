@@ -62,7 +62,12 @@ __device__ long long g_ktc_tl[64][8];
 __device__ long long g_ktc_tile[32][8];
 #define KTC_TSTAMP(t, i) do { if (blockIdx.x == 0 && it == 2 && (t) < 32) { long long t_; \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_ktc_tile[t][i] = t_; } } while (0)
+// candidates refined per iteration (all CTAs, both problems): [it][0] points, [it][1] candidates
+__device__ unsigned long long g_ktc_cand[64][2];
+#define KTC_CAND(np_, nc_) do { if (it < 64) { atomicAdd(&g_ktc_cand[it][0], (unsigned long long)(np_)); \
+    atomicAdd(&g_ktc_cand[it][1], (unsigned long long)(nc_)); } } while (0)
 #else
+#define KTC_CAND(np_, nc_) do { } while (0)
 #define KTC_TSTAMP(t, i) do { } while (0)
 #endif
 
@@ -71,6 +76,7 @@ void ktc_debug_timeline(long long* out, int n) {
   const int m = n < 64 * 8 ? n : 64 * 8;
   cudaMemcpyFromSymbol(out, g_ktc_tl, sizeof(long long) * m);
   if (n >= 64 * 8 + 32 * 8) cudaMemcpyFromSymbol(out + 64 * 8, g_ktc_tile, sizeof(long long) * 32 * 8);
+  if (n >= 64 * 8 + 32 * 8 + 64 * 2) cudaMemcpyFromSymbol(out + 64 * 8 + 32 * 8, g_ktc_cand, sizeof(long long) * 64 * 2);
 #else
   for (int i = 0; i < n; ++i) out[i] = 0;
 #endif
@@ -491,6 +497,15 @@ lloyd_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant_
             }
           }
           for (int w = (nc + 31) >> 5; w < 4; ++w) cms[r * 4 + w] = 0u;
+#ifdef CABS_PROFILE_KTC
+          {
+            const bool in = (int64_t)t * kKM + r < npts;
+            int cnt = in ? __popc(cms[r * 4]) + __popc(cms[r * 4 + 1]) + __popc(cms[r * 4 + 2]) + __popc(cms[r * 4 + 3]) : 0;
+            int np_ = in;
+            for (int o = 16; o > 0; o >>= 1) { cnt += __shfl_xor_sync(0xffffffffu, cnt, o); np_ += __shfl_xor_sync(0xffffffffu, np_, o); }
+            if (lane == 0) KTC_CAND(np_, cnt);
+          }
+#endif
           tc::fence_before_sync();
         }
         // candidates of the tile ready (mbarrier: the 4 epilogue warps arrive, warps 2-9 wait)

@@ -33,18 +33,39 @@ def _pad(dev, X, ld):
     return t
 
 
+def _separated_factors(g, m, n, r):
+    """U, s, V with U diag(s) V^T = X diag(sig) Y^T, X, Y orthonormal and sig geometric (relative
+    gaps 1%: the singular vectors are well determined at any r), U = X B for a well-conditioned
+    random B, so U^T U is a full (non-identity) Gram matrix."""
+    X = np.linalg.qr(g.standard_normal((m, r)))[0]
+    Y = np.linalg.qr(g.standard_normal((n, r)))[0]
+    sig = 3.0 * 0.99 ** np.arange(r)
+    B = np.eye(r) + 0.3 * g.standard_normal((r, r)) / np.sqrt(r)
+    s = g.uniform(0.5, 2.0, r)
+    U = X @ B
+    V = (Y * sig) @ np.linalg.inv(B).T / s
+    return U.astype(np.float32), s.astype(np.float32), V.astype(np.float32)
+
+
 @pytest.mark.parametrize("m,n,r,zero_cols", [(1000, 700, 20, 0), (20000, 10000, 50, 0), (777, 333, 64, 0),
-                                             (100, 50, 1, 0), (3000, 2000, 10, 3)])
+                                             (100, 50, 1, 0), (3000, 2000, 10, 3), (5000, 3000, 100, 0),
+                                             (100000, 50000, 100, 0), (4000, 2500, 200, 7), (3000, 2000, 300, 0),
+                                             (2000, 1000, 230, 0)])
 def test_orthogonalize_matches_oracle(dev, m, n, r, zero_cols):
+    """r <= 64 with Gaussian factors; r >= 100 with well-separated singular values (r = 230, 300
+    take the global-memory Cholesky)."""
     from paper_1607_07395_b200.dist import make_plan
     g = np.random.default_rng(m + r)
-    U = g.standard_normal((m, r)).astype(np.float32)
-    V = g.standard_normal((n, r)).astype(np.float32)
-    s = g.uniform(0.2, 3.0, r).astype(np.float32)
+    if r < 100:
+        U = g.standard_normal((m, r)).astype(np.float32)
+        V = g.standard_normal((n, r)).astype(np.float32)
+        s = g.uniform(0.2, 3.0, r).astype(np.float32)
+    else:
+        U, s, V = _separated_factors(g, m, n, r)
     if zero_cols:
         U[:, r - zero_cols:] = 0
         V[:, r - zero_cols:] = 0
-    plan = make_plan(m, n, 64)
+    plan = make_plan(m, n, max(64, r))
     ws = torch.zeros(C.cabs_workspace_bytes(plan), dtype=torch.uint8, device=dev)
     ld = C.cabs_padded_ld(r)
     Ut, Vt = _pad(dev, U, ld), _pad(dev, V, ld)
@@ -119,7 +140,8 @@ def test_leverage_pair_and_spec_example(dev):
     assert ra.cpu().tolist() == [0, 1] and rb.cpu().tolist() == [0, 1]
 
 
-@pytest.mark.parametrize("name,m,n,k,seed", [("c1", 2000, 1500, 20, 0), ("c2", 4000, 2000, 50, 1)])
+@pytest.mark.parametrize("name,m,n,k,seed", [("c1", 2000, 1500, 20, 0), ("c2", 4000, 2000, 50, 1),
+                                             ("c3", 8000, 4000, 100, 2)])
 def test_e2e_leverage_followup(dev, name, m, n, k, seed):
     from paper_1607_07395_b200.pipeline import CabsConfig, CabsPipeline
     from workloads import CONFIGS, make_A, scaled
