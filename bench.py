@@ -580,7 +580,14 @@ def main():
     km_path = C.cabs_kmeans_path(cfg.k2, d_emb)
     km_flops = 2.0 * cfg.iters * (m_loc_rows(plan) + n_loc_cols(plan)) * cfg.k2 * d_emb
     km_ms = step_mean["kmeans"]
-    if km_path == "tc":
+    if km_path == "prune":
+        km_peak, km_bound = ffma_tf, "alu"
+        km_src = (f"derived: FFMA peak 148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz = {ffma_tf:.1f} TFLOP/s; "
+                  f"achieved counts the method's 2 r k2 flop per point and pass (SURVEY 8(d)); the pruned kernel "
+                  f"evaluates only the candidates the triangle-inequality bounds leave")
+        km_kernel = ("lloyd_prune_kernel (cabs_kmeans_pair: exact Hamerly/Elkan bounds + FP32 direct differences, "
+                     "both sides, all iterations, one launch)")
+    elif km_path == "tc":
         km_peak, km_bound = tf32_tf / 3.0, "tensor"
         km_src = (f"MEASURED_PEAKS bf16_tflops {peaks.get('bf16_tflops')} x 0.5 (nominal TF32:BF16) / 3 "
                   f"(3xTF32: three MMAs per algorithmic flop)")

@@ -139,14 +139,18 @@ int32_t cabs_clear_status(void* ws, void* stream);
  * benchmarks report the delta over a timed region as their launch count). */
 int64_t cabs_launch_count(void);
 /* Which kernel family an entry point dispatches to for these sizes (host query, no launch):
- * op CABS_OP_KMEANS (k = k2, d = embedding width): CABS_PATH_FFMA (FP32 direct-difference
- * persistent Lloyd kernel) or CABS_PATH_TC (tcgen05 3xTF32 cross-term + FP32 refine);
+ * op CABS_OP_KMEANS (k = k2, d = embedding width): CABS_PATH_PRUNE (persistent Lloyd kernel
+ * whose candidates are pruned exactly by the triangle inequality against the centre-centre
+ * distances, then FP32 direct differences), CABS_PATH_FFMA (FP32 direct differences against
+ * every centre) or CABS_PATH_TC (tcgen05 FP16-split cross-term + FP32 refine); all three take
+ * bit-identical decisions;
  * op CABS_OP_RESIDUAL (k = ncomp, d ignored): CABS_PATH_FFMA or CABS_PATH_TC.  Returns -1 for
  * an unknown op.  Benchmarks use it to label the roofline of the kernel that actually ran. */
 #define CABS_OP_KMEANS 0
 #define CABS_OP_RESIDUAL 1
 #define CABS_PATH_FFMA 0
 #define CABS_PATH_TC 1
+#define CABS_PATH_PRUNE 2
 int32_t cabs_kernel_path(int32_t op, int32_t k, int32_t d);
 /* Synchronises `stream`, then copies the device status word to host *flags. */
 int32_t cabs_device_status(const void* ws, void* stream, uint32_t* flags);

@@ -36,7 +36,7 @@ DEV_SVD_NOCONV = 0x20
 
 TAG_PILOT_ROWS, TAG_PILOT_COLS, TAG_INIT_ROWS, TAG_INIT_COLS = 1, 2, 3, 4
 TAG_LEVERAGE_ROWS, TAG_LEVERAGE_COLS = 6, 7
-OP_KMEANS, OP_RESIDUAL, PATH_FFMA, PATH_TC = 0, 1, 0, 1
+OP_KMEANS, OP_RESIDUAL, PATH_FFMA, PATH_TC, PATH_PRUNE = 0, 1, 0, 1, 2
 ORTH_RMAX = 1024  # cabs_orthogonalize: largest supported r (= CABS_KMAX)
 
 
@@ -252,8 +252,8 @@ def cabs_kernel_path(op: int, k: int, d: int = 0) -> int:
 
 
 def cabs_kmeans_path(k2: int, d: int) -> str:
-    """'tc' or 'ffma': the k-means distance kernel cabs_kmeans(_pair) runs for (k2, d)."""
-    return "tc" if cabs_kernel_path(OP_KMEANS, k2, d) == PATH_TC else "ffma"
+    """'prune', 'tc' or 'ffma': the k-means kernel cabs_kmeans(_pair) runs for (k2, d)."""
+    return {PATH_PRUNE: "prune", PATH_TC: "tc"}.get(cabs_kernel_path(OP_KMEANS, k2, d), "ffma")
 
 
 def cabs_residual_path(ncomp: int) -> str:

@@ -94,8 +94,10 @@ int32_t cabs_debug_counters(int64_t* out, int32_t n) {
 #ifdef CABS_PROFILE_SNAP
   if (n >= 4) snap_debug_counters(reinterpret_cast<long long*>(out));
 #endif
-#ifdef CABS_PROFILE_KTC
+#if defined(CABS_PROFILE_KTC)
   if (n > 16) ktc_debug_timeline(reinterpret_cast<long long*>(out) + 16, n - 16);
+#elif defined(CABS_PROFILE_LEX)
+  if (n > 16) lex_debug_timeline(reinterpret_cast<long long*>(out) + 16, n - 16);
 #else
   if (n > 16) lloyd_debug_timeline(reinterpret_cast<long long*>(out) + 16, n - 16);
 #endif
@@ -105,7 +107,8 @@ int32_t cabs_debug_counters(int64_t* out, int32_t n) {
 int64_t cabs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int32_t cabs_kernel_path(int32_t op, int32_t k, int32_t d) {
-  if (op == CABS_OP_KMEANS) return kmeans_tc_selected(k, d) ? CABS_PATH_TC : CABS_PATH_FFMA;
+  if (op == CABS_OP_KMEANS)
+    return kmeans_prune_selected(k, d) ? CABS_PATH_PRUNE : kmeans_tc_selected(k, d) ? CABS_PATH_TC : CABS_PATH_FFMA;
   if (op == CABS_OP_RESIDUAL) return (k >= 1 && k <= residual_tc_kmax() && !getenv("CABS_RESIDUAL_FFMA")) ? CABS_PATH_TC
                                                                                                          : CABS_PATH_FFMA;
   return -1;
@@ -414,9 +417,15 @@ struct KmSlot {
   int64_t* idx;
   void* scr;
   size_t scr_bytes;
+  float* ebuf;  // the snap distance buffer of the slot (free during the k-means)
+  size_t ebuf_bytes;
+  long long* qbuf;
 };
 static KmSlot km_slot(void* ws, const Ws& L, int q) {
   KmSlot k;
+  k.ebuf = wsp<float>(ws, q ? L.dist2 : L.dist);
+  k.qbuf = wsp<long long>(ws, L.km_q) + (size_t)q * L.Nmax;
+  k.ebuf_bytes = sizeof(float) * (size_t)L.K * (size_t)L.Nmax;
   k.w = wsp<float>(ws, L.km_w) + (size_t)q * L.Nmax;
   k.cnt = wsp<int>(ws, L.km_cnt) + 16 * q;
   k.bounds = reinterpret_cast<unsigned*>(k.cnt + 2);
@@ -452,6 +461,7 @@ static LloydJob km_job(const cabs_km_problem& p, const KmSlot& k) {
   j.centres = p.centres; j.ldc = p.ldc; j.labels = p.labels; j.objective = p.objective; j.near_ties = p.near_ties;
   j.cluster_w = p.cluster_w; j.scratch = k.scr; j.scratch_bytes = k.scr_bytes;
   j.tie_log = p.tie_log; j.tie_cap = p.tie_log_cap; j.row_off = p.row_off;
+  j.ebuf = k.ebuf; j.ebuf_bytes = k.ebuf_bytes; j.qbuf = k.qbuf;
   return j;
 }
 
@@ -522,6 +532,13 @@ int32_t cabs_kmeans(const cabs_plan* plan, const float* X, int64_t ldx, int64_t 
   CABS_TRY(km_prepare(p, weight_kind, weight_p, seed, k, comm, stream));
   if (km_persistent_allowed(comm) && n_loc > 0) {
     const LloydJob j = km_job(p, k);
+    if (kmeans_prune_selected(k2, d)) {
+      if (launch_lloyd_prune(&j, 1, iters, S(stream))) {
+        CABS_LAUNCH_CHECK("lloyd_prune");
+        return CABS_OK;
+      }
+      cudaGetLastError();
+    }
     if (kmeans_tc_selected(k2, d)) {
       if (launch_lloyd_tc(&j, 1, iters, S(stream))) {
         CABS_LAUNCH_CHECK("lloyd_tc");
@@ -586,6 +603,13 @@ int32_t cabs_kmeans_pair(const cabs_plan* plan, const cabs_km_problem* a, const 
   }
   if (km_persistent_allowed(comm) && a->n_loc > 0 && b->n_loc > 0) {
     const LloydJob j[2] = {km_job(*a, ka), km_job(*b, kb)};
+    if (kmeans_prune_selected(a->k2, a->d) && kmeans_prune_selected(b->k2, b->d)) {
+      if (launch_lloyd_prune(j, 2, iters, S(stream))) {
+        CABS_LAUNCH_CHECK("lloyd_prune");
+        return CABS_OK;
+      }
+      cudaGetLastError();
+    }
     if (kmeans_tc_selected(a->k2, a->d) && kmeans_tc_selected(b->k2, b->d)) {
       if (launch_lloyd_tc(j, 2, iters, S(stream))) {
         CABS_LAUNCH_CHECK("lloyd_tc");

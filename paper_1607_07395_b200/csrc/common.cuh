@@ -30,6 +30,7 @@ struct Ws {
   size_t norm_part, norms, scales;
   size_t km_w, km_scr, km_pobj, km_ptie, km_red, km_cnt;  // km_w, km_scr, km_cnt: two problems
   size_t km_scr_bytes;                                     // per problem
+  size_t km_q;                                             // lloyd_prune: w ||x||^2 per point (int64), two problems
   size_t dist, cand_d, cand_i, cand_all;  // snap scratch of problem slot 0 ...
   size_t dist2, cand_d2, cand_i2, cand_all2;  // ... and slot 1 (cabs_select_pair)
   size_t hcand, idx;
@@ -82,6 +83,7 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.km_pobj = take(sizeof(double) * kAssignGrid);
   w.km_ptie = take(sizeof(int) * kAssignGrid);
   w.km_red = take(sizeof(double) * 2 * (K * Kp + K + 2));  // two problems' payloads (fused pair)
+  w.km_q = take(sizeof(long long) * 2 * w.Nmax);
   w.km_cnt = take(sizeof(int) * 64);
   w.dist = take(sizeof(float) * K * w.Nmax);
   w.cand_d = take(sizeof(float) * K * kSnapTMulti);

@@ -98,12 +98,20 @@ struct LloydJob {
   int* tie_log;      // near-tie log or null (km_tile.cuh: km_log_tie)
   int tie_cap;
   int64_t row_off;   // global index of local point 0
+  float* ebuf;       // lloyd_prune: per-point per-centre bound buffer (N x round_up(k2, 4)) or null
+  size_t ebuf_bytes;
+  long long* qbuf;   // lloyd_prune: N int64 (w ||x||^2 in fixed point) or null
 };
 bool launch_lloyd_persistent(const LloydJob* jobs, int njobs, int iters, long long* prof, cudaStream_t st);
 // lloyd_tc.cu: the same loop with the distance cross-term on the tensor cores (d, k2 <= 128);
 // the jobs' near-tie logs as km_log_tie.  False -> not applicable.
 void ktc_debug_timeline(long long* out, int n);
 bool launch_lloyd_tc(const LloydJob* jobs, int njobs, int iters, cudaStream_t st);
+// lloyd_ex.cu: the same loop with the candidates pruned exactly by the triangle inequality
+// against the centre-centre distances (d, k2 <= 128, shared-memory plan permitting)
+bool kmeans_prune_selected(int k2, int d);
+bool launch_lloyd_prune(const LloydJob* jobs, int njobs, int iters, cudaStream_t st);
+void lex_debug_timeline(long long* out, int n);
 void lloyd_debug_timeline(long long* out, int n);
 void embed_debug_timeline(long long* out);
 void snap_debug_counters(long long* out);

@@ -606,3 +606,48 @@ def test_kmeans_tensor_core_and_ffma_paths_agree(dev, monkeypatch, N, d, k2, ncl
     assert np.array_equal(l1, l2), f"{np.count_nonzero(l1 != l2)} labels differ"
     assert np.array_equal(c1, c2) and np.array_equal(w1, w2) and np.array_equal(t1, t2)
     assert np.allclose(o1, o2, rtol=1e-12)
+
+
+@pytest.mark.parametrize("N,d,k2,ncl,iters,spread,wk", [
+    (50000, 100, 100, 64, 12, 0.02, C.WEIGHT_CONST),   # the c3 shape: tight clusters, more centres than clusters
+    (30000, 50, 50, 30, 20, 0.02, C.WEIGHT_CONST),     # c2 shape, long run (delta iterations)
+    (20000, 50, 50, 8, 15, 1.0, C.WEIGHT_CONST),       # diffuse clusters: many candidates and label changes
+    (7001, 33, 19, 30, 9, 0.02, C.WEIGHT_POWER),       # odd d, power weights
+    (12000, 96, 112, 90, 6, 0.05, C.WEIGHT_CONST),     # near the shared-memory limit
+    (3000, 20, 20, 10, 10, 0.02, C.WEIGHT_CONST),      # c1
+    (517, 7, 5, 4, 6, 0.02, C.WEIGHT_CONST),           # tiny, ragged
+    (4000, 128, 64, 40, 5, 0.3, C.WEIGHT_CONST)])      # the largest d
+def test_kmeans_pruned_and_ffma_paths_agree(dev, monkeypatch, N, d, k2, ncl, iters, spread, wk):
+    """The pruned Lloyd kernel (exact triangle-inequality candidates against the centre-centre
+    distances, full / delta int64 updates) and the FFMA kernel (direct differences against
+    every centre, full sums every iteration) take the same decisions: labels, exact-integer
+    centres, cluster weights, near-tie counts and the near-tie log bit for bit; the objective is
+    computed from the exact per-cluster sums (Q - 2 c.S + W |c|^2) instead of summing the FP32
+    distances, so the two agree to FP32 rounding."""
+    X = _clustered(N, d, ncl, N + d + k2, spread=spread)
+    ld = C.cabs_padded_ld(d)
+    Xt = torch.zeros((N, ld), device=dev); Xt[:, :d] = torch.from_numpy(X).to(dev)
+    plan = _plan(N, N, max(d, k2))
+    ws = _ws(plan, dev)
+    monkeypatch.setenv("CABS_KMEANS_PRUNE", "1")  # also below the k2 d >= 4096 selection threshold
+    assert C.cabs_kmeans_path(k2, d) == "prune"
+    outs = []
+    for ffma in ("", "1"):
+        if ffma:
+            monkeypatch.setenv("CABS_KMEANS_FFMA", "1")
+            assert C.cabs_kmeans_path(k2, d) == "ffma"
+        cen = torch.zeros((k2, ld), device=dev)
+        lab = torch.zeros(N, dtype=torch.int32, device=dev)
+        cw = torch.zeros(k2, dtype=torch.float64, device=dev)
+        obj = torch.zeros(iters, dtype=torch.float64, device=dev)
+        ties = torch.zeros(iters, dtype=torch.int32, device=dev)
+        tl = C.new_tie_log(4096, dev)
+        C.cabs_kmeans(plan, Xt, N, N, 0, d, k2, iters, wk, 2.0, 3, C.TAG_INIT_ROWS, cen, lab, cw, obj, ws,
+                      near_ties=ties, tie_log=tl)
+        outs.append([t.cpu().numpy() for t in (cen, lab, cw, obj, ties)] + [C.read_tie_log(tl)])
+    (c1, l1, w1, o1, t1, g1), (c2, l2, w2, o2, t2, g2) = outs
+    assert np.array_equal(l1, l2), f"{np.count_nonzero(l1 != l2)} labels differ"
+    assert np.array_equal(c1, c2) and np.array_equal(w1, w2) and np.array_equal(t1, t2)
+    assert np.allclose(o1, o2, rtol=1e-5)
+    # the near-tie logs: same (iteration, point, nearest, gap) entries and the same count
+    assert g1[1] == g2[1] and [e[:3] + (e[4],) for e in g1[0]] == [e[:3] + (e[4],) for e in g2[0]]
