@@ -13,7 +13,8 @@ reference leg may import this module.  It shares no code with the CUDA path.
 Parity status per function:
   gather, svd_w, sketch, embeddings, argmin_with_gap, lloyd, snap, residual, cabs_run,
   row_sq_norms, hard_threshold_select, hard_threshold_followup, orthogonalize,
-  leverage_scores, leverage_sample, RbfSource, residual_sampled: pinned (tests/test_oracle_*.py).
+  leverage_scores, leverage_sample, RbfSource, residual_sampled, CsrSource, residual_sparse:
+  pinned (tests/test_oracle_*.py).
 """
 from __future__ import annotations
 
@@ -78,9 +79,52 @@ class RbfSource:
         return np.exp(-d2 / (2.0 * self.sigma ** 2))
 
 
+class CsrSource:
+    """A sparse A (PAPER.md P:119 "For sparse matrices"; Table 1 P:301-302 sparsity column;
+    SPEC S:23-28 SparseMat) in compressed sparse row form: the nonzeros of row i are
+    data[indptr[i]:indptr[i+1]] at columns indices[indptr[i]:indptr[i+1]] (strictly increasing,
+    no duplicates).  Every other entry is 0."""
+
+    def __init__(self, indptr, indices, data, shape):
+        self.indptr = np.asarray(indptr, np.int64)
+        self.indices = np.asarray(indices, np.int64)
+        self.data = np.asarray(data, np.float64)
+        self.shape = (int(shape[0]), int(shape[1]))
+        m, n = self.shape
+        if self.indptr.shape != (m + 1,) or self.indptr[0] != 0 or np.any(np.diff(self.indptr) < 0):
+            raise ValueError("bad indptr")
+        if self.indices.size != self.indptr[-1] or self.data.size != self.indices.size:
+            raise ValueError("indptr / indices / data sizes disagree")
+        if self.indices.size and (self.indices.min() < 0 or self.indices.max() >= n):
+            raise IndexError("column index out of range")  # S:26
+        for i in range(m):
+            c = self.indices[self.indptr[i]:self.indptr[i + 1]]
+            if np.any(np.diff(c) <= 0):
+                raise ValueError("columns of a row must be strictly increasing (no duplicates)")  # S:26-27
+
+    @property
+    def nnz(self):
+        return int(self.indices.size)
+
+    def entries(self, I, J):
+        """A[I][:, J] as float64 by the definition: row i is zero except data at indices."""
+        I = np.asarray(I, np.int64)
+        J = np.asarray(J, np.int64)
+        out = np.zeros((I.size, J.size))
+        for a, i in enumerate(I):
+            row = np.zeros(self.shape[1])
+            lo, hi = self.indptr[i], self.indptr[i + 1]
+            row[self.indices[lo:hi]] = self.data[lo:hi]
+            out[a] = row[J]
+        return out
+
+    def dense(self):
+        return self.entries(np.arange(self.shape[0]), np.arange(self.shape[1]))
+
+
 def _block(A, I, J):
-    """A[I][:, J] as float64 for a dense array or an implicit source."""
-    if isinstance(A, RbfSource):
+    """A[I][:, J] as float64 for a dense array or an implicit / sparse source."""
+    if isinstance(A, (RbfSource, CsrSource)):
         return A.entries(I, J)
     return np.asarray(A[np.ix_(I, J)], dtype=np.float64)
 
@@ -447,6 +491,28 @@ def residual(A, F, G, s=None, block=2048):
     return r2, a2
 
 
+def residual_sparse(A, F, G, s=None):
+    """The P:313 error of a sparse A (CsrSource) without forming A - F diag(s) G^T:
+        ||A - B||_F^2 = ||A||_F^2 - 2 <A, B> + ||B||_F^2,   B = F S G^T, S = diag(s),
+    where <A, B> = sum over the nonzeros a_ij of a_ij (F S G^T)_ij and
+        ||B||_F^2 = trace(S F^T F S G^T G) = sum_kl (F^T F)_kl s_k s_l (G^T G)_kl
+    (the r x r Gram products).  Returns (r^2, a^2) like residual()."""
+    F = np.asarray(F, np.float64)
+    G = np.asarray(G, np.float64)
+    sv = np.ones(F.shape[1]) if s is None else np.asarray(s, np.float64)
+    a2 = float(np.sum(A.data * A.data))
+    cross = 0.0
+    for i in range(A.shape[0]):
+        lo, hi = A.indptr[i], A.indptr[i + 1]
+        if hi > lo:
+            b = G[A.indices[lo:hi]] @ (F[i] * sv)     # (F S G^T)_ij at the row's nonzero columns
+            cross += float(np.sum(A.data[lo:hi] * b))
+    gf = F.T @ F
+    gg = G.T @ G
+    b2 = float(np.sum(gf * np.outer(sv, sv) * gg))
+    return a2 - 2.0 * cross + b2, a2
+
+
 def residual_sampled(A, F, G, i, j, s=None, chunk=1 << 20, f_rows=None):
     """The P:313 error on a uniform subset of entries (BASELINE.json configs[4] "residual
     estimated on a seeded 1e9-entry uniform subset"; reading Z23: T i.i.d. positions (i_t, j_t)).
@@ -466,7 +532,12 @@ def residual_sampled(A, F, G, i, j, s=None, chunk=1 << 20, f_rows=None):
     for c in range(0, T, chunk):
         ic, jc = i[c:c + chunk], j[c:c + chunk]
         fc = ic if f_rows is None else np.asarray(f_rows, np.int64)[c:c + chunk]
-        a = A.at(ic, jc) if isinstance(A, RbfSource) else np.asarray(A[ic, jc], np.float64)
+        if isinstance(A, RbfSource):
+            a = A.at(ic, jc)
+        elif isinstance(A, CsrSource):
+            a = np.array([A.entries([x], [y])[0, 0] for x, y in zip(ic, jc)])
+        else:
+            a = np.asarray(A[ic, jc], np.float64)
         e = a - np.sum(F[fc] * G[jc], axis=1)
         r2 += float(np.sum(e * e))
         a2 += float(np.sum(a * a))
@@ -507,7 +578,7 @@ def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
              init_rows=None, init_cols=None, with_residual=True, followup="kmeans", n_samples=0):
     """Algorithm 2 plus the evaluation residual.  followup="hard" /
     "leverage" replaces step 3 by the paper's variant (f) / (e) of P:312 (km_* / snap_* are None).
-    A: dense array or RbfSource.  n_samples > 0: the residual is the sampled estimate on the
+    A: dense array, RbfSource or CsrSource.  n_samples > 0: the residual is the sampled estimate on the
     pairs rng.residual_pairs(seed, n_samples, m, n)."""
     m, n = A.shape
     if not (1 <= k1 <= min(m, n)) or not (1 <= k2 <= min(m, n)):

@@ -49,6 +49,17 @@ CONFIGS = {
                       "Gaussian mixture, sigma = median pairwise distance of 1e4 pairs (configs[4], Z23)"),
 }
 
+# the paper's sparse Table-1 shapes, synthetic sparse_lowrank stand-ins
+# (a rank-r Gaussian-factor product with all but a `density` fraction of entries zeroed)
+SPARSE_CONFIGS = {
+    "s1": Config("s1", 27000, 46000, 100, 100, 25, "sparse_lowrank",
+                 note="sparse_lowrank rank 20 at the movie-ratings shape and density 0.56% (Table 1, P:301)"),
+    "s2": Config("s2", 18774, 61188, 100, 100, 25, "sparse_lowrank",
+                 note="sparse_lowrank rank 20 at the newsgroup shape and density 0.22% (Table 1, P:302)"),
+}
+SPARSE_DENSITY = {"s1": 0.0056, "s2": 0.0022}
+SPARSE_RANK = 20
+
 RBF_DIM = 16
 RBF_COMPONENTS = 100
 RBF_SIGMA_PAIRS = 10000
@@ -186,3 +197,45 @@ def make_rbf(cfg: Config):
     h = RBF_SIGMA_PAIRS // 2
     sigma = float(0.5 * (ds[h - 1] + ds[h]))
     return x, y, sigma
+
+
+def make_sparse(cfg: Config, density: float, device="cpu", rank: int = SPARSE_RANK):
+    """sparse_lowrank(m, n, r, density, seed): positions drawn per 250-row chunk (row i gets
+    Binomial(n, density) uniform columns, duplicates merged), values (G1 G2^T)_ij / sqrt(r) of
+    Gaussian factors at those positions (float64 products rounded once to float32).  Returns CSR
+    (indptr int64[m+1], indices int32, values float32) on `device`, columns increasing per row."""
+    d, s = torch.device(device), cfg.seed
+    m, n = cfg.m, cfg.n
+    G2 = _randn((n, rank), d, s, 40)
+    rows_l, cols_l, vals_l = [], [], []
+    for c0 in range(0, m, CHUNK):
+        rows = min(CHUNK, m - c0)
+        ci = c0 // CHUNK
+        g = _gen(d, s, 41, ci)
+        cnt = torch.binomial(torch.full((rows,), float(n), dtype=torch.float64, device=d),
+                             torch.full((rows,), float(density), dtype=torch.float64, device=d), generator=g)
+        cnt = cnt.to(torch.int64)
+        r = torch.repeat_interleave(torch.arange(rows, device=d), cnt)
+        c = torch.randint(0, n, (int(cnt.sum()),), generator=g, device=d)
+        key = torch.unique(r * n + c)  # sorted: rows, then columns; duplicates merged
+        r, c = key // n, key % n
+        G1 = _randn((rows, rank), d, s, 42, ci)
+        v = (G1[r] * G2[c]).sum(1) / math.sqrt(rank)
+        rows_l.append(r + c0)
+        cols_l.append(c)
+        vals_l.append(v.to(torch.float32))
+    r = torch.cat(rows_l)
+    indptr = torch.zeros(m + 1, dtype=torch.int64, device=d)
+    indptr[1:] = torch.cumsum(torch.bincount(r, minlength=m), 0)
+    return indptr, torch.cat(cols_l).to(torch.int32), torch.cat(vals_l)
+
+
+def csr_to_csc(indptr, indices, values, n):
+    """The same matrix in compressed sparse column form (col_ptr int64[n+1], row_idx int32,
+    values float32), rows increasing per column: a stable sort of the nonzeros by column."""
+    m = indptr.numel() - 1
+    rows = torch.repeat_interleave(torch.arange(m, device=indptr.device), indptr[1:] - indptr[:-1])
+    order = torch.argsort(indices.to(torch.int64) * m + rows)
+    col_ptr = torch.zeros(n + 1, dtype=torch.int64, device=indptr.device)
+    col_ptr[1:] = torch.cumsum(torch.bincount(indices.to(torch.int64), minlength=n), 0)
+    return col_ptr, rows[order].to(torch.int32), values[order]
