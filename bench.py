@@ -32,12 +32,31 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from workloads import CHUNK, CONFIGS, Generator, make_rbf  # noqa: E402
+from workloads import (CHUNK, CONFIGS, SPARSE_CONFIGS, SPARSE_DENSITY, Generator, csr_to_csc,  # noqa: E402
+                       make_rbf, make_sparse)
 
 METRIC = "CABS sketch wall time & k-means pts/s at 1/2/4/8 GPU; HBM GB/s vs peak"
 UNIT = "rows+cols/s"
 BASE_CFG = {1: "c3"}  # BASELINE.json configs[2]: the largest single-GPU configuration
 CFG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
+ALL_CONFIGS = {**CONFIGS, **SPARSE_CONFIGS}
+
+
+def workload_name(cfg):
+    if cfg.name in CFG_INDEX:
+        return f"{cfg.name} = BASELINE.json configs[{CFG_INDEX[cfg.name]}]: {cfg.note}"
+    return f"{cfg.name} = SURVEY NEXT-3 sparse source (not a BASELINE config): {cfg.note}"
+
+
+def sparse_block(cfg, r0, r1, dev):
+    """The sparse_lowrank matrix of a sparse config (built on the device) -> this rank's rows
+    [r0, r1) as CSR + CSC device tensors (library input, not part of the timed step)."""
+    ip, ix, v = make_sparse(cfg, SPARSE_DENSITY[cfg.name], device=dev)
+    lo, hi = int(ip[r0]), int(ip[r1])
+    bip = (ip[r0:r1 + 1] - lo).contiguous()
+    bix, bv = ix[lo:hi].contiguous(), v[lo:hi].contiguous()
+    cp, ri, cv = csr_to_csc(bip, bix, bv, cfg.n)
+    return (bip, bix, bv, cp, ri, cv), (ip, ix, v)
 C5_SAMPLES = 10 ** 9     # BASELINE.json configs[4]: "residual estimated on a seeded 1e9-entry uniform subset"
 ORACLE_RBF_SAMPLES = 1 << 20  # the oracle's bounded c5 sample: pairs of its leading block
 
@@ -152,7 +171,7 @@ def oracle_sample(cfg):
     """The bounded sample of a config the oracle is timed on (10-30 s of host CPU per step):
     the leading ms x ns block of the same matrix, same k1, k2 and Lloyd iterations."""
     ms, ns = {"c1": (2000, 1500), "c2": (8000, 4000), "c3": (6000, 3000), "c4": (6000, 3000),
-              "c5": (6000, 4000)}[cfg.name]
+              "c5": (6000, 4000), "s1": (6000, 9000), "s2": (5000, 12000)}[cfg.name]
     return min(ms, cfg.m), min(ns, cfg.n)
 
 
@@ -163,7 +182,21 @@ def oracle_source(cfg, ms, ns):
     if cfg.kind == "rbf_mixture":
         x, y, sigma = make_rbf(cfg)
         return O.RbfSource(x[:ms].numpy(), y[:ns].numpy(), sigma), ORACLE_RBF_SAMPLES
+    if cfg.kind == "sparse_lowrank":
+        return oracle_sparse_block(make_sparse(cfg, SPARSE_DENSITY[cfg.name]), ms, ns), 0
     return Generator(cfg, device="cpu").rows(0, ms)[:, :ns].numpy().copy(), 0
+
+
+def oracle_sparse_block(csr, ms, ns):
+    """The leading ms x ns block of a CSR matrix as the oracle's CsrSource."""
+    from oracle import cabs as O
+    ip, ix, v = (t.cpu().numpy() for t in csr)
+    rows = np.repeat(np.arange(ms), np.diff(ip[:ms + 1]))
+    sel = ix[:ip[ms]] < ns
+    r, c, val = rows[sel], ix[:ip[ms]][sel], v[:ip[ms]][sel]
+    bip = np.zeros(ms + 1, np.int64)
+    bip[1:] = np.cumsum(np.bincount(r, minlength=ms))
+    return O.CsrSource(bip, c, val, (ms, ns))
 
 
 def run_reference(args, cfg):
@@ -176,14 +209,15 @@ def run_reference(args, cfg):
     cores = len(os.sched_getaffinity(0))
     ms, ns = oracle_sample(cfg)
     A, T = oracle_source(cfg, ms, ns)
+    wk = O.WEIGHT_POWER if cfg.kind == "sparse_lowrank" else O.WEIGHT_CONST
     k1, k2 = min(cfg.k1, ms, ns), min(cfg.k2, ms, ns)
     times = []
     for i in range(args.warmup + args.steps):
         if i < args.warmup:  # warm-up: a small run (page-in, BLAS init)
-            O.cabs_run(A, min(k1, 20), min(k2, 20), 2, seed=cfg.seed, n_samples=min(T, 4096))
+            O.cabs_run(A, min(k1, 20), min(k2, 20), 2, seed=cfg.seed, n_samples=min(T, 4096), weight_kind=wk)
             continue
         t0 = time.perf_counter()
-        O.cabs_run(A, k1, k2, cfg.iters, seed=cfg.seed, n_samples=T)
+        O.cabs_run(A, k1, k2, cfg.iters, seed=cfg.seed, n_samples=T, weight_kind=wk)
         times.append(time.perf_counter() - t0)
     t = statistics.mean(times)
     v = (ms + ns) / t
@@ -193,7 +227,7 @@ def run_reference(args, cfg):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name} = BASELINE.json configs[{CFG_INDEX[cfg.name]}]: {cfg.note}",
+            "config": {"workload": workload_name(cfg),
                        "m": cfg.m, "n": cfg.n, "k1": cfg.k1, "k2": cfg.k2, "iters": cfg.iters},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -206,13 +240,14 @@ def oracle_cpu_baseline(cfg, A_host):
     from oracle import cabs as O
     cores = len(os.sched_getaffinity(0))
     ms, ns = oracle_sample(cfg)
-    if A_host is None:  # implicit source
+    if A_host is None:  # implicit or sparse source
         A, T = oracle_source(cfg, ms, ns)
     else:
         A, T = np.ascontiguousarray(A_host[:ms, :ns]), 0
     k1, k2 = min(cfg.k1, ms, ns), min(cfg.k2, ms, ns)
+    wk = O.WEIGHT_POWER if cfg.kind == "sparse_lowrank" else O.WEIGHT_CONST
     t0 = time.perf_counter()
-    O.cabs_run(A, k1, k2, cfg.iters, seed=cfg.seed, n_samples=T)
+    O.cabs_run(A, k1, k2, cfg.iters, seed=cfg.seed, n_samples=T, weight_kind=wk)
     t = time.perf_counter() - t0
     return {"value": (ms + ns) / t, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"leading {ms} x {ns} block of {cfg.name} (k1={k1}, k2={k2}, {cfg.iters} Lloyd iterations"
@@ -386,12 +421,47 @@ def parity_block_rbf(cfg, x, y, sigma, pipe, res, plan, dev, sample=2048, pairs=
 
 
 # ---------------------------------------------------------------------- our arm
+def parity_block_sparse(cfg, csr, pipe, res):
+    """Full-size sparse parity against the FP64 oracle's CsrSource of the SAME
+    matrix: S1 indices bit-exact; S2/S3 the gathered R and W bit-exact, a sample of C's rows bit-
+    exact; S10 the oracle's split residual (residual_sparse) on the GPU's follow-up factors vs the
+    GPU's (1e-6 of ||A||^2 + ||F S G^T||^2).  The whole pipeline is compared with the oracle at
+    reduced sizes in tests/test_gpu_sparse.py."""
+    from oracle import cabs as O
+    from oracle import rng
+    t0 = time.perf_counter()
+    ip, ix, v = (t.cpu().numpy() for t in csr)
+    osrc = O.CsrSource(ip, ix, v, (cfg.m, cfg.n))
+    out = {"kind": "full-size sparse, per-step checks (oracle CsrSource of the same nonzeros)"}
+    I = rng.floyd(cfg.m, cfg.k1, cfg.seed, rng.TAG_PILOT_ROWS)
+    J = rng.floyd(cfg.n, cfg.k1, cfg.seed, rng.TAG_PILOT_COLS)
+    out["S1_pilot_indices_exact"] = bool(np.array_equal(res["I"].numpy(), I) and np.array_equal(res["J"].numpy(), J))
+    Rg = res["R"].numpy()[:, :cfg.n]
+    Wg = res["W"].numpy()[:, :cfg.k1]
+    rows = np.arange(0, cfg.m, max(1, cfg.m // 2048))
+    Cg = res["C"].numpy()[rows][:, :cfg.k1]
+    out["S2_S3_gathers_exact"] = bool(np.array_equal(Rg, osrc.entries(I, np.arange(cfg.n)))
+                                      and np.array_equal(Wg, osrc.entries(I, J))
+                                      and np.array_equal(Cg, osrc.entries(rows, J)))
+    r2 = res["r2"]
+    U, V, s = res["U"].numpy()[:, :r2], res["V"].numpy()[:, :r2], res["s2"].numpy()[:r2]
+    rr, ra = O.residual_sparse(osrc, U, V, s)
+    b2 = float(np.sum((U.astype(np.float64).T @ U) * np.outer(s, s) * (V.astype(np.float64).T @ V)))
+    out["S10"] = {"gpu_resid_sq": res["resid_sq"], "oracle_resid_sq": rr, "gpu_a_sq": res["a_sq"], "oracle_a_sq": ra,
+                  "ok": bool(abs(res["resid_sq"] - rr) <= 1e-6 * (ra + b2) and abs(res["a_sq"] - ra) <= 1e-9 * ra)}
+    out["ok"] = bool(out["S1_pilot_indices_exact"] and out["S2_S3_gathers_exact"] and out["S10"]["ok"])
+    out["oracle_s"] = time.perf_counter() - t0
+    return out
+
+
 def time_variant(args, cfg, A, plan, rank, world, comm, flush, stream, followup, desc):
     """One of the paper's follow-up variants on the same matrix, timed like the main step."""
     from paper_1607_07395_b200.pipeline import CabsConfig, CabsPipeline
     samples = C5_SAMPLES if cfg.kind == "rbf_mixture" else 0
+    wk = 1 if cfg.kind == "sparse_lowrank" else 0  # WEIGHT_POWER for sparse inputs
     vp = CabsPipeline(A, cfg.m, cfg.n, CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, followup=followup,
-                                                  residual_samples=samples), rank, world, comm=comm, plan=plan)
+                                                  residual_samples=samples, weight_kind=wk), rank, world, comm=comm,
+                      plan=plan)
     for _ in range(args.warmup):
         vp.run()
     per = {}
@@ -442,7 +512,7 @@ def main():
     ap.add_argument("--no-variants", action="store_true", help="skip the variant (f) timing")
     ap.add_argument("--eager", action="store_true", help="time stream-ordered launches instead of the CUDA graph")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = ALL_CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -456,9 +526,13 @@ def main():
     C.load()
     plan = make_plan(cfg.m, cfg.n, max(cfg.k1, cfg.k2), rank, world, align=CHUNK)
     rbf = cfg.kind == "rbf_mixture"
+    sparse = cfg.kind == "sparse_lowrank"
     if rbf:  # implicit source: the points on every rank, entries generated on access
         xh, yh, sigma = make_rbf(cfg)
         A = C.RbfSource(xh.to(dev), yh.to(dev), sigma)
+    elif sparse:  # this rank's row block as CSR + CSC
+        sp_arrays, sp_full = sparse_block(cfg, plan.row_begin, plan.row_end, dev)
+        A = C.CsrSource(*sp_arrays, cfg.n)
     else:
         gen = Generator(cfg, device=dev)
         A = gen.rows(plan.row_begin, plan.row_end)
@@ -466,7 +540,10 @@ def main():
     torch.cuda.empty_cache()
     comm = TorchComm(dev) if world > 1 else None
     samples = C5_SAMPLES if rbf else 0
-    ccfg = CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, residual_samples=samples)
+    # sparse inputs: the power weighting Upsilon(x) = x^2 ("a fast-growing function for sparse
+    # matrices"; SPEC default p = 2), constant for dense
+    wk = C.WEIGHT_POWER if sparse else C.WEIGHT_CONST
+    ccfg = CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, residual_samples=samples, weight_kind=wk)
     pipe = CabsPipeline(A, cfg.m, cfg.n, ccfg, rank, world, comm=comm, plan=plan)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
@@ -525,6 +602,8 @@ def main():
     if not args.no_e2e:
         if rbf:  # the inputs are the points x, y
             ins = [(A.x, xh.pin_memory()), (A.y, yh.pin_memory())]
+        elif sparse:  # the CSR and CSC arrays
+            ins = [(t, t.cpu().pin_memory()) for t in sp_arrays]
         else:
             A_host = A.cpu().pin_memory()
             ins = [(A, A_host)]
@@ -607,6 +686,10 @@ def main():
     if rbf:  # sampled: two random factor rows per owned pair; entries generated
         res_bytes = 4.0 * 2 * r2n * samples * (m_loc / cfg.m)
         res_kernel = "residual_sampled_kernel (Philox pairs, generated entries, warp dot of random factor rows)"
+    elif sparse:  # the nonzeros once (value + column index), the row pointers, F and G once
+        res_bytes = 8.0 * A.nnz + 8.0 * (m_loc + 1) + 4.0 * r2n * (m_loc + 2 * cfg.n)
+        res_kernel = ("sparse_res_nnz_kernel + orth_gram (cabs_residual on a CSR source: nonzeros + the r x r "
+                      "Gram products, A - F S G^T never formed)")
     else:
         res_bytes = 4.0 * (m_loc * cfg.n + m_loc * cfg.k2 + cfg.n * cfg.k2)
         res_tc = C.cabs_residual_path(r2n) == "tc"
@@ -627,13 +710,15 @@ def main():
     a_gb = cfg.m * cfg.n * 4 / 1e9
     l2_note = (f"flushed (256 MiB write) before every timed step; implicit A, {samples:.0e} sampled entries read "
                f"{4.0 * 2 * r2n * samples / 1e12:.1f} TB of random factor rows (> L2)" if rbf else
+               f"flushed (256 MiB write) before every timed step; sparse A, {A.nnz} nonzeros "
+               f"({A.nnz / (cfg.m * cfg.n):.4%}), CSR + CSC {16.0 * A.nnz / 1e9:.2f} GB" if sparse else
                f"flushed (256 MiB write) before every timed step; A ({a_gb:.1f} GB) > L2")
     line = {
         "metric": METRIC, "value": (cfg.m + cfg.n) / (ms / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} = BASELINE.json configs[{CFG_INDEX[cfg.name]}]: {cfg.note}",
-                   "m": cfg.m, "n": cfg.n,
+        "config": {"workload": workload_name(cfg),
+                   "m": cfg.m, "n": cfg.n, "weights": "power 2" if sparse else "const",
                    "k1": cfg.k1, "k2": cfg.k2, "iters": cfg.iters, "mode": "stabilized", "parallelism": f"rows{world}",
                    "l2": l2_note, "residual_samples": samples or "exact",
                    "timing": "per-step CUDA events on the launching stream, barrier+sync both sides, max over ranks",
@@ -657,6 +742,10 @@ def main():
             A_np = None
             if not args.no_parity:
                 line["parity"] = parity_block_rbf(cfg, xh, yh, sigma, pipe, res, plan, dev)
+        elif sparse:
+            A_np = None
+            if not args.no_parity:
+                line["parity"] = parity_block_sparse(cfg, sp_full, pipe, res)
         else:
             A_np = A_host.numpy() if A_host is not None else A.cpu().numpy()
             if not args.no_parity:

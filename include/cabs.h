@@ -101,9 +101,17 @@ typedef struct cabs_plan {
  *   differences summed over the d coordinates in order, exp via ex2.approx) -- PAPER.md P:24
  *   "never knowing the remaining entries".  x: device, ALL m points (m x ldx, replicated on
  *   every rank); y: device, all n points (n x ldy); 1 <= d <= 64; inv_two_sigma2 = 1/(2 sigma^2) > 0.
- *   No gather crosses ranks; cabs_residual needs n_samples > 0 for this kind. */
+ *   No gather crosses ranks; cabs_residual needs n_samples > 0 for this kind.
+ * CABS_SOURCE_CSR_F32: a sparse A ("For sparse matrices", Table 1
+ *   P:301-302): the rank's row block in CSR (row gathers, W) and in CSC (column gathers), both
+ *   supplied by the caller (the library does not convert).  Entries not stored are 0; gathers
+ *   are exact copies, identical to the dense gathers of the densified matrix.  Rows sampled on
+ *   other ranks arrive through the allreduce, as for a dense source.  cabs_residual (exact)
+ *   evaluates ||A||^2 - 2 sum_nnz a_ij (F S G^T)_ij + sum_kl (F^T F)_kl s_k s_l (G^T G)_kl
+ *   (ncomp <= 512) without forming A - F S G^T; no index or value checks beyond the dims. */
 #define CABS_SOURCE_DENSE_F32 0
 #define CABS_SOURCE_RBF_F32 1
+#define CABS_SOURCE_CSR_F32 2
 typedef struct cabs_source {
   const float* a;         /* dense: device, (row_end - row_begin) x n, row-major */
   int64_t lda;            /* dense: >= n */
@@ -113,6 +121,13 @@ typedef struct cabs_source {
   const float* y;         /* RBF: n x ldy */
   int64_t ldx, ldy;       /* RBF: >= d */
   float inv_two_sigma2;   /* RBF */
+  /* CSR: the rank's row block twice, device arrays (row indices local to the block) */
+  const int64_t* row_ptr; /* CSR: int64[m_loc + 1], row_ptr[0] = 0 */
+  const int32_t* col_idx; /* CSR: int32[nnz], strictly increasing within a row */
+  const float* row_val;   /* CSR: float[nnz] */
+  const int64_t* col_ptr; /* CSC of the same block: int64[n + 1] */
+  const int32_t* row_idx; /* CSC: int32[nnz], local rows, strictly increasing within a column */
+  const float* col_val;   /* CSC: float[nnz] */
 } cabs_source;
 
 /* Collectives supplied by the caller (host struct).  Each callback sums `count`

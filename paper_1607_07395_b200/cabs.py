@@ -60,11 +60,14 @@ class Plan(ctypes.Structure):
 
 SOURCE_DENSE_F32 = 0
 SOURCE_RBF_F32 = 1
+SOURCE_CSR_F32 = 2
 
 
 class Source(ctypes.Structure):
     _fields_ = [("a", c_vp), ("lda", c_i64), ("kind", c_i32), ("d", c_i32), ("x", c_vp), ("y", c_vp),
-                ("ldx", c_i64), ("ldy", c_i64), ("inv_two_sigma2", c_f32)]
+                ("ldx", c_i64), ("ldy", c_i64), ("inv_two_sigma2", c_f32),
+                ("row_ptr", c_vp), ("col_idx", c_vp), ("row_val", c_vp), ("col_ptr", c_vp),
+                ("row_idx", c_vp), ("col_val", c_vp)]
 
 
 class RbfSource:
@@ -81,8 +84,31 @@ class RbfSource:
         self.device = x.device
 
 
+class CsrSource:
+    """A sparse row block (cabs.h CABS_SOURCE_CSR_F32): CSR (row_ptr int64[m_loc+1],
+    col_idx int32, row_val float32) and CSC of the same block (col_ptr int64[n+1], row_idx int32 local
+    rows, col_val float32), device tensors that must outlive the calls.  shape = (m_loc, n)."""
+
+    def __init__(self, row_ptr, col_idx, row_val, col_ptr, row_idx, col_val, n):
+        for t, dt in ((row_ptr, torch.int64), (col_idx, torch.int32), (row_val, torch.float32),
+                      (col_ptr, torch.int64), (row_idx, torch.int32), (col_val, torch.float32)):
+            if t.dtype != dt or not t.is_contiguous():
+                raise TypeError("CsrSource: int64 pointers, int32 indices, float32 values, contiguous")
+        self.row_ptr, self.col_idx, self.row_val = row_ptr, col_idx, row_val
+        self.col_ptr, self.row_idx, self.col_val = col_ptr, row_idx, col_val
+        self.shape = (row_ptr.numel() - 1, int(n))
+        self.device = row_ptr.device
+
+    @property
+    def nnz(self):
+        return int(self.col_idx.numel())
+
+
 def _source(A):
-    """cabs_source for a dense row block (a torch tensor) or an RbfSource."""
+    """cabs_source for a dense row block (a torch tensor), an RbfSource or a CsrSource."""
+    if isinstance(A, CsrSource):
+        return Source(None, 0, SOURCE_CSR_F32, 0, None, None, 0, 0, 0.0, A.row_ptr.data_ptr(), A.col_idx.data_ptr(),
+                      A.row_val.data_ptr(), A.col_ptr.data_ptr(), A.row_idx.data_ptr(), A.col_val.data_ptr())
     if isinstance(A, RbfSource):
         return Source(None, 0, SOURCE_RBF_F32, A.x.shape[1], A.x.data_ptr(), A.y.data_ptr(), A.x.stride(0),
                       A.y.stride(0), A.inv_two_sigma2)

@@ -191,6 +191,10 @@ static int32_t side_stream(SideStream** out) {
 
 // ---------------------------------------------------------------- sources
 static bool is_rbf(const cabs_source* s) { return s->kind == CABS_SOURCE_RBF_F32; }
+static bool is_csr(const cabs_source* s) { return s->kind == CABS_SOURCE_CSR_F32; }
+static CsrSrc csr_of(const cabs_source* s) {
+  return CsrSrc{s->row_ptr, s->col_idx, s->row_val, s->col_ptr, s->row_idx, s->col_val};
+}
 static RbfSrc rbf_of(const cabs_source* s) {
   return RbfSrc{s->x, s->y, s->ldx, s->ldy, s->d, s->inv_two_sigma2};
 }
@@ -206,6 +210,11 @@ static int32_t check_source(const cabs_plan& p, const cabs_source* src, const ch
       return arg_error(what);
     return CABS_OK;
   }
+  if (src->kind == CABS_SOURCE_CSR_F32) {
+    if (!src->row_ptr || !src->col_ptr || p.n >= 0x7FFFFFFFll || p.row_end - p.row_begin >= 0x7FFFFFFFll)
+      return arg_error(what);
+    return CABS_OK;
+  }
   return arg_error(what);
 }
 // C = A(rows of this rank, J)
@@ -213,6 +222,7 @@ static void src_cols(const cabs_plan& p, const cabs_source* src, const int64_t* 
                      void* ws, cudaStream_t st) {
   const int64_t m_loc = p.row_end - p.row_begin;
   if (is_rbf(src)) launch_rbf_cols(rbf_of(src), p.row_begin, m_loc, J, k, C, ldc, st);
+  else if (is_csr(src)) launch_csc_cols(csr_of(src), m_loc, p.n, J, k, C, ldc, st);
   else launch_gather_cols(src->a, src->lda, m_loc, p.n, J, k, C, ldc, ws, st);
 }
 // R = A(I, :): dense -- the rows this rank owns (others: completed by the caller's allreduce);
@@ -220,12 +230,14 @@ static void src_cols(const cabs_plan& p, const cabs_source* src, const int64_t* 
 static void src_rows(const cabs_plan& p, const cabs_source* src, const int64_t* I, int k, float* R, int64_t ldr,
                      void* ws, cudaStream_t st) {
   if (is_rbf(src)) launch_rbf_rows(rbf_of(src), I, k, p.n, R, ldr, st);
+  else if (is_csr(src)) launch_csr_rows(csr_of(src), p.row_begin, p.row_end, I, k, p.n, R, ldr, st);
   else launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, I, k, p.n, R, ldr, ws, st);
 }
 // W = A(I, J) straight from the source (single rank, or implicit)
 static void src_w(const cabs_plan& p, const cabs_source* src, const int64_t* I, const int64_t* J, int k, float* W,
                   int64_t ldw, cudaStream_t st) {
   if (is_rbf(src)) launch_rbf_w(rbf_of(src), I, J, k, W, ldw, st);
+  else if (is_csr(src)) launch_csr_w(csr_of(src), p.row_begin, p.row_end, I, J, k, W, ldw, st);
   else launch_gather_w_direct(src->a, src->lda, p.row_begin, p.row_end - p.row_begin, p.n, I, J, k, W, ldw, st);
 }
 // rows of R are exchanged only for a dense source on several ranks
@@ -937,6 +949,7 @@ int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float
   if (!F || !G || !out || ncomp < 0 || ncomp > CABS_KMAX || ldf < ncomp || ldg < ncomp || n_samples < 0)
     return arg_error("residual: bad arguments");
   const int64_t m_loc = p.row_end - p.row_begin;
+  if (n_samples > 0 && is_csr(src)) return arg_error("residual: the sampled estimate needs a dense or implicit source");
   if (n_samples > 0) {  // the sampled estimate (readings Z17 / Z23)
     if (p.m > (1ll << 32) || p.n > (1ll << 32)) return arg_error("residual: sampled dims must be <= 2^32");
     SampArgs a{};
@@ -955,6 +968,17 @@ int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float
     return CABS_OK;
   }
   if (is_rbf(src)) return arg_error("residual: the implicit source needs n_samples > 0");
+  if (is_csr(src)) {
+    if (!sparse_residual_supported(ncomp)) return arg_error("residual: sparse source needs ncomp <= 512");
+    cabsk::OrthArgs ga{};
+    ga.part = wsp<double>(ws, L.orth_part);
+    ga.gram = reinterpret_cast<double*>(static_cast<unsigned char*>(ws) + L.orth);
+    launch_residual_sparse(csr_of(src), m_loc, p.n, F, ldf, s, G, ldg, ncomp, ga, wsp<double>(ws, L.res_part), out,
+                           S(stream));
+    CABS_LAUNCH_CHECK("residual_sparse");
+    CABS_TRY(comm_f64(comm, out, 2, stream));
+    return CABS_OK;
+  }
   if (residual_tc_supported(src->a, src->lda, m_loc, p.n, ncomp)) {
     if (launch_residual_tc(src->a, src->lda, m_loc, p.n, F, ldf, s, G, ldg, ncomp, wsp<float>(ws, L.res_split),
                            wsp<double>(ws, L.res_part), out, S(stream)) != 0) {

@@ -186,6 +186,26 @@ void launch_orth_gram(OrthArgs& a, cudaStream_t st);
 void launch_orth_core(const OrthArgs& a, void* ws, cudaStream_t st);
 void launch_orth_finish(const OrthArgs& a, cudaStream_t st);
 
+// sparse.cu -- CSR / CSC source (cabs.h CABS_SOURCE_CSR_F32), this rank's row block
+struct CsrSrc {
+  const int64_t* row_ptr;  // m_loc + 1
+  const int32_t* col_idx;
+  const float* row_val;
+  const int64_t* col_ptr;  // n + 1
+  const int32_t* row_idx;  // local row indices
+  const float* col_val;
+};
+void launch_csr_rows(const CsrSrc& a, int64_t row_begin, int64_t row_end, const int64_t* I, int k, int64_t n, float* R,
+                     int64_t ldr, cudaStream_t st);
+void launch_csc_cols(const CsrSrc& a, int64_t m_loc, int64_t n, const int64_t* J, int k, float* C, int64_t ldc,
+                     cudaStream_t st);
+void launch_csr_w(const CsrSrc& a, int64_t row_begin, int64_t row_end, const int64_t* I, const int64_t* J, int k,
+                  float* W, int64_t ldw, cudaStream_t st);
+bool sparse_residual_supported(int ncomp);
+void launch_residual_sparse(const CsrSrc& a, int64_t m_loc, int64_t n, const float* F, int64_t ldf, const float* s,
+                            const float* G, int64_t ldg, int ncomp, OrthArgs& ga, double* part, double* out,
+                            cudaStream_t st);
+
 // residual.cu
 int launch_residual(const float* A, int64_t lda, int64_t m_loc, int64_t n, const float* F, int64_t ldf, const float* s,
                     const float* G, int64_t ldg, int ncomp, double* part, double* out, cudaStream_t st);
