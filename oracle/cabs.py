@@ -13,8 +13,9 @@ reference leg may import this module.  It shares no code with the CUDA path.
 Parity status per function:
   gather, svd_w, sketch, embeddings, argmin_with_gap, lloyd, snap, residual, cabs_run,
   row_sq_norms, hard_threshold_select, hard_threshold_followup, orthogonalize,
-  leverage_scores, leverage_sample, RbfSource, residual_sampled, CsrSource, residual_sparse:
-  pinned (tests/test_oracle_*.py).
+  leverage_scores, leverage_sample, RbfSource, residual_sampled, CsrSource, residual_sparse,
+  pinv, br_cur, sketch_cur, holdout_indices, holdout_errors, validate_rank: pinned
+  (tests/test_oracle_*.py).
 """
 from __future__ import annotations
 
@@ -630,6 +631,91 @@ def cabs_run(A, k1, k2, iters, seed=0, mode=STABILIZED, tol=DEFAULT_TOL,
     if with_residual:
         res.resid_sq, res.a_sq = _evaluate(A, follow, seed, n_samples)
     return res
+
+
+# --------------------------------------------------------------------------
+# the baselines of Section 2.2 on the same gathers -- BR-CUR (Algorithm 1,
+# P:83-103), Sketch-CUR (target rate 3x the base rate P:312 (a)) -- and the rank sweep
+# on a validation set ("use a validation set to choose the optimal number of
+# singular vectors")
+# --------------------------------------------------------------------------
+def pinv(X, tol=DEFAULT_TOL):
+    """Moore-Penrose pseudo-inverse by the thin SVD, singular values <= tol * sigma_1 dropped
+    (the truncation rule of the sketching routine)."""
+    X = np.asarray(X, np.float64)
+    U, sig, Vt = np.linalg.svd(X, full_matrices=False)
+    if sig.size == 0 or sig[0] == 0.0:
+        return np.zeros(X.T.shape)
+    r = int(np.sum(sig > tol * sig[0]))
+    return (Vt[:r].T / sig[:r]) @ U[:, :r].T
+
+
+@dataclass
+class CurResult:
+    C: np.ndarray   # m x k1 = A[:, base cols]
+    U: np.ndarray   # k1 x k1 middle matrix U*
+    R: np.ndarray   # k1 x n = A[base rows, :]
+
+    def dense(self):
+        return self.C @ self.U @ self.R
+
+
+def br_cur(A, Ibr, Ibc, Itr, Itc, tol=DEFAULT_TOL):
+    """Algorithm 1 step by step: 1 C = A[:, I^b_c], R = A[I^b_r, :]; 2 C_bar =
+    C[I^t_r, :], R_bar = R[:, I^t_c]; 3 M = A[I^t_r, I^t_c]; 4 U* = argmin ||M - C_bar U R_bar||_F
+    = C_bar^+ M R_bar^+ (the minimum-norm least-squares solution); 5 A ~ C U* R."""
+    m, n = A.shape
+    Ibr, Ibc = check_indices(Ibr, m, "base row"), check_indices(Ibc, n, "base column")
+    Itr, Itc = check_indices(Itr, m, "target row"), check_indices(Itc, n, "target column")
+    if Itr.size == 0 or Itc.size == 0:
+        raise ValueError("empty target sampling: M undefined")  # S:257
+    C = _block(A, np.arange(m), Ibc)
+    R = _block(A, Ibr, np.arange(n))
+    Cb = C[Itr, :]
+    Rb = R[:, Itc]
+    M = _block(A, Itr, Itc)
+    U = pinv(Cb, tol) @ M @ pinv(Rb, tol)
+    return CurResult(C=C, U=U, R=R)
+
+
+def sketch_cur(A, Ibr, Ibc, mult, seed, tol=DEFAULT_TOL):
+    """Sketch-CUR: BR-CUR with target rows / columns drawn uniformly and
+    independently of the base sampling (Floyd, tags TAG_TARGET_ROWS / _COLS), mult times as many
+    (P:312 (a): "the target sampling rate is chosen three times as much as the base")."""
+    m, n = A.shape
+    kt = mult * len(Ibr)
+    if kt > min(m, n):
+        raise ValueError("target sample larger than the matrix")  # S:261
+    Itr = rng.floyd(m, kt, seed, rng.TAG_TARGET_ROWS)
+    Itc = rng.floyd(n, kt, seed, rng.TAG_TARGET_COLS)
+    return br_cur(A, Ibr, Ibc, Itr, Itc, tol), Itr, Itc
+
+
+def holdout_indices(N, h, seed, tag, exclude):
+    """A validation sample: h uniform indices (Floyd, tag) less those in `exclude`
+    (the sketch's own rows or columns), ascending."""
+    idx = rng.floyd(N, h, seed, tag)
+    return idx[~np.isin(idx, np.asarray(exclude, np.int64))]
+
+
+def holdout_errors(A, U, s, V, Hr, Hc):
+    """The rank sweep on the validation block ("approximation error varies with the
+    number of singular vectors used"): e[rho] = ||A[Hr, Hc] - U[Hr, :rho] diag(s[:rho])
+    V[Hc, :rho]^T||_F^2 for rho = 0 .. r, by the definition (FP64)."""
+    B = _block(A, np.asarray(Hr, np.int64), np.asarray(Hc, np.int64))
+    Uh = np.asarray(U, np.float64)[np.asarray(Hr, np.int64)]
+    Vh = np.asarray(V, np.float64)[np.asarray(Hc, np.int64)]
+    sv = np.asarray(s, np.float64)
+    r = sv.size
+    return np.array([float(np.sum((B - (Uh[:, :rho] * sv[:rho]) @ Vh[:, :rho].T) ** 2)) for rho in range(r + 1)])
+
+
+def validate_rank(errors):
+    """the rank rho in 1..r with the smallest validation error, lowest on ties."""
+    e = np.asarray(errors, np.float64)
+    if e.size < 2:
+        raise ValueError("empty sweep")
+    return int(np.argmin(e[1:])) + 1
 
 
 def _evaluate(A, follow, seed, n_samples):

@@ -32,6 +32,10 @@ TAG_INIT_COLS = 4
 TAG_RESIDUAL_PAIRS = 5
 TAG_LEVERAGE_ROWS = 6
 TAG_LEVERAGE_COLS = 7
+TAG_TARGET_ROWS = 8    # Sketch-CUR target sampling
+TAG_TARGET_COLS = 9
+TAG_HOLDOUT_ROWS = 10  # validation block of the rank sweep
+TAG_HOLDOUT_COLS = 11
 
 
 def philox4x32_10(ctr, key):
