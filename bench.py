@@ -454,6 +454,51 @@ def parity_block_sparse(cfg, csr, pipe, res):
     return out
 
 
+def time_sketch_cur(args, cfg, A, flush, samples):
+    """The paper's Sketch-CUR baseline (P:115, P:312 (a): target rate 3x the base rate; SURVEY
+    NEXT-4) on the same matrix and kernels: base = the pilot's uniform k1 rows / columns, 3 k1
+    uniform targets, BR-CUR (Algorithm 1), the P:313 error."""
+    from paper_1607_07395_b200.pipeline import SketchCurRun
+    run = SketchCurRun(A, cfg.m, cfg.n, cfg.k1, mult=3, seed=cfg.seed, residual_samples=samples)
+    for _ in range(max(args.warmup, 2)):
+        run.run()
+    ts = []
+    for _ in range(min(args.steps, 3)):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        run.run(with_residual=False)
+        e1.record()
+        from paper_1607_07395_b200 import cabs as C
+        C.cabs_residual(run.plan, run.A, run.F, None, run.G, run.k1, run.out, run.ws, n_samples=samples, seed=cfg.seed)
+        e2.record()
+        torch.cuda.synchronize()
+        ts.append((e0.elapsed_time(e1), e1.elapsed_time(e2)))
+    sk = statistics.mean(t[0] for t in ts)
+    rs = statistics.mean(t[1] for t in ts)
+    return {"followup": "P:312 (a) Sketch-CUR: BR-CUR (Alg. 1, cabs_br_cur) with 3 k1 uniform targets",
+            "value": (cfg.m + cfg.n) / ((sk + rs) / 1e3), "unit": UNIT, "ms_per_step": sk + rs,
+            "breakdown_ms": {"br_cur": sk, "residual": rs},
+            "rel_err": math.sqrt(max(run.out[0].item(), 0) / run.out[1].item())}
+
+
+def time_rank_sweep(pipe, h=None):
+    """The validation rank sweep on the timed pipeline's follow-up sketch:
+    the holdout errors for every rank and the chosen one."""
+    from paper_1607_07395_b200.pipeline import rank_sweep
+    h = h or min(2 * pipe.cfg.k2, pipe.plan.kmax)
+    rank_sweep(pipe, h)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e, rank, Hr, Hc = rank_sweep(pipe, h)
+    dt = 1e3 * (time.perf_counter() - t0)
+    return {"desc": "P:232 validation set: holdout errors for rho = 0..r (cabs_holdout_errors), argmin",
+            "holdout": [int(Hr.numel()), int(Hc.numel())], "ms_wall": dt, "rank_chosen": rank,
+            "r": int(e.numel() - 1), "rel_err_at_chosen": math.sqrt(float(e[rank] / e[0])),
+            "rel_err_at_r": math.sqrt(float(e[-1] / e[0]))}
+
+
 def time_variant(args, cfg, A, plan, rank, world, comm, flush, stream, followup, desc):
     """One of the paper's follow-up variants on the same matrix, timed like the main step."""
     from paper_1607_07395_b200.pipeline import CabsConfig, CabsPipeline
@@ -644,6 +689,9 @@ def main():
         if args.no_variants:
             break
         variants[fu_name] = time_variant(args, cfg, A, plan, rank, world, comm, flush, stream, fu, fu_desc)
+    if not args.no_variants and world == 1:
+        variants["sketch_cur"] = time_sketch_cur(args, cfg, A, flush, samples)
+        variants["rank_sweep"] = time_rank_sweep(pipe)
 
     if rank != 0:
         return 0

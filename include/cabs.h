@@ -344,6 +344,34 @@ int32_t cabs_orthogonalize(const cabs_plan* plan, int32_t r, const float* U, int
                            float* so, float* Vo, int64_t ldvo, int32_t* r_out, double* sigma,
                            void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream);
 
+/* ---------------------------------------------------------------- NEXT-4 baselines
+ * BR-CUR, Algorithm 1, on the same gathers: C = A(:, Ibc) (m_loc x k1), R = A(Ibr, :)
+ * (k1 x n), C_bar = A(Itr, Ibc), R_bar = A(Ibr, Itc), M = A(Itr, Itc), U* = C_bar^+ M R_bar^+
+ * (step 4's minimum-norm least-squares solution; pseudo-inverses from the FP64 Jacobi SVD of the
+ * zero-padded k2 x k2 matrices, singular values <= tol * sigma_1 dropped).  Outputs the
+ * reconstruction A ~ F G^T as F = C U* (m_loc x k1, ldf) and G = R^T (n x k1, ldg), ready for
+ * cabs_residual(F, NULL, G, k1); Umid (device double[k1 * k1] row-major, or NULL) = U*.
+ * Sketch-CUR is this call with Itr, Itc drawn uniformly and independently of the base
+ * (P:312 (a): three times as many; cabs_uniform_indices with tags 8 / 9).  Ibr, Ibc: k1 indices,
+ * Itr, Itc: k2 indices (device int64; distinct, in range).  Single rank.  Errors: k1 < 1,
+ * k2 < k1, k2 > min(m, n, kmax), ld < k1, nranks > 1 -> INVALID_ARG. */
+int32_t cabs_br_cur(const cabs_plan* plan, const cabs_source* src, int32_t k1, const int64_t* Ibr,
+                    const int64_t* Ibc, int32_t k2, const int64_t* Itr, const int64_t* Itc, double tol,
+                    float* F, int64_t ldf, float* G, int64_t ldg, double* Umid, void* ws,
+                    size_t ws_bytes, const cabs_comm* comm, void* stream);
+
+/* The rank sweep on a validation block ("approximation error varies with the number
+ * of singular vectors used", "use a validation set to choose the optimal number"):
+ * errs[rho] = ||A(Hr, Hc) - U(Hr, :rho) diag(s[:rho]) V(Hc, :rho)^T||_F^2 for rho = 0..r (device
+ * double[r + 1]), from the exact entries of the hr x hc block and the expansion through the r x r
+ * Gram products (FP64).  U: m_loc x r (ldu), V: all n rows (ldv), s: device float[r]; Hr, Hc:
+ * device int64 (the caller keeps them disjoint from the sketch's own indices).  The rank
+ * chosen is the argmin over rho >= 1 (lowest on ties).  Single rank; 1 <= hr, hc, r <= kmax. */
+int32_t cabs_holdout_errors(const cabs_plan* plan, const cabs_source* src, const int64_t* Hr,
+                            int32_t hr, const int64_t* Hc, int32_t hc, const float* U, int64_t ldu,
+                            const float* s, const float* V, int64_t ldv, int32_t r, double* errs,
+                            void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream);
+
 /* Leverage-score follow-up (P:312 variant (e); Z27): k2 distinct
  * points of the orthonormal factor F (n_loc local rows of n_glob, global index = row_off +
  * local, r columns, ldf) drawn without replacement with probability proportional to the

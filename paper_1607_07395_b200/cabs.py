@@ -176,6 +176,10 @@ _SIGS = {
                                  c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_hard_select_pair": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(HardProblem),
                                       ctypes.POINTER(HardProblem), c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
+    "cabs_br_cur": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_i32, c_vp, c_vp, c_i32, c_vp, c_vp,
+                            ctypes.c_double, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp, c_vp]),
+    "cabs_holdout_errors": (c_i32, [ctypes.POINTER(Plan), ctypes.POINTER(Source), c_vp, c_i32, c_vp, c_i32, c_vp,
+                                    c_i64, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, ctypes.c_size_t, c_vp, c_vp]),
     "cabs_orthogonalize": (c_i32, [ctypes.POINTER(Plan), c_i32, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
                                    c_vp, c_i64, c_vp, c_vp, c_vp, c_sz, ctypes.POINTER(Comm), c_vp]),
     "cabs_leverage_select": (c_i32, [ctypes.POINTER(Plan), c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_u64,
@@ -465,3 +469,19 @@ def cabs_uniform_indices(N, k, seed, tag, out, stream=None):
 def cabs_svd(plan, k, W, tol, sigma, Uw, Vw, r, ws, stream=None):
     _check(load().cabs_svd(ctypes.byref(plan), int(k), _p(W), _ld(W), float(tol), _p(sigma), _p(Uw),
                            _p(Vw), _p(r), _p(ws), ws.numel(), _stream(stream)), "cabs_svd")
+
+
+def cabs_br_cur(plan, A, k1, Ibr, Ibc, k2, Itr, Itc, F, G, ws, tol=1e-12, Umid=None, comm=None, stream=None):
+    """BR-CUR (Algorithm 1): A ~ F G^T with F = C U*, G = R^T (cabs.h cabs_br_cur)."""
+    src = _source(A)
+    _check(load().cabs_br_cur(ctypes.byref(plan), ctypes.byref(src), int(k1), _p(Ibr), _p(Ibc), int(k2), _p(Itr),
+                              _p(Itc), float(tol), _p(F), _ld(F), _p(G), _ld(G), _p(Umid), _p(ws), ws.numel(),
+                              _comm(comm), _stream(stream)), "cabs_br_cur")
+
+
+def cabs_holdout_errors(plan, A, Hr, Hc, U, s, V, r, errs, ws, comm=None, stream=None):
+    """Rank sweep on the validation block A(Hr, Hc): errs[rho], rho = 0..r (cabs.h cabs_holdout_errors)."""
+    src = _source(A)
+    _check(load().cabs_holdout_errors(ctypes.byref(plan), ctypes.byref(src), _p(Hr), int(Hr.numel()), _p(Hc),
+                                      int(Hc.numel()), _p(U), _ld(U), _p(s), _p(V), _ld(V), int(r), _p(errs), _p(ws),
+                                      ws.numel(), _comm(comm), _stream(stream)), "cabs_holdout_errors")

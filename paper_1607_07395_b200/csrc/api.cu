@@ -909,6 +909,96 @@ int32_t cabs_orthogonalize(const cabs_plan* plan, int32_t r, const float* U, int
   return CABS_OK;
 }
 
+// ---------------------------------------------------------------- NEXT-4: BR-CUR / Sketch-CUR, rank sweep
+int32_t cabs_br_cur(const cabs_plan* plan, const cabs_source* src, int32_t k1, const int64_t* Ibr, const int64_t* Ibc,
+                    int32_t k2, const int64_t* Itr, const int64_t* Itc, double tol, float* F, int64_t ldf, float* G,
+                    int64_t ldg, double* Umid, void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  const cabs_plan& p = *plan;
+  if (multi(comm) || p.nranks > 1) return arg_error("br_cur: single rank only");
+  CABS_TRY(check_source(p, src, "br_cur: bad source"));
+  if (k1 < 1 || k2 < k1 || k2 > p.kmax || k2 > p.m || k2 > p.n) return arg_error("br_cur: need 1 <= k1 <= k2 <= min(m, n, kmax)");
+  if (!Ibr || !Ibc || !Itr || !Itc || !F || !G || ldf < k1 || ldg < k1) return arg_error("br_cur: bad buffers");
+  cudaStream_t st = S(stream);
+  const int64_t m_loc = p.row_end - p.row_begin;
+  float* Cb = wsp<float>(ws, L.cb);
+  float* Rb = wsp<float>(ws, L.rb);
+  float* Wb = wsp<float>(ws, L.wb);
+  const size_t KK = (size_t)L.K * L.K;
+  double* o = reinterpret_cast<double*>(static_cast<unsigned char*>(ws) + L.orth);
+  double *U1 = o, *V1 = o + KK, *U2 = o + 2 * KK, *V2 = o + 3 * KK, *sig1 = o + 4 * KK, *sig2 = sig1 + L.K;
+  double* M = wsp<double>(ws, L.w64);
+  double* tmp = wsp<double>(ws, L.orth_part);  // d1, d2, X1, Y, X2, U* (after the SVDs)
+  if (sizeof(double) * (2.0 * k2 + 3.0 * k1 * k2 + 1.0 * k1 * k1) > static_cast<double>(L.orth - L.orth_part))
+    return arg_error("br_cur: k1, k2 too large for the workspace");
+  double *d1 = tmp, *d2 = d1 + k2, *X1 = d2 + k2, *Y = X1 + (size_t)k1 * k2, *X2 = Y + (size_t)k1 * k2;
+  double* Ust = X2 + (size_t)k2 * k1;
+  // steps 1-2 (Alg. 1): C = A(:, I^b_c); R = A(I^b_r, :) -> G = R^T and R_bar = R(:, I^t_c) padded to k2 x k2
+  src_cols(p, src, Ibc, k1, Cb, L.Kp, ws, st);
+  src_rows(p, src, Ibr, k1, Rb, L.ldrb, ws, st);
+  CABS_LAUNCH_CHECK("br_cur gathers");
+  launch_transpose(Rb, L.ldrb, k1, p.n, G, ldg, st);
+  launch_pick_cols(Rb, L.ldrb, k1, Itc, k2, k2, Wb, L.Kp, nullptr, st);
+  launch_zero_rows(Wb, L.Kp, k1, k2, k2, st);
+  launch_svd(k2, Wb, L.Kp, tol, ws, L, sig2, U2, V2, nullptr, st);
+  CABS_LAUNCH_CHECK("br_cur svd R_bar");
+  // steps 2-3: the target rows A(I^t_r, :) -> C_bar = (.)(:, I^b_c) padded, M = (.)(:, I^t_c)
+  src_rows(p, src, Itr, k2, Rb, L.ldrb, ws, st);
+  launch_pick_cols(Rb, L.ldrb, k2, Ibc, k1, k2, Wb, L.Kp, nullptr, st);
+  launch_pick_cols(Rb, L.ldrb, k2, Itc, k2, k2, nullptr, 0, M, st);
+  CABS_LAUNCH_CHECK("br_cur targets");
+  launch_svd(k2, Wb, L.Kp, tol, ws, L, sig1, U1, V1, nullptr, st);
+  CABS_LAUNCH_CHECK("br_cur svd C_bar");
+  // step 4: U* = C_bar^+ M R_bar^+ (FP64); step 5: F = C U*, A ~ F G^T
+  launch_cur_middle(k1, k2, U1, V1, sig1, U2, V2, sig2, tol, M, d1, d2, X1, Y, X2, Ust, st);
+  float* Uf = wsp<float>(ws, L.uw32);
+  launch_f32_of(Ust, k1, k1, Uf, L.Kp, static_cast<int>(L.Kp), st);
+  cabsk::OrthArgs a{};
+  a.U = Cb; a.ldu = L.Kp; a.nu = m_loc; a.r = k1; a.TU = Uf; a.kp = L.Kp; a.Uo = F; a.lduo = ldf;
+  launch_orth_apply_u(a, st);
+  CABS_LAUNCH_CHECK("br_cur middle");
+  if (Umid) CABS_CUDA_TRY(cudaMemcpyAsync(Umid, Ust, sizeof(double) * k1 * k1, cudaMemcpyDeviceToDevice, st));
+  return CABS_OK;
+}
+
+int32_t cabs_holdout_errors(const cabs_plan* plan, const cabs_source* src, const int64_t* Hr, int32_t hr,
+                            const int64_t* Hc, int32_t hc, const float* U, int64_t ldu, const float* s, const float* V,
+                            int64_t ldv, int32_t r, double* errs, void* ws, size_t ws_bytes, const cabs_comm* comm,
+                            void* stream) {
+  CABS_TRY(check_plan(plan));
+  Ws L;
+  CABS_TRY(check_ws(plan, ws, ws_bytes, &L));
+  const cabs_plan& p = *plan;
+  if (multi(comm) || p.nranks > 1) return arg_error("holdout_errors: single rank only");
+  CABS_TRY(check_source(p, src, "holdout_errors: bad source"));
+  if (hr < 1 || hc < 1 || hr > p.kmax || hc > p.kmax || r < 1 || r > p.kmax) return arg_error("holdout_errors: bad sizes");
+  if (!Hr || !Hc || !U || !V || !s || !errs || ldu < r || ldv < r) return arg_error("holdout_errors: bad buffers");
+  cudaStream_t st = S(stream);
+  float* Rb = wsp<float>(ws, L.rb);
+  double* B = wsp<double>(ws, L.w64);
+  float* Uh = wsp<float>(ws, L.uw32);
+  float* Vh = wsp<float>(ws, L.vw32);
+  double* Uh64 = wsp<double>(ws, L.a64);
+  double* Vh64 = wsp<double>(ws, L.v64);
+  // the validation block B = A(Hr, Hc) (FP64 copy of exact entries), U_H = U(Hr, :r), V_H = V(Hc, :r)
+  src_rows(p, src, Hr, hr, Rb, L.ldrb, ws, st);
+  launch_pick_cols(Rb, L.ldrb, hr, Hc, hc, hc, nullptr, 0, B, st);
+  launch_pick_rows(U, ldu, Hr, hr, r, static_cast<int>(L.Kp), Uh, L.Kp, Uh64, st);
+  launch_pick_rows(V, ldv, Hc, hc, r, static_cast<int>(L.Kp), Vh, L.Kp, Vh64, st);
+  CABS_LAUNCH_CHECK("holdout gathers");
+  cabsk::OrthArgs a{};
+  a.U = Uh; a.ldu = L.Kp; a.nu = hr; a.V = Vh; a.ldv = L.Kp; a.nv = hc; a.r = r;
+  a.part = wsp<double>(ws, L.orth_part);
+  a.nblk = orth_gram_blocks(hr, hc, r);
+  a.gram = reinterpret_cast<double*>(static_cast<unsigned char*>(ws) + L.orth);
+  launch_orth_gram(a, st);  // U_H^T U_H, V_H^T V_H (exact FP64 products)
+  launch_sweep(B, hr, hc, Vh64, Uh64, s, a.gram, r, a.part, errs, st);
+  CABS_LAUNCH_CHECK("holdout sweep");
+  return CABS_OK;
+}
+
 static int32_t lev_run(const cabs_plan* plan, const cabs_hard_problem* const* pr, const uint32_t* tags, int nprob,
                        uint64_t seed, void* ws, size_t ws_bytes, const cabs_comm* comm, void* stream) {
   CABS_TRY(check_plan(plan));

@@ -185,6 +185,21 @@ int orth_gram_blocks(int64_t nu, int64_t nv, int r);
 void launch_orth_gram(OrthArgs& a, cudaStream_t st);
 void launch_orth_core(const OrthArgs& a, void* ws, cudaStream_t st);
 void launch_orth_finish(const OrthArgs& a, cudaStream_t st);
+void launch_orth_apply_u(const OrthArgs& a, cudaStream_t st);
+
+// cur.cu -- BR-CUR / Sketch-CUR middle matrix and the validation rank sweep
+void launch_pick_cols(const float* src, int64_t lds, int nr, const int64_t* cols, int nc, int pad, float* out,
+                      int64_t ldo, double* out64, cudaStream_t st);
+void launch_pick_rows(const float* X, int64_t ldx, const int64_t* rows, int nr, int ncol, int pad, float* out,
+                      int64_t ldo, double* out64, cudaStream_t st);
+void launch_transpose(const float* R, int64_t ldr, int k, int64_t n, float* G, int64_t ldg, cudaStream_t st);
+void launch_zero_rows(float* X, int64_t ldx, int nr, int npad, int ncol, cudaStream_t st);
+void launch_cur_middle(int k1, int k2, const double* U1, const double* V1, const double* sig1, const double* U2,
+                       const double* V2, const double* sig2, double tol, const double* M, double* d1, double* d2,
+                       double* X1, double* Y, double* X2, double* Ustar, cudaStream_t st);
+void launch_f32_of(const double* X, int rows, int cols, float* Y, int64_t ldy, int pad, cudaStream_t st);
+void launch_sweep(const double* B, int hr, int hc, const double* VH, const double* UH, const float* s,
+                  const double* gram, int r, double* W1, double* err, cudaStream_t st);
 
 // sparse.cu -- CSR / CSC source (cabs.h CABS_SOURCE_CSR_F32), this rank's row block
 struct CsrSrc {

@@ -312,6 +312,15 @@ void launch_orth_core(const OrthArgs& a, void* ws, cudaStream_t st) {
                       st>>>(a);
 }
 
+// Uo = U T_U only (the V side absent): the tiled apply, used for F = C U* by cur.cu
+void launch_orth_apply_u(const OrthArgs& a, cudaStream_t st) {
+  const int64_t nbu = ceil_div(a.nu, 64);
+  const int ncb = static_cast<int>(ceil_div(a.lduo, 64));
+  if (nbu == 0) return;
+  note_launch();
+  orth_apply_kernel<<<static_cast<unsigned>(nbu * ncb), kOrthThreads, 0, st>>>(a, static_cast<int>(nbu), ncb);
+}
+
 void launch_orth_finish(const OrthArgs& a, cudaStream_t st) {
   note_launch();
   orth_solve_kernel<<<2 * ((a.r + 31) / 32), 128, 0, st>>>(a);

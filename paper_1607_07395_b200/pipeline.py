@@ -236,3 +236,59 @@ class CabsPipeline:
                     r2=r2, U=cpu(self.U), V=cpu(self.V), s2=cpu(self.s2), sigma2=cpu(self.sigma2),
                     resid_sq=float(self.out[0]), a_sq=float(self.out[1]),
                     tie_log_r=C.read_tie_log(self.tlog_r), tie_log_c=C.read_tie_log(self.tlog_c))
+
+
+class SketchCurRun:
+    """The paper's Sketch-CUR baseline (P:312 (a)) on the library's kernels:
+    BR-CUR (Algorithm 1) with the pilot's uniform base sampling (Floyd tags 1 / 2, k1 rows and
+    columns) and mult * k1 uniform target rows / columns drawn independently (tags 8 / 9), then
+    the P:313 error of A ~ F G^T (F = C U*, G = R^T).  Single GPU."""
+
+    TAG_TARGET_ROWS, TAG_TARGET_COLS = 8, 9
+
+    def __init__(self, A, m, n, k1, mult=3, seed=0, tol=1e-12, residual_samples=0):
+        C.load()
+        self.A, self.m, self.n, self.k1, self.k2, self.seed, self.tol = A, m, n, k1, mult * k1, seed, tol
+        self.samples = residual_samples
+        self.plan = make_plan(m, n, self.k2)
+        dev = A.device
+        self.ws = torch.zeros(C.cabs_workspace_bytes(self.plan), dtype=torch.uint8, device=dev)
+        i64 = torch.int64
+        self.Ibr, self.Ibc = torch.zeros(k1, dtype=i64, device=dev), torch.zeros(k1, dtype=i64, device=dev)
+        self.Itr, self.Itc = (torch.zeros(self.k2, dtype=i64, device=dev), torch.zeros(self.k2, dtype=i64, device=dev))
+        ld = C.cabs_padded_ld(k1)
+        self.F = torch.zeros((max(self.plan.m_loc, 1), ld), device=dev)
+        self.G = torch.zeros((n, ld), device=dev)
+        self.Umid = torch.zeros((k1, k1), dtype=torch.float64, device=dev)
+        self.out = torch.zeros(2, dtype=torch.float64, device=dev)
+
+    def run(self, with_residual=True):
+        C.cabs_uniform_indices(self.m, self.k1, self.seed, 1, self.Ibr)
+        C.cabs_uniform_indices(self.n, self.k1, self.seed, 2, self.Ibc)
+        C.cabs_uniform_indices(self.m, self.k2, self.seed, self.TAG_TARGET_ROWS, self.Itr)
+        C.cabs_uniform_indices(self.n, self.k2, self.seed, self.TAG_TARGET_COLS, self.Itc)
+        C.cabs_br_cur(self.plan, self.A, self.k1, self.Ibr, self.Ibc, self.k2, self.Itr, self.Itc, self.F, self.G,
+                      self.ws, tol=self.tol, Umid=self.Umid)
+        if with_residual:
+            C.cabs_residual(self.plan, self.A, self.F, None, self.G, self.k1, self.out, self.ws,
+                            n_samples=self.samples, seed=self.seed)
+
+
+def rank_sweep(pipe: CabsPipeline, h: int, tags=(10, 11)):
+    """The validation rank sweep of P:232 on a finished single-GPU pipeline: h
+    uniform holdout rows / columns (Floyd, tags 10 / 11) less the follow-up sketch's own indices,
+    errs[rho] on that block for rho = 0..r (cabs_holdout_errors), and the chosen rank (argmin over
+    rho >= 1, lowest on ties).  Returns (errs as a host FP64 tensor, rank, Hr, Hc)."""
+    p, dev = pipe.plan, pipe.device
+    r = int(pipe.r2.item())
+    Hr = torch.zeros(h, dtype=torch.int64, device=dev)
+    Hc = torch.zeros(h, dtype=torch.int64, device=dev)
+    C.cabs_uniform_indices(p.m, h, pipe.cfg.seed, tags[0], Hr)
+    C.cabs_uniform_indices(p.n, h, pipe.cfg.seed, tags[1], Hc)
+    Hr = Hr[~torch.isin(Hr, pipe.Ib)].contiguous()
+    Hc = Hc[~torch.isin(Hc, pipe.Jb)].contiguous()
+    errs = torch.zeros(r + 1, dtype=torch.float64, device=dev)
+    C.cabs_holdout_errors(p, pipe.A, Hr, Hc, pipe.U, pipe.s2, pipe.G, r, errs, pipe.ws)
+    e = errs.cpu()
+    rank = int(torch.argmin(e[1:]).item()) + 1
+    return e, rank, Hr.cpu(), Hc.cpu()
