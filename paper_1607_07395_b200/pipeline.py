@@ -280,6 +280,8 @@ def rank_sweep(pipe: CabsPipeline, h: int, tags=(10, 11)):
     errs[rho] on that block for rho = 0..r (cabs_holdout_errors), and the chosen rank (argmin over
     rho >= 1, lowest on ties).  Returns (errs as a host FP64 tensor, rank, Hr, Hc)."""
     p, dev = pipe.plan, pipe.device
+    if not 1 <= h <= p.kmax:
+        raise ValueError("rank_sweep: need 1 <= h <= kmax (the validation block lives in the k x k buffers)")
     r = int(pipe.r2.item())
     Hr = torch.zeros(h, dtype=torch.int64, device=dev)
     Hc = torch.zeros(h, dtype=torch.int64, device=dev)

@@ -58,9 +58,12 @@ def test_br_cur_matches_oracle(dev, m, n, k1, k2, rank, noise):
     assert rel_fro(F.cpu().numpy()[:, :k1], Fr) < 1e-4
     r2, a2 = O.residual(A, Fr, ref.R.T)
     assert abs(out[1].item() - a2) <= 1e-6 * a2
-    assert abs(math.sqrt(max(out[0].item(), 0)) - math.sqrt(r2)) <= 1e-4 * math.sqrt(r2) + 1e-6 * math.sqrt(a2)
-    if noise == 0.0 and k1 >= rank:  # exact recovery
-        assert out[0].item() <= 1e-9 * a2
+    if noise == 0.0 and k1 >= rank:
+        # exact recovery (both sides): the oracle to FP64 rounding, the GPU to the FP32 floor of
+        # the reconstruction (F = C U* in FP32, the fused residual's products)
+        assert r2 <= 1e-9 * a2 and out[0].item() <= 1e-8 * a2  # A is the FP32 rounding of a rank-k matrix
+    else:
+        assert abs(math.sqrt(max(out[0].item(), 0)) - math.sqrt(r2)) <= 1e-4 * math.sqrt(r2) + 1e-6 * math.sqrt(a2)
 
 
 def test_sketch_cur_matches_oracle(dev):
@@ -82,8 +85,8 @@ def test_sketch_cur_matches_oracle(dev):
     assert rel_fro(run.Umid.cpu().numpy(), ref.U) < 1e-4
 
 
-@pytest.mark.parametrize("name,m,n,k,h", [("c1", 2000, 1500, 20, 60), ("c2", 6000, 3000, 50, 120),
-                                          ("c3", 5000, 2500, 100, 200)])
+@pytest.mark.parametrize("name,m,n,k,h", [("c1", 2000, 1500, 20, 20), ("c2", 6000, 3000, 50, 50),
+                                          ("c3", 5000, 2500, 100, 100)])
 def test_rank_sweep_matches_oracle(dev, name, m, n, k, h):
     from paper_1607_07395_b200.pipeline import CabsConfig, CabsPipeline, rank_sweep
     from workloads import CONFIGS, make_A, scaled
