@@ -168,6 +168,31 @@ __device__ __forceinline__ void lex_chain(const float (&x)[DP], const float* con
   }
 }
 
+// the first PD dimensions of the same chain (a prefix of the FP32 sum of non-negative terms, so
+// <= the full chain's value bit for bit: an exact lower bound)
+template <int DP, int PD, int NC>
+__device__ __forceinline__ void lex_chain_part(const float (&x)[DP], const float* const (&c)[NC], float (&acc)[NC]) {
+#pragma unroll
+  for (int q = 0; q < NC; ++q) acc[q] = 0.f;
+#pragma unroll
+  for (int i4 = 0; i4 < PD / 4; ++i4) {
+    float4 cv[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) cv[q] = *reinterpret_cast<const float4*>(c[q] + 4 * i4);
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      float f = x[4 * i4] - cv[q].x;
+      acc[q] = fmaf(f, f, acc[q]);
+      f = x[4 * i4 + 1] - cv[q].y;
+      acc[q] = fmaf(f, f, acc[q]);
+      f = x[4 * i4 + 2] - cv[q].z;
+      acc[q] = fmaf(f, f, acc[q]);
+      f = x[4 * i4 + 3] - cv[q].w;
+      acc[q] = fmaf(f, f, acc[q]);
+    }
+  }
+}
+
 template <int DP>
 __device__ __forceinline__ void lex_load_x(const float* row, int d, float (&x)[DP]) {
 #pragma unroll
@@ -595,37 +620,93 @@ __global__ void __launch_bounds__(kLxT, 1) lloyd_prune_kernel(LexArgs a) {
 #pragma unroll
       for (int w = 0; w < 4; ++w) rem[w] = __reduce_or_sync(0xffffffffu, rem[w]);
       LEX_CAND(act ? __popc(rem[0]) + __popc(rem[1]) + __popc(rem[2]) + __popc(rem[3]) : 0);
-      auto next = [&]() {
+      // partial distance search: the first PD dimensions of every union candidate's chain (warp-
+      // uniform, shared-memory broadcasts) are an exact lower bound of its distance; a candidate
+      // whose prefix exceeds (1 + eps) times the best distance known so far cannot be nearer or in
+      // the near-tie band, and its prefix becomes its stored bound.  The lane's survivors then
+      // complete their chains (from dimension 0: the same FP32 sums).  Iteration 0 first guesses
+      // the label as the centre of smallest prefix and evaluates it fully.
+      constexpr int PD = DP >= 48 ? 16 : 0;
+      int guess = -1;
+      auto each4 = [&](const uint32_t (&msk)[4], auto&& fn) {  // warp-uniform visit, 4 centres per step
+        uint32_t r[4] = {msk[0], msk[1], msk[2], msk[3]};
+        for (;;) {
+          int jj[4], cnt = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            int j = -1;
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+              if (j < 0 && r[w]) { j = 32 * w + __ffs(r[w]) - 1; r[w] &= r[w] - 1; }
+            jj[q] = j;
+            cnt += j >= 0;
+          }
+          if (cnt == 0) break;
+          fn(jj);
+        }
+      };
+      uint32_t sv[4] = {rem[0], rem[1], rem[2], rem[3]};
+      if (PD > 0) {
+        if (a0 < 0) {
+          float pmin = FLT_MAX;
+          int pj = 0;
+          each4(rem, [&](const int (&jj)[4]) {
+            const float* c[4] = {c32 + (jj[0] < 0 ? 0 : jj[0]) * cp, c32 + (jj[1] < 0 ? 0 : jj[1]) * cp,
+                                 c32 + (jj[2] < 0 ? 0 : jj[2]) * cp, c32 + (jj[3] < 0 ? 0 : jj[3]) * cp};
+            float acc[4];
+            lex_chain_part<DP, PD, 4>(x, c, acc);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (jj[q] >= 0 && (acc[q] < pmin || (acc[q] == pmin && jj[q] < pj))) { pmin = acc[q]; pj = jj[q]; }
+          });
+          const float* c[1] = {c32 + pj * cp};
+          float acc[1];
+          lex_chain<DP, 1>(x, c, acc);
+          take(acc[0], pj);
+          store_lb(pj, acc[0]);
+          guess = pj;
+        }
+        const float thrp = bd * (1.f + kEps);
+        sv[0] = sv[1] = sv[2] = sv[3] = 0u;
+        each4(rem, [&](const int (&jj)[4]) {
+          const float* c[4] = {c32 + (jj[0] < 0 ? 0 : jj[0]) * cp, c32 + (jj[1] < 0 ? 0 : jj[1]) * cp,
+                               c32 + (jj[2] < 0 ? 0 : jj[2]) * cp, c32 + (jj[3] < 0 ? 0 : jj[3]) * cp};
+          float acc[4];
+          lex_chain_part<DP, PD, 4>(x, c, acc);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = jj[q];
+            if (j < 0 || j == a0 || j == guess) continue;
+            if (acc[q] <= thrp) {
+              sv[j >> 5] |= 1u << (j & 31);
+            } else {
+              lbo = fminf(lbo, sqrtf(acc[q]) * (1.f - 2e-5f));
+              store_lb(j, acc[q]);
+            }
+          }
+        });
+      } else if (a0 >= 0) {
+        sv[a0 >> 5] &= ~(1u << (a0 & 31));
+      }
+      // the lane's survivors: full chains, two at a time
+      auto nxt = [&]() {
         int j = -1;
 #pragma unroll
         for (int w = 0; w < 4; ++w)
-          if (j < 0 && rem[w]) { j = 32 * w + __ffs(rem[w]) - 1; rem[w] &= rem[w] - 1; }
+          if (j < 0 && sv[w]) { j = 32 * w + __ffs(sv[w]) - 1; sv[w] &= sv[w] - 1; }
         return j;
       };
-      int nrem = __popc(rem[0]) + __popc(rem[1]) + __popc(rem[2]) + __popc(rem[3]);
-      while (nrem >= 3) {
-        const int j0 = next(), j1 = next(), j2 = next();
-        const int j3 = nrem >= 4 ? next() : j2;
-        nrem -= nrem >= 4 ? 4 : 3;
-        const float* c[4] = {c32 + j0 * cp, c32 + j1 * cp, c32 + j2 * cp, c32 + j3 * cp};
-        float acc[4];
-        lex_chain<DP, 4>(x, c, acc);
-        const int jj[4] = {j0, j1, j2, j3};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (q == 3 && j3 == j2) break;
-          if (jj[q] != a0) { take(acc[q], jj[q]); store_lb(jj[q], acc[q]); }
-        }
-      }
+      if (!act) sv[0] = sv[1] = sv[2] = sv[3] = 0u;
       for (;;) {
-        const int j0 = next();
+        const int j0 = nxt();
         if (j0 < 0) break;
-        const int j1 = next();
+        const int j1 = nxt();
         const float* c[2] = {c32 + j0 * cp, c32 + (j1 < 0 ? j0 : j1) * cp};
         float acc[2];
         lex_chain<DP, 2>(x, c, acc);
-        if (j0 != a0) { take(acc[0], j0); store_lb(j0, acc[0]); }
-        if (j1 >= 0 && j1 != a0) { take(acc[1], j1); store_lb(j1, acc[1]); }
+        take(acc[0], j0);
+        store_lb(j0, acc[0]);
+        if (j1 >= 0) { take(acc[1], j1); store_lb(j1, acc[1]); }
       }
       if (act) {
         ubv[pl] = sqrtf(bd) * (1.f + 2e-5f);
