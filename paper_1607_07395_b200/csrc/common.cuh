@@ -65,7 +65,7 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.status = take(256);
   w.scal = take(4096);
   w.w64 = take(sizeof(double) * K * K);
-  w.a64 = take(sizeof(double) * K * K);
+  w.a64 = take(sizeof(double) * K * K + sizeof(int) * K);  // (+ the QR pivots of the SVD preconditioner)
   w.v64 = take(sizeof(double) * K * K);
   w.sig64 = take(sizeof(double) * Kp);
   w.uw32 = take(sizeof(float) * K * Kp);

@@ -838,6 +838,187 @@ __device__ __forceinline__ void lane_rot(bool left, double on, double od, double
   r.i = pi * (q1 * c);
 }
 
+// ---------------------------------------------------------------- QR preconditioning (k <= 128)
+// W P = Q R by Householder QR with column pivoting (largest remaining column norm first, lowest
+// column on ties), FP64, one CTA.  One-sided Jacobi then runs on X = R^T instead of W: its
+// columns are much closer to orthogonal (the pivoted R is graded), so the sweep count drops
+// (c3's pilot W: 15 -> 8 sweeps, tools/dump_w.py + an offline replay).  With X = U_x S V_x^T:
+// W = (Q V_x) S (P U_x)^T, so the Jacobi pair starts CTA 1's accumulator from Q instead of I
+// (it ends as U_w = Q V_x) and CTA 0's normalised columns give V_w with rows permuted by P.
+// Outputs (row-major FP64, k x k): Xt = R^T, Qm = Q; piv[j] = the column of W at position j.
+// Layout: a group of 8 lanes owns one column (group q = thread / 8, rows gl + 8 e, e < E) and
+// keeps its TRAILING part in registers: row j is finalised at step j (R_jq goes to a global
+// scratch, the register is zeroed), so no step needs row masks.  After every step the group
+// stores the column to shared memory, where the next step's pivot column is read by everyone.
+// The pivot is the argmax of the per-warp bests published at the previous step (every warp
+// reduces the same 32 entries in the same order); its x_j and exact ||x(j:)||^2 give the
+// reflector's scalars without a reduction; every group updates its column (v^T a: one 3-level
+// group reduction) and forms its exact trailing norm ||a(j+1:)||^2 (the next pivot key).
+// Q = H_0 ... H_{k-1} is accumulated afterwards column by column in registers, no barriers.
+constexpr int kQrThreads = 1024;
+constexpr int kQrK = 128;
+
+template <int E>
+__global__ void __launch_bounds__(kQrThreads, 1)
+svd_qrcp_kernel(int k, const float* __restrict__ W, int64_t ldw, double* __restrict__ Xt, double* __restrict__ Qm,
+                int* __restrict__ piv_out, void* ws) {
+  constexpr int KP = 8 * E;                      // padded column length
+  extern __shared__ __align__(16) double qa[];  // [kQrK columns][KP rows]
+  __shared__ double s_wb[2][32];                // per-warp best key (-1: nothing left), by step parity
+  __shared__ int s_wi[2][32];
+  __shared__ double s_vj[kQrK], s_beta[kQrK], s_rd[kQrK];
+  __shared__ int s_piv[kQrK];
+  double* Rg = Qm;  // R above the diagonal by step and physical column, Rg[j k + q] (Q is written last)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = tid >> 3, gl = tid & 7;  // column, lane in the group (rows gl + 8 e)
+  double a[E];
+  bool bad = false;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = gl + 8 * e;
+    float v = 0.f;
+    if (i < k && q < k) v = W[(int64_t)i * ldw + q];
+    bad |= !isfinite(v);
+    a[e] = static_cast<double>(v);
+  }
+  if (bad) set_status(ws, CABS_DEV_NONFINITE);
+  auto group_best = [&](double key, int par) {  // (key, column) argmax over the warp's 4 groups
+    int idx = q;
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+      const double ok = __shfl_xor_sync(0xffffffffu, key, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ok > key || (ok == key && oi < idx)) { key = ok; idx = oi; }
+    }
+    if (lane == 0) { s_wb[par][warp] = key; s_wi[par][warp] = idx; }
+  };
+  auto sq_sum = [&]() {
+    double n0 = 0.0, n1 = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (e & 1) n1 = fma(a[e], a[e], n1); else n0 = fma(a[e], a[e], n0);
+    }
+    return group_sum<8>(n0 + n1);
+  };
+  double* col = qa + (q < kQrK ? q : 0) * KP;
+  {
+    const double key = sq_sum();
+    group_best(q < k ? key : -1.0, 0);
+#pragma unroll
+    for (int e = 0; e < E; ++e) col[gl + 8 * e] = a[e];
+  }
+  bool done = q >= k;
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    const int par = j & 1;
+    // pivot: argmax of the 32 warp bests (identical in every warp)
+    double bv = s_wb[par][lane];
+    int bq = s_wi[par][lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+      if (ov > bv || (ov == bv && oq < bq)) { bv = ov; bq = oq; }
+    }
+    const int ph = bq;
+    const double* xp = qa + ph * KP;
+    const double xj = xp[j], nn = fmax(bv, 0.0), sn = sqrt(nn);
+    const double alpha = xj >= 0.0 ? -sn : sn;                           // R_jj
+    const double vjj = xj - alpha;                                        // x_j + sign(x_j) ||x||
+    const double beta = nn > 0.0 ? 1.0 / (sn * (sn + fabs(xj))) : 0.0;    // 2 / v^T v
+    const double aj = col[j];                                             // this column's row j
+    if (q == ph) done = true;
+    // (the shuffles are warp-wide: finished groups compute too and discard)
+    double d0 = gl == 0 ? (vjj - xj) * aj : 0.0, d1 = 0.0;  // v = x with x_j replaced by vjj
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (e & 1) d1 = fma(xp[gl + 8 * e], a[e], d1); else d0 = fma(xp[gl + 8 * e], a[e], d0);
+    }
+    const double f = beta * group_sum<8>(d0 + d1);
+    const int je = j >> 3, jl = j & 7;
+    if (!done) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) a[e] = (e == je && gl == jl) ? 0.0 : fma(-f, xp[gl + 8 * e], a[e]);
+    }
+    const double key = sq_sum();  // exact ||a(j+1:)||^2: the next pivot key
+    group_best(done ? -1.0 : key, par ^ 1);
+    if (!done && gl == 0) Rg[(size_t)j * k + q] = fma(-f, vjj, aj);  // R_jq
+    if (tid == 0) {
+      s_piv[j] = ph;
+      s_vj[j] = vjj;
+      s_beta[j] = beta;
+      s_rd[j] = alpha;
+    }
+    __syncthreads();  // every read of the pivot column is done ...
+    if (!done) {      // ... before the updated columns are stored (the pivot column keeps x)
+#pragma unroll
+      for (int e = 0; e < E; ++e) col[gl + 8 * e] = a[e];
+    }
+    __syncthreads();
+  }
+  // X = R^T: X[i][c] = R[c][i] = Rg[c][piv[i]] above the diagonal (c < i), R_ii on it, 0 below
+  for (int e = tid; e < k * k; e += kQrThreads) {
+    const int i = e / k, c = e - i * k;
+    Xt[e] = c < i ? Rg[(size_t)c * k + s_piv[i]] : (c == i ? s_rd[i] : 0.0);
+  }
+  if (tid < k) piv_out[tid] = s_piv[tid];
+  __syncthreads();  // Rg (= Qm) read before Q overwrites it
+  // Q = H_0 H_1 ... H_{k-1}: column q starts as e_q; H_j (v_j = column piv[j] as stored at its
+  // step: rows < j zero, x_j replaced by vjj) applied for j = min(q, k - 1) down to 0
+  if (warp * 4 < k) {  // warp-uniform loop from the warp's last column (shuffles are warp-wide)
+    double y[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) y[e] = (gl + 8 * e == q) ? 1.0 : 0.0;
+    const int jtop = min(warp * 4 + 3, k - 1);
+    for (int j = jtop; j >= 0; --j) {
+      const double* xp = qa + s_piv[j] * KP;
+      const double vjj = s_vj[j], xj = xp[j];
+      const int je = j >> 3, jl = j & 7;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const double v = (e == je && gl == jl) ? vjj : xp[gl + 8 * e];
+        if (e & 1) d1 = fma(v, y[e], d1); else d0 = fma(v, y[e], d0);
+      }
+      (void)xj;
+      const double gsum = group_sum<8>(d0 + d1);
+      const double f = j <= q ? s_beta[j] * gsum : 0.0;  // H_j e_q = e_q for j > q
+#pragma unroll
+      for (int e = 0; e < E; ++e) y[e] = fma(-f, (e == je && gl == jl) ? vjj : xp[gl + 8 * e], y[e]);
+    }
+    if (q < k) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = gl + 8 * e;
+        if (i < k) Qm[(size_t)i * k + q] = y[e];
+      }
+    }
+  }
+}
+
+template <int E>
+static void launch_qrcp_e(int k, const float* W, int64_t ldw, double* Xt, double* Qm, int* piv, void* ws,
+                          cudaStream_t st) {
+  constexpr size_t smem = sizeof(double) * kQrK * 8 * E;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(svd_qrcp_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  svd_qrcp_kernel<E><<<1, kQrThreads, smem, st>>>(k, W, ldw, Xt, Qm, piv, ws);
+}
+
+static bool launch_qrcp(int k, const float* W, int64_t ldw, double* Xt, double* Qm, int* piv, void* ws,
+                        cudaStream_t st) {
+  if (k > kQrK) return false;
+  note_launch();
+  if (k <= 32) launch_qrcp_e<4>(k, W, ldw, Xt, Qm, piv, ws, st);
+  else if (k <= 64) launch_qrcp_e<8>(k, W, ldw, Xt, Qm, piv, ws, st);
+  else if (k <= 104) launch_qrcp_e<13>(k, W, ldw, Xt, Qm, piv, ws, st);
+  else launch_qrcp_e<16>(k, W, ldw, Xt, Qm, piv, ws, st);
+  return true;
+}
+
 // ---------------------------------------------------------------- k <= 64: four columns per slot
 // As svd_split_kernel (A on CTA 0, V on CTA 1 of a cluster pair, rotations streamed through
 // DSMEM), but every slot (LP lanes) holds FOUR consecutive positions of the odd-even network:
@@ -845,18 +1026,29 @@ __device__ __forceinline__ void lane_rot(bool left, double on, double od, double
 // across slots -- only two of the four columns move per odd round (half the shared-memory
 // traffic of two-column slots), and every round has two or three independent rotation chains
 // per warp.  n' = round_up(k, 4) positions (zero columns pad).
-template <int LP, int E>
+//
+// KM (64 or 128) bounds k.  CTA 1 follows CTA 0 by one SEGMENT of nseg (1, 2 or 4) equal
+// parts of a sweep (n4 / nseg rounds, even): the rotations of a segment are double-buffered
+// [segment parity][round][slot][4] in CTA 1's shared memory, one full / empty mbarrier pair
+// per parity; the scale fold and the stop decision stay at sweep boundaries.  k = 100 needs
+// nseg = 2 to fit (80 KB of rotations instead of 160).
+template <int LP, int E, int KM>
 __global__ void __launch_bounds__(256, 1) __cluster_dims__(2, 1, 1)
-svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, double* __restrict__ sigma_out,
+svd_quad_kernel(int k, int nseg, const float* __restrict__ W, int64_t ldw, const double* __restrict__ Xt,
+                const double* __restrict__ Qm, const int* __restrict__ piv, double tol, double* __restrict__ sigma_out,
                 double* __restrict__ Uw64, double* __restrict__ Vw64, float* __restrict__ uw32,
                 float* __restrict__ vw32, int64_t ld32, int* r_out, int* r_out2, void* ws) {
+  // Xt != nullptr: QR-preconditioned (svd_qrcp_kernel): CTA 0 starts from X = R^T, CTA 1 from Q;
+  // at the end CTA 1 holds U_w = Q V_x and CTA 0 the columns of V_w (rows permuted by piv)
+  const bool pre = Xt != nullptr;
   constexpr int G = 32 / LP;
   constexpr int SEAT = E * LP + ((LP - (E * LP) % 16) + 16) % 16;
+  constexpr int NS = KM / 4 + 4;      // seats (slots + the two outer ones, rounded up)
   extern __shared__ __align__(16) double smem_d[];
-  __shared__ double s_sig[64];
-  __shared__ int s_perm[64];
-  __shared__ int s_id[2][2][36];      // [parity][col0 | col3][seat]
-  __shared__ double s_st[2][18][4][3];  // CTA 0: published n, d, 1 / d [parity][seat][position]
+  __shared__ double s_sig[KM];
+  __shared__ int s_perm[KM];
+  __shared__ int s_id[2][2][NS];      // [parity][col0 | col3][seat]
+  __shared__ double s_st[2][NS][4][3];  // CTA 0: published n, d, 1 / d [parity][seat][position]
   __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2];
   __shared__ int s_last[2];
   const uint32_t crank = cg::this_cluster().block_rank();
@@ -880,15 +1072,24 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
     tc::mbar_fence_init();
   }
   for (int e = tid; e < 2 * (int)arr; e += blockDim.x) smem_d[e] = 0.0;
-  for (int e = tid; e < 2 * 18 * 4 * 3; e += blockDim.x) (&s_st[0][0][0][0])[e] = (e % 3 == 0) ? 0.0 : 1.0;
-  for (int e = tid; e < 2 * 2 * 36; e += blockDim.x) (&s_id[0][0][0])[e] = 1 << 30;
+  for (int e = tid; e < 2 * NS * 4 * 3; e += blockDim.x) (&s_st[0][0][0][0])[e] = (e % 3 == 0) ? 0.0 : 1.0;
+  for (int e = tid; e < 2 * 2 * NS; e += blockDim.x) (&s_id[0][0][0])[e] = 1 << 30;
   cluster_sync_all();
 
   double a[4][E];
   int id[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) id[c] = 4 * g + c;
-  if (crank == 0) {
+  if (pre) {
+    const double* src = crank == 0 ? Xt : Qm;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = gl + LP * e;
+        a[c][e] = (live && i < k && id[c] < k) ? src[(size_t)i * k + id[c]] : 0.0;
+      }
+  } else if (crank == 0) {
     bool bad = false;
 #pragma unroll
     for (int c = 0; c < 4; ++c)
@@ -917,7 +1118,8 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
   const uint32_t full_remote0 = dsmem_map(&bar_full[0], 1), full_remote1 = dsmem_map(&bar_full[1], 1);
   const uint32_t empty_remote0 = dsmem_map(&bar_empty[0], 0), empty_remote1 = dsmem_map(&bar_empty[1], 0);
   const uint32_t last_remote = dsmem_map(&s_last[0], 1);
-  double* dvs = prm + (size_t)2 * n4 * Q * 4;  // CTA 1: column scales at sweep end [parity][position]
+  const int HS = n4 / nseg;                     // rounds per segment (even)
+  double* dvs = prm + (size_t)2 * HS * Q * 4;   // CTA 1: column scales at sweep end [parity][position]
   const uint32_t dvs_remote = dsmem_map(dvs, 1);
   // Scaled columns: actual column = d * stored.  The scalar state of position p of the slot
   // (squared norm n, scale d, 1 / d) lives on lanes 2p, 2p + 1 of the group ("owners"), and
@@ -936,12 +1138,6 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
   for (; !last; ++sweep) {
     const int sp = sweep & 1;
 #ifdef CABS_PROFILE_SVD
-    const long long w0 = clock64();
-#endif
-    if (crank == 0 && sweep >= 2) mbar_wait_cluster(&bar_empty[sp], static_cast<uint32_t>(((sweep - 2) >> 1) & 1));
-    if (crank == 1) mbar_wait_cluster(&bar_full[sp], static_cast<uint32_t>((sweep >> 1) & 1));
-#ifdef CABS_PROFILE_SVD
-    q_wait += clock64() - w0;
     const long long s0 = clock64();
 #endif
     int rotated = 0;
@@ -963,8 +1159,19 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
       oi = 1.0;
     }
     for (int rnd = 0; rnd < n4; rnd += 2) {
+      const int seg = rnd / HS, gs = sweep * nseg + seg, bp = gs & 1;  // segment, global index, parity
+      if (rnd == seg * HS) {  // segment start: CTA 0 needs a free buffer, CTA 1 a full one
+#ifdef CABS_PROFILE_SVD
+        const long long w0 = clock64();
+#endif
+        if (crank == 0 && gs >= 2) mbar_wait_cluster(&bar_empty[bp], static_cast<uint32_t>(((gs - 2) >> 1) & 1));
+        if (crank == 1) mbar_wait_cluster(&bar_full[bp], static_cast<uint32_t>((gs >> 1) & 1));
+#ifdef CABS_PROFILE_SVD
+        q_wait += clock64() - w0;
+#endif
+      }
       // ---- even round: pairs (0,1) (lanes 0-3) and (2,3) (lanes 4-7), rotated and swapped
-      const int pidx = ((sp * n4 + rnd) * Q + (live ? g : 0)) * 4;  // [parity][round][slot][4]
+      const int pidx = ((bp * HS + rnd - seg * HS) * Q + (live ? g : 0)) * 4;  // [parity][round][slot][4]
       double al01, be01, al23, be23;
       if (crank == 0) {
         double p01a = 0.0, p01b = 0.0, p23a = 0.0, p23b = 0.0;
@@ -1097,7 +1304,19 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
       }
       if (!lastslot) id[3] = s_id[par][0][g + 2];
       if (!first) id[0] = s_id[par][1][g];
+      if (rnd + 2 == (seg + 1) * HS && seg + 1 < nseg) {  // segment end inside the sweep: hand over
+        __syncthreads();
+        if (tid == 0) {
+          if (crank == 0) {
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            mbar_arrive_remote(bp ? full_remote1 : full_remote0);
+          } else {
+            mbar_arrive_remote(bp ? empty_remote1 : empty_remote0);
+          }
+        }
+      }
     }
+    const int bpl = (sweep * nseg + nseg - 1) & 1;  // the sweep's last segment parity
 #ifdef CABS_PROFILE_SVD
     q_sweep += clock64() - s0;
 #endif
@@ -1110,7 +1329,7 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
       if (tid == 0) {
         dsmem_st_s32(last_remote + 4 * sp, last ? 1 : 0);
         asm volatile("fence.acq_rel.cluster;" ::: "memory");
-        mbar_arrive_remote(sp ? full_remote1 : full_remote0);
+        mbar_arrive_remote(bpl ? full_remote1 : full_remote0);
       }
     } else {
       if (live) {
@@ -1124,7 +1343,7 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
       __syncthreads();
       last = s_last[sp] != 0;
       __syncthreads();
-      if (tid == 0) mbar_arrive_remote(sp ? empty_remote1 : empty_remote0);
+      if (tid == 0) mbar_arrive_remote(bpl ? empty_remote1 : empty_remote0);
     }
   }
   if (crank == 0) {
@@ -1146,13 +1365,16 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
   // ---- epilogue from the registers: sigma_c = |a_c| and the canonical sign (the largest-|.|
   // entry of U_w's column positive, lowest row on ties) per column, rank order by one thread
   // per column, then every group writes its own columns (CTA 0: U_w, CTA 1: V_w) in rank order.
-  __shared__ double s_sgn[64];
-  __shared__ int s_rank[64];
+  __shared__ double s_sgn[KM];
+  __shared__ int s_rank[KM];
   __shared__ int s_r;
 #ifdef CABS_PROFILE_SVD
   const long long q_e0 = clock64();
 #endif
-  if (crank == 0) {
+  // the CTA holding U_w's columns fixes the signs (CTA 0, or CTA 1 when preconditioned)
+  const bool usgn = pre ? crank == 1 : crank == 0;
+  {
+    const uint32_t sgn0 = dsmem_map(s_sgn, 0);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       double ss = 0.0, best = -1.0;
@@ -1174,11 +1396,13 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; neg = on2; }
       }
       if (gl == 0 && live && id[c] < k) {
-        s_sig[id[c]] = sqrt(ss);
-        s_sgn[id[c]] = neg ? -1.0 : 1.0;
+        if (crank == 0) s_sig[id[c]] = sqrt(ss);
+        if (usgn) dsmem_st_f64(sgn0 + 8u * id[c], neg ? -1.0 : 1.0);
       }
     }
-    __syncthreads();
+  }
+  cluster_sync_all();  // sigma and signs in CTA 0
+  if (crank == 0) {
     const uint32_t rank_remote = dsmem_map(s_rank, 1), sgn_remote = dsmem_map(s_sgn, 1);
     for (int c = tid; c < k; c += blockDim.x) {
       const double sc = s_sig[c];
@@ -1214,8 +1438,11 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
 #endif
   {
     const int r = s_r;
-    double* o64 = crank == 0 ? Uw64 : Vw64;
-    float* o32 = crank == 0 ? uw32 : vw32;
+    // CTA 0: its columns / sigma (U_w; V_w when preconditioned, rows permuted by piv); CTA 1:
+    // its columns (V_w; U_w = Q V_x when preconditioned)
+    const bool to_u = (crank == 0) != pre;
+    double* o64 = to_u ? Uw64 : Vw64;
+    float* o32 = to_u ? uw32 : vw32;
     if (live) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -1231,8 +1458,9 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          const int i = gl + LP * e;
-          if (i < k) {
+          const int i0 = gl + LP * e;
+          if (i0 < k) {
+            const int i = (pre && crank == 0) ? piv[i0] : i0;
             const double u = a[c][e] * mul;
             if (o64) o64[(size_t)i * k + jr] = u;
             if (o32) o32[(size_t)i * ld32 + jr] = static_cast<float>(u);
@@ -1256,25 +1484,42 @@ svd_quad_kernel(int k, const float* __restrict__ W, int64_t ldw, double tol, dou
 #endif
 }
 
-template <int LP, int E>
+template <int LP, int E, int KM = 64>
 static bool launch_quad(int k, const float* W, int64_t ldw, double tol, double* sig, double* Uw64, double* Vw64,
-                        float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st) {
+                        float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st,
+                        const Ws* L = nullptr) {
   constexpr int G = 32 / LP;
   constexpr int SEAT = E * LP + ((LP - (E * LP) % 16) + 16) % 16;
   const int n4 = (k + 3) & ~3, Q = n4 / 4;
   const int nw = (Q + G - 1) / G;
+  if (k > KM || k > E * LP || nw * G + 2 > KM / 4 + 4 || nw > 8) return false;
   const size_t xch = sizeof(double) * 2 * 2 * (size_t)(nw * G + 2) * SEAT;
-  const size_t prm = sizeof(double) * 2 * (size_t)n4 * (Q * 4 + 1);
-  const size_t smem = xch + prm;
   constexpr int kCap = 200 * 1024;
-  if (smem > kCap) return false;
+  int nseg = 0;
+  size_t smem = 0;
+  for (int ns = 1; ns <= 4 && !nseg; ns *= 2) {  // fewest segments whose rotation buffers fit
+    if (n4 % (2 * ns)) continue;
+    smem = xch + sizeof(double) * 2 * ((size_t)(n4 / ns) * Q * 4 + n4);
+    if (smem <= kCap) nseg = ns;
+  }
+  if (!nseg) return false;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(svd_quad_kernel<LP, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCap);
+    cudaFuncSetAttribute(svd_quad_kernel<LP, E, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCap);
     attr = true;
   }
-  svd_quad_kernel<LP, E><<<2, 32 * nw, smem, st>>>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user,
-                                                   ws);
+  // QR preconditioning (L given, k > 2; CABS_SVD_NOQR: plain Jacobi on W)
+  const double* Xt = nullptr;
+  const double* Qm = nullptr;
+  const int* piv = nullptr;
+  if (L && k > 2 && !getenv("CABS_SVD_NOQR")) {
+    double* x = wsp<double>(ws, L->a64);
+    double* q = wsp<double>(ws, L->v64);
+    int* pv = reinterpret_cast<int*>(x + (size_t)L->K * L->K);
+    if (launch_qrcp(k, W, ldw, x, q, pv, ws, st)) { Xt = x; Qm = q; piv = pv; }
+  }
+  svd_quad_kernel<LP, E, KM><<<2, 32 * nw, smem, st>>>(k, nseg, W, ldw, Xt, Qm, piv, tol, sig, Uw64, Vw64, uw32, vw32,
+                                                       ld32, r_ws, r_user, ws);
   return true;
 }
 
@@ -1417,10 +1662,10 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
     // A on one SM, V on its cluster partner; four columns per 8-lane slot (the two-column
     // svd_split_kernel stays selectable for comparison)
     if (!getenv("CABS_SVD_SPLIT")) {
-      if (k <= 16) launch_quad<8, 2>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
-      else if (k <= 32) launch_quad<8, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
-      else if (k <= 56) launch_quad<8, 7>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
-      else launch_quad<8, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
+      if (k <= 16) launch_quad<8, 2>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st, &L);
+      else if (k <= 32) launch_quad<8, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st, &L);
+      else if (k <= 56) launch_quad<8, 7>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st, &L);
+      else launch_quad<8, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st, &L);
     } else if (k <= 16) {
       launch_split<8, 2>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
     } else if (k <= 32) {
@@ -1430,6 +1675,12 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
     } else {
       launch_split<8, 8>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
     }
+  } else if (k > 64 && k <= 128 && !getenv("CABS_SVD_CLUSTER") && !getenv("CABS_SVD_ONE_CTA") &&
+             (k <= 104 ? launch_quad<8, 13, 128>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st,
+                                                 &L)
+                       : launch_quad<8, 16, 128>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws,
+                                                 st, &L))) {
+    // 64 < k <= 128: the four-column slots of k <= 64 with 7-8 warps and segment handover
   } else if (k <= 64 && !getenv("CABS_SVD_SMEM")) {
     // register-resident systolic Jacobi, 4 lanes per column pair
     if (k <= 16) launch_systolic<4, 4>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);

@@ -126,18 +126,24 @@ def test_pilot_invalid_k(dev):
 
 # ------------------------------------------------------------------ S4 SVD
 _SVD_KERNELS = {"default": None, "split": "CABS_SVD_SPLIT", "one_sm": "CABS_SVD_ONE_SM", "smem": "CABS_SVD_SMEM",
-                "one_cta": "CABS_SVD_ONE_CTA"}
+                "one_cta": "CABS_SVD_ONE_CTA", "cluster": "CABS_SVD_CLUSTER", "noqr": "CABS_SVD_NOQR"}
 
 
-@pytest.mark.parametrize("kernel", ["default", "split", "one_sm", "smem", "one_cta"])
+@pytest.mark.parametrize("kernel", ["default", "split", "one_sm", "smem", "one_cta", "cluster", "noqr"])
 @pytest.mark.parametrize("k,rank", [(20, 20), (50, 50), (64, 40), (65, 65), (100, 100), (112, 60), (150, 150),
                                     (200, 200), (256, 130), (300, 300), (7, 3), (1, 1)])
 def test_svd_matches_lapack(dev, k, rank, kernel, monkeypatch):
     """Every SVD kernel variant: k <= 64 the default 4-columns-per-slot cluster pair, the
-    2-column pair, the one-SM systolic and the shared-memory kernels; k > 64 the default
-    block Jacobi over a thread-block cluster (svd_cluster.cu) and the single-CTA kernel."""
+    2-column pair, the one-SM systolic and the shared-memory kernels (k <= 128: the default runs
+    Jacobi on R^T of a pivoted Householder QR, "noqr" on W itself); 64 < k <= 128 the default
+    4-columns-per-slot pair with segment handover; k > 128 the default block Jacobi over a
+    thread-block cluster (svd_cluster.cu, also forced at 64 < k <= 128) and the single-CTA kernel."""
     if kernel in ("split", "one_sm") and k > 64:
         pytest.skip("k <= 64 variant")
+    if kernel == "cluster" and not (64 < k <= 128):
+        pytest.skip("forced only where the quad kernel is the default")
+    if kernel == "noqr" and not (2 < k <= 128):
+        pytest.skip("the quad kernel without its QR preconditioner")
     if kernel == "one_cta" and not (64 < k <= 150):
         pytest.skip("k > 64 variant (slow beyond 150)")
     if _SVD_KERNELS[kernel]:

@@ -147,8 +147,8 @@ def probe_svd_quad_prof(k=50):
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "svdqprof":
-    probe_svd_quad_prof(50)
-    probe_svd_quad_prof(20)
+    for kk in [int(x) for x in sys.argv[2:]] or [50, 20]:
+        probe_svd_quad_prof(kk)
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "svdprof":
