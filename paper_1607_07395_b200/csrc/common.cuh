@@ -27,6 +27,7 @@ __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_
 struct Ws {
   size_t status, scal;
   size_t w64, a64, v64, sig64, uw32, vw32;
+  size_t qr;  // SVD QR preconditioner: R scratch (K x K FP64) + pivots (K int)
   size_t norm_part, norms, scales;
   size_t km_w, km_scr, km_pobj, km_ptie, km_red, km_cnt;  // km_w, km_scr, km_cnt: two problems
   size_t km_scr_bytes;                                     // per problem
@@ -65,8 +66,9 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.status = take(256);
   w.scal = take(4096);
   w.w64 = take(sizeof(double) * K * K);
-  w.a64 = take(sizeof(double) * K * K + sizeof(int) * K);  // (+ the QR pivots of the SVD preconditioner)
-  w.v64 = take(sizeof(double) * K * K);
+  w.a64 = take(sizeof(double) * K * K);
+  w.v64 = take(sizeof(double) * (K * K + K));  // (+ K: the QR preconditioner's reflector scales)
+  w.qr = take(sizeof(double) * K * K + sizeof(int) * K);
   w.sig64 = take(sizeof(double) * Kp);
   w.uw32 = take(sizeof(float) * K * Kp);
   w.vw32 = take(sizeof(float) * K * Kp);

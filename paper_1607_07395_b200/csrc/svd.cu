@@ -843,117 +843,166 @@ __device__ __forceinline__ void lane_rot(bool left, double on, double od, double
 // column on ties), FP64, one CTA.  One-sided Jacobi then runs on X = R^T instead of W: its
 // columns are much closer to orthogonal (the pivoted R is graded), so the sweep count drops
 // (c3's pilot W: 15 -> 8 sweeps, tools/dump_w.py + an offline replay).  With X = U_x S V_x^T:
-// W = (Q V_x) S (P U_x)^T, so the Jacobi pair starts CTA 1's accumulator from Q instead of I
-// (it ends as U_w = Q V_x) and CTA 0's normalised columns give V_w with rows permuted by P.
-// Outputs (row-major FP64, k x k): Xt = R^T, Qm = Q; piv[j] = the column of W at position j.
-// Layout: a group of 8 lanes owns one column (group q = thread / 8, rows gl + 8 e, e < E) and
-// keeps its TRAILING part in registers: row j is finalised at step j (R_jq goes to a global
-// scratch, the register is zeroed), so no step needs row masks.  After every step the group
-// stores the column to shared memory, where the next step's pivot column is read by everyone.
-// The pivot is the argmax of the per-warp bests published at the previous step (every warp
-// reduces the same 32 entries in the same order); its x_j and exact ||x(j:)||^2 give the
-// reflector's scalars without a reduction; every group updates its column (v^T a: one 3-level
-// group reduction) and forms its exact trailing norm ||a(j+1:)||^2 (the next pivot key).
-// Q = H_0 ... H_{k-1} is accumulated afterwards column by column in registers, no barriers.
-constexpr int kQrThreads = 1024;
+// W = (Q V_x) S (P U_x)^T, so the Jacobi pair's CTA 1 starts its accumulator from Q instead of I
+// (forming Q = H_0 ... H_{k-1} from the reflectors itself, while CTA 0 runs the first segment)
+// and ends with U_w = Q V_x; CTA 0's normalised columns give V_w with rows permuted by P.
+// Outputs: Xt = R^T (k x k row-major), Hv = the reflectors (row j = v_j: 0 above j, vjj at j,
+// x below; then k scales beta_j = 2 / v_j^T v_j), piv[j] = the column of W at position j.
+// Layout: 8 warps; a group of 8 lanes owns four columns (q = group + 32 t, rows gl + 8 e) in
+// registers, stored to shared memory after every step (the next pivot column is read there).
+// A step: the pivot is the argmax of the 8 per-warp bests of the previous step (every warp
+// reduces the same entries in the same order); x_j and the exact ||x(j:)||^2 give the
+// reflector's scalars without a reduction; row j of every column moves to R (a global scratch)
+// and is cleared in the registers, so rows above j are zero everywhere and no step needs a row
+// mask; every group updates its columns (v^T a: one 3-level group reduction per column; column
+// slots finished in the whole warp are skipped) and forms their exact trailing
+// norms ||a(j+1:)||^2 (the next pivot keys); row j of R goes to a global scratch.
+constexpr int kQrThreads = 256;
 constexpr int kQrK = 128;
 
 template <int E>
 __global__ void __launch_bounds__(kQrThreads, 1)
-svd_qrcp_kernel(int k, const float* __restrict__ W, int64_t ldw, double* __restrict__ Xt, double* __restrict__ Qm,
-                int* __restrict__ piv_out, void* ws) {
+svd_qrcp_kernel(int k, const float* __restrict__ W, int64_t ldw, double* __restrict__ Xt, double* __restrict__ Hv,
+                double* __restrict__ Rg, int* __restrict__ piv_out, void* ws) {
   constexpr int KP = 8 * E;                      // padded column length
   extern __shared__ __align__(16) double qa[];  // [kQrK columns][KP rows]
-  __shared__ double s_wb[2][32];                // per-warp best key (-1: nothing left), by step parity
-  __shared__ int s_wi[2][32];
-  __shared__ double s_vj[kQrK], s_beta[kQrK], s_rd[kQrK];
+  __shared__ double s_wb[2][8];                 // per-warp best key (-1: nothing left), by step parity
+  __shared__ int s_wi[2][8];
+  __shared__ double s_rd[kQrK];
   __shared__ int s_piv[kQrK];
-  double* Rg = Qm;  // R above the diagonal by step and physical column, Rg[j k + q] (Q is written last)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int q = tid >> 3, gl = tid & 7;  // column, lane in the group (rows gl + 8 e)
-  double a[E];
+  const int g = tid >> 3, gl = tid & 7;  // group, lane in the group (rows gl + 8 e)
+  double a[4][E];
   bool bad = false;
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = gl + 8 * e;
-    float v = 0.f;
-    if (i < k && q < k) v = W[(int64_t)i * ldw + q];
-    bad |= !isfinite(v);
-    a[e] = static_cast<double>(v);
-  }
-  if (bad) set_status(ws, CABS_DEV_NONFINITE);
-  auto group_best = [&](double key, int par) {  // (key, column) argmax over the warp's 4 groups
-    int idx = q;
-#pragma unroll
-    for (int o = 8; o < 32; o <<= 1) {
-      const double ok = __shfl_xor_sync(0xffffffffu, key, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-      if (ok > key || (ok == key && oi < idx)) { key = ok; idx = oi; }
-    }
-    if (lane == 0) { s_wb[par][warp] = key; s_wi[par][warp] = idx; }
-  };
-  auto sq_sum = [&]() {
-    double n0 = 0.0, n1 = 0.0;
+  for (int t = 0; t < 4; ++t)
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      if (e & 1) n1 = fma(a[e], a[e], n1); else n0 = fma(a[e], a[e], n0);
+      const int i = gl + 8 * e, q = g + 32 * t;
+      float v = 0.f;
+      if (i < k && q < k) v = W[(int64_t)i * ldw + q];
+      bad |= !isfinite(v);
+      a[t][e] = static_cast<double>(v);
     }
-    return group_sum<8>(n0 + n1);
-  };
-  double* col = qa + (q < kQrK ? q : 0) * KP;
-  {
-    const double key = sq_sum();
-    group_best(q < k ? key : -1.0, 0);
+  if (bad) set_status(ws, CABS_DEV_NONFINITE);
+  uint32_t done = 0;  // bit t: column g + 32 t eliminated (or absent)
 #pragma unroll
-    for (int e = 0; e < E; ++e) col[gl + 8 * e] = a[e];
+  for (int t = 0; t < 4; ++t)
+    if (g + 32 * t >= k) done |= 1u << t;
+  // (key, column) argmax over the group's four columns and the warp's four groups -> s_wb
+  auto publish_best = [&](const double (&key)[4], int par) {
+    double bk = -1.0;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const double kk = ((done >> t) & 1) ? -1.0 : key[t];
+      if (kk > bk) { bk = kk; bi = g + 32 * t; }
+    }
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+      const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ok > bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+    }
+    if (lane == 0) { s_wb[par][warp] = bk; s_wi[par][warp] = bi; }
+  };
+  {
+    double key[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      double n0 = 0.0, n1 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (e & 1) n1 = fma(a[t][e], a[t][e], n1); else n0 = fma(a[t][e], a[t][e], n0);
+      }
+      key[t] = n0 + n1;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) key[t] = group_sum<8>(key[t]);
+    publish_best(key, 0);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int e = 0; e < E; ++e) qa[(g + 32 * t) * KP + gl + 8 * e] = a[t][e];
   }
-  bool done = q >= k;
   __syncthreads();
   for (int j = 0; j < k; ++j) {
     const int par = j & 1;
-    // pivot: argmax of the 32 warp bests (identical in every warp)
-    double bv = s_wb[par][lane];
-    int bq = s_wi[par][lane];
+    // pivot: argmax of the 8 warp bests (identical in every warp)
+    double bv = lane < 8 ? s_wb[par][lane] : -1.0;
+    int bq = lane < 8 ? s_wi[par][lane] : 0x7fffffff;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 4; o > 0; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
       if (ov > bv || (ov == bv && oq < bq)) { bv = ov; bq = oq; }
     }
-    const int ph = bq;
+    bv = __shfl_sync(0xffffffffu, bv, 0);
+    const int ph = __shfl_sync(0xffffffffu, bq, 0);
     const double* xp = qa + ph * KP;
     const double xj = xp[j], nn = fmax(bv, 0.0), sn = sqrt(nn);
     const double alpha = xj >= 0.0 ? -sn : sn;                           // R_jj
     const double vjj = xj - alpha;                                        // x_j + sign(x_j) ||x||
     const double beta = nn > 0.0 ? 1.0 / (sn * (sn + fabs(xj))) : 0.0;    // 2 / v^T v
-    const double aj = col[j];                                             // this column's row j
-    if (q == ph) done = true;
-    // (the shuffles are warp-wide: finished groups compute too and discard)
-    double d0 = gl == 0 ? (vjj - xj) * aj : 0.0, d1 = 0.0;  // v = x with x_j replaced by vjj
+    // every column's rows above j are zero (cleared at their step), the pivot's too
+    double x[E], mz[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      if (e & 1) d1 = fma(xp[gl + 8 * e], a[e], d1); else d0 = fma(xp[gl + 8 * e], a[e], d0);
+      x[e] = xp[gl + 8 * e];
+      mz[e] = gl + 8 * e == j ? 0.0 : 1.0;  // clears row j (it moves to R)
     }
-    const double f = beta * group_sum<8>(d0 + d1);
-    const int je = j >> 3, jl = j & 7;
-    if (!done) {
 #pragma unroll
-      for (int e = 0; e < E; ++e) a[e] = (e == je && gl == jl) ? 0.0 : fma(-f, xp[gl + 8 * e], a[e]);
+    for (int t = 0; t < 4; ++t)
+      if (g + 32 * t == ph) done |= 1u << t;
+    double aj[4], d[4], key[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      aj[t] = qa[(g + 32 * t) * KP + j];
+      d[t] = 0.0;
+      key[t] = -1.0;
     }
-    const double key = sq_sum();  // exact ||a(j+1:)||^2: the next pivot key
-    group_best(done ? -1.0 : key, par ^ 1);
-    if (!done && gl == 0) Rg[(size_t)j * k + q] = fma(-f, vjj, aj);  // R_jq
-    if (tid == 0) {
-      s_piv[j] = ph;
-      s_vj[j] = vjj;
-      s_beta[j] = beta;
-      s_rd[j] = alpha;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (!__any_sync(0xffffffffu, !((done >> t) & 1))) continue;  // the warp's columns t are all done
+      double d0 = gl == 0 ? (vjj - xj) * aj[t] : 0.0, d1 = 0.0;  // v = x with x_j replaced by vjj
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (e & 1) d1 = fma(x[e], a[t][e], d1); else d0 = fma(x[e], a[t][e], d0);
+      }
+      const double gsum = group_sum<8>(d0 + d1);  // (warp-wide shuffles: outside any branch)
+      d[t] = ((done >> t) & 1) ? 0.0 : beta * gsum;  // finished columns: a unchanged
+      double n0 = 0.0, n1 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        a[t][e] = fma(-d[t], x[e], a[t][e]) * mz[e];
+        if (e & 1) n1 = fma(a[t][e], a[t][e], n1); else n0 = fma(a[t][e], a[t][e], n0);
+      }
+      key[t] = group_sum<8>(n0 + n1);  // exact ||a(j+1:)||^2: the next pivot key
+    }
+    publish_best(key, par ^ 1);
+    if (gl == 0) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (!((done >> t) & 1)) Rg[(size_t)j * k + g + 32 * t] = fma(-d[t], vjj, aj[t]);  // R_jq
+    }
+    if (g == 0) {  // reflector j
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = gl + 8 * e;
+        if (i < k) Hv[(size_t)j * k + i] = i == j ? vjj : x[e];
+      }
+      if (gl == 0) {
+        Hv[(size_t)k * k + j] = beta;
+        s_piv[j] = ph;
+        s_rd[j] = alpha;
+      }
     }
     __syncthreads();  // every read of the pivot column is done ...
-    if (!done) {      // ... before the updated columns are stored (the pivot column keeps x)
 #pragma unroll
-      for (int e = 0; e < E; ++e) col[gl + 8 * e] = a[e];
-    }
+    for (int t = 0; t < 4; ++t)  // ... before the updated columns are stored (finished ones stay)
+      if (!((done >> t) & 1))
+#pragma unroll
+        for (int e = 0; e < E; ++e) qa[(g + 32 * t) * KP + gl + 8 * e] = a[t][e];
     __syncthreads();
   }
   // X = R^T: X[i][c] = R[c][i] = Rg[c][piv[i]] above the diagonal (c < i), R_ii on it, 0 below
@@ -962,42 +1011,10 @@ svd_qrcp_kernel(int k, const float* __restrict__ W, int64_t ldw, double* __restr
     Xt[e] = c < i ? Rg[(size_t)c * k + s_piv[i]] : (c == i ? s_rd[i] : 0.0);
   }
   if (tid < k) piv_out[tid] = s_piv[tid];
-  __syncthreads();  // Rg (= Qm) read before Q overwrites it
-  // Q = H_0 H_1 ... H_{k-1}: column q starts as e_q; H_j (v_j = column piv[j] as stored at its
-  // step: rows < j zero, x_j replaced by vjj) applied for j = min(q, k - 1) down to 0
-  if (warp * 4 < k) {  // warp-uniform loop from the warp's last column (shuffles are warp-wide)
-    double y[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) y[e] = (gl + 8 * e == q) ? 1.0 : 0.0;
-    const int jtop = min(warp * 4 + 3, k - 1);
-    for (int j = jtop; j >= 0; --j) {
-      const double* xp = qa + s_piv[j] * KP;
-      const double vjj = s_vj[j], xj = xp[j];
-      const int je = j >> 3, jl = j & 7;
-      double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const double v = (e == je && gl == jl) ? vjj : xp[gl + 8 * e];
-        if (e & 1) d1 = fma(v, y[e], d1); else d0 = fma(v, y[e], d0);
-      }
-      (void)xj;
-      const double gsum = group_sum<8>(d0 + d1);
-      const double f = j <= q ? s_beta[j] * gsum : 0.0;  // H_j e_q = e_q for j > q
-#pragma unroll
-      for (int e = 0; e < E; ++e) y[e] = fma(-f, (e == je && gl == jl) ? vjj : xp[gl + 8 * e], y[e]);
-    }
-    if (q < k) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int i = gl + 8 * e;
-        if (i < k) Qm[(size_t)i * k + q] = y[e];
-      }
-    }
-  }
 }
 
 template <int E>
-static void launch_qrcp_e(int k, const float* W, int64_t ldw, double* Xt, double* Qm, int* piv, void* ws,
+static void launch_qrcp_e(int k, const float* W, int64_t ldw, double* Xt, double* Hv, double* Rg, int* piv, void* ws,
                           cudaStream_t st) {
   constexpr size_t smem = sizeof(double) * kQrK * 8 * E;
   static bool attr = false;
@@ -1005,17 +1022,17 @@ static void launch_qrcp_e(int k, const float* W, int64_t ldw, double* Xt, double
     cudaFuncSetAttribute(svd_qrcp_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  svd_qrcp_kernel<E><<<1, kQrThreads, smem, st>>>(k, W, ldw, Xt, Qm, piv, ws);
+  svd_qrcp_kernel<E><<<1, kQrThreads, smem, st>>>(k, W, ldw, Xt, Hv, Rg, piv, ws);
 }
 
-static bool launch_qrcp(int k, const float* W, int64_t ldw, double* Xt, double* Qm, int* piv, void* ws,
+static bool launch_qrcp(int k, const float* W, int64_t ldw, double* Xt, double* Hv, double* Rg, int* piv, void* ws,
                         cudaStream_t st) {
   if (k > kQrK) return false;
   note_launch();
-  if (k <= 32) launch_qrcp_e<4>(k, W, ldw, Xt, Qm, piv, ws, st);
-  else if (k <= 64) launch_qrcp_e<8>(k, W, ldw, Xt, Qm, piv, ws, st);
-  else if (k <= 104) launch_qrcp_e<13>(k, W, ldw, Xt, Qm, piv, ws, st);
-  else launch_qrcp_e<16>(k, W, ldw, Xt, Qm, piv, ws, st);
+  if (k <= 32) launch_qrcp_e<4>(k, W, ldw, Xt, Hv, Rg, piv, ws, st);
+  else if (k <= 64) launch_qrcp_e<8>(k, W, ldw, Xt, Hv, Rg, piv, ws, st);
+  else if (k <= 104) launch_qrcp_e<13>(k, W, ldw, Xt, Hv, Rg, piv, ws, st);
+  else launch_qrcp_e<16>(k, W, ldw, Xt, Hv, Rg, piv, ws, st);
   return true;
 }
 
@@ -1038,7 +1055,8 @@ svd_quad_kernel(int k, int nseg, const float* __restrict__ W, int64_t ldw, const
                 const double* __restrict__ Qm, const int* __restrict__ piv, double tol, double* __restrict__ sigma_out,
                 double* __restrict__ Uw64, double* __restrict__ Vw64, float* __restrict__ uw32,
                 float* __restrict__ vw32, int64_t ld32, int* r_out, int* r_out2, void* ws) {
-  // Xt != nullptr: QR-preconditioned (svd_qrcp_kernel): CTA 0 starts from X = R^T, CTA 1 from Q;
+  // Xt != nullptr: QR-preconditioned (svd_qrcp_kernel): CTA 0 starts from X = R^T, CTA 1 from Q
+  // (formed from the reflectors Qm = Hv);
   // at the end CTA 1 holds U_w = Q V_x and CTA 0 the columns of V_w (rows permuted by piv)
   const bool pre = Xt != nullptr;
   constexpr int G = 32 / LP;
@@ -1080,15 +1098,52 @@ svd_quad_kernel(int k, int nseg, const float* __restrict__ W, int64_t ldw, const
   int id[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) id[c] = 4 * g + c;
-  if (pre) {
-    const double* src = crank == 0 ? Xt : Qm;
+  if (pre && crank == 0) {
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int i = gl + LP * e;
-        a[c][e] = (live && i < k && id[c] < k) ? src[(size_t)i * k + id[c]] : 0.0;
+        a[c][e] = (live && i < k && id[c] < k) ? Xt[(size_t)i * k + id[c]] : 0.0;
       }
+  } else if (pre) {
+    // Q = H_0 H_1 ... H_{k-1} applied to this slot's unit columns, reflectors from the QR
+    // kernel (Qm = Hv: row j = v_j, then the k scales); hidden behind CTA 0's first segment
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int e = 0; e < E; ++e) a[c][e] = (live && gl + LP * e == id[c] && id[c] < k) ? 1.0 : 0.0;
+    double vn[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) vn[e] = gl + LP * e < k ? Qm[(size_t)(k - 1) * k + gl + LP * e] : 0.0;
+    double bn = Qm[(size_t)k * k + k - 1];
+    for (int j = k - 1; j >= 0; --j) {
+      double v[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = vn[e];
+      const double bj = bn;
+      if (j > 0) {  // prefetch the next reflector
+#pragma unroll
+        for (int e = 0; e < E; ++e) vn[e] = gl + LP * e < k ? Qm[(size_t)(j - 1) * k + gl + LP * e] : 0.0;
+        bn = Qm[(size_t)k * k + j - 1];
+      }
+      double dq[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if (e & 1) d1 = fma(v[e], a[c][e], d1); else d0 = fma(v[e], a[c][e], d0);
+        }
+        dq[c] = d0 + d1;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dq[c] = bj * group_sum<LP>(dq[c]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int e = 0; e < E; ++e) a[c][e] = fma(-dq[c], v[e], a[c][e]);
+    }
   } else if (crank == 0) {
     bool bad = false;
 #pragma unroll
@@ -1514,9 +1569,10 @@ static bool launch_quad(int k, const float* W, int64_t ldw, double tol, double* 
   const int* piv = nullptr;
   if (L && k > 2 && !getenv("CABS_SVD_NOQR")) {
     double* x = wsp<double>(ws, L->a64);
-    double* q = wsp<double>(ws, L->v64);
-    int* pv = reinterpret_cast<int*>(x + (size_t)L->K * L->K);
-    if (launch_qrcp(k, W, ldw, x, q, pv, ws, st)) { Xt = x; Qm = q; piv = pv; }
+    double* hv = wsp<double>(ws, L->v64);
+    double* rg = wsp<double>(ws, L->qr);
+    int* pv = reinterpret_cast<int*>(rg + (size_t)L->K * L->K);
+    if (launch_qrcp(k, W, ldw, x, hv, rg, pv, ws, st)) { Xt = x; Qm = hv; piv = pv; }
   }
   svd_quad_kernel<LP, E, KM><<<2, 32 * nw, smem, st>>>(k, nseg, W, ldw, Xt, Qm, piv, tol, sig, Uw64, Vw64, uw32, vw32,
                                                        ld32, r_ws, r_user, ws);
