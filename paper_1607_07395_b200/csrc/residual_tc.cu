@@ -119,6 +119,32 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float (&v)[32])
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 64 columns of 32-bit TMEM -> registers, load and wait in one statement
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v)[64]) {
+  uint32_t r[64];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ unsigned long long rs_pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ unsigned long long rs_fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float rs_lo(unsigned long long v) { return __uint_as_float(static_cast<unsigned>(v)); }
+__device__ __forceinline__ float rs_hi(unsigned long long v) { return __uint_as_float(static_cast<unsigned>(v >> 32)); }
+
 // after tcgen05.wait::ld: ties the registers of a no-wait load to this point (volatile asm
 // order), so no use can be scheduled before the wait
 __device__ __forceinline__ void tmem_regs_fence(float (&v)[32]) {
@@ -370,8 +396,10 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
                 const uint32_t fh = fh0 + static_cast<uint32_t>(8 * q);
                 if (H) {
                   mma_f16_ts(d, fh, bh + 2 * q, idesc, (c | q) ? 1u : 0u);
-                  mma_f16_ts(d, fh, bl + 2 * q, idesc, 1u);
-                  mma_f16_ts(d, fh + static_cast<uint32_t>(kp), bh + 2 * q, idesc, 1u);
+                  if (!(dbg & 8)) {
+                    mma_f16_ts(d, fh, bl + 2 * q, idesc, 1u);
+                    mma_f16_ts(d, fh + static_cast<uint32_t>(kp), bh + 2 * q, idesc, 1u);
+                  }
                 } else {
                   mma_tf32_ts(d, fh, bh + 2 * q, idesc, (c | q) ? 1u : 0u);
                   if (!(dbg & 8)) {
@@ -433,51 +461,54 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         inv = 1.f / (f_row_scale(fa, m, rb * kTcBM + row) * gs);  // a power of two: exact
       }
       const int sc = static_cast<int>(i % nacc);
-      RES_WAIT(11, tc::mbar_wait(&S.acc_full[sc], ring_parity(i, nacc)));
-      tc::fence_after_sync();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(sc * kTcBN);
-      float tr0 = 0.f, ta0 = 0.f, tr1 = 0.f, ta1 = 0.f;
-      // the group's two 32-column halves one after the other (register budget): the A box
-      // (rows of a 128B-swizzled box: 16-byte chunk c of row r is at chunk c ^ (r & 7)),
-      // released once in registers, and the matching 32 accumulator columns
+      // the group's 64 columns: both A boxes (rows of a 128B-swizzled box: 16-byte chunk c of row
+      // r is at chunk c ^ (r & 7)) into registers and released, then (acc_full) the 64 accumulator columns
+      // in one TMEM load (the stage is released right after), then the sums in packed FP32 pairs
+      // (e = a - inv acc exactly as a - (acc inv): inv is a power of two)
+      float av[64], v[64];
 #pragma unroll
       for (int hh = 0; hh < kHalf; ++hh) {
         const int64_t li = kHalfAQ * i + hh;
         const int sa = eg * kAR + static_cast<int>(li % kAR);
-        float av[32], v[32];
         RES_WAIT(10, tc::mbar_wait(&S.a_full[sa], ring_parity(li, kAR)));
         const uint8_t* arow = S.a[sa] + row * 128;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const float4 a4 = *reinterpret_cast<const float4*>(arow + ((c ^ (row & 7)) << 4));
-          av[4 * c] = a4.x; av[4 * c + 1] = a4.y; av[4 * c + 2] = a4.z; av[4 * c + 3] = a4.w;
+          av[32 * hh + 4 * c] = a4.x; av[32 * hh + 4 * c + 1] = a4.y;
+          av[32 * hh + 4 * c + 2] = a4.z; av[32 * hh + 4 * c + 3] = a4.w;
         }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&S.a_empty[sa]);
-        // load + wait back to back: between a no-wait tcgen05.ld and its wait the compiler may
-        // move or reuse the destination registers, which the load then overwrites asynchronously
-        tc::tmem_ld32(tbase + 32 * (kHalf * eg + hh), v);
-        if (dbg & 1) {
+      }
+      __syncwarp();
+      if (lane == 0) {
 #pragma unroll
-          for (int x = 0; x < 32; ++x) v[x] = 0.f;
-        }
-        if (H) {
+        for (int hh = 0; hh < kHalf; ++hh)
+          tc::mbar_arrive(&S.a_empty[eg * kAR + static_cast<int>((kHalfAQ * i + hh) % kAR)]);
+      }
+      // the A slots are free BEFORE the wait for the tile's accumulator: the producer streams the
+      // next tile's A while the MMA finishes this one
+      RES_WAIT(11, tc::mbar_wait(&S.acc_full[sc], ring_parity(i, nacc)));
+      tc::fence_after_sync();
+      tmem_ld64(tbase + 32 * kHalf * eg, v);
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);  // the accumulator stage is in registers
+      if (dbg & 1) {
 #pragma unroll
-          for (int x = 0; x < 32; ++x) v[x] *= inv;
-        }
-        if (hh == kHalf - 1) {  // the accumulator stage is in registers: release it
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);
-        }
+        for (int x = 0; x < 64; ++x) v[x] = 0.f;
+      }
+      const unsigned long long ninv = rs_pack(H ? -inv : -1.f, H ? -inv : -1.f);
+      unsigned long long tr0 = 0ull, tr1 = 0ull, ta0 = 0ull, ta1 = 0ull;  // (even, odd) column pairs
 #pragma unroll
-        for (int x = 0; x < 32; x += 2) {
-          const float e0 = av[x] - v[x], e1 = av[x + 1] - v[x + 1];
-          tr0 = fmaf(e0, e0, tr0);
-          ta0 = fmaf(av[x], av[x], ta0);
-          tr1 = fmaf(e1, e1, tr1);
-          ta1 = fmaf(av[x + 1], av[x + 1], ta1);
-        }
+      for (int x = 0; x < 64; x += 4) {
+        const unsigned long long a01 = rs_pack(av[x], av[x + 1]), a23 = rs_pack(av[x + 2], av[x + 3]);
+        const unsigned long long e01 = rs_fma2(ninv, rs_pack(v[x], v[x + 1]), a01);
+        const unsigned long long e23 = rs_fma2(ninv, rs_pack(v[x + 2], v[x + 3]), a23);
+        tr0 = rs_fma2(e01, e01, tr0);
+        ta0 = rs_fma2(a01, a01, ta0);
+        tr1 = rs_fma2(e23, e23, tr1);
+        ta1 = rs_fma2(a23, a23, ta1);
       }
       // nf = 1: the band's last tile is in registers; the MMA released the F buffer when it
       // finished this tile (f_free commits after the tile's MMAs): load the next band now
@@ -487,8 +518,8 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         tc::fence_after_sync();
         load_band(rb + 1, fcol0, &S.f_ready[0]);
       }
-      r2 += static_cast<double>(tr0 + tr1);
-      a2 += static_cast<double>(ta0 + ta1);
+      r2 += static_cast<double>((rs_lo(tr0) + rs_hi(tr0)) + (rs_lo(tr1) + rs_hi(tr1)));
+      a2 += static_cast<double>((rs_lo(ta0) + rs_hi(ta0)) + (rs_lo(ta1) + rs_hi(ta1)));
     }
     r2 = warp_sum_d(r2);
     a2 = warp_sum_d(a2);
@@ -886,8 +917,12 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
     const int64_t g = T < nsm ? T : nsm;
     const int ksteps = static_cast<int>(ceil_div(ncomp, 16));
     note_launch();
+    int dbg16 = 0;
+#ifdef CABS_PROFILE_RES
+    if (const char* e = getenv("CABS_RES_DBG")) dbg16 = atoi(e);
+#endif
     residual_tc_kernel<true><<<static_cast<unsigned>(g), kTcThreads, smem, st>>>(tA, tGh, tGl, fa, m_loc, n, ksteps, tp,
-                                                                                part, gmax, 0);
+                                                                                part, gmax, dbg16);
     launch_residual_final(part, static_cast<int>(g), out, st);
     return 0;
   }
