@@ -1213,9 +1213,11 @@ svd_quad_kernel(int k, int nseg, const float* __restrict__ W, int64_t ldw, const
       od = 1.0;
       oi = 1.0;
     }
-    for (int rnd = 0; rnd < n4; rnd += 2) {
-      const int seg = rnd / HS, gs = sweep * nseg + seg, bp = gs & 1;  // segment, global index, parity
-      if (rnd == seg * HS) {  // segment start: CTA 0 needs a free buffer, CTA 1 a full one
+    int seg = 0, sro = 0;  // segment of the sweep, round offset inside it (no division in the loop)
+    for (int rnd = 0; rnd < n4; rnd += 2, sro += 2) {
+      if (sro == HS) { ++seg; sro = 0; }
+      const int gs = sweep * nseg + seg, bp = gs & 1;  // global segment index, its buffer parity
+      if (sro == 0) {  // segment start: CTA 0 needs a free buffer, CTA 1 a full one
 #ifdef CABS_PROFILE_SVD
         const long long w0 = clock64();
 #endif
@@ -1226,7 +1228,7 @@ svd_quad_kernel(int k, int nseg, const float* __restrict__ W, int64_t ldw, const
 #endif
       }
       // ---- even round: pairs (0,1) (lanes 0-3) and (2,3) (lanes 4-7), rotated and swapped
-      const int pidx = ((bp * HS + rnd - seg * HS) * Q + (live ? g : 0)) * 4;  // [parity][round][slot][4]
+      const int pidx = ((bp * HS + sro) * Q + (live ? g : 0)) * 4;  // [parity][round][slot][4]
       double al01, be01, al23, be23;
       if (crank == 0) {
         double p01a = 0.0, p01b = 0.0, p23a = 0.0, p23b = 0.0;
@@ -1359,7 +1361,7 @@ svd_quad_kernel(int k, int nseg, const float* __restrict__ W, int64_t ldw, const
       }
       if (!lastslot) id[3] = s_id[par][0][g + 2];
       if (!first) id[0] = s_id[par][1][g];
-      if (rnd + 2 == (seg + 1) * HS && seg + 1 < nseg) {  // segment end inside the sweep: hand over
+      if (sro + 2 == HS && seg + 1 < nseg) {  // segment end inside the sweep: hand over
         __syncthreads();
         if (tid == 0) {
           if (crank == 0) {
@@ -1574,6 +1576,7 @@ static bool launch_quad(int k, const float* W, int64_t ldw, double tol, double* 
     int* pv = reinterpret_cast<int*>(rg + (size_t)L->K * L->K);
     if (launch_qrcp(k, W, ldw, x, hv, rg, pv, ws, st)) { Xt = x; Qm = hv; piv = pv; }
   }
+  note_launch();
   svd_quad_kernel<LP, E, KM><<<2, 32 * nw, smem, st>>>(k, nseg, W, ldw, Xt, Qm, piv, tol, sig, Uw64, Vw64, uw32, vw32,
                                                        ld32, r_ws, r_user, ws);
   return true;
@@ -1680,6 +1683,7 @@ static void launch_systolic(int k, const float* W, int64_t ldw, double tol, doub
     cudaFuncSetAttribute(svd_systolic_kernel<LP, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr = true;
   }
+  note_launch();
   svd_systolic_kernel<LP, E><<<1, 32 * nw, smem, st>>>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws,
                                                       r_user, ws);
 }
@@ -1702,6 +1706,7 @@ static bool launch_split(int k, const float* W, int64_t ldw, double tol, double*
     cudaFuncSetAttribute(svd_split_kernel<LP, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCap);
     attr = true;
   }
+  note_launch();
   svd_split_kernel<LP, E><<<2, 32 * nw, smem, st>>>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user,
                                                     ws);
   return true;
@@ -1713,7 +1718,7 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
   int* r_ws = wsp<int>(ws, L.scal) + SCAL_R_TMP;
   float* uw32 = wsp<float>(ws, L.uw32);
   float* vw32 = wsp<float>(ws, L.vw32);
-  note_launch();
+  // (every launcher notes its own kernel launches: the QR preconditioner adds one)
   if (k <= 64 && !getenv("CABS_SVD_SMEM") && !getenv("CABS_SVD_ONE_SM")) {
     // A on one SM, V on its cluster partner; four columns per 8-lane slot (the two-column
     // svd_split_kernel stays selectable for comparison)
@@ -1761,6 +1766,7 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
               : k <= kSvdSmemK ? svd_jacobi_kernel<4, true> : k <= 128 ? svd_jacobi_kernel<4, false>
               : k <= 256 ? svd_jacobi_kernel<8, false> : k <= 320 ? svd_jacobi_kernel<10, false>
                          : svd_jacobi_kernel<32, false>;
+    note_launch();
     kern<<<1, kSvdThreads, smem, st>>>(k, W, ldw, tol, wsp<double>(ws, L.a64), wsp<double>(ws, L.v64), sig, Uw64, Vw64,
                                        uw32, vw32, L.Kp, r_ws, r_user, use_smem, ws);
   }
