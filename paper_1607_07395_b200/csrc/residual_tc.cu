@@ -392,7 +392,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           if (tc::elect_one()) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              if (q < nk) {
+              if (q < nk && !(dbg & 64)) {
                 const uint32_t fh = fh0 + static_cast<uint32_t>(8 * q);
                 if (H) {
                   mma_f16_ts(d, fh, bh + 2 * q, idesc, (c | q) ? 1u : 0u);
@@ -475,7 +475,8 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         const uint8_t* arow = S.a[sa] + row * 128;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const float4 a4 = *reinterpret_cast<const float4*>(arow + ((c ^ (row & 7)) << 4));
+          const float4 a4 = (dbg & 32) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                       : *reinterpret_cast<const float4*>(arow + ((c ^ (row & 7)) << 4));
           av[32 * hh + 4 * c] = a4.x; av[32 * hh + 4 * c + 1] = a4.y;
           av[32 * hh + 4 * c + 2] = a4.z; av[32 * hh + 4 * c + 3] = a4.w;
         }
@@ -490,7 +491,12 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       // next tile's A while the MMA finishes this one
       RES_WAIT(11, tc::mbar_wait(&S.acc_full[sc], ring_parity(i, nacc)));
       tc::fence_after_sync();
-      tmem_ld64(tbase + 32 * kHalf * eg, v);
+      if (dbg & 16) {  // diagnostics: no TMEM read
+#pragma unroll
+        for (int x = 0; x < 64; ++x) v[x] = av[x] * 0.5f;
+      } else {
+        tmem_ld64(tbase + 32 * kHalf * eg, v);
+      }
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&S.acc_empty[sc]);  // the accumulator stage is in registers
