@@ -1250,7 +1250,11 @@ svd_quad_kernel(int k, int nseg, const float* __restrict__ W, int64_t ldw, const
         const double pd = __shfl_xor_sync(0xffffffffu, od, 2);
         const double pi = __shfl_xor_sync(0xffffffffu, oi, 2);
         LaneRot r;
+#if defined(SVQ_EXP) && (SVQ_EXP & 1)  // diagnostics: a cheap stand-in for the rotation chain
+        r.t = gsum * 1e-30; r.need = false; r.tu = r.t; r.tv = r.t; r.n = on; r.d = od; r.i = oi; (void)pn; (void)pd; (void)pi;
+#else
         lane_rot(!mid, on, od, oi, pn, pd, pi, gsum, tol_rot2, r);
+#endif
         al01 = __shfl_sync(0xffffffffu, r.tu, base);  // lanes 0 and 4: left lanes
         be01 = __shfl_sync(0xffffffffu, r.tv, base);
         al23 = __shfl_sync(0xffffffffu, r.tu, base + 4);
@@ -1293,7 +1297,9 @@ svd_quad_kernel(int k, int nseg, const float* __restrict__ W, int64_t ldw, const
       if (crank == 0 && (gl & 1) == 0) {  // every position's n, d, 1 / d: [parity][seat][position]
         s_st[par][g + 1][own][0] = on; s_st[par][g + 1][own][1] = od; s_st[par][g + 1][own][2] = oi;
       }
+#if !(defined(SVQ_EXP) && (SVQ_EXP & 2))  // diagnostics: no barrier (wrong data, timing only)
       __syncthreads();
+#endif
       const size_t lft = ((size_t)par * nseat + g) * SEAT + gl;      // left slot's column 3
       const size_t rgt = ((size_t)par * nseat + g + 2) * SEAT + gl;  // right slot's column 0
       double rl[E], rr[E];
@@ -1328,7 +1334,11 @@ svd_quad_kernel(int k, int nseg, const float* __restrict__ W, int64_t ldw, const
         const int pseat = own == 0 ? g : (own == 3 ? g + 2 : g + 1), ppos = own ^ 3;
         const double* ps = s_st[par][pseat][ppos];
         LaneRot r;
+#if defined(SVQ_EXP) && (SVQ_EXP & 1)
+        r.t = gsum * 1e-30; r.need = false; r.tu = r.t; r.tv = r.t; r.n = on; r.d = od; r.i = oi; (void)ps;
+#else
         lane_rot(mid, on, od, oi, ps[0], ps[1], ps[2], gsum, tol_rot2, r);
+#endif
         al12 = __shfl_sync(0xffffffffu, r.tu, base + 2);  // lanes 2 and 6: left lanes
         be12 = __shfl_sync(0xffffffffu, r.tv, base + 2);
         const double alR0 = __shfl_sync(0xffffffffu, r.tu, base + 6);
