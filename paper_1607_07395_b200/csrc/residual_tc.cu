@@ -280,7 +280,13 @@ template <bool H>
 __global__ void __launch_bounds__(kTcThreads, 1)
 residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmGh,
                    const __grid_constant__ CUtensorMap tmGl, const FArgs fa, int64_t m, int64_t n, int ksteps,
-                   const TmemPlan tp, double* __restrict__ part, const unsigned* __restrict__ gmax_bits, int dbg) {
+                   const TmemPlan tp, double* __restrict__ part, const unsigned* __restrict__ gmax_bits, int dbg_arg) {
+#ifdef CABS_PROFILE_RES
+  const int dbg = dbg_arg;  // diagnostics switches (profiling builds only)
+#else
+  constexpr int dbg = 0;    // the diagnostics paths compile away
+  (void)dbg_arg;
+#endif
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -314,15 +320,20 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint64_t pol = tc::policy_evict_first();  // A is read exactly once
+      // tile coordinates and ring positions advanced incrementally (no 64-bit divisions per tile)
+      int64_t rb = t_beg / ntc, cb = t_beg % ntc;
+      int as = 0;          // ring slot (both groups' rings advance in step)
+      uint32_t aph = 0;    // phase parity of that slot's current use
       for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
-        const int64_t rb = t / ntc, cb = t % ntc;
         // A (the HBM stream the kernel is bound by): kAQ boxes of 128 x 32 per tile
-        for (int h = 0; h < kAQ; ++h) {
-          // box h of the tile goes to the ring of the epilogue group reading it (columns
-          // [0, 64) group 0, [64, 128) group 1); li = its index within that ring's sequence
-          const int64_t li = kHalfAQ * i + (h % kHalfAQ);
-          const int sa = (h / kHalfAQ) * kAR + static_cast<int>(li % kAR);
-          if (li >= kAR) RES_WAIT(1, tc::mbar_wait(&S.a_empty[sa], ring_parity(li - kAR, kAR)));
+        for (int hh = 0; hh < kHalfAQ; ++hh) {
+          // box hh of each group: slot as of the group's ring; li = kHalfAQ i + hh is its index in
+          // that ring's sequence, so the wait is for the use li - kAR (parity aph ^ 1)
+          const int64_t li = kHalfAQ * i + hh;
+          for (int grp = 0; grp < 2; ++grp) {
+          const int h = grp * kHalfAQ + hh;
+          const int sa = grp * kAR + as;
+          if (li >= kAR) RES_WAIT(1, tc::mbar_wait(&S.a_empty[sa], aph ^ 1u));
           if ((dbg & 4) && i > 0) {  // diagnostics: no A traffic after the first tile
             tc::mbar_arrive(&S.a_full[sa]);
             continue;
@@ -330,7 +341,10 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           tc::mbar_expect_tx(&S.a_full[sa], kABoxBytes);
           tc::tma_load_2d_hint(S.a[sa], &tmA, static_cast<int>(cb * kTcBN + 32 * h), static_cast<int>(rb * kTcBM),
                                &S.a_full[sa], pol);
+          }
+          if (++as == kAR) { as = 0; aph ^= 1u; }
         }
+        if (++cb == ntc) { cb = 0; ++rb; }
       }
     }
   } else if (warp == 6) {
@@ -339,8 +353,8 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     if (lane == 0) {
       const uint64_t pol = tc::policy_evict_last();  // G is re-read by every row band
       int64_t j = 0;  // chunk sequence number
-      for (int64_t t = t_beg; t < t_end; ++t) {
-        const int64_t cb = t % ntc;
+      int64_t cb = t_beg % ntc;
+      for (int64_t t = t_beg; t < t_end; ++t, cb = (cb + 1 == ntc) ? 0 : cb + 1) {
         for (int c = 0; c < nch; ++c, ++j) {
           const int sg = static_cast<int>(j % kGS);
           if (j >= kGS) RES_WAIT(2, tc::mbar_wait(&S.g_empty[sg], ring_parity(j - kGS, kGS)));
@@ -367,9 +381,10 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       const uint64_t dgh0 = tc::desc_sw128(tc::smem_u32(S.gh[0])), dgl0 = tc::desc_sw128(tc::smem_u32(S.gl[0]));
       int64_t prev_rb = -1, band = -1, j = 0;
       uint32_t fcol = 0;
+      int64_t rb = t_beg / ntc, cbm = t_beg % ntc;  // advanced incrementally below
+      int sc = 0;
+      uint32_t accph = 0;  // parity of the current use of stage sc
       for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
-        const int64_t rb = t / ntc;
-        const int sc = static_cast<int>(i % nacc);
         if (rb != prev_rb) {
           if (band >= 0 && tc::elect_one()) tc::mma_commit(&S.f_free[band % nf]);  // previous band's F no longer read
           __syncwarp();
@@ -378,7 +393,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           fcol = fcol0 + static_cast<uint32_t>((band % nf) * 2 * kp);
           prev_rb = rb;
         }
-        if (i >= nacc) RES_WAIT(6, tc::mbar_wait(&S.acc_empty[sc], ring_parity(i - nacc, nacc)));
+        if (i >= nacc) RES_WAIT(6, tc::mbar_wait(&S.acc_empty[sc], accph ^ 1u));
         tc::fence_after_sync();
         const uint32_t d = tmem + static_cast<uint32_t>(sc * kTcBN);
         for (int c = 0; c < nch; ++c, ++j) {
@@ -415,6 +430,8 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         }
         if (tc::elect_one()) tc::mma_commit(&S.acc_full[sc]);
         __syncwarp();
+        if (++sc == nacc) { sc = 0; accph ^= 1u; }
+        if (++cbm == ntc) { cbm = 0; ++rb; }
       }
     }
   } else {
@@ -444,8 +461,10 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     float inv = 1.f;
     double r2 = 0.0, a2 = 0.0;
     int64_t prev_rb = rb0;
+    int64_t rb = rb0, cbe = t_beg % ntc;  // advanced incrementally below
+    int sc = 0, as = 0;                   // accumulator stage, A ring slot (of this group)
+    uint32_t accph = 0, aph = 0;          // their phase parities
     for (int64_t t = t_beg, i = 0; t < t_end; ++t, ++i) {
-      const int64_t rb = t / ntc;
       if (nf == 2 && rb != prev_rb && eg == 0) {  // entering band j: stage band j + 1 into band j - 1's buffer
         prev_rb = rb;
         const int64_t jb = rb - rb0;
@@ -460,7 +479,6 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         inv_rb = rb;
         inv = 1.f / (f_row_scale(fa, m, rb * kTcBM + row) * gs);  // a power of two: exact
       }
-      const int sc = static_cast<int>(i % nacc);
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(sc * kTcBN);
       // the group's 64 columns: both A boxes (rows of a 128B-swizzled box: 16-byte chunk c of row
       // r is at chunk c ^ (r & 7)) into registers and released, then (acc_full) the 64 accumulator columns
@@ -468,15 +486,22 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       // (e = a - inv acc exactly as a - (acc inv): inv is a power of two)
       float av[64], v[64];
 #pragma unroll
+      int sas[kHalf];
       for (int hh = 0; hh < kHalf; ++hh) {
-        const int64_t li = kHalfAQ * i + hh;
-        const int sa = eg * kAR + static_cast<int>(li % kAR);
-        RES_WAIT(10, tc::mbar_wait(&S.a_full[sa], ring_parity(li, kAR)));
-        const uint8_t* arow = S.a[sa] + row * 128;
+        const int sa = eg * kAR + as;
+        sas[hh] = sa;
+        RES_WAIT(10, tc::mbar_wait(&S.a_full[sa], aph));
+        if (++as == kAR) { as = 0; aph ^= 1u; }
+        // 32-bit shared-memory addresses (S is reached through an aligned generic pointer, so plain
+        // C++ loads would be generic LD with 64-bit address arithmetic)
+        const uint32_t arow = tc::smem_u32(S.a[sa]) + static_cast<uint32_t>(row * 128);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const float4 a4 = (dbg & 32) ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                       : *reinterpret_cast<const float4*>(arow + ((c ^ (row & 7)) << 4));
+          float4 a4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (!(dbg & 32))
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(a4.x), "=f"(a4.y), "=f"(a4.z), "=f"(a4.w)
+                         : "r"(arow + static_cast<uint32_t>((c ^ (row & 7)) << 4)));
           av[32 * hh + 4 * c] = a4.x; av[32 * hh + 4 * c + 1] = a4.y;
           av[32 * hh + 4 * c + 2] = a4.z; av[32 * hh + 4 * c + 3] = a4.w;
         }
@@ -484,12 +509,11 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       __syncwarp();
       if (lane == 0) {
 #pragma unroll
-        for (int hh = 0; hh < kHalf; ++hh)
-          tc::mbar_arrive(&S.a_empty[eg * kAR + static_cast<int>((kHalfAQ * i + hh) % kAR)]);
+        for (int hh = 0; hh < kHalf; ++hh) tc::mbar_arrive(&S.a_empty[sas[hh]]);
       }
       // the A slots are free BEFORE the wait for the tile's accumulator: the producer streams the
       // next tile's A while the MMA finishes this one
-      RES_WAIT(11, tc::mbar_wait(&S.acc_full[sc], ring_parity(i, nacc)));
+      RES_WAIT(11, tc::mbar_wait(&S.acc_full[sc], accph));
       tc::fence_after_sync();
       if (dbg & 16) {  // diagnostics: no TMEM read
 #pragma unroll
@@ -518,7 +542,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       }
       // nf = 1: the band's last tile is in registers; the MMA released the F buffer when it
       // finished this tile (f_free commits after the tile's MMAs): load the next band now
-      if (nf == 1 && eg == 0 && t + 1 < t_end && (t + 1) / ntc != rb) {
+      if (nf == 1 && eg == 0 && t + 1 < t_end && cbe + 1 == ntc) {
         const int64_t jb = rb - rb0;
         tc::mbar_wait(&S.f_free[0], static_cast<uint32_t>(jb & 1));
         tc::fence_after_sync();
@@ -526,6 +550,8 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       }
       r2 += static_cast<double>((rs_lo(tr0) + rs_hi(tr0)) + (rs_lo(tr1) + rs_hi(tr1)));
       a2 += static_cast<double>((rs_lo(ta0) + rs_hi(ta0)) + (rs_lo(ta1) + rs_hi(ta1)));
+      if (++sc == nacc) { sc = 0; accph ^= 1u; }
+      if (++cbe == ntc) { cbe = 0; ++rb; }
     }
     r2 = warp_sum_d(r2);
     a2 = warp_sum_d(a2);
