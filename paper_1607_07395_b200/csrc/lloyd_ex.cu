@@ -837,7 +837,10 @@ static bool lex_launch(LexArgs& a, int njobs, const LloydJob* jobs, int iters, i
     if (tot < c * njobs) continue;
     int64_t g[2] = {tot, 0};
     if (njobs > 1) {
-      g[0] = (int64_t)llround(static_cast<double>(tot) * static_cast<double>(jobs[0].N) / Ntot / c) * c;
+      // CTAs in proportion to the points (CABS_KM_SPLIT = the first problem's share, diagnostics)
+      double share = static_cast<double>(jobs[0].N) / Ntot;
+      if (const char* e = getenv("CABS_KM_SPLIT")) share = atof(e);
+      g[0] = (int64_t)llround(static_cast<double>(tot) * share / c) * c;
       g[0] = g[0] < c ? c : (g[0] > tot - c ? tot - c : g[0]);
       g[1] = tot - g[0];
     }
