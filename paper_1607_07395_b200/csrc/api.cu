@@ -288,10 +288,17 @@ static int32_t embed_core(const cabs_plan& p, const Ws& L, int32_t k, const floa
     CABS_LAUNCH_CHECK("embed_fused");
     return CABS_OK;
   }
+  // the two products (Y_c = C V_w here, Y_r = R^T U_w on the side stream) run concurrently
+  SideStream* ss = nullptr;
+  CABS_TRY(side_stream(&ss));
+  CABS_CUDA_TRY(cudaEventRecord(ss->fork, st));
+  CABS_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
   if (m_loc > 0) CABS_CUDA_TRY(cudaMemsetAsync(Y1, 0, sizeof(float) * ld1 * m_loc, st));
-  if (n_sl > 0) CABS_CUDA_TRY(cudaMemsetAsync(Y2, 0, sizeof(float) * ld2 * n_sl, st));
-  launch_embed_products(m_loc, n_sl, k, C, ldc, R + p.col_begin, ldr, Y1, ld1, Y2, ld2, ws, L, st);
+  if (n_sl > 0) CABS_CUDA_TRY(cudaMemsetAsync(Y2, 0, sizeof(float) * ld2 * n_sl, ss->s));
+  launch_embed_products(m_loc, n_sl, k, C, ldc, R + p.col_begin, ldr, Y1, ld1, Y2, ld2, ws, L, st, ss->s);
   CABS_LAUNCH_CHECK("embed_products");
+  CABS_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
+  CABS_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));
   double* norms = wsp<double>(ws, L.norms);
   if (multi(comm)) {
     // one message carries both norm vectors: [N_c^2 (Kp) | N_r^2 (Kp)]

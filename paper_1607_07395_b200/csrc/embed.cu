@@ -253,7 +253,9 @@ __global__ void __launch_bounds__(256) reduce_cols_kernel(const double* __restri
 
 int launch_embed_products(int64_t m_loc, int64_t n_sl, int k, const float* C, int64_t ldc, const float* R_slice,
                           int64_t ldr, float* Yc, int64_t ldyc, float* Yr, int64_t ldyr, void* ws, const Ws& L,
-                          cudaStream_t st) {
+                          cudaStream_t st, cudaStream_t st2) {
+  // st2 (optional): Y_r's product and norm reduction run there, concurrently with Y_c's
+  if (!st2) st2 = st;
   double* part = wsp<double>(ws, L.norm_part);
   double* norms = wsp<double>(ws, L.norms);
   const int gy = static_cast<int>(ceil_div(k, kGemmBN));
@@ -272,12 +274,12 @@ int launch_embed_products(int64_t m_loc, int64_t n_sl, int k, const float* C, in
   if (n_sl > 0) {
     dim3 g(static_cast<unsigned>(ceil_div(n_sl, kGemmBM)), gy);
     note_launch();
-    embed_gemm_kernel<true><<<g, 256, 0, st>>>(R_slice, ldr, n_sl, k, wsp<float>(ws, L.uw32), L.Kp, Yr, ldyr, part_r,
-                                               L.Kp);
+    embed_gemm_kernel<true><<<g, 256, 0, st2>>>(R_slice, ldr, n_sl, k, wsp<float>(ws, L.uw32), L.Kp, Yr, ldyr, part_r,
+                                                L.Kp);
     note_launch();
-    reduce_cols_kernel<<<k, 256, 0, st>>>(part_r, ceil_div(n_sl, kGemmBM), L.Kp, k, norms + L.Kp);
+    reduce_cols_kernel<<<k, 256, 0, st2>>>(part_r, ceil_div(n_sl, kGemmBM), L.Kp, k, norms + L.Kp);
   } else {
-    cudaMemsetAsync(norms + L.Kp, 0, sizeof(double) * k, st);
+    cudaMemsetAsync(norms + L.Kp, 0, sizeof(double) * k, st2);
   }
   return 0;
 }

@@ -34,7 +34,8 @@ bool launch_svd_cluster(int k, const float* W, int64_t ldw, double tol, double* 
 // embed.cu
 int launch_embed_products(int64_t m_loc, int64_t n_sl, int k, const float* C, int64_t ldc, const float* R_slice,
                           int64_t ldr, float* Yc, int64_t ldyc, float* Yr, int64_t ldyr, void* ws, const Ws& L,
-                          cudaStream_t st);
+                          cudaStream_t st,
+                          cudaStream_t st2 = nullptr);
 int launch_embed_finalize(int k, int mode, double m, double n, double ksamp, int kind, float* s_out, int* r_user,
                           void* ws, const Ws& L, cudaStream_t st);
 int launch_scale_compact(float* Y, int64_t ldy, int64_t N, int k, int which, void* ws, const Ws& L, cudaStream_t st);
