@@ -68,7 +68,11 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.w64 = take(sizeof(double) * K * K);
   w.a64 = take(sizeof(double) * K * K);
   w.v64 = take(sizeof(double) * (K * K + K));  // (+ K: the QR preconditioner's reflector scales)
-  w.qr = take(sizeof(double) * K * K + sizeof(int) * K);
+  // QR preconditioner: R scratch (K x K) + pivots (K int); for k > 128 (grid kernel) also the
+  // double-buffered column copies [2][K][round_up(K, 32)], the per-CTA bests [2][128][2], R_jj
+  // (K) and the barrier counter
+  w.qr = take(sizeof(double) * K * K + sizeof(int) * K +
+              (K > 128 ? sizeof(double) * (2 * K * Kp + 2 * 128 * 2 + K) + 256 : 0));
   w.sig64 = take(sizeof(double) * Kp);
   w.uw32 = take(sizeof(float) * K * Kp);
   w.vw32 = take(sizeof(float) * K * Kp);

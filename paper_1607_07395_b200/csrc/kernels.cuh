@@ -28,8 +28,19 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
                double* Vw64, int* r_user, cudaStream_t st);
 
 // svd_cluster.cu: k in (1, 320] on a cluster of ceil(k / 32) CTAs (false: not launched)
+// QR-preconditioner buffers in the workspace (svd.cu fills them from the layout): Xt (K x K),
+// Hv (K x K + K), Rg (K x K), piv (K), extra = the grid kernel's scratch (k > 128)
+struct SvdQrBufs {
+  double* Xt;
+  double* Hv;
+  double* Rg;
+  int* piv;
+  double* extra;
+  int64_t K;
+};
 bool launch_svd_cluster(int k, const float* W, int64_t ldw, double tol, double* sig, double* Uw64, double* Vw64,
-                        float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st);
+                        float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st,
+                        const struct SvdQrBufs* qb = nullptr);
 
 // embed.cu
 int launch_embed_products(int64_t m_loc, int64_t n_sl, int k, const float* C, int64_t ldc, const float* R_slice,

@@ -1561,7 +1561,7 @@ static bool launch_quad(int k, const float* W, int64_t ldw, double tol, double* 
   const int nw = (Q + G - 1) / G;
   if (k > KM || k > E * LP || nw * G + 2 > KM / 4 + 4 || nw > 8) return false;
   const size_t xch = sizeof(double) * 2 * 2 * (size_t)(nw * G + 2) * SEAT;
-  constexpr int kCap = 200 * 1024;
+  constexpr int kCap = 214 * 1024;  // (+ ~10.6 KB static: within the 227 KB opt-in)
   int nseg = 0;
   size_t smem = 0;
   for (int ns = 1; ns <= 4 && !nseg; ns *= 2) {  // fewest segments whose rotation buffers fit
@@ -1729,6 +1729,16 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
   float* uw32 = wsp<float>(ws, L.uw32);
   float* vw32 = wsp<float>(ws, L.vw32);
   // (every launcher notes its own kernel launches: the QR preconditioner adds one)
+  SvdQrBufs qbufs{};
+  {
+    qbufs.K = L.K;
+    qbufs.Xt = wsp<double>(ws, L.a64);
+    qbufs.Hv = wsp<double>(ws, L.v64);
+    qbufs.Rg = wsp<double>(ws, L.qr);
+    qbufs.piv = reinterpret_cast<int*>(qbufs.Rg + (size_t)L.K * L.K);
+    const size_t off = ((sizeof(double) * (size_t)L.K * L.K + sizeof(int) * (size_t)L.K) + 15) & ~size_t(15);
+    qbufs.extra = L.K > 128 ? reinterpret_cast<double*>(reinterpret_cast<char*>(qbufs.Rg) + off) : nullptr;
+  }
   if (k <= 64 && !getenv("CABS_SVD_SMEM") && !getenv("CABS_SVD_ONE_SM")) {
     // A on one SM, V on its cluster partner; four columns per 8-lane slot (the two-column
     // svd_split_kernel stays selectable for comparison)
@@ -1759,7 +1769,7 @@ int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const W
     else if (k <= 52) launch_systolic<4, 13>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
     else launch_systolic<4, 16>(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st);
   } else if (k <= 320 && !getenv("CABS_SVD_ONE_CTA") &&
-             launch_svd_cluster(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st)) {
+             launch_svd_cluster(k, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, L.Kp, r_ws, r_user, ws, st, &qbufs)) {
     // k > 64: block Jacobi over a thread-block cluster (svd_cluster.cu)
   } else {
     static bool attr_set = false;

@@ -145,11 +145,152 @@ __device__ __forceinline__ int sc_rr(int j, int r, int n) {
   return j == 0 ? 0 : 1 + x;
 }
 
+// ---------------------------------------------------------------- QR preconditioner, 128 < k <= 320
+// The pivoted Householder QR of svd.cu's svd_qrcp_kernel (same pivot rule, same reflector
+// arithmetic, same outputs Xt = R^T, Hv = reflectors + scales, piv) for matrices too large for
+// one CTA's registers: a cooperative grid of ceil(k/4) CTAs, one warp per column (rows
+// lane + 32 e in registers), one grid barrier per pivot step.  Every column is published to a
+// double-buffered global copy each step (the next pivot column is read from there, through L2)
+// and every CTA its best (key, column) of the next step.
+struct QrGrid {
+  double* colbuf;  // [2][k][kr]
+  double* bests;   // [2][128][2]: key, column
+  double* rd;      // R_jj
+  unsigned* bar;   // arrival counter (zeroed before the launch)
+  int kr;
+};
+
+__device__ __forceinline__ void qg_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire_gpu(bar) < target) __nanosleep(20);
+  }
+  __syncthreads();
+}
+
+template <int E>
+__global__ void __launch_bounds__(128) svd_qrcp_grid_kernel(int k, const float* __restrict__ W, int64_t ldw,
+                                                            double* __restrict__ Xt, double* __restrict__ Hv,
+                                                            double* __restrict__ Rg, int* __restrict__ piv_out,
+                                                            QrGrid g, void* ws) {
+  __shared__ double s_k[4];
+  __shared__ int s_i[4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = blockIdx.x * 4 + warp;
+  const int NB = gridDim.x;
+  const int kr = g.kr;
+  double a[E];
+  bool bad = false;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane + 32 * e;
+    float v = 0.f;
+    if (i < k && q < k) v = W[(int64_t)i * ldw + q];
+    bad |= !isfinite(v);
+    a[e] = static_cast<double>(v);
+  }
+  if (bad) set_status(ws, CABS_DEV_NONFINITE);
+  bool done = q >= k;
+  unsigned nbar = 0;
+  auto publish = [&](int par, double key) {  // column copy + the CTA's best (lowest column on ties)
+    if (!done) {
+      double* cb = g.colbuf + ((size_t)par * k + q) * kr;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (lane + 32 * e < kr) cb[lane + 32 * e] = a[e];
+    }
+    if (lane == 0) { s_k[warp] = done ? -1.0 : key; s_i[warp] = q; }
+    __syncthreads();
+    if (tid == 0) {
+      double bk = -1.0;
+      int bi = 0x7fffffff;
+      for (int w2 = 0; w2 < 4; ++w2)
+        if (s_k[w2] > bk) { bk = s_k[w2]; bi = s_i[w2]; }
+      g.bests[((size_t)par * 128 + blockIdx.x) * 2] = bk;
+      g.bests[((size_t)par * 128 + blockIdx.x) * 2 + 1] = static_cast<double>(bi);
+    }
+  };
+  {
+    double n0 = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) n0 = fma(a[e], a[e], n0);
+    publish(0, warp_sum_d(n0));
+  }
+  qg_barrier(g.bar, static_cast<unsigned>(NB) * ++nbar);
+  for (int j = 0; j < k; ++j) {
+    const int par = j & 1;
+    // pivot: argmax of the NB CTA bests (identical in every warp)
+    double bv = -1.0;
+    int bq = 0x7fffffff;
+    for (int c = lane; c < NB; c += 32) {
+      const double kk = __ldcg(g.bests + ((size_t)par * 128 + c) * 2);
+      const int ii = static_cast<int>(__ldcg(g.bests + ((size_t)par * 128 + c) * 2 + 1));
+      if (kk > bv || (kk == bv && ii < bq)) { bv = kk; bq = ii; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+      if (ov > bv || (ov == bv && oq < bq)) { bv = ov; bq = oq; }
+    }
+    const int ph = bq;
+    const double* xp = g.colbuf + ((size_t)par * k + ph) * kr;
+    const double xj = __ldcg(xp + j), nn = fmax(bv, 0.0), sn = sqrt(nn);
+    const double alpha = xj >= 0.0 ? -sn : sn;                           // R_jj
+    const double vjj = xj - alpha;                                        // x_j + sign(x_j) ||x||
+    const double beta = nn > 0.0 ? 1.0 / (sn * (sn + fabs(xj))) : 0.0;    // 2 / v^T v
+    double x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = lane + 32 * e < kr ? __ldcg(xp + lane + 32 * e) : 0.0;
+    if (q == ph) done = true;
+    // rows above j are zero in every column (cleared as they move to R)
+    const double aj = (!done && q < k) ? __ldcg(g.colbuf + ((size_t)par * k + q) * kr + j) : 0.0;
+    double d0 = lane == 0 ? (vjj - xj) * aj : 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) d0 = fma(x[e], a[e], d0);
+    const double f = done ? 0.0 : beta * warp_sum_d(d0);
+    double n0 = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      a[e] = lane + 32 * e == j ? 0.0 : fma(-f, x[e], a[e]);
+      n0 = fma(a[e], a[e], n0);
+    }
+    const double key = warp_sum_d(n0);  // exact ||a(j+1:)||^2
+    if (!done && lane == 0) Rg[(size_t)j * k + q] = fma(-f, vjj, aj);  // R_jq
+    if (blockIdx.x == 0 && warp == 0) {  // reflector j (every warp holds it)
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = lane + 32 * e;
+        if (i < k) Hv[(size_t)j * k + i] = i == j ? vjj : x[e];
+      }
+      if (lane == 0) {
+        Hv[(size_t)k * k + j] = beta;
+        piv_out[j] = ph;
+        g.rd[j] = alpha;
+      }
+    }
+    publish(par ^ 1, key);
+    qg_barrier(g.bar, static_cast<unsigned>(NB) * ++nbar);
+  }
+  // X = R^T: X[i][c] = R[c][i] = Rg[c][piv[i]] above the diagonal, R_ii on it, 0 below
+  for (int64_t e = (int64_t)blockIdx.x * 128 + tid; e < (int64_t)k * k; e += (int64_t)NB * 128) {
+    const int i = static_cast<int>(e / k), c = static_cast<int>(e - (int64_t)i * k);
+    Xt[e] = c < i ? __ldcg(Rg + (size_t)c * k + __ldcg(piv_out + i)) : (c == i ? __ldcg(g.rd + i) : 0.0);
+  }
+}
+
 template <int EPL>
 __global__ void __launch_bounds__(kScThreads, 1)
-svd_cluster_kernel(int k, int w, const float* __restrict__ W, int64_t ldw, double tol, double* __restrict__ sigma_out,
-                   double* __restrict__ Uw64, double* __restrict__ Vw64, float* __restrict__ uw32,
-                   float* __restrict__ vw32, int64_t ld32, int* r_out, int* r_out2, void* ws) {
+svd_cluster_kernel(int k, int w, const float* __restrict__ W, int64_t ldw, const double* __restrict__ Xt,
+                   const double* __restrict__ Hq, const int* __restrict__ piv, double tol,
+                   double* __restrict__ sigma_out, double* __restrict__ Uw64, double* __restrict__ Vw64,
+                   float* __restrict__ uw32, float* __restrict__ vw32, int64_t ld32, int* r_out, int* r_out2,
+                   void* ws) {
+  // Xt != nullptr: QR-preconditioned (svd_qrcp_grid_kernel): A = R^T, V = Q (formed here from
+  // the reflectors Hq); the V columns end as U_w = Q V_x, the A columns give V_w (rows permuted)
+  const bool pre = Xt != nullptr;
   extern __shared__ __align__(16) double sm[];
   __shared__ double s_sig[kScKmax];  // CTA 0: sigma by column id
   __shared__ int s_rank[kScKmax];    // CTA 0: rank by column id
@@ -179,7 +320,41 @@ svd_cluster_kernel(int k, int w, const float* __restrict__ W, int64_t ldw, doubl
   int blk[2] = {static_cast<int>(cr), nb - 1 - static_cast<int>(cr)};
 
   // ---- load A = W (columns), V = I; zero padding rows / columns
-  {
+  if (pre) {
+    for (int e = tid; e < 2 * w * kp; e += kScThreads) {
+      const int j = e / kp, i = e - j * kp;
+      const int gc = blk[j / w] * w + (j % w);
+      col(j)[i] = (i < k && gc < k) ? Xt[(size_t)i * k + gc] : 0.0;
+      col(j)[kp + i] = (i == gc && gc < k) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    // V = Q = H_0 ... H_{k-1} on the local unit columns: H_j for j = k - 1 down to 0, one warp per
+    // column (H_j e_c = e_c for j > c: skipped exactly)
+    for (int jl = warp; jl < 2 * w; jl += kScThreads / 32) {
+      const int gc = blk[jl / w] * w + (jl % w);
+      if (gc >= k) continue;
+      double* vc = col(jl) + kp;
+      double y[EPL];
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) y[e] = vc[lane + 32 * e];
+      for (int j = gc; j >= 0; --j) {
+        const double* hv = Hq + (size_t)j * k;
+        double dd = 0.0, hvr[EPL];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const int i = lane + 32 * e;
+          hvr[e] = i < k ? __ldg(hv + i) : 0.0;
+          dd = fma(hvr[e], y[e], dd);
+        }
+        const double f = __ldg(Hq + (size_t)k * k + j) * warp_sum_d(dd);
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) y[e] = fma(-f, hvr[e], y[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) vc[lane + 32 * e] = y[e];
+    }
+    __syncthreads();
+  } else {
     bool bad = false;
     for (int e = tid; e < 2 * w * kp; e += kScThreads) {
       const int j = e / kp, i = e - j * kp;
@@ -385,10 +560,11 @@ svd_cluster_kernel(int k, int w, const float* __restrict__ W, int64_t ldw, doubl
       asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(sg) : "r"(sig0 + 8u * gc) : "memory");
       const double* a = col(j);
       const double* v = a + kp;
+      const double* uc = pre ? v : a;  // the column holding U_w's direction fixes the sign
       double best = -1.0;
       int bi = 0x7fffffff;
       for (int i = lane; i < k; i += 32) {
-        const double x = fabs(a[i]);
+        const double x = fabs(uc[i]);
         if (x > best || (x == best && i < bi)) { best = x; bi = i; }
       }
 #pragma unroll
@@ -398,15 +574,17 @@ svd_cluster_kernel(int k, int w, const float* __restrict__ W, int64_t ldw, doubl
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
       const bool keep = jr < r;
-      const double sign = (bi < k && a[bi] < 0) ? -1.0 : 1.0;
+      const double sign = (bi < k && uc[bi] < 0) ? -1.0 : 1.0;
       const double inv = (keep && sg > 0) ? sign / sg : 0.0;
       const double vs = keep ? sign : 0.0;
       for (int i = lane; i < k; i += 32) {
-        const double u = a[i] * inv, vv = v[i] * vs;
+        // plain: U_w = a / sigma, V_w = v; preconditioned: U_w = v (= Q V_x), V_w(piv) = a / sigma
+        const double u = pre ? v[i] * vs : a[i] * inv, vv = pre ? a[i] * inv : v[i] * vs;
+        const int iv = pre ? piv[i] : i;
         if (Uw64) Uw64[(size_t)i * k + jr] = u;
-        if (Vw64) Vw64[(size_t)i * k + jr] = vv;
+        if (Vw64) Vw64[(size_t)iv * k + jr] = vv;
         if (uw32) uw32[(size_t)i * ld32 + jr] = static_cast<float>(u);
-        if (vw32) vw32[(size_t)i * ld32 + jr] = static_cast<float>(vv);
+        if (vw32) vw32[(size_t)iv * ld32 + jr] = static_cast<float>(vv);
       }
     }
   }
@@ -414,9 +592,9 @@ svd_cluster_kernel(int k, int w, const float* __restrict__ W, int64_t ldw, doubl
 }
 
 template <int EPL>
-static bool launch_sc(int k, int w, int P, const float* W, int64_t ldw, double tol, double* sig, double* Uw64,
-                      double* Vw64, float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws,
-                      cudaStream_t st) {
+static bool launch_sc(int k, int w, int P, const float* W, int64_t ldw, const double* Xt, const double* Hq,
+                      const int* piv, double tol, double* sig, double* Uw64, double* Vw64, float* uw32, float* vw32,
+                      int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st) {
   const size_t smem = sizeof(double) * 2 * (size_t)w * 2 * 32 * EPL * (EPL <= 5 ? 2 : 1);
   auto kern = svd_cluster_kernel<EPL>;
   static bool attr = false;
@@ -438,23 +616,58 @@ static bool launch_sc(int k, int w, int P, const float* W, int64_t ldw, double t
   cfg.attrs = at;
   cfg.numAttrs = 1;
   note_launch();
-  return cudaLaunchKernelEx(&cfg, kern, k, w, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws) ==
-         cudaSuccess;
+  return cudaLaunchKernelEx(&cfg, kern, k, w, W, ldw, Xt, Hq, piv, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws,
+                            r_user, ws) == cudaSuccess;
+}
+
+template <int E>
+static bool launch_qrg(int k, const float* W, int64_t ldw, const SvdQrBufs& b, void* ws, cudaStream_t st) {
+  QrGrid g{};
+  g.kr = static_cast<int>(round_up(k, 32));
+  g.colbuf = b.extra;
+  g.bests = g.colbuf + (size_t)2 * b.K * round_up(b.K, 32);
+  g.rd = g.bests + 2 * 128 * 2;
+  g.bar = reinterpret_cast<unsigned*>(g.rd + b.K);
+  if (cudaMemsetAsync(g.bar, 0, sizeof(unsigned), st) != cudaSuccess) return false;
+  const int nb = static_cast<int>(ceil_div(k, 4));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(nb));
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // one barrier per pivot step: every CTA co-resident
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, svd_qrcp_grid_kernel<E>, k, W, ldw, b.Xt, b.Hv, b.Rg, b.piv, g, ws) == cudaSuccess;
 }
 
 // k in (16, 320]: 2P blocks of w <= 16 columns on a cluster of P CTAs
 bool launch_svd_cluster(int k, const float* W, int64_t ldw, double tol, double* sig, double* Uw64, double* Vw64,
-                        float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st) {
+                        float* uw32, float* vw32, int64_t ld32, int* r_ws, int* r_user, void* ws, cudaStream_t st,
+                        const SvdQrBufs* qb) {
   if (k < 2 || k > kScKmax) return false;
   const int P = static_cast<int>(ceil_div(k, 32));
   const int w = static_cast<int>(ceil_div(k, 2 * P));
   if (w > 16) return false;
   const int epl = static_cast<int>(ceil_div(k, 32));
+  // QR preconditioning for k > 128 (the grid QR kernel; CABS_SVD_NOQR: plain Jacobi on W)
+  const double* Xt = nullptr;
+  const double* Hq = nullptr;
+  const int* piv = nullptr;
+  if (qb && qb->extra && k > 128 && !getenv("CABS_SVD_NOQR")) {
+    bool q = false;
+    if (epl <= 5) q = launch_qrg<5>(k, W, ldw, *qb, ws, st);
+    else if (epl <= 8) q = launch_qrg<8>(k, W, ldw, *qb, ws, st);
+    else q = launch_qrg<10>(k, W, ldw, *qb, ws, st);
+    if (q) { Xt = qb->Xt; Hq = qb->Hv; piv = qb->piv; } else { cudaGetLastError(); }
+  }
   bool ok;
-  if (epl <= 4) ok = launch_sc<4>(k, w, P, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
-  else if (epl <= 5) ok = launch_sc<5>(k, w, P, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
-  else if (epl <= 7) ok = launch_sc<7>(k, w, P, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
-  else ok = launch_sc<10>(k, w, P, W, ldw, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
+  if (epl <= 4) ok = launch_sc<4>(k, w, P, W, ldw, Xt, Hq, piv, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
+  else if (epl <= 5) ok = launch_sc<5>(k, w, P, W, ldw, Xt, Hq, piv, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
+  else if (epl <= 7) ok = launch_sc<7>(k, w, P, W, ldw, Xt, Hq, piv, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
+  else ok = launch_sc<10>(k, w, P, W, ldw, Xt, Hq, piv, tol, sig, Uw64, Vw64, uw32, vw32, ld32, r_ws, r_user, ws, st);
   if (!ok) cudaGetLastError();
   return ok;
 }

@@ -135,15 +135,16 @@ _SVD_KERNELS = {"default": None, "split": "CABS_SVD_SPLIT", "one_sm": "CABS_SVD_
 def test_svd_matches_lapack(dev, k, rank, kernel, monkeypatch):
     """Every SVD kernel variant: k <= 64 the default 4-columns-per-slot cluster pair, the
     2-column pair, the one-SM systolic and the shared-memory kernels (k <= 128: the default runs
-    Jacobi on R^T of a pivoted Householder QR, "noqr" on W itself); 64 < k <= 128 the default
+    Jacobi on R^T of a pivoted Householder QR, "noqr" on W itself; k > 128 likewise with the
+    cooperative grid QR in front of the cluster kernel); 64 < k <= 128 the default
     4-columns-per-slot pair with segment handover; k > 128 the default block Jacobi over a
     thread-block cluster (svd_cluster.cu, also forced at 64 < k <= 128) and the single-CTA kernel."""
     if kernel in ("split", "one_sm") and k > 64:
         pytest.skip("k <= 64 variant")
     if kernel == "cluster" and not (64 < k <= 128):
         pytest.skip("forced only where the quad kernel is the default")
-    if kernel == "noqr" and not (2 < k <= 128):
-        pytest.skip("the quad kernel without its QR preconditioner")
+    if kernel == "noqr" and not (2 < k <= 320):
+        pytest.skip("the Jacobi kernels without their QR preconditioner")
     if kernel == "one_cta" and not (64 < k <= 150):
         pytest.skip("k > 64 variant (slow beyond 150)")
     if _SVD_KERNELS[kernel]:
