@@ -626,7 +626,10 @@ __global__ void __launch_bounds__(kLxT, 1) lloyd_prune_kernel(LexArgs a) {
       // the near-tie band, and its prefix becomes its stored bound.  The lane's survivors then
       // complete their chains (from dimension 0: the same FP32 sums).  Iteration 0 first guesses
       // the label as the centre of smallest prefix and evaluates it fully.
-      constexpr int PD = DP >= 48 ? 16 : 0;
+#ifndef CABS_LEX_PD
+#define CABS_LEX_PD 24  // measured on c3: 8 / 16 / 24 / 32 -> 4.23 / 4.16 / 4.10 / 4.20 ms
+#endif
+      constexpr int PD = DP >= 48 ? CABS_LEX_PD : 0;
       int guess = -1;
       auto each4 = [&](const uint32_t (&msk)[4], auto&& fn) {  // warp-uniform visit, 4 centres per step
         uint32_t r[4] = {msk[0], msk[1], msk[2], msk[3]};
