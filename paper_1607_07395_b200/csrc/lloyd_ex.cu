@@ -27,7 +27,7 @@
 // straight into the global slot (red.add), and every CTA keeps the running totals in shared
 // memory.  Integer sums do not depend on the order of the additions, so both modes give the
 // totals of a full recomputation bit for bit.  The mode of iteration t is full iff more than
-// N/16 points changed label at iteration t - 1 (iteration 0 is full), read from a global
+// N/8 points changed label at iteration t - 1 (iteration 0 is full), read from a global
 // counter after the grid barrier: uniform per problem.
 // Objective (Eq. 6): J_t = sum_j (Q_j - 2 c_j . S_j + W_j ||c_j||^2) from the exact totals of
 // iteration t and its FP32 centres, in FP64 (relative rounding ~1e-16 x sum w ||x||^2 / J: 1e-12
@@ -108,6 +108,8 @@ struct LexArgs {
   int cp;    // centre pitch (floats): >= DP, 16-byte rows
   int k2p;   // D row pitch: round_up(k2max, 4)
   float cand_factor;  // pass-2 candidates: lower bound <= cand_factor u (>= 1 + eps)
+  int dperiod;        // ||c_i - c_j|| recomputed exactly every dperiod-th iteration (decayed between)
+  int fulldiv;        // an iteration accumulates every point iff > N / fulldiv labels changed before
   uint32_t off_s, off_c, off_d, off_lab, off_ord, off_bd, off_lb, off_qs, off_wd, off_dl, off_cd, total;
 };
 
@@ -367,7 +369,7 @@ __global__ void __launch_bounds__(kLxT, 1) lloyd_prune_kernel(LexArgs a) {
       long long* fs_next = pr.fsum + (size_t)((it + 1) % 3) * Eqp;
       for (int64_t e = (int64_t)b * kLxT + tid; e < Eq; e += (int64_t)Gb * kLxT) fs_next[e] = 0;
       if (tid == 0) {
-        s_full = __ldcg(pr.chg + it - 1) * 16LL > pr.N;
+        s_full = __ldcg(pr.chg + it - 1) * static_cast<long long>(a.fulldiv) > pr.N;
         s_dmax = 0.f;
       }
       __syncthreads();
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(kLxT, 1) lloyd_prune_kernel(LexArgs a) {
       }
       __syncthreads();
       LEX_STAMP(1);
-      if ((it & 3) == 1) {
+      if (it % a.dperiod == 1 % a.dperiod) {
       // Dn_ij = ||c_i - c_j||: one warp per row i of this CTA's share (rows i = crank mod csize),
       // lane l takes j = l + 32 q (consecutive lanes on consecutive rows of c32: odd pitch in
       // 16-byte units, conflict-free; c_i is a broadcast); then every CTA copies the other rows
@@ -879,6 +881,14 @@ static bool lex_launch(LexArgs& a, int njobs, const LloydJob* jobs, int iters, i
     // measured on c3 (tools/kcand.py): 1.0003 / 1.01 / 1.05 / 1.2 -> 4.02 / 4.05 / 4.12 / 4.29 ms
     a.cand_factor = cf ? static_cast<float>(atof(cf)) : 1.0003f;
     if (!(a.cand_factor >= 1.f + kCandSlack)) a.cand_factor = 1.f + kCandSlack;
+    // measured on c3 (tools/ktune.py, period:divisor): 4:16 4.02, 8:16 3.97, 4:8 3.95, 8:8 3.90,
+    // 16:8 3.91, 1:16 4.25, 4:64 4.38 ms
+    const char* dp = getenv("CABS_KM_DPERIOD");  // (diagnostics)
+    a.dperiod = dp ? atoi(dp) : 8;
+    if (a.dperiod < 1) a.dperiod = 1;
+    const char* fd = getenv("CABS_KM_FULLDIV");
+    a.fulldiv = fd ? atoi(fd) : 8;
+    if (a.fulldiv < 1) a.fulldiv = 1;
   }
   a.nprob = njobs;
   a.iters = iters;
