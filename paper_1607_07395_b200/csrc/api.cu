@@ -109,7 +109,7 @@ int64_t cabs_launch_count(void) { return g_launches.load(std::memory_order_relax
 int32_t cabs_kernel_path(int32_t op, int32_t k, int32_t d) {
   if (op == CABS_OP_KMEANS)
     return kmeans_prune_selected(k, d) ? CABS_PATH_PRUNE : kmeans_tc_selected(k, d) ? CABS_PATH_TC : CABS_PATH_FFMA;
-  if (op == CABS_OP_RESIDUAL) return (k >= 1 && k <= residual_tc_kmax() && !getenv("CABS_RESIDUAL_FFMA")) ? CABS_PATH_TC
+  if (op == CABS_OP_RESIDUAL) return residual_tc_covers(k) ? CABS_PATH_TC
                                                                                                          : CABS_PATH_FFMA;
   return -1;
 }

@@ -36,7 +36,7 @@ struct Ws {
   size_t dist2, cand_d2, cand_i2, cand_all2;  // ... and slot 1 (cabs_select_pair)
   size_t hcand, idx;
   size_t cb, rb, wb;
-  size_t res_part, res_split;  // res_split: G_hi, G_lo (n x round_up(ncomp, 32) each, <= 192)
+  size_t res_part, res_split;  // res_split: G_hi, G_lo (TF32: n x round_up(ncomp, 32) each, <= 192; FP16: n x round_up(ncomp, 64) halves, <= 384)
   size_t hcand_side;
   size_t orth_part, orth;  // cabs_orthogonalize: Gram partials | gram, U_K, V_K, sigma, r, K, T_U, T_V
   size_t total;

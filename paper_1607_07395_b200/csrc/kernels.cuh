@@ -242,6 +242,7 @@ void launch_residual_final(const double* part, int G, double* out, cudaStream_t 
 // residual_tc.cu (tcgen05 3xTF32 path; ncomp <= 192)
 void residual_debug_counters(long long* out, int n);
 int residual_tc_kmax();
+bool residual_tc_covers(int ncomp);
 // lloyd_tc.cu: whether cabs_kmeans(_pair) takes the tensor-core distance path for (k2, d)
 bool kmeans_tc_selected(int k2, int d);
 bool residual_tc_supported(const float* A, int64_t lda, int64_t m_loc, int64_t n, int ncomp);

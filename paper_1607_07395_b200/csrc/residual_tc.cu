@@ -21,8 +21,9 @@
 //   warps 7-10 epilogue (group 1): the same for columns [64, 128) (two warps per TMEM lane
 //            quarter: the epilogue, which bounds the kernel otherwise, runs at twice the rate).
 // Tile order is row-band major over a static contiguous tile range per CTA; fixed-order
-// block and grid reductions: bit-reproducible.  ncomp <= 192 (K padded to a multiple of 32;
-// G streamed in 32-wide K chunks through a 4-deep ring; TMEM plan in tmem_plan()).
+// block and grid reductions: bit-reproducible.  FP16 split (default): ncomp <= 384 (K padded to a
+// multiple of 64); 3xTF32 (CABS_RESIDUAL_TF32): ncomp <= 192 (K padded to a multiple of 32).  G
+// streamed in 128-byte K chunks through a 4-deep ring; TMEM plan in tmem_plan().
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -41,8 +42,9 @@ constexpr int kEpiWarps = 8;
 constexpr int kAR = kAS / 2;                       // A ring slots per epilogue group (its own ring: a
                                                     // group never waits on a slot phase of the other)
 constexpr int kResKpMax = 192;                      // largest padded K, 3xTF32 (hi + lo F in TMEM + 1 acc stage)
-constexpr int kResKpMaxF16 = 128;                   // ... FP16 split (two K elements per TMEM column; the
-                                                    // one-F-buffer plan for K > 128 fails parity: not used)
+constexpr int kResKpMaxF16 = 384;                   // ... FP16 split (two K elements per TMEM column:
+                                                    // F hi + lo = round_up(K, 64) columns; K > 256: one
+                                                    // accumulator stage, 128 + 384 <= 512 columns)
 constexpr uint32_t kGAtomBytes = kTcBN * 128;      // 16 KB: 128 G rows x 32 floats (one K chunk)
 constexpr uint32_t kABoxBytes = kTcBM * 128;       // 16 KB: 128 rows x 32 floats = a quarter A tile
 constexpr uint32_t kTmemCols = 512;
@@ -906,13 +908,24 @@ void residual_debug_counters(long long* out, int n) {
 #endif
 }
 
-int residual_tc_kmax() { return kResKpMax; }
+// largest ncomp of the FP16 split path (CABS_RES_F16_MAX overrides: experiments)
+static int res_f16_kmax() {
+  const char* e = getenv("CABS_RES_F16_MAX");
+  return e ? atoi(e) : kResKpMaxF16;
+}
+
+int residual_tc_kmax() { return res_f16_kmax() > kResKpMax ? res_f16_kmax() : kResKpMax; }
+
+// the tensor-core kernels cover this ncomp (FP16 split up to res_f16_kmax(), 3xTF32 up to kResKpMax)
+bool residual_tc_covers(int ncomp) {
+  if (ncomp < 1 || ncomp > residual_tc_kmax() || getenv("CABS_RESIDUAL_FFMA")) return false;
+  return !((getenv("CABS_RESIDUAL_TF32") || ncomp > res_f16_kmax()) && round_up(ncomp, 32) > kResKpMax);
+}
 
 bool residual_tc_supported(const float* A, int64_t lda, int64_t m_loc, int64_t n, int ncomp) {
-  if (ncomp < 1 || ncomp > residual_tc_kmax() || m_loc < 1 || n < 1) return false;
+  if (!residual_tc_covers(ncomp) || m_loc < 1 || n < 1) return false;
   if ((lda % 4) != 0 || (reinterpret_cast<uintptr_t>(A) & 15) != 0) return false;
   if (m_loc > 0x7fffffff || n > 0x7fffffff) return false;
-  if (getenv("CABS_RESIDUAL_FFMA")) return false;
   return encoder() != nullptr;
 }
 
@@ -923,7 +936,7 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   FArgs fa{F, ldf, s, ncomp, (reinterpret_cast<uintptr_t>(F) & 15) == 0 && (ldf % 4) == 0};
-  if (!getenv("CABS_RESIDUAL_TF32") && ncomp <= kResKpMaxF16) {
+  if (!getenv("CABS_RESIDUAL_TF32") && ncomp <= res_f16_kmax()) {
     // FP16 hi/lo split (default): K in chunks of 64, 16 per MMA
     const int kp16 = static_cast<int>(round_up(ncomp, 64));
     const TmemPlan tp = tmem_plan(kp16 / 2);
@@ -959,6 +972,7 @@ int launch_residual_tc(const float* A, int64_t lda, int64_t m_loc, int64_t n, co
     return 0;
   }
   const int kp = static_cast<int>(round_up(ncomp, 32));
+  if (kp > kResKpMax) return -1;
   const TmemPlan tp = tmem_plan(kp);
   float* gh = split;
   float* gl = gh + n * kp;

@@ -335,7 +335,8 @@ def test_sketch_flags_bad_indices(dev):
 @pytest.mark.parametrize("m,n,k,use_s", [(2000, 1500, 20, True), (1000, 777, 50, False), (129, 257, 7, True),
                                          (4096, 2048, 100, True), (300, 200, 1, False), (8000, 1000, 128, True),
                                          (2600, 1900, 192, True), (5000, 3001, 160, False), (1500, 1300, 200, True),
-                                         (1000, 700, 300, False)])
+                                         (1000, 700, 300, False), (3000, 2100, 256, True), (2048, 1536, 384, False),
+                                         (20000, 6000, 300, True)])
 def test_residual_matches_oracle(dev, m, n, k, use_s):
     A, T = _A(m, n, m + k, dev, r=k)
     g = np.random.default_rng(k)
@@ -356,7 +357,32 @@ def test_residual_matches_oracle(dev, m, n, k, use_s):
     assert abs(math.sqrt(o[0]) - math.sqrt(r2)) <= 1e-4 * math.sqrt(r2) + 1e-6 * math.sqrt(a2)
 
 
-@pytest.mark.parametrize("k", [16, 120, 190])
+@pytest.mark.parametrize("m,n,k", [(40000, 640, 300), (40000, 700, 200), (8192, 6000, 256), (30000, 1000, 100),
+                                   (12000, 1300, 384)])
+def test_residual_near_factorisation(dev, m, n, k):
+    """A = F diag(s) G^T + 1e-3 noise: the residual is ~1e-3 of ||A||, so a reconstruction error
+    of the tensor-core split shows at full weight.  Narrow n gives every CTA several row bands
+    (the one-F-buffer TMEM plan reloads F at each band change)."""
+    g = np.random.default_rng(m + k)
+    F = (g.standard_normal((m, k)) * 0.1).astype(np.float32)
+    G = (g.standard_normal((n, k)) * 0.1).astype(np.float32)
+    s = g.uniform(0.5, 2.0, k).astype(np.float32)
+    A = ((F.astype(np.float64) * s) @ G.T.astype(np.float64) + 1e-3 * g.standard_normal((m, n))).astype(np.float32)
+    plan = _plan(m, n, k)
+    ws = _ws(plan, dev)
+    ld = C.cabs_padded_ld(k)
+    Ft = torch.zeros((m, ld), device=dev); Ft[:, :k] = torch.from_numpy(F).to(dev)
+    Gt = torch.zeros((n, ld), device=dev); Gt[:, :k] = torch.from_numpy(G).to(dev)
+    out = torch.zeros(2, dtype=torch.float64, device=dev)
+    assert C.cabs_residual_path(k) == "tc"
+    C.cabs_residual(plan, torch.from_numpy(A).to(dev), Ft, torch.from_numpy(s).to(dev), Gt, k, out, ws)
+    r2, a2 = O.residual(A, F, G, s)
+    o = out.cpu().numpy()
+    assert abs(o[1] - a2) <= 1e-6 * a2
+    assert abs(math.sqrt(o[0]) - math.sqrt(r2)) <= 1e-4 * math.sqrt(r2)
+
+
+@pytest.mark.parametrize("k", [16, 120, 190, 300])
 def test_residual_exact_factorisation_is_small(dev, k):
     # A = F G^T exactly representable: residual at the FP32 rounding floor, far below ||A||
     m, n = 1024, 768
