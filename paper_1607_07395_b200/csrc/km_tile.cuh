@@ -27,8 +27,8 @@ __device__ __forceinline__ void km_log_tie(int* log, int cap, int it, int64_t p,
 }
 
 struct KmTileSmem {
-  float Xs[kTileD][kTileP + 4];
-  float Cs[kTileD][kTileC + 4];
+  __align__(16) float Xs[kTileD][kTileP + 4];  // rows of 68 floats: 16-byte aligned float4 reads
+  __align__(16) float Cs[kTileD][kTileC + 4];
   float sb_d[16][kTileP + 1];
   int sb_j[16][kTileP + 1];
   float ss_d[16][kTileP + 1];
@@ -43,16 +43,30 @@ __device__ __forceinline__ float ld_centre(const float* p) {
   return __ldg(p);
 }
 
-// acc[a][b] = ||X_{p0 + tp + 16a} - c_{j0 + tc + 16b}||^2 for one 64 x 64 block.
+__device__ __forceinline__ unsigned long long kt_dup(float x) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ unsigned long long kt_pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+
+// acc[a][b] = ||X_{p0 + 4 tp + a} - c_{j0 + 4 tc + b}||^2 for one 64 x 64 block: per dimension
+// one 16-byte shared-memory read of the thread's four point values and one of its four centre
+// values, and the 16 (point, centre) terms as packed FP32 pairs (sub.rn.f32x2 / fma.rn.f32x2:
+// per lane the IEEE results of FADD / FFMA, so every distance is the same ascending-dimension
+// fmaf chain as a scalar loop).
 template <bool COHERENT>
 __device__ __forceinline__ void km_tile_block(const float* __restrict__ X, int64_t ldx, int64_t N, int d,
                                               const float* __restrict__ centres, int64_t ldc, int k2, int64_t p0,
                                               int j0, KmTileSmem& sm, float (&acc)[4][4]) {
   const int tid = threadIdx.x, tp = tid & 15, tc = tid >> 4;
+  unsigned long long acc2[4][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+  for (int a = 0; a < 4; ++a) acc2[a][0] = acc2[a][1] = 0ull;
   // stage i0 + kTileD is loaded into registers while stage i0 is computed from shared memory
   const int pp = tid >> 2, ii = (tid & 3) * 4;
   const int64_t p = p0 + pp;
@@ -77,20 +91,28 @@ __device__ __forceinline__ void km_tile_block(const float* __restrict__ X, int64
     if (i0 + kTileD < d) load_stage(i0 + kTileD);
 #pragma unroll
     for (int ii2 = 0; ii2 < kTileD; ++ii2) {
-      float x[4], c[4];
+      const float4 xv = *reinterpret_cast<const float4*>(&sm.Xs[ii2][4 * tp]);
+      const float4 cv = *reinterpret_cast<const float4*>(&sm.Cs[ii2][4 * tc]);
+      const unsigned long long c01 = kt_pack(cv.x, cv.y), c23 = kt_pack(cv.z, cv.w);
+      const float xa[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-      for (int a = 0; a < 4; ++a) x[a] = sm.Xs[ii2][tp + 16 * a];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) c[b] = sm.Cs[ii2][tc + 16 * b];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const float df = x[a] - c[b];
-          acc[a][b] = fmaf(df, df, acc[a][b]);
-        }
+      for (int a = 0; a < 4; ++a) {
+        const unsigned long long x2 = kt_dup(xa[a]);
+        unsigned long long df;
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(df) : "l"(x2), "l"(c01));
+        asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc2[a][0]) : "l"(df));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(df) : "l"(x2), "l"(c23));
+        asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc2[a][1]) : "l"(df));
+      }
     }
     __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    acc[a][0] = __uint_as_float(static_cast<unsigned>(acc2[a][0]));
+    acc[a][1] = __uint_as_float(static_cast<unsigned>(acc2[a][0] >> 32));
+    acc[a][2] = __uint_as_float(static_cast<unsigned>(acc2[a][1]));
+    acc[a][3] = __uint_as_float(static_cast<unsigned>(acc2[a][1] >> 32));
   }
 }
 
@@ -110,7 +132,7 @@ __device__ __forceinline__ void km_tile_argmin(const float* __restrict__ X, int6
     km_tile_block<COHERENT>(X, ldx, N, d, centres, ldc, k2, p0, j0, sm, acc);
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int j = j0 + tc + 16 * b;
+      const int j = j0 + 4 * tc + b;
       if (j >= k2) continue;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
@@ -129,10 +151,10 @@ __device__ __forceinline__ void km_tile_argmin(const float* __restrict__ X, int6
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    sm.sb_d[tc][tp + 16 * a] = bd[a];
-    sm.sb_j[tc][tp + 16 * a] = bj[a];
-    sm.ss_d[tc][tp + 16 * a] = sd[a];
-    sm.ss_j[tc][tp + 16 * a] = sj[a];
+    sm.sb_d[tc][4 * tp + a] = bd[a];
+    sm.sb_j[tc][4 * tp + a] = bj[a];
+    sm.ss_d[tc][4 * tp + a] = sd[a];
+    sm.ss_j[tc][4 * tp + a] = sj[a];
   }
   __syncthreads();
   if (tid < kTileP) {
@@ -168,11 +190,11 @@ __device__ __forceinline__ void km_tile_distmat(const float* __restrict__ X, int
     km_tile_block<false>(X, ldx, N, d, centres, ldc, k2, p0, j0, sm, acc);
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int j = j0 + tc + 16 * b;
+      const int j = j0 + 4 * tc + b;
       if (j >= k2) continue;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        const int64_t p = p0 + tp + 16 * a;
+        const int64_t p = p0 + 4 * tp + a;
         if (p < N) D[(int64_t)j * ldd + p] = acc[a][b];
       }
     }

@@ -237,27 +237,34 @@ __device__ __forceinline__ void taken_put(int64_t* tab, int64_t x) {
 __device__ unsigned long long g_snap_prof[4];  // rescans, greedy-pass cycles
 #endif
 // The taken set of the greedy pass: a bitmap over the local point indices when the rank owns
-// all points (single GPU, N <= kBitmapMax and fits shared memory: one byte per point, one load per candidate), else
-// the open-addressing hash table of global indices.
-constexpr int64_t kBitmapMax = 1 << 18;
+// all points (single GPU) and the bitmap fits shared memory (one BIT per point: 1.3e6 points in
+// 160 KB; a put is one plain read-modify-write by the single writing lane), else the
+// open-addressing hash table of global indices.
+constexpr int64_t kBitmapMax = int64_t(1) << 22;
 struct TakenSet {
-  unsigned char* bits;  // one byte per local point (a put is one plain store); null: hash table
+  unsigned* bits;  // one bit per local point; null: hash table
   int64_t* tab;
   int64_t off;
   __device__ __forceinline__ bool has(int64_t x) const {
-    if (bits) return bits[x - off] != 0;
+    if (bits) {
+      const int64_t l = x - off;
+      return (bits[l >> 5] >> (l & 31)) & 1u;
+    }
     return taken_has(tab, x);
   }
   __device__ __forceinline__ void put(int64_t x) {
     if (bits) {
-      bits[x - off] = 1;
+      const int64_t l = x - off;
+      bits[l >> 5] |= 1u << (l & 31);
     } else {
       taken_put(tab, x);
     }
   }
 };
 
-__global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, const int64_t* cand_i, int k2, int T,
+constexpr int kDedupeThreads = 1024;  // the greedy pass is one warp; the rescans use every thread
+
+__global__ void __launch_bounds__(kDedupeThreads) snap_dedupe_kernel(const float* cand_d, const int64_t* cand_i, int k2, int T,
                                                           const double* __restrict__ cluster_w,
                                                           const float* __restrict__ D, int64_t ldd, int64_t N,
                                                           int64_t row_off, bool can_rescan,
@@ -271,8 +278,8 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
   __shared__ double s_w[CABS_KMAX];
   __shared__ int s_next;      // next position in `order` to process
   __shared__ int s_rescan;    // centre needing a rescan, or -1
-  __shared__ float rd[8], rs[8];
-  __shared__ int64_t ri[8], ri2[8];
+  __shared__ float rd[kDedupeThreads / 32], rs[kDedupeThreads / 32];
+  __shared__ int64_t ri[kDedupeThreads / 32], ri2[kDedupeThreads / 32];
   __shared__ unsigned char s_t1[CABS_KMAX], s_t2[CABS_KMAX];  // fast path: chosen candidate slots
   // dynamic: candidates in visiting order [k2][T] (int64 | float), then the bitmap
   extern __shared__ __align__(16) unsigned char cand_smem[];
@@ -288,9 +295,9 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
   taken.off = row_off;
   taken.bits = nullptr;
   if (use_bitmap) {
-    taken.bits = cand_smem + (staged ? (((size_t)k2 * T * (sizeof(int64_t) + sizeof(float)) + 15) & ~size_t(15)) : 0);
-    unsigned* w32 = reinterpret_cast<unsigned*>(taken.bits);
-    for (int64_t e = tid; e < (N + 3) / 4; e += blockDim.x) w32[e] = 0u;
+    taken.bits = reinterpret_cast<unsigned*>(
+        cand_smem + (staged ? (((size_t)k2 * T * (sizeof(int64_t) + sizeof(float)) + 15) & ~size_t(15)) : 0));
+    for (int64_t e = tid; e < (N + 31) / 32; e += blockDim.x) taken.bits[e] = 0u;
   } else {
     for (int e = tid; e < kTakenCap; e += blockDim.x) tab[e] = -1;
   }
@@ -400,13 +407,39 @@ __global__ void __launch_bounds__(256) snap_dedupe_kernel(const float* cand_d, c
     float b1 = FLT_MAX, b2 = FLT_MAX;
     int64_t i1 = INT64_MAX, i2 = INT64_MAX;
     const float* row = D + (int64_t)j * ldd;
-    for (int64_t p = tid; p < N; p += blockDim.x) {
+    // 16-byte loads (four in flight per thread, 64 KB per CTA: one SM streams the row at a useful
+    // rate); the taken set is probed only for an entry that would enter the thread's top two (the
+    // same result: the others cannot)
+    auto consider = [&](float v, int64_t p) {
       const int64_t gi = row_off + p;
-      if (taken.has(gi)) continue;
-      const float v = row[p];
+      if (!lex_less(v, gi, b2, i2) || taken.has(gi)) return;
       if (lex_less(v, gi, b1, i1)) { b2 = b1; i2 = i1; b1 = v; i1 = gi; }
-      else if (lex_less(v, gi, b2, i2)) { b2 = v; i2 = gi; }
+      else { b2 = v; i2 = gi; }
+    };
+    const int64_t head = N < 4 ? N : static_cast<int64_t>((4 - ((reinterpret_cast<uintptr_t>(row) >> 2) & 3)) & 3);
+    if (tid < head) consider(__ldcg(row + tid), tid);
+    const int64_t nv = (N - head) >> 2;  // whole float4 groups after the head
+    const float4* rv = reinterpret_cast<const float4*>(row + head);
+    constexpr int kRu = 4;
+    for (int64_t v0 = tid; v0 < nv; v0 += kRu * (int64_t)blockDim.x) {
+      float4 vb[kRu];
+#pragma unroll
+      for (int u = 0; u < kRu; ++u) {
+        const int64_t v = v0 + (int64_t)u * blockDim.x;
+        vb[u] = v < nv ? __ldcg(rv + v) : make_float4(FLT_MAX, FLT_MAX, FLT_MAX, FLT_MAX);
+      }
+#pragma unroll
+      for (int u = 0; u < kRu; ++u) {
+        const int64_t v = v0 + (int64_t)u * blockDim.x;
+        if (v >= nv) continue;
+        const int64_t p = head + 4 * v;
+        consider(vb[u].x, p);
+        consider(vb[u].y, p + 1);
+        consider(vb[u].z, p + 2);
+        consider(vb[u].w, p + 3);
+      }
     }
+    for (int64_t p = head + 4 * nv + tid; p < N; p += blockDim.x) consider(__ldcg(row + p), p);
     // reduce the (best, runner-up) pairs: warp butterflies, then the 8 warp results; the
     // lexicographic (distance, index) order is total, so the top two are unique and the
     // merge order does not matter
@@ -483,11 +516,11 @@ void launch_snap_dedupe(const float* cand_d, const int64_t* cand_i, int k2, int 
   size_t cand = (((size_t)k2 * T * (sizeof(int64_t) + sizeof(float))) + 15) & ~size_t(15);
   const bool staged = cand <= kCap;
   if (!staged) cand = 0;
-  const size_t bits = ((N + 15) / 16) * 16;  // one byte per point
+  const size_t bits = ((N + 127) / 128) * 16;  // one bit per point (16-byte multiple)
   const bool bitmap = can_rescan && N <= kBitmapMax && cand + bits <= kCap && !getenv("CABS_SNAP_HASH");
   const size_t bytes = cand + (bitmap ? bits : 0);
   note_launch();
-  snap_dedupe_kernel<<<1, 256, bytes, st>>>(cand_d, cand_i, k2, T, cluster_w, D, ldd, N, row_off, can_rescan,
+  snap_dedupe_kernel<<<1, kDedupeThreads, bytes, st>>>(cand_d, cand_i, k2, T, cluster_w, D, ldd, N, row_off, can_rescan,
                                             rep_of_centre, gap, reps_sorted, ws, staged, bitmap, unresolved);
 }
 

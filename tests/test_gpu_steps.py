@@ -519,6 +519,42 @@ def test_select_bitmap_and_hash_taken_sets_agree(dev, monkeypatch):
     assert len(set(res[0][0].tolist())) == k2
 
 
+@pytest.mark.parametrize("N", [5000, 300000, 300001])
+def test_select_exhausted_lists(dev, monkeypatch, N):
+    """Centres that all sit near the same point share their nearest points, so after the first
+    few centres every candidate list is exhausted and the greedy pass rescans the distance row
+    (the regime of unclustered data, e.g. c4).  N = 300000 exceeds 2^18: the one-bit-per-point
+    taken set.  Representatives equal the oracle's (first divergence a near tie) and the hash
+    taken set's."""
+    d, k2 = 8, 64
+    g = np.random.default_rng(N)
+    X = g.standard_normal((N, d)).astype(np.float32)
+    cen = (1e-3 * g.standard_normal((k2, d))).astype(np.float32)
+    cw = g.integers(1, 1000, k2).astype(np.float64)
+    ld = C.cabs_padded_ld(d)
+    Xt = torch.zeros((N, ld), device=dev); Xt[:, :d] = torch.from_numpy(X).to(dev)
+    cen_t = torch.zeros((k2, ld), device=dev); cen_t[:, :d] = torch.from_numpy(cen).to(dev)
+    plan = _plan(N, N, max(d, k2))
+    ws = _ws(plan, dev)
+    res = []
+    for force_hash in (False, True):
+        if force_hash:
+            monkeypatch.setenv("CABS_SNAP_HASH", "1")
+        reps = torch.zeros(k2, dtype=torch.int64, device=dev)
+        roc = torch.zeros(k2, dtype=torch.int64, device=dev)
+        C.cabs_select(plan, Xt, N, N, 0, d, cen_t, k2, torch.from_numpy(cw).to(dev), reps, ws, rep_of_centre=roc)
+        res.append((reps.cpu().numpy(), roc.cpu().numpy()))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    ref = O.snap(X, cen.astype(np.float64), cw)
+    got = res[0][1]
+    assert np.unique(got).size == k2
+    if not np.array_equal(got, ref.rep_of_centre):
+        for j in ref.order:
+            if got[j] != ref.rep_of_centre[j]:
+                assert ref.gap[j] < NEAR_TIE, f"centre {j}: {got[j]} vs {ref.rep_of_centre[j]} gap {ref.gap[j]}"
+                break
+
+
 @pytest.mark.parametrize("kind", ["embed", "sketch"])
 def test_fused_and_unfused_s5_identical(dev, monkeypatch, kind):
     """The single-GPU fused S5 kernel and the multi-pass path (GEMMs, norm reduction,
