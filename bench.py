@@ -689,6 +689,18 @@ def main():
         if args.no_variants:
             break
         variants[fu_name] = time_variant(args, cfg, A, plan, rank, world, comm, flush, stream, fu, fu_desc)
+    if (not args.no_variants and world == 1 and isinstance(A, torch.Tensor)
+            and 2.4 * A.numel() * 4 < torch.cuda.get_device_properties(dev).total_memory):
+        # the same CABS with the block held column-major (cabs_source.transposed): contiguous column
+        # gathers, k (n + m/8) gather sectors instead of k (m + n/8); results identical (tests/test_gpu_transposed.py)
+        At = torch.empty((cfg.n, cfg.m), dtype=torch.float32, device=dev)
+        for r0 in range(0, cfg.m, 8192):  # block-wise transpose: no second full-size temporary
+            At[:, r0:r0 + 8192] = A[r0:r0 + 8192, :cfg.n].t()
+        variants["colmajor_layout"] = time_variant(args, cfg, C.TransposedDense(At), plan, rank, world, comm, flush,
+                                                   stream, "kmeans", "Algorithm 2 unchanged; A held column-major "
+                                                   "(cabs_source.transposed = 1)")
+        del At
+        torch.cuda.empty_cache()
     if not args.no_variants and world == 1:
         variants["sketch_cur"] = time_sketch_cur(args, cfg, A, flush, samples)
         variants["rank_sweep"] = time_rank_sweep(pipe)

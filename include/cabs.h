@@ -95,7 +95,15 @@ typedef struct cabs_plan {
 /* Source of the matrix A (host struct).  A zero-initialised struct with a / lda set is dense.
  *
  * CABS_SOURCE_DENSE_F32: row i of the rank's block is at a + (i - row_begin)*lda (device,
- *   (row_end - row_begin) x n, row-major, lda >= n).
+ *   (row_end - row_begin) x n, row-major, lda >= n).  With transposed = 1 the same
+ *   block is held column-major instead: A(i, j) is at a + j*lda + (i - row_begin), i.e. `a` is
+ *   the n x (row_end - row_begin) row-major array A^T, lda >= row_end - row_begin.  Every entry
+ *   point computes exactly what it computes for the row-major copy (same I, J, C, R, W, P, Q,
+ *   representatives, U, s, V -- the gathers are exact copies, so everything downstream of them
+ *   is bit-identical; only the residual's summation order differs): the column gather becomes
+ *   contiguous reads and the row gather the one-element-per-sector one, k (n + m/8) sectors
+ *   instead of k (m + n/8), fewer whenever m > n.  The residual runs the same kernels on A^T
+ *   with F and G exchanged (||A - F S G^T||_F = ||A^T - G S F^T||_F).
  * CABS_SOURCE_RBF_F32: the implicit matrix of BASELINE.json configs[4] (reading Z23),
  *   A_ij = exp(-|x_i - y_j|^2 * inv_two_sigma2), generated on access in FP32 (direct
  *   differences summed over the d coordinates in order, exp via ex2.approx) -- PAPER.md P:24
@@ -128,6 +136,8 @@ typedef struct cabs_source {
   const int64_t* col_ptr; /* CSC of the same block: int64[n + 1] */
   const int32_t* row_idx; /* CSC: int32[nnz], local rows, strictly increasing within a column */
   const float* col_val;   /* CSC: float[nnz] */
+  int32_t transposed;     /* dense only: 0 = row-major block, 1 = column-major block (see above);
+                             any other value, or 1 with another kind -> INVALID_ARG */
 } cabs_source;
 
 /* Collectives supplied by the caller (host struct).  Each callback sums `count`

@@ -67,7 +67,20 @@ class Source(ctypes.Structure):
     _fields_ = [("a", c_vp), ("lda", c_i64), ("kind", c_i32), ("d", c_i32), ("x", c_vp), ("y", c_vp),
                 ("ldx", c_i64), ("ldy", c_i64), ("inv_two_sigma2", c_f32),
                 ("row_ptr", c_vp), ("col_idx", c_vp), ("row_val", c_vp), ("col_ptr", c_vp),
-                ("row_idx", c_vp), ("col_val", c_vp)]
+                ("row_idx", c_vp), ("col_val", c_vp), ("transposed", c_i32)]
+
+
+class TransposedDense:
+    """A dense row block held column-major (cabs.h: CABS_SOURCE_DENSE_F32 with transposed = 1, SURVEY
+    H1): `At` is the device float32 tensor A^T of this rank's block, shape (n, m_loc), row-major with
+    stride(0) >= m_loc.  Same results as the row-major block; the column gather reads contiguously."""
+
+    def __init__(self, At):
+        if At.dtype != torch.float32 or not At.is_cuda or At.dim() != 2 or (At.shape[1] > 1 and At.stride(1) != 1):
+            raise TypeError("TransposedDense: a 2-D float32 CUDA tensor with unit column stride")
+        self.At = At
+        self.shape = (At.shape[1], At.shape[0])
+        self.device = At.device
 
 
 class RbfSource:
@@ -112,6 +125,10 @@ def _source(A):
     if isinstance(A, RbfSource):
         return Source(None, 0, SOURCE_RBF_F32, A.x.shape[1], A.x.data_ptr(), A.y.data_ptr(), A.x.stride(0),
                       A.y.stride(0), A.inv_two_sigma2)
+    if isinstance(A, TransposedDense):
+        src = Source(A.At.data_ptr(), _ld(A.At), SOURCE_DENSE_F32, 0, None, None, 0, 0, 0.0)
+        src.transposed = 1
+        return src
     return Source(A.data_ptr(), _ld(A), SOURCE_DENSE_F32, 0, None, None, 0, 0, 0.0)
 
 

@@ -200,8 +200,11 @@ static RbfSrc rbf_of(const cabs_source* s) {
 }
 static int32_t check_source(const cabs_plan& p, const cabs_source* src, const char* what) {
   if (!src) return arg_error(what);
+  if (src->transposed != 0 && (src->transposed != 1 || src->kind != CABS_SOURCE_DENSE_F32)) return arg_error(what);
   if (src->kind == CABS_SOURCE_DENSE_F32) {
-    if ((p.row_end > p.row_begin && !src->a) || src->lda < p.n) return arg_error(what);
+    // row-major block: lda >= n; column-major block (transposed): lda >= m_loc
+    if ((p.row_end > p.row_begin && !src->a) || src->lda < (src->transposed ? p.row_end - p.row_begin : p.n))
+      return arg_error(what);
     return CABS_OK;
   }
   if (src->kind == CABS_SOURCE_RBF_F32) {
@@ -223,6 +226,7 @@ static void src_cols(const cabs_plan& p, const cabs_source* src, const int64_t* 
   const int64_t m_loc = p.row_end - p.row_begin;
   if (is_rbf(src)) launch_rbf_cols(rbf_of(src), p.row_begin, m_loc, J, k, C, ldc, st);
   else if (is_csr(src)) launch_csc_cols(csr_of(src), m_loc, p.n, J, k, C, ldc, st);
+  else if (src->transposed) launch_gather_cols_t(src->a, src->lda, m_loc, p.n, J, k, C, ldc, ws, st);
   else launch_gather_cols(src->a, src->lda, m_loc, p.n, J, k, C, ldc, ws, st);
 }
 // R = A(I, :): dense -- the rows this rank owns (others: completed by the caller's allreduce);
@@ -231,6 +235,7 @@ static void src_rows(const cabs_plan& p, const cabs_source* src, const int64_t* 
                      void* ws, cudaStream_t st) {
   if (is_rbf(src)) launch_rbf_rows(rbf_of(src), I, k, p.n, R, ldr, st);
   else if (is_csr(src)) launch_csr_rows(csr_of(src), p.row_begin, p.row_end, I, k, p.n, R, ldr, st);
+  else if (src->transposed) launch_gather_rows_t(src->a, src->lda, p.row_begin, p.row_end, I, k, p.n, R, ldr, ws, st);
   else launch_gather_rows(src->a, src->lda, p.row_begin, p.row_end, I, k, p.n, R, ldr, ws, st);
 }
 // W = A(I, J) straight from the source (single rank, or implicit)
@@ -238,6 +243,7 @@ static void src_w(const cabs_plan& p, const cabs_source* src, const int64_t* I, 
                   int64_t ldw, cudaStream_t st) {
   if (is_rbf(src)) launch_rbf_w(rbf_of(src), I, J, k, W, ldw, st);
   else if (is_csr(src)) launch_csr_w(csr_of(src), p.row_begin, p.row_end, I, J, k, W, ldw, st);
+  else if (src->transposed) launch_gather_w_t(src->a, src->lda, p.row_begin, p.row_end - p.row_begin, p.n, I, J, k, W, ldw, st);
   else launch_gather_w_direct(src->a, src->lda, p.row_begin, p.row_end - p.row_begin, p.n, I, J, k, W, ldw, st);
 }
 // rows of R are exchanged only for a dense source on several ranks
@@ -1051,7 +1057,7 @@ int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float
     if (p.m > (1ll << 32) || p.n > (1ll << 32)) return arg_error("residual: sampled dims must be <= 2^32");
     SampArgs a{};
     if (is_rbf(src)) a.rbf = rbf_of(src);
-    else { a.A = src->a; a.lda = src->lda; }
+    else { a.A = src->a; a.lda = src->lda; a.transposed = src->transposed; }
     a.m = static_cast<uint64_t>(p.m);
     a.n = static_cast<uint64_t>(p.n);
     a.row_begin = p.row_begin;
@@ -1076,14 +1082,21 @@ int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float
     CABS_TRY(comm_f64(comm, out, 2, stream));
     return CABS_OK;
   }
-  if (residual_tc_supported(src->a, src->lda, m_loc, p.n, ncomp)) {
-    if (launch_residual_tc(src->a, src->lda, m_loc, p.n, F, ldf, s, G, ldg, ncomp, wsp<float>(ws, L.res_split),
+  // a column-major block is the row-major n x m_loc matrix A^T: ||A - F S G^T|| = ||A^T - G S F^T||,
+  // so the same kernels run with the factors exchanged (res_split holds max(n, m_loc) rows)
+  const bool tr = src->transposed != 0;
+  const int64_t ra = tr ? p.n : m_loc, ca = tr ? m_loc : p.n;
+  const float* Fa = tr ? G : F;
+  const float* Ga = tr ? F : G;
+  const int64_t ldfa = tr ? ldg : ldf, ldga = tr ? ldf : ldg;
+  if (residual_tc_supported(src->a, src->lda, ra, ca, ncomp)) {
+    if (launch_residual_tc(src->a, src->lda, ra, ca, Fa, ldfa, s, Ga, ldga, ncomp, wsp<float>(ws, L.res_split),
                            wsp<double>(ws, L.res_part), out, S(stream)) != 0) {
       cabs_set_error_msg("residual: tensor map encoding failed");
       return CABS_ERR_CUDA;
     }
   } else {
-    launch_residual(src->a, src->lda, m_loc, p.n, F, ldf, s, G, ldg, ncomp, wsp<double>(ws, L.res_part), out,
+    launch_residual(src->a, src->lda, ra, ca, Fa, ldfa, s, Ga, ldga, ncomp, wsp<double>(ws, L.res_part), out,
                     S(stream));
   }
   CABS_LAUNCH_CHECK("residual");

@@ -112,8 +112,9 @@ inline Ws ws_layout(const cabs_plan& p) {
   w.rb = take(sizeof(float) * K * w.ldrb);
   w.wb = take(sizeof(float) * K * Kp);
   w.res_part = take(sizeof(double) * 2 * kResGrid);
-  w.res_split = take(sizeof(float) * 2 * (size_t)p.n * (Kp < 192 ? Kp : 192) + 256);  // G hi/lo (TF32: pitch round_up(K, 32) <= 192;
-                                                                                   // FP16: round_up(K, 64) <= 384 halves) + max
+  // G hi/lo (TF32: pitch round_up(K, 32) <= 192; FP16: round_up(K, 64) <= 384 halves) + max; G has n rows, or
+  // m_loc rows when the block is column-major (cabs_source.transposed: the factors are exchanged)
+  w.res_split = take(sizeof(float) * 2 * (size_t)(p.n > w.m_loc ? p.n : w.m_loc) * (Kp < 192 ? Kp : 192) + 256);
   w.total = off;
   return w;
 }

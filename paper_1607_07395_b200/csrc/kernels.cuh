@@ -22,6 +22,13 @@ void launch_gather_cols(const float* A, int64_t lda, int64_t m_loc, int64_t n, c
 void launch_gather_w(const float* R, int64_t ldr, int64_t n, const int64_t* J, int32_t k, float* W, int64_t ldw, cudaStream_t st);
 void launch_gather_w_direct(const float* A, int64_t lda, int64_t row_begin, int64_t m_loc, int64_t n,
                             const int64_t* I, const int64_t* J, int32_t k, float* W, int64_t ldw, cudaStream_t st);
+// the same gathers from a column-major block At = A^T (n x m_loc, ldt): cabs_source.transposed
+void launch_gather_cols_t(const float* At, int64_t ldt, int64_t m_loc, int64_t n, const int64_t* J, int32_t k,
+                          float* C, int64_t ldc, void* ws, cudaStream_t st);
+void launch_gather_rows_t(const float* At, int64_t ldt, int64_t row_begin, int64_t row_end, const int64_t* I,
+                          int32_t k, int64_t n, float* R, int64_t ldr, void* ws, cudaStream_t st);
+void launch_gather_w_t(const float* At, int64_t ldt, int64_t row_begin, int64_t m_loc, int64_t n, const int64_t* I,
+                       const int64_t* J, int32_t k, float* W, int64_t ldw, cudaStream_t st);
 
 // svd.cu
 int launch_svd(int k, const float* W, int64_t ldw, double tol, void* ws, const Ws& L, double* sigma_user, double* Uw64,
@@ -261,6 +268,7 @@ struct RbfSrc {
 struct SampArgs {
   const float* A;  // dense source (rbf.x == nullptr): the rank's rows
   int64_t lda;
+  int transposed;  // dense: A(i, j) at A + j*lda + (i - row_begin) (cabs_source.transposed)
   RbfSrc rbf;      // implicit source when rbf.x != nullptr
   uint64_t m, n, thr_m, thr_n;
   int64_t row_begin, row_end;

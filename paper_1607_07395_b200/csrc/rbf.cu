@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) residual_sampled_kernel(SampArgs a, doubl
           }
           aij = rbf_entry(d2, a.rbf.g);
         } else {
-          aij = __ldg(a.A + (i - a.row_begin) * a.lda + j);
+          aij = __ldg(a.transposed ? a.A + j * a.lda + (i - a.row_begin) : a.A + (i - a.row_begin) * a.lda + j);
         }
       }
     }
