@@ -57,6 +57,7 @@ def sparse_block(cfg, r0, r1, dev):
     bix, bv = ix[lo:hi].contiguous(), v[lo:hi].contiguous()
     cp, ri, cv = csr_to_csc(bip, bix, bv, cfg.n)
     return (bip, bix, bv, cp, ri, cv), (ip, ix, v)
+LIN_SAMPLES = 10 ** 6    # sampled-error pairs of the host-resident (linear access) end-to-end line
 C5_SAMPLES = 10 ** 9     # BASELINE.json configs[4]: "residual estimated on a seeded 1e9-entry uniform subset"
 ORACLE_RBF_SAMPLES = 1 << 20  # the oracle's bounded c5 sample: pairs of its leading block
 
@@ -679,6 +680,74 @@ def main():
         e2e = {"value": (cfg.m + cfg.n) / (e2e_t / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t}
 
+    # ---- linear access end to end ("never knowing the remaining entries"): A never leaves pinned
+    # host memory (cabs_source.host_resident); S1-S9 read only the sampled rows and columns through the mapped
+    # address, the error is the sampled estimate (Z17) on LIN_SAMPLES seeded pairs; the sketch and the metric
+    # are read back as in `e2e`.  Not the contract's `e2e` (which copies all of A): an extra line.
+    e2e_lin = None
+    At = None  # A^T on the device (block-wise transpose: no second full-size temporary), when it fits
+    if (world == 1 and isinstance(A, torch.Tensor) and not (args.no_variants and A_host is None)
+            and 2.4 * A.numel() * 4 < torch.cuda.get_device_properties(dev).total_memory):
+        At = torch.empty((cfg.n, cfg.m), dtype=torch.float32, device=dev)
+        for r0 in range(0, cfg.m, 8192):
+            At[:, r0:r0 + 8192] = A[r0:r0 + 8192, :cfg.n].t()
+    if A_host is not None and world == 1:
+        from paper_1607_07395_b200.pipeline import CabsConfig, CabsPipeline
+        lcfg = CabsConfig(cfg.k1, cfg.k2, cfg.iters, seed=cfg.seed, residual_samples=LIN_SAMPLES)
+        At_host = None  # both layouts in host memory (cabs_source.at)
+        if At is not None:
+            At_host = torch.empty(At.shape, dtype=torch.float32, pin_memory=True)
+            At_host.copy_(At)
+        hp = CabsPipeline(C.HostDense(A_host, dev, At=At_host), cfg.m, cfg.n, lcfg, plan=plan)
+        for _ in range(2):
+            hp.run()
+        torch.cuda.synchronize()
+        outs_h = [hp.U, hp.s2, hp.V, hp.Ib, hp.Jb, hp.out]
+        host_h = [torch.empty_like(t, device="cpu").pin_memory() for t in outs_h]
+        lin_ms = []
+        for _ in range(max(2, min(args.steps, 5))):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            hp.run()
+            for h, t in zip(host_h, outs_h):
+                h.copy_(t, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            lin_ms.append(e0.elapsed_time(e1))
+        lt = statistics.mean(lin_ms)
+        hp.run(timed=True)
+        lin_steps = hp.step_ms()
+        same = bool(torch.equal(hp.Ib, pipe.Ib) and torch.equal(hp.Jb, pipe.Jb) and torch.equal(hp.U, pipe.U)
+                    and torch.equal(hp.V, pipe.V) and torch.equal(hp.s2, pipe.s2))
+        kk = cfg.k1 + cfg.k2
+        e2e_lin = {"value": (cfg.m + cfg.n) / (lt / 1e3), "unit": UNIT, "ms_per_step": lt,
+                   "what": "S1-S9 + sampled error with A resident in pinned HOST memory (zero-copy gathers of the "
+                           "sampled rows / columns only; nothing else of A crosses the interconnect)",
+                   "residual_samples": LIN_SAMPLES, "breakdown_ms": lin_steps,
+                   "interconnect_bytes_per_step": {"useful": 4 * kk * (cfg.m + cfg.n) + 4 * LIN_SAMPLES,
+                                                   "as_32B_sectors": kk * (32 * cfg.m + 4 * cfg.n) + 32 * LIN_SAMPLES},
+                   "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in outs_h),
+                   "factors_identical_to_device_resident_run": same,
+                   "rel_err_sampled": math.sqrt(max(float(hp.out[0]), 0.0) / float(hp.out[1]))}
+        e2e_lin["layouts"] = "row-major + column-major copies in host memory (cabs_source.at)" if At_host is not None \
+            else "row-major only"
+        if At_host is not None:  # the single-layout figure beside it: column gathers as one 32-byte sector per element
+            hp1 = CabsPipeline(C.HostDense(A_host, dev), cfg.m, cfg.n, lcfg, plan=plan)
+            hp1.run()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            hp1.run()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e2e_lin["row_major_only_ms_per_step"] = e0.elapsed_time(e1)
+            e2e_lin["interconnect_bytes_per_step"]["as_32B_sectors_row_major_only"] = \
+                e2e_lin["interconnect_bytes_per_step"].pop("as_32B_sectors")
+            del hp1
+        del hp, At_host
+
     # ---- the paper's follow-up variant (f) (hard threshold) on the same
     # matrix: S6-S8 replaced by cabs_hard_select_pair; timed the same way (graph on one GPU)
     variants = {}
@@ -689,18 +758,18 @@ def main():
         if args.no_variants:
             break
         variants[fu_name] = time_variant(args, cfg, A, plan, rank, world, comm, flush, stream, fu, fu_desc)
-    if (not args.no_variants and world == 1 and isinstance(A, torch.Tensor)
-            and 2.4 * A.numel() * 4 < torch.cuda.get_device_properties(dev).total_memory):
+    if not args.no_variants and At is not None:
         # the same CABS with the block held column-major (cabs_source.transposed): contiguous column
         # gathers, k (n + m/8) gather sectors instead of k (m + n/8); results identical (tests/test_gpu_transposed.py)
-        At = torch.empty((cfg.n, cfg.m), dtype=torch.float32, device=dev)
-        for r0 in range(0, cfg.m, 8192):  # block-wise transpose: no second full-size temporary
-            At[:, r0:r0 + 8192] = A[r0:r0 + 8192, :cfg.n].t()
         variants["colmajor_layout"] = time_variant(args, cfg, C.TransposedDense(At), plan, rank, world, comm, flush,
                                                    stream, "kmeans", "Algorithm 2 unchanged; A held column-major "
                                                    "(cabs_source.transposed = 1)")
-        del At
-        torch.cuda.empty_cache()
+        # and with both layouts resident (cabs_source.at): every gather a contiguous copy
+        variants["dual_layout"] = time_variant(args, cfg, C.DualDense(A, At), plan, rank, world, comm, flush, stream,
+                                               "kmeans", "Algorithm 2 unchanged; A held row-major and column-major "
+                                               "(cabs_source.at)")
+    del At
+    torch.cuda.empty_cache()
     if not args.no_variants and world == 1:
         variants["sketch_cur"] = time_sketch_cur(args, cfg, A, flush, samples)
         variants["rank_sweep"] = time_rank_sweep(pipe)
@@ -795,6 +864,8 @@ def main():
                     "near_ties_rows": int(res["tie_r"].sum()), "near_ties_cols": int(res["tie_c"].sum())},
     }
     line["variants"] = variants
+    if e2e_lin is not None:
+        line["e2e_linear_access"] = e2e_lin
     if e2e:
         line["e2e"] = e2e
     if world == 1 and not (args.no_cpu_baseline and args.no_parity):

@@ -138,6 +138,24 @@ typedef struct cabs_source {
   const float* col_val;   /* CSC: float[nnz] */
   int32_t transposed;     /* dense only: 0 = row-major block, 1 = column-major block (see above);
                              any other value, or 1 with another kind -> INVALID_ARG */
+  int32_t host_resident;  /* dense only: 1 = `a` is pinned host memory mapped into the device address
+                             space (cudaHostAlloc / cudaHostRegister; same address under UVA) instead of
+                             device memory: nothing is copied, the gathers read exactly the sampled rows
+                             and columns over the interconnect ("never knowing the remaining
+                             entries", P:29 matrices that do not fit in memory), results bit-identical
+                             to the device-resident block; the exact residual then reads all of A over
+                             the interconnect with plain loads (no TMA) -- use n_samples > 0 instead.
+                             Any value but 0 / 1, or 1 with another kind -> INVALID_ARG */
+  const float* at;        /* dense only, optional (NULL = absent): the SAME block held column-major as
+                             well, A(i, j) at at + j*ldat + (i - row_begin) (the n x m_loc row-major
+                             array A^T, as for transposed = 1; same memory space as `a`).  When given,
+                             the column gathers read `at` and the row gathers read `a`, so both are
+                             contiguous copies: 4 k (m + n) bytes per gather pair instead of one 32-byte
+                             sector per element (the sparse kind's CSR + CSC pair is the same
+                             idea).  The two copies must hold the same values (not checked); results
+                             are then bit-identical to the single-layout run.  Requires transposed = 0
+                             and ldat >= row_end - row_begin, else INVALID_ARG */
+  int64_t ldat;
 } cabs_source;
 
 /* Collectives supplied by the caller (host struct).  Each callback sums `count`

@@ -67,7 +67,8 @@ class Source(ctypes.Structure):
     _fields_ = [("a", c_vp), ("lda", c_i64), ("kind", c_i32), ("d", c_i32), ("x", c_vp), ("y", c_vp),
                 ("ldx", c_i64), ("ldy", c_i64), ("inv_two_sigma2", c_f32),
                 ("row_ptr", c_vp), ("col_idx", c_vp), ("row_val", c_vp), ("col_ptr", c_vp),
-                ("row_idx", c_vp), ("col_val", c_vp), ("transposed", c_i32)]
+                ("row_idx", c_vp), ("col_val", c_vp), ("transposed", c_i32), ("host_resident", c_i32),
+                ("at", c_vp), ("ldat", c_i64)]
 
 
 class TransposedDense:
@@ -81,6 +82,40 @@ class TransposedDense:
         self.At = At
         self.shape = (At.shape[1], At.shape[0])
         self.device = At.device
+
+
+class HostDense:
+    """A dense row-major row block that stays in pinned (page-locked, device-mapped) HOST memory
+    (cabs.h: cabs_source.host_resident): the gathers read only the sampled rows and columns over the
+    interconnect, the paper's linear access taken literally ("matrices which won't fit in
+    the main memory").  A: pinned CPU float32 tensor (m_loc, n); At (optional): the same block held
+    column-major too, a pinned (n, m_loc) tensor (cabs_source.at: contiguous column gathers); device:
+    the CUDA device the kernels run on.  Results are those of the device-resident copy, bit for bit."""
+
+    def __init__(self, A, device, At=None):
+        for t in (A,) + ((At,) if At is not None else ()):
+            if t.dtype != torch.float32 or t.is_cuda or not t.is_pinned() or t.dim() != 2 or t.stride(1) != 1:
+                raise TypeError("HostDense: pinned 2-D float32 CPU tensors with unit column stride")
+        if At is not None and tuple(At.shape) != (A.shape[1], A.shape[0]):
+            raise ValueError("HostDense: At must be (n, m_loc)")
+        self.A, self.At = A, At
+        self.shape = tuple(A.shape)
+        self.device = torch.device(device)
+
+
+class DualDense:
+    """A device-resident dense block in both layouts (cabs.h: cabs_source.a + cabs_source.at): A (m_loc, n)
+    row-major and At (n, m_loc) = A^T row-major, the same values; row and column gathers both contiguous."""
+
+    def __init__(self, A, At):
+        for t in (A, At):
+            if t.dtype != torch.float32 or not t.is_cuda or t.dim() != 2 or t.stride(1) != 1:
+                raise TypeError("DualDense: 2-D float32 CUDA tensors with unit column stride")
+        if tuple(At.shape) != (A.shape[1], A.shape[0]):
+            raise ValueError("DualDense: At must be (n, m_loc)")
+        self.A, self.At = A, At
+        self.shape = tuple(A.shape)
+        self.device = A.device
 
 
 class RbfSource:
@@ -125,6 +160,12 @@ def _source(A):
     if isinstance(A, RbfSource):
         return Source(None, 0, SOURCE_RBF_F32, A.x.shape[1], A.x.data_ptr(), A.y.data_ptr(), A.x.stride(0),
                       A.y.stride(0), A.inv_two_sigma2)
+    if isinstance(A, (HostDense, DualDense)):
+        src = Source(A.A.data_ptr(), _ld(A.A), SOURCE_DENSE_F32, 0, None, None, 0, 0, 0.0)
+        src.host_resident = 1 if isinstance(A, HostDense) else 0
+        if A.At is not None:
+            src.at, src.ldat = A.At.data_ptr(), _ld(A.At)
+        return src
     if isinstance(A, TransposedDense):
         src = Source(A.At.data_ptr(), _ld(A.At), SOURCE_DENSE_F32, 0, None, None, 0, 0, 0.0)
         src.transposed = 1

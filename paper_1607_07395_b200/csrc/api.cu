@@ -201,6 +201,9 @@ static RbfSrc rbf_of(const cabs_source* s) {
 static int32_t check_source(const cabs_plan& p, const cabs_source* src, const char* what) {
   if (!src) return arg_error(what);
   if (src->transposed != 0 && (src->transposed != 1 || src->kind != CABS_SOURCE_DENSE_F32)) return arg_error(what);
+  if (src->host_resident != 0 && (src->host_resident != 1 || src->kind != CABS_SOURCE_DENSE_F32)) return arg_error(what);
+  if (src->at && (src->kind != CABS_SOURCE_DENSE_F32 || src->transposed || src->ldat < p.row_end - p.row_begin))
+    return arg_error(what);
   if (src->kind == CABS_SOURCE_DENSE_F32) {
     // row-major block: lda >= n; column-major block (transposed): lda >= m_loc
     if ((p.row_end > p.row_begin && !src->a) || src->lda < (src->transposed ? p.row_end - p.row_begin : p.n))
@@ -226,6 +229,7 @@ static void src_cols(const cabs_plan& p, const cabs_source* src, const int64_t* 
   const int64_t m_loc = p.row_end - p.row_begin;
   if (is_rbf(src)) launch_rbf_cols(rbf_of(src), p.row_begin, m_loc, J, k, C, ldc, st);
   else if (is_csr(src)) launch_csc_cols(csr_of(src), m_loc, p.n, J, k, C, ldc, st);
+  else if (src->at) launch_gather_cols_t(src->at, src->ldat, m_loc, p.n, J, k, C, ldc, ws, st);  // second, column-major copy
   else if (src->transposed) launch_gather_cols_t(src->a, src->lda, m_loc, p.n, J, k, C, ldc, ws, st);
   else launch_gather_cols(src->a, src->lda, m_loc, p.n, J, k, C, ldc, ws, st);
 }
@@ -1089,7 +1093,8 @@ int32_t cabs_residual(const cabs_plan* plan, const cabs_source* src, const float
   const float* Fa = tr ? G : F;
   const float* Ga = tr ? F : G;
   const int64_t ldfa = tr ? ldg : ldf, ldga = tr ? ldf : ldg;
-  if (residual_tc_supported(src->a, src->lda, ra, ca, ncomp)) {
+  // a host-resident block (pinned, mapped) is read with plain loads over the interconnect, not by TMA
+  if (!src->host_resident && residual_tc_supported(src->a, src->lda, ra, ca, ncomp)) {
     if (launch_residual_tc(src->a, src->lda, ra, ca, Fa, ldfa, s, Ga, ldga, ncomp, wsp<float>(ws, L.res_split),
                            wsp<double>(ws, L.res_part), out, S(stream)) != 0) {
       cabs_set_error_msg("residual: tensor map encoding failed");

@@ -57,7 +57,7 @@ class CabsPipeline:
         p = self.plan
         if isinstance(A_local, C.RbfSource):  # implicit source: every rank holds all points
             assert A_local.shape == (m, n)
-        elif isinstance(A_local, C.TransposedDense):  # the block held column-major
+        elif isinstance(A_local, (C.TransposedDense, C.HostDense, C.DualDense)):  # column-major block / pinned host block
             assert A_local.shape == (p.m_loc, n)
         else:
             assert A_local.shape[0] == p.m_loc and A_local.shape[1] >= n
