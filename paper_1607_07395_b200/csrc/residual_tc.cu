@@ -54,10 +54,11 @@ constexpr uint32_t kTmemCols = 512;
 // Kp <= 128: 2 acc + 1 F; Kp <= 192: 1 acc + 1 F.
 struct TmemPlan {
   int kp, nacc, nf;
+  int ftop;  // nf = 1: the next band's F is loaded at the top of its first tile (before that tile's A boxes are read)
   __host__ __device__ uint32_t fcol0() const { return static_cast<uint32_t>(nacc * kTcBN); }
 };
 inline TmemPlan tmem_plan(int kp) {
-  TmemPlan t{kp, 2, 2};
+  TmemPlan t{kp, 2, 2, getenv("CABS_RES_FTOP") ? atoi(getenv("CABS_RES_FTOP")) : 0};
   if (kp > 64 || getenv("CABS_RES_NF1")) t.nf = 1;  // (the variable forces the 1-buffer plan: tests)
   if (kp > 128) t.nacc = 1;
   return t;
@@ -477,6 +478,12 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           load_band(rb + 1, fcol0 + static_cast<uint32_t>(fb * 2 * kp), &S.f_ready[fb]);
         }
       }
+      if (nf == 1 && tp.ftop && eg == 0 && i > 0 && cbe == 0) {  // first tile of a later band
+        const int64_t jb = rb - rb0 - 1;                         // the band just finished
+        tc::mbar_wait(&S.f_free[0], static_cast<uint32_t>(jb & 1));
+        tc::fence_after_sync();
+        load_band(rb, fcol0, &S.f_ready[0]);
+      }
       if (H && rb != inv_rb) {
         inv_rb = rb;
         inv = 1.f / (f_row_scale(fa, m, rb * kTcBM + row) * gs);  // a power of two: exact
@@ -544,7 +551,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       }
       // nf = 1: the band's last tile is in registers; the MMA released the F buffer when it
       // finished this tile (f_free commits after the tile's MMAs): load the next band now
-      if (nf == 1 && eg == 0 && t + 1 < t_end && cbe + 1 == ntc) {
+      if (nf == 1 && !tp.ftop && eg == 0 && t + 1 < t_end && cbe + 1 == ntc) {
         const int64_t jb = rb - rb0;
         tc::mbar_wait(&S.f_free[0], static_cast<uint32_t>(jb & 1));
         tc::fence_after_sync();
@@ -919,6 +926,16 @@ int residual_tc_kmax() { return res_f16_kmax() > kResKpMax ? res_f16_kmax() : kR
 // the tensor-core kernels cover this ncomp (FP16 split up to res_f16_kmax(), 3xTF32 up to kResKpMax)
 bool residual_tc_covers(int ncomp) {
   if (ncomp < 1 || ncomp > residual_tc_kmax() || getenv("CABS_RESIDUAL_FFMA")) return false;
+  // The single-F-buffer TMEM plan (nf = 1: K chunk pitch kp > 64, i.e. ncomp > 128 on the FP16 path, > 64 on
+  // 3xTF32) has an unresolved race: tools/res_flaky.py shows ~5e-4 wrong partial sums per band transition
+  // (both the error and the ||A||^2 partial of a CTA, i.e. stale A boxes, when the pipeline drains for the F
+  // reload; bit-identical results otherwise).  Until it is found, those ncomp take the FFMA kernel;
+  // CABS_RES_NF1_TC=1 re-enables the tensor-core plan (diagnostics, tools/res_flaky.py).
+  if (!getenv("CABS_RES_NF1_TC")) {
+    const bool tf32 = getenv("CABS_RESIDUAL_TF32") || ncomp > res_f16_kmax();
+    const int kp = tf32 ? static_cast<int>(round_up(ncomp, 32)) : static_cast<int>(round_up(ncomp, 64)) / 2;
+    if (kp > 64) return false;
+  }
   return !((getenv("CABS_RESIDUAL_TF32") || ncomp > res_f16_kmax()) && round_up(ncomp, 32) > kResKpMax);
 }
 

@@ -374,12 +374,16 @@ def test_residual_near_factorisation(dev, m, n, k):
     Ft = torch.zeros((m, ld), device=dev); Ft[:, :k] = torch.from_numpy(F).to(dev)
     Gt = torch.zeros((n, ld), device=dev); Gt[:, :k] = torch.from_numpy(G).to(dev)
     out = torch.zeros(2, dtype=torch.float64, device=dev)
-    assert C.cabs_residual_path(k) == "tc"
-    C.cabs_residual(plan, torch.from_numpy(A).to(dev), Ft, torch.from_numpy(s).to(dev), Gt, k, out, ws)
+    # ncomp > 128 (the single-F-buffer TMEM plan) is routed to the FFMA kernel until its race is fixed
+    # (residual_tc.cu residual_tc_covers, tools/res_flaky.py); repeated so that a flaky path cannot pass by luck
+    assert C.cabs_residual_path(k) == ("tc" if k <= 128 else "ffma")
+    A_t, s_t = torch.from_numpy(A).to(dev), torch.from_numpy(s).to(dev)
     r2, a2 = O.residual(A, F, G, s)
-    o = out.cpu().numpy()
-    assert abs(o[1] - a2) <= 1e-6 * a2
-    assert abs(math.sqrt(o[0]) - math.sqrt(r2)) <= 1e-4 * math.sqrt(r2)
+    for _ in range(8):
+        C.cabs_residual(plan, A_t, Ft, s_t, Gt, k, out, ws)
+        o = out.cpu().numpy()
+        assert abs(o[1] - a2) <= 1e-6 * a2
+        assert abs(math.sqrt(o[0]) - math.sqrt(r2)) <= 1e-4 * math.sqrt(r2)
 
 
 @pytest.mark.parametrize("k", [16, 120, 190, 300])
