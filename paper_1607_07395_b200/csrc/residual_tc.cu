@@ -391,6 +391,9 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         if (rb != prev_rb) {
           if (band >= 0 && tc::elect_one()) tc::mma_commit(&S.f_free[band % nf]);  // previous band's F no longer read
           __syncwarp();
+          if ((tp.ftop & 2) && band >= 0) {  // diagnostics (CABS_RES_FTOP=2): drain the pipeline at every band change
+            for (int z = 0; z < 64; ++z) __nanosleep(100);
+          }
           ++band;
           RES_WAIT(4, tc::mbar_wait(&S.f_ready[band % nf], static_cast<uint32_t>((band / nf) & 1)));
           fcol = fcol0 + static_cast<uint32_t>((band % nf) * 2 * kp);
@@ -478,7 +481,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           load_band(rb + 1, fcol0 + static_cast<uint32_t>(fb * 2 * kp), &S.f_ready[fb]);
         }
       }
-      if (nf == 1 && tp.ftop && eg == 0 && i > 0 && cbe == 0) {  // first tile of a later band
+      if (nf == 1 && (tp.ftop & 1) && eg == 0 && i > 0 && cbe == 0) {  // first tile of a later band
         const int64_t jb = rb - rb0 - 1;                         // the band just finished
         tc::mbar_wait(&S.f_free[0], static_cast<uint32_t>(jb & 1));
         tc::fence_after_sync();
@@ -551,7 +554,7 @@ residual_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       }
       // nf = 1: the band's last tile is in registers; the MMA released the F buffer when it
       // finished this tile (f_free commits after the tile's MMAs): load the next band now
-      if (nf == 1 && !tp.ftop && eg == 0 && t + 1 < t_end && cbe + 1 == ntc) {
+      if (nf == 1 && !(tp.ftop & 1) && eg == 0 && t + 1 < t_end && cbe + 1 == ntc) {
         const int64_t jb = rb - rb0;
         tc::mbar_wait(&S.f_free[0], static_cast<uint32_t>(jb & 1));
         tc::fence_after_sync();
